@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""Benchmark: fused LN-backward + per-example-norm HBM GB/s and % overhead vs plain LN-backward.
+
+Workload (BASELINE.json configs[1]): LayerNorm backward + per-example
+||dgamma_b||^2, ||dbeta_b||^2 over the sweep D in {768, 1024, 2048, 4096, 8192},
+B=32 T=1024 per GPU, bf16 rows / fp32 accumulation.  One "step" = one fused
+backward per D of the sweep (plus, for N > 1, the NCCL all-reduce of each
+layer's packed {dgamma, dbeta, sum raw norms}).  Inputs are synthetic
+(SURVEY §8(d) recipe, generated on the device; identical to the oracle's).
+
+value      = sum over ranks and D of algorithmic bytes / max-over-ranks device time
+             bytes(D) = N*D*(2*s_in + s_out) + 8N + 12D + 16B; s = 2 (bf16)
+e2e        = same metric through the C ABI with HOST (pinned) buffers: H2D of x, dy,
+             mean, rstd, the kernel, D2H of dx, dgamma, dbeta, raw norms and sums
+overhead   = (t_fused - t_plain) / t_plain, same kernel with norms compiled out
+L2         = flushed (256 MiB write) before every timed kernel, outside the events
+
+--impl reference times the reference's own CPU implementation (oracle/_ref:
+the unmodified gnstk sources compiled from /root/reference, multi-threaded over
+example slices) on bounded samples of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SWEEP_D = [768, 1024, 2048, 4096, 8192]
+B_LOCAL, T = 32, 1024
+METRIC = "fused LN-bwd+per-example-norm HBM GB/s & % overhead vs plain LN-bwd"
+WORKLOAD = "cfg2: LayerNorm backward + per-example dgamma/dbeta norms, sweep D=768..8192, B=32 T=1024 per GPU, bf16 in / fp32 acc"
+
+
+def alg_bytes(B, T_, D, s_in=2, s_out=2, norms=True):
+    N = B * T_
+    return N * D * (2 * s_in + s_out) + 8 * N + 4 * D + 8 * D + (16 * B if norms else 0)
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms",
+                 "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self._proc = None
+        return self
+
+    def _read(self):
+        for line in self._proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self._proc is not None:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=2)
+            except Exception:
+                self._proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def ref_layer_sample(ref, orc, D, b_sample, threads):
+    """One bounded sample: b_sample examples of the cfg2 workload at width D,
+    the reference's layernorm_backward_simultaneous over `threads` example slices."""
+    import numpy as np
+
+    x, dy, gamma, beta = orc.synth_ln(b_sample, T, D, B_div=B_LOCAL, bf16=True)
+    _, xhat, inv = ref.ln_forward(x.astype(np.float64), gamma.astype(np.float64), beta.astype(np.float64))
+    g = dy.astype(np.float64)
+    gm = gamma.astype(np.float64)
+    t0 = time.perf_counter()
+    ref.ln_backward(xhat, inv, g, gm, threads=threads)
+    return time.perf_counter() - t0
+
+
+def run_reference_arm(args):
+    import numpy as np  # noqa: F401
+
+    from oracle import ffi
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    if not ffi.reference_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libgnstk_ref.so not built"}))
+        return 0
+    ref, orc = ffi.reference(), ffi.oracle()
+    threads = os.cpu_count() or 1
+    b_sample = min(B_LOCAL, threads)
+    times = []
+    for i in range(args.warmup + args.steps):
+        step_t = sum(ref_layer_sample(ref, orc, D, b_sample, threads) for D in SWEEP_D)
+        if i >= args.warmup:
+            times.append(step_t)
+    sample_bytes = sum(alg_bytes(b_sample, T, D) for D in SWEEP_D)
+    gbs = sample_bytes / statistics.median(times) / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": statistics.median(times) * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "B": B_LOCAL, "T": T, "D": SWEEP_D},
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "reference",
+                         "sample": f"{b_sample} of {B_LOCAL} examples x T={T} per D of the sweep per step, "
+                                   f"gnstk::layernorm_backward_simultaneous over {threads} example slices, fp64; "
+                                   "bytes counted with the bf16 workload formula"},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ----------------------------------------------------------------------------- our arm
+class LnCase:
+    """Device buffers + raw C-ABI argument tuples for one D of the sweep."""
+
+    def __init__(self, m, lib, D, B, rank, dev, torch):
+        self.D, self.B = D, B
+        bf = torch.bfloat16
+        self.x, self.dy, self.gamma, self.beta = m.synth_ln(B, T, D, bf, dev, b_offset=rank * B, B_div=B)
+        layer = m.LayerNormLayer(self.gamma, self.beta)
+        f = m.layernorm_forward(layer, self.x)
+        self.mean, self.rstd = f.cache.mean, f.cache.inv_std
+        self.dx = torch.empty_like(self.x)
+        # packed all-reduce buffer: [dgamma (D), dbeta (D)] fp32 then sums (4 fp64 -> 8 fp32 slots)
+        self.pack = torch.zeros(2 * D + 8, dtype=torch.float32, device=dev)
+        self.dgamma, self.dbeta = self.pack[:D], self.pack[D:2 * D]
+        self.sums = self.pack[2 * D:].view(torch.float64)
+        self.raw_g = torch.zeros(B, dtype=torch.float64, device=dev)
+        self.raw_b = torch.zeros(B, dtype=torch.float64, device=dev)
+        nbytes = m.layers.ctypes_size(B, T, D, 1)
+        self.ws = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+        self.lib = lib
+        self.bytes = alg_bytes(B, T, D)
+        self.bytes_plain = alg_bytes(B, T, D, norms=False)
+
+    def run(self, norms, stream_ptr):
+        p = lambda t: t.data_ptr()
+        rc = self.lib.gnsb_ln_bwd(
+            p(self.x), p(self.mean), p(self.rstd), p(self.dy), p(self.gamma), p(self.dx), p(self.dgamma),
+            p(self.dbeta), p(self.raw_g), p(self.raw_b), p(self.sums), 1 if norms else 0, self.B, T, self.D, 1,
+            p(self.ws), self.ws.numel(), stream_ptr)
+        if rc:
+            raise RuntimeError(self.lib.gnsb_last_error().decode())
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2411_00999_b200 as m
+    from paper_2411_00999_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    lib = _lib.lib()
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+    sweep = args.d_list
+    cases = [LnCase(m, lib, D, B_LOCAL, rank, dev, torch) for D in sweep]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize()
+
+    def timed(case, norms, with_collective):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        case.run(norms, sp)
+        if with_collective and world > 1:
+            dist.all_reduce(case.pack)
+        e1.record(stream)
+        return e0, e1
+
+    # warm-up
+    for _ in range(args.warmup):
+        for c in cases:
+            timed(c, True, True)
+            timed(c, False, False)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps of the fused sweep (value) ----
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            ev.append([timed(c, True, True) for c in cases])
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    fused_ms = np.array([[a.elapsed_time(b) for a, b in step] for step in ev])  # [K, nD]
+    step_ms = fused_ms.sum(1)
+    ms_per_step = float(np.median(step_ms))
+    t_local = float(step_ms.sum())
+    t = torch.tensor([t_local], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_max_ms = float(t.item())
+    total_bytes = sum(c.bytes for c in cases) * world * args.steps
+    value = total_bytes / (t_max_ms * 1e-3) / 1e9
+
+    # ---- kernel-only fused vs plain (overhead), alternating, same flush ----
+    reps = max(args.steps, 20)
+    fk = np.zeros((reps, len(cases)))
+    pk = np.zeros((reps, len(cases)))
+    for r in range(reps):
+        pairs = []
+        for i, c in enumerate(cases):
+            pairs.append((timed(c, True, False), timed(c, False, False)))
+        torch.cuda.synchronize()
+        for i, (a, b) in enumerate(pairs):
+            fk[r, i] = a[0].elapsed_time(a[1])
+            pk[r, i] = b[0].elapsed_time(b[1])
+    peak, peak_kind = load_peaks()
+    sweep_rows = []
+    for i, c in enumerate(cases):
+        tf, tp = float(np.median(fk[:, i])), float(np.median(pk[:, i]))
+        geo = m.ln_bwd_geometry(c.B, T, c.D, torch.bfloat16)
+        sweep_rows.append({
+            "D": c.D, "fused_us": tf * 1e3, "plain_us": tp * 1e3, "fused_GBps": c.bytes / tf / 1e6,
+            "plain_GBps": c.bytes_plain / tp / 1e6, "frac_of_measured_peak": c.bytes / tf / 1e6 / peak,
+            "frac_of_8TBps": c.bytes / tf / 1e6 / 8000.0, "overhead_pct": 100.0 * (tf - tp) / tp,
+            "grid": geo["grid"], "threads": geo["threads"], "stages": geo["stages"],
+        })
+    tot_f = sum(float(np.median(fk[:, i])) for i in range(len(cases)))
+    tot_p = sum(float(np.median(pk[:, i])) for i in range(len(cases)))
+    achieved = sum(c.bytes for c in cases) / (tot_f * 1e-3) / 1e9
+    big = [r for r in sweep_rows if r["D"] >= 1024]
+    overhead_ge1024 = 100.0 * (sum(r["fused_us"] for r in big) - sum(r["plain_us"] for r in big)) / max(
+        sum(r["plain_us"] for r in big), 1e-9)
+
+    # ---- e2e through the C ABI with host buffers ----
+    e2e = run_e2e(args, m, lib, cases, dev, stream, torch, np)
+
+    # ---- CPU baseline (rank 0, bounded sample) ----
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        cpu = cpu_baseline(args)
+
+    traffic = load_traffic()
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (SURVEY §8(d) recipe, generated on device)",
+        "config": {"workload": WORKLOAD, "B": B_LOCAL, "T": T, "D": sweep, "global_batch": B_LOCAL * world,
+                   "parallelism": f"dp{world}", "l2": "flushed (256 MiB write) before every timed kernel"},
+        "overhead_pct": 100.0 * (tot_f - tot_p) / tot_p, "overhead_pct_D_ge_1024": overhead_ge1024,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "peak_kind": peak_kind, "frac_of_8TBps": achieved / 8000.0, "traffic": traffic,
+                     "kernel": "ln_bwd_kernel<bf16,...,HAS_MEAN=1,NORMS=1>"},
+        "sweep": sweep_rows, "e2e": e2e, "cpu_baseline": cpu,
+        "gpu_launches": len(cases) * args.steps, "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(args, m, lib, cases, dev, stream, torch, np):
+    """Same metric through the public C ABI with host-resident inputs/outputs."""
+    sp = stream.cuda_stream
+    host = []
+    for c in cases:
+        h = {
+            "x": c.x.cpu().pin_memory(), "dy": c.dy.cpu().pin_memory(), "mean": c.mean.cpu().pin_memory(),
+            "rstd": c.rstd.cpu().pin_memory(), "dx": torch.empty(c.dx.shape, dtype=c.dx.dtype).pin_memory(),
+            "pack": torch.empty(c.pack.shape, dtype=c.pack.dtype).pin_memory(),
+            "raw_g": torch.empty(c.B, dtype=torch.float64).pin_memory(),
+            "raw_b": torch.empty(c.B, dtype=torch.float64).pin_memory(),
+        }
+        host.append(h)
+    h2d = sum(h["x"].numel() * 2 + h["dy"].numel() * 2 + h["mean"].numel() * 4 + h["rstd"].numel() * 4 for h in host)
+    d2h = sum(h["dx"].numel() * 2 + h["pack"].numel() * 4 + 16 * c.B for h, c in zip(host, cases))
+
+    def step():
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for c, h in zip(cases, host):
+            c.x.copy_(h["x"], non_blocking=True)
+            c.dy.copy_(h["dy"], non_blocking=True)
+            c.mean.copy_(h["mean"], non_blocking=True)
+            c.rstd.copy_(h["rstd"], non_blocking=True)
+            c.run(True, sp)
+            h["dx"].copy_(c.dx, non_blocking=True)
+            h["pack"].copy_(c.pack, non_blocking=True)
+            h["raw_g"].copy_(c.raw_g, non_blocking=True)
+            h["raw_b"].copy_(c.raw_b, non_blocking=True)
+        e1.record(stream)
+        return e0, e1
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    evs = [step() for _ in range(max(3, min(args.steps, 10)))]
+    torch.cuda.synchronize()
+    ms = float(np.median([a.elapsed_time(b) for a, b in evs]))
+    value = sum(c.bytes for c in cases) / (ms * 1e-3) / 1e9
+    return {"value": value, "unit": "GB/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "ms_per_step": ms, "path": "gnsb_ln_bwd (C ABI) with pinned host buffers, copies inside the timing"}
+
+
+def cpu_baseline(args):
+    from oracle import ffi
+
+    if not ffi.reference_available():
+        return None
+    ref, orc = ffi.reference(), ffi.oracle()
+    threads = os.cpu_count() or 1
+    b_sample = min(B_LOCAL, threads)
+    t0 = time.perf_counter()
+    tsum, nbytes = 0.0, 0
+    for D in args.d_list:
+        tsum += ref_layer_sample(ref, orc, D, b_sample, threads)
+        nbytes += alg_bytes(b_sample, T, D)
+        if time.perf_counter() - t0 > 60:
+            break
+    return {"value": nbytes / tsum / 1e9, "unit": "GB/s", "cores": threads, "kind": "reference",
+            "sample": f"{b_sample} examples x T={T} per D (one pass of the sweep), reference gnstk fp64 "
+                      f"layernorm_backward_simultaneous over {threads} threads; bytes by the bf16 workload formula"}
+
+
+def load_traffic():
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get("ln_bwd_bf16_D4096_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--d-list", type=lambda s: [int(v) for v in s.split(",")], default=SWEEP_D)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,189 @@
+/*
+ * gnsb.h — C ABI of the B200-native per-example-gradient-norm / GNS path.
+ *
+ * This is the drop-in boundary for the reference library `gnstk`
+ * (/root/reference/proj, citations below are relative to it).  The reference
+ * exposes a C++ value-semantics API (free functions in namespace gnstk over
+ * fp64 gnstk::Tensor, errors as std::invalid_argument); this header is the
+ * thin C layer underneath the B200 C++ drop-in (include/gnstk/*.hpp).  Every
+ * entry point below names the reference interface it replaces.
+ *
+ * Conventions
+ *   - All tensor pointers are DEVICE pointers owned by the caller, row-major,
+ *     contiguous.  Rows of one example are contiguous: an input of reference
+ *     shape [B, ..., D] is viewed as (B, M, D), M = product of middle extents
+ *     (proj/src/layers.cpp:19-28).
+ *   - Row data (x, xhat, dy, dx, y) have dtype `dt`.  Per-feature and per-row
+ *     statistics (gamma, beta, dgamma, dbeta, mean, rstd) are fp32 for
+ *     GNSB_F32/GNSB_BF16 and fp64 for GNSB_F64.  Norm outputs are always fp64.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
+ *     stream-ordered and asynchronous; the library keeps no per-call state and
+ *     is safe to call concurrently on distinct streams with distinct
+ *     workspaces.
+ *   - Validation failures return GNSB_EINVAL; gnsb_last_error() then holds the
+ *     reference's message, including its prefix ("layers: ", "gns: ",
+ *     "costmodel: ").  CUDA failures return GNSB_ECUDA.
+ *   - No CPU fallback: without a CUDA device every compute entry point returns
+ *     GNSB_ECUDA.
+ */
+#ifndef GNSB_H
+#define GNSB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { GNSB_OK = 0, GNSB_EINVAL = 1, GNSB_ECUDA = 2, GNSB_ENCCL = 3, GNSB_ENOMEM = 4 } gnsb_status;
+typedef enum { GNSB_F32 = 0, GNSB_BF16 = 1, GNSB_F64 = 2 } gnsb_dtype;
+
+/* Library version string and the calling thread's last error message. */
+const char* gnsb_version(void);
+const char* gnsb_last_error(void);
+
+/* ------------------------------------------------------------------------
+ * LayerNorm forward.
+ * Replaces gnstk::layernorm_forward (proj/include/gnstk/layers.hpp:76-77,
+ * proj/src/layers.cpp:189-229).  Writes y (nullable), per-row mean/rstd
+ * (nullable; the B200 backward's cache) and xhat (nullable; the reference's
+ * LayerNormCache::normalized, whose inv_std is `rstd`).
+ * Errors (reference wording): eps <= 0, D < 2.
+ */
+gnsb_status gnsb_ln_fwd(const void* x, const void* gamma, const void* beta, void* y, void* mean, void* rstd,
+                        void* xhat, int64_t rows, int64_t D, double eps, gnsb_dtype dt, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Fused LayerNorm backward + per-example squared gradient norms.
+ * Replaces gnstk::layernorm_backward_simultaneous
+ * (proj/include/gnstk/layers.hpp:79-80, proj/src/layers.cpp:231-298).
+ *
+ *   x_or_xhat, mean : with mean != NULL the input is x and
+ *                     xhat = (x - mean) * rstd; with mean == NULL the input is
+ *                     the reference cache's `normalized` tensor.
+ *   rstd            : [B*M] (the reference cache's inv_std)
+ *   dy              : [B*M*D] upstream gradient of a MEAN-reduced loss
+ *   dx              : [B*M*D] (nullable: skip the input gradient)
+ *   dgamma, dbeta   : [D] batch-summed parameter gradients
+ *   raw_sq_gamma/beta : [B] uncorrected per-example ||dgamma_b||^2, ||dbeta_b||^2
+ *                     (LayerGradOutput::per_example_sqnorms_raw), nullable
+ *   sums            : [4] nullable: { sum_b raw_gamma, sum_b raw_beta,
+ *                     ||dgamma||^2, ||dbeta||^2 }.  The reference's corrected
+ *                     value (per_example_sqnorms) is sums[i] / B * B^2.
+ *   with_norms      : 0 runs the otherwise-identical plain LayerNorm backward
+ *                     (same kernel, norms compiled out; raw/sums untouched).
+ *   ws, ws_bytes    : device workspace of at least
+ *                     gnsb_ln_bwd_workspace_size() bytes.  It must be
+ *                     zero-filled before its first use; every call leaves it
+ *                     ready for the next.  One workspace per concurrent stream.
+ * Errors (reference wording): B == 0 ("empty batch"), D < 1.
+ * Deterministic: results are bitwise identical run to run on a given GPU.
+ */
+gnsb_status gnsb_ln_bwd_workspace_size(int64_t B, int64_t M, int64_t D, gnsb_dtype dt, size_t* bytes);
+gnsb_status gnsb_ln_bwd(const void* x_or_xhat, const void* mean, const void* rstd, const void* dy,
+                        const void* gamma, void* dx, void* dgamma, void* dbeta, double* raw_sq_gamma,
+                        double* raw_sq_beta, double* sums, int32_t with_norms, int64_t B, int64_t M, int64_t D,
+                        gnsb_dtype dt, void* ws, size_t ws_bytes, void* stream);
+/* Launch geometry the backward uses for this shape (reporting / roofline). */
+gnsb_status gnsb_ln_bwd_geometry(int64_t B, int64_t M, int64_t D, gnsb_dtype dt, int32_t* grid, int32_t* threads,
+                                 int32_t* stages);
+
+/* ------------------------------------------------------------------------
+ * Deterministic fp64 squared norm of a device vector (fp32 or fp64 data):
+ * out[0] = sum_i v[i]^2.  Used after the batch-sharded all-reduce, where
+ * ||G_big||^2 must be formed from the REDUCED gradient.
+ */
+gnsb_status gnsb_sqnorm(const void* v, int64_t n, gnsb_dtype dt, double* out, void* stream);
+
+/* ------------------------------------------------------------------------
+ * GNS estimator (host functions).  Replace proj/include/gnstk/gns.hpp:16-74 /
+ * proj/src/gns.cpp:14-89 with identical arithmetic and error conditions.
+ */
+typedef struct {
+    double g_big_sqnorm;
+    double g_small_sqnorm_mean;
+    int64_t b_big;
+    int64_t b_small;
+    int64_t n_small;
+} gnsb_grad_stats; /* gnstk::GradStats, gns.hpp:16-22 */
+
+typedef struct {
+    double g2;
+    double s;
+    double b_simple;
+    int32_t b_simple_defined;
+} gnsb_gns_estimate; /* gnstk::GnsEstimate, gns.hpp:26-31 */
+
+typedef struct {
+    double alpha;
+    double value;
+    int64_t count;
+} gnsb_ema_state; /* gnstk::EmaState, gns.hpp:36-40 */
+
+enum { GNSB_LAYER_EMBEDDING = 0, GNSB_LAYER_LINEAR = 1, GNSB_LAYER_LAYERNORM = 2 }; /* gns.hpp:42 */
+
+gnsb_status gnsb_estimate_g2(const gnsb_grad_stats* st, double* out);          /* gns.cpp:31-36 */
+gnsb_status gnsb_estimate_s(const gnsb_grad_stats* st, double* out);           /* gns.cpp:38-43 */
+void gnsb_make_gns_estimate(double g2, double s, gnsb_gns_estimate* out);       /* gns.cpp:45-54 */
+gnsb_status gnsb_ema_update(gnsb_ema_state* st, double x);                      /* gns.cpp:56-64 */
+gnsb_status gnsb_smoothed_gns(const gnsb_ema_state* g2, const gnsb_ema_state* s,
+                              gnsb_gns_estimate* out);                          /* gns.cpp:66-69 */
+/* gns.cpp:71-89.  layers in gnstk::LayerKey order; group < 0 = no filter. */
+gnsb_status gnsb_aggregate(const gnsb_grad_stats* stats, const int32_t* layer_types, int32_t n, int32_t group,
+                           gnsb_grad_stats* out);
+
+/* ------------------------------------------------------------------------
+ * Device GNS accumulator (one step of the PerExample estimator).
+ * Replaces the per-step GradStats packaging + fill_group of Trainer::step
+ * (proj/src/trainer.cpp:324-325, 363-415) with a single-CTA kernel.
+ *
+ *   layer_sums  : device [n_layers][4] fp64 records, one per layer, in
+ *                 LayerKey order: { sum_b raw(p0), sum_b raw(p1),
+ *                 ||grad p0||^2, ||grad p1||^2 } exactly as gnsb_ln_bwd's
+ *                 `sums` (p0 = gamma, p1 = beta; for a linear layer p0 =
+ *                 weight, p1 = bias or zeros).  Parameters are summed in the
+ *                 reference's name order (p1 first: "beta" < "gamma",
+ *                 "bias" < "weight").
+ *   layer_types : HOST [n_layers] GNSB_LAYER_*
+ *   B           : global batch (b_big = B, b_small = 1, n_small = B)
+ *   state       : device [8] gnsb_ema_state for groups {total, embedding,
+ *                 linear, layernorm} x {g2, s}; zero-filled before the first
+ *                 step (count = 0).  `alpha` is applied to every state.
+ *   out_groups  : device [4][4] fp64 {g2_raw, s_raw, gns_ema, defined(0/1)};
+ *                 a group with no layers is skipped (all NaN, state untouched).
+ *   out_layers  : device [n_layers][2] fp64 {g2, s} per layer (nullable).
+ * Errors: B < 2 (trainer.cpp:291-292), alpha outside (0, 1].
+ */
+gnsb_status gnsb_gns_step(const double* layer_sums, const int32_t* layer_types, int32_t n_layers, int64_t B,
+                          double alpha, gnsb_ema_state* state, double* out_groups, double* out_layers,
+                          void* stream);
+
+/* ------------------------------------------------------------------------
+ * Cost model / dispatch rule.  Replaces proj/include/gnstk/costmodel.hpp:33-47
+ * (proj/src/costmodel.cpp:25-64).  method 0 = simultaneous (weight-grad form),
+ * 1 = frobenius (Gram form); criterion 0 = IO, 1 = FLOPS.  out[2] =
+ * {weight_grad, grad_norms}.
+ */
+gnsb_status gnsb_flops(int64_t b, int64_t t, int64_t k, int64_t l, int32_t method, int64_t* out);
+gnsb_status gnsb_io_values(int64_t b, int64_t t, int64_t k, int64_t l, int32_t method, int64_t* out);
+gnsb_status gnsb_crossover_t(int64_t k, int64_t l, int32_t criterion, double* out);
+
+/* ------------------------------------------------------------------------
+ * Synthetic workload generators (SURVEY.md §8(d) recipes), bit-identical
+ * with the CPU oracle's.  Fill device buffers of dtype dt (gamma/beta as the
+ * statistics dtype).  Any pointer may be NULL.
+ *   LN:     x = Z(s0,idx) + 0.5 Z(s0+1,row); dy = (Z(s0+2,t*D+d) + sigma Z(s0+3,idx)) / B_div;
+ *           gamma = 1 + 0.1 Z(s0+4,d); beta = 0.1 Z(s0+5,d)
+ *   linear: x = Z(s0,idx); dy = (Z(s0+1,t*L+l) + Z(s0+2,idx)) / (B_div*sqrt(T))
+ * idx/row use the GLOBAL example index b + b_offset (batch sharding).
+ */
+gnsb_status gnsb_synth_ln(void* x, void* dy, void* gamma, void* beta, int64_t B, int64_t T, int64_t D,
+                          int64_t b_offset, int64_t B_div, float sigma, uint64_t stream0, gnsb_dtype dt, void* stream);
+gnsb_status gnsb_synth_linear(void* x, void* dy, int64_t B, int64_t T, int64_t K, int64_t L, int64_t b_offset,
+                              int64_t B_div, uint64_t stream0, gnsb_dtype dt, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GNSB_H */

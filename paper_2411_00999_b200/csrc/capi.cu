@@ -1,0 +1,430 @@
+// capi.cu — the extern "C" boundary (include/gnsb.h): argument validation in
+// the reference's wording, dtype dispatch, and the small device kernels that
+// do not deserve their own file (squared norm, GNS accumulator).
+#include <math_constants.h>
+
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/gnsb.h"
+#include "common.cuh"
+#include "internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+gnsb_status fail(gnsb_status s, const std::string& msg) {
+    g_err = msg;
+    return s;
+}
+gnsb_status cuda_fail(cudaError_t e, const char* where) {
+    g_err = std::string("cuda: ") + where + ": " + cudaGetErrorString(e);
+    return GNSB_ECUDA;
+}
+
+gnsb_status need_device() {
+    int n = 0;
+    const cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        g_err = "cuda: no CUDA device available (the B200 path has no CPU fallback)";
+        return GNSB_ECUDA;
+    }
+    return GNSB_OK;
+}
+
+size_t stat_size(gnsb_dtype dt) { return dt == GNSB_F64 ? 8 : 4; }
+
+// splitmix64 + mix_seed (proj/include/gnstk/rng.hpp:19-24, 42-45)
+uint64_t sm64(uint64_t* st) {
+    uint64_t z = (*st += 0x9e3779b97f4a7c15ull);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+uint64_t mix_seed(uint64_t seed, uint64_t tag) {
+    uint64_t s = seed ^ (0x9e3779b97f4a7c15ull * (tag + 1));
+    return sm64(&s);
+}
+gnsb::SynthSeeds seeds(uint64_t stream0) {
+    gnsb::SynthSeeds s;
+    for (int k = 0; k < 8; ++k) s.s[k] = mix_seed(2411u, stream0 + (uint64_t)k);
+    return s;
+}
+
+// layers.cpp:39-42
+double corrected_mean_sqnorm(double sum_sq, int64_t batch) {
+    const double b = (double)batch;
+    return sum_sq / b * (b * b);
+}
+
+}  // namespace
+
+namespace gnsb {
+
+int device_sm_count() {
+    static std::mutex mu;
+    static int cache[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev < 64 && cache[dev]) return cache[dev];
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    if (v <= 0) v = 1;
+    if (dev < 64) cache[dev] = v;
+    return v;
+}
+
+// ------------------------------------------------------- squared norm ----
+template <typename V>
+__global__ void __launch_bounds__(1024) sqnorm_kernel(const V* v, int64_t n, double* out) {
+    __shared__ double red[32];
+    double acc = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const double x = (double)v[i];
+        acc += x * x;
+    }
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+        t = warp_sum(t);
+        if (threadIdx.x == 0) *out = t;
+    }
+}
+
+// ------------------------------------------------------- GNS accumulator --
+struct GnsStepArgs {
+    const double* sums;
+    int n;
+    int64_t B;
+    double alpha;
+    gnsb_ema_state* state;
+    double* out_groups;
+    double* out_layers;
+    int8_t types[512];
+};
+
+__device__ double d_corrected(double sum_sq, int64_t batch) {
+    const double b = (double)batch;
+    return sum_sq / b * (b * b);
+}
+
+// Single thread: O(#layers) scalar work in the reference's operation order
+// (trainer.cpp:363-415, gns.cpp:31-89).
+__global__ void gns_step_kernel(const __grid_constant__ GnsStepArgs a) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const double bb = (double)a.B, bs = 1.0;
+    for (int grp = 0; grp < 4; ++grp) {
+        const int filter = grp - 1;  // -1 total, 0 embedding, 1 linear, 2 layernorm
+        bool any = false;
+        double big = 0.0, small = 0.0;
+        for (int l = 0; l < a.n; ++l) {
+            if (filter >= 0 && a.types[l] != filter) continue;
+            const double* s = a.sums + 4 * l;
+            double lb = 0.0, ls = 0.0;
+            lb += s[3];
+            lb += s[2];
+            ls += d_corrected(s[1], a.B);
+            ls += d_corrected(s[0], a.B);
+            if (grp == 0 && a.out_layers) {
+                a.out_layers[2 * l + 0] = (bb * lb - bs * ls) / (bb - bs);
+                a.out_layers[2 * l + 1] = (ls - lb) / (1.0 / bs - 1.0 / bb);
+            }
+            big += lb;
+            small += ls;
+            any = true;
+        }
+        double* o = a.out_groups + 4 * grp;
+        if (!any) {
+            o[0] = o[1] = o[2] = o[3] = CUDART_NAN;
+            continue;
+        }
+        const double g2 = (bb * big - bs * small) / (bb - bs);
+        const double s = (small - big) / (1.0 / bs - 1.0 / bb);
+        gnsb_ema_state* eg = a.state + 2 * grp;
+        gnsb_ema_state* es = eg + 1;
+        eg->alpha = a.alpha;
+        es->alpha = a.alpha;
+        eg->value = eg->count == 0 ? g2 : (1.0 - a.alpha) * eg->value + a.alpha * g2;
+        es->value = es->count == 0 ? s : (1.0 - a.alpha) * es->value + a.alpha * s;
+        ++eg->count;
+        ++es->count;
+        o[0] = g2;
+        o[1] = s;
+        const bool def = fabs(eg->value) >= 1e-12;
+        o[2] = def ? es->value / eg->value : 0.0;
+        o[3] = def ? 1.0 : 0.0;
+    }
+}
+
+}  // namespace gnsb
+
+extern "C" {
+
+const char* gnsb_version(void) { return "gnsb 0.1 (sm_100a)"; }
+const char* gnsb_last_error(void) { return g_err.c_str(); }
+
+gnsb_status gnsb_ln_fwd(const void* x, const void* gamma, const void* beta, void* y, void* mean, void* rstd, void* xhat,
+                        int64_t rows, int64_t D, double eps, gnsb_dtype dt, void* stream) {
+    if (!(eps > 0.0)) return fail(GNSB_EINVAL, "layers: epsilon must be positive");          // layers.cpp:192
+    if (D < 2) return fail(GNSB_EINVAL, "layers: layernorm needs trailing extent >= 2");     // layers.cpp:194
+    if (rows < 0) return fail(GNSB_EINVAL, "layers: negative row count");
+    if (gnsb_status s = need_device()) return s;
+    if (rows == 0) return GNSB_OK;
+    if (!x || !gamma || !beta) return fail(GNSB_EINVAL, "layers: null input pointer");
+    gnsb::LnFwdCall c{x, gamma, beta, y, mean, rstd, xhat, rows, D, eps};
+    const char* why = nullptr;
+    cudaError_t ce = cudaSuccess;
+    int rc = 1;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    switch (dt) {
+        case GNSB_F32: rc = gnsb::ln_fwd_run<float>(c, st, &why, &ce); break;
+        case GNSB_BF16: rc = gnsb::ln_fwd_run<__nv_bfloat16>(c, st, &why, &ce); break;
+        case GNSB_F64: rc = gnsb::ln_fwd_run<double>(c, st, &why, &ce); break;
+        default: return fail(GNSB_EINVAL, "layers: unknown dtype");
+    }
+    if (rc == 1) return fail(GNSB_EINVAL, why ? why : "layers: invalid argument");
+    if (rc == 2) return cuda_fail(ce, "ln_fwd launch");
+    return GNSB_OK;
+}
+
+gnsb_status gnsb_ln_bwd_workspace_size(int64_t B, int64_t M, int64_t D, gnsb_dtype dt, size_t* bytes) {
+    if (!bytes) return fail(GNSB_EINVAL, "layers: null output pointer");
+    if (B < 0 || M < 0 || D < 1) return fail(GNSB_EINVAL, "layers: invalid extents");
+    if (gnsb_status s = need_device()) return s;
+    const char* why = nullptr;
+    int rc = 1;
+    switch (dt) {
+        case GNSB_F32: rc = gnsb::ln_bwd_workspace<float>(B, M, D, bytes, &why); break;
+        case GNSB_BF16: rc = gnsb::ln_bwd_workspace<__nv_bfloat16>(B, M, D, bytes, &why); break;
+        case GNSB_F64: rc = gnsb::ln_bwd_workspace<double>(B, M, D, bytes, &why); break;
+        default: return fail(GNSB_EINVAL, "layers: unknown dtype");
+    }
+    if (rc) return fail(GNSB_EINVAL, why ? why : "layers: invalid argument");
+    return GNSB_OK;
+}
+
+gnsb_status gnsb_ln_bwd_geometry(int64_t B, int64_t M, int64_t D, gnsb_dtype dt, int32_t* grid, int32_t* threads,
+                                 int32_t* stages) {
+    if (gnsb_status s = need_device()) return s;
+    int g = 0, t = 0, st = 0, rc = 1;
+    switch (dt) {
+        case GNSB_F32: rc = gnsb::ln_bwd_geometry<float>(B, M, D, &g, &t, &st); break;
+        case GNSB_BF16: rc = gnsb::ln_bwd_geometry<__nv_bfloat16>(B, M, D, &g, &t, &st); break;
+        case GNSB_F64: rc = gnsb::ln_bwd_geometry<double>(B, M, D, &g, &t, &st); break;
+        default: return fail(GNSB_EINVAL, "layers: unknown dtype");
+    }
+    if (rc) return fail(GNSB_EINVAL, "layers: unsupported shape");
+    if (grid) *grid = g;
+    if (threads) *threads = t;
+    if (stages) *stages = st;
+    return GNSB_OK;
+}
+
+gnsb_status gnsb_ln_bwd(const void* x, const void* mean, const void* rstd, const void* dy, const void* gamma, void* dx,
+                        void* dgamma, void* dbeta, double* raw_g, double* raw_b, double* sums, int32_t with_norms,
+                        int64_t B, int64_t M, int64_t D, gnsb_dtype dt, void* ws, size_t ws_bytes, void* stream) {
+    if (B == 0) return fail(GNSB_EINVAL, "layers: empty batch");  // layers.cpp:239
+    if (B < 0 || M < 0) return fail(GNSB_EINVAL, "layers: invalid extents");
+    if (D < 1) return fail(GNSB_EINVAL, "layers: gradient trailing extent does not match gamma");
+    if (dt != GNSB_F32 && dt != GNSB_BF16 && dt != GNSB_F64) return fail(GNSB_EINVAL, "layers: unknown dtype");
+    if (gnsb_status s = need_device()) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (M == 0) {  // no rows: every gradient and norm is zero (layers.cpp:248-275 with an empty loop)
+        cudaError_t e = cudaSuccess;
+        if (dgamma) e = cudaMemsetAsync(dgamma, 0, (size_t)D * stat_size(dt), st);
+        if (e == cudaSuccess && dbeta) e = cudaMemsetAsync(dbeta, 0, (size_t)D * stat_size(dt), st);
+        if (with_norms) {
+            if (e == cudaSuccess && raw_g) e = cudaMemsetAsync(raw_g, 0, (size_t)B * 8, st);
+            if (e == cudaSuccess && raw_b) e = cudaMemsetAsync(raw_b, 0, (size_t)B * 8, st);
+            if (e == cudaSuccess && sums) e = cudaMemsetAsync(sums, 0, 4 * 8, st);
+        }
+        return e == cudaSuccess ? GNSB_OK : cuda_fail(e, "memset");
+    }
+    if (!x || !rstd || !dy || !gamma || !dgamma || !dbeta || !ws)
+        return fail(GNSB_EINVAL, "layers: null input pointer");
+    gnsb::LnBwdCall c{x, mean, rstd, dy, gamma, dx, dgamma, dbeta, raw_g, raw_b, sums, with_norms ? 1 : 0,
+                      B, M, D, ws, ws_bytes};
+    const char* why = nullptr;
+    cudaError_t ce = cudaSuccess;
+    int rc = 1;
+    switch (dt) {
+        case GNSB_F32: rc = gnsb::ln_bwd_run<float>(c, st, &why, &ce); break;
+        case GNSB_BF16: rc = gnsb::ln_bwd_run<__nv_bfloat16>(c, st, &why, &ce); break;
+        case GNSB_F64: rc = gnsb::ln_bwd_run<double>(c, st, &why, &ce); break;
+        default: break;
+    }
+    if (rc == 1) return fail(GNSB_EINVAL, why ? why : "layers: invalid argument");
+    if (rc == 2) return cuda_fail(ce, "ln_bwd launch");
+    return GNSB_OK;
+}
+
+gnsb_status gnsb_sqnorm(const void* v, int64_t n, gnsb_dtype dt, double* out, void* stream) {
+    if (n < 0 || !out) return fail(GNSB_EINVAL, "gns: invalid sqnorm arguments");
+    if (gnsb_status s = need_device()) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (dt == GNSB_F64)
+        gnsb::sqnorm_kernel<double><<<1, 1024, 0, st>>>(static_cast<const double*>(v), n, out);
+    else if (dt == GNSB_F32)
+        gnsb::sqnorm_kernel<float><<<1, 1024, 0, st>>>(static_cast<const float*>(v), n, out);
+    else
+        return fail(GNSB_EINVAL, "gns: sqnorm expects fp32 or fp64 data");
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? GNSB_OK : cuda_fail(e, "sqnorm launch");
+}
+
+// ---------------------------------------------------------------- GNS ----
+gnsb_status gnsb_estimate_g2(const gnsb_grad_stats* st, double* out) {
+    if (st->b_small < 1) return fail(GNSB_EINVAL, "gns: b_small must be >= 1");
+    if (st->b_big <= st->b_small) return fail(GNSB_EINVAL, "gns: b_big must exceed b_small");
+    if (st->n_small < 1) return fail(GNSB_EINVAL, "gns: n_small must be >= 1");
+    const double bb = (double)st->b_big, bs = (double)st->b_small;
+    *out = (bb * st->g_big_sqnorm - bs * st->g_small_sqnorm_mean) / (bb - bs);
+    return GNSB_OK;
+}
+
+gnsb_status gnsb_estimate_s(const gnsb_grad_stats* st, double* out) {
+    if (st->b_small < 1) return fail(GNSB_EINVAL, "gns: b_small must be >= 1");
+    if (st->b_big <= st->b_small) return fail(GNSB_EINVAL, "gns: b_big must exceed b_small");
+    if (st->n_small < 1) return fail(GNSB_EINVAL, "gns: n_small must be >= 1");
+    const double bb = (double)st->b_big, bs = (double)st->b_small;
+    *out = (st->g_small_sqnorm_mean - st->g_big_sqnorm) / (1.0 / bs - 1.0 / bb);
+    return GNSB_OK;
+}
+
+void gnsb_make_gns_estimate(double g2, double s, gnsb_gns_estimate* out) {
+    out->g2 = g2;
+    out->s = s;
+    out->b_simple = 0.0;
+    out->b_simple_defined = 0;
+    if (std::fabs(g2) >= 1e-12) {  // kGnsRatioGuard, gns.hpp:34
+        out->b_simple = s / g2;
+        out->b_simple_defined = 1;
+    }
+}
+
+gnsb_status gnsb_ema_update(gnsb_ema_state* st, double x) {
+    if (!(st->alpha > 0.0) || st->alpha > 1.0) return fail(GNSB_EINVAL, "gns: ema alpha must be in (0, 1]");
+    if (st->count == 0)
+        st->value = x;
+    else
+        st->value = (1.0 - st->alpha) * st->value + st->alpha * x;
+    ++st->count;
+    return GNSB_OK;
+}
+
+gnsb_status gnsb_smoothed_gns(const gnsb_ema_state* g2, const gnsb_ema_state* s, gnsb_gns_estimate* out) {
+    if (g2->count < 1 || s->count < 1)
+        return fail(GNSB_EINVAL, "gns: smoothed_gns needs at least one sample in each state");
+    gnsb_make_gns_estimate(g2->value, s->value, out);
+    return GNSB_OK;
+}
+
+gnsb_status gnsb_aggregate(const gnsb_grad_stats* stats, const int32_t* types, int32_t n, int32_t group,
+                           gnsb_grad_stats* out) {
+    bool first = true;
+    for (int32_t i = 0; i < n; ++i) {
+        if (group >= 0 && types[i] != group) continue;
+        if (first) {
+            *out = stats[i];
+            out->g_big_sqnorm = 0.0;
+            out->g_small_sqnorm_mean = 0.0;
+            first = false;
+        } else if (stats[i].b_big != out->b_big || stats[i].b_small != out->b_small ||
+                   stats[i].n_small != out->n_small) {
+            return fail(GNSB_EINVAL, "gns: aggregate requires matching batch sizes across layers");
+        }
+        out->g_big_sqnorm += stats[i].g_big_sqnorm;
+        out->g_small_sqnorm_mean += stats[i].g_small_sqnorm_mean;
+    }
+    if (first) return fail(GNSB_EINVAL, "gns: aggregate over an empty selection");
+    return GNSB_OK;
+}
+
+gnsb_status gnsb_gns_step(const double* layer_sums, const int32_t* layer_types, int32_t n_layers, int64_t B,
+                          double alpha, gnsb_ema_state* state, double* out_groups, double* out_layers, void* stream) {
+    if (B < 2) return fail(GNSB_EINVAL, "trainer: per-example estimation needs batch >= 2");
+    if (!(alpha > 0.0) || alpha > 1.0) return fail(GNSB_EINVAL, "gns: ema alpha must be in (0, 1]");
+    if (n_layers < 1 || n_layers > 512) return fail(GNSB_EINVAL, "gns: layer count must be in [1, 512]");
+    if (!layer_sums || !layer_types || !state || !out_groups) return fail(GNSB_EINVAL, "gns: null pointer");
+    if (gnsb_status s = need_device()) return s;
+    gnsb::GnsStepArgs a{};
+    a.sums = layer_sums;
+    a.n = n_layers;
+    a.B = B;
+    a.alpha = alpha;
+    a.state = state;
+    a.out_groups = out_groups;
+    a.out_layers = out_layers;
+    for (int i = 0; i < n_layers; ++i) {
+        if (layer_types[i] < 0 || layer_types[i] > 2) return fail(GNSB_EINVAL, "gns: unknown layer type");
+        a.types[i] = (int8_t)layer_types[i];
+    }
+    gnsb::gns_step_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? GNSB_OK : cuda_fail(e, "gns_step launch");
+}
+
+// ------------------------------------------------------------ costmodel ---
+static gnsb_status cost_check(int64_t b, int64_t t, int64_t k, int64_t l) {
+    if (b < 1 || t < 1 || k < 1 || l < 1) return fail(GNSB_EINVAL, "costmodel: shape dims must be positive");
+    return GNSB_OK;
+}
+
+gnsb_status gnsb_flops(int64_t b, int64_t t, int64_t k, int64_t l, int32_t method, int64_t* out) {
+    if (gnsb_status s = cost_check(b, t, k, l)) return s;
+    if (method == 0) {  // costmodel.cpp:25-37
+        out[0] = b * k * l * (2 * t - 1) + k * l * (b - 1);
+        out[1] = b * k * l + b * (k * l - 1);
+    } else {
+        out[0] = k * l * (2 * b * t - 1);
+        out[1] = b * t * t * (2 * k + 2 * l - 2) + b * t * t;
+    }
+    return GNSB_OK;
+}
+
+gnsb_status gnsb_io_values(int64_t b, int64_t t, int64_t k, int64_t l, int32_t method, int64_t* out) {
+    if (gnsb_status s = cost_check(b, t, k, l)) return s;
+    if (method == 0) {  // costmodel.cpp:39-51
+        out[0] = b * k * l + b * k * t + b * l * t;
+        out[1] = b * k * l + b;
+    } else {
+        out[0] = b * k * t + b * l * t + k * l;
+        out[1] = 2 * b * t * t + b;
+    }
+    return GNSB_OK;
+}
+
+gnsb_status gnsb_crossover_t(int64_t k, int64_t l, int32_t criterion, double* out) {
+    if (k < 1 || l < 1) return fail(GNSB_EINVAL, "costmodel: dims must be positive");
+    const double kd = (double)k, ld = (double)l;  // costmodel.cpp:58-64
+    *out = criterion == 0 ? std::sqrt(2.0 * kd * ld) / 2.0 : std::sqrt((2.0 * kd * ld - 1.0) / (2.0 * kd + 2.0 * ld - 1.0));
+    return GNSB_OK;
+}
+
+// ------------------------------------------------------------- synthetic --
+gnsb_status gnsb_synth_ln(void* x, void* dy, void* gamma, void* beta, int64_t B, int64_t T, int64_t D,
+                          int64_t b_offset, int64_t B_div, float sigma, uint64_t stream0, gnsb_dtype dt, void* stream) {
+    if (B < 0 || T < 0 || D < 1 || B_div < 1) return fail(GNSB_EINVAL, "synth: invalid extents");
+    if (gnsb_status s = need_device()) return s;
+    const cudaError_t e = gnsb::launch_synth_ln((int)dt, x, dy, gamma, beta, B, T, D, b_offset, (float)B_div, sigma,
+                                                seeds(stream0), static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? GNSB_OK : cuda_fail(e, "synth_ln launch");
+}
+
+gnsb_status gnsb_synth_linear(void* x, void* dy, int64_t B, int64_t T, int64_t K, int64_t L, int64_t b_offset,
+                              int64_t B_div, uint64_t stream0, gnsb_dtype dt, void* stream) {
+    if (B < 0 || T < 1 || K < 1 || L < 1 || B_div < 1) return fail(GNSB_EINVAL, "synth: invalid extents");
+    if (gnsb_status s = need_device()) return s;
+    const float scale = (float)B_div * sqrtf((float)T);
+    const cudaError_t e = gnsb::launch_synth_linear((int)dt, x, dy, B, T, K, L, b_offset, scale, seeds(stream0),
+                                                    static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? GNSB_OK : cuda_fail(e, "synth_linear launch");
+}
+
+}  // extern "C"

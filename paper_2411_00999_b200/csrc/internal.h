@@ -1,0 +1,44 @@
+// internal.h — launcher declarations shared between the kernel translation
+// units and the C-ABI layer (capi.cu).  Not part of the public interface.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace gnsb {
+
+struct SynthSeeds {
+    uint64_t s[8];  // mix_seed(2411, stream0 + k), k = 0..7
+};
+
+cudaError_t launch_synth_ln(int dt, void* x, void* dy, void* gamma, void* beta, int64_t B, int64_t T, int64_t D,
+                            int64_t b_off, float bdiv, float sigma, SynthSeeds s, cudaStream_t st);
+cudaError_t launch_synth_linear(int dt, void* x, void* dy, int64_t B, int64_t T, int64_t K, int64_t L, int64_t b_off,
+                                float scale, SynthSeeds s, cudaStream_t st);
+
+// LayerNorm forward / backward (ln_launch.cuh, instantiated per dtype)
+struct LnFwdCall {
+    const void* x; const void* gamma; const void* beta;
+    void* y; void* mean; void* rstd; void* xhat;
+    int64_t N, D; double eps;
+};
+struct LnBwdCall {
+    const void* x; const void* mean; const void* rstd; const void* dy; const void* gamma;
+    void* dx; void* dgamma; void* dbeta;
+    double* raw_g; double* raw_b; double* sums;
+    int norms;
+    int64_t B, M, D;
+    void* ws; size_t ws_bytes;
+};
+
+// Returns 0 ok, 1 invalid (message in *why), 2 CUDA error (cudaError_t in *cerr).
+template <typename T> int ln_fwd_run(const LnFwdCall& c, cudaStream_t st, const char** why, cudaError_t* cerr);
+template <typename T> int ln_bwd_run(const LnBwdCall& c, cudaStream_t st, const char** why, cudaError_t* cerr);
+template <typename T> int ln_bwd_workspace(int64_t B, int64_t M, int64_t D, size_t* bytes, const char** why);
+// launch geometry actually used (for reporting): grid, threads, stages
+template <typename T> int ln_bwd_geometry(int64_t B, int64_t M, int64_t D, int* grid, int* threads, int* stages);
+
+int device_sm_count();
+
+}  // namespace gnsb

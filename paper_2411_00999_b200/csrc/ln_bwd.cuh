@@ -1,0 +1,489 @@
+// ln_bwd.cuh — fused LayerNorm backward + per-example ||dgamma_b||^2, ||dbeta_b||^2
+// (and its plain twin, NORMS=false) for sm_100a.
+//
+// Semantics: gnstk::layernorm_backward_simultaneous (proj/src/layers.cpp:231-298):
+//   gamma'_b = sum_m xhat*g, beta'_b = sum_m g          (per example, :251-258)
+//   raw_b    = ||gamma'_b||^2, ||beta'_b||^2            (square AFTER the sum, :259-262)
+//   dgamma   = sum_b gamma'_b, dbeta = sum_b beta'_b     (:265-268)
+//   dx       = rstd*(h - mean(h) - xhat*mean(h*xhat)), h = gamma*g   (:277-296)
+//
+// Design (one HBM pass over x/xhat, dy; one write of dx):
+//   * persistent cooperative grid, one CTA per SM; CTA c owns the contiguous
+//     row range [c*N/grid, (c+1)*N/grid) (rows of an example are contiguous);
+//   * one producer warp streams R-row stages of x and dy into a shared-memory
+//     ring with 1-D TMA (cp.async.bulk, L2 evict_first) signalled on mbarriers;
+//     mean/rstd ride along in the same stage;
+//   * consumer warps form G row groups of GW warps; a thread owns VPT 16-byte
+//     column vectors for the whole kernel, so the per-example dgamma/dbeta
+//     partials accumulate over the sequence axis in registers;
+//   * row reductions mean(h), mean(h*xhat): warp shuffles + one named barrier
+//     per group per stage (RPG rows batched per barrier);
+//   * at each example boundary a group flushes its register partials to a slot
+//     (cta + example, group) of an L2-resident workspace;
+//   * stage 2 after a software grid barrier: column chunks sum the slots of
+//     each example in fixed (cta, group) order -> gamma'_b; square and reduce
+//     over D in fp64 -> per-(example, chunk) partial norms; fixed-order sum
+//     over b -> dgamma/dbeta;
+//   * the last CTA (ticket) folds chunk partials into raw_b and the scalar sums
+//     and resets the workspace counters.  No float atomics anywhere: results
+//     are bitwise deterministic run to run.
+#pragma once
+
+#include "common.cuh"
+
+namespace gnsb {
+
+struct LnBwdArgs {
+    const void* x;      // x rows (HAS_MEAN) or xhat rows, [N, D] of T
+    const void* mean;   // [N] Acc, only when HAS_MEAN
+    const void* rstd;   // [N] Acc
+    const void* dy;     // [N, D] of T
+    const void* gamma;  // [D] Acc
+    void* dx;           // [N, D] of T (may be null: skip dx)
+    void* dgamma;       // [D] Acc
+    void* dbeta;        // [D] Acc
+    double* raw_g;      // [B] or null
+    double* raw_b;      // [B] or null
+    double* sums;       // [4] or null: sum raw_g, sum raw_b, ||dgamma||^2, ||dbeta||^2
+    int64_t B, M, N, D;
+    int Dp;             // smem row stride in elements (D rounded up to the vector width)
+    int stages;         // ring depth
+    int aligned;        // 1: rows are 16-byte aligned -> TMA producer
+    void* partial;      // [(grid + B) * G][2][Dp] Acc
+    double* q;          // [B][nchunks][2]
+    double* qbig;       // [nchunks][2]
+    double* rawws;      // [B][2]
+    unsigned* counters; // [2] grid barrier, final ticket (zero on entry, zero on exit)
+    int nchunks;
+};
+
+constexpr int kChunk = 16;  // stage-2 column chunk (half a warp)
+
+template <typename T, int GW, int VPT, int G, int RPG>
+struct LnBwdCfg {
+    using Acc = typename Traits<T>::Acc;
+    static constexpr int W = Traits<T>::W;
+    static constexpr int kConsumerWarps = GW * G;
+    static constexpr int kThreads = (kConsumerWarps + 1) * 32;
+    static constexpr int R = G * RPG;           // rows per stage
+    static constexpr int GT = GW * 32;          // threads per row group
+    static constexpr int kMaxVec = GT * VPT;    // vectors per row covered
+    static constexpr int kRedElems = 2 * G * GW * 2 * RPG;
+    // byte offsets inside dynamic shared memory
+    static __host__ __device__ constexpr size_t bars_bytes(int S) { return (size_t)16 * S; }
+    static __host__ __device__ constexpr size_t red_off(int S) { return (bars_bytes(S) + 15) / 16 * 16; }
+    static __host__ __device__ constexpr size_t stats_off(int S) {
+        return red_off(S) + (size_t)kRedElems * sizeof(Acc);
+    }
+    static __host__ __device__ constexpr size_t gam_off(int S) {
+        return (stats_off(S) + (size_t)S * R * 2 * sizeof(Acc) + 15) / 16 * 16;
+    }
+    static __host__ __device__ constexpr size_t rows_off(int S, int Dp) {
+        return (gam_off(S) + (size_t)Dp * sizeof(Acc) + 127) / 128 * 128;
+    }
+    static __host__ __device__ constexpr size_t stage_row_bytes(int Dp) { return (size_t)2 * R * Dp * sizeof(T); }
+    static __host__ __device__ constexpr size_t smem_bytes(int S, int Dp) {
+        // the ring doubles as the stage-2 scratch (16 B per thread)
+        const size_t ring = (size_t)S * stage_row_bytes(Dp);
+        const size_t scratch = (size_t)16 * kThreads;
+        return rows_off(S, Dp) + (ring > scratch ? ring : scratch);
+    }
+};
+
+template <typename T, int GW, int VPT, int G, int RPG, bool HAS_MEAN, bool NORMS>
+__global__ void __launch_bounds__(LnBwdCfg<T, GW, VPT, G, RPG>::kThreads, 1) ln_bwd_kernel(LnBwdArgs a) {
+    using C = LnBwdCfg<T, GW, VPT, G, RPG>;
+    using Acc = typename C::Acc;
+    constexpr int W = C::W;
+    constexpr int R = C::R;
+    constexpr int GT = C::GT;
+    constexpr int NCW = C::kConsumerWarps;
+
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int S = a.stages;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* empty = full + S;
+    Acc* red = reinterpret_cast<Acc*>(smem + C::red_off(S));
+    Acc* stats = reinterpret_cast<Acc*>(smem + C::stats_off(S));
+    Acc* gam_s = reinterpret_cast<Acc*>(smem + C::gam_off(S));
+    T* ring = reinterpret_cast<T*>(smem + C::rows_off(S, a.Dp));
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int grid = gridDim.x, cta = blockIdx.x;
+    const int64_t N = a.N, M = a.M, D = a.D;
+    const int Dp = a.Dp;
+    const int NVp = Dp / W;  // vectors per (padded) row
+    const int64_t r_begin = (int64_t)cta * N / grid, r_end = (int64_t)(cta + 1) * N / grid;
+    const int64_t n_stage = (r_end - r_begin + R - 1) / R;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NCW);
+        }
+        fence_mbar_init();
+    }
+    {  // gamma lives in shared memory (zero in the pad columns)
+        const Acc* gg = static_cast<const Acc*>(a.gamma);
+        for (int i = threadIdx.x; i < a.Dp; i += blockDim.x) gam_s[i] = i < a.D ? gg[i] : Acc(0);
+    }
+    if (!a.aligned) {  // padded rows: the pad columns must read as zero
+        uint4* p = reinterpret_cast<uint4*>(ring);
+        const size_t n16 = (size_t)S * C::stage_row_bytes(Dp) / 16;
+        for (size_t i = threadIdx.x; i < n16; i += blockDim.x) p[i] = make_uint4(0, 0, 0, 0);
+    }
+    __syncthreads();
+
+    if (warp == NCW) {
+        // ------------------------------------------------------- producer --
+        const T* xg = static_cast<const T*>(a.x);
+        const T* dyg = static_cast<const T*>(a.dy);
+        const Acc* meang = static_cast<const Acc*>(a.mean);
+        const Acc* rstdg = static_cast<const Acc*>(a.rstd);
+        const uint64_t pol = policy_evict_first();
+        for (int64_t it = 0; it < n_stage; ++it) {
+            const int slot = (int)(it % S);
+            const uint32_t ph = (uint32_t)((it / S) & 1);
+            mbar_wait(&empty[slot], ph ^ 1u);
+            const int64_t r0 = r_begin + it * R;
+            const int nr = (int)((r_end - r0) < (int64_t)R ? (r_end - r0) : (int64_t)R);
+            T* sx = ring + (size_t)slot * 2 * R * Dp;
+            T* sdy = sx + (size_t)R * Dp;
+            if (a.aligned) {
+                if (lane == 0) {
+                    const uint32_t bytes = (uint32_t)(nr * D * (int64_t)sizeof(T));
+                    mbar_expect_tx(&full[slot], 2 * bytes);
+                    bulk_g2s(sx, xg + r0 * D, bytes, &full[slot], pol);
+                    bulk_g2s(sdy, dyg + r0 * D, bytes, &full[slot], pol);
+                }
+            } else {
+                const int64_t ne = (int64_t)nr * D;
+                for (int64_t e = lane; e < ne; e += 32) {
+                    const int64_t rr = e / D, cc = e - rr * D;
+                    sx[rr * Dp + cc] = xg[r0 * D + e];
+                    sdy[rr * Dp + cc] = dyg[r0 * D + e];
+                }
+            }
+            for (int j = lane; j < nr; j += 32) {
+                stats[((size_t)slot * R + j) * 2 + 0] = HAS_MEAN ? meang[r0 + j] : Acc(0);
+                stats[((size_t)slot * R + j) * 2 + 1] = rstdg[r0 + j];
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[slot]);
+        }
+    } else {
+        // ------------------------------------------------------ consumers --
+        const int g = warp / GW, wig = warp % GW;
+        const int tig = wig * 32 + lane;
+        Acc* partial = static_cast<Acc*>(a.partial);
+        T* dxg = static_cast<T*>(a.dx);
+        const Acc invD = Acc(1) / Acc(D);
+
+        // gamma vector k of this thread, from shared memory
+        auto load_gam = [&](int k, Acc* out) {
+            const int v = tig + k * GT;
+            const Acc* p = gam_s + (size_t)(v < NVp ? v : 0) * W;
+#pragma unroll
+            for (int e = 0; e < W; e += (int)(16 / sizeof(Acc))) {
+                if constexpr (sizeof(Acc) == 4) {
+                    const float4 q = *reinterpret_cast<const float4*>(p + e);
+                    out[e] = q.x; out[e + 1] = q.y; out[e + 2] = q.z; out[e + 3] = q.w;
+                } else {
+                    const double2 q = *reinterpret_cast<const double2*>(p + e);
+                    out[e] = q.x; out[e + 1] = q.y;
+                }
+            }
+        };
+        Acc ag[VPT][W], ab[VPT][W];
+#pragma unroll
+        for (int k = 0; k < VPT; ++k)
+#pragma unroll
+            for (int e = 0; e < W; ++e) ag[k][e] = ab[k][e] = Acc(0);
+
+        int64_t cur_ex = r_begin / M;
+        int64_t next_bound = (cur_ex + 1) * M;
+
+        // write this group's register partials to slot (cta + ex, g)
+        auto write_slot = [&](int64_t ex, bool zero) {
+            Acc* base = partial + ((size_t)(cta + ex) * G + g) * 2 * Dp;
+#pragma unroll
+            for (int k = 0; k < VPT; ++k) {
+                const int v = tig + k * GT;
+                if (v < NVp) {
+#pragma unroll
+                    for (int e = 0; e < W; ++e) {
+                        base[(size_t)v * W + e] = zero ? Acc(0) : ag[k][e];
+                        base[(size_t)Dp + (size_t)v * W + e] = zero ? Acc(0) : ab[k][e];
+                    }
+                }
+            }
+        };
+        auto flush_to = [&](int64_t new_ex) {
+            write_slot(cur_ex, false);
+#pragma unroll
+            for (int k = 0; k < VPT; ++k)
+#pragma unroll
+                for (int e = 0; e < W; ++e) ag[k][e] = ab[k][e] = Acc(0);
+            for (int64_t ex = cur_ex + 1; ex < new_ex; ++ex) write_slot(ex, true);
+            cur_ex = new_ex;
+            next_bound = (cur_ex + 1) * M;
+        };
+
+        int rbuf = 0;
+        for (int64_t it = 0; it < n_stage; ++it) {
+            const int slot = (int)(it % S);
+            const uint32_t ph = (uint32_t)((it / S) & 1);
+            mbar_wait(&full[slot], ph);
+            const int64_t r0 = r_begin + it * R;
+            const int nr = (int)((r_end - r0) < (int64_t)R ? (r_end - r0) : (int64_t)R);
+            const T* sx = ring + (size_t)slot * 2 * R * Dp;
+            const T* sdy = sx + (size_t)R * Dp;
+
+            uint4 ux[RPG][VPT], ug[RPG][VPT];
+            Acc mu[RPG], rs[RPG];
+#pragma unroll
+            for (int i = 0; i < RPG; ++i) {
+                const int j = g * RPG + i;
+                const bool valid = j < nr;
+                mu[i] = valid ? stats[((size_t)slot * R + j) * 2 + 0] : Acc(0);
+                rs[i] = valid ? stats[((size_t)slot * R + j) * 2 + 1] : Acc(0);
+#pragma unroll
+                for (int k = 0; k < VPT; ++k) {
+                    const int v = tig + k * GT;
+                    if (valid && v < NVp) {
+                        ux[i][k] = *reinterpret_cast<const uint4*>(sx + (size_t)j * Dp + (size_t)v * W);
+                        ug[i][k] = *reinterpret_cast<const uint4*>(sdy + (size_t)j * Dp + (size_t)v * W);
+                    } else {
+                        ux[i][k] = ug[i][k] = make_uint4(0, 0, 0, 0);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[slot]);  // slot may be refilled now
+
+            Acc s1[RPG], s2[RPG];
+#pragma unroll
+            for (int i = 0; i < RPG; ++i) {
+                const int j = g * RPG + i;
+                const int64_t row = r0 + j;
+                if (j < nr && row >= next_bound) flush_to(row / M);  // group-uniform
+                s1[i] = s2[i] = Acc(0);
+#pragma unroll
+                for (int k = 0; k < VPT; ++k) {
+                    Acc xf[W], gf[W], gm[W];
+                    unpack<T>(ux[i][k], xf);
+                    unpack<T>(ug[i][k], gf);
+                    load_gam(k, gm);
+#pragma unroll
+                    for (int e = 0; e < W; ++e) {
+                        const Acc xh = HAS_MEAN ? (xf[e] - mu[i]) * rs[i] : xf[e];
+                        const Acc h = gm[e] * gf[e];
+                        s1[i] += h;
+                        s2[i] += h * xh;
+                        ag[k][e] += xh * gf[e];
+                        ab[k][e] += gf[e];
+                    }
+                }
+            }
+            // row reductions over the group
+#pragma unroll
+            for (int i = 0; i < RPG; ++i) {
+                s1[i] = warp_sum(s1[i]);
+                s2[i] = warp_sum(s2[i]);
+            }
+            if constexpr (GW > 1) {
+                Acc* rb = red + ((size_t)(rbuf * G + g) * GW) * 2 * RPG;
+                if (lane == 0) {
+#pragma unroll
+                    for (int i = 0; i < RPG; ++i) {
+                        rb[wig * 2 * RPG + 2 * i] = s1[i];
+                        rb[wig * 2 * RPG + 2 * i + 1] = s2[i];
+                    }
+                }
+                named_bar_sync(1 + g, GT);
+#pragma unroll
+                for (int i = 0; i < RPG; ++i) {
+                    Acc t1 = 0, t2 = 0;
+#pragma unroll
+                    for (int w = 0; w < GW; ++w) {
+                        t1 += rb[w * 2 * RPG + 2 * i];
+                        t2 += rb[w * 2 * RPG + 2 * i + 1];
+                    }
+                    s1[i] = t1;
+                    s2[i] = t2;
+                }
+                rbuf ^= 1;
+            }
+            // dx = rstd*(h - mean(h)) - rstd*mean(h*xhat)*xhat
+            if (dxg != nullptr) {
+#pragma unroll
+                for (int i = 0; i < RPG; ++i) {
+                    const int j = g * RPG + i;
+                    if (j >= nr) continue;
+                    const int64_t row = r0 + j;
+                    const Acc c1 = s1[i] * invD;
+                    const Acc c2 = rs[i] * s2[i] * invD;
+#pragma unroll
+                    for (int k = 0; k < VPT; ++k) {
+                        const int v = tig + k * GT;
+                        if (v >= NVp) continue;
+                        Acc xf[W], gf[W], gm[W], o[W];
+                        unpack<T>(ux[i][k], xf);
+                        unpack<T>(ug[i][k], gf);
+                        load_gam(k, gm);
+#pragma unroll
+                        for (int e = 0; e < W; ++e) {
+                            const Acc xh = HAS_MEAN ? (xf[e] - mu[i]) * rs[i] : xf[e];
+                            o[e] = rs[i] * (gm[e] * gf[e] - c1) - c2 * xh;
+                        }
+                        if (a.aligned) {
+                            st_stream(dxg + row * D + (int64_t)v * W, pack<T>(o));
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < W; ++e) {
+                                const int64_t col = (int64_t)v * W + e;
+                                if (col < D) dxg[row * D + col] = from_acc<T>(o[e]);
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        flush_to((r_end - 1) / M + 1);
+    }
+
+    // ------------------------------------------------------------ stage 2 --
+    grid_barrier(&a.counters[0]);
+
+    const Acc* partial = static_cast<const Acc*>(a.partial);
+    Acc* dgam = static_cast<Acc*>(a.dgamma);
+    Acc* dbet = static_cast<Acc*>(a.dbeta);
+    const int nthreads = blockDim.x;
+    const int NB = nthreads / kChunk;
+    const int cl = threadIdx.x % kChunk, bl = threadIdx.x / kChunk;
+    const unsigned hmask = 0xffffu << (lane & 16);
+    double* sred = reinterpret_cast<double*>(smem + C::rows_off(S, Dp));  // ring is free now
+    const int64_t B = a.B;
+    auto cta_of = [&](int64_t r) -> int64_t { return ((r + 1) * grid - 1) / N; };
+
+    for (int chunk = cta; chunk < a.nchunks; chunk += grid) {
+        const int64_t col = (int64_t)chunk * kChunk + cl;
+        const bool cv = col < D;
+        double sg = 0.0, sb = 0.0;
+        for (int64_t b = bl; b < B; b += NB) {
+            const int64_t c0 = cta_of(b * M), c1 = cta_of((b + 1) * M - 1);
+            double vg = 0.0, vb = 0.0;
+            if (cv) {
+                for (int64_t cc = c0; cc <= c1; ++cc) {
+                    const Acc* base = partial + (size_t)(cc + b) * G * 2 * Dp + col;
+#pragma unroll
+                    for (int gg = 0; gg < G; ++gg) {
+                        vg += (double)__ldcg(base + (size_t)gg * 2 * Dp);
+                        vb += (double)__ldcg(base + (size_t)gg * 2 * Dp + Dp);
+                    }
+                }
+            }
+            sg += vg;
+            sb += vb;
+            if constexpr (NORMS) {
+                double qg = vg * vg, qb = vb * vb;
+#pragma unroll
+                for (int o = kChunk / 2; o > 0; o >>= 1) {
+                    qg += __shfl_xor_sync(hmask, qg, o);
+                    qb += __shfl_xor_sync(hmask, qb, o);
+                }
+                if (cl == 0) {
+                    a.q[((size_t)b * a.nchunks + chunk) * 2 + 0] = qg;
+                    a.q[((size_t)b * a.nchunks + chunk) * 2 + 1] = qb;
+                }
+            }
+        }
+        sred[(size_t)bl * kChunk + cl] = sg;
+        sred[(size_t)(NB + bl) * kChunk + cl] = sb;
+        __syncthreads();
+        if (bl == 0) {
+            double tg = 0.0, tb = 0.0;
+            for (int k = 0; k < NB; ++k) {
+                tg += sred[(size_t)k * kChunk + cl];
+                tb += sred[(size_t)(NB + k) * kChunk + cl];
+            }
+            if (cv) {
+                dgam[col] = (Acc)tg;
+                dbet[col] = (Acc)tb;
+            }
+            if constexpr (NORMS) {
+                const double fg = cv ? (double)(Acc)tg : 0.0, fb = cv ? (double)(Acc)tb : 0.0;
+                double qg = fg * fg, qb = fb * fb;
+#pragma unroll
+                for (int o = kChunk / 2; o > 0; o >>= 1) {
+                    qg += __shfl_xor_sync(0xffffu, qg, o);
+                    qb += __shfl_xor_sync(0xffffu, qb, o);
+                }
+                if (cl == 0) {
+                    a.qbig[(size_t)chunk * 2 + 0] = qg;
+                    a.qbig[(size_t)chunk * 2 + 1] = qb;
+                }
+            }
+        }
+        __syncthreads();
+    }
+
+    // ------------------------------------------------------- final ticket --
+    __shared__ unsigned s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned t = atomicAdd(&a.counters[1], 1u);
+        s_last = (t == (unsigned)grid - 1u) ? 1u : 0u;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if constexpr (NORMS) {
+        const int nwarps = nthreads / 32;
+        for (int64_t b = warp; b < B; b += nwarps) {
+            double rg = 0.0, rb = 0.0;
+            for (int ch = lane; ch < a.nchunks; ch += 32) {
+                rg += __ldcg(a.q + ((size_t)b * a.nchunks + ch) * 2 + 0);
+                rb += __ldcg(a.q + ((size_t)b * a.nchunks + ch) * 2 + 1);
+            }
+            rg = warp_sum(rg);
+            rb = warp_sum(rb);
+            if (lane == 0) {
+                a.rawws[b * 2 + 0] = rg;
+                a.rawws[b * 2 + 1] = rb;
+                if (a.raw_g) a.raw_g[b] = rg;
+                if (a.raw_b) a.raw_b[b] = rb;
+            }
+        }
+        __syncthreads();
+        if (warp == 0 && a.sums != nullptr) {
+            double tg = 0.0, tb = 0.0, bg = 0.0, bb = 0.0;
+            for (int64_t b = lane; b < B; b += 32) {
+                tg += a.rawws[b * 2 + 0];
+                tb += a.rawws[b * 2 + 1];
+            }
+            for (int ch = lane; ch < a.nchunks; ch += 32) {
+                bg += __ldcg(a.qbig + (size_t)ch * 2 + 0);
+                bb += __ldcg(a.qbig + (size_t)ch * 2 + 1);
+            }
+            tg = warp_sum(tg);
+            tb = warp_sum(tb);
+            bg = warp_sum(bg);
+            bb = warp_sum(bb);
+            if (lane == 0) {
+                a.sums[0] = tg;
+                a.sums[1] = tb;
+                a.sums[2] = bg;
+                a.sums[3] = bb;
+            }
+        }
+    }
+    if (threadIdx.x == 0) {
+        a.counters[0] = 0u;
+        a.counters[1] = 0u;
+        __threadfence();
+    }
+}
+
+}  // namespace gnsb

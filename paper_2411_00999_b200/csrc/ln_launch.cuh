@@ -1,0 +1,263 @@
+// ln_launch.cuh — host-side planning and launch of the LayerNorm kernels.
+// Included once per row dtype (ln_f32.cu, ln_bf16.cu, ln_f64.cu) so the
+// template instantiations compile in parallel.
+#pragma once
+
+#include <mutex>
+
+#include "internal.h"
+#include "ln_bwd.cuh"
+#include "ln_fwd.cuh"
+
+namespace gnsb {
+
+namespace {
+
+inline int smem_optin_bytes() {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return v;
+}
+
+inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+inline bool ptr16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Per-(kernel, device) "max dynamic smem" attribute, set lazily.
+template <typename K>
+cudaError_t ensure_smem(K kernel, size_t bytes) {
+    static std::mutex mu;
+    static size_t set_for[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev < 64 && set_for[dev] >= bytes) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess && dev < 64) set_for[dev] = bytes;
+    return e;
+}
+
+struct BwdPlan {
+    int Dp = 0, stages = 0, threads = 0, grid = 0, nchunks = 0, G = 0;
+    size_t smem = 0;
+    size_t off_partial = 0, off_q = 0, off_qbig = 0, off_raw = 0, total = 0;
+};
+
+template <typename T, int GW, int VPT, int G, int RPG>
+int plan_bwd(int64_t B, int64_t M, int64_t D, BwdPlan& p, const char** why) {
+    using C = LnBwdCfg<T, GW, VPT, G, RPG>;
+    using Acc = typename Traits<T>::Acc;
+    constexpr int W = Traits<T>::W;
+    p.Dp = (int)((D + W - 1) / W * W);
+    const size_t budget = (size_t)smem_optin_bytes() - 1024;
+    p.stages = 0;
+    for (int s = 8; s >= 1; --s)
+        if (C::smem_bytes(s, p.Dp) <= budget) {
+            p.stages = s;
+            break;
+        }
+    if (p.stages == 0) {
+        *why = "layers: trailing extent too wide for the shared-memory row ring";
+        return 1;
+    }
+    p.smem = C::smem_bytes(p.stages, p.Dp);
+    p.threads = C::kThreads;
+    p.G = G;
+    const int64_t N = B * M;
+    const int sms = device_sm_count();
+    p.grid = (int)(N < sms ? N : sms);
+    if (p.grid < 1) p.grid = 1;
+    p.nchunks = (int)((D + kChunk - 1) / kChunk);
+    size_t off = 256;  // counters
+    p.off_partial = off;
+    off = align_up(off + (size_t)(sms + B) * G * 2 * p.Dp * sizeof(Acc), 256);
+    p.off_q = off;
+    off = align_up(off + (size_t)B * p.nchunks * 2 * sizeof(double), 256);
+    p.off_qbig = off;
+    off = align_up(off + (size_t)p.nchunks * 2 * sizeof(double), 256);
+    p.off_raw = off;
+    off = align_up(off + (size_t)B * 2 * sizeof(double), 256);
+    p.total = off;
+    return 0;
+}
+
+template <typename T, int GW, int VPT, int G, int RPG>
+struct BwdOp {
+    static int plan(int64_t B, int64_t M, int64_t D, BwdPlan& p, const char** why) {
+        return plan_bwd<T, GW, VPT, G, RPG>(B, M, D, p, why);
+    }
+    static int run(const LnBwdCall& c, cudaStream_t st, const char** why, cudaError_t* cerr) {
+        BwdPlan p;
+        if (plan_bwd<T, GW, VPT, G, RPG>(c.B, c.M, c.D, p, why)) return 1;
+        if (c.ws_bytes < p.total) {
+            *why = "layers: workspace too small (query gnsb_ln_bwd_workspace_size)";
+            return 1;
+        }
+        LnBwdArgs a{};
+        a.x = c.x;
+        a.mean = c.mean;
+        a.rstd = c.rstd;
+        a.dy = c.dy;
+        a.gamma = c.gamma;
+        a.dx = c.dx;
+        a.dgamma = c.dgamma;
+        a.dbeta = c.dbeta;
+        a.raw_g = c.raw_g;
+        a.raw_b = c.raw_b;
+        a.sums = c.sums;
+        a.B = c.B;
+        a.M = c.M;
+        a.N = c.B * c.M;
+        a.D = c.D;
+        a.Dp = p.Dp;
+        a.stages = p.stages;
+        a.aligned = ((c.D * (int64_t)sizeof(T)) % 16 == 0) && ptr16(c.x) && ptr16(c.dy) && (c.dx == nullptr || ptr16(c.dx));
+        unsigned char* ws = static_cast<unsigned char*>(c.ws);
+        a.counters = reinterpret_cast<unsigned*>(ws);
+        a.partial = ws + p.off_partial;
+        a.q = reinterpret_cast<double*>(ws + p.off_q);
+        a.qbig = reinterpret_cast<double*>(ws + p.off_qbig);
+        a.rawws = reinterpret_cast<double*>(ws + p.off_raw);
+        a.nchunks = p.nchunks;
+
+        void (*k)(LnBwdArgs) = nullptr;
+        const bool hm = c.mean != nullptr;
+        if (hm && c.norms) k = ln_bwd_kernel<T, GW, VPT, G, RPG, true, true>;
+        else if (hm) k = ln_bwd_kernel<T, GW, VPT, G, RPG, true, false>;
+        else if (c.norms) k = ln_bwd_kernel<T, GW, VPT, G, RPG, false, true>;
+        else k = ln_bwd_kernel<T, GW, VPT, G, RPG, false, false>;
+        cudaError_t e = ensure_smem(k, p.smem);
+        if (e != cudaSuccess) {
+            *cerr = e;
+            return 2;
+        }
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(p.grid);
+        cfg.blockDim = dim3(p.threads);
+        cfg.dynamicSmemBytes = p.smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, k, a);
+        if (e != cudaSuccess) {
+            *cerr = e;
+            return 2;
+        }
+        return 0;
+    }
+};
+
+template <typename T, int GW, int VPT>
+struct FwdOp {
+    static int run(const LnFwdCall& c, cudaStream_t st, const char**, cudaError_t* cerr) {
+        using F = LnFwdCfg<T, GW, VPT>;
+        LnFwdArgs a{};
+        a.x = c.x;
+        a.gamma = c.gamma;
+        a.beta = c.beta;
+        a.y = c.y;
+        a.mean = c.mean;
+        a.rstd = c.rstd;
+        a.xhat = c.xhat;
+        a.N = c.N;
+        a.D = c.D;
+        a.eps = c.eps;
+        a.aligned = ((c.D * (int64_t)sizeof(T)) % 16 == 0) && ptr16(c.x) && (c.y == nullptr || ptr16(c.y)) &&
+                    (c.xhat == nullptr || ptr16(c.xhat));
+        const int sms = device_sm_count();
+        int64_t blocks = (c.N + F::G - 1) / F::G;
+        const int64_t cap = (int64_t)sms * (2048 / F::kThreads);
+        if (blocks > cap) blocks = cap;
+        if (blocks < 1) blocks = 1;
+        ln_fwd_kernel<T, GW, VPT><<<(int)blocks, F::kThreads, 0, st>>>(a);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) {
+            *cerr = e;
+            return 2;
+        }
+        return 0;
+    }
+};
+
+// Configuration table: number of 16-byte vectors per row -> (GW, VPT, G, RPG).
+template <typename T, template <typename, int, int, int, int> class Op, typename R, typename... A>
+R dispatch_bwd(int64_t D, const char** why, R bad, A&&... args) {
+    constexpr int W = Traits<T>::W;
+    const int64_t nv = (D + W - 1) / W;
+    // <= 12 consumer warps (+1 producer) keeps the per-SMSP register cap at
+    // >= 128/thread; the wide-row configs use 8 consumer warps (cap 168).
+    if (nv <= 32) return Op<T, 1, 1, 8, 2>::call(args...);
+    if (nv <= 64) return Op<T, 2, 1, 4, 2>::call(args...);
+    if (nv <= 96) return Op<T, 3, 1, 4, 2>::call(args...);
+    if (nv <= 128) return Op<T, 4, 1, 3, 2>::call(args...);
+    if (nv <= 256) return Op<T, 4, 2, 3, 2>::call(args...);
+    if (nv <= 512) return Op<T, 8, 2, 1, 2>::call(args...);
+    if (nv <= 1024) return Op<T, 8, 4, 1, 1>::call(args...);
+    if (nv <= 2048) return Op<T, 16, 4, 1, 1>::call(args...);
+    *why = "layers: trailing extent exceeds the kernel limit (2048 16-byte vectors per row)";
+    return bad;
+}
+
+template <typename T, int GW, int VPT, int G, int RPG>
+struct BwdRunOp {
+    static int call(const LnBwdCall& c, cudaStream_t st, const char** why, cudaError_t* cerr) {
+        return BwdOp<T, GW, VPT, G, RPG>::run(c, st, why, cerr);
+    }
+};
+template <typename T, int GW, int VPT, int G, int RPG>
+struct BwdPlanOp {
+    static int call(int64_t B, int64_t M, int64_t D, BwdPlan* p, const char** why) {
+        return BwdOp<T, GW, VPT, G, RPG>::plan(B, M, D, *p, why);
+    }
+};
+template <typename T, int GW, int VPT, int G, int RPG>
+struct FwdRunOp {
+    static int call(const LnFwdCall& c, cudaStream_t st, const char** why, cudaError_t* cerr) {
+        return FwdOp<T, GW, VPT>::run(c, st, why, cerr);
+    }
+};
+
+}  // namespace
+
+template <typename T>
+int ln_bwd_run(const LnBwdCall& c, cudaStream_t st, const char** why, cudaError_t* cerr) {
+    return dispatch_bwd<T, BwdRunOp>(c.D, why, 1, c, st, why, cerr);
+}
+
+template <typename T>
+int ln_bwd_workspace(int64_t B, int64_t M, int64_t D, size_t* bytes, const char** why) {
+    BwdPlan p;
+    const int rc = dispatch_bwd<T, BwdPlanOp>(D, why, 1, B, M, D, &p, why);
+    if (rc == 0) *bytes = p.total;
+    return rc;
+}
+
+template <typename T>
+int ln_bwd_geometry(int64_t B, int64_t M, int64_t D, int* grid, int* threads, int* stages) {
+    BwdPlan p;
+    const char* why = nullptr;
+    const int rc = dispatch_bwd<T, BwdPlanOp>(D, &why, 1, B, M, D, &p, &why);
+    if (rc == 0) {
+        *grid = p.grid;
+        *threads = p.threads;
+        *stages = p.stages;
+    }
+    return rc;
+}
+
+template <typename T>
+int ln_fwd_run(const LnFwdCall& c, cudaStream_t st, const char** why, cudaError_t* cerr) {
+    return dispatch_bwd<T, FwdRunOp>(c.D, why, 1, c, st, why, cerr);
+}
+
+#define GNSB_INSTANTIATE_LN(T)                                                                          \
+    template int ln_bwd_run<T>(const LnBwdCall&, cudaStream_t, const char**, cudaError_t*);             \
+    template int ln_bwd_workspace<T>(int64_t, int64_t, int64_t, size_t*, const char**);                 \
+    template int ln_bwd_geometry<T>(int64_t, int64_t, int64_t, int*, int*, int*);                       \
+    template int ln_fwd_run<T>(const LnFwdCall&, cudaStream_t, const char**, cudaError_t*);
+
+}  // namespace gnsb

@@ -1,0 +1,149 @@
+"""The C ABI library on CPU: it loads, exports every symbol include/gnsb.h
+declares, and its host-side functions (GNS estimators, cost model) match the
+reference known answers and the oracle.  No GPU needed.
+"""
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import ROOT
+
+
+def _header_symbols():
+    src = open(os.path.join(ROOT, "include", "gnsb.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(gnsb_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2411_00999_b200 import _lib
+
+    h = _lib.lib()
+    syms = _header_symbols()
+    assert len(syms) >= 19
+    for s in syms:
+        assert hasattr(h, s), s
+    assert set(syms) == set(_lib.exported_symbols()), set(syms) ^ set(_lib.exported_symbols())
+    assert _lib.lib().gnsb_version().decode().startswith("gnsb")
+
+
+def test_gns_worked_arithmetic():
+    # proj/tests/test_gns.cpp:15-23, acceptance.cpp:307-313 — exact
+    from paper_2411_00999_b200 import gns
+
+    st = gns.GradStats(1.25, 1.5, 2, 1, 2)
+    assert gns.estimate_g2(st) == 1.0
+    assert gns.estimate_s(st) == 0.5
+    e = gns.make_gns_estimate(gns.estimate_g2(st), gns.estimate_s(st))
+    assert e.b_simple_defined and e.b_simple == 0.5
+
+
+def test_gns_zero_noise_and_scaling_and_preconditions():
+    from paper_2411_00999_b200 import gns
+
+    assert gns.estimate_g2(gns.GradStats(1.0, 1.0, 2, 1, 2)) == 1.0          # test_gns.cpp:25-32
+    assert gns.estimate_s(gns.GradStats(1.0, 1.0, 2, 1, 2)) == 0.0
+    z = gns.GradStats(0.0, 0.0, 2, 1, 2)
+    assert gns.estimate_g2(z) == 0.0
+    assert not gns.make_gns_estimate(gns.estimate_g2(z), gns.estimate_s(z)).b_simple_defined
+    a, b = gns.GradStats(1.25, 1.5, 2, 1, 2), gns.GradStats(1.25 * 9, 1.5 * 9, 2, 1, 2)  # :34-42
+    assert gns.estimate_g2(b) == 9 * gns.estimate_g2(a) and gns.estimate_s(b) == 9 * gns.estimate_s(a)
+    with pytest.raises(ValueError, match="gns: b_big must exceed b_small"):      # :44-48
+        gns.estimate_g2(gns.GradStats(1.0, 1.0, 2, 2, 1))
+    with pytest.raises(ValueError, match="gns: b_small must be >= 1"):
+        gns.estimate_s(gns.GradStats(1.0, 1.0, 2, 0, 1))
+
+
+def test_ema_and_smoothed():
+    # proj/tests/test_gns.cpp:50-87
+    from paper_2411_00999_b200 import gns
+
+    s = gns.ema_update(gns.EmaState(0.5), 1.0)
+    assert s.value == 1.0
+    s = gns.ema_update(s, 3.0)
+    assert s.value == 2.0
+    ident = gns.EmaState(1.0)
+    for x in (4.0, -2.0, 7.5):
+        ident = gns.ema_update(ident, x)
+        assert ident.value == x
+    fix = gns.EmaState(0.3)
+    for _ in range(20):
+        fix = gns.ema_update(fix, 5.0)
+    assert abs(fix.value - 5.0) < 1e-12 * 6
+    with pytest.raises(ValueError, match="gns: ema alpha must be in"):
+        gns.ema_update(gns.EmaState(0.0), 1.0)
+    with pytest.raises(ValueError):
+        gns.ema_update(gns.EmaState(1.5), 1.0)
+    g2 = gns.ema_update(gns.EmaState(1.0), 1.0)
+    sv = gns.ema_update(gns.EmaState(1.0), 0.5)
+    assert gns.smoothed_gns(g2, sv).b_simple == 0.5
+    g0 = gns.ema_update(gns.EmaState(1.0), 0.0)
+    assert not gns.smoothed_gns(g0, sv).b_simple_defined
+    with pytest.raises(ValueError, match="smoothed_gns needs at least one sample"):
+        gns.smoothed_gns(gns.EmaState(0.5), sv)
+
+
+def test_aggregate():
+    # proj/tests/test_gns.cpp:89-124
+    from paper_2411_00999_b200 import gns
+
+    by = {("a", "linear"): gns.GradStats(1.0, 2.0, 4, 1, 4), ("b", "linear"): gns.GradStats(2.0, 3.0, 4, 1, 4),
+          ("c", "layernorm"): gns.GradStats(1.0, 0.5, 4, 1, 4)}
+    al = gns.aggregate(by, None)
+    assert (al.g_big_sqnorm, al.g_small_sqnorm_mean, al.b_big) == (4.0, 5.5, 4)
+    assert gns.aggregate(by, "layernorm").g_big_sqnorm == 1.0
+    with pytest.raises(ValueError, match="gns: aggregate over an empty selection"):
+        gns.aggregate(by, "embedding")
+    by[("d", "linear")] = gns.GradStats(1.0, 1.0, 8, 1, 8)
+    with pytest.raises(ValueError, match="matching batch sizes"):
+        gns.aggregate(by, None)
+    ex = {("a", "linear"): gns.GradStats(3.0, 5.0, 2, 1, 2), ("b", "embedding"): gns.GradStats(7.0, 2.0, 2, 1, 2),
+          ("c", "layernorm"): gns.GradStats(1.0, 6.0, 2, 1, 2)}
+    agg = gns.aggregate(ex, None)
+    assert gns.estimate_g2(agg) == sum(gns.estimate_g2(v) for v in ex.values())
+    assert gns.estimate_s(agg) == sum(gns.estimate_s(v) for v in ex.values())
+
+
+def test_costmodel_matches_oracle(orc):
+    import ctypes
+
+    from paper_2411_00999_b200 import _lib
+
+    h = _lib.lib()
+    for k, l in [(1024, 1024), (4096, 4096), (768, 3072), (1, 1), (7, 5)]:
+        for crit in (0, 1):
+            out = ctypes.c_double()
+            _lib.check(h.gnsb_crossover_t(k, l, crit, ctypes.byref(out)))
+            assert out.value == orc.crossover_t(k, l, crit)
+    for shape in [(16, 2048, 4096, 4096), (2, 3, 4, 5), (1, 1, 1, 1)]:
+        for meth in (0, 1):
+            f = (ctypes.c_int64 * 2)()
+            io = (ctypes.c_int64 * 2)()
+            _lib.check(h.gnsb_flops(*shape, meth, f))
+            _lib.check(h.gnsb_io_values(*shape, meth, io))
+            assert (f[0], f[1]) == orc.flops(*shape, meth)
+            assert (io[0], io[1]) == orc.io_values(*shape, meth)
+    out = ctypes.c_double()
+    assert h.gnsb_crossover_t(0, 4, 0, ctypes.byref(out)) == _lib.GNSB_EINVAL
+    assert "costmodel: dims must be positive" in _lib.last_error()
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_compute_entry_points_fail_loudly_without_gpu():
+    """No CPU fallback: compute calls return GNSB_ECUDA (raised as GnsbCudaError)."""
+    from paper_2411_00999_b200 import _lib
+
+    h = _lib.lib()
+    rc = h.gnsb_ln_fwd(None, None, None, None, None, None, None, 4, 8, 1e-5, 0, None)
+    assert rc == _lib.GNSB_ECUDA
+    assert "no CUDA device" in _lib.last_error()
+    with pytest.raises(_lib.GnsbCudaError):
+        _lib.check(rc)
+    # argument validation still reports the reference's message first
+    assert h.gnsb_ln_bwd(None, None, None, None, None, None, None, None, None, None, None, 1, 0, 4, 8, 0, None, 0,
+                         None) == _lib.GNSB_EINVAL
+    assert _lib.last_error() == "layers: empty batch"

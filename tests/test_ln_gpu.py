@@ -1,0 +1,314 @@
+"""GPU parity of the fused LayerNorm backward (+ per-example norms) and forward.
+
+Every check compares the CUDA path (libgnsb.so through the C ABI) with the
+reference: the golden vectors produced by the unmodified reference library
+(tests/golden) and the oracle restatement (oracle/) on identical inputs.
+
+Tolerances (BASELINE.json north_star / SURVEY §8(d)):
+  fp64 rows : rtol 1e-11 (summation order differs from the sequential reference)
+  fp32 rows : dx/dgamma/dbeta rtol 1e-5 with atol = 1e-5*||ref||_inf (test_helpers.hpp close());
+              per-example norms and corrected values rtol 1e-4
+  bf16 rows : the oracle consumes the same bf16 values; dx (bf16 output) rtol 2^-8 + atol 2^-8*||ref||_inf;
+              dgamma/dbeta rtol 1e-4 (+1e-4*||ref||_inf); norms rtol 1e-4
+"""
+import numpy as np
+import pytest
+import torch
+
+from conftest import close
+
+pytestmark = pytest.mark.gpu
+
+F32_TOL = 1e-5
+NORM_TOL = 1e-4
+BF16_DX = 2.0 ** -8
+
+
+def _mod():
+    import paper_2411_00999_b200 as m
+
+    return m
+
+
+def _t(a, dt, dev):
+    return torch.tensor(np.asarray(a), dtype=dt, device=dev)
+
+
+def _close_inf(got, ref, rtol, scale=None):
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    s = np.max(np.abs(ref)) if scale is None else scale
+    return close(got, ref, rtol, rtol * s)
+
+
+# --------------------------------------------------------------------------- fp64 vs golden
+@pytest.mark.parametrize("fam", ["ln_rand31", "acc1_ln", "ln_zero", "ln_fwd_kat"])
+def test_fp64_backward_matches_reference_golden(golden, cuda, fam):
+    m = _mod()
+    cases = [c for c in golden if c["family"] == fam]
+    assert cases
+    for c in cases:
+        shape = tuple(c["shape"])
+        layer = m.LayerNormLayer(_t(c["gamma"], torch.float64, cuda), _t(c["beta"], torch.float64, cuda), c["eps"])
+        cache = m.LayerNormCache(normalized=_t(c["xhat"], torch.float64, cuda).reshape(shape),
+                                 inv_std=_t(c["inv_std"], torch.float64, cuda).reshape(shape[:-1]))
+        r = m.layernorm_backward_simultaneous(layer, cache, _t(c["g"], torch.float64, cuda).reshape(shape))
+        torch.cuda.synchronize()
+        assert close(r.input_grad.cpu().numpy().ravel(), c["dx"], 1e-11, 1e-14), fam
+        assert close(r.grads.weight_grads["gamma"].cpu().numpy(), c["dgamma"], 1e-11, 1e-14)
+        assert close(r.grads.weight_grads["beta"].cpu().numpy(), c["dbeta"], 1e-11, 1e-14)
+        assert close(r.grads.per_example_sqnorms_raw["gamma"].cpu().numpy(), c["raw_gamma"], 1e-11, 1e-14)
+        assert close(r.grads.per_example_sqnorms_raw["beta"].cpu().numpy(), c["raw_beta"], 1e-11, 1e-14)
+        assert close(float(r.grads.per_example_sqnorms["gamma"]), c["corrected"][0], 1e-11, 1e-14)
+        assert close(float(r.grads.per_example_sqnorms["beta"]), c["corrected"][1], 1e-11, 1e-14)
+        assert r.grads.batch_size == shape[0]
+
+
+def test_fp64_hand_worked(cuda):
+    # proj/tests/test_layers.cpp:167-176 — exact
+    m = _mod()
+    layer = m.LayerNormLayer(_t([1, 1], torch.float64, cuda), _t([0, 0], torch.float64, cuda), 1e-5)
+    cache = m.LayerNormCache(normalized=_t([[[1, -1]]], torch.float64, cuda), inv_std=_t([[1.0]], torch.float64, cuda))
+    r = m.layernorm_backward_simultaneous(layer, cache, _t([[[2, 3]]], torch.float64, cuda))
+    assert r.grads.weight_grads["gamma"].tolist() == [2.0, -3.0]
+    assert r.grads.weight_grads["beta"].tolist() == [2.0, 3.0]
+    assert float(r.grads.per_example_sqnorms["gamma"]) == 13.0
+    assert float(r.grads.per_example_sqnorms["beta"]) == 13.0
+
+
+@pytest.mark.parametrize("fam", ["ln_rand31", "acc1_ln", "ln_fwd_kat"])
+def test_fp64_forward_matches_reference_golden(golden, cuda, fam):
+    m = _mod()
+    for c in [c for c in golden if c["family"] == fam]:
+        shape = tuple(c["shape"])
+        layer = m.LayerNormLayer(_t(c["gamma"], torch.float64, cuda), _t(c["beta"], torch.float64, cuda), c["eps"])
+        f = m.layernorm_forward(layer, _t(c["x"], torch.float64, cuda).reshape(shape), keep_normalized=True)
+        assert close(f.output.cpu().numpy().ravel(), c["y"], 1e-11, 1e-13)
+        assert close(f.cache.normalized.cpu().numpy().ravel(), c["xhat"], 1e-11, 1e-13)
+        assert close(f.cache.inv_std.cpu().numpy().ravel(), c["inv_std"], 1e-11)
+
+
+# --------------------------------------------------------------------------- fp32 cfg1 vs golden
+def test_cfg1_fp32_matches_reference(golden, orc, cuda):
+    """BASELINE config 1: B=8 T=128 D=768 fp32, synthetic recipe, vs the reference run."""
+    m = _mod()
+    c = [c for c in golden if c["family"] == "ln_cfg1"][0]
+    B, T, D = c["shape"]
+    x, dy, gamma, beta = m.synth_ln(B, T, D, torch.float32, cuda, sigma=c["sigma"], stream0=c["stream0"])
+    xo, dyo, go, bo = orc.synth_ln(B, T, D, sigma=c["sigma"], stream0=c["stream0"])
+    # the device generator is bit-identical with the oracle's
+    np.testing.assert_array_equal(x.cpu().numpy(), xo)
+    np.testing.assert_array_equal(dy.cpu().numpy(), dyo)
+    np.testing.assert_array_equal(gamma.cpu().numpy(), go)
+    np.testing.assert_array_equal(beta.cpu().numpy(), bo)
+
+    layer = m.LayerNormLayer(gamma, beta, 1e-5)
+    f = m.layernorm_forward(layer, x)
+    assert _close_inf(f.cache.inv_std.cpu().numpy().ravel(), c["inv_std"], F32_TOL)
+    idx = np.array(c["dx_sample_idx"], dtype=np.int64)
+    assert _close_inf(f.output.cpu().numpy().ravel()[idx], c["y_sample"], F32_TOL)
+    r = m.layernorm_backward_simultaneous(layer, f.cache, dy)
+    torch.cuda.synchronize()
+    assert _close_inf(r.grads.weight_grads["gamma"].cpu().numpy(), c["dgamma"], F32_TOL)
+    assert _close_inf(r.grads.weight_grads["beta"].cpu().numpy(), c["dbeta"], F32_TOL)
+    assert close(r.grads.per_example_sqnorms_raw["gamma"].cpu().numpy(), c["raw_gamma"], NORM_TOL)
+    assert close(r.grads.per_example_sqnorms_raw["beta"].cpu().numpy(), c["raw_beta"], NORM_TOL)
+    assert close(float(r.grads.per_example_sqnorms["gamma"]), c["corrected"][0], NORM_TOL)
+    assert close(float(r.grads.per_example_sqnorms["beta"]), c["corrected"][1], NORM_TOL)
+    dx = r.input_grad.cpu().numpy().ravel()
+    scale = np.max(np.abs(c["dx_sample"]))
+    assert close(dx[idx], c["dx_sample"], F32_TOL, F32_TOL * scale)
+    assert close(dx.reshape(B * T, D).astype(np.float64).sum(1), c["dx_row_sum"], F32_TOL, F32_TOL * scale * 10)
+
+
+def _oracle_on_device_stats(orc, x, dy, gamma, mean, rstd):
+    """Reference backward on the same (x, mean, rstd) the kernel consumed."""
+    return orc.ln_backward(x.cpu().double().numpy(), rstd.cpu().double().numpy(), dy.cpu().double().numpy(),
+                           gamma.cpu().double().numpy(), mean=mean.cpu().double().numpy())
+
+
+@pytest.mark.parametrize(
+    "dt,B,T,D",
+    [
+        (torch.float32, 8, 128, 768),
+        (torch.float32, 3, 5, 6),
+        (torch.float32, 4, 7, 5),      # unaligned rows: non-TMA producer
+        (torch.float32, 2, 33, 1024),
+        (torch.float32, 5, 9, 4096),
+        (torch.float32, 2, 4, 8192),
+        (torch.bfloat16, 4, 64, 768),
+        (torch.bfloat16, 4, 64, 1024),
+        (torch.bfloat16, 3, 50, 2048),
+        (torch.bfloat16, 2, 40, 4096),
+        (torch.bfloat16, 2, 20, 8192),
+        (torch.bfloat16, 2, 9, 16384),
+        (torch.bfloat16, 3, 5, 13),    # unaligned
+        (torch.float64, 3, 17, 2048),
+        (torch.float64, 2, 5, 7),      # unaligned
+        (torch.float32, 300, 1, 64),   # many examples per CTA
+        (torch.float32, 1, 1000, 256), # one example spread over every CTA
+        (torch.bfloat16, 1, 3, 8),     # fewer rows than SMs
+    ],
+)
+def test_backward_matches_oracle(orc, cuda, dt, B, T, D):
+    m = _mod()
+    bf = dt == torch.bfloat16
+    x, dy, gamma, beta = m.synth_ln(B, T, D, dt, cuda, stream0=7)
+    xo, dyo, _, _ = orc.synth_ln(B, T, D, stream0=7, bf16=bf)
+    np.testing.assert_array_equal(x.float().cpu().numpy(), xo)
+    np.testing.assert_array_equal(dy.float().cpu().numpy(), dyo)
+    layer = m.LayerNormLayer(gamma, beta, 1e-5)
+    f = m.layernorm_forward(layer, x)
+    r = m.layernorm_backward_simultaneous(layer, f.cache, dy)
+    ref = _oracle_on_device_stats(orc, x, dy, gamma, f.cache.mean, f.cache.inv_std)
+    torch.cuda.synchronize()
+    dxt = {torch.float64: 1e-11, torch.float32: F32_TOL, torch.bfloat16: BF16_DX}[dt]
+    gt = {torch.float64: 1e-11, torch.float32: F32_TOL, torch.bfloat16: NORM_TOL}[dt]
+    nt = {torch.float64: 1e-11, torch.float32: NORM_TOL, torch.bfloat16: NORM_TOL}[dt]
+    assert _close_inf(r.input_grad.double().cpu().numpy(), ref["dx"], dxt)
+    assert _close_inf(r.grads.weight_grads["gamma"].double().cpu().numpy(), ref["dgamma"], gt)
+    assert _close_inf(r.grads.weight_grads["beta"].double().cpu().numpy(), ref["dbeta"], gt)
+    assert close(r.grads.per_example_sqnorms_raw["gamma"].cpu().numpy(), ref["raw_gamma"], nt)
+    assert close(r.grads.per_example_sqnorms_raw["beta"].cpu().numpy(), ref["raw_beta"], nt)
+    assert close(float(r.grads.per_example_sqnorms["gamma"]), ref["corrected"][0], nt)
+    assert close(float(r.grads.per_example_sqnorms["beta"]), ref["corrected"][1], nt)
+    # ||dgamma||^2, ||dbeta||^2 records (used by the GNS accumulator)
+    s = r.grads.sums4.cpu().numpy()
+    dg = r.grads.weight_grads["gamma"].double().cpu().numpy()
+    db = r.grads.weight_grads["beta"].double().cpu().numpy()
+    assert close(s[2], np.dot(dg, dg), 1e-12) and close(s[3], np.dot(db, db), 1e-12)
+
+
+@pytest.mark.parametrize("dt,D", [(torch.bfloat16, 4096), (torch.float32, 768), (torch.float64, 6), (torch.bfloat16, 5)])
+def test_plain_equals_fused_bitwise(cuda, dt, D):
+    """The plain LN backward is the same kernel with norms compiled out: identical dx/dgamma/dbeta."""
+    m = _mod()
+    x, dy, gamma, beta = m.synth_ln(4, 100, D, dt, cuda, stream0=3)
+    layer = m.LayerNormLayer(gamma, beta)
+    f = m.layernorm_forward(layer, x)
+    a = m.layernorm_backward_simultaneous(layer, f.cache, dy, with_norms=True)
+    b = m.layernorm_backward_simultaneous(layer, f.cache, dy, with_norms=False)
+    assert torch.equal(a.input_grad, b.input_grad)
+    assert torch.equal(a.grads.weight_grads["gamma"], b.grads.weight_grads["gamma"])
+    assert torch.equal(a.grads.weight_grads["beta"], b.grads.weight_grads["beta"])
+    assert b.grads.per_example_sqnorms == {}
+
+
+@pytest.mark.parametrize("dt,B,T,D", [(torch.bfloat16, 32, 256, 4096), (torch.float32, 7, 33, 768)])
+def test_deterministic_run_to_run(cuda, dt, B, T, D):
+    m = _mod()
+    x, dy, gamma, beta = m.synth_ln(B, T, D, dt, cuda, stream0=5)
+    layer = m.LayerNormLayer(gamma, beta)
+    f = m.layernorm_forward(layer, x)
+    outs = [m.layernorm_backward_simultaneous(layer, f.cache, dy) for _ in range(3)]
+    for o in outs[1:]:
+        assert torch.equal(o.input_grad, outs[0].input_grad)
+        assert torch.equal(o.grads.weight_grads["gamma"], outs[0].grads.weight_grads["gamma"])
+        assert torch.equal(o.grads.per_example_sqnorms_raw["gamma"], outs[0].grads.per_example_sqnorms_raw["gamma"])
+        assert torch.equal(o.grads.sums4, outs[0].grads.sums4)
+
+
+def test_rank2_and_rank4_views(orc, cuda):
+    """(B, M, D) view: rank-2 input has M = 1; rank-4 collapses middle axes (layers.cpp:19-28)."""
+    m = _mod()
+    for shape in [(6, 32), (2, 3, 4, 16)]:
+        B, D = shape[0], shape[-1]
+        M = int(np.prod(shape[1:-1])) if len(shape) > 2 else 1
+        x, dy, gamma, beta = m.synth_ln(B, M, D, torch.float32, cuda, stream0=11)
+        x = x.reshape(shape)
+        dy = dy.reshape(shape)
+        layer = m.LayerNormLayer(gamma, beta)
+        f = m.layernorm_forward(layer, x)
+        r = m.layernorm_backward_simultaneous(layer, f.cache, dy)
+        ref = _oracle_on_device_stats(orc, x.reshape(B, M, D), dy.reshape(B, M, D), gamma, f.cache.mean.reshape(B, M),
+                                      f.cache.inv_std.reshape(B, M))
+        assert r.input_grad.shape == shape
+        assert close(r.grads.per_example_sqnorms_raw["gamma"].cpu().numpy(), ref["raw_gamma"], NORM_TOL)
+        assert _close_inf(r.input_grad.reshape(B, M, D).double().cpu().numpy(), ref["dx"], F32_TOL)
+
+
+def test_empty_middle_axis_and_errors(cuda):
+    m = _mod()
+    layer = m.LayerNormLayer(torch.ones(8, device=cuda), torch.zeros(8, device=cuda))
+    cache = m.LayerNormCache(normalized=torch.empty(3, 0, 8, device=cuda), inv_std=torch.empty(3, 0, device=cuda))
+    r = m.layernorm_backward_simultaneous(layer, cache, torch.empty(3, 0, 8, device=cuda))
+    assert r.grads.weight_grads["gamma"].abs().sum().item() == 0
+    assert r.grads.per_example_sqnorms_raw["gamma"].tolist() == [0.0, 0.0, 0.0]
+    assert float(r.grads.per_example_sqnorms["beta"]) == 0.0
+    with pytest.raises(ValueError, match="layers: empty batch"):
+        m.layernorm_backward_simultaneous(
+            layer, m.LayerNormCache(torch.empty(0, 2, 8, device=cuda), torch.empty(0, 2, device=cuda)),
+            torch.empty(0, 2, 8, device=cuda))
+    with pytest.raises(ValueError, match="layers: cache/gradient shape mismatch"):
+        m.layernorm_backward_simultaneous(
+            layer, m.LayerNormCache(torch.zeros(2, 3, 8, device=cuda), torch.ones(2, 3, device=cuda)),
+            torch.zeros(2, 3, 9, device=cuda))
+    with pytest.raises(ValueError, match="layers: epsilon must be positive"):
+        m.layernorm_forward(m.LayerNormLayer(torch.ones(8, device=cuda), torch.zeros(8, device=cuda), 0.0),
+                            torch.zeros(2, 8, device=cuda))
+    # zero upstream gradient -> zero norms and zero dx (test_layers.cpp:178-188)
+    x = torch.randn(2, 3, 8, device=cuda)
+    f = m.layernorm_forward(layer, x)
+    r = m.layernorm_backward_simultaneous(layer, f.cache, torch.zeros_like(x))
+    assert float(r.grads.per_example_sqnorms["gamma"]) == 0.0 and r.input_grad.abs().sum().item() == 0.0
+
+
+def test_scaling_gradient_scales_norms_quadratically(cuda):
+    # proj/tests/test_layers.cpp:349-362 analogue for LN: g*2 -> norms*4 exactly (fp64 rows)
+    m = _mod()
+    x, dy, gamma, beta = m.synth_ln(3, 10, 64, torch.float64, cuda, stream0=2)
+    layer = m.LayerNormLayer(gamma, beta)
+    f = m.layernorm_forward(layer, x)
+    a = m.layernorm_backward_simultaneous(layer, f.cache, dy)
+    b = m.layernorm_backward_simultaneous(layer, f.cache, dy * 2)
+    assert float(b.grads.per_example_sqnorms["gamma"]) == 4 * float(a.grads.per_example_sqnorms["gamma"])
+    assert float(b.grads.per_example_sqnorms["beta"]) == 4 * float(a.grads.per_example_sqnorms["beta"])
+
+
+def test_cfg2_full_size_properties(orc, cuda):
+    """BASELINE config 2 at full size (B=32 T=1024 D=4096 bf16): sampled examples
+    against the oracle (per-example quantities depend on that example only),
+    and dgamma/dbeta against an fp64 per-example sum of all examples."""
+    m = _mod()
+    B, T, D = 32, 1024, 4096
+    x, dy, gamma, beta = m.synth_ln(B, T, D, torch.bfloat16, cuda)
+    layer = m.LayerNormLayer(gamma, beta)
+    f = m.layernorm_forward(layer, x)
+    r = m.layernorm_backward_simultaneous(layer, f.cache, dy)
+    torch.cuda.synchronize()
+    rg = r.grads.per_example_sqnorms_raw["gamma"].cpu().numpy()
+    rb = r.grads.per_example_sqnorms_raw["beta"].cpu().numpy()
+    for b in (0, 13, 31):
+        ref = _oracle_on_device_stats(orc, x[b:b + 1], dy[b:b + 1], gamma, f.cache.mean[b:b + 1],
+                                      f.cache.inv_std[b:b + 1])
+        assert close(rg[b], ref["raw_gamma"][0], NORM_TOL)
+        assert close(rb[b], ref["raw_beta"][0], NORM_TOL)
+        assert _close_inf(r.input_grad[b].double().cpu().numpy(), ref["dx"][0], BF16_DX)
+    # batch sums: dgamma = sum_b gamma'_b, computed in fp64 on the GPU by torch as an independent check
+    xh = (x.double() - f.cache.mean.double()[..., None]) * f.cache.inv_std.double()[..., None]
+    ref_dg = (xh * dy.double()).sum((0, 1)).cpu().numpy()
+    ref_db = dy.double().sum((0, 1)).cpu().numpy()
+    pg = (xh * dy.double()).sum(1)
+    ref_raw = (pg * pg).sum(1).cpu().numpy()
+    assert _close_inf(r.grads.weight_grads["gamma"].double().cpu().numpy(), ref_dg, NORM_TOL)
+    assert _close_inf(r.grads.weight_grads["beta"].double().cpu().numpy(), ref_db, NORM_TOL)
+    assert close(rg, ref_raw, NORM_TOL)
+    assert close(float(r.grads.per_example_sqnorms["gamma"]), B * ref_raw.sum(), NORM_TOL)
+
+
+def test_two_streams_distinct_workspaces(cuda):
+    m = _mod()
+    x, dy, gamma, beta = m.synth_ln(8, 256, 1024, torch.bfloat16, cuda, stream0=9)
+    layer = m.LayerNormLayer(gamma, beta)
+    f = m.layernorm_forward(layer, x)
+    base = m.layernorm_backward_simultaneous(layer, f.cache, dy)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    outs = []
+    for s in (s1, s2, s1, s2):
+        with torch.cuda.stream(s):
+            outs.append(m.layernorm_backward_simultaneous(layer, f.cache, dy))
+    torch.cuda.synchronize()
+    for o in outs:
+        assert torch.equal(o.input_grad, base.input_grad)
+        assert torch.equal(o.grads.sums4, base.grads.sums4)
