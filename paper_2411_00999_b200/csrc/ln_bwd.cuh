@@ -65,6 +65,9 @@ struct LnBwdCfg {
     static constexpr int W = Traits<T>::W;
     static constexpr int kConsumerWarps = GW * G;
     static constexpr int kThreads = (kConsumerWarps + 1) * 32;
+    // registers are allocated for warps in groups of 4: bound the register
+    // budget by the rounded-up block so one CTA always fits on an SM
+    static constexpr int kBoundThreads = (kThreads + 127) / 128 * 128;
     static constexpr int R = G * RPG;           // rows per stage
     static constexpr int GT = GW * 32;          // threads per row group
     static constexpr int kMaxVec = GT * VPT;    // vectors per row covered
@@ -91,7 +94,7 @@ struct LnBwdCfg {
 };
 
 template <typename T, int GW, int VPT, int G, int RPG, bool HAS_MEAN, bool NORMS>
-__global__ void __launch_bounds__(LnBwdCfg<T, GW, VPT, G, RPG>::kThreads, 1) ln_bwd_kernel(LnBwdArgs a) {
+__global__ void __launch_bounds__(LnBwdCfg<T, GW, VPT, G, RPG>::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a) {
     using C = LnBwdCfg<T, GW, VPT, G, RPG>;
     using Acc = typename C::Acc;
     constexpr int W = C::W;

@@ -132,6 +132,23 @@ struct BwdOp {
             *cerr = e;
             return 2;
         }
+        // one CTA per SM must fit (cooperative launch); shrink the ring if not
+        for (;;) {
+            int occ = 0;
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, p.threads, p.smem);
+            if (e != cudaSuccess) {
+                *cerr = e;
+                return 2;
+            }
+            if (occ >= 1) break;
+            if (p.stages <= 1) {
+                *cerr = cudaErrorCooperativeLaunchTooLarge;
+                return 2;
+            }
+            --p.stages;
+            p.smem = LnBwdCfg<T, GW, VPT, G, RPG>::smem_bytes(p.stages, p.Dp);
+        }
+        a.stages = p.stages;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(p.grid);
         cfg.blockDim = dim3(p.threads);
@@ -194,7 +211,7 @@ R dispatch_bwd(int64_t D, const char** why, R bad, A&&... args) {
     if (nv <= 64) return Op<T, 2, 1, 4, 2>::call(args...);
     if (nv <= 96) return Op<T, 3, 1, 4, 2>::call(args...);
     if (nv <= 128) return Op<T, 4, 1, 3, 2>::call(args...);
-    if (nv <= 256) return Op<T, 4, 2, 3, 2>::call(args...);
+    if (nv <= 256) return Op<T, 4, 2, 2, 2>::call(args...);
     if (nv <= 512) return Op<T, 8, 2, 1, 2>::call(args...);
     if (nv <= 1024) return Op<T, 8, 4, 1, 1>::call(args...);
     if (nv <= 2048) return Op<T, 16, 4, 1, 1>::call(args...);
