@@ -79,6 +79,95 @@ template <> __device__ __forceinline__ float from_acc<float>(float v) { return v
 template <> __device__ __forceinline__ __nv_bfloat16 from_acc<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
 template <> __device__ __forceinline__ double from_acc<double>(double v) { return v; }
 
+// ------------------------------------------------------------ pairs ------
+// Row math runs on element pairs: fp32 pairs map to the sm_100 packed
+// FFMA2 / FADD2 / FMUL2 instructions (two lanes of fp32 per instruction);
+// fp64 pairs are two scalar ops.
+template <typename A> struct Pair;
+template <> struct Pair<float> {
+    using P = float2;
+    static __device__ __forceinline__ P make(float a, float b) { return make_float2(a, b); }
+    static __device__ __forceinline__ P splat(float a) { return make_float2(a, a); }
+    static __device__ __forceinline__ P add(P a, P b) { return __fadd2_rn(a, b); }
+    static __device__ __forceinline__ P mul(P a, P b) { return __fmul2_rn(a, b); }
+    static __device__ __forceinline__ P fma(P a, P b, P c) { return __ffma2_rn(a, b, c); }
+};
+template <> struct Pair<double> {
+    using P = double2;
+    static __device__ __forceinline__ P make(double a, double b) { return make_double2(a, b); }
+    static __device__ __forceinline__ P splat(double a) { return make_double2(a, a); }
+    static __device__ __forceinline__ P add(P a, P b) { return make_double2(a.x + b.x, a.y + b.y); }
+    static __device__ __forceinline__ P mul(P a, P b) { return make_double2(a.x * b.x, a.y * b.y); }
+    static __device__ __forceinline__ P fma(P a, P b, P c) { return make_double2(::fma(a.x, b.x, c.x), ::fma(a.y, b.y, c.y)); }
+};
+
+// 16-byte vector -> W/2 pairs of Acc
+template <typename T>
+__device__ __forceinline__ void unpack2(const uint4& v, typename Pair<typename Traits<T>::Acc>::P* o);
+template <>
+__device__ __forceinline__ void unpack2<float>(const uint4& v, float2* o) {
+    o[0] = make_float2(__uint_as_float(v.x), __uint_as_float(v.y));
+    o[1] = make_float2(__uint_as_float(v.z), __uint_as_float(v.w));
+}
+template <>
+__device__ __forceinline__ void unpack2<__nv_bfloat16>(const uint4& v, float2* o) {
+    o[0] = make_float2(__uint_as_float(v.x << 16), __uint_as_float(v.x & 0xffff0000u));
+    o[1] = make_float2(__uint_as_float(v.y << 16), __uint_as_float(v.y & 0xffff0000u));
+    o[2] = make_float2(__uint_as_float(v.z << 16), __uint_as_float(v.z & 0xffff0000u));
+    o[3] = make_float2(__uint_as_float(v.w << 16), __uint_as_float(v.w & 0xffff0000u));
+}
+template <>
+__device__ __forceinline__ void unpack2<double>(const uint4& v, double2* o) {
+    o[0] = make_double2(__hiloint2double((int)v.y, (int)v.x), __hiloint2double((int)v.w, (int)v.z));
+}
+
+// W/2 pairs of Acc -> 16-byte vector of T (round to nearest even)
+template <typename T>
+__device__ __forceinline__ uint4 pack2(const typename Pair<typename Traits<T>::Acc>::P* i);
+template <>
+__device__ __forceinline__ uint4 pack2<float>(const float2* i) {
+    return make_uint4(__float_as_uint(i[0].x), __float_as_uint(i[0].y), __float_as_uint(i[1].x), __float_as_uint(i[1].y));
+}
+template <>
+__device__ __forceinline__ uint4 pack2<__nv_bfloat16>(const float2* i) {
+    return make_uint4(pack_bf16x2(i[0].x, i[0].y), pack_bf16x2(i[1].x, i[1].y), pack_bf16x2(i[2].x, i[2].y),
+                      pack_bf16x2(i[3].x, i[3].y));
+}
+template <>
+__device__ __forceinline__ uint4 pack2<double>(const double2* i) {
+    return make_uint4((uint32_t)__double2loint(i[0].x), (uint32_t)__double2hiint(i[0].x),
+                      (uint32_t)__double2loint(i[0].y), (uint32_t)__double2hiint(i[0].y));
+}
+
+// Sum NQ per-lane values over a warp with a transposed butterfly: NQ-1 + 5 -
+// log2(NQ) shuffles instead of 5*NQ.  On return v[0] holds, in every lane,
+// the warp total of quantity q = butterfly_q<NQ>(lane).
+template <int NQ, typename V>
+__device__ __forceinline__ void butterfly_sum(V* v, int lane) {
+    int n = NQ;
+    int m = 16;
+#pragma unroll
+    for (; n > 1; n >>= 1, m >>= 1) {
+        const bool upper = (lane & m) != 0;
+#pragma unroll
+        for (int j = 0; j < n / 2; ++j) {
+            const V send = upper ? v[j] : v[j + n / 2];
+            const V keep = upper ? v[j + n / 2] : v[j];
+            v[j] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+        }
+    }
+#pragma unroll
+    for (; m >= 1; m >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], m);
+}
+template <int NQ>
+__device__ __forceinline__ int butterfly_q(int lane) {
+    int q = 0, n = NQ, m = 16;
+#pragma unroll
+    for (; n > 1; n >>= 1, m >>= 1)
+        if (lane & m) q += n / 2;
+    return q;
+}
+
 // ------------------------------------------------------------ shared mem --
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));

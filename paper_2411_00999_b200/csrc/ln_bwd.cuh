@@ -71,7 +71,7 @@ struct LnBwdCfg {
     static constexpr int R = G * RPG;           // rows per stage
     static constexpr int GT = GW * 32;          // threads per row group
     static constexpr int kMaxVec = GT * VPT;    // vectors per row covered
-    static constexpr int kRedElems = 2 * G * GW * 2 * RPG;
+    static constexpr int kRedElems = 2 * G * (GW == 3 ? 4 : GW) * 2 * RPG;
     // byte offsets inside dynamic shared memory
     static __host__ __device__ constexpr size_t bars_bytes(int S) { return (size_t)16 * S; }
     static __host__ __device__ constexpr size_t red_off(int S) { return (bars_bytes(S) + 15) / 16 * 16; }
@@ -182,26 +182,23 @@ __global__ void __launch_bounds__(LnBwdCfg<T, GW, VPT, G, RPG>::kBoundThreads, 1
         T* dxg = static_cast<T*>(a.dx);
         const Acc invD = Acc(1) / Acc(D);
 
-        // gamma vector k of this thread, from shared memory
-        auto load_gam = [&](int k, Acc* out) {
-            const int v = tig + k * GT;
-            const Acc* p = gam_s + (size_t)(v < NVp ? v : 0) * W;
+        using PR = Pair<Acc>;
+        using P = typename PR::P;
+        constexpr int NP = W / 2;          // pairs per 16-byte vector
+        constexpr int NQ = 2 * RPG;        // row sums reduced per stage: (s1, s2) per row
+        constexpr int GWP = GW == 3 ? 4 : GW;  // power-of-two padding for the cross-warp tree
+        static_assert(NQ * GWP <= 32, "cross-warp reduction layout");
+
+        // this thread's column vectors
+        bool vok[VPT];
 #pragma unroll
-            for (int e = 0; e < W; e += (int)(16 / sizeof(Acc))) {
-                if constexpr (sizeof(Acc) == 4) {
-                    const float4 q = *reinterpret_cast<const float4*>(p + e);
-                    out[e] = q.x; out[e + 1] = q.y; out[e + 2] = q.z; out[e + 3] = q.w;
-                } else {
-                    const double2 q = *reinterpret_cast<const double2*>(p + e);
-                    out[e] = q.x; out[e + 1] = q.y;
-                }
-            }
-        };
-        Acc ag[VPT][W], ab[VPT][W];
+        for (int k = 0; k < VPT; ++k) vok[k] = (tig + k * GT) < NVp;
+
+        P ag[VPT][NP], ab[VPT][NP];
 #pragma unroll
         for (int k = 0; k < VPT; ++k)
 #pragma unroll
-            for (int e = 0; e < W; ++e) ag[k][e] = ab[k][e] = Acc(0);
+            for (int p = 0; p < NP; ++p) ag[k][p] = ab[k][p] = PR::splat(Acc(0));
 
         int64_t cur_ex = r_begin / M;
         int64_t next_bound = (cur_ex + 1) * M;
@@ -211,13 +208,13 @@ __global__ void __launch_bounds__(LnBwdCfg<T, GW, VPT, G, RPG>::kBoundThreads, 1
             Acc* base = partial + ((size_t)(cta + ex) * G + g) * 2 * Dp;
 #pragma unroll
             for (int k = 0; k < VPT; ++k) {
+                if (!vok[k]) continue;
                 const int v = tig + k * GT;
-                if (v < NVp) {
 #pragma unroll
-                    for (int e = 0; e < W; ++e) {
-                        base[(size_t)v * W + e] = zero ? Acc(0) : ag[k][e];
-                        base[(size_t)Dp + (size_t)v * W + e] = zero ? Acc(0) : ab[k][e];
-                    }
+                for (int p = 0; p < NP; ++p) {
+                    const P z = PR::splat(Acc(0));
+                    *reinterpret_cast<P*>(base + (size_t)v * W + 2 * p) = zero ? z : ag[k][p];
+                    *reinterpret_cast<P*>(base + (size_t)Dp + (size_t)v * W + 2 * p) = zero ? z : ab[k][p];
                 }
             }
         };
@@ -226,7 +223,7 @@ __global__ void __launch_bounds__(LnBwdCfg<T, GW, VPT, G, RPG>::kBoundThreads, 1
 #pragma unroll
             for (int k = 0; k < VPT; ++k)
 #pragma unroll
-                for (int e = 0; e < W; ++e) ag[k][e] = ab[k][e] = Acc(0);
+                for (int p = 0; p < NP; ++p) ag[k][p] = ab[k][p] = PR::splat(Acc(0));
             for (int64_t ex = cur_ex + 1; ex < new_ex; ++ex) write_slot(ex, true);
             cur_ex = new_ex;
             next_bound = (cur_ex + 1) * M;
@@ -239,23 +236,23 @@ __global__ void __launch_bounds__(LnBwdCfg<T, GW, VPT, G, RPG>::kBoundThreads, 1
             mbar_wait(&full[slot], ph);
             const int64_t r0 = r_begin + it * R;
             const int nr = (int)((r_end - r0) < (int64_t)R ? (r_end - r0) : (int64_t)R);
-            const T* sx = ring + (size_t)slot * 2 * R * Dp;
+            const T* sx = ring + (size_t)slot * 2 * R * Dp + (size_t)(g * RPG) * Dp;
             const T* sdy = sx + (size_t)R * Dp;
+            const Acc* st = stats + ((size_t)slot * R + g * RPG) * 2;
 
             uint4 ux[RPG][VPT], ug[RPG][VPT];
             Acc mu[RPG], rs[RPG];
 #pragma unroll
             for (int i = 0; i < RPG; ++i) {
-                const int j = g * RPG + i;
-                const bool valid = j < nr;
-                mu[i] = valid ? stats[((size_t)slot * R + j) * 2 + 0] : Acc(0);
-                rs[i] = valid ? stats[((size_t)slot * R + j) * 2 + 1] : Acc(0);
+                const bool valid = g * RPG + i < nr;
+                mu[i] = valid ? st[2 * i + 0] : Acc(0);
+                rs[i] = valid ? st[2 * i + 1] : Acc(0);
 #pragma unroll
                 for (int k = 0; k < VPT; ++k) {
-                    const int v = tig + k * GT;
-                    if (valid && v < NVp) {
-                        ux[i][k] = *reinterpret_cast<const uint4*>(sx + (size_t)j * Dp + (size_t)v * W);
-                        ug[i][k] = *reinterpret_cast<const uint4*>(sdy + (size_t)j * Dp + (size_t)v * W);
+                    const size_t off = (size_t)i * Dp + (size_t)(tig + k * GT) * W;
+                    if (valid && vok[k]) {
+                        ux[i][k] = *reinterpret_cast<const uint4*>(sx + off);
+                        ug[i][k] = *reinterpret_cast<const uint4*>(sdy + off);
                     } else {
                         ux[i][k] = ug[i][k] = make_uint4(0, 0, 0, 0);
                     }
@@ -264,88 +261,85 @@ __global__ void __launch_bounds__(LnBwdCfg<T, GW, VPT, G, RPG>::kBoundThreads, 1
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[slot]);  // slot may be refilled now
 
-            Acc s1[RPG], s2[RPG];
+            // pass 1: xhat, h = gamma*g kept in registers; row sums; column partials
+            P xh[RPG][VPT][NP], hh[RPG][VPT][NP];
+            Acc q[NQ];
 #pragma unroll
             for (int i = 0; i < RPG; ++i) {
-                const int j = g * RPG + i;
-                const int64_t row = r0 + j;
-                if (j < nr && row >= next_bound) flush_to(row / M);  // group-uniform
-                s1[i] = s2[i] = Acc(0);
+                const int64_t row = r0 + g * RPG + i;
+                if (g * RPG + i < nr && row >= next_bound) flush_to(row / M);  // group-uniform
+                const P rs2 = PR::splat(rs[i]);
+                const P nmr2 = PR::splat(-mu[i] * rs[i]);
+                P s1 = PR::splat(Acc(0)), s2 = PR::splat(Acc(0));
 #pragma unroll
                 for (int k = 0; k < VPT; ++k) {
-                    Acc xf[W], gf[W], gm[W];
-                    unpack<T>(ux[i][k], xf);
-                    unpack<T>(ug[i][k], gf);
-                    load_gam(k, gm);
+                    P xf[NP], gf[NP], gm[NP];
+                    unpack2<T>(ux[i][k], xf);
+                    unpack2<T>(ug[i][k], gf);
+                    const P* gp = reinterpret_cast<const P*>(gam_s + (size_t)(vok[k] ? tig + k * GT : 0) * W);
 #pragma unroll
-                    for (int e = 0; e < W; ++e) {
-                        const Acc xh = HAS_MEAN ? (xf[e] - mu[i]) * rs[i] : xf[e];
-                        const Acc h = gm[e] * gf[e];
-                        s1[i] += h;
-                        s2[i] += h * xh;
-                        ag[k][e] += xh * gf[e];
-                        ab[k][e] += gf[e];
+                    for (int p = 0; p < NP; ++p) gm[p] = gp[p];
+#pragma unroll
+                    for (int p = 0; p < NP; ++p) {
+                        const P x2 = HAS_MEAN ? PR::fma(xf[p], rs2, nmr2) : xf[p];
+                        const P h2 = PR::mul(gm[p], gf[p]);
+                        s1 = PR::add(s1, h2);
+                        s2 = PR::fma(h2, x2, s2);
+                        ag[k][p] = PR::fma(x2, gf[p], ag[k][p]);
+                        ab[k][p] = PR::add(ab[k][p], gf[p]);
+                        xh[i][k][p] = x2;
+                        hh[i][k][p] = h2;
                     }
                 }
+                q[2 * i] = s1.x + s1.y;
+                q[2 * i + 1] = s2.x + s2.y;
             }
-            // row reductions over the group
+            // row reductions over the group: transposed butterfly within the
+            // warp, then a padded xor tree over the group's warps
+            butterfly_sum<NQ>(q, lane);
+            Acc tot[NQ];
+            if constexpr (GW == 1) {
 #pragma unroll
-            for (int i = 0; i < RPG; ++i) {
-                s1[i] = warp_sum(s1[i]);
-                s2[i] = warp_sum(s2[i]);
-            }
-            if constexpr (GW > 1) {
-                Acc* rb = red + ((size_t)(rbuf * G + g) * GW) * 2 * RPG;
-                if (lane == 0) {
-#pragma unroll
-                    for (int i = 0; i < RPG; ++i) {
-                        rb[wig * 2 * RPG + 2 * i] = s1[i];
-                        rb[wig * 2 * RPG + 2 * i + 1] = s2[i];
-                    }
-                }
+                for (int j = 0; j < NQ; ++j) tot[j] = __shfl_sync(0xffffffffu, q[0], j * (32 / NQ));
+            } else {
+                Acc* rb = red + (size_t)(rbuf * G + g) * NQ * GWP;
+                if ((lane & (32 / NQ - 1)) == 0) rb[(lane / (32 / NQ)) * GWP + wig] = q[0];
                 named_bar_sync(1 + g, GT);
-#pragma unroll
-                for (int i = 0; i < RPG; ++i) {
-                    Acc t1 = 0, t2 = 0;
-#pragma unroll
-                    for (int w = 0; w < GW; ++w) {
-                        t1 += rb[w * 2 * RPG + 2 * i];
-                        t2 += rb[w * 2 * RPG + 2 * i + 1];
-                    }
-                    s1[i] = t1;
-                    s2[i] = t2;
+                Acc t = Acc(0);
+                if (lane < NQ * GWP) {
+                    const int w = lane % GWP;
+                    t = w < GW ? rb[lane] : Acc(0);
                 }
+#pragma unroll
+                for (int m = GWP / 2; m >= 1; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
+#pragma unroll
+                for (int j = 0; j < NQ; ++j) tot[j] = __shfl_sync(0xffffffffu, t, j * GWP);
                 rbuf ^= 1;
             }
-            // dx = rstd*(h - mean(h)) - rstd*mean(h*xhat)*xhat
+            // pass 2: dx = rstd*(h - mean(h)) - rstd*mean(h*xhat)*xhat
             if (dxg != nullptr) {
 #pragma unroll
                 for (int i = 0; i < RPG; ++i) {
-                    const int j = g * RPG + i;
-                    if (j >= nr) continue;
-                    const int64_t row = r0 + j;
-                    const Acc c1 = s1[i] * invD;
-                    const Acc c2 = rs[i] * s2[i] * invD;
+                    if (g * RPG + i >= nr) continue;
+                    const int64_t row = r0 + g * RPG + i;
+                    const P rs2 = PR::splat(rs[i]);
+                    const P k1 = PR::splat(-rs[i] * tot[2 * i] * invD);
+                    const P nc2 = PR::splat(-rs[i] * tot[2 * i + 1] * invD);
 #pragma unroll
                     for (int k = 0; k < VPT; ++k) {
+                        if (!vok[k]) continue;
                         const int v = tig + k * GT;
-                        if (v >= NVp) continue;
-                        Acc xf[W], gf[W], gm[W], o[W];
-                        unpack<T>(ux[i][k], xf);
-                        unpack<T>(ug[i][k], gf);
-                        load_gam(k, gm);
+                        P o[NP];
 #pragma unroll
-                        for (int e = 0; e < W; ++e) {
-                            const Acc xh = HAS_MEAN ? (xf[e] - mu[i]) * rs[i] : xf[e];
-                            o[e] = rs[i] * (gm[e] * gf[e] - c1) - c2 * xh;
-                        }
+                        for (int p = 0; p < NP; ++p) o[p] = PR::fma(nc2, xh[i][k][p], PR::fma(hh[i][k][p], rs2, k1));
                         if (a.aligned) {
-                            st_stream(dxg + row * D + (int64_t)v * W, pack<T>(o));
+                            st_stream(dxg + row * D + (int64_t)v * W, pack2<T>(o));
                         } else {
+                            const Acc* of = reinterpret_cast<const Acc*>(o);
 #pragma unroll
                             for (int e = 0; e < W; ++e) {
                                 const int64_t col = (int64_t)v * W + e;
-                                if (col < D) dxg[row * D + col] = from_acc<T>(o[e]);
+                                if (col < D) dxg[row * D + col] = from_acc<T>(of[e]);
                             }
                         }
                     }

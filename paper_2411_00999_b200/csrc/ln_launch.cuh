@@ -3,7 +3,9 @@
 // template instantiations compile in parallel.
 #pragma once
 
+#include <map>
 #include <mutex>
+#include <utility>
 
 #include "internal.h"
 #include "ln_bwd.cuh"
@@ -25,16 +27,16 @@ inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 inline bool ptr16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 // Per-(kernel, device) "max dynamic smem" attribute, set lazily.
-template <typename K>
-cudaError_t ensure_smem(K kernel, size_t bytes) {
+inline cudaError_t ensure_smem(const void* kernel, size_t bytes) {
     static std::mutex mu;
-    static size_t set_for[64] = {0};
+    static std::map<std::pair<const void*, int>, size_t> set_for;
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lk(mu);
-    if (dev < 64 && set_for[dev] >= bytes) return cudaSuccess;
+    auto& cur = set_for[{kernel, dev}];
+    if (cur >= bytes) return cudaSuccess;
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    if (e == cudaSuccess && dev < 64) set_for[dev] = bytes;
+    if (e == cudaSuccess) cur = bytes;
     return e;
 }
 
@@ -127,7 +129,7 @@ struct BwdOp {
         else if (hm) k = ln_bwd_kernel<T, GW, VPT, G, RPG, true, false>;
         else if (c.norms) k = ln_bwd_kernel<T, GW, VPT, G, RPG, false, true>;
         else k = ln_bwd_kernel<T, GW, VPT, G, RPG, false, false>;
-        cudaError_t e = ensure_smem(k, p.smem);
+        cudaError_t e = ensure_smem(reinterpret_cast<const void*>(k), p.smem);
         if (e != cudaSuccess) {
             *cerr = e;
             return 2;
