@@ -29,6 +29,8 @@
 //     are bitwise deterministic run to run.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace gnsb {
@@ -144,9 +146,9 @@ __global__ void __launch_bounds__(LnBwdCfg<T, GW, VPT, G, RPG>::kBoundThreads, 1
         const Acc* meang = static_cast<const Acc*>(a.mean);
         const Acc* rstdg = static_cast<const Acc*>(a.rstd);
         const uint64_t pol = policy_evict_first();
+        int slot = 0;
+        uint32_t ph = 0;
         for (int64_t it = 0; it < n_stage; ++it) {
-            const int slot = (int)(it % S);
-            const uint32_t ph = (uint32_t)((it / S) & 1);
             mbar_wait(&empty[slot], ph ^ 1u);
             const int64_t r0 = r_begin + it * R;
             const int nr = (int)((r_end - r0) < (int64_t)R ? (r_end - r0) : (int64_t)R);
@@ -173,6 +175,10 @@ __global__ void __launch_bounds__(LnBwdCfg<T, GW, VPT, G, RPG>::kBoundThreads, 1
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&full[slot]);
+            if (++slot == S) {
+                slot = 0;
+                ph ^= 1u;
+            }
         }
     } else {
         // ------------------------------------------------------ consumers --
@@ -230,12 +236,16 @@ __global__ void __launch_bounds__(LnBwdCfg<T, GW, VPT, G, RPG>::kBoundThreads, 1
         };
 
         int rbuf = 0;
-        for (int64_t it = 0; it < n_stage; ++it) {
-            const int slot = (int)(it % S);
-            const uint32_t ph = (uint32_t)((it / S) & 1);
-            mbar_wait(&full[slot], ph);
-            const int64_t r0 = r_begin + it * R;
-            const int nr = (int)((r_end - r0) < (int64_t)R ? (r_end - r0) : (int64_t)R);
+        int slot = 0;
+        uint32_t ph = 0;
+        int vo[VPT];  // element offset of this thread's k-th vector inside a row
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) vo[k] = (vok[k] ? tig + k * GT : 0) * W;
+
+        // One stage.  FULL: every row of the stage is valid (all but the last
+        // stage), so the body is free of row-validity predicates.
+        auto stage = [&](auto full_tag, int64_t r0, int nr) {
+            constexpr bool FULL = decltype(full_tag)::value;
             const T* sx = ring + (size_t)slot * 2 * R * Dp + (size_t)(g * RPG) * Dp;
             const T* sdy = sx + (size_t)R * Dp;
             const Acc* st = stats + ((size_t)slot * R + g * RPG) * 2;
@@ -244,12 +254,12 @@ __global__ void __launch_bounds__(LnBwdCfg<T, GW, VPT, G, RPG>::kBoundThreads, 1
             Acc mu[RPG], rs[RPG];
 #pragma unroll
             for (int i = 0; i < RPG; ++i) {
-                const bool valid = g * RPG + i < nr;
+                const bool valid = FULL || g * RPG + i < nr;
                 mu[i] = valid ? st[2 * i + 0] : Acc(0);
                 rs[i] = valid ? st[2 * i + 1] : Acc(0);
 #pragma unroll
                 for (int k = 0; k < VPT; ++k) {
-                    const size_t off = (size_t)i * Dp + (size_t)(tig + k * GT) * W;
+                    const int off = i * Dp + vo[k];
                     if (valid && vok[k]) {
                         ux[i][k] = *reinterpret_cast<const uint4*>(sx + off);
                         ug[i][k] = *reinterpret_cast<const uint4*>(sdy + off);
@@ -267,7 +277,7 @@ __global__ void __launch_bounds__(LnBwdCfg<T, GW, VPT, G, RPG>::kBoundThreads, 1
 #pragma unroll
             for (int i = 0; i < RPG; ++i) {
                 const int64_t row = r0 + g * RPG + i;
-                if (g * RPG + i < nr && row >= next_bound) flush_to(row / M);  // group-uniform
+                if ((FULL || g * RPG + i < nr) && row >= next_bound) flush_to(row / M);  // group-uniform
                 const P rs2 = PR::splat(rs[i]);
                 const P nmr2 = PR::splat(-mu[i] * rs[i]);
                 P s1 = PR::splat(Acc(0)), s2 = PR::splat(Acc(0));
@@ -276,7 +286,7 @@ __global__ void __launch_bounds__(LnBwdCfg<T, GW, VPT, G, RPG>::kBoundThreads, 1
                     P xf[NP], gf[NP], gm[NP];
                     unpack2<T>(ux[i][k], xf);
                     unpack2<T>(ug[i][k], gf);
-                    const P* gp = reinterpret_cast<const P*>(gam_s + (size_t)(vok[k] ? tig + k * GT : 0) * W);
+                    const P* gp = reinterpret_cast<const P*>(gam_s + vo[k]);
 #pragma unroll
                     for (int p = 0; p < NP; ++p) gm[p] = gp[p];
 #pragma unroll
@@ -318,32 +328,44 @@ __global__ void __launch_bounds__(LnBwdCfg<T, GW, VPT, G, RPG>::kBoundThreads, 1
             }
             // pass 2: dx = rstd*(h - mean(h)) - rstd*mean(h*xhat)*xhat
             if (dxg != nullptr) {
+                T* dxs = dxg + (r0 + g * RPG) * D;  // 64-bit base once per stage
 #pragma unroll
                 for (int i = 0; i < RPG; ++i) {
-                    if (g * RPG + i >= nr) continue;
-                    const int64_t row = r0 + g * RPG + i;
+                    if (!FULL && g * RPG + i >= nr) continue;
                     const P rs2 = PR::splat(rs[i]);
                     const P k1 = PR::splat(-rs[i] * tot[2 * i] * invD);
                     const P nc2 = PR::splat(-rs[i] * tot[2 * i + 1] * invD);
 #pragma unroll
                     for (int k = 0; k < VPT; ++k) {
                         if (!vok[k]) continue;
-                        const int v = tig + k * GT;
                         P o[NP];
 #pragma unroll
                         for (int p = 0; p < NP; ++p) o[p] = PR::fma(nc2, xh[i][k][p], PR::fma(hh[i][k][p], rs2, k1));
+                        T* dst = dxs + (uint32_t)(i * (int)D + vo[k]);
                         if (a.aligned) {
-                            st_stream(dxg + row * D + (int64_t)v * W, pack2<T>(o));
+                            st_stream(dst, pack2<T>(o));
                         } else {
                             const Acc* of = reinterpret_cast<const Acc*>(o);
 #pragma unroll
-                            for (int e = 0; e < W; ++e) {
-                                const int64_t col = (int64_t)v * W + e;
-                                if (col < D) dxg[row * D + col] = from_acc<T>(of[e]);
-                            }
+                            for (int e = 0; e < W; ++e)
+                                if (vo[k] + e < D) dst[e] = from_acc<T>(of[e]);
                         }
                     }
                 }
+            }
+        };
+
+        const int64_t n_full = (r_end - r_begin) / R;
+        for (int64_t it = 0; it < n_stage; ++it) {
+            mbar_wait(&full[slot], ph);
+            const int64_t r0 = r_begin + it * R;
+            if (it < n_full)
+                stage(std::true_type{}, r0, R);
+            else
+                stage(std::false_type{}, r0, (int)(r_end - r0));
+            if (++slot == S) {
+                slot = 0;
+                ph ^= 1u;
             }
         }
         flush_to((r_end - 1) / M + 1);
