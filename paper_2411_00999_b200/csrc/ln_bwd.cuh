@@ -72,13 +72,15 @@ struct LnBwdCfg {
     static constexpr int kBoundThreads = (kThreads + 127) / 128 * 128;
     static constexpr int R = G * RPG;           // rows per stage
     static constexpr int GT = GW * 32;          // threads per row group
-    static constexpr int kMaxVec = GT * VPT;    // vectors per row covered
-    static constexpr int kRedElems = 2 * G * (GW == 3 ? 4 : GW) * 2 * RPG;
+    static constexpr int NQ = 2 * RPG;          // row sums per stage and group: (s1, s2) per row
+    static constexpr int GWP = GW == 3 ? 4 : GW;  // power-of-two padded warps per group
+    static constexpr int kRedSlots = 4;         // deferred pass 2 keeps <= 3 stages of row sums live
+    static constexpr int kRedElems = G * kRedSlots * NQ * GWP;
     // byte offsets inside dynamic shared memory
-    static __host__ __device__ constexpr size_t bars_bytes(int S) { return (size_t)16 * S; }
+    static __host__ __device__ constexpr size_t bars_bytes(int S) { return (size_t)8 * (2 * S + G * kRedSlots); }
     static __host__ __device__ constexpr size_t red_off(int S) { return (bars_bytes(S) + 15) / 16 * 16; }
     static __host__ __device__ constexpr size_t stats_off(int S) {
-        return red_off(S) + (size_t)kRedElems * sizeof(Acc);
+        return red_off(S) + ((size_t)kRedElems * sizeof(Acc) + 15) / 16 * 16;
     }
     static __host__ __device__ constexpr size_t gam_off(int S) {
         return (stats_off(S) + (size_t)S * R * 2 * sizeof(Acc) + 15) / 16 * 16;
@@ -108,6 +110,7 @@ __global__ void __launch_bounds__(LnBwdCfg<T, GW, VPT, G, RPG>::kBoundThreads, 1
     const int S = a.stages;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + S;
+    uint64_t* redbar = empty + S;  // [G][kRedSlots]
     Acc* red = reinterpret_cast<Acc*>(smem + C::red_off(S));
     Acc* stats = reinterpret_cast<Acc*>(smem + C::stats_off(S));
     Acc* gam_s = reinterpret_cast<Acc*>(smem + C::gam_off(S));
@@ -126,11 +129,8 @@ __global__ void __launch_bounds__(LnBwdCfg<T, GW, VPT, G, RPG>::kBoundThreads, 1
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], NCW);
         }
+        for (int s = 0; s < G * C::kRedSlots; ++s) mbar_init(&redbar[s], GW);
         fence_mbar_init();
-    }
-    {  // gamma lives in shared memory (zero in the pad columns)
-        const Acc* gg = static_cast<const Acc*>(a.gamma);
-        for (int i = threadIdx.x; i < a.Dp; i += blockDim.x) gam_s[i] = i < a.D ? gg[i] : Acc(0);
     }
     if (!a.aligned) {  // padded rows: the pad columns must read as zero
         uint4* p = reinterpret_cast<uint4*>(ring);
@@ -182,23 +182,39 @@ __global__ void __launch_bounds__(LnBwdCfg<T, GW, VPT, G, RPG>::kBoundThreads, 1
         }
     } else {
         // ------------------------------------------------------ consumers --
+        using PR = Pair<Acc>;
+        using P = typename PR::P;
+        constexpr int NP = W / 2;     // pairs per 16-byte vector
+        constexpr int NQ = C::NQ;
+        constexpr int GWP = C::GWP;
+        static_assert(NQ * GWP <= 32, "cross-warp reduction layout");
         const int g = warp / GW, wig = warp % GW;
         const int tig = wig * 32 + lane;
         Acc* partial = static_cast<Acc*>(a.partial);
         T* dxg = static_cast<T*>(a.dx);
         const Acc invD = Acc(1) / Acc(D);
 
-        using PR = Pair<Acc>;
-        using P = typename PR::P;
-        constexpr int NP = W / 2;          // pairs per 16-byte vector
-        constexpr int NQ = 2 * RPG;        // row sums reduced per stage: (s1, s2) per row
-        constexpr int GWP = GW == 3 ? 4 : GW;  // power-of-two padding for the cross-warp tree
-        static_assert(NQ * GWP <= 32, "cross-warp reduction layout");
+        // gamma -> shared memory (consumers only; the producer is already streaming)
+        {
+            const Acc* gg = static_cast<const Acc*>(a.gamma);
+            const int nt = NCW * 32;
+            if (a.aligned && (D * (int64_t)sizeof(Acc)) % 16 == 0) {
+                constexpr int E = 16 / sizeof(Acc);
+                for (int i = threadIdx.x; i < Dp / E; i += nt)
+                    *reinterpret_cast<uint4*>(gam_s + i * E) = __ldg(reinterpret_cast<const uint4*>(gg) + i);
+            } else {
+                for (int i = threadIdx.x; i < Dp; i += nt) gam_s[i] = i < D ? gg[i] : Acc(0);
+            }
+            named_bar_sync(15, nt);
+        }
 
-        // this thread's column vectors
         bool vok[VPT];
+        int vo[VPT];  // element offset of this thread's k-th vector inside a row
 #pragma unroll
-        for (int k = 0; k < VPT; ++k) vok[k] = (tig + k * GT) < NVp;
+        for (int k = 0; k < VPT; ++k) {
+            vok[k] = (tig + k * GT) < NVp;
+            vo[k] = (vok[k] ? tig + k * GT : 0) * W;
+        }
 
         P ag[VPT][NP], ab[VPT][NP];
 #pragma unroll
@@ -215,12 +231,11 @@ __global__ void __launch_bounds__(LnBwdCfg<T, GW, VPT, G, RPG>::kBoundThreads, 1
 #pragma unroll
             for (int k = 0; k < VPT; ++k) {
                 if (!vok[k]) continue;
-                const int v = tig + k * GT;
 #pragma unroll
                 for (int p = 0; p < NP; ++p) {
                     const P z = PR::splat(Acc(0));
-                    *reinterpret_cast<P*>(base + (size_t)v * W + 2 * p) = zero ? z : ag[k][p];
-                    *reinterpret_cast<P*>(base + (size_t)Dp + (size_t)v * W + 2 * p) = zero ? z : ab[k][p];
+                    *reinterpret_cast<P*>(base + vo[k] + 2 * p) = zero ? z : ag[k][p];
+                    *reinterpret_cast<P*>(base + (size_t)Dp + vo[k] + 2 * p) = zero ? z : ab[k][p];
                 }
             }
         };
@@ -235,112 +250,104 @@ __global__ void __launch_bounds__(LnBwdCfg<T, GW, VPT, G, RPG>::kBoundThreads, 1
             next_bound = (cur_ex + 1) * M;
         };
 
-        int rbuf = 0;
-        int slot = 0;
-        uint32_t ph = 0;
-        int vo[VPT];  // element offset of this thread's k-th vector inside a row
+        // xhat and h = gamma*g of row i, vector k, recomputed from the staged rows
+        auto load_row = [&](const T* sx, const T* sdy, int i, int k, Acc mu, Acc rs, P* x2, P* h2, P* g2) {
+            const int off = i * Dp + vo[k];
+            P xf[NP];
+            unpack2<T>(*reinterpret_cast<const uint4*>(sx + off), xf);
+            unpack2<T>(*reinterpret_cast<const uint4*>(sdy + off), g2);
+            const P* gp = reinterpret_cast<const P*>(gam_s + vo[k]);
+            const P rs2 = PR::splat(rs), nmr2 = PR::splat(-mu * rs);
 #pragma unroll
-        for (int k = 0; k < VPT; ++k) vo[k] = (vok[k] ? tig + k * GT : 0) * W;
+            for (int p = 0; p < NP; ++p) {
+                x2[p] = HAS_MEAN ? PR::fma(xf[p], rs2, nmr2) : xf[p];
+                h2[p] = PR::mul(gp[p], g2[p]);
+            }
+        };
 
-        // One stage.  FULL: every row of the stage is valid (all but the last
-        // stage), so the body is free of row-validity predicates.
-        auto stage = [&](auto full_tag, int64_t r0, int nr) {
+        // Pass 1 of a stage: column partials, per-row sums -> per-warp totals
+        // published to red[rslot] and announced on redbar.  FULL: every row of
+        // the stage is valid (all but the last stage).
+        auto pass1 = [&](auto full_tag, int slot, int rslot, int64_t r0, int nr) {
             constexpr bool FULL = decltype(full_tag)::value;
             const T* sx = ring + (size_t)slot * 2 * R * Dp + (size_t)(g * RPG) * Dp;
             const T* sdy = sx + (size_t)R * Dp;
             const Acc* st = stats + ((size_t)slot * R + g * RPG) * 2;
-
-            uint4 ux[RPG][VPT], ug[RPG][VPT];
-            Acc mu[RPG], rs[RPG];
-#pragma unroll
-            for (int i = 0; i < RPG; ++i) {
-                const bool valid = FULL || g * RPG + i < nr;
-                mu[i] = valid ? st[2 * i + 0] : Acc(0);
-                rs[i] = valid ? st[2 * i + 1] : Acc(0);
-#pragma unroll
-                for (int k = 0; k < VPT; ++k) {
-                    const int off = i * Dp + vo[k];
-                    if (valid && vok[k]) {
-                        ux[i][k] = *reinterpret_cast<const uint4*>(sx + off);
-                        ug[i][k] = *reinterpret_cast<const uint4*>(sdy + off);
-                    } else {
-                        ux[i][k] = ug[i][k] = make_uint4(0, 0, 0, 0);
-                    }
-                }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[slot]);  // slot may be refilled now
-
-            // pass 1: xhat, h = gamma*g kept in registers; row sums; column partials
-            P xh[RPG][VPT][NP], hh[RPG][VPT][NP];
             Acc q[NQ];
 #pragma unroll
             for (int i = 0; i < RPG; ++i) {
+                const bool valid = FULL || g * RPG + i < nr;
+                q[2 * i] = q[2 * i + 1] = Acc(0);
+                if (!valid) continue;
                 const int64_t row = r0 + g * RPG + i;
-                if ((FULL || g * RPG + i < nr) && row >= next_bound) flush_to(row / M);  // group-uniform
-                const P rs2 = PR::splat(rs[i]);
-                const P nmr2 = PR::splat(-mu[i] * rs[i]);
+                if (row >= next_bound) flush_to(row / M);  // group-uniform
+                const Acc mu = st[2 * i], rs = st[2 * i + 1];
                 P s1 = PR::splat(Acc(0)), s2 = PR::splat(Acc(0));
 #pragma unroll
                 for (int k = 0; k < VPT; ++k) {
-                    P xf[NP], gf[NP], gm[NP];
-                    unpack2<T>(ux[i][k], xf);
-                    unpack2<T>(ug[i][k], gf);
-                    const P* gp = reinterpret_cast<const P*>(gam_s + vo[k]);
-#pragma unroll
-                    for (int p = 0; p < NP; ++p) gm[p] = gp[p];
+                    if (!vok[k]) continue;
+                    P x2[NP], h2[NP], g2[NP];
+                    load_row(sx, sdy, i, k, mu, rs, x2, h2, g2);
 #pragma unroll
                     for (int p = 0; p < NP; ++p) {
-                        const P x2 = HAS_MEAN ? PR::fma(xf[p], rs2, nmr2) : xf[p];
-                        const P h2 = PR::mul(gm[p], gf[p]);
-                        s1 = PR::add(s1, h2);
-                        s2 = PR::fma(h2, x2, s2);
-                        ag[k][p] = PR::fma(x2, gf[p], ag[k][p]);
-                        ab[k][p] = PR::add(ab[k][p], gf[p]);
-                        xh[i][k][p] = x2;
-                        hh[i][k][p] = h2;
+                        s1 = PR::add(s1, h2[p]);
+                        s2 = PR::fma(h2[p], x2[p], s2);
+                        ag[k][p] = PR::fma(x2[p], g2[p], ag[k][p]);
+                        ab[k][p] = PR::add(ab[k][p], g2[p]);
                     }
                 }
                 q[2 * i] = s1.x + s1.y;
                 q[2 * i + 1] = s2.x + s2.y;
             }
-            // row reductions over the group: transposed butterfly within the
-            // warp, then a padded xor tree over the group's warps
-            butterfly_sum<NQ>(q, lane);
+            butterfly_sum<NQ>(q, lane);  // q[0] = warp total of quantity lane / (32/NQ)
+            if constexpr (GW == 1) {
+                if ((lane & (32 / NQ - 1)) == 0) red[((size_t)g * C::kRedSlots + rslot) * NQ + lane / (32 / NQ)] = q[0];
+                __syncwarp();
+            } else {
+                Acc* rb = red + ((size_t)g * C::kRedSlots + rslot) * NQ * GWP;
+                if ((lane & (32 / NQ - 1)) == 0) rb[(lane / (32 / NQ)) * GWP + wig] = q[0];
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&redbar[g * C::kRedSlots + rslot]);
+            }
+        };
+
+        // Pass 2 of a stage (deferred by one stage so the cross-warp wait is
+        // hidden behind the next stage's pass 1): dx, then release the slot.
+        auto pass2 = [&](auto full_tag, int slot, int rslot, uint32_t rph, int64_t r0, int nr) {
+            constexpr bool FULL = decltype(full_tag)::value;
             Acc tot[NQ];
             if constexpr (GW == 1) {
 #pragma unroll
-                for (int j = 0; j < NQ; ++j) tot[j] = __shfl_sync(0xffffffffu, q[0], j * (32 / NQ));
+                for (int j = 0; j < NQ; ++j) tot[j] = red[((size_t)g * C::kRedSlots + rslot) * NQ + j];
             } else {
-                Acc* rb = red + (size_t)(rbuf * G + g) * NQ * GWP;
-                if ((lane & (32 / NQ - 1)) == 0) rb[(lane / (32 / NQ)) * GWP + wig] = q[0];
-                named_bar_sync(1 + g, GT);
+                mbar_wait(&redbar[g * C::kRedSlots + rslot], rph);
+                const Acc* rb = red + ((size_t)g * C::kRedSlots + rslot) * NQ * GWP;
                 Acc t = Acc(0);
-                if (lane < NQ * GWP) {
-                    const int w = lane % GWP;
-                    t = w < GW ? rb[lane] : Acc(0);
-                }
+                if (lane < NQ * GWP && (lane % GWP) < GW) t = rb[lane];
 #pragma unroll
                 for (int m = GWP / 2; m >= 1; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
 #pragma unroll
                 for (int j = 0; j < NQ; ++j) tot[j] = __shfl_sync(0xffffffffu, t, j * GWP);
-                rbuf ^= 1;
             }
-            // pass 2: dx = rstd*(h - mean(h)) - rstd*mean(h*xhat)*xhat
+            const T* sx = ring + (size_t)slot * 2 * R * Dp + (size_t)(g * RPG) * Dp;
+            const T* sdy = sx + (size_t)R * Dp;
+            const Acc* st = stats + ((size_t)slot * R + g * RPG) * 2;
             if (dxg != nullptr) {
                 T* dxs = dxg + (r0 + g * RPG) * D;  // 64-bit base once per stage
 #pragma unroll
                 for (int i = 0; i < RPG; ++i) {
                     if (!FULL && g * RPG + i >= nr) continue;
-                    const P rs2 = PR::splat(rs[i]);
-                    const P k1 = PR::splat(-rs[i] * tot[2 * i] * invD);
-                    const P nc2 = PR::splat(-rs[i] * tot[2 * i + 1] * invD);
+                    const Acc mu = st[2 * i], rs = st[2 * i + 1];
+                    const P rs2 = PR::splat(rs);
+                    const P k1 = PR::splat(-rs * tot[2 * i] * invD);
+                    const P nc2 = PR::splat(-rs * tot[2 * i + 1] * invD);
 #pragma unroll
                     for (int k = 0; k < VPT; ++k) {
                         if (!vok[k]) continue;
-                        P o[NP];
+                        P x2[NP], h2[NP], g2[NP], o[NP];
+                        load_row(sx, sdy, i, k, mu, rs, x2, h2, g2);
 #pragma unroll
-                        for (int p = 0; p < NP; ++p) o[p] = PR::fma(nc2, xh[i][k][p], PR::fma(hh[i][k][p], rs2, k1));
+                        for (int p = 0; p < NP; ++p) o[p] = PR::fma(nc2, x2[p], PR::fma(h2[p], rs2, k1));
                         T* dst = dxs + (uint32_t)(i * (int)D + vo[k]);
                         if (a.aligned) {
                             st_stream(dst, pack2<T>(o));
@@ -353,21 +360,41 @@ __global__ void __launch_bounds__(LnBwdCfg<T, GW, VPT, G, RPG>::kBoundThreads, 1
                     }
                 }
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[slot]);  // slot may be refilled now
         };
 
         const int64_t n_full = (r_end - r_begin) / R;
+        auto run_pass2 = [&](int64_t it, int slot, int rslot, uint32_t rph) {
+            const int64_t r0 = r_begin + it * R;
+            if (it < n_full)
+                pass2(std::true_type{}, slot, rslot, rph, r0, R);
+            else
+                pass2(std::false_type{}, slot, rslot, rph, r0, (int)(r_end - r0));
+        };
+        int slot = 0, rslot = 0, pslot = 0, prslot = 0;
+        uint32_t ph = 0, rph = 0, prph = 0;
         for (int64_t it = 0; it < n_stage; ++it) {
             mbar_wait(&full[slot], ph);
             const int64_t r0 = r_begin + it * R;
             if (it < n_full)
-                stage(std::true_type{}, r0, R);
+                pass1(std::true_type{}, slot, rslot, r0, R);
             else
-                stage(std::false_type{}, r0, (int)(r_end - r0));
+                pass1(std::false_type{}, slot, rslot, r0, (int)(r_end - r0));
+            if (it > 0) run_pass2(it - 1, pslot, prslot, prph);
+            pslot = slot;
+            prslot = rslot;
+            prph = rph;
             if (++slot == S) {
                 slot = 0;
                 ph ^= 1u;
             }
+            if (++rslot == C::kRedSlots) {
+                rslot = 0;
+                rph ^= 1u;
+            }
         }
+        if (n_stage > 0) run_pass2(n_stage - 1, pslot, prslot, prph);
         flush_to((r_end - 1) / M + 1);
     }
 

@@ -54,7 +54,7 @@ int plan_bwd(int64_t B, int64_t M, int64_t D, BwdPlan& p, const char** why) {
     p.Dp = (int)((D + W - 1) / W * W);
     const size_t budget = (size_t)smem_optin_bytes() - 1024;
     p.stages = 0;
-    for (int s = 8; s >= 1; --s)
+    for (int s = 8; s >= 2; --s)  // >= 2: pass 2 holds a slot while the next stage is consumed
         if (C::smem_bytes(s, p.Dp) <= budget) {
             p.stages = s;
             break;
@@ -143,7 +143,7 @@ struct BwdOp {
                 return 2;
             }
             if (occ >= 1) break;
-            if (p.stages <= 1) {
+            if (p.stages <= 2) {
                 *cerr = cudaErrorCooperativeLaunchTooLarge;
                 return 2;
             }
