@@ -10,16 +10,19 @@
 // Design (one HBM pass over x/xhat, dy; one write of dx):
 //   * persistent cooperative grid, one CTA per SM; CTA c owns the contiguous
 //     row range [c*N/grid, (c+1)*N/grid) (rows of an example are contiguous);
-//   * one producer warp streams R-row stages of x and dy into a shared-memory
-//     ring with 1-D TMA (cp.async.bulk, L2 evict_first) signalled on mbarriers;
-//     mean/rstd ride along in the same stage;
-//   * consumer warps form G row groups of GW warps; a thread owns VPT 16-byte
-//     column vectors for the whole kernel, so the per-example dgamma/dbeta
-//     partials accumulate over the sequence axis in registers;
-//   * row reductions mean(h), mean(h*xhat): warp shuffles + one named barrier
-//     per group per stage (RPG rows batched per barrier);
-//   * at each example boundary a group flushes its register partials to a slot
-//     (cta + example, group) of an L2-resident workspace;
+//   * R-row stages of x and dy stream into a shared-memory ring by 1-D TMA
+//     (cp.async.bulk, L2 evict_first) completing on mbarriers.  There is no
+//     dedicated producer warp: lane 0 of warp 0 refills a slot as soon as
+//     every warp released it, so all 16 warps do row math;
+//   * mean/rstd are read straight from global memory one stage ahead;
+//   * warps form G row groups of GW warps; a thread owns VPT 16-byte column
+//     vectors for the whole kernel, so the per-example dgamma/dbeta partials
+//     accumulate over the sequence axis in registers (packed fp32x2 math:
+//     FFMA2/FADD2/FMUL2);
+//   * row reductions mean(h), mean(h*xhat): a transposed butterfly inside
+//     the warp, then a padded xor tree across the group's warps;
+//   * at each example boundary a group flushes its register partials to a
+//     slot (cta + example, group) of an L2-resident workspace;
 //   * stage 2 after a software grid barrier: column chunks sum the slots of
 //     each example in fixed (cta, group) order -> gamma'_b; square and reduce
 //     over D in fp64 -> per-(example, chunk) partial norms; fixed-order sum
@@ -65,25 +68,22 @@ template <typename T, int GW, int VPT, int G, int RPG>
 struct LnBwdCfg {
     using Acc = typename Traits<T>::Acc;
     static constexpr int W = Traits<T>::W;
-    static constexpr int kConsumerWarps = GW * G;
-    static constexpr int kThreads = (kConsumerWarps + 1) * 32;
+    static constexpr int kWarps = GW * G;
+    static constexpr int kThreads = kWarps * 32;
     // registers are allocated for warps in groups of 4: bound the register
     // budget by the rounded-up block so one CTA always fits on an SM
     static constexpr int kBoundThreads = (kThreads + 127) / 128 * 128;
     static constexpr int R = G * RPG;           // rows per stage
     static constexpr int GT = GW * 32;          // threads per row group
     static constexpr int NQ = 2 * RPG;          // row sums per stage and group: (s1, s2) per row
-    static constexpr int GWP = GW == 3 ? 4 : GW;  // power-of-two padded warps per group
-    static constexpr int kRedSlots = 4;         // deferred pass 2 keeps <= 3 stages of row sums live
-    static constexpr int kRedElems = G * kRedSlots * NQ * GWP;
+    static constexpr int GWP = GW == 3 ? 4 : (GW == 5 ? 8 : GW);  // power-of-two padded warps per group
+    static constexpr bool KEEP = VPT * RPG <= 2;  // keep xhat/h of a stage in registers
+    static constexpr int kRedElems = 2 * G * NQ * GWP;
     // byte offsets inside dynamic shared memory
-    static __host__ __device__ constexpr size_t bars_bytes(int S) { return (size_t)8 * (2 * S + G * kRedSlots); }
+    static __host__ __device__ constexpr size_t bars_bytes(int S) { return (size_t)8 * 2 * S; }
     static __host__ __device__ constexpr size_t red_off(int S) { return (bars_bytes(S) + 15) / 16 * 16; }
-    static __host__ __device__ constexpr size_t stats_off(int S) {
-        return red_off(S) + ((size_t)kRedElems * sizeof(Acc) + 15) / 16 * 16;
-    }
     static __host__ __device__ constexpr size_t gam_off(int S) {
-        return (stats_off(S) + (size_t)S * R * 2 * sizeof(Acc) + 15) / 16 * 16;
+        return red_off(S) + ((size_t)kRedElems * sizeof(Acc) + 15) / 16 * 16;
     }
     static __host__ __device__ constexpr size_t rows_off(int S, int Dp) {
         return (gam_off(S) + (size_t)Dp * sizeof(Acc) + 127) / 128 * 128;
@@ -101,18 +101,23 @@ template <typename T, int GW, int VPT, int G, int RPG, bool HAS_MEAN, bool NORMS
 __global__ void __launch_bounds__(LnBwdCfg<T, GW, VPT, G, RPG>::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a) {
     using C = LnBwdCfg<T, GW, VPT, G, RPG>;
     using Acc = typename C::Acc;
+    using PR = Pair<Acc>;
+    using P = typename PR::P;
     constexpr int W = C::W;
     constexpr int R = C::R;
     constexpr int GT = C::GT;
-    constexpr int NCW = C::kConsumerWarps;
+    constexpr int NW = C::kWarps;
+    constexpr int NP = W / 2;     // pairs per 16-byte vector
+    constexpr int NQ = C::NQ;
+    constexpr int GWP = C::GWP;
+    constexpr bool KEEP = C::KEEP;
+    static_assert(NQ * GWP <= 32, "cross-warp reduction layout");
 
     extern __shared__ __align__(128) unsigned char smem[];
     const int S = a.stages;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + S;
-    uint64_t* redbar = empty + S;  // [G][kRedSlots]
     Acc* red = reinterpret_cast<Acc*>(smem + C::red_off(S));
-    Acc* stats = reinterpret_cast<Acc*>(smem + C::stats_off(S));
     Acc* gam_s = reinterpret_cast<Acc*>(smem + C::gam_off(S));
     T* ring = reinterpret_cast<T*>(smem + C::rows_off(S, a.Dp));
 
@@ -123,13 +128,16 @@ __global__ void __launch_bounds__(LnBwdCfg<T, GW, VPT, G, RPG>::kBoundThreads, 1
     const int NVp = Dp / W;  // vectors per (padded) row
     const int64_t r_begin = (int64_t)cta * N / grid, r_end = (int64_t)(cta + 1) * N / grid;
     const int64_t n_stage = (r_end - r_begin + R - 1) / R;
+    const T* xg = static_cast<const T*>(a.x);
+    const T* dyg = static_cast<const T*>(a.dy);
+    const Acc* meang = static_cast<const Acc*>(a.mean);
+    const Acc* rstdg = static_cast<const Acc*>(a.rstd);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], NCW);
+            mbar_init(&empty[s], NW);
         }
-        for (int s = 0; s < G * C::kRedSlots; ++s) mbar_init(&redbar[s], GW);
         fence_mbar_init();
     }
     if (!a.aligned) {  // padded rows: the pad columns must read as zero
@@ -139,269 +147,291 @@ __global__ void __launch_bounds__(LnBwdCfg<T, GW, VPT, G, RPG>::kBoundThreads, 1
     }
     __syncthreads();
 
-    if (warp == NCW) {
-        // ------------------------------------------------------- producer --
-        const T* xg = static_cast<const T*>(a.x);
-        const T* dyg = static_cast<const T*>(a.dy);
-        const Acc* meang = static_cast<const Acc*>(a.mean);
-        const Acc* rstdg = static_cast<const Acc*>(a.rstd);
-        const uint64_t pol = policy_evict_first();
-        int slot = 0;
-        uint32_t ph = 0;
-        for (int64_t it = 0; it < n_stage; ++it) {
-            mbar_wait(&empty[slot], ph ^ 1u);
-            const int64_t r0 = r_begin + it * R;
-            const int nr = (int)((r_end - r0) < (int64_t)R ? (r_end - r0) : (int64_t)R);
-            T* sx = ring + (size_t)slot * 2 * R * Dp;
-            T* sdy = sx + (size_t)R * Dp;
-            if (a.aligned) {
-                if (lane == 0) {
-                    const uint32_t bytes = (uint32_t)(nr * D * (int64_t)sizeof(T));
-                    mbar_expect_tx(&full[slot], 2 * bytes);
-                    bulk_g2s(sx, xg + r0 * D, bytes, &full[slot], pol);
-                    bulk_g2s(sdy, dyg + r0 * D, bytes, &full[slot], pol);
-                }
-            } else {
-                const int64_t ne = (int64_t)nr * D;
-                for (int64_t e = lane; e < ne; e += 32) {
-                    const int64_t rr = e / D, cc = e - rr * D;
-                    sx[rr * Dp + cc] = xg[r0 * D + e];
-                    sdy[rr * Dp + cc] = dyg[r0 * D + e];
-                }
+    // ------------------------------------------------------------ producer --
+    // Fill stage `st` into its slot.  Called by warp 0 only (lane 0 issues the
+    // TMA; the generic path copies with the whole warp).
+    const uint64_t pol = policy_evict_first();
+    auto issue = [&](int64_t st) {
+        const int slot = (int)(st % S);
+        const int64_t r0 = r_begin + st * R;
+        const int nr = (int)((r_end - r0) < (int64_t)R ? (r_end - r0) : (int64_t)R);
+        T* sx = ring + (size_t)slot * 2 * R * Dp;
+        T* sdy = sx + (size_t)R * Dp;
+        if (a.aligned) {
+            if (lane == 0) {
+                const uint32_t bytes = (uint32_t)(nr * D * (int64_t)sizeof(T));
+                mbar_expect_tx(&full[slot], 2 * bytes);
+                bulk_g2s(sx, xg + r0 * D, bytes, &full[slot], pol);
+                bulk_g2s(sdy, dyg + r0 * D, bytes, &full[slot], pol);
+                mbar_arrive(&full[slot]);
             }
-            for (int j = lane; j < nr; j += 32) {
-                stats[((size_t)slot * R + j) * 2 + 0] = HAS_MEAN ? meang[r0 + j] : Acc(0);
-                stats[((size_t)slot * R + j) * 2 + 1] = rstdg[r0 + j];
+        } else {
+            const int64_t ne = (int64_t)nr * D;
+            for (int64_t e = lane; e < ne; e += 32) {
+                const int64_t rr = e / D, cc = e - rr * D;
+                sx[rr * Dp + cc] = xg[r0 * D + e];
+                sdy[rr * Dp + cc] = dyg[r0 * D + e];
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&full[slot]);
-            if (++slot == S) {
-                slot = 0;
-                ph ^= 1u;
-            }
         }
-    } else {
-        // ------------------------------------------------------ consumers --
-        using PR = Pair<Acc>;
-        using P = typename PR::P;
-        constexpr int NP = W / 2;     // pairs per 16-byte vector
-        constexpr int NQ = C::NQ;
-        constexpr int GWP = C::GWP;
-        static_assert(NQ * GWP <= 32, "cross-warp reduction layout");
-        const int g = warp / GW, wig = warp % GW;
-        const int tig = wig * 32 + lane;
-        Acc* partial = static_cast<Acc*>(a.partial);
-        T* dxg = static_cast<T*>(a.dx);
-        const Acc invD = Acc(1) / Acc(D);
-
-        // gamma -> shared memory (consumers only; the producer is already streaming)
-        {
-            const Acc* gg = static_cast<const Acc*>(a.gamma);
-            const int nt = NCW * 32;
-            if (a.aligned && (D * (int64_t)sizeof(Acc)) % 16 == 0) {
-                constexpr int E = 16 / sizeof(Acc);
-                for (int i = threadIdx.x; i < Dp / E; i += nt)
-                    *reinterpret_cast<uint4*>(gam_s + i * E) = __ldg(reinterpret_cast<const uint4*>(gg) + i);
+    };
+    int64_t issued = 0;  // warp 0: stages handed to the ring so far
+    if (warp == 0) {
+        for (; issued < n_stage && issued < S; ++issued) issue(issued);
+    }
+    // warp 0 refills every slot whose stage all warps have released; `need`
+    // forces progress up to that stage (blocking on its slot's release)
+    auto refill = [&](int64_t need) {
+        for (; issued < n_stage; ++issued) {
+            const int slot = (int)(issued % S);
+            const uint32_t par = (uint32_t)(((issued / S) - 1) & 1);  // phase of the release of stage issued - S
+            if (issued > need) {
+                const bool ok = __shfl_sync(0xffffffffu, lane == 0 ? (int)mbar_try_wait(&empty[slot], par) : 0, 0) != 0;
+                if (!ok) break;
             } else {
-                for (int i = threadIdx.x; i < Dp; i += nt) gam_s[i] = i < D ? gg[i] : Acc(0);
+                mbar_wait(&empty[slot], par);
             }
-            named_bar_sync(15, nt);
+            issue(issued);
         }
+    };
 
-        bool vok[VPT];
-        int vo[VPT];  // element offset of this thread's k-th vector inside a row
+    // ----------------------------------------------------------- consumers --
+    const int g = warp / GW, wig = warp % GW;
+    const int tig = wig * 32 + lane;
+    Acc* partial = static_cast<Acc*>(a.partial);
+    T* dxg = static_cast<T*>(a.dx);
+    const Acc invD = Acc(1) / Acc(D);
+
+    {  // gamma -> shared memory (while the first stages are in flight)
+        const Acc* gg = static_cast<const Acc*>(a.gamma);
+        if (a.aligned && (D * (int64_t)sizeof(Acc)) % 16 == 0) {
+            constexpr int E = 16 / sizeof(Acc);
+            for (int i = threadIdx.x; i < Dp / E; i += blockDim.x)
+                *reinterpret_cast<uint4*>(gam_s + i * E) = __ldg(reinterpret_cast<const uint4*>(gg) + i);
+        } else {
+            for (int i = threadIdx.x; i < Dp; i += blockDim.x) gam_s[i] = i < D ? gg[i] : Acc(0);
+        }
+        __syncthreads();
+    }
+
+    bool vok[VPT];
+    int vo[VPT];  // element offset of this thread's k-th vector inside a row
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+        vok[k] = (tig + k * GT) < NVp;
+        vo[k] = (vok[k] ? tig + k * GT : 0) * W;
+    }
+
+    P ag[VPT][NP], ab[VPT][NP];
+#pragma unroll
+    for (int k = 0; k < VPT; ++k)
+#pragma unroll
+        for (int p = 0; p < NP; ++p) ag[k][p] = ab[k][p] = PR::splat(Acc(0));
+
+    int64_t cur_ex = r_begin / M;
+    int64_t next_bound = (cur_ex + 1) * M;
+
+    // write this group's register partials to slot (cta + ex, g)
+    auto write_slot = [&](int64_t ex, bool zero) {
+        Acc* base = partial + ((size_t)(cta + ex) * G + g) * 2 * Dp;
 #pragma unroll
         for (int k = 0; k < VPT; ++k) {
-            vok[k] = (tig + k * GT) < NVp;
-            vo[k] = (vok[k] ? tig + k * GT : 0) * W;
+            if (!vok[k]) continue;
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                const P z = PR::splat(Acc(0));
+                *reinterpret_cast<P*>(base + vo[k] + 2 * p) = zero ? z : ag[k][p];
+                *reinterpret_cast<P*>(base + (size_t)Dp + vo[k] + 2 * p) = zero ? z : ab[k][p];
+            }
         }
-
-        P ag[VPT][NP], ab[VPT][NP];
+    };
+    auto flush_to = [&](int64_t new_ex) {
+        write_slot(cur_ex, false);
 #pragma unroll
         for (int k = 0; k < VPT; ++k)
 #pragma unroll
             for (int p = 0; p < NP; ++p) ag[k][p] = ab[k][p] = PR::splat(Acc(0));
+        for (int64_t ex = cur_ex + 1; ex < new_ex; ++ex) write_slot(ex, true);
+        cur_ex = new_ex;
+        next_bound = (cur_ex + 1) * M;
+    };
 
-        int64_t cur_ex = r_begin / M;
-        int64_t next_bound = (cur_ex + 1) * M;
+    // per-row statistics of this group's rows, prefetched one stage ahead
+    auto load_stats = [&](int64_t st, Acc* mu, Acc* rs) {
+#pragma unroll
+        for (int i = 0; i < RPG; ++i) {
+            int64_t row = r_begin + st * R + g * RPG + i;
+            if (row >= r_end || st >= n_stage) row = r_begin;  // clamp (value unused)
+            mu[i] = HAS_MEAN ? __ldg(meang + row) : Acc(0);
+            rs[i] = __ldg(rstdg + row);
+        }
+    };
 
-        // write this group's register partials to slot (cta + ex, g)
-        auto write_slot = [&](int64_t ex, bool zero) {
-            Acc* base = partial + ((size_t)(cta + ex) * G + g) * 2 * Dp;
+    // xhat and h = gamma*g of a staged vector
+    auto make_xh = [&](const uint4& ux, const uint4& ug, int k, Acc mu, Acc rs, P* x2, P* h2, P* g2) {
+        P xf[NP];
+        unpack2<T>(ux, xf);
+        unpack2<T>(ug, g2);
+        const P* gp = reinterpret_cast<const P*>(gam_s + vo[k]);
+        const P rs2 = PR::splat(rs), nmr2 = PR::splat(-mu * rs);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            x2[p] = HAS_MEAN ? PR::fma(xf[p], rs2, nmr2) : xf[p];
+            h2[p] = PR::mul(gp[p], g2[p]);
+        }
+    };
+
+    // One stage.  FULL: every row of the stage is valid (all but the last).
+    int rbuf = 0;
+    auto stage = [&](auto full_tag, int slot, int64_t r0, int nr, const Acc* mu, const Acc* rs) {
+        constexpr bool FULL = decltype(full_tag)::value;
+        const T* sx = ring + (size_t)slot * 2 * R * Dp + (size_t)(g * RPG) * Dp;
+        const T* sdy = sx + (size_t)R * Dp;
+
+        uint4 ux[RPG][VPT], ug[RPG][VPT];
+#pragma unroll
+        for (int i = 0; i < RPG; ++i) {
+            const bool valid = FULL || g * RPG + i < nr;
 #pragma unroll
             for (int k = 0; k < VPT; ++k) {
-                if (!vok[k]) continue;
-#pragma unroll
-                for (int p = 0; p < NP; ++p) {
-                    const P z = PR::splat(Acc(0));
-                    *reinterpret_cast<P*>(base + vo[k] + 2 * p) = zero ? z : ag[k][p];
-                    *reinterpret_cast<P*>(base + (size_t)Dp + vo[k] + 2 * p) = zero ? z : ab[k][p];
+                const int off = i * Dp + vo[k];
+                if (valid && vok[k]) {
+                    ux[i][k] = *reinterpret_cast<const uint4*>(sx + off);
+                    ug[i][k] = *reinterpret_cast<const uint4*>(sdy + off);
+                } else {
+                    ux[i][k] = ug[i][k] = make_uint4(0, 0, 0, 0);
                 }
             }
-        };
-        auto flush_to = [&](int64_t new_ex) {
-            write_slot(cur_ex, false);
-#pragma unroll
-            for (int k = 0; k < VPT; ++k)
-#pragma unroll
-                for (int p = 0; p < NP; ++p) ag[k][p] = ab[k][p] = PR::splat(Acc(0));
-            for (int64_t ex = cur_ex + 1; ex < new_ex; ++ex) write_slot(ex, true);
-            cur_ex = new_ex;
-            next_bound = (cur_ex + 1) * M;
-        };
+        }
+        if constexpr (KEEP) {  // everything needed is in registers: release the slot now
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[slot]);
+        }
 
-        // xhat and h = gamma*g of row i, vector k, recomputed from the staged rows
-        auto load_row = [&](const T* sx, const T* sdy, int i, int k, Acc mu, Acc rs, P* x2, P* h2, P* g2) {
-            const int off = i * Dp + vo[k];
-            P xf[NP];
-            unpack2<T>(*reinterpret_cast<const uint4*>(sx + off), xf);
-            unpack2<T>(*reinterpret_cast<const uint4*>(sdy + off), g2);
-            const P* gp = reinterpret_cast<const P*>(gam_s + vo[k]);
-            const P rs2 = PR::splat(rs), nmr2 = PR::splat(-mu * rs);
+        // pass 1: row sums (split chains per vector), column partials
+        P xh[KEEP ? RPG : 1][KEEP ? VPT : 1][NP], hh[KEEP ? RPG : 1][KEEP ? VPT : 1][NP];
+        Acc q[NQ];
 #pragma unroll
-            for (int p = 0; p < NP; ++p) {
-                x2[p] = HAS_MEAN ? PR::fma(xf[p], rs2, nmr2) : xf[p];
-                h2[p] = PR::mul(gp[p], g2[p]);
+        for (int i = 0; i < RPG; ++i) {
+            const bool valid = FULL || g * RPG + i < nr;
+            const int64_t row = r0 + g * RPG + i;
+            if (valid && row >= next_bound) flush_to(row / M);  // group-uniform
+            P s1[VPT], s2[VPT];
+#pragma unroll
+            for (int k = 0; k < VPT; ++k) {
+                s1[k] = s2[k] = PR::splat(Acc(0));
+                P x2[NP], h2[NP], g2[NP];
+                make_xh(ux[i][k], ug[i][k], k, valid ? mu[i] : Acc(0), valid ? rs[i] : Acc(0), x2, h2, g2);
+#pragma unroll
+                for (int p = 0; p < NP; ++p) {
+                    s1[k] = PR::add(s1[k], h2[p]);
+                    s2[k] = PR::fma(h2[p], x2[p], s2[k]);
+                    ag[k][p] = PR::fma(x2[p], g2[p], ag[k][p]);
+                    ab[k][p] = PR::add(ab[k][p], g2[p]);
+                    if constexpr (KEEP) {
+                        xh[i][k][p] = x2[p];
+                        hh[i][k][p] = h2[p];
+                    }
+                }
             }
-        };
-
-        // Pass 1 of a stage: column partials, per-row sums -> per-warp totals
-        // published to red[rslot] and announced on redbar.  FULL: every row of
-        // the stage is valid (all but the last stage).
-        auto pass1 = [&](auto full_tag, int slot, int rslot, int64_t r0, int nr) {
-            constexpr bool FULL = decltype(full_tag)::value;
-            const T* sx = ring + (size_t)slot * 2 * R * Dp + (size_t)(g * RPG) * Dp;
-            const T* sdy = sx + (size_t)R * Dp;
-            const Acc* st = stats + ((size_t)slot * R + g * RPG) * 2;
-            Acc q[NQ];
+#pragma unroll
+            for (int k = 1; k < VPT; ++k) {
+                s1[0] = PR::add(s1[0], s1[k]);
+                s2[0] = PR::add(s2[0], s2[k]);
+            }
+            q[2 * i] = s1[0].x + s1[0].y;
+            q[2 * i + 1] = s2[0].x + s2[0].y;
+        }
+        // row reductions over the group: transposed butterfly within the
+        // warp, then a padded xor tree over the group's warps
+        butterfly_sum<NQ>(q, lane);
+        Acc tot[NQ];
+        if constexpr (GW == 1) {
+#pragma unroll
+            for (int j = 0; j < NQ; ++j) tot[j] = __shfl_sync(0xffffffffu, q[0], j * (32 / NQ));
+        } else {
+            Acc* rb = red + (size_t)(rbuf * G + g) * NQ * GWP;
+            if ((lane & (32 / NQ - 1)) == 0) rb[(lane / (32 / NQ)) * GWP + wig] = q[0];
+            named_bar_sync(1 + g, GT);
+            Acc t = Acc(0);
+            if (lane < NQ * GWP && (lane % GWP) < GW) t = rb[lane];
+#pragma unroll
+            for (int m = GWP / 2; m >= 1; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
+#pragma unroll
+            for (int j = 0; j < NQ; ++j) tot[j] = __shfl_sync(0xffffffffu, t, j * GWP);
+            rbuf ^= 1;
+        }
+        // pass 2: dx = rstd*(h - mean(h)) - rstd*mean(h*xhat)*xhat
+        if (dxg != nullptr) {
+            T* dxs = dxg + (r0 + g * RPG) * D;  // 64-bit base once per stage
 #pragma unroll
             for (int i = 0; i < RPG; ++i) {
-                const bool valid = FULL || g * RPG + i < nr;
-                q[2 * i] = q[2 * i + 1] = Acc(0);
-                if (!valid) continue;
-                const int64_t row = r0 + g * RPG + i;
-                if (row >= next_bound) flush_to(row / M);  // group-uniform
-                const Acc mu = st[2 * i], rs = st[2 * i + 1];
-                P s1 = PR::splat(Acc(0)), s2 = PR::splat(Acc(0));
+                if (!FULL && g * RPG + i >= nr) continue;
+                const P rs2 = PR::splat(rs[i]);
+                const P k1 = PR::splat(-rs[i] * tot[2 * i] * invD);
+                const P nc2 = PR::splat(-rs[i] * tot[2 * i + 1] * invD);
 #pragma unroll
                 for (int k = 0; k < VPT; ++k) {
                     if (!vok[k]) continue;
-                    P x2[NP], h2[NP], g2[NP];
-                    load_row(sx, sdy, i, k, mu, rs, x2, h2, g2);
+                    P o[NP];
+                    if constexpr (KEEP) {
 #pragma unroll
-                    for (int p = 0; p < NP; ++p) {
-                        s1 = PR::add(s1, h2[p]);
-                        s2 = PR::fma(h2[p], x2[p], s2);
-                        ag[k][p] = PR::fma(x2[p], g2[p], ag[k][p]);
-                        ab[k][p] = PR::add(ab[k][p], g2[p]);
-                    }
-                }
-                q[2 * i] = s1.x + s1.y;
-                q[2 * i + 1] = s2.x + s2.y;
-            }
-            butterfly_sum<NQ>(q, lane);  // q[0] = warp total of quantity lane / (32/NQ)
-            if constexpr (GW == 1) {
-                if ((lane & (32 / NQ - 1)) == 0) red[((size_t)g * C::kRedSlots + rslot) * NQ + lane / (32 / NQ)] = q[0];
-                __syncwarp();
-            } else {
-                Acc* rb = red + ((size_t)g * C::kRedSlots + rslot) * NQ * GWP;
-                if ((lane & (32 / NQ - 1)) == 0) rb[(lane / (32 / NQ)) * GWP + wig] = q[0];
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&redbar[g * C::kRedSlots + rslot]);
-            }
-        };
-
-        // Pass 2 of a stage (deferred by one stage so the cross-warp wait is
-        // hidden behind the next stage's pass 1): dx, then release the slot.
-        auto pass2 = [&](auto full_tag, int slot, int rslot, uint32_t rph, int64_t r0, int nr) {
-            constexpr bool FULL = decltype(full_tag)::value;
-            Acc tot[NQ];
-            if constexpr (GW == 1) {
-#pragma unroll
-                for (int j = 0; j < NQ; ++j) tot[j] = red[((size_t)g * C::kRedSlots + rslot) * NQ + j];
-            } else {
-                mbar_wait(&redbar[g * C::kRedSlots + rslot], rph);
-                const Acc* rb = red + ((size_t)g * C::kRedSlots + rslot) * NQ * GWP;
-                Acc t = Acc(0);
-                if (lane < NQ * GWP && (lane % GWP) < GW) t = rb[lane];
-#pragma unroll
-                for (int m = GWP / 2; m >= 1; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
-#pragma unroll
-                for (int j = 0; j < NQ; ++j) tot[j] = __shfl_sync(0xffffffffu, t, j * GWP);
-            }
-            const T* sx = ring + (size_t)slot * 2 * R * Dp + (size_t)(g * RPG) * Dp;
-            const T* sdy = sx + (size_t)R * Dp;
-            const Acc* st = stats + ((size_t)slot * R + g * RPG) * 2;
-            if (dxg != nullptr) {
-                T* dxs = dxg + (r0 + g * RPG) * D;  // 64-bit base once per stage
-#pragma unroll
-                for (int i = 0; i < RPG; ++i) {
-                    if (!FULL && g * RPG + i >= nr) continue;
-                    const Acc mu = st[2 * i], rs = st[2 * i + 1];
-                    const P rs2 = PR::splat(rs);
-                    const P k1 = PR::splat(-rs * tot[2 * i] * invD);
-                    const P nc2 = PR::splat(-rs * tot[2 * i + 1] * invD);
-#pragma unroll
-                    for (int k = 0; k < VPT; ++k) {
-                        if (!vok[k]) continue;
-                        P x2[NP], h2[NP], g2[NP], o[NP];
-                        load_row(sx, sdy, i, k, mu, rs, x2, h2, g2);
+                        for (int p = 0; p < NP; ++p) o[p] = PR::fma(nc2, xh[i][k][p], PR::fma(hh[i][k][p], rs2, k1));
+                    } else {
+                        P x2[NP], h2[NP], g2[NP];
+                        make_xh(ux[i][k], ug[i][k], k, mu[i], rs[i], x2, h2, g2);
 #pragma unroll
                         for (int p = 0; p < NP; ++p) o[p] = PR::fma(nc2, x2[p], PR::fma(h2[p], rs2, k1));
-                        T* dst = dxs + (uint32_t)(i * (int)D + vo[k]);
-                        if (a.aligned) {
-                            st_stream(dst, pack2<T>(o));
-                        } else {
-                            const Acc* of = reinterpret_cast<const Acc*>(o);
+                    }
+                    T* dst = dxs + (uint32_t)(i * (int)D + vo[k]);
+                    if (a.aligned) {
+                        st_stream(dst, pack2<T>(o));
+                    } else {
+                        const Acc* of = reinterpret_cast<const Acc*>(o);
 #pragma unroll
-                            for (int e = 0; e < W; ++e)
-                                if (vo[k] + e < D) dst[e] = from_acc<T>(of[e]);
-                        }
+                        for (int e = 0; e < W; ++e)
+                            if (vo[k] + e < D) dst[e] = from_acc<T>(of[e]);
                     }
                 }
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[slot]);  // slot may be refilled now
-        };
-
-        const int64_t n_full = (r_end - r_begin) / R;
-        auto run_pass2 = [&](int64_t it, int slot, int rslot, uint32_t rph) {
-            const int64_t r0 = r_begin + it * R;
-            if (it < n_full)
-                pass2(std::true_type{}, slot, rslot, rph, r0, R);
-            else
-                pass2(std::false_type{}, slot, rslot, rph, r0, (int)(r_end - r0));
-        };
-        int slot = 0, rslot = 0, pslot = 0, prslot = 0;
-        uint32_t ph = 0, rph = 0, prph = 0;
-        for (int64_t it = 0; it < n_stage; ++it) {
-            mbar_wait(&full[slot], ph);
-            const int64_t r0 = r_begin + it * R;
-            if (it < n_full)
-                pass1(std::true_type{}, slot, rslot, r0, R);
-            else
-                pass1(std::false_type{}, slot, rslot, r0, (int)(r_end - r0));
-            if (it > 0) run_pass2(it - 1, pslot, prslot, prph);
-            pslot = slot;
-            prslot = rslot;
-            prph = rph;
-            if (++slot == S) {
-                slot = 0;
-                ph ^= 1u;
-            }
-            if (++rslot == C::kRedSlots) {
-                rslot = 0;
-                rph ^= 1u;
-            }
         }
-        if (n_stage > 0) run_pass2(n_stage - 1, pslot, prslot, prph);
-        flush_to((r_end - 1) / M + 1);
+        if constexpr (!KEEP) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[slot]);
+        }
+    };
+
+    const int64_t n_full = (r_end - r_begin) / R;
+    Acc mu[RPG], rs[RPG], mu_n[RPG], rs_n[RPG];
+    load_stats(0, mu, rs);
+    int slot = 0;
+    uint32_t ph = 0;
+    for (int64_t it = 0; it < n_stage; ++it) {
+        load_stats(it + 1, mu_n, rs_n);
+        if (warp == 0) refill(it);
+        mbar_wait(&full[slot], ph);
+        const int64_t r0 = r_begin + it * R;
+        if (it < n_full)
+            stage(std::true_type{}, slot, r0, R, mu, rs);
+        else
+            stage(std::false_type{}, slot, r0, (int)(r_end - r0), mu, rs);
+#pragma unroll
+        for (int i = 0; i < RPG; ++i) {
+            mu[i] = mu_n[i];
+            rs[i] = rs_n[i];
+        }
+        if (++slot == S) {
+            slot = 0;
+            ph ^= 1u;
+        }
     }
+    flush_to((r_end - 1) / M + 1);
 
     // ------------------------------------------------------------ stage 2 --
     grid_barrier(&a.counters[0]);
 
-    const Acc* partial = static_cast<const Acc*>(a.partial);
+    const Acc* part_r = static_cast<const Acc*>(a.partial);
     Acc* dgam = static_cast<Acc*>(a.dgamma);
     Acc* dbet = static_cast<Acc*>(a.dbeta);
     const int nthreads = blockDim.x;
@@ -421,7 +451,7 @@ __global__ void __launch_bounds__(LnBwdCfg<T, GW, VPT, G, RPG>::kBoundThreads, 1
             double vg = 0.0, vb = 0.0;
             if (cv) {
                 for (int64_t cc = c0; cc <= c1; ++cc) {
-                    const Acc* base = partial + (size_t)(cc + b) * G * 2 * Dp + col;
+                    const Acc* base = part_r + (size_t)(cc + b) * G * 2 * Dp + col;
 #pragma unroll
                     for (int gg = 0; gg < G; ++gg) {
                         vg += (double)__ldcg(base + (size_t)gg * 2 * Dp);

@@ -207,15 +207,14 @@ template <typename T, template <typename, int, int, int, int> class Op, typename
 R dispatch_bwd(int64_t D, const char** why, R bad, A&&... args) {
     constexpr int W = Traits<T>::W;
     const int64_t nv = (D + W - 1) / W;
-    // <= 12 consumer warps (+1 producer) keeps the per-SMSP register cap at
-    // >= 128/thread; the wide-row configs use 8 consumer warps (cap 168).
-    if (nv <= 32) return Op<T, 1, 1, 8, 2>::call(args...);
-    if (nv <= 64) return Op<T, 2, 1, 4, 2>::call(args...);
-    if (nv <= 96) return Op<T, 3, 1, 4, 2>::call(args...);
-    if (nv <= 128) return Op<T, 4, 1, 3, 2>::call(args...);
-    if (nv <= 256) return Op<T, 4, 2, 2, 2>::call(args...);
-    if (nv <= 512) return Op<T, 8, 2, 1, 2>::call(args...);
-    if (nv <= 1024) return Op<T, 8, 4, 1, 1>::call(args...);
+    // 16 warps (15 for D/W <= 96) at <= 128 registers; no producer warp.
+    if (nv <= 32) return Op<T, 1, 1, 16, 1>::call(args...);
+    if (nv <= 64) return Op<T, 2, 1, 8, 1>::call(args...);
+    if (nv <= 96) return Op<T, 3, 1, 5, 2>::call(args...);
+    if (nv <= 128) return Op<T, 4, 1, 4, 2>::call(args...);
+    if (nv <= 256) return Op<T, 8, 1, 2, 2>::call(args...);
+    if (nv <= 512) return Op<T, 8, 2, 2, 1>::call(args...);
+    if (nv <= 1024) return Op<T, 16, 2, 1, 1>::call(args...);
     if (nv <= 2048) return Op<T, 16, 4, 1, 1>::call(args...);
     *why = "layers: trailing extent exceeds the kernel limit (2048 16-byte vectors per row)";
     return bad;
