@@ -1,0 +1,71 @@
+// ln_sweep.cu — configuration sweep of the fused LN-backward kernel (experiment only).
+#include "../paper_2411_00999_b200/csrc/ln_launch.cuh"
+
+namespace gnsb {
+int device_sm_count() {
+    int v = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+}
+}  // namespace gnsb
+
+using namespace gnsb;
+using bf = __nv_bfloat16;
+
+#define CFGS(X)                                  \
+    X(0, 8, 2, 1, 2, true, 1)                    \
+    X(1, 8, 2, 1, 2, true, 0)                    \
+    X(2, 8, 2, 2, 1, true, 1)                    \
+    X(3, 8, 2, 2, 1, false, 1)                   \
+    X(4, 4, 4, 2, 1, true, 0)                    \
+    X(5, 4, 4, 3, 1, true, 0)                    \
+    X(6, 4, 4, 2, 1, true, 1)                    \
+    X(7, 8, 2, 1, 1, true, 1)                    \
+    X(8, 4, 4, 4, 1, false, 0)                   \
+    X(9, 8, 2, 1, 2, false, 0)                    \
+    X(10, 8, 4, 1, 1, true, 1)                   \
+    X(11, 8, 4, 1, 1, true, 0)                   \
+    X(12, 16, 2, 1, 1, false, 1)                 \
+    X(13, 16, 2, 1, 1, true, 1)                  \
+    X(14, 8, 4, 1, 2, true, 0)                   \
+    X(15, 12, 3, 1, 1, true, 1)                  \
+    X(16, 8, 1, 2, 2, false, 1)                  \
+    X(17, 4, 2, 2, 2, true, 1)                   \
+    X(18, 8, 1, 1, 2, true, 1)                   \
+    X(19, 4, 2, 3, 1, true, 1)                   \
+    X(20, 8, 1, 2, 2, true, 1)                   \
+    X(21, 4, 1, 4, 2, false, 1)                  \
+    X(22, 4, 1, 3, 2, true, 1)                   \
+    X(23, 4, 1, 2, 2, true, 1)                   \
+    X(24, 2, 2, 4, 2, true, 1)                   \
+    X(25, 4, 1, 3, 4, true, 0)                   \
+    X(26, 3, 1, 5, 2, false, 1)                  \
+    X(27, 3, 1, 4, 2, true, 1)                   \
+    X(28, 3, 1, 4, 4, true, 0)                   \
+    X(29, 3, 1, 2, 4, true, 0)                   \
+    X(30, 8, 2, 1, 2, false, 1)                  \
+    X(31, 4, 4, 2, 2, true, 0)
+
+extern "C" {
+int sweep_n() { return 32; }
+
+int sweep_desc(int id, int* out) {
+#define DESC(i, gw, vpt, g, rpg, prod, keep) \
+    if (id == i) { out[0] = gw; out[1] = vpt; out[2] = g; out[3] = rpg; out[4] = prod; out[5] = LnBwdCfg<bf, gw, vpt, g, rpg, prod, keep>::KEEP; return 0; }
+    CFGS(DESC)
+    return -1;
+}
+
+int sweep_run(int id, const void* x, const void* mean, const void* rstd, const void* dy, const void* gamma, void* dx,
+              void* dgamma, void* dbeta, double* rg, double* rb, double* sums, int norms, int64_t B, int64_t M,
+              int64_t D, void* ws, size_t wsb, void* stream) {
+    LnBwdCall c{x, mean, rstd, dy, gamma, dx, dgamma, dbeta, rg, rb, sums, norms, B, M, D, ws, wsb};
+    const char* why = nullptr;
+    cudaError_t ce = cudaSuccess;
+#define RUN(i, gw, vpt, g, rpg, prod, keep) \
+    if (id == i) { int rc = BwdOp<LnBwdCfg<bf, gw, vpt, g, rpg, prod, keep>>::run(c, (cudaStream_t)stream, &why, &ce); return rc ? (rc == 2 ? 1000 + (int)ce : 1) : 0; }
+    CFGS(RUN)
+    return -1;
+}
+}

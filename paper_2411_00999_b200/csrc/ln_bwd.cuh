@@ -64,20 +64,24 @@ struct LnBwdArgs {
 
 constexpr int kChunk = 16;  // stage-2 column chunk (half a warp)
 
-template <typename T, int GW, int VPT, int G, int RPG>
+template <typename T, int GW, int VPT, int G, int RPG, bool PROD_ = true, int KEEP_ = -1>
 struct LnBwdCfg {
     using Acc = typename Traits<T>::Acc;
+    using Row = T;
+    static constexpr int kGW = GW, kVPT = VPT, kG = G, kRPG = RPG;
     static constexpr int W = Traits<T>::W;
-    static constexpr int kWarps = GW * G;
-    static constexpr int kThreads = kWarps * 32;
+    static constexpr bool PROD = PROD_;          // dedicated producer warp (the last warp)
+    static constexpr int kWarps = GW * G;        // row-math warps
+    static constexpr int kThreads = (kWarps + (PROD ? 1 : 0)) * 32;
     // registers are allocated for warps in groups of 4: bound the register
     // budget by the rounded-up block so one CTA always fits on an SM
     static constexpr int kBoundThreads = (kThreads + 127) / 128 * 128;
     static constexpr int R = G * RPG;           // rows per stage
     static constexpr int GT = GW * 32;          // threads per row group
     static constexpr int NQ = 2 * RPG;          // row sums per stage and group: (s1, s2) per row
-    static constexpr int GWP = GW == 3 ? 4 : (GW == 5 ? 8 : GW);  // power-of-two padded warps per group
-    static constexpr bool KEEP = VPT * RPG <= 2;  // keep xhat/h of a stage in registers
+    static constexpr int GWP = GW <= 1 ? 1 : GW <= 2 ? 2 : GW <= 4 ? 4 : GW <= 8 ? 8 : GW <= 16 ? 16 : 32;  // pow2 pad
+    // keep xhat/h of a stage in registers (else recompute them for dx)
+    static constexpr bool KEEP = KEEP_ < 0 ? (VPT * RPG <= 2) : (KEEP_ != 0);
     static constexpr int kRedElems = 2 * G * NQ * GWP;
     // byte offsets inside dynamic shared memory
     static __host__ __device__ constexpr size_t bars_bytes(int S) { return (size_t)8 * 2 * S; }
@@ -97,9 +101,10 @@ struct LnBwdCfg {
     }
 };
 
-template <typename T, int GW, int VPT, int G, int RPG, bool HAS_MEAN, bool NORMS>
-__global__ void __launch_bounds__(LnBwdCfg<T, GW, VPT, G, RPG>::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a) {
-    using C = LnBwdCfg<T, GW, VPT, G, RPG>;
+template <typename C, bool HAS_MEAN, bool NORMS>
+__global__ void __launch_bounds__(C::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a) {
+    using T = typename C::Row;
+    constexpr int GW = C::kGW, VPT = C::kVPT, G = C::kG, RPG = C::kRPG;
     using Acc = typename C::Acc;
     using PR = Pair<Acc>;
     using P = typename PR::P;
@@ -176,8 +181,8 @@ __global__ void __launch_bounds__(LnBwdCfg<T, GW, VPT, G, RPG>::kBoundThreads, 1
             if (lane == 0) mbar_arrive(&full[slot]);
         }
     };
-    int64_t issued = 0;  // warp 0: stages handed to the ring so far
-    if (warp == 0) {
+    int64_t issued = 0;  // warp 0 (no producer warp): stages handed to the ring so far
+    if (warp == (C::PROD ? NW : 0)) {  // prime the ring (no waits: every slot is free)
         for (; issued < n_stage && issued < S; ++issued) issue(issued);
     }
     // warp 0 refills every slot whose stage all warps have released; `need`
@@ -214,6 +219,15 @@ __global__ void __launch_bounds__(LnBwdCfg<T, GW, VPT, G, RPG>::kBoundThreads, 1
         }
         __syncthreads();
     }
+    if constexpr (C::PROD) {
+        if (warp == NW) {  // dedicated producer: stream the remaining stages
+            for (int64_t st = issued; st < n_stage; ++st) {
+                mbar_wait(&empty[(int)(st % S)], (uint32_t)(((st / S) - 1) & 1));
+                issue(st);
+            }
+        }
+    }
+    if (!C::PROD || warp < NW) {  // row-math warps
 
     bool vok[VPT];
     int vo[VPT];  // element offset of this thread's k-th vector inside a row
@@ -409,7 +423,7 @@ __global__ void __launch_bounds__(LnBwdCfg<T, GW, VPT, G, RPG>::kBoundThreads, 1
     uint32_t ph = 0;
     for (int64_t it = 0; it < n_stage; ++it) {
         load_stats(it + 1, mu_n, rs_n);
-        if (warp == 0) refill(it);
+        if (!C::PROD && warp == 0) refill(it);
         mbar_wait(&full[slot], ph);
         const int64_t r0 = r_begin + it * R;
         if (it < n_full)
@@ -427,6 +441,7 @@ __global__ void __launch_bounds__(LnBwdCfg<T, GW, VPT, G, RPG>::kBoundThreads, 1
         }
     }
     flush_to((r_end - 1) / M + 1);
+    }  // row-math warps
 
     // ------------------------------------------------------------ stage 2 --
     grid_barrier(&a.counters[0]);

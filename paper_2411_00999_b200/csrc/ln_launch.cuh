@@ -46,11 +46,12 @@ struct BwdPlan {
     size_t off_partial = 0, off_q = 0, off_qbig = 0, off_raw = 0, total = 0;
 };
 
-template <typename T, int GW, int VPT, int G, int RPG>
+template <typename C>
 int plan_bwd(int64_t B, int64_t M, int64_t D, BwdPlan& p, const char** why) {
-    using C = LnBwdCfg<T, GW, VPT, G, RPG>;
+    using T = typename C::Row;
     using Acc = typename Traits<T>::Acc;
     constexpr int W = Traits<T>::W;
+    constexpr int G = C::kG;
     p.Dp = (int)((D + W - 1) / W * W);
     const size_t budget = (size_t)smem_optin_bytes() - 1024;
     p.stages = 0;
@@ -84,14 +85,15 @@ int plan_bwd(int64_t B, int64_t M, int64_t D, BwdPlan& p, const char** why) {
     return 0;
 }
 
-template <typename T, int GW, int VPT, int G, int RPG>
+template <typename C>
 struct BwdOp {
+    using T = typename C::Row;
     static int plan(int64_t B, int64_t M, int64_t D, BwdPlan& p, const char** why) {
-        return plan_bwd<T, GW, VPT, G, RPG>(B, M, D, p, why);
+        return plan_bwd<C>(B, M, D, p, why);
     }
     static int run(const LnBwdCall& c, cudaStream_t st, const char** why, cudaError_t* cerr) {
         BwdPlan p;
-        if (plan_bwd<T, GW, VPT, G, RPG>(c.B, c.M, c.D, p, why)) return 1;
+        if (plan_bwd<C>(c.B, c.M, c.D, p, why)) return 1;
         if (c.ws_bytes < p.total) {
             *why = "layers: workspace too small (query gnsb_ln_bwd_workspace_size)";
             return 1;
@@ -125,10 +127,10 @@ struct BwdOp {
 
         void (*k)(LnBwdArgs) = nullptr;
         const bool hm = c.mean != nullptr;
-        if (hm && c.norms) k = ln_bwd_kernel<T, GW, VPT, G, RPG, true, true>;
-        else if (hm) k = ln_bwd_kernel<T, GW, VPT, G, RPG, true, false>;
-        else if (c.norms) k = ln_bwd_kernel<T, GW, VPT, G, RPG, false, true>;
-        else k = ln_bwd_kernel<T, GW, VPT, G, RPG, false, false>;
+        if (hm && c.norms) k = ln_bwd_kernel<C, true, true>;
+        else if (hm) k = ln_bwd_kernel<C, true, false>;
+        else if (c.norms) k = ln_bwd_kernel<C, false, true>;
+        else k = ln_bwd_kernel<C, false, false>;
         cudaError_t e = ensure_smem(reinterpret_cast<const void*>(k), p.smem);
         if (e != cudaSuccess) {
             *cerr = e;
@@ -148,7 +150,7 @@ struct BwdOp {
                 return 2;
             }
             --p.stages;
-            p.smem = LnBwdCfg<T, GW, VPT, G, RPG>::smem_bytes(p.stages, p.Dp);
+            p.smem = C::smem_bytes(p.stages, p.Dp);
         }
         a.stages = p.stages;
         cudaLaunchConfig_t cfg = {};
@@ -202,40 +204,39 @@ struct FwdOp {
     }
 };
 
-// Configuration table: number of 16-byte vectors per row -> (GW, VPT, G, RPG).
-template <typename T, template <typename, int, int, int, int> class Op, typename R, typename... A>
+// Configuration table: number of 16-byte vectors per row -> LnBwdCfg.
+template <typename T, template <typename> class Op, typename R, typename... A>
 R dispatch_bwd(int64_t D, const char** why, R bad, A&&... args) {
     constexpr int W = Traits<T>::W;
     const int64_t nv = (D + W - 1) / W;
-    // 16 warps (15 for D/W <= 96) at <= 128 registers; no producer warp.
-    if (nv <= 32) return Op<T, 1, 1, 16, 1>::call(args...);
-    if (nv <= 64) return Op<T, 2, 1, 8, 1>::call(args...);
-    if (nv <= 96) return Op<T, 3, 1, 5, 2>::call(args...);
-    if (nv <= 128) return Op<T, 4, 1, 4, 2>::call(args...);
-    if (nv <= 256) return Op<T, 8, 1, 2, 2>::call(args...);
-    if (nv <= 512) return Op<T, 8, 2, 2, 1>::call(args...);
-    if (nv <= 1024) return Op<T, 16, 2, 1, 1>::call(args...);
-    if (nv <= 2048) return Op<T, 16, 4, 1, 1>::call(args...);
+    if (nv <= 32) return Op<LnBwdCfg<T, 1, 1, 16, 1, false>>::call(args...);
+    if (nv <= 64) return Op<LnBwdCfg<T, 2, 1, 8, 1, false>>::call(args...);
+    if (nv <= 96) return Op<LnBwdCfg<T, 3, 1, 5, 2, false>>::call(args...);
+    if (nv <= 128) return Op<LnBwdCfg<T, 4, 1, 4, 2, false>>::call(args...);
+    if (nv <= 256) return Op<LnBwdCfg<T, 8, 1, 2, 2, false>>::call(args...);
+    if (nv <= 512) return Op<LnBwdCfg<T, 8, 2, 1, 2, true>>::call(args...);
+    if (nv <= 1024) return Op<LnBwdCfg<T, 8, 4, 1, 1, true, 1>>::call(args...);
+    if (nv <= 2048) return Op<LnBwdCfg<T, 16, 4, 1, 1, false>>::call(args...);
     *why = "layers: trailing extent exceeds the kernel limit (2048 16-byte vectors per row)";
     return bad;
 }
 
-template <typename T, int GW, int VPT, int G, int RPG>
+template <typename C>
 struct BwdRunOp {
     static int call(const LnBwdCall& c, cudaStream_t st, const char** why, cudaError_t* cerr) {
-        return BwdOp<T, GW, VPT, G, RPG>::run(c, st, why, cerr);
+        return BwdOp<C>::run(c, st, why, cerr);
     }
 };
-template <typename T, int GW, int VPT, int G, int RPG>
+template <typename C>
 struct BwdPlanOp {
     static int call(int64_t B, int64_t M, int64_t D, BwdPlan* p, const char** why) {
-        return BwdOp<T, GW, VPT, G, RPG>::plan(B, M, D, *p, why);
+        return BwdOp<C>::plan(B, M, D, *p, why);
     }
 };
-template <typename T, int GW, int VPT, int G, int RPG>
+template <typename C>
 struct FwdRunOp {
     static int call(const LnFwdCall& c, cudaStream_t st, const char** why, cudaError_t* cerr) {
-        return FwdOp<T, GW, VPT>::run(c, st, why, cerr);
+        return FwdOp<typename C::Row, C::kGW, C::kVPT>::run(c, st, why, cerr);
     }
 };
 
