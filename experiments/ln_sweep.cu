@@ -15,40 +15,28 @@ using bf = __nv_bfloat16;
 
 #define CFGS(X)                                  \
     X(0, 8, 2, 1, 2, true, 1)                    \
-    X(1, 8, 2, 1, 2, true, 0)                    \
-    X(2, 8, 2, 2, 1, true, 1)                    \
-    X(3, 8, 2, 2, 1, false, 1)                   \
-    X(4, 4, 4, 2, 1, true, 0)                    \
-    X(5, 4, 4, 3, 1, true, 0)                    \
-    X(6, 4, 4, 2, 1, true, 1)                    \
-    X(7, 8, 2, 1, 1, true, 1)                    \
-    X(8, 4, 4, 4, 1, false, 0)                   \
-    X(9, 8, 2, 1, 2, false, 0)                    \
-    X(10, 8, 4, 1, 1, true, 1)                   \
-    X(11, 8, 4, 1, 1, true, 0)                   \
-    X(12, 16, 2, 1, 1, false, 1)                 \
-    X(13, 16, 2, 1, 1, true, 1)                  \
-    X(14, 8, 4, 1, 2, true, 0)                   \
-    X(15, 12, 3, 1, 1, true, 1)                  \
-    X(16, 8, 1, 2, 2, false, 1)                  \
-    X(17, 4, 2, 2, 2, true, 1)                   \
-    X(18, 8, 1, 1, 2, true, 1)                   \
-    X(19, 4, 2, 3, 1, true, 1)                   \
-    X(20, 8, 1, 2, 2, true, 1)                   \
-    X(21, 4, 1, 4, 2, false, 1)                  \
-    X(22, 4, 1, 3, 2, true, 1)                   \
-    X(23, 4, 1, 2, 2, true, 1)                   \
-    X(24, 2, 2, 4, 2, true, 1)                   \
-    X(25, 4, 1, 3, 4, true, 0)                   \
-    X(26, 3, 1, 5, 2, false, 1)                  \
-    X(27, 3, 1, 4, 2, true, 1)                   \
-    X(28, 3, 1, 4, 4, true, 0)                   \
-    X(29, 3, 1, 2, 4, true, 0)                   \
-    X(30, 8, 2, 1, 2, false, 1)                  \
-    X(31, 4, 4, 2, 2, true, 0)
+    X(1, 4, 4, 2, 1, true, 1)                    \
+    X(2, 2, 8, 4, 1, true, 0)                    \
+    X(3, 8, 4, 1, 1, true, 1)                    \
+    X(4, 16, 2, 1, 1, true, 1)                   \
+    X(5, 4, 2, 3, 1, true, 1)                    \
+    X(6, 2, 4, 4, 1, true, 0)                    \
+    X(7, 2, 4, 6, 1, true, 0)                    \
+    X(8, 4, 1, 3, 2, true, 1)                    \
+    X(9, 1, 4, 8, 1, true, 0)                    \
+    X(10, 1, 4, 8, 1, true, 1)                   \
+    X(11, 1, 4, 12, 1, true, 0)                  \
+    X(12, 2, 2, 4, 2, true, 1)                   \
+    X(13, 2, 2, 6, 1, true, 1)                   \
+    X(14, 3, 1, 4, 2, true, 1)                   \
+    X(15, 1, 3, 8, 1, true, 1)                   \
+    X(16, 1, 3, 12, 1, true, 1)                  \
+    X(17, 1, 3, 8, 2, true, 0)                   \
+    X(18, 1, 3, 12, 1, true, 0)                  \
+    X(19, 2, 2, 6, 2, true, 1)
 
 extern "C" {
-int sweep_n() { return 32; }
+int sweep_n() { return 20; }
 
 int sweep_desc(int id, int* out) {
 #define DESC(i, gw, vpt, g, rpg, prod, keep) \

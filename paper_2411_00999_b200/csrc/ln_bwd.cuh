@@ -443,6 +443,26 @@ __global__ void __launch_bounds__(C::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a
     flush_to((r_end - 1) / M + 1);
     }  // row-math warps
 
+    if constexpr (G > 1) {
+        // CTA-local pre-combine: fold the G group partials of every example this
+        // CTA touched into group 0's slot (fixed order g = 0..G-1), so stage 2
+        // reads one slot per (cta, example)
+        __syncthreads();
+        const int64_t e0 = r_begin / M, e1 = (r_end - 1) / M;
+        for (int64_t ex = e0; ex <= e1; ++ex) {
+            Acc* base = static_cast<Acc*>(a.partial) + (size_t)(cta + ex) * G * 2 * Dp;
+            for (int i = threadIdx.x; i < 2 * Dp; i += blockDim.x) {
+                Acc v[G];
+#pragma unroll
+                for (int gg = 0; gg < G; ++gg) v[gg] = base[(size_t)gg * 2 * Dp + i];
+                Acc t = v[0];
+#pragma unroll
+                for (int gg = 1; gg < G; ++gg) t += v[gg];
+                base[i] = t;
+            }
+        }
+    }
+
     // ------------------------------------------------------------ stage 2 --
     grid_barrier(&a.counters[0]);
 
@@ -465,12 +485,21 @@ __global__ void __launch_bounds__(C::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a
             const int64_t c0 = cta_of(b * M), c1 = cta_of((b + 1) * M - 1);
             double vg = 0.0, vb = 0.0;
             if (cv) {
-                for (int64_t cc = c0; cc <= c1; ++cc) {
-                    const Acc* base = part_r + (size_t)(cc + b) * G * 2 * Dp + col;
+                // one (pre-combined) slot per CTA that touched example b; issue
+                // four CTAs' loads at a time, then add in fixed CTA order
+                for (int64_t cc = c0; cc <= c1; cc += 4) {
+                    Acc lg[4], lb[4];
 #pragma unroll
-                    for (int gg = 0; gg < G; ++gg) {
-                        vg += (double)__ldcg(base + (size_t)gg * 2 * Dp);
-                        vb += (double)__ldcg(base + (size_t)gg * 2 * Dp + Dp);
+                    for (int u = 0; u < 4; ++u) {
+                        const bool ok = cc + u <= c1;
+                        const Acc* base = part_r + (size_t)(ok ? cc + u + b : 0) * G * 2 * Dp + col;
+                        lg[u] = ok ? __ldcg(base) : Acc(0);
+                        lb[u] = ok ? __ldcg(base + Dp) : Acc(0);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        vg += (double)lg[u];
+                        vb += (double)lb[u];
                     }
                 }
             }
