@@ -14,7 +14,7 @@
 //     (cp.async.bulk, L2 evict_first) completing on mbarriers.  There is no
 //     dedicated producer warp: lane 0 of warp 0 refills a slot as soon as
 //     every warp released it, so all 16 warps do row math;
-//   * mean/rstd are read straight from global memory one stage ahead;
+//   * mean/rstd ride along with each stage (producer lanes, S stages ahead);
 //   * warps form G row groups of GW warps; a thread owns VPT 16-byte column
 //     vectors for the whole kernel, so the per-example dgamma/dbeta partials
 //     accumulate over the sequence axis in registers (packed fp32x2 math:
@@ -86,8 +86,11 @@ struct LnBwdCfg {
     // byte offsets inside dynamic shared memory
     static __host__ __device__ constexpr size_t bars_bytes(int S) { return (size_t)8 * 2 * S; }
     static __host__ __device__ constexpr size_t red_off(int S) { return (bars_bytes(S) + 15) / 16 * 16; }
-    static __host__ __device__ constexpr size_t gam_off(int S) {
+    static __host__ __device__ constexpr size_t stats_off(int S) {
         return red_off(S) + ((size_t)kRedElems * sizeof(Acc) + 15) / 16 * 16;
+    }
+    static __host__ __device__ constexpr size_t gam_off(int S) {
+        return (stats_off(S) + (size_t)S * R * 2 * sizeof(Acc) + 15) / 16 * 16;
     }
     static __host__ __device__ constexpr size_t rows_off(int S, int Dp) {
         return (gam_off(S) + (size_t)Dp * sizeof(Acc) + 127) / 128 * 128;
@@ -123,6 +126,7 @@ __global__ void __launch_bounds__(C::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + S;
     Acc* red = reinterpret_cast<Acc*>(smem + C::red_off(S));
+    Acc* stats = reinterpret_cast<Acc*>(smem + C::stats_off(S));  // [S][R][mean, rstd]
     Acc* gam_s = reinterpret_cast<Acc*>(smem + C::gam_off(S));
     T* ring = reinterpret_cast<T*>(smem + C::rows_off(S, a.Dp));
 
@@ -168,7 +172,6 @@ __global__ void __launch_bounds__(C::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a
                 mbar_expect_tx(&full[slot], 2 * bytes);
                 bulk_g2s(sx, xg + r0 * D, bytes, &full[slot], pol);
                 bulk_g2s(sdy, dyg + r0 * D, bytes, &full[slot], pol);
-                mbar_arrive(&full[slot]);
             }
         } else {
             const int64_t ne = (int64_t)nr * D;
@@ -177,9 +180,15 @@ __global__ void __launch_bounds__(C::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a
                 sx[rr * Dp + cc] = xg[r0 * D + e];
                 sdy[rr * Dp + cc] = dyg[r0 * D + e];
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&full[slot]);
         }
+        // per-row mean/rstd ride along with the stage (loaded S stages ahead)
+        Acc* sst = stats + (size_t)slot * R * 2;
+        for (int j = lane; j < nr; j += 32) {
+            sst[2 * j] = HAS_MEAN ? __ldg(meang + r0 + j) : Acc(0);
+            sst[2 * j + 1] = __ldg(rstdg + r0 + j);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[slot]);
     };
     int64_t issued = 0;  // warp 0 (no producer warp): stages handed to the ring so far
     if (warp == (C::PROD ? NW : 0)) {  // prime the ring (no waits: every slot is free)
@@ -271,17 +280,6 @@ __global__ void __launch_bounds__(C::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a
         next_bound = (cur_ex + 1) * M;
     };
 
-    // per-row statistics of this group's rows, prefetched one stage ahead
-    auto load_stats = [&](int64_t st, Acc* mu, Acc* rs) {
-#pragma unroll
-        for (int i = 0; i < RPG; ++i) {
-            int64_t row = r_begin + st * R + g * RPG + i;
-            if (row >= r_end || st >= n_stage) row = r_begin;  // clamp (value unused)
-            mu[i] = HAS_MEAN ? __ldg(meang + row) : Acc(0);
-            rs[i] = __ldg(rstdg + row);
-        }
-    };
-
     // xhat and h = gamma*g of a staged vector
     auto make_xh = [&](const uint4& ux, const uint4& ug, int k, Acc mu, Acc rs, P* x2, P* h2, P* g2) {
         P xf[NP];
@@ -298,10 +296,18 @@ __global__ void __launch_bounds__(C::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a
 
     // One stage.  FULL: every row of the stage is valid (all but the last).
     int rbuf = 0;
-    auto stage = [&](auto full_tag, int slot, int64_t r0, int nr, const Acc* mu, const Acc* rs) {
+    auto stage = [&](auto full_tag, int slot, int64_t r0, int nr) {
         constexpr bool FULL = decltype(full_tag)::value;
         const T* sx = ring + (size_t)slot * 2 * R * Dp + (size_t)(g * RPG) * Dp;
         const T* sdy = sx + (size_t)R * Dp;
+        const Acc* stp = stats + ((size_t)slot * R + g * RPG) * 2;
+        Acc mu[RPG], rs[RPG];
+#pragma unroll
+        for (int i = 0; i < RPG; ++i) {
+            const bool valid = FULL || g * RPG + i < nr;
+            mu[i] = valid ? stp[2 * i] : Acc(0);
+            rs[i] = valid ? stp[2 * i + 1] : Acc(0);
+        }
 
         uint4 ux[RPG][VPT], ug[RPG][VPT];
 #pragma unroll
@@ -417,24 +423,16 @@ __global__ void __launch_bounds__(C::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a
     };
 
     const int64_t n_full = (r_end - r_begin) / R;
-    Acc mu[RPG], rs[RPG], mu_n[RPG], rs_n[RPG];
-    load_stats(0, mu, rs);
     int slot = 0;
     uint32_t ph = 0;
     for (int64_t it = 0; it < n_stage; ++it) {
-        load_stats(it + 1, mu_n, rs_n);
         if (!C::PROD && warp == 0) refill(it);
         mbar_wait(&full[slot], ph);
         const int64_t r0 = r_begin + it * R;
         if (it < n_full)
-            stage(std::true_type{}, slot, r0, R, mu, rs);
+            stage(std::true_type{}, slot, r0, R);
         else
-            stage(std::false_type{}, slot, r0, (int)(r_end - r0), mu, rs);
-#pragma unroll
-        for (int i = 0; i < RPG; ++i) {
-            mu[i] = mu_n[i];
-            rs[i] = rs_n[i];
-        }
+            stage(std::false_type{}, slot, r0, (int)(r_end - r0));
         if (++slot == S) {
             slot = 0;
             ph ^= 1u;
