@@ -13,30 +13,32 @@ int device_sm_count() {
 using namespace gnsb;
 using bf = __nv_bfloat16;
 
-#define CFGS(X)                                  \
-    X(0, 8, 2, 1, 2, true, 1)                    \
-    X(1, 4, 4, 2, 1, true, 1)                    \
-    X(2, 2, 8, 4, 1, true, 0)                    \
-    X(3, 8, 4, 1, 1, true, 1)                    \
-    X(4, 16, 2, 1, 1, true, 1)                   \
-    X(5, 4, 2, 3, 1, true, 1)                    \
-    X(6, 2, 4, 4, 1, true, 0)                    \
-    X(7, 2, 4, 6, 1, true, 0)                    \
-    X(8, 4, 1, 3, 2, true, 1)                    \
-    X(9, 1, 4, 8, 1, true, 0)                    \
-    X(10, 1, 4, 8, 1, true, 1)                   \
-    X(11, 1, 4, 12, 1, true, 0)                  \
-    X(12, 2, 2, 4, 2, true, 1)                   \
-    X(13, 2, 2, 6, 1, true, 1)                   \
-    X(14, 3, 1, 4, 2, true, 1)                   \
-    X(15, 1, 3, 8, 1, true, 1)                   \
-    X(16, 1, 3, 12, 1, true, 1)                  \
-    X(17, 1, 3, 8, 2, true, 0)                   \
-    X(18, 1, 3, 12, 1, true, 0)                  \
-    X(19, 2, 2, 6, 2, true, 1)
+#define CFGS(X) \
+    X(0, 8, 2, 1, 2, true, 1) \
+    X(1, 16, 1, 1, 2, true, 1) \
+    X(2, 16, 1, 1, 1, true, 1) \
+    X(3, 8, 2, 2, 1, true, 1) \
+    X(4, 16, 2, 1, 1, true, 1) \
+    X(5, 16, 4, 1, 1, true, 0) \
+    X(6, 8, 1, 2, 2, true, 1) \
+    X(7, 4, 1, 4, 2, true, 1) \
+    X(8, 8, 1, 2, 1, true, 1) \
+    X(9, 4, 2, 3, 1, true, 1) \
+    X(10, 4, 1, 4, 4, true, 1) \
+    X(11, 2, 2, 8, 1, true, 1) \
+    X(12, 4, 1, 4, 1, true, 1) \
+    X(13, 4, 1, 3, 2, true, 1) \
+    X(14, 2, 1, 8, 2, true, 1) \
+    X(15, 3, 1, 5, 2, true, 1) \
+    X(16, 3, 1, 5, 1, true, 1) \
+    X(17, 2, 2, 8, 1, true, 1) \
+    X(18, 3, 1, 4, 2, true, 1) \
+    X(19, 3, 1, 5, 4, true, 1) \
+    X(20, 1, 3, 16, 1, true, 1) \
+    X(21, 2, 2, 6, 1, true, 1) \
 
 extern "C" {
-int sweep_n() { return 20; }
+int sweep_n() { return 22; }
 
 int sweep_desc(int id, int* out) {
 #define DESC(i, gw, vpt, g, rpg, prod, keep) \

@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(C::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a
     constexpr int NQ = C::NQ;
     constexpr int GWP = C::GWP;
     constexpr bool KEEP = C::KEEP;
-    static_assert(NQ * GWP <= 32, "cross-warp reduction layout");
+    static_assert((NQ & (NQ - 1)) == 0 && NQ <= 32, "rows per group per stage must be a power of two");
 
     extern __shared__ __align__(128) unsigned char smem[];
     const int S = a.stages;
@@ -374,12 +374,21 @@ __global__ void __launch_bounds__(C::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a
             Acc* rb = red + (size_t)(rbuf * G + g) * NQ * GWP;
             if ((lane & (32 / NQ - 1)) == 0) rb[(lane / (32 / NQ)) * GWP + wig] = q[0];
             named_bar_sync(1 + g, GT);
-            Acc t = Acc(0);
-            if (lane < NQ * GWP && (lane % GWP) < GW) t = rb[lane];
+            // rb is [NQ][GWP]; each lane folds E entries over the GWP-lane groups
+            constexpr int TOT = NQ * GWP;
+            constexpr int E = TOT > 32 ? TOT / 32 : 1;
+            Acc t[E];
 #pragma unroll
-            for (int m = GWP / 2; m >= 1; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
+            for (int e = 0; e < E; ++e) {
+                const int idx = lane + 32 * e;
+                t[e] = (idx < TOT && (idx % GWP) < GW) ? rb[idx] : Acc(0);
+            }
 #pragma unroll
-            for (int j = 0; j < NQ; ++j) tot[j] = __shfl_sync(0xffffffffu, t, j * GWP);
+            for (int m = GWP / 2; m >= 1; m >>= 1)
+#pragma unroll
+                for (int e = 0; e < E; ++e) t[e] += __shfl_xor_sync(0xffffffffu, t[e], m);
+#pragma unroll
+            for (int j = 0; j < NQ; ++j) tot[j] = __shfl_sync(0xffffffffu, t[(j * GWP) / 32], (j * GWP) % 32);
             rbuf ^= 1;
         }
         // pass 2: dx = rstd*(h - mean(h)) - rstd*mean(h*xhat)*xhat
