@@ -10,6 +10,9 @@ sys.path.insert(0, ROOT)
 import paper_2411_00999_b200 as m  # noqa: E402
 
 lib = ctypes.CDLL(os.path.join(ROOT, "experiments", "libln_sweep.so"))
+_vp, _i64 = ctypes.c_void_p, ctypes.c_int64
+lib.sweep_run.argtypes = [ctypes.c_int] + [_vp] * 11 + [ctypes.c_int, _i64, _i64, _i64, _vp, ctypes.c_size_t, _vp]
+lib.sweep_run.restype = ctypes.c_int
 dev = torch.device("cuda")
 B, T = 32, 1024
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
