@@ -14,7 +14,7 @@ _vp, _i64 = ctypes.c_void_p, ctypes.c_int64
 lib.sweep_run.argtypes = [ctypes.c_int] + [_vp] * 11 + [ctypes.c_int, _i64, _i64, _i64, _vp, ctypes.c_size_t, _vp]
 lib.sweep_run.restype = ctypes.c_int
 dev = torch.device("cuda")
-B, T = 32, 1024
+B, T = int(os.environ.get('SWEEP_B', '32')), 1024
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 Ds = [int(v) for v in sys.argv[1].split(",")] if len(sys.argv) > 1 else [768, 1024, 2048, 4096, 8192]
 ids = [int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else list(range(lib.sweep_n()))

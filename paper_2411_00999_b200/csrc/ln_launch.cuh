@@ -212,12 +212,12 @@ R dispatch_bwd(int64_t D, const char** why, R bad, A&&... args) {
     // measured on B200 (experiments/ln_sweep.py): a dedicated producer warp
     // and xhat/h kept in registers win at every width
     if (nv <= 32) return Op<LnBwdCfg<T, 1, 1, 8, 2, true>>::call(args...);
-    if (nv <= 64) return Op<LnBwdCfg<T, 2, 1, 4, 2, true>>::call(args...);
-    if (nv <= 96) return Op<LnBwdCfg<T, 3, 1, 4, 2, true>>::call(args...);
-    if (nv <= 128) return Op<LnBwdCfg<T, 4, 1, 3, 2, true>>::call(args...);
+    if (nv <= 64) return Op<LnBwdCfg<T, 2, 1, 8, 1, true>>::call(args...);
+    if (nv <= 96) return Op<LnBwdCfg<T, 3, 1, 5, 2, true>>::call(args...);
+    if (nv <= 128) return Op<LnBwdCfg<T, 4, 1, 4, 2, true>>::call(args...);
     if (nv <= 256) return Op<LnBwdCfg<T, 4, 2, 3, 1, true>>::call(args...);
     if (nv <= 512) return Op<LnBwdCfg<T, 8, 2, 1, 2, true, 1>>::call(args...);
-    if (nv <= 1024) return Op<LnBwdCfg<T, 8, 4, 1, 1, true, 1>>::call(args...);
+    if (nv <= 1024) return Op<LnBwdCfg<T, 16, 2, 1, 1, true, 1>>::call(args...);
     if (nv <= 2048) return Op<LnBwdCfg<T, 16, 4, 1, 1, false>>::call(args...);
     *why = "layers: trailing extent exceeds the kernel limit (2048 16-byte vectors per row)";
     return bad;
