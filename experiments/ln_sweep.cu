@@ -49,8 +49,8 @@ int sweep_desc(int id, int* out) {
 
 int sweep_run(int id, const void* x, const void* mean, const void* rstd, const void* dy, const void* gamma, void* dx,
               void* dgamma, void* dbeta, double* rg, double* rb, double* sums, int norms, int64_t B, int64_t M,
-              int64_t D, void* ws, size_t wsb, void* stream) {
-    LnBwdCall c{x, mean, rstd, dy, gamma, dx, dgamma, dbeta, rg, rb, sums, norms, B, M, D, ws, wsb};
+              int64_t D, void* ws, size_t wsb, void* stream, unsigned long long* trace) {
+    LnBwdCall c{x, mean, rstd, dy, gamma, dx, dgamma, dbeta, rg, rb, sums, norms, B, M, D, ws, wsb, trace};
     const char* why = nullptr;
     cudaError_t ce = cudaSuccess;
 #define RUN(i, gw, vpt, g, rpg, prod, keep) \

@@ -11,11 +11,13 @@ import paper_2411_00999_b200 as m  # noqa: E402
 
 lib = ctypes.CDLL(os.path.join(ROOT, "experiments", "libln_sweep.so"))
 _vp, _i64 = ctypes.c_void_p, ctypes.c_int64
-lib.sweep_run.argtypes = [ctypes.c_int] + [_vp] * 11 + [ctypes.c_int, _i64, _i64, _i64, _vp, ctypes.c_size_t, _vp]
+lib.sweep_run.argtypes = [ctypes.c_int] + [_vp] * 11 + [ctypes.c_int, _i64, _i64, _i64, _vp, ctypes.c_size_t, _vp, _vp]
 lib.sweep_run.restype = ctypes.c_int
 dev = torch.device("cuda")
 B, T = int(os.environ.get('SWEEP_B', '32')), 1024
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+TRACE = os.environ.get("SWEEP_TRACE") == "1"
+trace = torch.zeros(148 * 6, dtype=torch.int64, device=dev)
 Ds = [int(v) for v in sys.argv[1].split(",")] if len(sys.argv) > 1 else [768, 1024, 2048, 4096, 8192]
 ids = [int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else list(range(lib.sweep_n()))
 for D in Ds:
@@ -49,7 +51,8 @@ for D in Ds:
                                    ctypes.c_void_p(dg.data_ptr()), ctypes.c_void_p(db.data_ptr()),
                                    ctypes.c_void_p(rg.data_ptr()), ctypes.c_void_p(rb.data_ptr()),
                                    ctypes.c_void_p(sums.data_ptr()), norms, B, T, D, ctypes.c_void_p(ws.data_ptr()),
-                                   ctypes.c_size_t(ws.numel()), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+                                   ctypes.c_size_t(ws.numel()), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream),
+                                   ctypes.c_void_p(trace.data_ptr() if TRACE else 0))
                 e1.record()
                 if rc:
                     break
@@ -62,6 +65,14 @@ for D in Ds:
             ts.sort()
             res[norms] = ts[len(ts) // 2]
         ok = ""
+        if TRACE:
+            tr = trace.view(-1, 6).cpu().numpy().astype("int64")
+            t0 = tr[:, 0].min()
+            rel = (tr - t0) / 1000.0
+            last = rel[:, 5].max()
+            print(f"   trace(us): start max {rel[:,0].max():.1f} | rowmath end min {rel[:,1].min():.1f} med {sorted(rel[:,1])[74]:.1f} max {rel[:,1].max():.1f}"
+                  f" | precombine end max {rel[:,2].max():.1f} | barrier out min {rel[:,3].min():.1f} max {rel[:,3].max():.1f}"
+                  f" | stage2 end max {rel[:,4].max():.1f} | final end {last:.1f}")
         if not isinstance(res.get(1), str):
             err = (dx.float() - ref.input_grad.float()).abs().max().item()
             nerr = ((rg - ref.grads.per_example_sqnorms_raw["gamma"]).abs() / ref.grads.per_example_sqnorms_raw["gamma"]).max().item()

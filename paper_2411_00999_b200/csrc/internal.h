@@ -30,6 +30,7 @@ struct LnBwdCall {
     int norms;
     int64_t B, M, D;
     void* ws; size_t ws_bytes;
+    unsigned long long* trace = nullptr;  // profiling only: [grid][6] phase stamps
 };
 
 // Returns 0 ok, 1 invalid (message in *why), 2 CUDA error (cudaError_t in *cerr).

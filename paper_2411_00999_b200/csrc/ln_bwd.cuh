@@ -60,6 +60,7 @@ struct LnBwdArgs {
     double* rawws;      // [B][2]
     unsigned* counters; // [2] grid barrier, final ticket (zero on entry, zero on exit)
     int nchunks;
+    unsigned long long* trace;  // optional [grid][6] globaltimer stamps (profiling only)
 };
 
 constexpr int kChunk = 16;  // stage-2 column chunk (half a warp)
@@ -142,6 +143,10 @@ __global__ void __launch_bounds__(C::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a
     const Acc* meang = static_cast<const Acc*>(a.mean);
     const Acc* rstdg = static_cast<const Acc*>(a.rstd);
 
+    auto stamp = [&](int k) {
+        if (a.trace != nullptr && threadIdx.x == 0) a.trace[(size_t)cta * 6 + k] = globaltimer_ns();
+    };
+    stamp(0);
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
@@ -450,6 +455,7 @@ __global__ void __launch_bounds__(C::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a
     flush_to((r_end - 1) / M + 1);
     }  // row-math warps
 
+    stamp(1);
     if constexpr (G > 1) {
         // CTA-local pre-combine: fold the G group partials of every example this
         // CTA touched into group 0's slot (fixed order g = 0..G-1), so stage 2
@@ -471,7 +477,9 @@ __global__ void __launch_bounds__(C::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a
     }
 
     // ------------------------------------------------------------ stage 2 --
+    stamp(2);
     grid_barrier(&a.counters[0]);
+    stamp(3);
 
     const Acc* part_r = static_cast<const Acc*>(a.partial);
     Acc* dgam = static_cast<Acc*>(a.dgamma);
@@ -558,6 +566,7 @@ __global__ void __launch_bounds__(C::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a
     // ------------------------------------------------------- final ticket --
     __shared__ unsigned s_last;
     __syncthreads();
+    stamp(4);
     if (threadIdx.x == 0) {
         __threadfence();
         const unsigned t = atomicAdd(&a.counters[1], 1u);
@@ -611,6 +620,7 @@ __global__ void __launch_bounds__(C::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a
         a.counters[1] = 0u;
         __threadfence();
     }
+    stamp(5);
 }
 
 }  // namespace gnsb

@@ -124,6 +124,7 @@ struct BwdOp {
         a.qbig = reinterpret_cast<double*>(ws + p.off_qbig);
         a.rawws = reinterpret_cast<double*>(ws + p.off_raw);
         a.nchunks = p.nchunks;
+        a.trace = c.trace;
 
         void (*k)(LnBwdArgs) = nullptr;
         const bool hm = c.mean != nullptr;
