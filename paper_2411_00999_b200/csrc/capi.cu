@@ -3,6 +3,7 @@
 // do not deserve their own file (squared norm, GNS accumulator).
 #include <math_constants.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -26,12 +27,15 @@ gnsb_status cuda_fail(cudaError_t e, const char* where) {
 }
 
 gnsb_status need_device() {
+    static std::atomic<bool> seen{false};  // a device, once found, stays
+    if (seen.load(std::memory_order_relaxed)) return GNSB_OK;
     int n = 0;
     const cudaError_t e = cudaGetDeviceCount(&n);
     if (e != cudaSuccess || n == 0) {
         g_err = "cuda: no CUDA device available (the B200 path has no CPU fallback)";
         return GNSB_ECUDA;
     }
+    seen.store(true, std::memory_order_relaxed);
     return GNSB_OK;
 }
 

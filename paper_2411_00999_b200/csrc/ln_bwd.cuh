@@ -462,16 +462,21 @@ __global__ void __launch_bounds__(C::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a
         // reads one slot per (cta, example)
         __syncthreads();
         const int64_t e0 = r_begin / M, e1 = (r_end - 1) / M;
+        constexpr int E = 16 / sizeof(Acc);  // Acc per 16-byte vector (Dp is a multiple of E)
         for (int64_t ex = e0; ex <= e1; ++ex) {
             Acc* base = static_cast<Acc*>(a.partial) + (size_t)(cta + ex) * G * 2 * Dp;
-            for (int i = threadIdx.x; i < 2 * Dp; i += blockDim.x) {
-                Acc v[G];
+            for (int i = threadIdx.x; i < 2 * Dp / E; i += blockDim.x) {
+                uint4 v[G];
 #pragma unroll
-                for (int gg = 0; gg < G; ++gg) v[gg] = base[(size_t)gg * 2 * Dp + i];
-                Acc t = v[0];
+                for (int gg = 0; gg < G; ++gg) v[gg] = *reinterpret_cast<const uint4*>(base + (size_t)gg * 2 * Dp + i * E);
+                Acc t[E];
 #pragma unroll
-                for (int gg = 1; gg < G; ++gg) t += v[gg];
-                base[i] = t;
+                for (int e = 0; e < E; ++e) t[e] = reinterpret_cast<const Acc*>(&v[0])[e];
+#pragma unroll
+                for (int gg = 1; gg < G; ++gg)
+#pragma unroll
+                    for (int e = 0; e < E; ++e) t[e] += reinterpret_cast<const Acc*>(&v[gg])[e];
+                *reinterpret_cast<uint4*>(base + i * E) = *reinterpret_cast<const uint4*>(t);
             }
         }
     }
@@ -501,18 +506,18 @@ __global__ void __launch_bounds__(C::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a
             double vg = 0.0, vb = 0.0;
             if (cv) {
                 // one (pre-combined) slot per CTA that touched example b; issue
-                // four CTAs' loads at a time, then add in fixed CTA order
-                for (int64_t cc = c0; cc <= c1; cc += 4) {
-                    Acc lg[4], lb[4];
+                // eight CTAs' loads at a time, then add in fixed CTA order
+                for (int64_t cc = c0; cc <= c1; cc += 8) {
+                    Acc lg[8], lb[8];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
+                    for (int u = 0; u < 8; ++u) {
                         const bool ok = cc + u <= c1;
                         const Acc* base = part_r + (size_t)(ok ? cc + u + b : 0) * G * 2 * Dp + col;
                         lg[u] = ok ? __ldcg(base) : Acc(0);
                         lb[u] = ok ? __ldcg(base + Dp) : Acc(0);
                     }
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
+                    for (int u = 0; u < 8; ++u) {
                         vg += (double)lg[u];
                         vb += (double)lb[u];
                     }

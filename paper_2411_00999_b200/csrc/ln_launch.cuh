@@ -91,9 +91,61 @@ struct BwdOp {
     static int plan(int64_t B, int64_t M, int64_t D, BwdPlan& p, const char** why) {
         return plan_bwd<C>(B, M, D, p, why);
     }
+    // Launch plans are cached per (device, B, M, D): the steady-state launch
+    // path does no driver queries besides the launch itself.
+    struct PlanKey {
+        int dev;
+        int64_t B, M, D;
+        bool operator<(const PlanKey& o) const {
+            return dev != o.dev ? dev < o.dev : B != o.B ? B < o.B : M != o.M ? M < o.M : D < o.D;
+        }
+    };
+    static int cached_plan(int64_t B, int64_t M, int64_t D, BwdPlan& p, const char** why, cudaError_t* cerr) {
+        static std::mutex mu;
+        static std::map<PlanKey, BwdPlan> cache;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const PlanKey key{dev, B, M, D};
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            auto it = cache.find(key);
+            if (it != cache.end()) {
+                p = it->second;
+                return 0;
+            }
+        }
+        if (plan_bwd<C>(B, M, D, p, why)) return 1;
+        // one CTA per SM must fit (cooperative launch); shrink the ring if not.
+        // All four kernel variants share geometry and shared memory: set the
+        // attribute on each, check occupancy on the largest (fused) one.
+        void (*ks[4])(LnBwdArgs) = {ln_bwd_kernel<C, true, true>, ln_bwd_kernel<C, true, false>,
+                                    ln_bwd_kernel<C, false, true>, ln_bwd_kernel<C, false, false>};
+        for (;;) {
+            cudaError_t e = cudaSuccess;
+            for (auto k : ks)
+                if (e == cudaSuccess) e = ensure_smem(reinterpret_cast<const void*>(k), p.smem);
+            int occ = 0;
+            if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ks[0], p.threads, p.smem);
+            if (e != cudaSuccess) {
+                *cerr = e;
+                return 2;
+            }
+            if (occ >= 1) break;
+            if (p.stages <= 2) {
+                *cerr = cudaErrorCooperativeLaunchTooLarge;
+                return 2;
+            }
+            --p.stages;
+            p.smem = C::smem_bytes(p.stages, p.Dp);
+        }
+        std::lock_guard<std::mutex> lk(mu);
+        cache[key] = p;
+        return 0;
+    }
+
     static int run(const LnBwdCall& c, cudaStream_t st, const char** why, cudaError_t* cerr) {
         BwdPlan p;
-        if (plan_bwd<C>(c.B, c.M, c.D, p, why)) return 1;
+        if (int rc = cached_plan(c.B, c.M, c.D, p, why, cerr)) return rc;
         if (c.ws_bytes < p.total) {
             *why = "layers: workspace too small (query gnsb_ln_bwd_workspace_size)";
             return 1;
@@ -132,28 +184,6 @@ struct BwdOp {
         else if (hm) k = ln_bwd_kernel<C, true, false>;
         else if (c.norms) k = ln_bwd_kernel<C, false, true>;
         else k = ln_bwd_kernel<C, false, false>;
-        cudaError_t e = ensure_smem(reinterpret_cast<const void*>(k), p.smem);
-        if (e != cudaSuccess) {
-            *cerr = e;
-            return 2;
-        }
-        // one CTA per SM must fit (cooperative launch); shrink the ring if not
-        for (;;) {
-            int occ = 0;
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, p.threads, p.smem);
-            if (e != cudaSuccess) {
-                *cerr = e;
-                return 2;
-            }
-            if (occ >= 1) break;
-            if (p.stages <= 2) {
-                *cerr = cudaErrorCooperativeLaunchTooLarge;
-                return 2;
-            }
-            --p.stages;
-            p.smem = C::smem_bytes(p.stages, p.Dp);
-        }
-        a.stages = p.stages;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(p.grid);
         cfg.blockDim = dim3(p.threads);
@@ -164,7 +194,7 @@ struct BwdOp {
         attr[0].val.cooperative = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        e = cudaLaunchKernelEx(&cfg, k, a);
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, k, a);
         if (e != cudaSuccess) {
             *cerr = e;
             return 2;
