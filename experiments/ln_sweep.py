@@ -17,6 +17,8 @@ dev = torch.device("cuda")
 B, T = int(os.environ.get('SWEEP_B', '32')), 1024
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 TRACE = os.environ.get("SWEEP_TRACE") == "1"
+FLUSH = os.environ.get("SWEEP_FLUSH", "write")
+flush_sink = torch.zeros((), dtype=torch.int64, device=dev)
 trace = torch.zeros(148 * 6, dtype=torch.int64, device=dev)
 Ds = [int(v) for v in sys.argv[1].split(",")] if len(sys.argv) > 1 else [768, 1024, 2048, 4096, 8192]
 ids = [int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else list(range(lib.sweep_n()))
@@ -42,7 +44,10 @@ for D in Ds:
         for norms in (1, 0):
             ts = []
             for r in range(12):
-                flush.zero_()
+                if FLUSH == "write":
+                    flush.zero_()
+                elif FLUSH == "read":
+                    flush_sink.copy_(flush.view(torch.int64).sum())
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
                 rc = lib.sweep_run(i, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(f.cache.mean.data_ptr()),
