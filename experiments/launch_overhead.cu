@@ -35,3 +35,13 @@ extern "C" int run_empty(int coop, int threads, int smem, int reps, int back2bac
     *ms = tot / (reps - 1);
     return cudaGetLastError();
 }
+
+__global__ void marker_kernel(unsigned long long* p) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    *p = t;
+}
+extern "C" int marker(void* p, void* stream) {
+    marker_kernel<<<1, 1, 0, (cudaStream_t)stream>>>((unsigned long long*)p);
+    return cudaGetLastError();
+}

@@ -17,6 +17,8 @@ dev = torch.device("cuda")
 B, T = int(os.environ.get('SWEEP_B', '32')), 1024
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 TRACE = os.environ.get("SWEEP_TRACE") == "1"
+mk = ctypes.CDLL(os.path.join(ROOT, "experiments", "liblaunch_overhead.so"))
+marks = torch.zeros(2, dtype=torch.int64, device=dev)
 FLUSH = os.environ.get("SWEEP_FLUSH", "write")
 flush_sink = torch.zeros((), dtype=torch.int64, device=dev)
 trace = torch.zeros(148 * 6, dtype=torch.int64, device=dev)
@@ -50,6 +52,8 @@ for D in Ds:
                     flush_sink.copy_(flush.view(torch.int64).sum())
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
+                if TRACE:
+                    mk.marker(ctypes.c_void_p(marks.data_ptr()), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
                 rc = lib.sweep_run(i, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(f.cache.mean.data_ptr()),
                                    ctypes.c_void_p(f.cache.inv_std.data_ptr()), ctypes.c_void_p(dy.data_ptr()),
                                    ctypes.c_void_p(gamma.data_ptr()), ctypes.c_void_p(dx.data_ptr()),
@@ -58,6 +62,8 @@ for D in Ds:
                                    ctypes.c_void_p(sums.data_ptr()), norms, B, T, D, ctypes.c_void_p(ws.data_ptr()),
                                    ctypes.c_size_t(ws.numel()), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream),
                                    ctypes.c_void_p(trace.data_ptr() if TRACE else 0))
+                if TRACE:
+                    mk.marker(ctypes.c_void_p(marks.data_ptr() + 8), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
                 e1.record()
                 if rc:
                     break
@@ -72,7 +78,9 @@ for D in Ds:
         ok = ""
         if TRACE:
             tr = trace.view(-1, 6).cpu().numpy().astype("int64")
+            mks = marks.cpu().numpy().astype("int64")
             t0 = tr[:, 0].min()
+            print(f"   marker before -> first CTA start {(t0 - mks[0]) / 1000:.1f} us; last CTA end -> marker after {(mks[1] - tr[:, 5].max()) / 1000:.1f} us")
             rel = (tr - t0) / 1000.0
             last = rel[:, 5].max()
             print(f"   trace(us): start max {rel[:,0].max():.1f} | rowmath end min {rel[:,1].min():.1f} med {sorted(rel[:,1])[74]:.1f} max {rel[:,1].max():.1f}"

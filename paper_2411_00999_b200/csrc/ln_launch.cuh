@@ -176,6 +176,7 @@ struct BwdOp {
         a.qbig = reinterpret_cast<double*>(ws + p.off_qbig);
         a.rawws = reinterpret_cast<double*>(ws + p.off_raw);
         a.nchunks = p.nchunks;
+        a.scratch_bytes = (int64_t)(p.smem - C::rows_off(p.stages, p.Dp));
         a.trace = c.trace;
 
         void (*k)(LnBwdArgs) = nullptr;
