@@ -488,115 +488,67 @@ __global__ void __launch_bounds__(C::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a
     grid_barrier(&a.counters[0]);
     stamp(3);
 
-    // Column chunk c (kChunk columns) is owned by CTA c % grid.  For each chunk
-    // the CTA gathers gamma'_b, beta'_b for every example b (sum of that
-    // example's per-CTA slots, fixed CTA order) with all slot loads of a thread
-    // in flight together, stages them in shared memory, then reduces in fixed
-    // order: over b -> dgamma/dbeta; squares over the chunk's columns -> the
-    // per-(example, chunk) norm partials q.
     const Acc* part_r = static_cast<const Acc*>(a.partial);
     Acc* dgam = static_cast<Acc*>(a.dgamma);
     Acc* dbet = static_cast<Acc*>(a.dbeta);
     const int nthreads = blockDim.x;
+    const int NB = nthreads / kChunk;
+    const int cl = threadIdx.x % kChunk, bl = threadIdx.x / kChunk;
+    const unsigned hmask = 0xffffu << (lane & 16);
+    double* sred = reinterpret_cast<double*>(smem + C::rows_off(S, Dp));  // ring is free now
     const int64_t B = a.B;
-    double* sv = reinterpret_cast<double*>(smem + C::rows_off(S, Dp));  // the ring is free now
-    const int BT = (int)((int64_t)a.scratch_bytes / (2 * kChunk * 8) < B ? (int64_t)a.scratch_bytes / (2 * kChunk * 8) : B);
-    double* svg = sv;                              // [BT][kChunk]
-    double* svb = sv + (size_t)BT * kChunk;         // [BT][kChunk]
     auto cta_of = [&](int64_t r) -> int64_t { return ((r + 1) * grid - 1) / N; };
-    constexpr int IB = 2;  // items per load batch
-    const int J = nthreads / kChunk;  // partial-sum lanes per column for the sum over b
 
     for (int chunk = cta; chunk < a.nchunks; chunk += grid) {
-        double tg_part = 0.0, tb_part = 0.0;  // this thread's share of the sum over b
-        const int cl_r = threadIdx.x % kChunk, j_r = threadIdx.x / kChunk;
-        const int64_t colr = (int64_t)chunk * kChunk + cl_r;
-        for (int64_t b0 = 0; b0 < B; b0 += BT) {
-            const int nb = (int)(B - b0 < BT ? B - b0 : BT);
-            const int nitems = nb * kChunk;
-            for (int i0 = threadIdx.x; i0 < nitems; i0 += IB * nthreads) {
-                double vg[IB], vb[IB];
-                int64_t c0[IB], c1[IB], bb[IB], colv[IB];
-                bool ok[IB];
+        const int64_t col = (int64_t)chunk * kChunk + cl;
+        const bool cv = col < D;
+        double sg = 0.0, sb = 0.0;
+        for (int64_t b = bl; b < B; b += NB) {
+            const int64_t c0 = cta_of(b * M), c1 = cta_of((b + 1) * M - 1);
+            double vg = 0.0, vb = 0.0;
+            if (cv) {
+                // one (pre-combined) slot per CTA that touched example b; issue
+                // eight CTAs' loads at a time, then add in fixed CTA order
+                for (int64_t cc = c0; cc <= c1; cc += 8) {
+                    Acc lg[8], lb[8];
 #pragma unroll
-                for (int u = 0; u < IB; ++u) {
-                    const int it = i0 + u * nthreads;
-                    ok[u] = it < nitems;
-                    bb[u] = b0 + (ok[u] ? it / kChunk : 0);
-                    colv[u] = (int64_t)chunk * kChunk + it % kChunk;
-                    ok[u] = ok[u] && colv[u] < D;
-                    c0[u] = cta_of(bb[u] * M);
-                    c1[u] = cta_of((bb[u] + 1) * M - 1);
-                    vg[u] = vb[u] = 0.0;
-                }
-                int64_t span = 0;
+                    for (int u = 0; u < 8; ++u) {
+                        const bool ok = cc + u <= c1;
+                        const Acc* base = part_r + (size_t)(ok ? cc + u + b : 0) * G * 2 * Dp + col;
+                        lg[u] = ok ? __ldcg(base) : Acc(0);
+                        lb[u] = ok ? __ldcg(base + Dp) : Acc(0);
+                    }
 #pragma unroll
-                for (int u = 0; u < IB; ++u) span = ok[u] && c1[u] - c0[u] + 1 > span ? c1[u] - c0[u] + 1 : span;
-                for (int64_t k0 = 0; k0 < span; k0 += 8) {
-                    Acc lg[IB][8], lb[IB][8];
-#pragma unroll
-                    for (int u = 0; u < IB; ++u)
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) {
-                            const int64_t cc = c0[u] + k0 + k;
-                            const bool v = ok[u] && cc <= c1[u];
-                            const Acc* base = part_r + (size_t)(v ? cc + bb[u] : 0) * G * 2 * Dp + (v ? colv[u] : 0);
-                            lg[u][k] = v ? __ldcg(base) : Acc(0);
-                            lb[u][k] = v ? __ldcg(base + Dp) : Acc(0);
-                        }
-#pragma unroll
-                    for (int u = 0; u < IB; ++u)
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) {
-                            vg[u] += (double)lg[u][k];
-                            vb[u] += (double)lb[u][k];
-                        }
-                }
-#pragma unroll
-                for (int u = 0; u < IB; ++u) {
-                    const int it = i0 + u * nthreads;
-                    if (it < nitems) {
-                        svg[it] = vg[u];
-                        svb[it] = vb[u];
+                    for (int u = 0; u < 8; ++u) {
+                        vg += (double)lg[u];
+                        vb += (double)lb[u];
                     }
                 }
             }
-            __syncthreads();
-            // per-example norm partials over this chunk's columns (fixed column order)
+            sg += vg;
+            sb += vb;
             if constexpr (NORMS) {
-                for (int bl = threadIdx.x; bl < nb; bl += nthreads) {
-                    double qg = 0.0, qb = 0.0;
+                double qg = vg * vg, qb = vb * vb;
 #pragma unroll
-                    for (int k = 0; k < kChunk; ++k) {
-                        const double xg = svg[bl * kChunk + k], xb = svb[bl * kChunk + k];
-                        qg += xg * xg;
-                        qb += xb * xb;
-                    }
-                    a.q[((size_t)(b0 + bl) * a.nchunks + chunk) * 2 + 0] = qg;
-                    a.q[((size_t)(b0 + bl) * a.nchunks + chunk) * 2 + 1] = qb;
+                for (int o = kChunk / 2; o > 0; o >>= 1) {
+                    qg += __shfl_xor_sync(hmask, qg, o);
+                    qb += __shfl_xor_sync(hmask, qb, o);
+                }
+                if (cl == 0) {
+                    a.q[((size_t)b * a.nchunks + chunk) * 2 + 0] = qg;
+                    a.q[((size_t)b * a.nchunks + chunk) * 2 + 1] = qb;
                 }
             }
-            // sum over b: lane (cl_r, j_r) folds b = j_r, j_r + J, ... of this tile
-            for (int bl = j_r; bl < nb; bl += J) {
-                tg_part += svg[bl * kChunk + cl_r];
-                tb_part += svb[bl * kChunk + cl_r];
-            }
-            __syncthreads();
         }
-        // fold the J partial sums of each column in fixed j order ([J][kChunk] each)
-        double* fgs = sv;
-        double* fbs = sv + nthreads;
-        fgs[threadIdx.x] = tg_part;
-        fbs[threadIdx.x] = tb_part;
+        sred[(size_t)bl * kChunk + cl] = sg;
+        sred[(size_t)(NB + bl) * kChunk + cl] = sb;
         __syncthreads();
-        if (threadIdx.x < kChunk) {
+        if (bl == 0) {
             double tg = 0.0, tb = 0.0;
-            for (int j = 0; j < J; ++j) {
-                tg += fgs[j * kChunk + threadIdx.x];
-                tb += fbs[j * kChunk + threadIdx.x];
+            for (int k = 0; k < NB; ++k) {
+                tg += sred[(size_t)k * kChunk + cl];
+                tb += sred[(size_t)(NB + k) * kChunk + cl];
             }
-            const int64_t col = (int64_t)chunk * kChunk + threadIdx.x;
-            const bool cv = col < D;
             if (cv) {
                 dgam[col] = (Acc)tg;
                 dbet[col] = (Acc)tb;
@@ -609,13 +561,12 @@ __global__ void __launch_bounds__(C::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a
                     qg += __shfl_xor_sync(0xffffu, qg, o);
                     qb += __shfl_xor_sync(0xffffu, qb, o);
                 }
-                if (threadIdx.x == 0) {
+                if (cl == 0) {
                     a.qbig[(size_t)chunk * 2 + 0] = qg;
                     a.qbig[(size_t)chunk * 2 + 1] = qb;
                 }
             }
         }
-        (void)colr;
         __syncthreads();
     }
 
