@@ -90,6 +90,42 @@ gnsb_status gnsb_ln_bwd_geometry(int64_t B, int64_t M, int64_t D, gnsb_dtype dt,
                                  int32_t* stages);
 
 /* ------------------------------------------------------------------------
+ * Linear layer: per-example squared weight-gradient norms (3-D regime).
+ * Replaces gnstk::linear_backward_simultaneous (proj/include/gnstk/layers.hpp:69,
+ * proj/src/layers.cpp:80-157) and gnstk::linear_perexample_sqnorm_frobenius
+ * (layers.hpp:74, layers.cpp:159-187).  x [B, T, K], g [B, T, L] (g from a
+ * MEAN-reduced loss).
+ *
+ *   form 1 (weight-gradient / "simultaneous" form): dW_b = sum_t x_t^T g_t per
+ *          example, raw_w[b] = ||dW_b||_F^2, dW = sum_b dW_b (dW nullable).
+ *          bf16 rows with T % 64 == 0, K % 128 == 0, L % 256 == 0 run on the
+ *          tcgen05 tensor-core kernel (fp32 accumulate); other shapes/dtypes run
+ *          a generic fp64-accumulating CUDA kernel.
+ *   form 2 (Gram / Frobenius form): raw_w[b] = <X_b X_b^T, G_b G_b^T>_F; dW must
+ *          be NULL (the reference's Frobenius function returns norms only).
+ *   form 0 (auto): form 1 when dW is requested; otherwise the cheaper form by
+ *          the FLOP model (Gram when T*(K+L) < 2*K*L, proj/src/costmodel.cpp:25-37).
+ *   dW    : [K, L] fp32 (fp64 for GNSB_F64 rows).
+ *   raw_w : [B] fp64 uncorrected per-example norms (nullable).
+ *   sums  : [4] fp64 (nullable); writes sums[0] = sum_b raw_w and, for form 1,
+ *           sums[2] = ||dW||^2 (slots 1 and 3 belong to the bias).
+ * Errors: B == 0 ("empty batch"), non-positive extents.
+ */
+gnsb_status gnsb_linear_pe_workspace_size(int64_t B, int64_t T, int64_t K, int64_t L, gnsb_dtype dt, size_t* bytes);
+gnsb_status gnsb_linear_pe_norms(const void* x, const void* g, void* dW, double* raw_w, double* sums, int64_t B,
+                                 int64_t T, int64_t K, int64_t L, int32_t form, gnsb_dtype dt, void* ws,
+                                 size_t ws_bytes, void* stream);
+/* Bias of a linear layer: bias'_b = sum_t g[b,t,:], raw_b[b] = ||bias'_b||^2,
+ * dbias = sum_b bias'_b (layers.cpp:118-119, 125-130).  sums[1] = sum_b raw_b,
+ * sums[3] = ||dbias||^2.  Workspace: gnsb_linear_pe_workspace_size(B, T, 1, L). */
+gnsb_status gnsb_linear_bias_pe(const void* g, void* dbias, double* raw_b, double* sums, int64_t B, int64_t T,
+                                int64_t L, gnsb_dtype dt, void* ws, size_t ws_bytes, void* stream);
+/* Input gradient dx[r, i] = sum_j g[r, j] W[i, j] (layers.cpp:142-155); W [K, L]
+ * fp32 (fp64 for GNSB_F64). */
+gnsb_status gnsb_linear_dx(const void* g, const void* W, void* dx, int64_t rows, int64_t K, int64_t L, gnsb_dtype dt,
+                           void* stream);
+
+/* ------------------------------------------------------------------------
  * Deterministic fp64 squared norm of a device vector (fp32 or fp64 data):
  * out[0] = sum_i v[i]^2.  Used after the batch-sharded all-reduce, where
  * ||G_big||^2 must be formed from the REDUCED gradient.

@@ -65,6 +65,11 @@ _SIGS = {
         [c_i64, c_i64, c_i64, c_i32, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32), ctypes.POINTER(c_i32)],
     ),
     "gnsb_sqnorm": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp]),
+    "gnsb_linear_pe_workspace_size": (c_i32, [c_i64, c_i64, c_i64, c_i64, c_i32, c_szp]),
+    "gnsb_linear_pe_norms": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i32, c_i32, c_vp,
+                                     ctypes.c_size_t, c_vp]),
+    "gnsb_linear_bias_pe": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i32, c_vp, ctypes.c_size_t, c_vp]),
+    "gnsb_linear_dx": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i32, c_vp]),
     "gnsb_estimate_g2": (c_i32, [ctypes.POINTER(GradStats), c_dp]),
     "gnsb_estimate_s": (c_i32, [ctypes.POINTER(GradStats), c_dp]),
     "gnsb_make_gns_estimate": (None, [c_f64, c_f64, ctypes.POINTER(GnsEstimate)]),

@@ -268,6 +268,68 @@ gnsb_status gnsb_ln_bwd(const void* x, const void* mean, const void* rstd, const
     return GNSB_OK;
 }
 
+// ---------------------------------------------------------------- linear --
+static bool use_tc_wgrad(gnsb_dtype dt, int64_t B, int64_t T, int64_t K, int64_t L) {
+    return dt == GNSB_BF16 && gnsb::wgrad_shape_ok(B, T, K, L);
+}
+
+gnsb_status gnsb_linear_pe_workspace_size(int64_t B, int64_t T, int64_t K, int64_t L, gnsb_dtype dt, size_t* bytes) {
+    if (!bytes || B < 0 || T < 0 || K < 1 || L < 1) return fail(GNSB_EINVAL, "layers: invalid extents");
+    size_t n = gnsb::generic_workspace(B, T, K, L);
+    if (use_tc_wgrad(dt, B, T, K, L)) {
+        const size_t m = gnsb::wgrad_workspace(B, K, L);
+        n = n > m ? n : m;
+    }
+    *bytes = n;
+    return GNSB_OK;
+}
+
+gnsb_status gnsb_linear_pe_norms(const void* x, const void* g, void* dW, double* raw_w, double* sums, int64_t B,
+                                 int64_t T, int64_t K, int64_t L, int32_t form, gnsb_dtype dt, void* ws,
+                                 size_t ws_bytes, void* stream) {
+    if (B == 0) return fail(GNSB_EINVAL, "layers: empty batch");  // layers.cpp:89
+    if (B < 0 || T < 0 || K < 1 || L < 1) return fail(GNSB_EINVAL, "layers: invalid extents");
+    if (form < 0 || form > 2) return fail(GNSB_EINVAL, "layers: form must be 0 (auto), 1 (weight-grad) or 2 (gram)");
+    if (form == 2 && dW) return fail(GNSB_EINVAL, "layers: the gram form computes norms only (dW must be NULL)");
+    if (dt != GNSB_F32 && dt != GNSB_BF16 && dt != GNSB_F64) return fail(GNSB_EINVAL, "layers: unknown dtype");
+    if (gnsb_status s = need_device()) return s;
+    size_t need = 0;
+    gnsb_linear_pe_workspace_size(B, T, K, L, dt, &need);
+    if (!ws || ws_bytes < need) return fail(GNSB_EINVAL, "layers: workspace too small (query gnsb_linear_pe_workspace_size)");
+    if ((T > 0) && (!x || !g)) return fail(GNSB_EINVAL, "layers: null input pointer");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (form == 0) form = (dW != nullptr || T * (K + L) >= 2 * K * L) ? 1 : 2;
+    cudaError_t e;
+    if (form == 1 && use_tc_wgrad(dt, B, T, K, L))
+        e = gnsb::launch_wgrad_norms(x, g, static_cast<float*>(dW), raw_w, sums, B, T, K, L, ws, st);
+    else
+        e = gnsb::launch_linear_generic((int)dt, form == 1 ? 0 : 2, x, g, dW, dt == GNSB_F64, raw_w, sums, 0, B, T, K,
+                                        L, ws, st);
+    return e == cudaSuccess ? GNSB_OK : cuda_fail(e, "linear_pe_norms launch");
+}
+
+gnsb_status gnsb_linear_bias_pe(const void* g, void* dbias, double* raw_b, double* sums, int64_t B, int64_t T,
+                                int64_t L, gnsb_dtype dt, void* ws, size_t ws_bytes, void* stream) {
+    if (B == 0) return fail(GNSB_EINVAL, "layers: empty batch");
+    if (B < 0 || T < 0 || L < 1) return fail(GNSB_EINVAL, "layers: invalid extents");
+    if (dt != GNSB_F32 && dt != GNSB_BF16 && dt != GNSB_F64) return fail(GNSB_EINVAL, "layers: unknown dtype");
+    if (gnsb_status s = need_device()) return s;
+    if (!ws || ws_bytes < gnsb::generic_workspace(B, T, 1, L))
+        return fail(GNSB_EINVAL, "layers: workspace too small (query gnsb_linear_pe_workspace_size)");
+    const cudaError_t e = gnsb::launch_linear_generic((int)dt, 1, nullptr, g, dbias, dt == GNSB_F64, raw_b, sums, 1, B,
+                                                      T, 1, L, ws, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? GNSB_OK : cuda_fail(e, "linear_bias_pe launch");
+}
+
+gnsb_status gnsb_linear_dx(const void* g, const void* W, void* dx, int64_t rows, int64_t K, int64_t L, gnsb_dtype dt,
+                           void* stream) {
+    if (rows < 0 || K < 1 || L < 1) return fail(GNSB_EINVAL, "layers: invalid extents");
+    if (dt != GNSB_F32 && dt != GNSB_BF16 && dt != GNSB_F64) return fail(GNSB_EINVAL, "layers: unknown dtype");
+    if (gnsb_status s = need_device()) return s;
+    const cudaError_t e = gnsb::launch_linear_dx((int)dt, g, W, dx, rows, K, L, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? GNSB_OK : cuda_fail(e, "linear_dx launch");
+}
+
 gnsb_status gnsb_sqnorm(const void* v, int64_t n, gnsb_dtype dt, double* out, void* stream) {
     if (n < 0 || !out) return fail(GNSB_EINVAL, "gns: invalid sqnorm arguments");
     if (gnsb_status s = need_device()) return s;

@@ -42,4 +42,17 @@ template <typename T> int ln_bwd_geometry(int64_t B, int64_t M, int64_t D, int* 
 
 int device_sm_count();
 
+// linear-layer per-example norms (linear_pe.cu)
+bool wgrad_shape_ok(int64_t B, int64_t T, int64_t K, int64_t L);
+size_t wgrad_workspace(int64_t B, int64_t K, int64_t L);
+cudaError_t launch_wgrad_norms(const void* x, const void* g, float* dW, double* raw, double* sums, int64_t B,
+                               int64_t T, int64_t K, int64_t L, void* ws, cudaStream_t st);
+size_t generic_workspace(int64_t B, int64_t T, int64_t K, int64_t L);
+// kind 0: weight (simultaneous form), 1: bias, 2: Gram form (norms only)
+cudaError_t launch_linear_generic(int dt, int kind, const void* x, const void* g, void* out_grad, int out_f64,
+                                  double* raw, double* sums, int sum_slot, int64_t B, int64_t T, int64_t K, int64_t L,
+                                  void* ws, cudaStream_t st);
+cudaError_t launch_linear_dx(int dt, const void* g, const void* W, void* dx, int64_t rows, int64_t K, int64_t L,
+                             cudaStream_t st);
+
 }  // namespace gnsb

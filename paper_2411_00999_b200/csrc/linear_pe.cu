@@ -1,0 +1,516 @@
+// linear_pe.cu — per-example squared gradient norms of a linear layer on
+// sm_100a tensor cores (tcgen05 + TMEM + TMA).
+//
+// Semantics (proj/src/layers.cpp:80-157, the "simultaneous" / weight-gradient
+// form): for each example b, dW_b = sum_t x_{b,t}^T g_{b,t} (K x L);
+// raw_b = ||dW_b||_F^2 (the square is taken AFTER the sum over t);
+// dW = sum_b dW_b.  And the Gram / Frobenius form (layers.cpp:159-187):
+// raw_b = <X_b X_b^T, G_b G_b^T>_F.
+//
+// Weight-gradient form kernel (wgrad_norms_kernel):
+//   * persistent, one CTA per SM, static round-robin over 128 x 256 output
+//     tiles of dW; for every tile the CTA walks all examples b;
+//   * warp 0: TMA producer.  A = X_b^T and B = G_b are MN-major operands read
+//     straight from the [B, T, K] / [B, T, L] row-major tensors through 3-D
+//     tensor maps (box 64 features x 64 tokens, 128-byte swizzle), 4-stage ring;
+//   * warp 1: a single elected thread issues tcgen05.mma (M=128, N=256, K=16,
+//     bf16 -> fp32) into a per-example TMEM accumulator; two 256-column
+//     accumulators (all 512 TMEM columns) alternate between examples so the
+//     epilogue of example b overlaps the MMAs of example b+1;
+//   * warps 2..9: epilogue.  tcgen05.ld the example's tile, square-accumulate
+//     (-> the tile's share of raw_b) and add it into the running sum_b dW held
+//     in registers (128 columns x 1 row per thread); after the last example the
+//     tile of dW is stored once.
+//   * per-(example, tile) partial norms are folded by a deterministic second
+//     kernel; no floating-point atomics.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <mutex>
+
+#include "common.cuh"
+#include "internal.h"
+#include "tc.cuh"
+
+namespace gnsb {
+
+namespace wg {
+constexpr int BM = 128, BN = 256, BK = 64;   // tile and K-block (tokens per stage)
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;         // 16 KB
+constexpr int B_BYTES = BN * BK * 2;         // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int EPI_WARPS = 8;
+constexpr int THREADS = (2 + EPI_WARPS) * 32;
+constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 1024;  // align slack + ring + barriers
+constexpr int TMEM_COLS = 512;
+}  // namespace wg
+
+struct WgradArgs {
+    int B, T, K, L;
+    int tiles_m, tiles_n;
+    float* dW;     // [K, L] or null
+    double* q;     // [B][tiles] per-(example, tile) ||dW_b tile||^2
+    double* qbig;  // [tiles] ||dW tile||^2
+};
+
+__global__ void __launch_bounds__(wg::THREADS, 1)
+    wgrad_norms_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmg, WgradArgs a) {
+    using namespace wg;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char* ring = smem;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)STAGES * STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;   // [2]
+    uint64_t* tempty = tfull + 2;       // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    float* red = reinterpret_cast<float*>(tmem_slot + 4);  // [EPI_WARPS]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ntiles = a.tiles_m * a.tiles_n;
+    const int kblocks = a.T / BK;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&tfull[s], 1);
+            mbar_init(&tempty[s], EPI_WARPS);
+        }
+        fence_mbar_init();
+        tc::prefetch_tmap(&tmx);
+        tc::prefetch_tmap(&tmg);
+    }
+    if (warp == 1) tc::tmem_alloc<TMEM_COLS>(tmem_slot);
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------------ TMA producer --
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                const int i0 = (tile % a.tiles_m) * BM, j0 = (tile / a.tiles_m) * BN;
+                for (int b = 0; b < a.B; ++b)
+                    for (int kb = 0; kb < kblocks; ++kb) {
+                        mbar_wait(&empty[s], ph ^ 1u);
+                        unsigned char* st = ring + (size_t)s * STAGE_BYTES;
+                        mbar_expect_tx(&full[s], STAGE_BYTES);
+                        const int t0 = kb * BK;
+#pragma unroll
+                        for (int h = 0; h < BM / 64; ++h) tc::tma_load_3d(st + h * 8192, &tmx, i0 + 64 * h, t0, b, &full[s]);
+#pragma unroll
+                        for (int h = 0; h < BN / 64; ++h)
+                            tc::tma_load_3d(st + A_BYTES + h * 8192, &tmg, j0 + 64 * h, t0, b, &full[s]);
+                        if (++s == STAGES) {
+                            s = 0;
+                            ph ^= 1u;
+                        }
+                    }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------- MMA issuer --
+        if (lane == 0) {
+            constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, true, true);
+            int s = 0, buf = 0;
+            uint32_t ph = 0, tph = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                for (int b = 0; b < a.B; ++b) {
+                    mbar_wait(&tempty[buf], tph ^ 1u);  // epilogue drained this accumulator
+                    tc::fence_after_sync();
+                    const uint32_t dcol = tmem + (uint32_t)(buf * BN);
+                    for (int kb = 0; kb < kblocks; ++kb) {
+                        mbar_wait(&full[s], ph);
+                        tc::fence_after_sync();
+                        const uint32_t abase = smem_u32(ring + (size_t)s * STAGE_BYTES);
+                        const uint32_t bbase = abase + A_BYTES;
+#pragma unroll
+                        for (int k = 0; k < BK / 16; ++k) {
+                            // MN-major SW128: 64-element x 8-row atoms; SBO = next 8 rows (1 KB),
+                            // LBO = next 64 features (8 KB); a K step of 16 rows = 2 KB
+                            const uint64_t ad = tc::smem_desc_sw128(abase + k * 2048, 8192, 1024);
+                            const uint64_t bd = tc::smem_desc_sw128(bbase + k * 2048, 8192, 1024);
+                            tc::mma_bf16(dcol, ad, bd, idesc, (kb | k) != 0);
+                        }
+                        tc::commit(&empty[s]);  // smem slot free once these MMAs retire
+                        if (++s == STAGES) {
+                            s = 0;
+                            ph ^= 1u;
+                        }
+                    }
+                    tc::commit(&tfull[buf]);  // accumulator of example b complete
+                    if (++buf == 2) {
+                        buf = 0;
+                        tph ^= 1u;
+                    }
+                }
+            }
+        }
+    } else {
+        // --------------------------------------------------------- epilogue --
+        const int e = warp - 2;
+        const int quad = warp & 3;      // TMEM lanes this warp may access
+        const int half = e / 4;         // column half of the 256-wide tile
+        const int row = quad * 32 + lane;
+        int buf = 0;
+        uint32_t tph = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const int i0 = (tile % a.tiles_m) * BM, j0 = (tile / a.tiles_m) * BN;
+            float S[128];
+#pragma unroll
+            for (int c = 0; c < 128; ++c) S[c] = 0.f;
+            for (int b = 0; b < a.B; ++b) {
+                mbar_wait(&tfull[buf], tph);
+                tc::fence_after_sync();
+                float sq = 0.f;
+                const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN + half * 128);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t r[32];
+                    tc::tmem_ld_32x32b_x32(base + c * 32, r);
+                    tc::tmem_ld_wait();
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) {
+                        const float v = __uint_as_float(r[k]);
+                        sq = fmaf(v, v, sq);
+                        S[c * 32 + k] += v;
+                    }
+                }
+                tc::fence_before_sync();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[buf]);
+                // tile's share of raw_b: warp tree, then fixed-order sum over warps
+                sq = warp_sum(sq);
+                if (lane == 0) red[e] = sq;
+                named_bar_sync(1, EPI_WARPS * 32);
+                if (e == 0 && lane == 0) {
+                    double t = 0.0;
+#pragma unroll
+                    for (int w = 0; w < EPI_WARPS; ++w) t += (double)red[w];
+                    a.q[(size_t)b * ntiles + tile] = t;
+                }
+                named_bar_sync(1, EPI_WARPS * 32);
+                if (++buf == 2) {
+                    buf = 0;
+                    tph ^= 1u;
+                }
+            }
+            float sb = 0.f;
+#pragma unroll
+            for (int c = 0; c < 128; ++c) sb = fmaf(S[c], S[c], sb);
+            sb = warp_sum(sb);
+            if (lane == 0) red[e] = sb;
+            named_bar_sync(1, EPI_WARPS * 32);
+            if (e == 0 && lane == 0) {
+                double t = 0.0;
+#pragma unroll
+                for (int w = 0; w < EPI_WARPS; ++w) t += (double)red[w];
+                a.qbig[tile] = t;
+            }
+            named_bar_sync(1, EPI_WARPS * 32);
+            if (a.dW != nullptr) {
+                float4* dst = reinterpret_cast<float4*>(a.dW + (size_t)(i0 + row) * a.L + j0 + half * 128);
+#pragma unroll
+                for (int c = 0; c < 32; ++c) dst[c] = make_float4(S[4 * c], S[4 * c + 1], S[4 * c + 2], S[4 * c + 3]);
+            }
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc::fence_after_sync();
+        tc::tmem_dealloc<TMEM_COLS>(tmem);
+    }
+}
+
+// raw[b] = sum_j q[b][j] (fixed order), sums[0] = sum_b raw[b]
+__global__ void __launch_bounds__(256) fold_rows_kernel(const double* q, int nb, int ncol, double* raw, double* sums,
+                                                        int sum_slot) {
+    __shared__ double rs[1024];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int b = warp; b < nb; b += blockDim.x / 32) {
+        double t = 0.0;
+        for (int j = lane; j < ncol; j += 32) t += q[(size_t)b * ncol + j];
+        t = warp_sum(t);
+        if (lane == 0) {
+            if (raw) raw[b] = t;
+            if (b < 1024) rs[b] = t;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && sums != nullptr) {
+        double t = 0.0;
+        for (int b = 0; b < nb && b < 1024; ++b) t += rs[b];
+        sums[sum_slot] = t;
+    }
+}
+
+// ------------------------------------------------------------------ host --
+namespace {
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    });
+    return fn;
+}
+
+// [B, T, F] bf16 row-major viewed as a 3-D tensor (F innermost), box 64 x 64 x 1, 128B swizzle
+bool make_map_btf(CUtensorMap* m, const void* base, int B, int T, int F) {
+    EncodeFn enc = encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)F, (cuuint64_t)T, (cuuint64_t)B};
+    cuuint64_t strides[2] = {(cuuint64_t)F * 2, (cuuint64_t)T * F * 2};
+    cuuint32_t box[3] = {64, 64, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+bool wgrad_shape_ok(int64_t B, int64_t T, int64_t K, int64_t L) {
+    return B >= 1 && T >= wg::BK && T % wg::BK == 0 && K % wg::BM == 0 && L % wg::BN == 0 && K > 0 && L > 0 &&
+           T < (1 << 30) && B < (1 << 30);
+}
+
+size_t wgrad_workspace(int64_t B, int64_t K, int64_t L) {
+    const int64_t tiles = (K / wg::BM) * (L / wg::BN);
+    return (size_t)(B + 1) * tiles * sizeof(double) + 256;
+}
+
+cudaError_t launch_wgrad_norms(const void* x, const void* g, float* dW, double* raw, double* sums, int64_t B,
+                               int64_t T, int64_t K, int64_t L, void* ws, cudaStream_t st) {
+    CUtensorMap mx, mg;
+    if (!make_map_btf(&mx, x, (int)B, (int)T, (int)K) || !make_map_btf(&mg, g, (int)B, (int)T, (int)L))
+        return cudaErrorInvalidValue;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaFuncSetAttribute(wgrad_norms_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wg::SMEM);
+    });
+    WgradArgs a{};
+    a.B = (int)B;
+    a.T = (int)T;
+    a.K = (int)K;
+    a.L = (int)L;
+    a.tiles_m = (int)(K / wg::BM);
+    a.tiles_n = (int)(L / wg::BN);
+    a.dW = dW;
+    const int ntiles = a.tiles_m * a.tiles_n;
+    a.q = static_cast<double*>(ws);
+    a.qbig = a.q + (size_t)B * ntiles;
+    const int sms = device_sm_count();
+    const int grid = ntiles < sms ? ntiles : sms;
+    wgrad_norms_kernel<<<grid, wg::THREADS, wg::SMEM, st>>>(mx, mg, a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    fold_rows_kernel<<<1, 256, 0, st>>>(a.q, (int)B, ntiles, raw, sums, 0);
+    if (sums) fold_rows_kernel<<<1, 256, 0, st>>>(a.qbig, 1, ntiles, nullptr, sums, 2);
+    return cudaGetLastError();
+}
+
+// -------------------------------------------------------- generic paths --
+// Any shape and dtype, fp64 accumulation: used when the tensor-core tiling
+// does not apply (unaligned K/L/T, fp32/fp64 rows).  One thread per weight
+// entry (i, j); per example b it forms dW_b[i, j] = sum_t x*g in fixed t
+// order, adds it to dW and contributes its square to the block's share of
+// raw_b (fixed-order block tree).
+template <typename T>
+__global__ void __launch_bounds__(256) wgrad_generic_kernel(const T* x, const T* g, int64_t B, int64_t Tn, int64_t K,
+                                                            int64_t L, void* dW, int dw_f64, double* q, int nblk) {
+    __shared__ double red[256];
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool ok = idx < K * L;
+    const int64_t i = ok ? idx / L : 0, j = ok ? idx % L : 0;
+    double S = 0.0;
+    for (int64_t b = 0; b < B; ++b) {
+        double v = 0.0;
+        if (ok)
+            for (int64_t t = 0; t < Tn; ++t)
+                v += (double)to_acc<T>(x[(b * Tn + t) * K + i]) * (double)to_acc<T>(g[(b * Tn + t) * L + j]);
+        S += v;
+        red[threadIdx.x] = v * v;
+        __syncthreads();
+        for (int o = 128; o > 0; o >>= 1) {
+            if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) q[(size_t)b * nblk + blockIdx.x] = red[0];
+        __syncthreads();
+    }
+    red[threadIdx.x] = S * S;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) q[(size_t)B * nblk + blockIdx.x] = red[0];
+    if (ok && dW) {
+        if (dw_f64)
+            static_cast<double*>(dW)[idx] = S;
+        else
+            static_cast<float*>(dW)[idx] = (float)S;
+    }
+}
+
+// per-example bias gradients: bias'_b[j] = sum_t g[b,t,j]; dbias = sum_b; ||bias'_b||^2
+template <typename T>
+__global__ void __launch_bounds__(256) bias_pe_kernel(const T* g, int64_t B, int64_t Tn, int64_t L, void* db,
+                                                      int db_f64, double* q, int nblk) {
+    __shared__ double red[256];
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool ok = j < L;
+    double S = 0.0;
+    for (int64_t b = 0; b < B; ++b) {
+        double v = 0.0;
+        if (ok)
+            for (int64_t t = 0; t < Tn; ++t) v += (double)to_acc<T>(g[(b * Tn + t) * L + j]);
+        S += v;
+        red[threadIdx.x] = v * v;
+        __syncthreads();
+        for (int o = 128; o > 0; o >>= 1) {
+            if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) q[(size_t)b * nblk + blockIdx.x] = red[0];
+        __syncthreads();
+    }
+    red[threadIdx.x] = S * S;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) q[(size_t)B * nblk + blockIdx.x] = red[0];
+    if (ok && db) {
+        if (db_f64)
+            static_cast<double*>(db)[j] = S;
+        else
+            static_cast<float*>(db)[j] = (float)S;
+    }
+}
+
+// dx[row, i] = sum_j g[row, j] * W[i, j] (layers.cpp:142-155), fp64 accumulation
+template <typename T, typename WT>
+__global__ void __launch_bounds__(256) linear_dx_kernel(const T* g, const WT* W, T* dx, int64_t rows, int64_t K,
+                                                        int64_t L) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= rows * K) return;
+    const int64_t r = idx / K, i = idx % K;
+    double acc = 0.0;
+    for (int64_t j = 0; j < L; ++j) acc += (double)to_acc<T>(g[r * L + j]) * (double)W[i * L + j];
+    dx[idx] = from_acc<T>((typename Traits<T>::Acc)acc);
+}
+
+// Gram form, generic: raw_b = sum_{t,u} (x_t . x_u)(g_t . g_u), one thread per (t, u)
+template <typename T>
+__global__ void __launch_bounds__(256) gram_generic_kernel(const T* x, const T* g, int64_t B, int64_t Tn, int64_t K,
+                                                           int64_t L, double* q, int nblk) {
+    __shared__ double red[256];
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool ok = idx < Tn * Tn;
+    const int64_t t = ok ? idx / Tn : 0, u = ok ? idx % Tn : 0;
+    for (int64_t b = 0; b < B; ++b) {
+        double xx = 0.0, gg = 0.0;
+        if (ok) {
+            for (int64_t i = 0; i < K; ++i)
+                xx += (double)to_acc<T>(x[(b * Tn + t) * K + i]) * (double)to_acc<T>(x[(b * Tn + u) * K + i]);
+            for (int64_t j = 0; j < L; ++j)
+                gg += (double)to_acc<T>(g[(b * Tn + t) * L + j]) * (double)to_acc<T>(g[(b * Tn + u) * L + j]);
+        }
+        red[threadIdx.x] = xx * gg;
+        __syncthreads();
+        for (int o = 128; o > 0; o >>= 1) {
+            if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) q[(size_t)b * nblk + blockIdx.x] = red[0];
+        __syncthreads();
+    }
+}
+
+size_t generic_workspace(int64_t B, int64_t T, int64_t K, int64_t L) {
+    const int64_t n1 = (K * L + 255) / 256, n2 = (L + 255) / 256, n3 = (T * T + 255) / 256;
+    int64_t n = n1 > n2 ? n1 : n2;
+    n = n > n3 ? n : n3;
+    return (size_t)(B + 1) * n * sizeof(double) + 256;
+}
+
+template <typename T>
+cudaError_t launch_generic_t(int kind, const void* x, const void* g, void* out_grad, int out_f64, double* raw,
+                             double* sums, int sum_slot, int64_t B, int64_t Tn, int64_t K, int64_t L, void* ws,
+                             cudaStream_t st) {
+    double* q = static_cast<double*>(ws);
+    int nblk = 0;
+    if (kind == 0) {  // weight, simultaneous form
+        nblk = (int)((K * L + 255) / 256);
+        wgrad_generic_kernel<T><<<nblk, 256, 0, st>>>(static_cast<const T*>(x), static_cast<const T*>(g), B, Tn, K, L,
+                                                      out_grad, out_f64, q, nblk);
+    } else if (kind == 1) {  // bias
+        nblk = (int)((L + 255) / 256);
+        bias_pe_kernel<T><<<nblk, 256, 0, st>>>(static_cast<const T*>(g), B, Tn, L, out_grad, out_f64, q, nblk);
+    } else {  // Gram form (norms only)
+        nblk = (int)((Tn * Tn + 255) / 256);
+        gram_generic_kernel<T><<<nblk, 256, 0, st>>>(static_cast<const T*>(x), static_cast<const T*>(g), B, Tn, K, L,
+                                                     q, nblk);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    fold_rows_kernel<<<1, 256, 0, st>>>(q, (int)B, nblk, raw, sums, sum_slot);
+    if (sums && kind != 2) fold_rows_kernel<<<1, 256, 0, st>>>(q + (size_t)B * nblk, 1, nblk, nullptr, sums, sum_slot + 2);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_linear_generic(int dt, int kind, const void* x, const void* g, void* out_grad, int out_f64,
+                                  double* raw, double* sums, int sum_slot, int64_t B, int64_t T, int64_t K, int64_t L,
+                                  void* ws, cudaStream_t st) {
+    switch (dt) {
+        case 0: return launch_generic_t<float>(kind, x, g, out_grad, out_f64, raw, sums, sum_slot, B, T, K, L, ws, st);
+        case 1:
+            return launch_generic_t<__nv_bfloat16>(kind, x, g, out_grad, out_f64, raw, sums, sum_slot, B, T, K, L, ws,
+                                                   st);
+        case 2: return launch_generic_t<double>(kind, x, g, out_grad, out_f64, raw, sums, sum_slot, B, T, K, L, ws, st);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_linear_dx(int dt, const void* g, const void* W, void* dx, int64_t rows, int64_t K, int64_t L,
+                             cudaStream_t st) {
+    const int64_t n = rows * K;
+    const int grid = (int)((n + 255) / 256);
+    if (n == 0) return cudaSuccess;
+    switch (dt) {
+        case 0:
+            linear_dx_kernel<float, float><<<grid, 256, 0, st>>>((const float*)g, (const float*)W, (float*)dx, rows, K, L);
+            break;
+        case 1:
+            linear_dx_kernel<__nv_bfloat16, float><<<grid, 256, 0, st>>>((const __nv_bfloat16*)g, (const float*)W,
+                                                                         (__nv_bfloat16*)dx, rows, K, L);
+            break;
+        case 2:
+            linear_dx_kernel<double, double><<<grid, 256, 0, st>>>((const double*)g, (const double*)W, (double*)dx,
+                                                                   rows, K, L);
+            break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace gnsb
