@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(wg::THREADS, 1)
                     for (int kb = 0; kb < kblocks; ++kb) {
                         mbar_wait(&empty[s], ph ^ 1u);
                         unsigned char* st = ring + (size_t)s * STAGE_BYTES;
-                        mbar_expect_tx(&full[s], STAGE_BYTES);
+                        mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
                         const int t0 = kb * BK;
 #pragma unroll
                         for (int h = 0; h < BM / 64; ++h) tc::tma_load_3d(st + h * 8192, &tmx, i0 + 64 * h, t0, b, &full[s]);
