@@ -49,6 +49,10 @@ constexpr int TMEM_COLS = 512;
 struct WgradArgs {
     int B, T, K, L;
     int tiles_m, tiles_n;
+    int64_t units;         // tiles * B (tile-major, example-minor)
+    float* part;           // [tiles][max_parts][BM][BN] partial sum_b dW of split tiles
+    unsigned* ticket;      // [tiles], zero on entry and on exit
+    int max_parts;
     float* dW;     // [K, L] or null
     double* q;     // [B][tiles] per-(example, tile) ||dW_b tile||^2
     double* qbig;  // [tiles] ||dW tile||^2
@@ -70,6 +74,10 @@ __global__ void __launch_bounds__(wg::THREADS, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntiles = a.tiles_m * a.tiles_n;
     const int kblocks = a.T / BK;
+    // balanced split of the (tile, example) units: CTA c owns [u0, u1)
+    const int64_t u0 = (int64_t)blockIdx.x * a.units / gridDim.x;
+    const int64_t u1 = (int64_t)(blockIdx.x + 1) * a.units / gridDim.x;
+    auto cta_of_unit = [&](int64_t u) -> int { return (int)(((u + 1) * gridDim.x - 1) / a.units); };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -95,9 +103,10 @@ __global__ void __launch_bounds__(wg::THREADS, 1)
         if (lane == 0) {
             int s = 0;
             uint32_t ph = 0;
-            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            for (int64_t u = u0; u < u1; ++u) {
+                const int tile = (int)(u / a.B), b = (int)(u % a.B);
                 const int i0 = (tile % a.tiles_m) * BM, j0 = (tile / a.tiles_m) * BN;
-                for (int b = 0; b < a.B; ++b)
+                {
                     for (int kb = 0; kb < kblocks; ++kb) {
                         mbar_wait(&empty[s], ph ^ 1u);
                         unsigned char* st = ring + (size_t)s * STAGE_BYTES;
@@ -113,6 +122,7 @@ __global__ void __launch_bounds__(wg::THREADS, 1)
                             ph ^= 1u;
                         }
                     }
+                }
             }
         }
     } else if (warp == 1) {
@@ -121,8 +131,8 @@ __global__ void __launch_bounds__(wg::THREADS, 1)
             constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, true, true);
             int s = 0, buf = 0;
             uint32_t ph = 0, tph = 0;
-            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                for (int b = 0; b < a.B; ++b) {
+            for (int64_t u = u0; u < u1; ++u) {
+                {
                     mbar_wait(&tempty[buf], tph ^ 1u);  // epilogue drained this accumulator
                     tc::fence_after_sync();
                     const uint32_t dcol = tmem + (uint32_t)(buf * BN);
@@ -159,68 +169,108 @@ __global__ void __launch_bounds__(wg::THREADS, 1)
         const int quad = warp & 3;      // TMEM lanes this warp may access
         const int half = e / 4;         // column half of the 256-wide tile
         const int row = quad * 32 + lane;
+        unsigned* flag = reinterpret_cast<unsigned*>(red + EPI_WARPS);
         int buf = 0;
         uint32_t tph = 0;
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            const int i0 = (tile % a.tiles_m) * BM, j0 = (tile / a.tiles_m) * BN;
-            float S[128];
-#pragma unroll
-            for (int c = 0; c < 128; ++c) S[c] = 0.f;
-            for (int b = 0; b < a.B; ++b) {
-                mbar_wait(&tfull[buf], tph);
-                tc::fence_after_sync();
-                float sq = 0.f;
-                const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN + half * 128);
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    uint32_t r[32];
-                    tc::tmem_ld_32x32b_x32(base + c * 32, r);
-                    tc::tmem_ld_wait();
-#pragma unroll
-                    for (int k = 0; k < 32; ++k) {
-                        const float v = __uint_as_float(r[k]);
-                        sq = fmaf(v, v, sq);
-                        S[c * 32 + k] += v;
-                    }
-                }
-                tc::fence_before_sync();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&tempty[buf]);
-                // tile's share of raw_b: warp tree, then fixed-order sum over warps
-                sq = warp_sum(sq);
-                if (lane == 0) red[e] = sq;
-                named_bar_sync(1, EPI_WARPS * 32);
-                if (e == 0 && lane == 0) {
-                    double t = 0.0;
-#pragma unroll
-                    for (int w = 0; w < EPI_WARPS; ++w) t += (double)red[w];
-                    a.q[(size_t)b * ntiles + tile] = t;
-                }
-                named_bar_sync(1, EPI_WARPS * 32);
-                if (++buf == 2) {
-                    buf = 0;
-                    tph ^= 1u;
-                }
-            }
-            float sb = 0.f;
-#pragma unroll
-            for (int c = 0; c < 128; ++c) sb = fmaf(S[c], S[c], sb);
-            sb = warp_sum(sb);
-            if (lane == 0) red[e] = sb;
+        float S[128];
+        // fixed-order fold of per-warp float partials -> one double (thread e==0, lane 0)
+        auto fold8 = [&](float v, double* dst) {
+            v = warp_sum(v);
+            if (lane == 0) red[e] = v;
             named_bar_sync(1, EPI_WARPS * 32);
             if (e == 0 && lane == 0) {
                 double t = 0.0;
 #pragma unroll
                 for (int w = 0; w < EPI_WARPS; ++w) t += (double)red[w];
-                a.qbig[tile] = t;
+                *dst = t;
             }
             named_bar_sync(1, EPI_WARPS * 32);
+        };
+        auto store_tile = [&](int tile) {
+            const int i0 = (tile % a.tiles_m) * BM, j0 = (tile / a.tiles_m) * BN;
+            float sb = 0.f;
+#pragma unroll
+            for (int c = 0; c < 128; ++c) sb = fmaf(S[c], S[c], sb);
+            fold8(sb, &a.qbig[tile]);
             if (a.dW != nullptr) {
                 float4* dst = reinterpret_cast<float4*>(a.dW + (size_t)(i0 + row) * a.L + j0 + half * 128);
 #pragma unroll
                 for (int c = 0; c < 32; ++c) dst[c] = make_float4(S[4 * c], S[4 * c + 1], S[4 * c + 2], S[4 * c + 3]);
             }
+        };
+        // A tile whose examples are split over several CTAs: every part is
+        // parked in the workspace; the last CTA to finish (ticket) sums the
+        // parts in CTA order, so the result is deterministic.
+        auto flush_tile = [&](int tile) {
+            const int cf = cta_of_unit((int64_t)tile * a.B), cl = cta_of_unit((int64_t)(tile + 1) * a.B - 1);
+            if (cf == cl) {
+                store_tile(tile);
+                return;
+            }
+            const int nparts = cl - cf + 1, mypart = (int)blockIdx.x - cf;
+            auto slot = [&](int p) {
+                return reinterpret_cast<float4*>(a.part + (((size_t)tile * a.max_parts + p) * BM + row) * BN + half * 128);
+            };
+            float4* mine = slot(mypart);
+#pragma unroll
+            for (int c = 0; c < 32; ++c) mine[c] = make_float4(S[4 * c], S[4 * c + 1], S[4 * c + 2], S[4 * c + 3]);
+            __threadfence();
+            named_bar_sync(1, EPI_WARPS * 32);
+            if (e == 0 && lane == 0) *flag = atomicAdd(&a.ticket[tile], 1u);
+            named_bar_sync(1, EPI_WARPS * 32);
+            if (*flag != (unsigned)(nparts - 1)) return;  // not the last part: done
+            __threadfence();
+#pragma unroll
+            for (int c = 0; c < 128; ++c) S[c] = 0.f;
+            for (int p = 0; p < nparts; ++p) {
+                const float4* src = slot(p);
+#pragma unroll
+                for (int c = 0; c < 32; ++c) {
+                    const float4 v = __ldcg(src + c);
+                    S[4 * c] += v.x;
+                    S[4 * c + 1] += v.y;
+                    S[4 * c + 2] += v.z;
+                    S[4 * c + 3] += v.w;
+                }
+            }
+            if (e == 0 && lane == 0) a.ticket[tile] = 0u;
+            store_tile(tile);
+        };
+        int cur = -1;
+        for (int64_t u = u0; u < u1; ++u) {
+            const int tile = (int)(u / a.B), b = (int)(u % a.B);
+            if (tile != cur) {
+                if (cur >= 0) flush_tile(cur);
+                cur = tile;
+#pragma unroll
+                for (int c = 0; c < 128; ++c) S[c] = 0.f;
+            }
+            mbar_wait(&tfull[buf], tph);
+            tc::fence_after_sync();
+            float sq = 0.f;
+            const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN + half * 128);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                uint32_t r[32];
+                tc::tmem_ld_32x32b_x32(base + c * 32, r);
+                tc::tmem_ld_wait();
+#pragma unroll
+                for (int k = 0; k < 32; ++k) {
+                    const float v = __uint_as_float(r[k]);
+                    sq = fmaf(v, v, sq);
+                    S[c * 32 + k] += v;
+                }
+            }
+            tc::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[buf]);
+            fold8(sq, &a.q[(size_t)b * ntiles + tile]);  // the tile's share of raw_b
+            if (++buf == 2) {
+                buf = 0;
+                tph ^= 1u;
+            }
         }
+        if (cur >= 0) flush_tile(cur);
     }
     __syncthreads();
     if (warp == 1) {
@@ -291,10 +341,32 @@ bool wgrad_shape_ok(int64_t B, int64_t T, int64_t K, int64_t L) {
            T < (1 << 30) && B < (1 << 30);
 }
 
-size_t wgrad_workspace(int64_t B, int64_t K, int64_t L) {
-    const int64_t tiles = (K / wg::BM) * (L / wg::BN);
-    return (size_t)(B + 1) * tiles * sizeof(double) + 256;
+namespace {
+int wgrad_max_parts(int64_t B, int64_t tiles, int grid) {
+    const int64_t per = tiles * B / grid;  // min units per CTA
+    return per <= 0 ? (int)B : (int)((B + per - 1) / per + 1);
 }
+struct WgradLayout {
+    size_t q, qbig, ticket, part, total;
+};
+WgradLayout wgrad_layout(int64_t B, int64_t K, int64_t L, int grid) {
+    const int64_t tiles = (K / wg::BM) * (L / wg::BN);
+    WgradLayout w;
+    w.q = 0;
+    w.qbig = (size_t)B * tiles * sizeof(double);
+    w.ticket = (w.qbig + (size_t)tiles * sizeof(double) + 255) / 256 * 256;
+    w.part = (w.ticket + (size_t)tiles * sizeof(unsigned) + 255) / 256 * 256;
+    w.total = w.part + (size_t)tiles * wgrad_max_parts(B, tiles, grid) * wg::BM * wg::BN * sizeof(float);
+    return w;
+}
+int wgrad_grid(int64_t B, int64_t K, int64_t L) {
+    const int64_t units = (K / wg::BM) * (L / wg::BN) * B;
+    const int sms = device_sm_count();
+    return (int)(units < sms ? units : sms);
+}
+}  // namespace
+
+size_t wgrad_workspace(int64_t B, int64_t K, int64_t L) { return wgrad_layout(B, K, L, wgrad_grid(B, K, L)).total; }
 
 cudaError_t launch_wgrad_norms(const void* x, const void* g, float* dW, double* raw, double* sums, int64_t B,
                                int64_t T, int64_t K, int64_t L, void* ws, cudaStream_t st) {
@@ -314,10 +386,15 @@ cudaError_t launch_wgrad_norms(const void* x, const void* g, float* dW, double* 
     a.tiles_n = (int)(L / wg::BN);
     a.dW = dW;
     const int ntiles = a.tiles_m * a.tiles_n;
-    a.q = static_cast<double*>(ws);
-    a.qbig = a.q + (size_t)B * ntiles;
-    const int sms = device_sm_count();
-    const int grid = ntiles < sms ? ntiles : sms;
+    const int grid = wgrad_grid(B, K, L);
+    const WgradLayout w = wgrad_layout(B, K, L, grid);
+    unsigned char* base = static_cast<unsigned char*>(ws);
+    a.q = reinterpret_cast<double*>(base + w.q);
+    a.qbig = reinterpret_cast<double*>(base + w.qbig);
+    a.ticket = reinterpret_cast<unsigned*>(base + w.ticket);
+    a.part = reinterpret_cast<float*>(base + w.part);
+    a.units = (int64_t)ntiles * B;
+    a.max_parts = wgrad_max_parts(B, ntiles, grid);
     wgrad_norms_kernel<<<grid, wg::THREADS, wg::SMEM, st>>>(mx, mg, a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
