@@ -236,15 +236,11 @@ __global__ void __launch_bounds__(wg::THREADS, 1)
             if (e == 0 && lane == 0) a.ticket[tile] = 0u;
             store_tile(tile);
         };
-        int cur = -1;
-        for (int64_t u = u0; u < u1; ++u) {
-            const int tile = (int)(u / a.B), b = (int)(u % a.B);
-            if (tile != cur) {
-                if (cur >= 0) flush_tile(cur);
-                cur = tile;
+        // walk the units; a tile change (or the end) flushes the finished tile
+        int tile = (int)(u0 / a.B), b = (int)(u0 % a.B);
 #pragma unroll
-                for (int c = 0; c < 128; ++c) S[c] = 0.f;
-            }
+        for (int c = 0; c < 128; ++c) S[c] = 0.f;
+        for (int64_t u = u0; u < u1; ++u) {
             mbar_wait(&tfull[buf], tph);
             tc::fence_after_sync();
             float sq = 0.f;
@@ -269,8 +265,16 @@ __global__ void __launch_bounds__(wg::THREADS, 1)
                 buf = 0;
                 tph ^= 1u;
             }
+            if (++b == a.B || u + 1 == u1) {
+                flush_tile(tile);
+#pragma unroll
+                for (int c = 0; c < 128; ++c) S[c] = 0.f;
+                if (b == a.B) {
+                    b = 0;
+                    ++tile;
+                }
+            }
         }
-        if (cur >= 0) flush_tile(cur);
     }
     __syncthreads();
     if (warp == 1) {
