@@ -49,7 +49,6 @@ constexpr int TMEM_COLS = 512;
 struct WgradArgs {
     int B, T, K, L;
     int tiles_m, tiles_n;
-    int64_t units;         // tiles * B (tile-major, example-minor)
     float* part;           // [tiles][max_parts][BM][BN] partial sum_b dW of split tiles
     unsigned* ticket;      // [tiles], zero on entry and on exit
     int max_parts;
@@ -74,10 +73,29 @@ __global__ void __launch_bounds__(wg::THREADS, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntiles = a.tiles_m * a.tiles_n;
     const int kblocks = a.T / BK;
-    // balanced split of the (tile, example) units: CTA c owns [u0, u1)
-    const int64_t u0 = (int64_t)blockIdx.x * a.units / gridDim.x;
-    const int64_t u1 = (int64_t)(blockIdx.x + 1) * a.units / gridDim.x;
-    auto cta_of_unit = [&](int64_t u) -> int { return (int)(((u + 1) * gridDim.x - 1) / a.units); };
+    // Schedule (identical in every role).  Full rounds: CTA c takes tile
+    // r*grid + c with all examples, so at any moment every CTA works on the
+    // same example and X_b, G_b are shared through L2.  The remaining
+    // R = tiles % grid tiles are split into P = grid / R example ranges each.
+    const int grid = gridDim.x, c = blockIdx.x;
+    const int full_rounds = ntiles / grid, R = ntiles % grid;
+    const int P = R > 0 ? (grid / R < a.B ? grid / R : a.B) : 1;
+    const int nseg = full_rounds + ((R > 0 && c < R * P) ? 1 : 0);
+    auto segment = [&](int si, int& tile, int& b0, int& b1, int& nparts, int& part) {
+        if (si < full_rounds) {
+            tile = si * grid + c;
+            b0 = 0;
+            b1 = a.B;
+            nparts = 1;
+            part = 0;
+        } else {
+            tile = full_rounds * grid + c / P;
+            part = c % P;
+            nparts = P;
+            b0 = (int)((int64_t)a.B * part / P);
+            b1 = (int)((int64_t)a.B * (part + 1) / P);
+        }
+    };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -103,10 +121,11 @@ __global__ void __launch_bounds__(wg::THREADS, 1)
         if (lane == 0) {
             int s = 0;
             uint32_t ph = 0;
-            for (int64_t u = u0; u < u1; ++u) {
-                const int tile = (int)(u / a.B), b = (int)(u % a.B);
+            for (int si = 0; si < nseg; ++si) {
+                int tile, b0, b1, np_, pt;
+                segment(si, tile, b0, b1, np_, pt);
                 const int i0 = (tile % a.tiles_m) * BM, j0 = (tile / a.tiles_m) * BN;
-                {
+                for (int b = b0; b < b1; ++b) {
                     for (int kb = 0; kb < kblocks; ++kb) {
                         mbar_wait(&empty[s], ph ^ 1u);
                         unsigned char* st = ring + (size_t)s * STAGE_BYTES;
@@ -131,8 +150,10 @@ __global__ void __launch_bounds__(wg::THREADS, 1)
             constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, true, true);
             int s = 0, buf = 0;
             uint32_t ph = 0, tph = 0;
-            for (int64_t u = u0; u < u1; ++u) {
-                {
+            for (int si = 0; si < nseg; ++si) {
+                int tile, b0, b1, np_, pt;
+                segment(si, tile, b0, b1, np_, pt);
+                for (int b = b0; b < b1; ++b) {
                     mbar_wait(&tempty[buf], tph ^ 1u);  // epilogue drained this accumulator
                     tc::fence_after_sync();
                     const uint32_t dcol = tmem + (uint32_t)(buf * BN);
@@ -201,13 +222,11 @@ __global__ void __launch_bounds__(wg::THREADS, 1)
         // A tile whose examples are split over several CTAs: every part is
         // parked in the workspace; the last CTA to finish (ticket) sums the
         // parts in CTA order, so the result is deterministic.
-        auto flush_tile = [&](int tile) {
-            const int cf = cta_of_unit((int64_t)tile * a.B), cl = cta_of_unit((int64_t)(tile + 1) * a.B - 1);
-            if (cf == cl) {
+        auto flush_tile = [&](int tile, int nparts, int mypart) {
+            if (nparts == 1) {
                 store_tile(tile);
                 return;
             }
-            const int nparts = cl - cf + 1, mypart = (int)blockIdx.x - cf;
             auto slot = [&](int p) {
                 return reinterpret_cast<float4*>(a.part + (((size_t)tile * a.max_parts + p) * BM + row) * BN + half * 128);
             };
@@ -236,44 +255,38 @@ __global__ void __launch_bounds__(wg::THREADS, 1)
             if (e == 0 && lane == 0) a.ticket[tile] = 0u;
             store_tile(tile);
         };
-        // walk the units; a tile change (or the end) flushes the finished tile
-        int tile = (int)(u0 / a.B), b = (int)(u0 % a.B);
+        for (int si = 0; si < nseg; ++si) {
+            int tile, b0, b1, nparts, mypart;
+            segment(si, tile, b0, b1, nparts, mypart);
 #pragma unroll
-        for (int c = 0; c < 128; ++c) S[c] = 0.f;
-        for (int64_t u = u0; u < u1; ++u) {
-            mbar_wait(&tfull[buf], tph);
-            tc::fence_after_sync();
-            float sq = 0.f;
-            const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN + half * 128);
+            for (int cc = 0; cc < 128; ++cc) S[cc] = 0.f;
+            for (int b = b0; b < b1; ++b) {
+                mbar_wait(&tfull[buf], tph);
+                tc::fence_after_sync();
+                float sq = 0.f;
+                const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN + half * 128);
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                uint32_t r[32];
-                tc::tmem_ld_32x32b_x32(base + c * 32, r);
-                tc::tmem_ld_wait();
+                for (int cc = 0; cc < 4; ++cc) {
+                    uint32_t r[32];
+                    tc::tmem_ld_32x32b_x32(base + cc * 32, r);
+                    tc::tmem_ld_wait();
 #pragma unroll
-                for (int k = 0; k < 32; ++k) {
-                    const float v = __uint_as_float(r[k]);
-                    sq = fmaf(v, v, sq);
-                    S[c * 32 + k] += v;
+                    for (int k = 0; k < 32; ++k) {
+                        const float v = __uint_as_float(r[k]);
+                        sq = fmaf(v, v, sq);
+                        S[cc * 32 + k] += v;
+                    }
+                }
+                tc::fence_before_sync();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[buf]);
+                fold8(sq, &a.q[(size_t)b * ntiles + tile]);  // the tile's share of raw_b
+                if (++buf == 2) {
+                    buf = 0;
+                    tph ^= 1u;
                 }
             }
-            tc::fence_before_sync();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[buf]);
-            fold8(sq, &a.q[(size_t)b * ntiles + tile]);  // the tile's share of raw_b
-            if (++buf == 2) {
-                buf = 0;
-                tph ^= 1u;
-            }
-            if (++b == a.B || u + 1 == u1) {
-                flush_tile(tile);
-#pragma unroll
-                for (int c = 0; c < 128; ++c) S[c] = 0.f;
-                if (b == a.B) {
-                    b = 0;
-                    ++tile;
-                }
-            }
+            flush_tile(tile, nparts, mypart);
         }
     }
     __syncthreads();
@@ -347,8 +360,10 @@ bool wgrad_shape_ok(int64_t B, int64_t T, int64_t K, int64_t L) {
 
 namespace {
 int wgrad_max_parts(int64_t B, int64_t tiles, int grid) {
-    const int64_t per = tiles * B / grid;  // min units per CTA
-    return per <= 0 ? (int)B : (int)((B + per - 1) / per + 1);
+    const int64_t R = tiles % grid;
+    if (R == 0) return 1;
+    const int64_t P = grid / R;
+    return (int)(P < B ? P : B);
 }
 struct WgradLayout {
     size_t q, qbig, ticket, part, total;
@@ -368,6 +383,7 @@ int wgrad_grid(int64_t B, int64_t K, int64_t L) {
     const int sms = device_sm_count();
     return (int)(units < sms ? units : sms);
 }
+// (grid may exceed the tile count: the extra CTAs take example ranges of tiles)
 }  // namespace
 
 size_t wgrad_workspace(int64_t B, int64_t K, int64_t L) { return wgrad_layout(B, K, L, wgrad_grid(B, K, L)).total; }
@@ -397,7 +413,6 @@ cudaError_t launch_wgrad_norms(const void* x, const void* g, float* dW, double* 
     a.qbig = reinterpret_cast<double*>(base + w.qbig);
     a.ticket = reinterpret_cast<unsigned*>(base + w.ticket);
     a.part = reinterpret_cast<float*>(base + w.part);
-    a.units = (int64_t)ntiles * B;
     a.max_parts = wgrad_max_parts(B, ntiles, grid);
     wgrad_norms_kernel<<<grid, wg::THREADS, wg::SMEM, st>>>(mx, mg, a);
     cudaError_t e = cudaGetLastError();
