@@ -1,0 +1,349 @@
+// gnstk_dropin.cu — host implementation of the gnstk drop-in API
+// (include/gnstk/*.hpp) over the C ABI of include/gnsb.h.
+//
+// Value semantics like the reference: fp64 host Tensors in, fp64 host Tensors
+// out.  Each call uploads its operands, runs the B200 kernels on the current
+// device (legacy default stream), and downloads the results; argument
+// validation happens first, in the reference's order and wording
+// (proj/src/layers.cpp:13-35, gns.cpp:10-18), so error behaviour is identical.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "gnsb.h"
+#include "gnstk/costmodel.hpp"
+#include "gnstk/gns.hpp"
+#include "gnstk/layers.hpp"
+#include "gnstk/tensor.hpp"
+
+namespace gnstk {
+
+// ---------------------------------------------------------------- Tensor --
+namespace {
+std::size_t numel(const Shape& s) {
+    std::size_t n = 1;
+    for (Index e : s) {
+        if (e < 0) throw std::invalid_argument("tensor: negative extent");
+        n *= static_cast<std::size_t>(e);
+    }
+    return n;
+}
+}  // namespace
+
+Tensor::Tensor(Shape shape) : shape_(std::move(shape)), data_(numel(shape_), 0.0) {}
+Tensor::Tensor(Shape shape, std::vector<double> data) : shape_(std::move(shape)), data_(std::move(data)) {
+    if (data_.size() != numel(shape_)) throw std::invalid_argument("tensor: data size does not match shape");
+}
+Tensor Tensor::scalar(double v) { return Tensor(Shape{}, std::vector<double>{v}); }
+Tensor Tensor::full(Shape shape, double v) {
+    Tensor t(std::move(shape));
+    for (auto& x : t.data_) x = v;
+    return t;
+}
+double Tensor::item() const {
+    if (data_.size() != 1) throw std::invalid_argument("tensor: item() needs exactly one element");
+    return data_[0];
+}
+Tensor scale(const Tensor& a, double c) {
+    Tensor r(a.shape());
+    for (Index i = 0; i < a.size(); ++i) r[i] = a[i] * c;
+    return r;
+}
+double sum_all(const Tensor& a) {
+    double s = 0.0;
+    for (Index i = 0; i < a.size(); ++i) s += a[i];
+    return s;
+}
+double sqnorm_all(const Tensor& a) {
+    double s = 0.0;
+    for (Index i = 0; i < a.size(); ++i) s += a[i] * a[i];
+    return s;
+}
+
+// ------------------------------------------------------- device plumbing --
+namespace {
+
+[[noreturn]] void fail(const std::string& msg) { throw std::invalid_argument("layers: " + msg); }
+
+void check(gnsb_status s) {
+    if (s == GNSB_OK) return;
+    if (s == GNSB_EINVAL) throw std::invalid_argument(gnsb_last_error());
+    throw std::runtime_error(gnsb_last_error());
+}
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string("cuda: ") + what + ": " + cudaGetErrorString(e));
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    explicit DevBuf(std::size_t bytes, bool zero = false) {
+        if (bytes) {
+            cuda_check(cudaMalloc(&p, bytes), "cudaMalloc");
+            if (zero) cuda_check(cudaMemset(p, 0, bytes), "cudaMemset");
+        }
+    }
+    DevBuf(DevBuf&& o) noexcept : p(o.p) { o.p = nullptr; }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+DevBuf upload(const Tensor& t) {
+    DevBuf d(sizeof(double) * static_cast<std::size_t>(t.size()));
+    if (t.size()) cuda_check(cudaMemcpy(d.p, t.data(), sizeof(double) * t.size(), cudaMemcpyHostToDevice), "upload");
+    return d;
+}
+void download(Tensor& t, const DevBuf& d) {
+    if (t.size()) cuda_check(cudaMemcpy(t.data(), d.p, sizeof(double) * t.size(), cudaMemcpyDeviceToHost), "download");
+}
+void download(double* dst, const DevBuf& d, std::size_t n) {
+    if (n) cuda_check(cudaMemcpy(dst, d.p, sizeof(double) * n, cudaMemcpyDeviceToHost), "download");
+}
+
+// (B, M, K) view of a rank >= 2 tensor (layers.cpp:19-28)
+struct Bmk {
+    Index b, m, k;
+};
+Bmk bmk_view(const Tensor& t) {
+    if (t.rank() < 2) fail("expected rank >= 2");
+    Index m = 1;
+    for (Index d = 1; d + 1 < t.rank(); ++d) m *= t.shape()[static_cast<std::size_t>(d)];
+    return {t.shape().front(), m, t.shape().back()};
+}
+void check_same_leading(const Tensor& x, const Tensor& g) {
+    if (x.rank() != g.rank()) fail("x and g rank mismatch");
+    for (Index d = 0; d + 1 < x.rank(); ++d)
+        if (x.shape()[static_cast<std::size_t>(d)] != g.shape()[static_cast<std::size_t>(d)])
+            fail("x and g leading shape mismatch");
+}
+double corrected(double sum_sq, Index batch) {  // layers.cpp:39-42
+    const double b = static_cast<double>(batch);
+    return sum_sq / b * (b * b);
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------- layers --
+LayerNormForwardResult layernorm_forward(const LayerNormLayer& layer, const Tensor& x) {
+    const Index k = layer.gamma.shape().empty() ? 0 : layer.gamma.shape()[0];
+    if (layer.beta.shape() != Shape{k}) fail("gamma/beta extent mismatch");
+    if (layer.epsilon <= 0.0) fail("epsilon must be positive");
+    if (x.rank() < 1 || x.shape().back() != k) fail("input trailing extent does not match gamma");
+    if (k < 2) fail("layernorm needs trailing extent >= 2");
+    Index rows = 1;
+    for (Index d = 0; d + 1 < x.rank(); ++d) rows *= x.shape()[static_cast<std::size_t>(d)];
+
+    LayerNormForwardResult res;
+    res.output = Tensor(x.shape());
+    res.cache.normalized = Tensor(x.shape());
+    res.cache.inv_std = Tensor(Shape(x.shape().begin(), x.shape().end() - 1));
+    if (rows == 0) return res;
+    DevBuf dx = upload(x), dg = upload(layer.gamma), db = upload(layer.beta);
+    DevBuf dy(sizeof(double) * x.size()), dxh(sizeof(double) * x.size()), dr(sizeof(double) * rows);
+    check(gnsb_ln_fwd(dx.p, dg.p, db.p, dy.p, nullptr, dr.p, dxh.p, rows, k, layer.epsilon, GNSB_F64, nullptr));
+    download(res.output, dy);
+    download(res.cache.normalized, dxh);
+    download(res.cache.inv_std, dr);
+    return res;
+}
+
+LayerNormBackwardResult layernorm_backward_simultaneous(const LayerNormLayer& layer, const LayerNormCache& cache,
+                                                        const Tensor& g) {
+    const Index k = layer.gamma.shape().empty() ? 0 : layer.gamma.shape()[0];
+    if (!cache.normalized.same_shape(g)) fail("cache/gradient shape mismatch");
+    if (g.rank() < 2) fail("backward expects a leading batch axis");
+    const Bmk v = bmk_view(g);
+    if (v.k != k) fail("gradient trailing extent does not match gamma");
+    if (v.b == 0) fail("empty batch");
+
+    LayerNormBackwardResult res;
+    res.grads.batch_size = v.b;
+    Tensor dgamma({k}), dbeta({k}), rg({v.b}), rb({v.b});
+    res.input_grad = Tensor(g.shape());
+    double sums[4] = {0, 0, 0, 0};
+    DevBuf dxh = upload(cache.normalized), dinv = upload(cache.inv_std), dgr = upload(g), dgam = upload(layer.gamma);
+    DevBuf ddx(sizeof(double) * g.size()), ddg(sizeof(double) * k), ddb(sizeof(double) * k);
+    DevBuf drg(sizeof(double) * v.b), drb(sizeof(double) * v.b), dsums(sizeof(double) * 4, true);
+    std::size_t wsb = 0;
+    check(gnsb_ln_bwd_workspace_size(v.b, v.m, k, GNSB_F64, &wsb));
+    DevBuf ws(wsb, true);
+    check(gnsb_ln_bwd(dxh.p, nullptr, dinv.p, dgr.p, dgam.p, ddx.p, ddg.p, ddb.p, drg.as<double>(), drb.as<double>(),
+                      dsums.as<double>(), 1, v.b, v.m, k, GNSB_F64, ws.p, wsb, nullptr));
+    download(res.input_grad, ddx);
+    download(dgamma, ddg);
+    download(dbeta, ddb);
+    download(rg, drg);
+    download(rb, drb);
+    download(sums, dsums, 4);
+    res.grads.weight_grads["gamma"] = std::move(dgamma);
+    res.grads.weight_grads["beta"] = std::move(dbeta);
+    res.grads.per_example_sqnorms["gamma"] = corrected(sums[0], v.b);
+    res.grads.per_example_sqnorms["beta"] = corrected(sums[1], v.b);
+    res.grads.per_example_sqnorms_raw["gamma"] = std::move(rg);
+    res.grads.per_example_sqnorms_raw["beta"] = std::move(rb);
+    return res;
+}
+
+LinearBackwardResult linear_backward_simultaneous(const LinearLayer& layer, const Tensor& x, const Tensor& g) {
+    const Index k = layer.weight.rank() == 2 ? layer.weight.shape()[0] : 0;
+    const Index l = layer.weight.rank() == 2 ? layer.weight.shape()[1] : 0;
+    check_same_leading(x, g);
+    const Bmk vx = bmk_view(x), vg = bmk_view(g);
+    if (vx.k != k) fail("input trailing extent does not match weight rows");
+    if (vg.k != l) fail("gradient trailing extent does not match weight columns");
+    if (vx.b == 0) fail("empty batch");
+
+    LinearBackwardResult res;
+    res.grads.batch_size = vx.b;
+    Tensor dW({k, l}), rw({vx.b});
+    double sums[4] = {0, 0, 0, 0};
+    DevBuf dx = upload(x), dg = upload(g), dWt = upload(layer.weight);
+    DevBuf ddW(sizeof(double) * k * l), drw(sizeof(double) * vx.b), dsums(sizeof(double) * 4, true);
+    std::size_t wsb = 0, wsb2 = 0;
+    check(gnsb_linear_pe_workspace_size(vx.b, vx.m, k, l, GNSB_F64, &wsb));
+    check(gnsb_linear_pe_workspace_size(vx.b, vx.m, 1, l, GNSB_F64, &wsb2));
+    DevBuf ws(wsb > wsb2 ? wsb : wsb2, true);
+    check(gnsb_linear_pe_norms(dx.p, dg.p, ddW.p, drw.as<double>(), dsums.as<double>(), vx.b, vx.m, k, l, 1, GNSB_F64,
+                               ws.p, wsb > wsb2 ? wsb : wsb2, nullptr));
+    download(dW, ddW);
+    download(rw, drw);
+    if (layer.bias) {
+        if (layer.bias->shape() != Shape{l}) fail("bias extent does not match weight columns");
+        Tensor db({l}), rb({vx.b});
+        DevBuf ddb(sizeof(double) * l), drb(sizeof(double) * vx.b);
+        check(gnsb_linear_bias_pe(dg.p, ddb.p, drb.as<double>(), dsums.as<double>(), vx.b, vx.m, l, GNSB_F64, ws.p,
+                                  wsb > wsb2 ? wsb : wsb2, nullptr));
+        download(db, ddb);
+        download(rb, drb);
+        res.grads.weight_grads["bias"] = std::move(db);
+        res.grads.per_example_sqnorms_raw["bias"] = std::move(rb);
+    }
+    download(sums, dsums, 4);
+    res.grads.weight_grads["weight"] = std::move(dW);
+    res.grads.per_example_sqnorms["weight"] = corrected(sums[0], vx.b);
+    res.grads.per_example_sqnorms_raw["weight"] = std::move(rw);
+    if (layer.bias) res.grads.per_example_sqnorms["bias"] = corrected(sums[1], vx.b);
+    res.input_grad = Tensor(x.shape());
+    DevBuf ddx(sizeof(double) * x.size());
+    check(gnsb_linear_dx(dg.p, dWt.p, ddx.p, vx.b * vx.m, k, l, GNSB_F64, nullptr));
+    download(res.input_grad, ddx);
+    return res;
+}
+
+Tensor linear_perexample_sqnorm_frobenius(const Tensor& x, const Tensor& g) {
+    if (x.rank() != 3 || g.rank() != 3) fail("frobenius path expects strictly 3-axis inputs");
+    if (x.shape()[0] != g.shape()[0] || x.shape()[1] != g.shape()[1]) fail("x and g leading shape mismatch");
+    const Index b = x.shape()[0], t = x.shape()[1], k = x.shape()[2], l = g.shape()[2];
+    Tensor out({b});
+    if (b == 0) return out;
+    if (k == 0 || l == 0 || t == 0) return out;  // empty contractions: zero norms
+    DevBuf dx = upload(x), dg = upload(g), dout(sizeof(double) * b);
+    std::size_t wsb = 0;
+    check(gnsb_linear_pe_workspace_size(b, t, k, l, GNSB_F64, &wsb));
+    DevBuf ws(wsb, true);
+    check(gnsb_linear_pe_norms(dx.p, dg.p, nullptr, dout.as<double>(), nullptr, b, t, k, l, 2, GNSB_F64, ws.p, wsb,
+                               nullptr));
+    download(out, dout);
+    return out;
+}
+
+// -------------------------------------------------------------------- gns --
+namespace {
+gnsb_grad_stats to_c(const GradStats& s) {
+    return gnsb_grad_stats{s.g_big_sqnorm, s.g_small_sqnorm_mean, s.b_big, s.b_small, s.n_small};
+}
+}  // namespace
+
+std::string layer_type_name(LayerType t) {
+    switch (t) {
+        case LayerType::Embedding: return "embedding";
+        case LayerType::Linear: return "linear";
+        case LayerType::LayerNorm: return "layernorm";
+    }
+    throw std::invalid_argument("gns: unknown layer type");
+}
+
+double estimate_g2(const GradStats& stats) {
+    const gnsb_grad_stats c = to_c(stats);
+    double out = 0.0;
+    check(gnsb_estimate_g2(&c, &out));
+    return out;
+}
+
+double estimate_s(const GradStats& stats) {
+    const gnsb_grad_stats c = to_c(stats);
+    double out = 0.0;
+    check(gnsb_estimate_s(&c, &out));
+    return out;
+}
+
+GnsEstimate make_gns_estimate(double g2, double s) {
+    gnsb_gns_estimate e;
+    gnsb_make_gns_estimate(g2, s, &e);
+    return GnsEstimate{e.g2, e.s, e.b_simple, e.b_simple_defined != 0};
+}
+
+EmaState ema_update(EmaState state, double x) {
+    gnsb_ema_state c{state.alpha, state.value, state.count};
+    check(gnsb_ema_update(&c, x));
+    return EmaState{c.alpha, c.value, c.count};
+}
+
+GnsEstimate smoothed_gns(const EmaState& g2_ema, const EmaState& s_ema) {
+    const gnsb_ema_state a{g2_ema.alpha, g2_ema.value, g2_ema.count}, b{s_ema.alpha, s_ema.value, s_ema.count};
+    gnsb_gns_estimate e;
+    check(gnsb_smoothed_gns(&a, &b, &e));
+    return GnsEstimate{e.g2, e.s, e.b_simple, e.b_simple_defined != 0};
+}
+
+GradStats aggregate(const std::map<LayerKey, GradStats>& stats_by_layer, std::optional<LayerType> group) {
+    std::vector<gnsb_grad_stats> st;
+    std::vector<int32_t> ty;
+    for (const auto& [key, s] : stats_by_layer) {  // std::map: LayerKey order, like the reference
+        st.push_back(to_c(s));
+        ty.push_back(static_cast<int32_t>(key.type));
+    }
+    gnsb_grad_stats out{};
+    check(gnsb_aggregate(st.data(), ty.data(), static_cast<int32_t>(st.size()),
+                         group ? static_cast<int32_t>(*group) : -1, &out));
+    return GradStats{out.g_big_sqnorm, out.g_small_sqnorm_mean, out.b_big, out.b_small, out.n_small};
+}
+
+// -------------------------------------------------------------- costmodel --
+std::string cost_method_name(CostMethod m) { return m == CostMethod::Simultaneous ? "simultaneous" : "frobenius"; }
+
+CostPair flops(const CostShape& s, CostMethod m) {
+    int64_t out[2];
+    check(gnsb_flops(s.b, s.t, s.k, s.l, m == CostMethod::Simultaneous ? 0 : 1, out));
+    return CostPair{out[0], out[1]};
+}
+
+CostPair io_values(const CostShape& s, CostMethod m) {
+    int64_t out[2];
+    check(gnsb_io_values(s.b, s.t, s.k, s.l, m == CostMethod::Simultaneous ? 0 : 1, out));
+    return CostPair{out[0], out[1]};
+}
+
+CostPair io_bytes(const CostShape& s, CostMethod m) {
+    if (s.bytes_per_value < 1) throw std::invalid_argument("costmodel: bytes_per_value must be positive");
+    const CostPair v = io_values(s, m);
+    return CostPair{v.weight_grad * s.bytes_per_value, v.grad_norms * s.bytes_per_value};
+}
+
+double crossover_t(std::int64_t k, std::int64_t l, CostCriterion c) {
+    double out = 0.0;
+    check(gnsb_crossover_t(k, l, c == CostCriterion::IO ? 0 : 1, &out));
+    return out;
+}
+
+}  // namespace gnstk

@@ -147,3 +147,15 @@ def test_compute_entry_points_fail_loudly_without_gpu():
     assert h.gnsb_ln_bwd(None, None, None, None, None, None, None, None, None, None, None, 1, 0, 4, 8, 0, None, 0,
                          None) == _lib.GNSB_EINVAL
     assert _lib.last_error() == "layers: empty batch"
+
+
+@pytest.mark.gpu
+def test_cpp_dropin_suite():
+    """The C++ drop-in (include/gnstk/*.hpp) against the reference unit-test expectations."""
+    import subprocess
+
+    exe = os.path.join(ROOT, "tests", "cpp", "test_dropin")
+    assert os.path.exists(exe), "build the C++ drop-in test first (make cpptest)"
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert " 0 failed" in r.stdout
