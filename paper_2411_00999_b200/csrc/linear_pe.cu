@@ -414,6 +414,12 @@ cudaError_t launch_wgrad_norms(const void* x, const void* g, float* dW, double* 
     a.ticket = reinterpret_cast<unsigned*>(base + w.ticket);
     a.part = reinterpret_cast<float*>(base + w.part);
     a.max_parts = wgrad_max_parts(B, ntiles, grid);
+    // the split-tile tickets must start at zero; the workspace may have been
+    // used by another linear-path kernel with a different layout since
+    if (a.max_parts > 1) {
+        cudaError_t me = cudaMemsetAsync(a.ticket, 0, (size_t)ntiles * sizeof(unsigned), st);
+        if (me != cudaSuccess) return me;
+    }
     wgrad_norms_kernel<<<grid, wg::THREADS, wg::SMEM, st>>>(mx, mg, a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -103,8 +103,10 @@ class _Workspace:
         self._bufs = {}
         self._lock = threading.Lock()
 
-    def get(self, device: torch.device, nbytes: int) -> torch.Tensor:
-        key = (device.index, torch.cuda.current_stream(device).cuda_stream)
+    def get(self, device: torch.device, nbytes: int, op: str = "ln") -> torch.Tensor:
+        # one buffer per (op, device, stream): the ops lay out their counters
+        # differently, so a buffer is never shared between them
+        key = (op, device.index, torch.cuda.current_stream(device).cuda_stream)
         with self._lock:
             buf = self._bufs.get(key)
             if buf is None or buf.numel() < nbytes:

@@ -81,7 +81,7 @@ def linear_backward_simultaneous(layer: LinearLayer, x: torch.Tensor, g: torch.T
     raw_w = torch.empty(B, dtype=torch.float64, device=dev)
     sums = torch.zeros(4, dtype=torch.float64, device=dev)
     nbytes = _workspace_bytes(B, M, K, L, dt)
-    ws = _WS.get(dev, nbytes)
+    ws = _WS.get(dev, nbytes, "linear")
     h = _lib.lib()
     sp = _stream_ptr(dev)
     _lib.check(h.gnsb_linear_pe_norms(_ptr(x), _ptr(g), _ptr(dW), _ptr(raw_w), _ptr(sums), B, M, K, L, FORMS[form],
@@ -93,7 +93,7 @@ def linear_backward_simultaneous(layer: LinearLayer, x: torch.Tensor, g: torch.T
     if layer.bias is not None:
         db = torch.empty(L, dtype=sd, device=dev)
         raw_b = torch.empty(B, dtype=torch.float64, device=dev)
-        ws2 = _WS.get(dev, max(nbytes, _workspace_bytes(B, M, 1, L, dt)))
+        ws2 = _WS.get(dev, _workspace_bytes(B, M, 1, L, dt), "linear_bias")
         _lib.check(h.gnsb_linear_bias_pe(_ptr(g), _ptr(db), _ptr(raw_b), _ptr(sums), B, M, L, dt, _ptr(ws2),
                                          ws2.numel(), sp))
         weight_grads["bias"] = db
@@ -120,7 +120,7 @@ def linear_perexample_sqnorm_frobenius(x: torch.Tensor, g: torch.Tensor) -> torc
     if B == 0:
         return out
     dt = gnsb_dtype(x.dtype)
-    ws = _WS.get(x.device, _workspace_bytes(B, T, K, L, dt))
+    ws = _WS.get(x.device, _workspace_bytes(B, T, K, L, dt), "linear")
     _lib.check(_lib.lib().gnsb_linear_pe_norms(_ptr(x.contiguous()), _ptr(g.contiguous()), None, _ptr(out), None, B, T,
                                                K, L, 2, dt, _ptr(ws), ws.numel(), _stream_ptr(x.device)))
     return out
