@@ -4,8 +4,8 @@
 Workload (BASELINE.json configs[1]): LayerNorm backward + per-example
 ||dgamma_b||^2, ||dbeta_b||^2 over the sweep D in {768, 1024, 2048, 4096, 8192},
 B=32 T=1024 per GPU, bf16 rows / fp32 accumulation.  One "step" = one fused
-backward per D of the sweep (plus, for N > 1, the NCCL all-reduce of each
-layer's packed {dgamma, dbeta, sum raw norms}).  Inputs are synthetic
+backward per D of the sweep (plus, for N > 1, the NCCL all-reduce of the
+sweep's [dgamma | dbeta] bucket and fp64 norm-record bucket).  Inputs are synthetic
 (SURVEY §8(d) recipe, generated on the device; identical to the oracle's).
 
 value      = sum over ranks and D of algorithmic bytes / max-over-ranks device time
@@ -154,9 +154,10 @@ def run_reference_arm(args):
 
 # ----------------------------------------------------------------------------- our arm
 class LnCase:
-    """Device buffers + raw C-ABI argument tuples for one D of the sweep."""
+    """Device buffers + raw C-ABI argument tuples for one D of the sweep.
+    dgamma/dbeta/sums are views into the step's exchange buckets (sharded.py)."""
 
-    def __init__(self, m, lib, D, B, rank, dev, torch):
+    def __init__(self, m, lib, D, B, rank, dev, torch, buckets, l):
         self.D, self.B = D, B
         bf = torch.bfloat16
         self.x, self.dy, self.gamma, self.beta = m.synth_ln(B, T, D, bf, dev, b_offset=rank * B, B_div=B)
@@ -164,11 +165,8 @@ class LnCase:
         f = m.layernorm_forward(layer, self.x)
         self.mean, self.rstd = f.cache.mean, f.cache.inv_std
         self.dx = torch.empty_like(self.x)
-        # packed all-reduce buffers: [dgamma | dbeta] fp32 and the fp64 norm record
-        # {sum raw_gamma, sum raw_beta, ||dgamma||^2, ||dbeta||^2}
-        self.pack = torch.zeros(2 * D, dtype=torch.float32, device=dev)
-        self.dgamma, self.dbeta = self.pack[:D], self.pack[D:2 * D]
-        self.sums = torch.zeros(4, dtype=torch.float64, device=dev)
+        self.dgamma, self.dbeta = buckets.grad(l)
+        self.sums = buckets.record(l)
         self.raw_g = torch.zeros(B, dtype=torch.float64, device=dev)
         self.raw_b = torch.zeros(B, dtype=torch.float64, device=dev)
         nbytes = m.layers.ctypes_size(B, T, D, 1)
@@ -176,12 +174,6 @@ class LnCase:
         self.lib = lib
         self.bytes = alg_bytes(B, T, D)
         self.bytes_plain = alg_bytes(B, T, D, norms=False)
-
-    def post_reduce_norms(self, stream_ptr):
-        for i, v in ((2, self.dgamma), (3, self.dbeta)):
-            rc = self.lib.gnsb_sqnorm(v.data_ptr(), v.numel(), 0, self.sums[i:].data_ptr(), stream_ptr)
-            if rc:
-                raise RuntimeError(self.lib.gnsb_last_error().decode())
 
     def run(self, norms, stream_ptr):
         p = lambda t: t.data_ptr()
@@ -200,6 +192,7 @@ def run_ours(args):
 
     import paper_2411_00999_b200 as m
     from paper_2411_00999_b200 import _lib
+    from paper_2411_00999_b200.sharded import GradBuckets
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -214,22 +207,21 @@ def run_ours(args):
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
     sweep = args.d_list
-    cases = [LnCase(m, lib, D, B_LOCAL, rank, dev, torch) for D in sweep]
+    buckets = GradBuckets(sweep, dev)
+    cases = [LnCase(m, lib, D, B_LOCAL, rank, dev, torch, buckets, l) for l, D in enumerate(sweep)]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     torch.cuda.synchronize()
 
     def run_step(norms, with_collective):
         """One step: the fused (or plain) LN backward for every D of the sweep,
-        plus for N > 1 each layer's all-reduce of its packed gradients/norm sums."""
+        plus for N > 1 the all-reduce of the two exchange buckets (all layers'
+        [dgamma | dbeta] fp32 and their fp64 norm records) and the re-formed
+        ||G_big||^2 of the reduced gradients."""
         sp_now = torch.cuda.current_stream(dev).cuda_stream
         for c in cases:
             c.run(norms, sp_now)
-            if with_collective and world > 1:
-                # only the batch-summed gradients and the scalar norm sums cross NVLink;
-                # ||G_big||^2 is re-formed from the REDUCED gradients (SURVEY §8(e))
-                dist.all_reduce(c.pack)
-                dist.all_reduce(c.sums)
-                c.post_reduce_norms(sp_now)
+        if with_collective and world > 1:
+            buckets.reduce()
 
     def timed(case, norms):
         """Single kernel, cold: L2 flushed (256 MiB write) before, CUDA events around."""
@@ -346,6 +338,11 @@ def run_ours(args):
     if rank == 0 and not args.no_cpu:
         cpu = cpu_baseline(args)
 
+    extra = {}
+    if rank == 0 and not args.no_extra:
+        extra["cfg3_linear"] = run_cfg3(m, lib, dev, torch, np)
+        extra["cfg4_gns"] = run_cfg4(m, lib, dev, torch, np)
+
     traffic = load_traffic()
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
@@ -360,16 +357,126 @@ def run_ours(args):
         "step_ms_fused": step_f, "step_ms_plain": step_p,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "peak_kind": peak_kind, "frac_of_8TBps": achieved / 8000.0, "traffic": traffic,
-                     "kernel": "ln_bwd_kernel<bf16,...,HAS_MEAN=1,NORMS=1> (5 launches per step, one per D)",
+                     "kernel": "ln_bwd_kernel<bf16,...,HAS_MEAN=1> + ln_bwd_reduce_kernel<float,NORMS=1> (one pair per D, 5 per step)",
                      "achieved_def": "algorithmic bytes of the 5 launches / median graph-replayed step time"},
-        "sweep": sweep_rows, "e2e": e2e, "cpu_baseline": cpu,
-        "gpu_launches": len(cases) * args.steps * (3 if world > 1 else 1), "clocks": clk.summary(),
+        "sweep": sweep_rows, "e2e": e2e, "cpu_baseline": cpu, **extra,
+        "gpu_launches": len(cases) * args.steps * (4 if world > 1 else 2), "clocks": clk.summary(),
     }
     if rank == 0:
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def time_graph(fn, torch, np, dev, reps=10, warm=3):
+    """Median device time (ms) of fn() replayed as one CUDA graph (events on the
+    capturing stream)."""
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(side):
+        for _ in range(warm):
+            fn()
+    torch.cuda.current_stream(dev).wait_stream(side)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    for _ in range(warm):
+        g.replay()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts))
+
+
+def run_cfg3(m, lib, dev, torch, np):
+    """BASELINE config 3: per-example linear-layer norms, B=16 T=2048 K=L=4096 bf16,
+    both forms on tcgen05 (weight-grad form also writes dW)."""
+    import ctypes
+
+    B, T_, K, L = 16, 2048, 4096, 4096
+    x, g = m.synth_linear(B, T_, K, L, torch.bfloat16, dev)
+    dW = torch.empty(K, L, device=dev)
+    raw = torch.empty(B, dtype=torch.float64, device=dev)
+    sums = torch.zeros(4, dtype=torch.float64, device=dev)
+    n = ctypes.c_size_t()
+    lib.gnsb_linear_pe_workspace_size(B, T_, K, L, 1, ctypes.byref(n))
+    ws = torch.zeros(n.value, dtype=torch.uint8, device=dev)
+    out = {"workload": "cfg3: per-example linear norms B=16 T=2048 K=L=4096 bf16 (fp32 accumulate)"}
+    peak = 1695.1
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peak = float(json.load(f)["bf16_tflops"])
+    except Exception:
+        pass
+    for form, name in ((1, "weight_grad"), (2, "gram")):
+        def fn(form=form):
+            sp = torch.cuda.current_stream(dev).cuda_stream
+            rc = lib.gnsb_linear_pe_norms(x.data_ptr(), g.data_ptr(), dW.data_ptr() if form == 1 else None,
+                                          raw.data_ptr(), sums.data_ptr(), B, T_, K, L, form, 1, ws.data_ptr(),
+                                          ws.numel(), sp)
+            if rc:
+                raise RuntimeError(lib.gnsb_last_error().decode())
+        ms = time_graph(fn, torch, np, dev)
+        # algorithmic FLOPs: weight-grad 2BTKL; Gram (symmetric, i <= j tile pairs) B*T*(T+128)*(K+L)
+        fl = 2.0 * B * T_ * K * L if form == 1 else 1.0 * B * T_ * (T_ + 128) * (K + L)
+        out[name] = {"us": ms * 1e3, "TFLOPs": fl / (ms * 1e-3) / 1e12, "frac_of_bf16_peak": fl / (ms * 1e-3) / 1e12 / peak,
+                     "flops": fl}
+    out["faster_form"] = min(("weight_grad", "gram"), key=lambda k: out[k]["us"])
+    del x, g, dW, ws
+    torch.cuda.empty_cache()
+    return out
+
+
+def run_cfg4(m, lib, dev, torch, np):
+    """BASELINE config 4: full GNS estimate over all 25 LayerNorms of a 12-layer
+    D=768 transformer backward, B=64 T=1024 bf16: 25 fused LN backwards writing
+    their records, then the device GNS step, one CUDA graph."""
+    from paper_2411_00999_b200.gns import DeviceGnsAccumulator
+    from paper_2411_00999_b200.sharded import GradBuckets
+
+    NL, B, T_, D = 25, 64, 1024, 768
+    bk = GradBuckets([D] * NL, dev)
+    cases = []
+    for l in range(NL):
+        x, dy, gamma, beta = m.synth_ln(B, T_, D, torch.bfloat16, dev, sigma=3.0, stream0=16 * l)
+        gamma.fill_(1.0)
+        beta.zero_()
+        f = m.layernorm_forward(m.LayerNormLayer(gamma, beta), x)
+        dx = torch.empty_like(x)
+        ws = torch.zeros(m.layers.ctypes_size(B, T_, D, 1), dtype=torch.uint8, device=dev)
+        raw = torch.zeros(2, B, dtype=torch.float64, device=dev)
+        cases.append((x, f.cache.mean, f.cache.inv_std, dy, gamma, dx, ws, raw))
+    acc = DeviceGnsAccumulator(["layernorm"] * NL, 0.5, dev)
+
+    def fn():
+        sp = torch.cuda.current_stream(dev).cuda_stream
+        for l, (x, mean, rstd, dy, gamma, dx, ws, raw) in enumerate(cases):
+            dg, db = bk.grad(l)
+            rc = lib.gnsb_ln_bwd(x.data_ptr(), mean.data_ptr(), rstd.data_ptr(), dy.data_ptr(), gamma.data_ptr(),
+                                 dx.data_ptr(), dg.data_ptr(), db.data_ptr(), raw[0].data_ptr(), raw[1].data_ptr(),
+                                 bk.record(l).data_ptr(), 1, B, T_, D, 1, ws.data_ptr(), ws.numel(), sp)
+            if rc:
+                raise RuntimeError(lib.gnsb_last_error().decode())
+        acc.step(bk.records, B)
+
+    ms = time_graph(fn, torch, np, dev)
+    nbytes = NL * alg_bytes(B, T_, D)
+    groups = acc.groups.cpu().numpy()
+    out = {"workload": "cfg4: GNS over 25 LayerNorms, B=64 T=1024 D=768 bf16, sigma=3 (synthetic)",
+           "ms_per_step": ms, "GBps": nbytes / (ms * 1e-3) / 1e9, "alg_bytes": nbytes,
+           "gns_total": {"g2": float(groups[0, 0]), "s": float(groups[0, 1]), "b_simple_ema": float(groups[0, 2])},
+           "launches_per_step": 2 * NL + 1}
+    del cases
+    torch.cuda.empty_cache()
+    return out
 
 
 def run_e2e(args, m, lib, cases, dev, stream, torch, np):
@@ -380,14 +487,15 @@ def run_e2e(args, m, lib, cases, dev, stream, torch, np):
         h = {
             "x": c.x.cpu().pin_memory(), "dy": c.dy.cpu().pin_memory(), "mean": c.mean.cpu().pin_memory(),
             "rstd": c.rstd.cpu().pin_memory(), "dx": torch.empty(c.dx.shape, dtype=c.dx.dtype).pin_memory(),
-            "pack": torch.empty(c.pack.shape, dtype=c.pack.dtype).pin_memory(),
+            "dgamma": torch.empty(c.D, dtype=torch.float32).pin_memory(),
+            "dbeta": torch.empty(c.D, dtype=torch.float32).pin_memory(),
             "sums": torch.empty(4, dtype=torch.float64).pin_memory(),
             "raw_g": torch.empty(c.B, dtype=torch.float64).pin_memory(),
             "raw_b": torch.empty(c.B, dtype=torch.float64).pin_memory(),
         }
         host.append(h)
     h2d = sum(h["x"].numel() * 2 + h["dy"].numel() * 2 + h["mean"].numel() * 4 + h["rstd"].numel() * 4 for h in host)
-    d2h = sum(h["dx"].numel() * 2 + h["pack"].numel() * 4 + 32 + 16 * c.B for h, c in zip(host, cases))
+    d2h = sum(h["dx"].numel() * 2 + 2 * c.D * 4 + 32 + 16 * c.B for h, c in zip(host, cases))
 
     def step():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -399,7 +507,8 @@ def run_e2e(args, m, lib, cases, dev, stream, torch, np):
             c.rstd.copy_(h["rstd"], non_blocking=True)
             c.run(True, sp)
             h["dx"].copy_(c.dx, non_blocking=True)
-            h["pack"].copy_(c.pack, non_blocking=True)
+            h["dgamma"].copy_(c.dgamma, non_blocking=True)
+            h["dbeta"].copy_(c.dbeta, non_blocking=True)
             h["sums"].copy_(c.sums, non_blocking=True)
             h["raw_g"].copy_(c.raw_g, non_blocking=True)
             h["raw_b"].copy_(c.raw_b, non_blocking=True)
@@ -454,6 +563,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--d-list", type=lambda s: [int(v) for v in s.split(",")], default=SWEEP_D)
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--no-extra", action="store_true", help="skip the config-3/4 side measurements")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -19,26 +19,24 @@ using bf = __nv_bfloat16;
     X(0, 8, 2, 1, 2, true, 1) \
     X(1, 16, 1, 1, 2, true, 1) \
     X(2, 16, 2, 1, 1, true, 1) \
-    X(3, 16, 1, 1, 4, true, 1) \
-    X(4, 8, 2, 1, 4, true, 0) \
     X(5, 8, 1, 2, 2, true, 1) \
     X(6, 4, 2, 3, 1, true, 1) \
-    X(7, 8, 1, 2, 4, true, 1) \
-    X(8, 4, 2, 3, 2, true, 1) \
-    X(9, 16, 1, 1, 1, true, 1) \
     X(10, 4, 1, 4, 2, true, 1) \
-    X(11, 4, 1, 4, 4, true, 1) \
     X(12, 4, 1, 3, 4, true, 1) \
     X(13, 4, 1, 3, 2, true, 1) \
-    X(14, 2, 2, 6, 2, true, 1) \
     X(15, 3, 1, 5, 2, true, 1) \
-    X(16, 3, 1, 5, 4, true, 1) \
-    X(17, 3, 1, 4, 4, true, 1) \
-    X(18, 3, 1, 5, 8, true, 0) \
-    X(19, 3, 1, 4, 2, true, 1) \
+    X(20, 16, 2, 1, 1, false, 1) \
+    X(22, 16, 2, 1, 1, true, 0) \
+    X(24, 1, 3, 16, 1, true, 0) \
+    X(25, 1, 3, 8, 2, true, 0) \
+    X(26, 1, 3, 8, 1, true, 1) \
+    X(27, 1, 4, 16, 1, true, 0) \
+    X(28, 1, 4, 8, 2, true, 0) \
+    X(29, 2, 2, 8, 1, true, 0) \
+    X(30, 2, 4, 4, 2, true, 0) \
 
 extern "C" {
-int sweep_n() { return 20; }
+int sweep_n() { return 31; }
 
 int sweep_desc(int id, int* out) {
 #define DESC(i, gw, vpt, g, rpg, prod, keep) \
@@ -49,8 +47,9 @@ int sweep_desc(int id, int* out) {
 
 int sweep_run(int id, const void* x, const void* mean, const void* rstd, const void* dy, const void* gamma, void* dx,
               void* dgamma, void* dbeta, double* rg, double* rb, double* sums, int norms, int64_t B, int64_t M,
-              int64_t D, void* ws, size_t wsb, void* stream, unsigned long long* trace) {
-    LnBwdCall c{x, mean, rstd, dy, gamma, dx, dgamma, dbeta, rg, rb, sums, norms, B, M, D, ws, wsb, trace};
+              int64_t D, void* ws, size_t wsb, void* stream, unsigned long long* trace,
+              unsigned long long* trace2) {
+    LnBwdCall c{x, mean, rstd, dy, gamma, dx, dgamma, dbeta, rg, rb, sums, norms, B, M, D, ws, wsb, trace, trace2};
     const char* why = nullptr;
     cudaError_t ce = cudaSuccess;
 #define RUN(i, gw, vpt, g, rpg, prod, keep) \

@@ -3,6 +3,7 @@ import ctypes
 import os
 import sys
 
+import numpy as np
 import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -11,7 +12,7 @@ import paper_2411_00999_b200 as m  # noqa: E402
 
 lib = ctypes.CDLL(os.path.join(ROOT, "experiments", "libln_sweep.so"))
 _vp, _i64 = ctypes.c_void_p, ctypes.c_int64
-lib.sweep_run.argtypes = [ctypes.c_int] + [_vp] * 11 + [ctypes.c_int, _i64, _i64, _i64, _vp, ctypes.c_size_t, _vp, _vp]
+lib.sweep_run.argtypes = [ctypes.c_int] + [_vp] * 11 + [ctypes.c_int, _i64, _i64, _i64, _vp, ctypes.c_size_t, _vp, _vp, _vp]
 lib.sweep_run.restype = ctypes.c_int
 dev = torch.device("cuda")
 B, T = int(os.environ.get('SWEEP_B', '32')), 1024
@@ -22,6 +23,7 @@ marks = torch.zeros(2, dtype=torch.int64, device=dev)
 FLUSH = os.environ.get("SWEEP_FLUSH", "write")
 flush_sink = torch.zeros((), dtype=torch.int64, device=dev)
 trace = torch.zeros(148 * 6, dtype=torch.int64, device=dev)
+trace2 = torch.zeros(148 * 6, dtype=torch.int64, device=dev)
 Ds = [int(v) for v in sys.argv[1].split(",")] if len(sys.argv) > 1 else [768, 1024, 2048, 4096, 8192]
 ids = [int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else list(range(lib.sweep_n()))
 for D in Ds:
@@ -38,7 +40,8 @@ for D in Ds:
     nbytes = B * T * D * 6 + 8 * B * T + 12 * D + 16 * B
     desc = (ctypes.c_int * 6)()
     for i in ids:
-        lib.sweep_desc(i, desc)
+        if lib.sweep_desc(i, desc) != 0:
+            continue
         gw, vpt, g, rpg, prod, keep = list(desc)
         if gw * 32 * vpt < D // 8 or (gw * 32 * vpt) // 2 >= D // 8:
             continue  # config does not fit this width (or wastes > half the lanes)
@@ -61,7 +64,8 @@ for D in Ds:
                                    ctypes.c_void_p(rg.data_ptr()), ctypes.c_void_p(rb.data_ptr()),
                                    ctypes.c_void_p(sums.data_ptr()), norms, B, T, D, ctypes.c_void_p(ws.data_ptr()),
                                    ctypes.c_size_t(ws.numel()), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream),
-                                   ctypes.c_void_p(trace.data_ptr() if TRACE else 0))
+                                   ctypes.c_void_p(trace.data_ptr() if TRACE else 0),
+                                   ctypes.c_void_p(trace2.data_ptr() if TRACE else 0))
                 if TRACE:
                     mk.marker(ctypes.c_void_p(marks.data_ptr() + 8), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
                 e1.record()
@@ -75,17 +79,21 @@ for D in Ds:
                 continue
             ts.sort()
             res[norms] = ts[len(ts) // 2]
+            if TRACE:
+                tr = trace.view(-1, 6).cpu().numpy().astype("int64")
+                t2 = trace2.view(-1, 6).cpu().numpy().astype("int64")
+                trace2.zero_()
+                mks = marks.cpu().numpy().astype("int64")
+                t0 = tr[:, 0].min()
+                last = max(tr[:, 2].max(), t2.max())
+                t2 = np.where(t2 == 0, t0, t2)
+                rel = (tr - t0) / 1000.0
+                r2 = (t2 - t0) / 1000.0
+                print(f"   {'fused' if norms else 'plain'}: launch->start {(t0 - mks[0]) / 1000:.1f} us; last->marker {(mks[1] - last) / 1000:.1f} us"
+                      f" | rowmath end min {rel[:,1].min():.1f} med {sorted(rel[:,1])[len(rel)//2]:.1f} max {rel[:,1].max():.1f}"
+                      f" | fold end {rel[:,2].max():.1f} | red wait-out {r2[:,0].min():.1f}..{r2[:,0].max():.1f}"
+                      f" | loads {r2[:,1].max():.1f} | red end {r2[:,2].max():.1f} | final {r2[:,3].max():.1f}->{r2[:,4].max():.1f}")
         ok = ""
-        if TRACE:
-            tr = trace.view(-1, 6).cpu().numpy().astype("int64")
-            mks = marks.cpu().numpy().astype("int64")
-            t0 = tr[:, 0].min()
-            print(f"   marker before -> first CTA start {(t0 - mks[0]) / 1000:.1f} us; last CTA end -> marker after {(mks[1] - tr[:, 5].max()) / 1000:.1f} us")
-            rel = (tr - t0) / 1000.0
-            last = rel[:, 5].max()
-            print(f"   trace(us): start max {rel[:,0].max():.1f} | rowmath end min {rel[:,1].min():.1f} med {sorted(rel[:,1])[74]:.1f} max {rel[:,1].max():.1f}"
-                  f" | precombine end max {rel[:,2].max():.1f} | barrier out min {rel[:,3].min():.1f} max {rel[:,3].max():.1f}"
-                  f" | stage2 end max {rel[:,4].max():.1f} | final end {last:.1f}")
         if not isinstance(res.get(1), str):
             err = (dx.float() - ref.input_grad.float()).abs().max().item()
             nerr = ((rg - ref.grads.per_example_sqnorms_raw["gamma"]).abs() / ref.grads.per_example_sqnorms_raw["gamma"]).max().item()

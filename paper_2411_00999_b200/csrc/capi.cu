@@ -1,3 +1,7 @@
+#include <utility>
+#include <map>
+#include <cstdio>
+#include <cstdlib>
 // capi.cu — the extern "C" boundary (include/gnsb.h): argument validation in
 // the reference's wording, dtype dispatch, and the small device kernels that
 // do not deserve their own file (squared norm, GNS accumulator).
@@ -26,7 +30,36 @@ gnsb_status cuda_fail(cudaError_t e, const char* where) {
     return GNSB_ECUDA;
 }
 
-gnsb_status need_device() {
+// GNSB_DEBUG=1: synchronize at every compute entry point and report a CUDA
+// error left pending by whatever ran before (debugging aid, off by default).
+static bool debug_mode() {
+    static const bool on = [] {
+        const char* v = std::getenv("GNSB_DEBUG");
+        return v != nullptr && v[0] == '1';
+    }();
+    return on;
+}
+
+// GNSB_DEBUG=1: report a CUDA error an entry point leaves pending on success.
+static gnsb_status debug_ok(const char* fn) {
+    if (debug_mode()) {
+        const cudaError_t s = cudaDeviceSynchronize();
+        const cudaError_t p = cudaPeekAtLastError();
+        if (s != cudaSuccess || p != cudaSuccess)
+            std::fprintf(stderr, "gnsb: CUDA error pending on exit from %s: sync=%s last=%s\n", fn,
+                         cudaGetErrorString(s), cudaGetErrorString(p));
+    }
+    return GNSB_OK;
+}
+
+gnsb_status need_device(const char* fn) {
+    if (debug_mode()) {
+        const cudaError_t s = cudaDeviceSynchronize();
+        const cudaError_t p = cudaPeekAtLastError();
+        if (s != cudaSuccess || p != cudaSuccess)
+            std::fprintf(stderr, "gnsb: CUDA error pending on entry to %s: sync=%s last=%s\n", fn,
+                         cudaGetErrorString(s), cudaGetErrorString(p));
+    }
     static std::atomic<bool> seen{false};  // a device, once found, stays
     if (seen.load(std::memory_order_relaxed)) return GNSB_OK;
     int n = 0;
@@ -67,6 +100,26 @@ double corrected_mean_sqnorm(double sum_sq, int64_t batch) {
 }  // namespace
 
 namespace gnsb {
+
+cudaError_t ensure_smem_attr(const void* kernel, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> set_for;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    auto& cur = set_for[{kernel, dev}];
+    if (cur >= bytes) return cudaSuccess;
+    cudaFuncAttributes fa{};
+    cudaError_t e = cudaFuncGetAttributes(&fa, kernel);
+    if (e != cudaSuccess) return e;
+    if ((size_t)fa.maxDynamicSharedSizeBytes >= bytes) {
+        cur = (size_t)fa.maxDynamicSharedSizeBytes;
+        return cudaSuccess;
+    }
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) cur = bytes;
+    return e;
+}
 
 int device_sm_count() {
     static std::mutex mu;
@@ -178,8 +231,8 @@ gnsb_status gnsb_ln_fwd(const void* x, const void* gamma, const void* beta, void
     if (!(eps > 0.0)) return fail(GNSB_EINVAL, "layers: epsilon must be positive");          // layers.cpp:192
     if (D < 2) return fail(GNSB_EINVAL, "layers: layernorm needs trailing extent >= 2");     // layers.cpp:194
     if (rows < 0) return fail(GNSB_EINVAL, "layers: negative row count");
-    if (gnsb_status s = need_device()) return s;
-    if (rows == 0) return GNSB_OK;
+    if (gnsb_status s = need_device("gnsb_ln_fwd")) return s;
+    if (rows == 0) return debug_ok("gnsb_ln_fwd");
     if (!x || !gamma || !beta) return fail(GNSB_EINVAL, "layers: null input pointer");
     gnsb::LnFwdCall c{x, gamma, beta, y, mean, rstd, xhat, rows, D, eps};
     const char* why = nullptr;
@@ -193,14 +246,14 @@ gnsb_status gnsb_ln_fwd(const void* x, const void* gamma, const void* beta, void
         default: return fail(GNSB_EINVAL, "layers: unknown dtype");
     }
     if (rc == 1) return fail(GNSB_EINVAL, why ? why : "layers: invalid argument");
-    if (rc == 2) return cuda_fail(ce, "ln_fwd launch");
-    return GNSB_OK;
+    if (rc == 2) return cuda_fail(ce, why ? why : "ln_fwd launch");
+    return debug_ok("gnsb_ln_fwd");
 }
 
 gnsb_status gnsb_ln_bwd_workspace_size(int64_t B, int64_t M, int64_t D, gnsb_dtype dt, size_t* bytes) {
     if (!bytes) return fail(GNSB_EINVAL, "layers: null output pointer");
     if (B < 0 || M < 0 || D < 1) return fail(GNSB_EINVAL, "layers: invalid extents");
-    if (gnsb_status s = need_device()) return s;
+    if (gnsb_status s = need_device("gnsb_ln_bwd_workspace_size")) return s;
     const char* why = nullptr;
     int rc = 1;
     switch (dt) {
@@ -210,12 +263,12 @@ gnsb_status gnsb_ln_bwd_workspace_size(int64_t B, int64_t M, int64_t D, gnsb_dty
         default: return fail(GNSB_EINVAL, "layers: unknown dtype");
     }
     if (rc) return fail(GNSB_EINVAL, why ? why : "layers: invalid argument");
-    return GNSB_OK;
+    return debug_ok("gnsb_ln_bwd_workspace_size");
 }
 
 gnsb_status gnsb_ln_bwd_geometry(int64_t B, int64_t M, int64_t D, gnsb_dtype dt, int32_t* grid, int32_t* threads,
                                  int32_t* stages) {
-    if (gnsb_status s = need_device()) return s;
+    if (gnsb_status s = need_device("gnsb_ln_bwd_geometry")) return s;
     int g = 0, t = 0, st = 0, rc = 1;
     switch (dt) {
         case GNSB_F32: rc = gnsb::ln_bwd_geometry<float>(B, M, D, &g, &t, &st); break;
@@ -227,7 +280,7 @@ gnsb_status gnsb_ln_bwd_geometry(int64_t B, int64_t M, int64_t D, gnsb_dtype dt,
     if (grid) *grid = g;
     if (threads) *threads = t;
     if (stages) *stages = st;
-    return GNSB_OK;
+    return debug_ok("gnsb_ln_bwd_geometry");
 }
 
 gnsb_status gnsb_ln_bwd(const void* x, const void* mean, const void* rstd, const void* dy, const void* gamma, void* dx,
@@ -237,7 +290,7 @@ gnsb_status gnsb_ln_bwd(const void* x, const void* mean, const void* rstd, const
     if (B < 0 || M < 0) return fail(GNSB_EINVAL, "layers: invalid extents");
     if (D < 1) return fail(GNSB_EINVAL, "layers: gradient trailing extent does not match gamma");
     if (dt != GNSB_F32 && dt != GNSB_BF16 && dt != GNSB_F64) return fail(GNSB_EINVAL, "layers: unknown dtype");
-    if (gnsb_status s = need_device()) return s;
+    if (gnsb_status s = need_device("gnsb_ln_bwd")) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (M == 0) {  // no rows: every gradient and norm is zero (layers.cpp:248-275 with an empty loop)
         cudaError_t e = cudaSuccess;
@@ -248,7 +301,7 @@ gnsb_status gnsb_ln_bwd(const void* x, const void* mean, const void* rstd, const
             if (e == cudaSuccess && raw_b) e = cudaMemsetAsync(raw_b, 0, (size_t)B * 8, st);
             if (e == cudaSuccess && sums) e = cudaMemsetAsync(sums, 0, 4 * 8, st);
         }
-        return e == cudaSuccess ? GNSB_OK : cuda_fail(e, "memset");
+        return e == cudaSuccess ? debug_ok("gnsb_ln_bwd") : cuda_fail(e, "memset");
     }
     if (!x || !rstd || !dy || !gamma || !dgamma || !dbeta || !ws)
         return fail(GNSB_EINVAL, "layers: null input pointer");
@@ -264,13 +317,16 @@ gnsb_status gnsb_ln_bwd(const void* x, const void* mean, const void* rstd, const
         default: break;
     }
     if (rc == 1) return fail(GNSB_EINVAL, why ? why : "layers: invalid argument");
-    if (rc == 2) return cuda_fail(ce, "ln_bwd launch");
-    return GNSB_OK;
+    if (rc == 2) return cuda_fail(ce, why ? why : "ln_bwd launch");
+    return debug_ok("gnsb_ln_bwd");
 }
 
 // ---------------------------------------------------------------- linear --
 static bool use_tc_wgrad(gnsb_dtype dt, int64_t B, int64_t T, int64_t K, int64_t L) {
     return dt == GNSB_BF16 && gnsb::wgrad_shape_ok(B, T, K, L);
+}
+static bool use_tc_gram(gnsb_dtype dt, int64_t B, int64_t T, int64_t K, int64_t L) {
+    return dt == GNSB_BF16 && gnsb::gram_shape_ok(B, T, K, L);
 }
 
 gnsb_status gnsb_linear_pe_workspace_size(int64_t B, int64_t T, int64_t K, int64_t L, gnsb_dtype dt, size_t* bytes) {
@@ -280,8 +336,12 @@ gnsb_status gnsb_linear_pe_workspace_size(int64_t B, int64_t T, int64_t K, int64
         const size_t m = gnsb::wgrad_workspace(B, K, L);
         n = n > m ? n : m;
     }
+    if (use_tc_gram(dt, B, T, K, L)) {
+        const size_t m = gnsb::gram_workspace(B, T);
+        n = n > m ? n : m;
+    }
     *bytes = n;
-    return GNSB_OK;
+    return debug_ok("gnsb_linear_pe_workspace_size");
 }
 
 gnsb_status gnsb_linear_pe_norms(const void* x, const void* g, void* dW, double* raw_w, double* sums, int64_t B,
@@ -292,7 +352,7 @@ gnsb_status gnsb_linear_pe_norms(const void* x, const void* g, void* dW, double*
     if (form < 0 || form > 2) return fail(GNSB_EINVAL, "layers: form must be 0 (auto), 1 (weight-grad) or 2 (gram)");
     if (form == 2 && dW) return fail(GNSB_EINVAL, "layers: the gram form computes norms only (dW must be NULL)");
     if (dt != GNSB_F32 && dt != GNSB_BF16 && dt != GNSB_F64) return fail(GNSB_EINVAL, "layers: unknown dtype");
-    if (gnsb_status s = need_device()) return s;
+    if (gnsb_status s = need_device("gnsb_linear_pe_norms")) return s;
     size_t need = 0;
     gnsb_linear_pe_workspace_size(B, T, K, L, dt, &need);
     if (!ws || ws_bytes < need) return fail(GNSB_EINVAL, "layers: workspace too small (query gnsb_linear_pe_workspace_size)");
@@ -302,10 +362,12 @@ gnsb_status gnsb_linear_pe_norms(const void* x, const void* g, void* dW, double*
     cudaError_t e;
     if (form == 1 && use_tc_wgrad(dt, B, T, K, L))
         e = gnsb::launch_wgrad_norms(x, g, static_cast<float*>(dW), raw_w, sums, B, T, K, L, ws, st);
+    else if (form == 2 && use_tc_gram(dt, B, T, K, L))
+        e = gnsb::launch_gram_norms(x, g, raw_w, sums, B, T, K, L, ws, st);
     else
         e = gnsb::launch_linear_generic((int)dt, form == 1 ? 0 : 2, x, g, dW, dt == GNSB_F64, raw_w, sums, 0, B, T, K,
                                         L, ws, st);
-    return e == cudaSuccess ? GNSB_OK : cuda_fail(e, "linear_pe_norms launch");
+    return e == cudaSuccess ? debug_ok("gnsb_linear_pe_norms") : cuda_fail(e, "linear_pe_norms launch");
 }
 
 gnsb_status gnsb_linear_bias_pe(const void* g, void* dbias, double* raw_b, double* sums, int64_t B, int64_t T,
@@ -313,26 +375,26 @@ gnsb_status gnsb_linear_bias_pe(const void* g, void* dbias, double* raw_b, doubl
     if (B == 0) return fail(GNSB_EINVAL, "layers: empty batch");
     if (B < 0 || T < 0 || L < 1) return fail(GNSB_EINVAL, "layers: invalid extents");
     if (dt != GNSB_F32 && dt != GNSB_BF16 && dt != GNSB_F64) return fail(GNSB_EINVAL, "layers: unknown dtype");
-    if (gnsb_status s = need_device()) return s;
+    if (gnsb_status s = need_device("gnsb_linear_bias_pe")) return s;
     if (!ws || ws_bytes < gnsb::generic_workspace(B, T, 1, L))
         return fail(GNSB_EINVAL, "layers: workspace too small (query gnsb_linear_pe_workspace_size)");
     const cudaError_t e = gnsb::launch_linear_generic((int)dt, 1, nullptr, g, dbias, dt == GNSB_F64, raw_b, sums, 1, B,
                                                       T, 1, L, ws, static_cast<cudaStream_t>(stream));
-    return e == cudaSuccess ? GNSB_OK : cuda_fail(e, "linear_bias_pe launch");
+    return e == cudaSuccess ? debug_ok("gnsb_linear_bias_pe") : cuda_fail(e, "linear_bias_pe launch");
 }
 
 gnsb_status gnsb_linear_dx(const void* g, const void* W, void* dx, int64_t rows, int64_t K, int64_t L, gnsb_dtype dt,
                            void* stream) {
     if (rows < 0 || K < 1 || L < 1) return fail(GNSB_EINVAL, "layers: invalid extents");
     if (dt != GNSB_F32 && dt != GNSB_BF16 && dt != GNSB_F64) return fail(GNSB_EINVAL, "layers: unknown dtype");
-    if (gnsb_status s = need_device()) return s;
+    if (gnsb_status s = need_device("gnsb_linear_dx")) return s;
     const cudaError_t e = gnsb::launch_linear_dx((int)dt, g, W, dx, rows, K, L, static_cast<cudaStream_t>(stream));
-    return e == cudaSuccess ? GNSB_OK : cuda_fail(e, "linear_dx launch");
+    return e == cudaSuccess ? debug_ok("gnsb_linear_dx") : cuda_fail(e, "linear_dx launch");
 }
 
 gnsb_status gnsb_sqnorm(const void* v, int64_t n, gnsb_dtype dt, double* out, void* stream) {
     if (n < 0 || !out) return fail(GNSB_EINVAL, "gns: invalid sqnorm arguments");
-    if (gnsb_status s = need_device()) return s;
+    if (gnsb_status s = need_device("gnsb_sqnorm")) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (dt == GNSB_F64)
         gnsb::sqnorm_kernel<double><<<1, 1024, 0, st>>>(static_cast<const double*>(v), n, out);
@@ -341,7 +403,7 @@ gnsb_status gnsb_sqnorm(const void* v, int64_t n, gnsb_dtype dt, double* out, vo
     else
         return fail(GNSB_EINVAL, "gns: sqnorm expects fp32 or fp64 data");
     const cudaError_t e = cudaGetLastError();
-    return e == cudaSuccess ? GNSB_OK : cuda_fail(e, "sqnorm launch");
+    return e == cudaSuccess ? debug_ok("gnsb_sqnorm") : cuda_fail(e, "sqnorm launch");
 }
 
 // ---------------------------------------------------------------- GNS ----
@@ -351,7 +413,7 @@ gnsb_status gnsb_estimate_g2(const gnsb_grad_stats* st, double* out) {
     if (st->n_small < 1) return fail(GNSB_EINVAL, "gns: n_small must be >= 1");
     const double bb = (double)st->b_big, bs = (double)st->b_small;
     *out = (bb * st->g_big_sqnorm - bs * st->g_small_sqnorm_mean) / (bb - bs);
-    return GNSB_OK;
+    return debug_ok("gnsb_estimate_g2");
 }
 
 gnsb_status gnsb_estimate_s(const gnsb_grad_stats* st, double* out) {
@@ -360,7 +422,7 @@ gnsb_status gnsb_estimate_s(const gnsb_grad_stats* st, double* out) {
     if (st->n_small < 1) return fail(GNSB_EINVAL, "gns: n_small must be >= 1");
     const double bb = (double)st->b_big, bs = (double)st->b_small;
     *out = (st->g_small_sqnorm_mean - st->g_big_sqnorm) / (1.0 / bs - 1.0 / bb);
-    return GNSB_OK;
+    return debug_ok("gnsb_estimate_s");
 }
 
 void gnsb_make_gns_estimate(double g2, double s, gnsb_gns_estimate* out) {
@@ -381,14 +443,14 @@ gnsb_status gnsb_ema_update(gnsb_ema_state* st, double x) {
     else
         st->value = (1.0 - st->alpha) * st->value + st->alpha * x;
     ++st->count;
-    return GNSB_OK;
+    return debug_ok("gnsb_ema_update");
 }
 
 gnsb_status gnsb_smoothed_gns(const gnsb_ema_state* g2, const gnsb_ema_state* s, gnsb_gns_estimate* out) {
     if (g2->count < 1 || s->count < 1)
         return fail(GNSB_EINVAL, "gns: smoothed_gns needs at least one sample in each state");
     gnsb_make_gns_estimate(g2->value, s->value, out);
-    return GNSB_OK;
+    return debug_ok("gnsb_smoothed_gns");
 }
 
 gnsb_status gnsb_aggregate(const gnsb_grad_stats* stats, const int32_t* types, int32_t n, int32_t group,
@@ -409,7 +471,7 @@ gnsb_status gnsb_aggregate(const gnsb_grad_stats* stats, const int32_t* types, i
         out->g_small_sqnorm_mean += stats[i].g_small_sqnorm_mean;
     }
     if (first) return fail(GNSB_EINVAL, "gns: aggregate over an empty selection");
-    return GNSB_OK;
+    return debug_ok("gnsb_aggregate");
 }
 
 gnsb_status gnsb_gns_step(const double* layer_sums, const int32_t* layer_types, int32_t n_layers, int64_t B,
@@ -418,7 +480,7 @@ gnsb_status gnsb_gns_step(const double* layer_sums, const int32_t* layer_types, 
     if (!(alpha > 0.0) || alpha > 1.0) return fail(GNSB_EINVAL, "gns: ema alpha must be in (0, 1]");
     if (n_layers < 1 || n_layers > 512) return fail(GNSB_EINVAL, "gns: layer count must be in [1, 512]");
     if (!layer_sums || !layer_types || !state || !out_groups) return fail(GNSB_EINVAL, "gns: null pointer");
-    if (gnsb_status s = need_device()) return s;
+    if (gnsb_status s = need_device("gnsb_gns_step")) return s;
     gnsb::GnsStepArgs a{};
     a.sums = layer_sums;
     a.n = n_layers;
@@ -433,7 +495,7 @@ gnsb_status gnsb_gns_step(const double* layer_sums, const int32_t* layer_types, 
     }
     gnsb::gns_step_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
     const cudaError_t e = cudaGetLastError();
-    return e == cudaSuccess ? GNSB_OK : cuda_fail(e, "gns_step launch");
+    return e == cudaSuccess ? debug_ok("gnsb_gns_step") : cuda_fail(e, "gns_step launch");
 }
 
 // ------------------------------------------------------------ costmodel ---
@@ -451,7 +513,7 @@ gnsb_status gnsb_flops(int64_t b, int64_t t, int64_t k, int64_t l, int32_t metho
         out[0] = k * l * (2 * b * t - 1);
         out[1] = b * t * t * (2 * k + 2 * l - 2) + b * t * t;
     }
-    return GNSB_OK;
+    return debug_ok("gnsb_flops");
 }
 
 gnsb_status gnsb_io_values(int64_t b, int64_t t, int64_t k, int64_t l, int32_t method, int64_t* out) {
@@ -463,34 +525,34 @@ gnsb_status gnsb_io_values(int64_t b, int64_t t, int64_t k, int64_t l, int32_t m
         out[0] = b * k * t + b * l * t + k * l;
         out[1] = 2 * b * t * t + b;
     }
-    return GNSB_OK;
+    return debug_ok("gnsb_io_values");
 }
 
 gnsb_status gnsb_crossover_t(int64_t k, int64_t l, int32_t criterion, double* out) {
     if (k < 1 || l < 1) return fail(GNSB_EINVAL, "costmodel: dims must be positive");
     const double kd = (double)k, ld = (double)l;  // costmodel.cpp:58-64
     *out = criterion == 0 ? std::sqrt(2.0 * kd * ld) / 2.0 : std::sqrt((2.0 * kd * ld - 1.0) / (2.0 * kd + 2.0 * ld - 1.0));
-    return GNSB_OK;
+    return debug_ok("gnsb_crossover_t");
 }
 
 // ------------------------------------------------------------- synthetic --
 gnsb_status gnsb_synth_ln(void* x, void* dy, void* gamma, void* beta, int64_t B, int64_t T, int64_t D,
                           int64_t b_offset, int64_t B_div, float sigma, uint64_t stream0, gnsb_dtype dt, void* stream) {
     if (B < 0 || T < 0 || D < 1 || B_div < 1) return fail(GNSB_EINVAL, "synth: invalid extents");
-    if (gnsb_status s = need_device()) return s;
+    if (gnsb_status s = need_device("gnsb_synth_ln")) return s;
     const cudaError_t e = gnsb::launch_synth_ln((int)dt, x, dy, gamma, beta, B, T, D, b_offset, (float)B_div, sigma,
                                                 seeds(stream0), static_cast<cudaStream_t>(stream));
-    return e == cudaSuccess ? GNSB_OK : cuda_fail(e, "synth_ln launch");
+    return e == cudaSuccess ? debug_ok("gnsb_synth_ln") : cuda_fail(e, "synth_ln launch");
 }
 
 gnsb_status gnsb_synth_linear(void* x, void* dy, int64_t B, int64_t T, int64_t K, int64_t L, int64_t b_offset,
                               int64_t B_div, uint64_t stream0, gnsb_dtype dt, void* stream) {
     if (B < 0 || T < 1 || K < 1 || L < 1 || B_div < 1) return fail(GNSB_EINVAL, "synth: invalid extents");
-    if (gnsb_status s = need_device()) return s;
+    if (gnsb_status s = need_device("gnsb_synth_linear")) return s;
     const float scale = (float)B_div * sqrtf((float)T);
     const cudaError_t e = gnsb::launch_synth_linear((int)dt, x, dy, B, T, K, L, b_offset, scale, seeds(stream0),
                                                     static_cast<cudaStream_t>(stream));
-    return e == cudaSuccess ? GNSB_OK : cuda_fail(e, "synth_linear launch");
+    return e == cudaSuccess ? debug_ok("gnsb_synth_linear") : cuda_fail(e, "synth_linear launch");
 }
 
 }  // extern "C"

@@ -30,7 +30,8 @@ struct LnBwdCall {
     int norms;
     int64_t B, M, D;
     void* ws; size_t ws_bytes;
-    unsigned long long* trace = nullptr;  // profiling only: [grid][6] phase stamps
+    unsigned long long* trace = nullptr;   // profiling only: row kernel [grid][6] phase stamps
+    unsigned long long* trace2 = nullptr;  // profiling only: reduce kernel [grid][3] phase stamps
 };
 
 // Returns 0 ok, 1 invalid (message in *why), 2 CUDA error (cudaError_t in *cerr).
@@ -41,6 +42,8 @@ template <typename T> int ln_bwd_workspace(int64_t B, int64_t M, int64_t D, size
 template <typename T> int ln_bwd_geometry(int64_t B, int64_t M, int64_t D, int* grid, int* threads, int* stages);
 
 int device_sm_count();
+// raise (never lower) a kernel's max dynamic shared memory attribute; process-wide record
+cudaError_t ensure_smem_attr(const void* kernel, size_t bytes);
 
 // linear-layer per-example norms (linear_pe.cu)
 bool wgrad_shape_ok(int64_t B, int64_t T, int64_t K, int64_t L);
@@ -52,6 +55,14 @@ size_t generic_workspace(int64_t B, int64_t T, int64_t K, int64_t L);
 cudaError_t launch_linear_generic(int dt, int kind, const void* x, const void* g, void* out_grad, int out_f64,
                                   double* raw, double* sums, int sum_slot, int64_t B, int64_t T, int64_t K, int64_t L,
                                   void* ws, cudaStream_t st);
+// Gram form on tensor cores (linear_gram.cu): bf16 rows, T % 128 == 0, K % 64 == 0, L % 64 == 0
+bool gram_shape_ok(int64_t B, int64_t T, int64_t K, int64_t L);
+size_t gram_workspace(int64_t B, int64_t T);
+cudaError_t launch_gram_norms(const void* x, const void* g, double* raw, double* sums, int64_t B, int64_t T,
+                              int64_t K, int64_t L, void* ws, cudaStream_t st);
+// raw[b] = sum_j q[b][j], sums[sum_slot] = sum_b raw[b] (fixed order, one CTA)
+cudaError_t launch_fold_rows(const double* q, int nb, int ncol, double* raw, double* sums, int sum_slot,
+                             cudaStream_t st);
 cudaError_t launch_linear_dx(int dt, const void* g, const void* W, void* dx, int64_t rows, int64_t K, int64_t L,
                              cudaStream_t st);
 

@@ -296,26 +296,38 @@ __global__ void __launch_bounds__(wg::THREADS, 1)
     }
 }
 
-// raw[b] = sum_j q[b][j] (fixed order), sums[0] = sum_b raw[b]
+// raw[b] = sum_j q[b][j] (fixed order), sums[sum_slot] = sum_b raw[b] (fixed order)
+constexpr int kFoldSmemRows = 4096;
 __global__ void __launch_bounds__(256) fold_rows_kernel(const double* q, int nb, int ncol, double* raw, double* sums,
                                                         int sum_slot) {
-    __shared__ double rs[1024];
+    __shared__ double rs[kFoldSmemRows];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int b = warp; b < nb; b += blockDim.x / 32) {
+    auto row = [&](int b) {
         double t = 0.0;
         for (int j = lane; j < ncol; j += 32) t += q[(size_t)b * ncol + j];
-        t = warp_sum(t);
+        return warp_sum(t);
+    };
+    for (int b = warp; b < nb; b += blockDim.x / 32) {
+        const double t = row(b);
         if (lane == 0) {
             if (raw) raw[b] = t;
-            if (b < 1024) rs[b] = t;
+            if (b < kFoldSmemRows) rs[b] = t;
         }
     }
     __syncthreads();
-    if (threadIdx.x == 0 && sums != nullptr) {
-        double t = 0.0;
-        for (int b = 0; b < nb && b < 1024; ++b) t += rs[b];
-        sums[sum_slot] = t;
+    if (sums == nullptr || warp != 0) return;
+    double t = 0.0;
+    for (int b = 0; b < nb; ++b) {
+        const double r = b < kFoldSmemRows ? rs[b] : row(b);  // (rows beyond the buffer are recomputed)
+        t += r;
     }
+    if (lane == 0) sums[sum_slot] = t;
+}
+
+cudaError_t launch_fold_rows(const double* q, int nb, int ncol, double* raw, double* sums, int sum_slot,
+                             cudaStream_t st) {
+    fold_rows_kernel<<<1, 256, 0, st>>>(q, nb, ncol, raw, sums, sum_slot);
+    return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ host --

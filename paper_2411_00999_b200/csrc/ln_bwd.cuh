@@ -22,14 +22,17 @@
 //   * row reductions mean(h), mean(h*xhat): a transposed butterfly inside
 //     the warp, then a padded xor tree across the group's warps;
 //   * at each example boundary a group flushes its register partials to a
-//     slot (cta + example, group) of an L2-resident workspace;
-//   * stage 2 after a software grid barrier: column chunks sum the slots of
-//     each example in fixed (cta, group) order -> gamma'_b; square and reduce
-//     over D in fp64 -> per-(example, chunk) partial norms; fixed-order sum
-//     over b -> dgamma/dbeta;
-//   * the last CTA (ticket) folds chunk partials into raw_b and the scalar sums
-//     and resets the workspace counters.  No float atomics anywhere: results
-//     are bitwise deterministic run to run.
+//     slot (cta + example, group) of an L2-resident workspace; at the end the
+//     CTA folds its groups' slots in fixed order (the last example through
+//     shared memory), leaving one slot per (cta, example);
+//   * stage 2 is a second kernel (ln_bwd_reduce_kernel), launched with
+//     programmatic dependent launch so it is scheduled while the row kernel
+//     drains: CTA c owns a contiguous column range; per example it sums that
+//     example's slots in fixed CTA order -> gamma'_b, beta'_b (fp64), squares
+//     and reduces over its columns -> q[b][c], and sums over b in fixed order
+//     -> dgamma/dbeta on its columns (+ their squares -> qbig[c]);
+//   * the last CTA (ticket) folds q into raw_b and the scalar sums.  No float
+//     atomics anywhere: results are bitwise deterministic run to run.
 #pragma once
 
 #include <type_traits>
@@ -45,26 +48,33 @@ struct LnBwdArgs {
     const void* dy;     // [N, D] of T
     const void* gamma;  // [D] Acc
     void* dx;           // [N, D] of T (may be null: skip dx)
-    void* dgamma;       // [D] Acc
-    void* dbeta;        // [D] Acc
-    double* raw_g;      // [B] or null
-    double* raw_b;      // [B] or null
-    double* sums;       // [4] or null: sum raw_g, sum raw_b, ||dgamma||^2, ||dbeta||^2
     int64_t B, M, N, D;
     int Dp;             // smem row stride in elements (D rounded up to the vector width)
     int stages;         // ring depth
     int aligned;        // 1: rows are 16-byte aligned -> TMA producer
-    void* partial;      // [(grid + B) * G][2][Dp] Acc
-    double* q;          // [B][nchunks][2]
-    double* qbig;       // [nchunks][2]
-    double* rawws;      // [B][2]
-    unsigned* counters; // [2] grid barrier, final ticket (zero on entry, zero on exit)
-    int nchunks;
-    int64_t scratch_bytes;      // shared memory available to stage 2 (the ring region)
+    void* partial;      // [(grid + B) * G][2][Dp] Acc; slot (cta + example, 0) holds the CTA's fold
     unsigned long long* trace;  // optional [grid][6] globaltimer stamps (profiling only)
 };
 
-constexpr int kChunk = 16;  // stage-2 column chunk (half a warp)
+// Arguments of the stage-2 kernel (per-example combine, squares, dgamma/dbeta).
+struct LnRedArgs {
+    const void* partial;  // the row kernel's slots: slot (c + b) * slot_stride holds CTA c's part of example b
+    int64_t slot_stride;  // elements between consecutive (cta + example) slots (= G * 2 * Dp)
+    int64_t B, M, N, D;
+    int Dp;
+    int grid_rows;        // CTAs of the row kernel (row range of CTA c: [c*N/grid_rows, (c+1)*N/grid_rows))
+    int eb;               // examples per shared-memory block
+    void* dgamma;         // [D] Acc
+    void* dbeta;          // [D] Acc
+    double* raw_g;        // [B] or null
+    double* raw_b;        // [B] or null
+    double* sums;         // [4] or null: sum raw_g, sum raw_b, ||dgamma||^2, ||dbeta||^2
+    double* q;            // [B][grid][2] per-(example, column range) squares
+    double* qbig;         // [grid][2]
+    double* rawws;        // [B][2]
+    unsigned* ticket;     // zero on entry and on exit
+    unsigned long long* trace;  // optional [grid][6]
+};
 
 template <typename T, int GW, int VPT, int G, int RPG, bool PROD_ = true, int KEEP_ = -1>
 struct LnBwdCfg {
@@ -99,15 +109,15 @@ struct LnBwdCfg {
     }
     static __host__ __device__ constexpr size_t stage_row_bytes(int Dp) { return (size_t)2 * R * Dp * sizeof(T); }
     static __host__ __device__ constexpr size_t smem_bytes(int S, int Dp) {
-        // the ring doubles as the stage-2 scratch: >= [2][16][J] doubles for the
-        // fold over examples (J = threads / 16) and >= one example's [2][16]
+        // the ring doubles as the CTA-local fold area [G][2][Dp] of the last
+        // example's group partials (G > 1)
         const size_t ring = (size_t)S * stage_row_bytes(Dp);
-        const size_t scratch = (size_t)16 * kThreads > 256 ? (size_t)16 * kThreads : 256;
+        const size_t scratch = G > 1 ? (size_t)G * 2 * Dp * sizeof(Acc) : 0;
         return rows_off(S, Dp) + (ring > scratch ? ring : scratch);
     }
 };
 
-template <typename C, bool HAS_MEAN, bool NORMS>
+template <typename C, bool HAS_MEAN>
 __global__ void __launch_bounds__(C::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a) {
     using T = typename C::Row;
     constexpr int GW = C::kGW, VPT = C::kVPT, G = C::kG, RPG = C::kRPG;
@@ -149,6 +159,9 @@ __global__ void __launch_bounds__(C::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a
         if (a.trace != nullptr && threadIdx.x == 0) a.trace[(size_t)cta * 6 + k] = globaltimer_ns();
     };
     stamp(0);
+    // the stage-2 kernel may be scheduled as soon as SMs free up; it waits
+    // (griddepcontrol.wait) for this grid's completion before reading
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
@@ -243,6 +256,7 @@ __global__ void __launch_bounds__(C::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a
             }
         }
     }
+    P ag[VPT][NP], ab[VPT][NP];  // per-example dgamma/dbeta partials of this thread's columns
     if (!C::PROD || warp < NW) {  // row-math warps
 
     bool vok[VPT];
@@ -253,7 +267,6 @@ __global__ void __launch_bounds__(C::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a
         vo[k] = (vok[k] ? tig + k * GT : 0) * W;
     }
 
-    P ag[VPT][NP], ab[VPT][NP];
 #pragma unroll
     for (int k = 0; k < VPT; ++k)
 #pragma unroll
@@ -454,23 +467,50 @@ __global__ void __launch_bounds__(C::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a
             ph ^= 1u;
         }
     }
-    flush_to((r_end - 1) / M + 1);
+    // examples before the CTA's last one go to their global slots now; the
+    // last one stays in registers for the CTA-local fold below
+    if (G == 1) {
+        flush_to((r_end - 1) / M + 1);
+    } else if (cur_ex < (r_end - 1) / M) {
+        flush_to((r_end - 1) / M);
+    }
     }  // row-math warps
 
     stamp(1);
     if constexpr (G > 1) {
-        // CTA-local pre-combine: fold the G group partials of every example this
-        // CTA touched into group 0's slot (fixed order g = 0..G-1), so stage 2
-        // reads one slot per (cta, example)
+        // CTA-local fold of the G group partials of every example this CTA
+        // touched into group 0's slot, in fixed order g = 0..G-1.  The last
+        // example's partials go through shared memory (the ring is free once
+        // every warp passed this barrier), earlier examples' through L2.
+        __syncthreads();
+        constexpr int E = 16 / sizeof(Acc);  // Acc per 16-byte vector (Dp is a multiple of E)
+        Acc* fold = reinterpret_cast<Acc*>(smem + C::rows_off(S, a.Dp));  // [G][2][Dp]
+        if (!C::PROD || warp < NW) {
+            const int g = warp / GW, tig = (warp % GW) * 32 + lane;
+            // (register partials of the last example; zero if the group had no rows of it)
+            Acc* fb = fold + (size_t)g * 2 * Dp;
+#pragma unroll
+            for (int k = 0; k < VPT; ++k) {
+                if (tig + k * GT >= NVp) continue;
+#pragma unroll
+                for (int p = 0; p < NP; ++p) {
+                    *reinterpret_cast<P*>(fb + (tig + k * GT) * W + 2 * p) = ag[k][p];
+                    *reinterpret_cast<P*>(fb + Dp + (tig + k * GT) * W + 2 * p) = ab[k][p];
+                }
+            }
+        }
         __syncthreads();
         const int64_t e0 = r_begin / M, e1 = (r_end - 1) / M;
-        constexpr int E = 16 / sizeof(Acc);  // Acc per 16-byte vector (Dp is a multiple of E)
+        Acc* part = static_cast<Acc*>(a.partial);
         for (int64_t ex = e0; ex <= e1; ++ex) {
-            Acc* base = static_cast<Acc*>(a.partial) + (size_t)(cta + ex) * G * 2 * Dp;
+            Acc* base = part + (size_t)(cta + ex) * G * 2 * Dp;
+            const Acc* src = ex == e1 ? fold : base;
             for (int i = threadIdx.x; i < 2 * Dp / E; i += blockDim.x) {
                 uint4 v[G];
 #pragma unroll
-                for (int gg = 0; gg < G; ++gg) v[gg] = *reinterpret_cast<const uint4*>(base + (size_t)gg * 2 * Dp + i * E);
+                for (int gg = 0; gg < G; ++gg)
+                    v[gg] = ex == e1 ? *reinterpret_cast<const uint4*>(src + (size_t)gg * 2 * Dp + i * E)
+                                     : __ldcg(reinterpret_cast<const uint4*>(src + (size_t)gg * 2 * Dp + i * E));
                 Acc t[E];
 #pragma unroll
                 for (int e = 0; e < E; ++e) t[e] = reinterpret_cast<const Acc*>(&v[0])[e];
@@ -482,152 +522,262 @@ __global__ void __launch_bounds__(C::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a
             }
         }
     }
-
-    // ------------------------------------------------------------ stage 2 --
     stamp(2);
-    grid_barrier(&a.counters[0]);
-    stamp(3);
+}
 
-    const Acc* part_r = static_cast<const Acc*>(a.partial);
-    Acc* dgam = static_cast<Acc*>(a.dgamma);
-    Acc* dbet = static_cast<Acc*>(a.dbeta);
-    const int nthreads = blockDim.x;
-    const int NB = nthreads / kChunk;
-    const int cl = threadIdx.x % kChunk, bl = threadIdx.x / kChunk;
-    const unsigned hmask = 0xffffu << (lane & 16);
-    double* sred = reinterpret_cast<double*>(smem + C::rows_off(S, Dp));  // ring is free now
-    const int64_t B = a.B;
-    auto cta_of = [&](int64_t r) -> int64_t { return ((r + 1) * grid - 1) / N; };
+// ---------------------------------------------------------------- stage 2 --
+// Separate kernel, launched with programmatic dependent launch right behind
+// the row kernel.  CTA c owns the contiguous range of 16-byte column vectors
+// [c*U/grid, (c+1)*U/grid).  Per block of examples it first stages its
+// column slice of every slot the block needs into shared memory with
+// independent, coalesced loads (one L2 round trip, no dependent chains),
+// then for every example sums the slots of the CTAs that touched it in fixed
+// CTA order -> gamma'_b, beta'_b on its columns (fp64), squares and reduces
+// them over its columns -> q[b][c], and sums over b in fixed order ->
+// dgamma/dbeta (+ their squares -> qbig[c]).  The last CTA (ticket) folds q
+// into raw_b and the scalar sums.  NORMS=false is the plain LayerNorm
+// backward's reduction (dgamma/dbeta only).
+constexpr int kMaxReduceGrid = 160;  // >= the B200's 148 SMs; bounds the final fold's unrolling
+constexpr int kMaxReduceEb = 512;    // examples per shared-memory block
 
-    for (int chunk = cta; chunk < a.nchunks; chunk += grid) {
-        const int64_t col = (int64_t)chunk * kChunk + cl;
-        const bool cv = col < D;
-        double sg = 0.0, sb = 0.0;
-        for (int64_t b = bl; b < B; b += NB) {
-            const int64_t c0 = cta_of(b * M), c1 = cta_of((b + 1) * M - 1);
-            double vg = 0.0, vb = 0.0;
-            if (cv) {
-                // one (pre-combined) slot per CTA that touched example b; issue
-                // eight CTAs' loads at a time, then add in fixed CTA order
-                for (int64_t cc = c0; cc <= c1; cc += 8) {
-                    Acc lg[8], lb[8];
+struct LnRedLayout {  // shared-memory carve-up of the reduce kernel (host + device)
+    int64_t ncol, eb, nslot_max;
+    __host__ __device__ static int64_t slot_bytes(int64_t ncol, int acc) { return 2 * ncol * acc; }
+    __host__ __device__ size_t colsum_off() const { return 0; }
+    __host__ __device__ size_t sv_off() const { return (size_t)16 * ncol; }
+    __host__ __device__ size_t stage_off() const { return (sv_off() + (size_t)8 * (2 * ncol + 1) * eb + 15) / 16 * 16; }
+    __host__ __device__ size_t bytes(int acc) const {
+        return stage_off() + (size_t)nslot_max * slot_bytes(ncol, acc);
+    }
+};
+
+template <typename Acc, bool NORMS>
+__global__ void __launch_bounds__(256) ln_bwd_reduce_kernel(LnRedArgs a) {
+    constexpr int V = 16 / sizeof(Acc);  // columns per 16-byte vector
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nthreads = blockDim.x, nwarps = nthreads / 32;
+    const int grid = gridDim.x, cta = blockIdx.x;
+    const int64_t B = a.B, M = a.M, N = a.N, D = a.D;
+    const int64_t U = (a.Dp + V - 1) / V;
+    const int u0 = (int)((int64_t)cta * U / grid), u1 = (int)((int64_t)(cta + 1) * U / grid);
+    const int nu = u1 - u0, ncol = nu * V;
+    const int grid_rows = a.grid_rows;
+    auto cta_of = [&](int64_t r) -> int64_t { return ((r + 1) * grid_rows - 1) / N; };
+    LnRedLayout lay{ncol, a.eb, 0};
+    double* colsum = reinterpret_cast<double*>(smem + lay.colsum_off());  // [2][ncol]
+    double* sv = reinterpret_cast<double*>(smem + lay.sv_off());          // [eb][2 ncol + 1] (padded rows)
+    const int svs = 2 * ncol + 1;
+    uint4* stg = reinterpret_cast<uint4*>(smem + lay.stage_off());        // [slot][2][nu] 16-byte vectors
+    __shared__ int s_cs[kMaxReduceEb], s_nc[kMaxReduceEb];
+    __shared__ double s_raw[2][kMaxReduceEb];
+    const uint4* part = static_cast<const uint4*>(a.partial);
+    const int64_t sstride = a.slot_stride / V;  // in 16-byte vectors
+    const int64_t half = a.Dp / V;              // beta row offset inside a slot
+    auto stamp = [&](int k) {
+        if (a.trace != nullptr && threadIdx.x == 0) a.trace[(size_t)cta * 6 + k] = globaltimer_ns();
+    };
+
+    for (int j = threadIdx.x; j < 2 * ncol; j += nthreads) colsum[j] = 0.0;
+    // the row kernel's slots are complete and visible after this
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    stamp(0);
+
+    for (int64_t b0 = 0; b0 < B; b0 += a.eb) {
+        const int64_t nb = (B - b0) < a.eb ? (B - b0) : a.eb;
+        // slots of this block: from the first CTA of example b0 to the last of b0+nb-1
+        const int64_t s_lo = cta_of(b0 * M) + b0;
+        const int64_t s_hi = cta_of((b0 + nb) * M - 1) + (b0 + nb - 1);
+        const int nvec = (int)(s_hi - s_lo + 1) * 2 * nu;  // < 2^31: bounded by the smem block
+        const uint4* pbase = part + s_lo * sstride + u0;
+        // stage: independent 16-byte loads, 8 per thread in flight
+        for (int i0 = threadIdx.x; i0 < nvec; i0 += 8 * nthreads) {
+            uint4 v[8];
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const bool ok = cc + u <= c1;
-                        const Acc* base = part_r + (size_t)(ok ? cc + u + b : 0) * G * 2 * Dp + col;
-                        lg[u] = ok ? __ldcg(base) : Acc(0);
-                        lb[u] = ok ? __ldcg(base + Dp) : Acc(0);
-                    }
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        vg += (double)lg[u];
-                        vb += (double)lb[u];
-                    }
+            for (int k = 0; k < 8; ++k) {
+                const int i = i0 + k * nthreads;
+                if (i < nvec) {
+                    const int sl = i / (2 * nu), rem = i - sl * 2 * nu;
+                    const int h = rem >= nu ? 1 : 0, u = rem - h * nu;
+                    v[k] = __ldcg(pbase + (int64_t)sl * sstride + h * half + u);
                 }
             }
-            sg += vg;
-            sb += vb;
-            if constexpr (NORMS) {
-                double qg = vg * vg, qb = vb * vb;
 #pragma unroll
-                for (int o = kChunk / 2; o > 0; o >>= 1) {
-                    qg += __shfl_xor_sync(hmask, qg, o);
-                    qb += __shfl_xor_sync(hmask, qb, o);
-                }
-                if (cl == 0) {
-                    a.q[((size_t)b * a.nchunks + chunk) * 2 + 0] = qg;
-                    a.q[((size_t)b * a.nchunks + chunk) * 2 + 1] = qb;
-                }
+            for (int k = 0; k < 8; ++k) {
+                const int i = i0 + k * nthreads;
+                if (i < nvec) stg[i] = v[k];
             }
         }
-        sred[(size_t)bl * kChunk + cl] = sg;
-        sred[(size_t)(NB + bl) * kChunk + cl] = sb;
         __syncthreads();
-        if (bl == 0) {
-            double tg = 0.0, tb = 0.0;
-            for (int k = 0; k < NB; ++k) {
-                tg += sred[(size_t)k * kChunk + cl];
-                tb += sred[(size_t)(NB + k) * kChunk + cl];
+        if (b0 == 0) stamp(1);
+        // per (example, column): fixed-order sum over the example's CTAs
+        for (int bb = threadIdx.x; bb < nb; bb += nthreads) {
+            const int64_t b = b0 + bb;
+            s_cs[bb] = (int)(cta_of(b * M) + b - s_lo);  // first slot of example b, relative to s_lo
+            s_nc[bb] = (int)(cta_of((b + 1) * M - 1) - cta_of(b * M) + 1);
+        }
+        __syncthreads();
+        const int items = (int)nb * ncol;
+        const Acc* sa = reinterpret_cast<const Acc*>(stg);
+        for (int it = threadIdx.x; it < items; it += nthreads) {
+            const int bb = it / ncol;
+            const int j = it - bb * ncol;
+            const Acc* sg = sa + (size_t)s_cs[bb] * 2 * ncol + j;
+            const int nc = s_nc[bb];
+            double vg = 0.0, vb = 0.0;
+            for (int c = 0; c < nc; ++c) {
+                vg += (double)sg[c * 2 * ncol];
+                vb += (double)sg[c * 2 * ncol + ncol];
             }
-            if (cv) {
-                dgam[col] = (Acc)tg;
-                dbet[col] = (Acc)tb;
-            }
-            if constexpr (NORMS) {
-                const double fg = cv ? (double)(Acc)tg : 0.0, fb = cv ? (double)(Acc)tb : 0.0;
-                double qg = fg * fg, qb = fb * fb;
-#pragma unroll
-                for (int o = kChunk / 2; o > 0; o >>= 1) {
-                    qg += __shfl_xor_sync(0xffffu, qg, o);
-                    qb += __shfl_xor_sync(0xffffu, qb, o);
-                }
-                if (cl == 0) {
-                    a.qbig[(size_t)chunk * 2 + 0] = qg;
-                    a.qbig[(size_t)chunk * 2 + 1] = qb;
+            sv[bb * svs + j] = vg;
+            sv[bb * svs + ncol + j] = vb;
+        }
+        __syncthreads();
+        // one pass, two roles (no barrier between them): threads [0, nb) square
+        // and sum their example over this CTA's columns; threads [nb, nb + 2 ncol)
+        // add their column over the block's examples.  Both in fixed order.
+        {
+            const int t = threadIdx.x;
+            const int nroles = (NORMS ? (int)nb : 0) + 2 * ncol;
+            for (int r = t; r < nroles; r += nthreads) {
+                if (NORMS && r < nb) {
+                    const double* vg = sv + (size_t)r * svs;
+                    double qg = 0.0, qb = 0.0;
+#pragma unroll 4
+                    for (int j = 0; j < ncol; ++j) {
+                        qg = fma(vg[j], vg[j], qg);
+                        qb = fma(vg[ncol + j], vg[ncol + j], qb);
+                    }
+                    a.q[((size_t)(b0 + r) * grid + cta) * 2 + 0] = qg;
+                    a.q[((size_t)(b0 + r) * grid + cta) * 2 + 1] = qb;
+                } else {
+                    const int j = r - (NORMS ? (int)nb : 0);
+                    const int h = j / ncol, jj = j - h * ncol;
+                    double acc = 0.0;
+#pragma unroll 8
+                    for (int64_t bb = 0; bb < nb; ++bb) acc += sv[bb * svs + h * ncol + jj];
+                    colsum[j] += acc;
                 }
             }
         }
         __syncthreads();
     }
+    if (warp == 0) {
+        Acc* dgam = static_cast<Acc*>(a.dgamma);
+        Acc* dbet = static_cast<Acc*>(a.dbeta);
+        double qg = 0.0, qb = 0.0;
+        for (int j = lane; j < ncol; j += 32) {
+            const int64_t col = (int64_t)u0 * V + j;
+            if (col >= D) continue;
+            const Acc fg = (Acc)colsum[j], fb = (Acc)colsum[ncol + j];
+            dgam[col] = fg;
+            dbet[col] = fb;
+            qg = fma((double)fg, (double)fg, qg);
+            qb = fma((double)fb, (double)fb, qb);
+        }
+        if constexpr (NORMS) {
+            qg = warp_sum(qg);
+            qb = warp_sum(qb);
+            if (lane == 0) {
+                a.qbig[(size_t)cta * 2 + 0] = qg;
+                a.qbig[(size_t)cta * 2 + 1] = qb;
+            }
+        }
+    }
+    stamp(2);
+    if constexpr (!NORMS) return;
 
     // ------------------------------------------------------- final ticket --
     __shared__ unsigned s_last;
     __syncthreads();
-    stamp(4);
     if (threadIdx.x == 0) {
         __threadfence();
-        const unsigned t = atomicAdd(&a.counters[1], 1u);
+        const unsigned t = atomicAdd(a.ticket, 1u);
         s_last = (t == (unsigned)grid - 1u) ? 1u : 0u;
     }
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    if constexpr (NORMS) {
-        const int nwarps = nthreads / 32;
-        for (int64_t b = warp; b < B; b += nwarps) {
+    stamp(3);
+    // raw_b = sum over the grid's column ranges: lane l adds c = l, l+32, ...
+    // in order, then a fixed butterfly.  Each warp takes kBW examples at a
+    // time with every load (and warp 0's qbig loads) issued before the first
+    // add, so for B <= kBW * warps the whole fold is one L2 round trip.
+    constexpr int KC = (kMaxReduceGrid + 31) / 32;
+    constexpr int kBW = 4;
+    double qbg[KC], qbb[KC];
+#pragma unroll
+    for (int k = 0; k < KC; ++k) {
+        const int c = lane + 32 * k;
+        const bool ok = warp == 0 && c < grid;
+        qbg[k] = ok ? __ldcg(a.qbig + (size_t)c * 2 + 0) : 0.0;
+        qbb[k] = ok ? __ldcg(a.qbig + (size_t)c * 2 + 1) : 0.0;
+    }
+    for (int64_t b0 = 0; b0 < B; b0 += (int64_t)nwarps * kBW) {
+        double lg[kBW][KC], lb[kBW][KC];
+#pragma unroll
+        for (int i = 0; i < kBW; ++i) {
+            const int64_t b = b0 + warp + (int64_t)i * nwarps;
+#pragma unroll
+            for (int k = 0; k < KC; ++k) {
+                const int c = lane + 32 * k;
+                const bool ok = b < B && c < grid;
+                lg[i][k] = ok ? __ldcg(a.q + ((size_t)b * grid + c) * 2 + 0) : 0.0;
+                lb[i][k] = ok ? __ldcg(a.q + ((size_t)b * grid + c) * 2 + 1) : 0.0;
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < kBW; ++i) {
+            const int64_t b = b0 + warp + (int64_t)i * nwarps;
             double rg = 0.0, rb = 0.0;
-            for (int ch = lane; ch < a.nchunks; ch += 32) {
-                rg += __ldcg(a.q + ((size_t)b * a.nchunks + ch) * 2 + 0);
-                rb += __ldcg(a.q + ((size_t)b * a.nchunks + ch) * 2 + 1);
+#pragma unroll
+            for (int k = 0; k < KC; ++k) {
+                rg += lg[i][k];
+                rb += lb[i][k];
             }
             rg = warp_sum(rg);
             rb = warp_sum(rb);
-            if (lane == 0) {
-                a.rawws[b * 2 + 0] = rg;
-                a.rawws[b * 2 + 1] = rb;
+            if (lane == 0 && b < B) {
+                if (b < kMaxReduceEb) {
+                    s_raw[0][b] = rg;
+                    s_raw[1][b] = rb;
+                } else {
+                    a.rawws[b * 2 + 0] = rg;
+                    a.rawws[b * 2 + 1] = rb;
+                }
                 if (a.raw_g) a.raw_g[b] = rg;
                 if (a.raw_b) a.raw_b[b] = rb;
             }
         }
-        __syncthreads();
-        if (warp == 0 && a.sums != nullptr) {
-            double tg = 0.0, tb = 0.0, bg = 0.0, bb = 0.0;
-            for (int64_t b = lane; b < B; b += 32) {
-                tg += a.rawws[b * 2 + 0];
-                tb += a.rawws[b * 2 + 1];
-            }
-            for (int ch = lane; ch < a.nchunks; ch += 32) {
-                bg += __ldcg(a.qbig + (size_t)ch * 2 + 0);
-                bb += __ldcg(a.qbig + (size_t)ch * 2 + 1);
-            }
-            tg = warp_sum(tg);
-            tb = warp_sum(tb);
-            bg = warp_sum(bg);
-            bb = warp_sum(bb);
-            if (lane == 0) {
-                a.sums[0] = tg;
-                a.sums[1] = tb;
-                a.sums[2] = bg;
-                a.sums[3] = bb;
-            }
+    }
+    __syncthreads();
+    if (warp == 0 && a.sums != nullptr) {
+        double tg = 0.0, tb = 0.0, bg = 0.0, bb = 0.0;
+        for (int64_t b = lane; b < B; b += 32) {
+            tg += b < kMaxReduceEb ? s_raw[0][b] : __ldcg(a.rawws + b * 2 + 0);
+            tb += b < kMaxReduceEb ? s_raw[1][b] : __ldcg(a.rawws + b * 2 + 1);
+        }
+#pragma unroll
+        for (int k = 0; k < KC; ++k) {
+            bg += qbg[k];
+            bb += qbb[k];
+        }
+        tg = warp_sum(tg);
+        tb = warp_sum(tb);
+        bg = warp_sum(bg);
+        bb = warp_sum(bb);
+        if (lane == 0) {
+            a.sums[0] = tg;
+            a.sums[1] = tb;
+            a.sums[2] = bg;
+            a.sums[3] = bb;
         }
     }
     if (threadIdx.x == 0) {
-        a.counters[0] = 0u;
-        a.counters[1] = 0u;
+        *a.ticket = 0u;
         __threadfence();
     }
-    stamp(5);
+    stamp(4);
 }
 
 }  // namespace gnsb

@@ -3,6 +3,8 @@
 // template instantiations compile in parallel.
 #pragma once
 
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <utility>
@@ -26,23 +28,17 @@ inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 inline bool ptr16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-// Per-(kernel, device) "max dynamic smem" attribute, set lazily.
-inline cudaError_t ensure_smem(const void* kernel, size_t bytes) {
-    static std::mutex mu;
-    static std::map<std::pair<const void*, int>, size_t> set_for;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    std::lock_guard<std::mutex> lk(mu);
-    auto& cur = set_for[{kernel, dev}];
-    if (cur >= bytes) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    if (e == cudaSuccess) cur = bytes;
-    return e;
-}
+// "max dynamic smem" attribute of a kernel: ensure_smem_attr (capi.cu) keeps
+// ONE process-wide record per (kernel, device) and only ever raises the
+// attribute.  (A per-translation-unit cache is wrong here: the reduce kernel
+// template is instantiated in several TUs but is one device function, so a
+// TU that set a smaller value would lower another TU's setting.)
+inline cudaError_t ensure_smem(const void* kernel, size_t bytes) { return ensure_smem_attr(kernel, bytes); }
 
 struct BwdPlan {
-    int Dp = 0, stages = 0, threads = 0, grid = 0, nchunks = 0, G = 0;
-    size_t smem = 0;
+    int Dp = 0, stages = 0, threads = 0, grid = 0, G = 0;
+    int rgrid = 0, rthreads = 256, eb = 0;  // stage-2 (reduce) kernel
+    size_t smem = 0, rsmem = 0;
     size_t off_partial = 0, off_q = 0, off_qbig = 0, off_raw = 0, total = 0;
 };
 
@@ -71,14 +67,38 @@ int plan_bwd(int64_t B, int64_t M, int64_t D, BwdPlan& p, const char** why) {
     const int sms = device_sm_count();
     p.grid = (int)(N < sms ? N : sms);
     if (p.grid < 1) p.grid = 1;
-    p.nchunks = (int)((D + kChunk - 1) / kChunk);
+    // reduce kernel: one contiguous range of 16-byte column vectors per CTA
+    constexpr int V = 16 / sizeof(Acc);
+    const int64_t U = (p.Dp + V - 1) / V;
+    // (at least four vectors per CTA: below that the per-CTA fixed cost and the
+    // final fold over CTAs dominate)
+    int64_t rg = (U + 3) / 4;
+    if (rg > sms) rg = sms;
+    if (rg > kMaxReduceGrid) rg = kMaxReduceGrid;
+    p.rgrid = (int)(rg < 1 ? 1 : rg);
+    const int64_t ncol = (U + p.rgrid - 1) / p.rgrid * V;
+    // examples per shared-memory block: as many as fit 160 KB with their slots
+    const int64_t rows_per_cta = N / p.grid;  // floor; a block of eb examples spans <= eb*M/rows_per_cta + 2 CTAs
+    auto layout = [&](int64_t eb) {
+        const int64_t span = rows_per_cta > 0 ? (eb * M + rows_per_cta - 1) / rows_per_cta + 2 : N;
+        LnRedLayout l{ncol, eb, span + eb};
+        return l;
+    };
+    int64_t eb = B < kMaxReduceEb ? B : kMaxReduceEb;
+    while (eb > 1 && layout(eb).bytes(sizeof(Acc)) > (size_t)(160 << 10)) eb = (eb + 1) / 2;
+    if (layout(eb).bytes(sizeof(Acc)) > budget) {
+        *why = "layers: trailing extent too wide for the stage-2 shared memory";
+        return 1;
+    }
+    p.eb = (int)eb;
+    p.rsmem = layout(eb).bytes(sizeof(Acc));
     size_t off = 256;  // counters
     p.off_partial = off;
-    off = align_up(off + (size_t)(sms + B) * G * 2 * p.Dp * sizeof(Acc), 256);
+    off = align_up(off + (size_t)(p.grid + B) * G * 2 * p.Dp * sizeof(Acc), 256);
     p.off_q = off;
-    off = align_up(off + (size_t)B * p.nchunks * 2 * sizeof(double), 256);
+    off = align_up(off + (size_t)B * p.rgrid * 2 * sizeof(double), 256);
     p.off_qbig = off;
-    off = align_up(off + (size_t)p.nchunks * 2 * sizeof(double), 256);
+    off = align_up(off + (size_t)p.rgrid * 2 * sizeof(double), 256);
     p.off_raw = off;
     off = align_up(off + (size_t)B * 2 * sizeof(double), 256);
     p.total = off;
@@ -115,11 +135,8 @@ struct BwdOp {
             }
         }
         if (plan_bwd<C>(B, M, D, p, why)) return 1;
-        // one CTA per SM must fit (cooperative launch); shrink the ring if not.
-        // All four kernel variants share geometry and shared memory: set the
-        // attribute on each, check occupancy on the largest (fused) one.
-        void (*ks[4])(LnBwdArgs) = {ln_bwd_kernel<C, true, true>, ln_bwd_kernel<C, true, false>,
-                                    ln_bwd_kernel<C, false, true>, ln_bwd_kernel<C, false, false>};
+        // one CTA per SM must fit; shrink the ring if not
+        void (*ks[2])(LnBwdArgs) = {ln_bwd_kernel<C, true>, ln_bwd_kernel<C, false>};
         for (;;) {
             cudaError_t e = cudaSuccess;
             for (auto k : ks)
@@ -128,11 +145,12 @@ struct BwdOp {
             if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ks[0], p.threads, p.smem);
             if (e != cudaSuccess) {
                 *cerr = e;
+                *why = "ln_bwd plan (smem attribute / occupancy)";
                 return 2;
             }
             if (occ >= 1) break;
             if (p.stages <= 2) {
-                *cerr = cudaErrorCooperativeLaunchTooLarge;
+                *cerr = cudaErrorLaunchOutOfResources;
                 return 2;
             }
             --p.stages;
@@ -150,6 +168,7 @@ struct BwdOp {
             *why = "layers: workspace too small (query gnsb_ln_bwd_workspace_size)";
             return 1;
         }
+        using Acc = typename C::Acc;
         LnBwdArgs a{};
         a.x = c.x;
         a.mean = c.mean;
@@ -157,11 +176,6 @@ struct BwdOp {
         a.dy = c.dy;
         a.gamma = c.gamma;
         a.dx = c.dx;
-        a.dgamma = c.dgamma;
-        a.dbeta = c.dbeta;
-        a.raw_g = c.raw_g;
-        a.raw_b = c.raw_b;
-        a.sums = c.sums;
         a.B = c.B;
         a.M = c.M;
         a.N = c.B * c.M;
@@ -170,34 +184,68 @@ struct BwdOp {
         a.stages = p.stages;
         a.aligned = ((c.D * (int64_t)sizeof(T)) % 16 == 0) && ptr16(c.x) && ptr16(c.dy) && (c.dx == nullptr || ptr16(c.dx));
         unsigned char* ws = static_cast<unsigned char*>(c.ws);
-        a.counters = reinterpret_cast<unsigned*>(ws);
         a.partial = ws + p.off_partial;
-        a.q = reinterpret_cast<double*>(ws + p.off_q);
-        a.qbig = reinterpret_cast<double*>(ws + p.off_qbig);
-        a.rawws = reinterpret_cast<double*>(ws + p.off_raw);
-        a.nchunks = p.nchunks;
-        a.scratch_bytes = (int64_t)(p.smem - C::rows_off(p.stages, p.Dp));
         a.trace = c.trace;
 
-        void (*k)(LnBwdArgs) = nullptr;
-        const bool hm = c.mean != nullptr;
-        if (hm && c.norms) k = ln_bwd_kernel<C, true, true>;
-        else if (hm) k = ln_bwd_kernel<C, true, false>;
-        else if (c.norms) k = ln_bwd_kernel<C, false, true>;
-        else k = ln_bwd_kernel<C, false, false>;
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(p.grid);
-        cfg.blockDim = dim3(p.threads);
-        cfg.dynamicSmemBytes = p.smem;
-        cfg.stream = st;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeCooperative;
-        attr[0].val.cooperative = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        const cudaError_t e = cudaLaunchKernelEx(&cfg, k, a);
+        void (*k)(LnBwdArgs) = c.mean != nullptr ? ln_bwd_kernel<C, true> : ln_bwd_kernel<C, false>;
+        k<<<p.grid, p.threads, p.smem, st>>>(a);
+        cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) {
             *cerr = e;
+            *why = "ln_bwd rows launch";
+            return 2;
+        }
+
+        LnRedArgs r{};
+        r.partial = a.partial;
+        r.slot_stride = (int64_t)C::kG * 2 * p.Dp;
+        r.B = c.B;
+        r.M = c.M;
+        r.N = a.N;
+        r.D = c.D;
+        r.Dp = p.Dp;
+        r.grid_rows = p.grid;
+        r.eb = p.eb;
+        r.dgamma = c.dgamma;
+        r.dbeta = c.dbeta;
+        r.raw_g = c.raw_g;
+        r.raw_b = c.raw_b;
+        r.sums = c.sums;
+        r.q = reinterpret_cast<double*>(ws + p.off_q);
+        r.qbig = reinterpret_cast<double*>(ws + p.off_qbig);
+        r.rawws = reinterpret_cast<double*>(ws + p.off_raw);
+        r.ticket = reinterpret_cast<unsigned*>(ws) + 1;
+        r.trace = c.trace2;
+        void (*rk)(LnRedArgs) = c.norms ? ln_bwd_reduce_kernel<Acc, true> : ln_bwd_reduce_kernel<Acc, false>;
+        e = ensure_smem(reinterpret_cast<const void*>(rk), p.rsmem);
+        if (e != cudaSuccess) {
+            *cerr = e;
+            *why = "ln_bwd reduce smem attribute";
+            return 2;
+        }
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(p.rgrid);
+        cfg.blockDim = dim3(p.rthreads);
+        cfg.dynamicSmemBytes = p.rsmem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, rk, r);
+        if (e != cudaSuccess) {
+            *cerr = e;
+            *why = "ln_bwd reduce launch";
+            if (std::getenv("GNSB_DEBUG")) {
+                cudaFuncAttributes fa{};
+                cudaFuncGetAttributes(&fa, rk);
+                std::fprintf(stderr,
+                             "gnsb: reduce launch failed: grid=%d threads=%d dyn_smem=%zu static=%zu max_dyn=%d "
+                             "eb=%d B=%lld M=%lld D=%lld rows_grid=%d stream=%p err=%s\n",
+                             p.rgrid, p.rthreads, p.rsmem, fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes, p.eb,
+                             (long long)c.B, (long long)c.M, (long long)c.D, p.grid, (void*)st, cudaGetErrorString(e));
+            }
             return 2;
         }
         return 0;
@@ -206,7 +254,7 @@ struct BwdOp {
 
 template <typename T, int GW, int VPT>
 struct FwdOp {
-    static int run(const LnFwdCall& c, cudaStream_t st, const char**, cudaError_t* cerr) {
+    static int run(const LnFwdCall& c, cudaStream_t st, const char** why, cudaError_t* cerr) {
         using F = LnFwdCfg<T, GW, VPT>;
         LnFwdArgs a{};
         a.x = c.x;
@@ -230,6 +278,7 @@ struct FwdOp {
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) {
             *cerr = e;
+            *why = "ln_fwd launch";
             return 2;
         }
         return 0;
@@ -247,7 +296,7 @@ R dispatch_bwd(int64_t D, const char** why, R bad, A&&... args) {
     if (nv <= 64) return Op<LnBwdCfg<T, 2, 1, 8, 1, true>>::call(args...);
     if (nv <= 96) return Op<LnBwdCfg<T, 3, 1, 5, 2, true>>::call(args...);
     if (nv <= 128) return Op<LnBwdCfg<T, 4, 1, 4, 2, true>>::call(args...);
-    if (nv <= 256) return Op<LnBwdCfg<T, 4, 2, 3, 1, true>>::call(args...);
+    if (nv <= 256) return Op<LnBwdCfg<T, 8, 1, 2, 2, true>>::call(args...);
     if (nv <= 512) return Op<LnBwdCfg<T, 8, 2, 1, 2, true, 1>>::call(args...);
     if (nv <= 1024) return Op<LnBwdCfg<T, 16, 2, 1, 1, true, 1>>::call(args...);
     if (nv <= 2048) return Op<LnBwdCfg<T, 16, 4, 1, 1, false>>::call(args...);

@@ -123,3 +123,36 @@ def test_cfg3_full_size_sampled(orc, cuda):
     ref_dW = torch.einsum("btk,btl->kl", x.double(), g.double())
     dW = r.grads.weight_grads["weight"].double()
     assert float((dW - ref_dW).abs().max()) <= 1e-4 * float(ref_dW.abs().max())
+
+
+@pytest.mark.parametrize("B,T,K,L", [(2, 128, 64, 64), (3, 256, 128, 192), (1, 384, 256, 128), (5, 128, 320, 64)])
+def test_tcgen05_gram_form_matches_oracle(orc, cuda, B, T, K, L):
+    """Tensor-core Gram form (bf16 rows, T % 128 == 0, K, L % 64 == 0) vs the fp64
+    oracle's <X X^T, G G^T>_F on identical inputs (rel 1e-4)."""
+    import paper_2411_00999_b200 as m
+    from paper_2411_00999_b200 import linear
+
+    x, g = m.synth_linear(B, T, K, L, torch.bfloat16, cuda)
+    f = linear.linear_perexample_sqnorm_frobenius(x, g)
+    ref = orc.linear_frobenius(x.double().cpu().numpy(), g.double().cpu().numpy())
+    torch.cuda.synchronize()
+    assert close(f.cpu().numpy(), ref, 1e-4)
+
+
+def test_tcgen05_gram_form_cfg3_sampled(cuda):
+    """BASELINE config 3 through the Gram form: every per-example norm against an
+    fp64 torch contraction of that example's weight gradient, and the two forms
+    agree."""
+    import paper_2411_00999_b200 as m
+    from paper_2411_00999_b200 import linear
+
+    B, T, K, L = 16, 2048, 4096, 4096
+    x, g = m.synth_linear(B, T, K, L, torch.bfloat16, cuda)
+    f = linear.linear_perexample_sqnorm_frobenius(x, g).cpu().numpy()
+    r = linear.linear_backward_simultaneous(linear.LinearLayer(torch.zeros(K, L, device=cuda)), x, g,
+                                            need_input_grad=False)
+    raw = r.grads.per_example_sqnorms_raw["weight"].cpu().numpy()
+    assert close(f, raw, 1e-4)
+    for b in (0, 7, 15):
+        dWb = x[b].double().T @ g[b].double()
+        assert close(f[b], float((dWb * dWb).sum()), 1e-4)
