@@ -4,6 +4,12 @@
 #include "../paper_2411_00999_b200/csrc/ln_launch.cuh"
 
 namespace gnsb {
+cudaError_t ensure_smem_attr(const void* kernel, size_t bytes) {
+    cudaFuncAttributes fa{};
+    cudaError_t e = cudaFuncGetAttributes(&fa, kernel);
+    if (e != cudaSuccess || (size_t)fa.maxDynamicSharedSizeBytes >= bytes) return e;
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
 int device_sm_count() {
     int v = 0, dev = 0;
     cudaGetDevice(&dev);

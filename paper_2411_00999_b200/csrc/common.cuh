@@ -285,6 +285,24 @@ __device__ __forceinline__ V warp_sum(V v) {
     return v;
 }
 
+// N independent butterfly sums, interleaved stage by stage (latency overlap);
+// each result equals warp_sum of that element.
+template <int N, typename V>
+__device__ __forceinline__ void warp_sum_n(V (&v)[N]) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int i = 0; i < N; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+}
+
+// Atomic add with acquire-release semantics at GPU scope (the "last CTA"
+// ticket: releases this CTA's prior writes, acquires every earlier CTA's).
+__device__ __forceinline__ unsigned atomic_add_acq_rel_gpu(unsigned* p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

@@ -175,6 +175,10 @@ __global__ void __launch_bounds__(C::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a
         for (size_t i = threadIdx.x; i < n16; i += blockDim.x) p[i] = make_uint4(0, 0, 0, 0);
     }
     __syncthreads();
+    // Launched with programmatic dependent launch: everything above overlaps
+    // the previous kernel in the stream; no global memory is touched before
+    // the previous grid has completed and its writes are visible.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     // ------------------------------------------------------------ producer --
     // Fill stage `st` into its slot.  Called by warp 0 only (lane 0 issues the
@@ -539,6 +543,7 @@ __global__ void __launch_bounds__(C::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a
 // backward's reduction (dgamma/dbeta only).
 constexpr int kMaxReduceGrid = 160;  // >= the B200's 148 SMs; bounds the final fold's unrolling
 constexpr int kMaxReduceEb = 512;    // examples per shared-memory block
+constexpr int kReduceThreads = 512;
 
 struct LnRedLayout {  // shared-memory carve-up of the reduce kernel (host + device)
     int64_t ncol, eb, nslot_max;
@@ -552,7 +557,7 @@ struct LnRedLayout {  // shared-memory carve-up of the reduce kernel (host + dev
 };
 
 template <typename Acc, bool NORMS>
-__global__ void __launch_bounds__(256) ln_bwd_reduce_kernel(LnRedArgs a) {
+__global__ void __launch_bounds__(kReduceThreads) ln_bwd_reduce_kernel(LnRedArgs a) {
     constexpr int V = 16 / sizeof(Acc);  // columns per 16-byte vector
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -579,6 +584,9 @@ __global__ void __launch_bounds__(256) ln_bwd_reduce_kernel(LnRedArgs a) {
     };
 
     for (int j = threadIdx.x; j < 2 * ncol; j += nthreads) colsum[j] = 0.0;
+    // the next kernel in the stream may start its prologue now (it waits for
+    // this grid before touching global memory)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     // the row kernel's slots are complete and visible after this
     asm volatile("griddepcontrol.wait;" ::: "memory");
     stamp(0);
@@ -691,13 +699,15 @@ __global__ void __launch_bounds__(256) ln_bwd_reduce_kernel(LnRedArgs a) {
     __shared__ unsigned s_last;
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
-        const unsigned t = atomicAdd(a.ticket, 1u);
+        // release: the barrier above orders every thread's q/qbig stores
+        // before this (cumulative) gpu-scope release; acquire: the last CTA
+        // sees every other CTA's stores, and the barrier below passes that
+        // on to its threads
+        const unsigned t = atomic_add_acq_rel_gpu(a.ticket, 1u);
         s_last = (t == (unsigned)grid - 1u) ? 1u : 0u;
     }
     __syncthreads();
     if (!s_last) return;
-    __threadfence();
     stamp(3);
     // raw_b = sum over the grid's column ranges: lane l adds c = l, l+32, ...
     // in order, then a fixed butterfly.  Each warp takes kBW examples at a
@@ -726,17 +736,23 @@ __global__ void __launch_bounds__(256) ln_bwd_reduce_kernel(LnRedArgs a) {
                 lb[i][k] = ok ? __ldcg(a.q + ((size_t)b * grid + c) * 2 + 1) : 0.0;
             }
         }
+        double rr[2 * kBW];
 #pragma unroll
         for (int i = 0; i < kBW; ++i) {
-            const int64_t b = b0 + warp + (int64_t)i * nwarps;
             double rg = 0.0, rb = 0.0;
 #pragma unroll
             for (int k = 0; k < KC; ++k) {
                 rg += lg[i][k];
                 rb += lb[i][k];
             }
-            rg = warp_sum(rg);
-            rb = warp_sum(rb);
+            rr[2 * i] = rg;
+            rr[2 * i + 1] = rb;
+        }
+        warp_sum_n(rr);
+#pragma unroll
+        for (int i = 0; i < kBW; ++i) {
+            const int64_t b = b0 + warp + (int64_t)i * nwarps;
+            const double rg = rr[2 * i], rb = rr[2 * i + 1];
             if (lane == 0 && b < B) {
                 if (b < kMaxReduceEb) {
                     s_raw[0][b] = rg;
@@ -762,21 +778,16 @@ __global__ void __launch_bounds__(256) ln_bwd_reduce_kernel(LnRedArgs a) {
             bg += qbg[k];
             bb += qbb[k];
         }
-        tg = warp_sum(tg);
-        tb = warp_sum(tb);
-        bg = warp_sum(bg);
-        bb = warp_sum(bb);
+        double t4[4] = {tg, tb, bg, bb};
+        warp_sum_n(t4);
         if (lane == 0) {
-            a.sums[0] = tg;
-            a.sums[1] = tb;
-            a.sums[2] = bg;
-            a.sums[3] = bb;
+            a.sums[0] = t4[0];
+            a.sums[1] = t4[1];
+            a.sums[2] = t4[2];
+            a.sums[3] = t4[3];
         }
     }
-    if (threadIdx.x == 0) {
-        *a.ticket = 0u;
-        __threadfence();
-    }
+    if (threadIdx.x == 0) *a.ticket = 0u;  // (visible to the next kernel at grid completion)
     stamp(4);
 }
 

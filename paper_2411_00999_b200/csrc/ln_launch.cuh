@@ -37,7 +37,7 @@ inline cudaError_t ensure_smem(const void* kernel, size_t bytes) { return ensure
 
 struct BwdPlan {
     int Dp = 0, stages = 0, threads = 0, grid = 0, G = 0;
-    int rgrid = 0, rthreads = 256, eb = 0;  // stage-2 (reduce) kernel
+    int rgrid = 0, rthreads = kReduceThreads, eb = 0;  // stage-2 (reduce) kernel
     size_t smem = 0, rsmem = 0;
     size_t off_partial = 0, off_q = 0, off_qbig = 0, off_raw = 0, total = 0;
 };
@@ -188,8 +188,17 @@ struct BwdOp {
         a.trace = c.trace;
 
         void (*k)(LnBwdArgs) = c.mean != nullptr ? ln_bwd_kernel<C, true> : ln_bwd_kernel<C, false>;
-        k<<<p.grid, p.threads, p.smem, st>>>(a);
-        cudaError_t e = cudaGetLastError();
+        cudaLaunchAttribute pdl[1];
+        pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        pdl[0].val.programmaticStreamSerializationAllowed = 1;
+        cudaLaunchConfig_t kcfg = {};
+        kcfg.gridDim = dim3(p.grid);
+        kcfg.blockDim = dim3(p.threads);
+        kcfg.dynamicSmemBytes = p.smem;
+        kcfg.stream = st;
+        kcfg.attrs = pdl;
+        kcfg.numAttrs = 1;
+        cudaError_t e = cudaLaunchKernelEx(&kcfg, k, a);
         if (e != cudaSuccess) {
             *cerr = e;
             *why = "ln_bwd rows launch";

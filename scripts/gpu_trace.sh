@@ -1,5 +1,4 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -25 > gpurun_out/pytest_gpu.log
-LD_LIBRARY_PATH=paper_2411_00999_b200/lib timeout 300 ./tests/cpp/test_dropin > gpurun_out/cpptest.log 2>&1; echo "cpptest rc=$?" >> gpurun_out/cpptest.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
-timeout 900 python bench.py > gpurun_out/bench.log 2>&1
+timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -5 > gpurun_out/pytest_gpu.log
+SWEEP_TRACE=1 timeout 300 python experiments/ln_sweep.py 768,1024,2048,4096,8192 15,10,5,0,2 > gpurun_out/trace.log 2>&1
+timeout 600 python bench.py --no-cpu --no-extra > gpurun_out/bench.log 2>&1
