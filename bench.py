@@ -425,8 +425,9 @@ def run_cfg3(m, lib, dev, torch, np):
             if rc:
                 raise RuntimeError(lib.gnsb_last_error().decode())
         ms = time_graph(fn, torch, np, dev)
-        # algorithmic FLOPs: weight-grad 2BTKL; Gram (symmetric, i <= j tile pairs) B*T*(T+128)*(K+L)
-        fl = 2.0 * B * T_ * K * L if form == 1 else 1.0 * B * T_ * (T_ + 128) * (K + L)
+        # algorithmic FLOPs: weight-grad form 2BTKL; Gram form with symmetry
+        # B*T^2*(K+L) (half of 2BT^2(K+L); the kernel executes ~12% more: 128x256 blocks on the diagonal)
+        fl = 2.0 * B * T_ * K * L if form == 1 else 1.0 * B * T_ * T_ * (K + L)
         out[name] = {"us": ms * 1e3, "TFLOPs": fl / (ms * 1e-3) / 1e12, "frac_of_bf16_peak": fl / (ms * 1e-3) / 1e12 / peak,
                      "flops": fl}
     out["faster_form"] = min(("weight_grad", "gram"), key=lambda k: out[k]["us"])

@@ -21,6 +21,7 @@ from .layers import (
     synth_linear,
     synth_ln,
 )
+from .nn import GnsTracker, LayerNormPE
 from .linear import LinearBackwardResult, LinearLayer, linear_backward_simultaneous, linear_perexample_sqnorm_frobenius
 from .gns import (
     DeviceGnsAccumulator,
@@ -40,5 +41,5 @@ __all__ = [
     "layernorm_backward_simultaneous", "layernorm_forward", "ln_bwd_geometry", "sqnorm", "synth_linear", "synth_ln",
     "DeviceGnsAccumulator", "EmaState", "GnsEstimate", "GradStats", "aggregate", "ema_update", "estimate_g2",
     "estimate_s", "make_gns_estimate", "smoothed_gns", "LinearBackwardResult", "LinearLayer",
-    "linear_backward_simultaneous", "linear_perexample_sqnorm_frobenius",
+    "linear_backward_simultaneous", "linear_perexample_sqnorm_frobenius", "GnsTracker", "LayerNormPE",
 ]

@@ -5,27 +5,29 @@
 // (proj/src/layers.cpp:159-187):
 //     raw_b = < X_b X_b^T , G_b G_b^T >_F = sum_{t,u} (x_t . x_u)(g_t . g_u)
 // which equals ||sum_t x_t^T g_t||_F^2, the weight-gradient form's norm
-// (SPEC.md:157), at 2*T^2*(K+L) instead of 2*T*K*L FLOPs per example — and
-// half of that here, because both Grams are symmetric: only tile pairs
-// (i <= j) of the T x T grid are formed, off-diagonal pairs counted twice.
+// (SPEC.md:157), at 2*T^2*(K+L) instead of 2*T*K*L FLOPs per example — about
+// half of that here, because both Grams are symmetric.
 //
 // Kernel (gram_norms_kernel): persistent, one CTA per SM, static round-robin
-// over units (example b, tile pair i <= j) in example-major order, so all
-// CTAs work on the same example at once and X_b, G_b (2 x 16 MB at cfg3) are
-// shared through L2.
+// over units (example b, 128-token row tile i, 256-token column block J) with
+// 2J+1 >= i, i.e. every 128 x 128 tile pair (i, j) with j >= i is covered once
+// (the few j < i halves of blocks straddling the diagonal get weight 0),
+// example-major so all CTAs work on the same example and X_b, G_b (2 x 16 MB
+// at cfg3) are shared through L2.  M = 128, N = 256: per 64-feature stage the
+// MMA reads 48 KB of shared memory for 4.2 MFLOP, which keeps the tensor pipe
+// ahead of the shared-memory operand bandwidth (an N = 128 tile does not).
 //   * warp 0: TMA producer.  Rows t of X_b / G_b are K-major operands read
 //     straight from the [B, T, K] / [B, T, L] row-major tensors through 3-D
-//     tensor maps (box 64 features x 128 tokens, 128-byte swizzle); a diagonal
-//     pair loads its tile once and uses it as both operands;
-//   * warp 1: one thread issues tcgen05.mma (M=N=128, K=16, bf16 -> fp32):
-//     the X-Gram tile over K into TMEM columns [0,128) of the unit's buffer,
-//     then the G-Gram tile over L into [128,256); two buffers (all 512 TMEM
-//     columns) alternate between units so the epilogue of one unit overlaps
-//     the MMAs of the next;
-//   * warps 2..5: epilogue.  tcgen05.ld both tiles, sum of products per TMEM
-//     lane (fp32), fixed-order fold over the 4 warps in fp64 -> q[b][pair]
-//     (x2 off the diagonal).  A deterministic second kernel folds q over the
-//     pairs of each example.  No floating-point atomics.
+//     tensor maps (boxes 64 features x 128 / 256 tokens, 128-byte swizzle;
+//     tokens past T read as zero);
+//   * warp 1: one thread issues tcgen05.mma (M=128, N=256, K=16, bf16 -> fp32):
+//     the X-Gram block over K into TMEM columns [0,256), then the G-Gram block
+//     over L into [256,512);
+//   * warps 2..5: epilogue.  tcgen05.ld both blocks, per-half weighted sum of
+//     products per TMEM lane (fp32; weight 2 above the diagonal, 1 on it, 0
+//     below), fixed-order fold over the 4 warps in fp64 -> q[b][unit].  A
+//     deterministic second kernel folds q over each example's units.  No
+//     floating-point atomics.
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -38,49 +40,54 @@
 namespace gnsb {
 
 namespace gr {
-constexpr int BM = 128;                      // token tile (both Gram dimensions)
+constexpr int BM = 128;                      // token tile of the Gram rows (i)
+constexpr int BN = 256;                      // token block of the Gram columns (J): two 128-tiles
 constexpr int BK = 64;                       // features per stage: one 128-byte swizzle row
-constexpr int STAGES = 6;
-constexpr int OP_BYTES = BM * BK * 2;        // 16 KB
-constexpr int STAGE_BYTES = 2 * OP_BYTES;    // 32 KB
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;         // 16 KB
+constexpr int B_BYTES = BN * BK * 2;         // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int EPI_WARPS = 4;
 constexpr int THREADS = (2 + EPI_WARPS) * 32;
 constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 1024;
-constexpr int TMEM_COLS = 512;
+constexpr int TMEM_COLS = 512;               // X-Gram block [0, 256) + G-Gram block [256, 512)
 }  // namespace gr
 
 struct GramArgs {
     int B, T, K, L;
-    int nt;        // T / BM
-    int npairs;    // nt * (nt + 1) / 2
-    double* q;     // [B][npairs]
+    int nt;        // T / BM (row tiles)
+    int nJ;        // ceil(nt / 2) (column blocks)
+    int nunits;    // units per example: sum_i (nJ - i / 2)
+    double* q;     // [B][nunits]
 };
 
-// pair index p (row-major over i <= j) -> (i, j)
-__device__ __forceinline__ void pair_ij(int p, int nt, int& i, int& j) {
+// unit index p (row-major over i, then J >= i / 2) -> (i, J)
+__device__ __forceinline__ void unit_iJ(int p, int nt, int nJ, int& i, int& J) {
     i = 0;
-    while (p >= nt - i) {
-        p -= nt - i;
+    while (i < nt && p >= nJ - i / 2) {
+        p -= nJ - i / 2;
         ++i;
     }
-    j = i + p;
+    J = i / 2 + p;
 }
 
 __global__ void __launch_bounds__(gr::THREADS, 1)
-    gram_norms_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmg, GramArgs a) {
+    gram_norms_kernel(const __grid_constant__ CUtensorMap tmx_a, const __grid_constant__ CUtensorMap tmx_b,
+                      const __grid_constant__ CUtensorMap tmg_a, const __grid_constant__ CUtensorMap tmg_b,
+                      GramArgs a) {
     using namespace gr;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     unsigned char* ring = smem;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)STAGES * STAGE_BYTES);
     uint64_t* empty = full + STAGES;
-    uint64_t* tfull = empty + STAGES;  // [2]
-    uint64_t* tempty = tfull + 2;      // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
     double* red = reinterpret_cast<double*>(tmem_slot + 4);  // [EPI_WARPS]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t units = (int64_t)a.B * a.npairs;
+    const int64_t units = (int64_t)a.B * a.nunits;
     const int grid = gridDim.x, c = blockIdx.x;
     const int kbx = a.K / BK, kbg = a.L / BK;
 
@@ -89,13 +96,13 @@ __global__ void __launch_bounds__(gr::THREADS, 1)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        for (int s = 0; s < 2; ++s) {
-            mbar_init(&tfull[s], 1);
-            mbar_init(&tempty[s], EPI_WARPS);
-        }
+        mbar_init(tfull, 1);
+        mbar_init(tempty, EPI_WARPS);
         fence_mbar_init();
-        tc::prefetch_tmap(&tmx);
-        tc::prefetch_tmap(&tmg);
+        tc::prefetch_tmap(&tmx_a);
+        tc::prefetch_tmap(&tmx_b);
+        tc::prefetch_tmap(&tmg_a);
+        tc::prefetch_tmap(&tmg_b);
     }
     if (warp == 1) tc::tmem_alloc<TMEM_COLS>(tmem_slot);
     tc::fence_before_sync();
@@ -109,19 +116,20 @@ __global__ void __launch_bounds__(gr::THREADS, 1)
             int s = 0;
             uint32_t ph = 0;
             for (int64_t u = c; u < units; u += grid) {
-                const int b = (int)(u / a.npairs);
-                int i, j;
-                pair_ij((int)(u - (int64_t)b * a.npairs), a.nt, i, j);
-                const bool diag = i == j;
+                const int b = (int)(u / a.nunits);
+                int i, J;
+                unit_iJ((int)(u - (int64_t)b * a.nunits), a.nt, a.nJ, i, J);
                 for (int op = 0; op < 2; ++op) {  // 0: X over K, 1: G over L
-                    const CUtensorMap* m = op == 0 ? &tmx : &tmg;
+                    const CUtensorMap* ma = op == 0 ? &tmx_a : &tmg_a;
+                    const CUtensorMap* mb = op == 0 ? &tmx_b : &tmg_b;
                     const int nkb = op == 0 ? kbx : kbg;
                     for (int kb = 0; kb < nkb; ++kb) {
                         mbar_wait(&empty[s], ph ^ 1u);
                         unsigned char* st = ring + (size_t)s * STAGE_BYTES;
-                        mbar_arrive_expect_tx(&full[s], diag ? OP_BYTES : STAGE_BYTES);
-                        tc::tma_load_3d(st, m, kb * BK, i * BM, b, &full[s]);
-                        if (!diag) tc::tma_load_3d(st + OP_BYTES, m, kb * BK, j * BM, b, &full[s]);
+                        // full boxes always land (tokens past T are zero-filled)
+                        mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+                        tc::tma_load_3d(st, ma, kb * BK, i * BM, b, &full[s]);
+                        tc::tma_load_3d(st + A_BYTES, mb, kb * BK, J * BN, b, &full[s]);
                         if (++s == STAGES) {
                             s = 0;
                             ph ^= 1u;
@@ -133,24 +141,20 @@ __global__ void __launch_bounds__(gr::THREADS, 1)
     } else if (warp == 1) {
         // ------------------------------------------------------- MMA issuer --
         if (lane == 0) {
-            constexpr uint32_t idesc = tc::idesc_bf16(BM, BM, false, false);  // both K-major: D = A * B^T
-            int s = 0, buf = 0;
+            constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, false, false);  // both K-major: D = A * B^T
+            int s = 0;
             uint32_t ph = 0, tph = 0;
             for (int64_t u = c; u < units; u += grid) {
-                const int b = (int)(u / a.npairs);
-                int i, j;
-                pair_ij((int)(u - (int64_t)b * a.npairs), a.nt, i, j);
-                const bool diag = i == j;
-                mbar_wait(&tempty[buf], tph ^ 1u);  // epilogue drained this buffer
+                mbar_wait(tempty, tph ^ 1u);  // the epilogue drained the accumulators
                 tc::fence_after_sync();
                 for (int op = 0; op < 2; ++op) {
-                    const uint32_t dcol = tmem + (uint32_t)(buf * 2 * BM + op * BM);
+                    const uint32_t dcol = tmem + (uint32_t)(op * BN);
                     const int nkb = op == 0 ? kbx : kbg;
                     for (int kb = 0; kb < nkb; ++kb) {
                         mbar_wait(&full[s], ph);
                         tc::fence_after_sync();
                         const uint32_t abase = smem_u32(ring + (size_t)s * STAGE_BYTES);
-                        const uint32_t bbase = diag ? abase : abase + OP_BYTES;
+                        const uint32_t bbase = abase + A_BYTES;
 #pragma unroll
                         for (int k = 0; k < BK / 16; ++k) {
                             // K-major SW128: 8-row x 128-byte atoms, SBO = 1 KB; a K step of
@@ -166,54 +170,62 @@ __global__ void __launch_bounds__(gr::THREADS, 1)
                         }
                     }
                 }
-                tc::commit(&tfull[buf]);
-                if (++buf == 2) {
-                    buf = 0;
-                    tph ^= 1u;
-                }
+                tc::commit(tfull);
+                tph ^= 1u;
             }
         }
     } else {
         // --------------------------------------------------------- epilogue --
         const int e = warp - 2;
         const int quad = warp & 3;  // TMEM lanes this warp may access
-        int buf = 0;
         uint32_t tph = 0;
         for (int64_t u = c; u < units; u += grid) {
-            const int b = (int)(u / a.npairs);
-            const int p = (int)(u - (int64_t)b * a.npairs);
-            int i, j;
-            pair_ij(p, a.nt, i, j);
-            mbar_wait(&tfull[buf], tph);
+            const int b = (int)(u / a.nunits);
+            const int p = (int)(u - (int64_t)b * a.nunits);
+            int i, J;
+            unit_iJ(p, a.nt, a.nJ, i, J);
+            mbar_wait(tfull, tph);
+            tph ^= 1u;
             tc::fence_after_sync();
-            const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * 2 * BM);
-            float acc = 0.f;
+            const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16);
+            float w2[2];  // per 128-column half of the block
 #pragma unroll
-            for (int cc = 0; cc < BM / 32; ++cc) {
-                uint32_t rx[32], rg[32];
-                tc::tmem_ld_32x32b_x32(base + cc * 32, rx);
-                tc::tmem_ld_32x32b_x32(base + BM + cc * 32, rg);
-                tc::tmem_ld_wait();
+            for (int h = 0; h < 2; ++h) {
+                float acc = 0.f;
+#pragma unroll 1
+                for (int cc = 0; cc < BM / 32; ++cc) {
+                    uint32_t rx[32], rg[32];
+                    const uint32_t col = (uint32_t)(h * BM + cc * 32);
+                    tc::tmem_ld_32x32b_x32(base + col, rx);
+                    tc::tmem_ld_32x32b_x32(base + BN + col, rg);
+                    tc::tmem_ld_wait();
 #pragma unroll
-                for (int k = 0; k < 32; ++k) acc = fmaf(__uint_as_float(rx[k]), __uint_as_float(rg[k]), acc);
+                    for (int k = 0; k < 32; ++k) acc = fmaf(__uint_as_float(rx[k]), __uint_as_float(rg[k]), acc);
+                }
+                w2[h] = acc;
             }
             tc::fence_before_sync();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[buf]);
-            const float w = warp_sum(acc);
-            if (lane == 0) red[e] = (double)w;
+            if (lane == 0) mbar_arrive(tempty);
+            warp_sum_n(w2);
+            if (lane == 0) {
+                double t = 0.0;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int j = 2 * J + h;
+                    const double wgt = j < i ? 0.0 : (j == i ? 1.0 : 2.0);
+                    t += wgt * (double)w2[h];
+                }
+                red[e] = t;
+            }
             named_bar_sync(1, EPI_WARPS * 32);
             if (e == 0 && lane == 0) {
                 double t = 0.0;
 #pragma unroll
                 for (int k = 0; k < EPI_WARPS; ++k) t += red[k];
-                a.q[(size_t)b * a.npairs + p] = i == j ? t : 2.0 * t;
+                a.q[(size_t)b * a.nunits + p] = t;
             }
             named_bar_sync(1, EPI_WARPS * 32);
-            if (++buf == 2) {
-                buf = 0;
-                tph ^= 1u;
-            }
         }
     }
     __syncthreads();
@@ -243,57 +255,59 @@ EncodeFn encode_fn() {
     return fn;
 }
 
-// [B, T, F] bf16 row-major as a 3-D tensor (F innermost), box 64 features x 128 tokens, 128B swizzle
-bool make_map_rows(CUtensorMap* m, const void* base, int B, int T, int F) {
+// [B, T, F] bf16 row-major as a 3-D tensor (F innermost), box 64 features x `rows` tokens, 128B swizzle
+bool make_map_rows(CUtensorMap* m, const void* base, int B, int T, int F, int rows) {
     EncodeFn enc = encode_fn();
     if (!enc) return false;
     cuuint64_t dims[3] = {(cuuint64_t)F, (cuuint64_t)T, (cuuint64_t)B};
     cuuint64_t strides[2] = {(cuuint64_t)F * 2, (cuuint64_t)T * F * 2};
-    cuuint32_t box[3] = {(cuuint32_t)gr::BK, (cuuint32_t)gr::BM, 1};
+    cuuint32_t box[3] = {(cuuint32_t)gr::BK, (cuuint32_t)rows, 1};
     cuuint32_t estr[3] = {1, 1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-int gram_pairs(int64_t T) {
-    const int64_t nt = T / gr::BM;
-    return (int)(nt * (nt + 1) / 2);
+int gram_units(int64_t T) {  // units per example: sum over row tiles i of (nJ - i / 2)
+    const int64_t nt = T / gr::BM, nJ = (nt + 1) / 2;
+    int64_t n = 0;
+    for (int64_t i = 0; i < nt; ++i) n += nJ - i / 2;
+    return (int)n;
 }
 
 }  // namespace
 
 bool gram_shape_ok(int64_t B, int64_t T, int64_t K, int64_t L) {
     return B >= 1 && T >= gr::BM && T % gr::BM == 0 && K % gr::BK == 0 && L % gr::BK == 0 && K > 0 && L > 0 &&
-           T < (1 << 20) && B < (1 << 20) && (int64_t)B * gram_pairs(T) < (1ll << 31);
+           T < (1 << 20) && B < (1 << 20) && (int64_t)B * gram_units(T) < (1ll << 31);
 }
 
-size_t gram_workspace(int64_t B, int64_t T) { return (size_t)B * gram_pairs(T) * sizeof(double) + 256; }
+size_t gram_workspace(int64_t B, int64_t T) { return (size_t)B * gram_units(T) * sizeof(double) + 256; }
 
 cudaError_t launch_gram_norms(const void* x, const void* g, double* raw, double* sums, int64_t B, int64_t T,
                               int64_t K, int64_t L, void* ws, cudaStream_t st) {
-    CUtensorMap mx, mg;
-    if (!make_map_rows(&mx, x, (int)B, (int)T, (int)K) || !make_map_rows(&mg, g, (int)B, (int)T, (int)L))
+    CUtensorMap mxa, mxb, mga, mgb;
+    if (!make_map_rows(&mxa, x, (int)B, (int)T, (int)K, gr::BM) || !make_map_rows(&mxb, x, (int)B, (int)T, (int)K, gr::BN) ||
+        !make_map_rows(&mga, g, (int)B, (int)T, (int)L, gr::BM) || !make_map_rows(&mgb, g, (int)B, (int)T, (int)L, gr::BN))
         return cudaErrorInvalidValue;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        cudaFuncSetAttribute(gram_norms_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gr::SMEM);
-    });
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(gram_norms_kernel), gr::SMEM);
+    if (e != cudaSuccess) return e;
     GramArgs a{};
     a.B = (int)B;
     a.T = (int)T;
     a.K = (int)K;
     a.L = (int)L;
     a.nt = (int)(T / gr::BM);
-    a.npairs = gram_pairs(T);
+    a.nJ = (a.nt + 1) / 2;
+    a.nunits = gram_units(T);
     a.q = static_cast<double*>(ws);
-    const int64_t units = B * a.npairs;
+    const int64_t units = B * a.nunits;
     const int sms = device_sm_count();
     const int grid = (int)(units < sms ? units : sms);
-    gram_norms_kernel<<<grid, gr::THREADS, gr::SMEM, st>>>(mx, mg, a);
-    cudaError_t e = cudaGetLastError();
+    gram_norms_kernel<<<grid, gr::THREADS, gr::SMEM, st>>>(mxa, mxb, mga, mgb, a);
+    e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    return launch_fold_rows(a.q, (int)B, a.npairs, raw, sums, 0, st);
+    return launch_fold_rows(a.q, (int)B, a.nunits, raw, sums, 0, st);
 }
 
 }  // namespace gnsb
