@@ -197,10 +197,18 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # GNSB_DIST_BACKEND=gloo with more ranks than GPUs exercises the multi-rank
+    # path on one device (tests only; the measured path is NCCL, one GPU per rank)
+    backend = os.environ.get("GNSB_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     lib = _lib.lib()
@@ -349,7 +357,7 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (SURVEY §8(d) recipe, generated on device)",
         "config": {"workload": WORKLOAD, "B": B_LOCAL, "T": T, "D": sweep, "global_batch": B_LOCAL * world,
-                   "parallelism": f"dp{world}",
+                   "parallelism": f"dp{world}", "backend": backend if world > 1 else None,
                    "l2": "inputs larger than L2: a step streams %.2f GB (>> 126 MB L2) between reuses of any buffer"
                          % (step_bytes / 1e9),
                    "launch": "one CUDA graph per step" if graphs.get(True) is not None else "direct launches"},

@@ -1,0 +1,104 @@
+"""Batch-sharded fused LN backward on the GPU, world size 2.
+
+The pool has one GPU, so both ranks share cuda:0 and talk over gloo (the
+measured path is NCCL with one GPU per rank; the host logic is the same
+GradBuckets.reduce). Each rank runs the fused kernel on its contiguous block of
+examples of a globally-indexed synthetic batch (synth b_offset = the block
+start, dy scaled by 1/B_global). The reduced dgamma/dbeta, the re-formed
+||G_big||^2 and the B_global-corrected norms must match one process running
+the whole batch: dgamma/dbeta to fp32 summation-order tolerance (1e-5), norm
+records to 1e-6.
+"""
+import json
+import os
+import socket
+import subprocess
+import sys
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import ROOT, close
+
+pytestmark = pytest.mark.gpu
+
+B_GLOBAL, T, WIDTHS = 6, 64, (768, 1024)
+
+
+def _shard_records(b0, b1, dev):
+    import paper_2411_00999_b200 as m
+    from paper_2411_00999_b200.sharded import GradBuckets
+
+    bk = GradBuckets(WIDTHS, dev)
+    for l, D in enumerate(WIDTHS):
+        x, dy, gamma, beta = m.synth_ln(b1 - b0, T, D, torch.bfloat16, dev, b_offset=b0, B_div=B_GLOBAL,
+                                        stream0=16 * l)
+        layer = m.LayerNormLayer(gamma, beta)
+        f = m.layernorm_forward(layer, x)
+        r = m.layernorm_backward_simultaneous(layer, f.cache, dy, need_input_grad=False)
+        dg, db = bk.grad(l)
+        dg.copy_(r.grads.weight_grads["gamma"])
+        db.copy_(r.grads.weight_grads["beta"])
+        bk.record(l).copy_(r.grads.sums4)
+    return bk
+
+
+def _worker(rank, world, init_file, out):
+    from paper_2411_00999_b200.sharded import shard_bounds
+
+    dist.init_process_group("gloo", init_method=f"file://{init_file}", rank=rank, world_size=world)
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    b0, b1 = shard_bounds(B_GLOBAL, world, rank)
+    bk = _shard_records(b0, b1, dev)
+    bk.reduce()
+    torch.cuda.synchronize()
+    if rank == 0:
+        np.savez(out, grads=bk.grads.cpu().numpy(), records=bk.records.cpu().numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_world2_matches_single_process(cuda):
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "r.npz")
+        mp.spawn(_worker, args=(2, os.path.join(d, "pg"), out), nprocs=2, join=True)
+        res = np.load(out)
+    full = _shard_records(0, B_GLOBAL, cuda)
+    torch.cuda.synchronize()
+    g = full.grads.cpu().numpy()
+    assert close(res["grads"], g, 1e-5, 1e-5 * np.abs(g).max())
+    rec = full.records.cpu().numpy()
+    assert close(res["records"], rec, 1e-6)
+    # corrected per-example norm uses B_global: sum over ranks of local raw sums
+    from paper_2411_00999_b200.sharded import layer_grad_stats
+
+    for l in range(len(WIDTHS)):
+        a, b = layer_grad_stats(res["records"][l], B_GLOBAL), layer_grad_stats(rec[l], B_GLOBAL)
+        assert close(a.g_small_sqnorm_mean, b.g_small_sqnorm_mean, 1e-6)
+        assert close(a.g_big_sqnorm, b.g_big_sqnorm, 1e-6)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_bench_multirank_path_runs(cuda):
+    """bench.py under torchrun with 2 ranks (gloo, both on cuda:0): one JSON line
+    from rank 0 with n_gpus=2 and a positive value (timing is not meaningful here)."""
+    env = dict(os.environ, GNSB_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "2", "--warmup", "3", "--no-cpu", "--no-extra", "--d-list", "768,1024"]
+    p = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, p.stdout[-2000:]
+    rec = json.loads(lines[0])
+    assert rec["n_gpus"] == 2 and rec["value"] > 0 and rec["config"]["global_batch"] == 64
