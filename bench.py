@@ -350,6 +350,7 @@ def run_ours(args):
     if rank == 0 and not args.no_extra:
         extra["cfg3_linear"] = run_cfg3(m, lib, dev, torch, np)
         extra["cfg4_gns"] = run_cfg4(m, lib, dev, torch, np)
+        extra["cfg5_g1"] = run_cfg5(m, lib, dev, torch, np)
 
     traffic = load_traffic()
     line = {
@@ -488,6 +489,40 @@ def run_cfg4(m, lib, dev, torch, np):
     return out
 
 
+def run_cfg5(m, lib, dev, torch, np):
+    """BASELINE config 5 at G=1: the whole batch-sharded workload on one GPU,
+    B=256 T=2048 D=4096 bf16 (12.9 GB per step), fused LN backward + norms.
+    At G GPUs each rank runs B/G of these examples plus the bucket all-reduce."""
+    B, T_, D = 256, 2048, 4096
+    x, dy, gamma, beta = m.synth_ln(B, T_, D, torch.bfloat16, dev, B_div=B)
+    f = m.layernorm_forward(m.LayerNormLayer(gamma, beta), x)
+    dx = torch.empty_like(x)
+    dg = torch.empty(D, device=dev)
+    db = torch.empty(D, device=dev)
+    raw = torch.zeros(2, B, dtype=torch.float64, device=dev)
+    rec = torch.zeros(4, dtype=torch.float64, device=dev)
+    ws = torch.zeros(m.layers.ctypes_size(B, T_, D, 1), dtype=torch.uint8, device=dev)
+    mean, rstd = f.cache.mean, f.cache.inv_std
+
+    def fn():
+        sp = torch.cuda.current_stream(dev).cuda_stream
+        rc = lib.gnsb_ln_bwd(x.data_ptr(), mean.data_ptr(), rstd.data_ptr(), dy.data_ptr(), gamma.data_ptr(),
+                             dx.data_ptr(), dg.data_ptr(), db.data_ptr(), raw[0].data_ptr(), raw[1].data_ptr(),
+                             rec.data_ptr(), 1, B, T_, D, 1, ws.data_ptr(), ws.numel(), sp)
+        if rc:
+            raise RuntimeError(lib.gnsb_last_error().decode())
+
+    ms = time_graph(fn, torch, np, dev, reps=5)
+    nbytes = alg_bytes(B, T_, D)
+    peak, _ = load_peaks()
+    out = {"workload": "cfg5 at G=1: LN bwd + per-example norms B=256 T=2048 D=4096 bf16",
+           "ms_per_step": ms, "GBps": nbytes / (ms * 1e-3) / 1e9, "frac_of_measured_peak":
+           nbytes / (ms * 1e-3) / 1e9 / peak, "alg_bytes": nbytes}
+    del x, dy, dx, f, ws
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_e2e(args, m, lib, cases, dev, stream, torch, np):
     """Same metric through the public C ABI with host-resident inputs/outputs."""
     sp = stream.cuda_stream
@@ -506,33 +541,65 @@ def run_e2e(args, m, lib, cases, dev, stream, torch, np):
     h2d = sum(h["x"].numel() * 2 + h["dy"].numel() * 2 + h["mean"].numel() * 4 + h["rstd"].numel() * 4 for h in host)
     d2h = sum(h["dx"].numel() * 2 + 2 * c.D * 4 + 32 + 16 * c.B for h, c in zip(host, cases))
 
+    # Three streams: host->device copies, the kernels, device->host copies.
+    # Layer l's kernel waits for its inputs; its outputs go back while the
+    # next layer computes and the one after uploads (PCIe is full duplex).
+    # Per-layer device buffers are reused across steps, so a step's upload of
+    # layer l waits for the previous step's kernel l, and kernel l waits for
+    # the previous step's download of layer l.
+    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    n = len(cases)
+    comp_done = [None] * n
+    out_done = [None] * n
+
     def step():
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for c, h in zip(cases, host):
-            c.x.copy_(h["x"], non_blocking=True)
-            c.dy.copy_(h["dy"], non_blocking=True)
-            c.mean.copy_(h["mean"], non_blocking=True)
-            c.rstd.copy_(h["rstd"], non_blocking=True)
+        for l, (c, h) in enumerate(zip(cases, host)):
+            with torch.cuda.stream(s_in):
+                if comp_done[l] is not None:
+                    s_in.wait_event(comp_done[l])
+                c.x.copy_(h["x"], non_blocking=True)
+                c.dy.copy_(h["dy"], non_blocking=True)
+                c.mean.copy_(h["mean"], non_blocking=True)
+                c.rstd.copy_(h["rstd"], non_blocking=True)
+                in_done = torch.cuda.Event()
+                in_done.record(s_in)
+            stream.wait_event(in_done)
+            if out_done[l] is not None:
+                stream.wait_event(out_done[l])
             c.run(True, sp)
-            h["dx"].copy_(c.dx, non_blocking=True)
-            h["dgamma"].copy_(c.dgamma, non_blocking=True)
-            h["dbeta"].copy_(c.dbeta, non_blocking=True)
-            h["sums"].copy_(c.sums, non_blocking=True)
-            h["raw_g"].copy_(c.raw_g, non_blocking=True)
-            h["raw_b"].copy_(c.raw_b, non_blocking=True)
-        e1.record(stream)
-        return e0, e1
+            comp_done[l] = torch.cuda.Event()
+            comp_done[l].record(stream)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(comp_done[l])
+                h["dx"].copy_(c.dx, non_blocking=True)
+                h["dgamma"].copy_(c.dgamma, non_blocking=True)
+                h["dbeta"].copy_(c.dbeta, non_blocking=True)
+                h["sums"].copy_(c.sums, non_blocking=True)
+                h["raw_g"].copy_(c.raw_g, non_blocking=True)
+                h["raw_b"].copy_(c.raw_b, non_blocking=True)
+                out_done[l] = torch.cuda.Event()
+                out_done[l].record(s_out)
 
     for _ in range(2):
         step()
     torch.cuda.synchronize()
-    evs = [step() for _ in range(max(3, min(args.steps, 10)))]
+    k = max(3, min(args.steps, 10))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s_in)
+    stream.wait_stream(s_in)
+    s_out.wait_stream(s_in)
+    for _ in range(k):
+        step()
+    s_out.wait_stream(stream)
+    s_out.wait_stream(s_in)
+    e1.record(s_out)
     torch.cuda.synchronize()
-    ms = float(np.median([a.elapsed_time(b) for a, b in evs]))
+    ms = e0.elapsed_time(e1) / k
     value = sum(c.bytes for c in cases) / (ms * 1e-3) / 1e9
     return {"value": value, "unit": "GB/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "ms_per_step": ms, "path": "gnsb_ln_bwd (C ABI) with pinned host buffers, copies inside the timing"}
+            "ms_per_step": ms, "steps": k,
+            "path": "gnsb_ln_bwd (C ABI) with pinned host buffers; H2D, kernels and D2H on three streams, "
+                    "copies inside the timing"}
 
 
 def cpu_baseline(args):
