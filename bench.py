@@ -175,6 +175,18 @@ class LnCase:
         self.bytes = alg_bytes(B, T, D)
         self.bytes_plain = alg_bytes(B, T, D, norms=False)
 
+    def run_rows(self, stream_ptr):
+        p = lambda t: t.data_ptr()
+        rc = self.lib.gnsb_ln_bwd_rows(p(self.x), p(self.mean), p(self.rstd), p(self.dy), p(self.gamma), p(self.dx),
+                                       self.B, T, self.D, 1, p(self.ws), self.ws.numel(), stream_ptr)
+        if rc:
+            raise RuntimeError(self.lib.gnsb_last_error().decode())
+
+    def pending(self, _lib):
+        return _lib.LnBwdPending(self.ws.data_ptr(), self.ws.numel(), self.B, T, self.D, 1, self.dgamma.data_ptr(),
+                                 self.dbeta.data_ptr(), self.raw_g.data_ptr(), self.raw_b.data_ptr(),
+                                 self.sums.data_ptr())
+
     def run(self, norms, stream_ptr):
         p = lambda t: t.data_ptr()
         rc = self.lib.gnsb_ln_bwd(
@@ -220,14 +232,21 @@ def run_ours(args):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     torch.cuda.synchronize()
 
+    pend = (_lib.LnBwdPending * len(cases))(*[c.pending(_lib) for c in cases])
+
     def run_step(norms, with_collective):
         """One step: the fused (or plain) LN backward for every D of the sweep,
+        as a backward pass runs it: the row pass of each layer as it comes, then
+        the deferred stage 2 of all of them in one launch (gnsb_ln_bwd_reduce);
         plus for N > 1 the all-reduce of the two exchange buckets (all layers'
         [dgamma | dbeta] fp32 and their fp64 norm records) and the re-formed
         ||G_big||^2 of the reduced gradients."""
         sp_now = torch.cuda.current_stream(dev).cuda_stream
         for c in cases:
-            c.run(norms, sp_now)
+            c.run_rows(sp_now)
+        rc = lib.gnsb_ln_bwd_reduce(pend, len(cases), 1 if norms else 0, sp_now)
+        if rc:
+            raise RuntimeError(lib.gnsb_last_error().decode())
         if with_collective and world > 1:
             buckets.reduce()
 
@@ -361,15 +380,16 @@ def run_ours(args):
                    "parallelism": f"dp{world}", "backend": backend if world > 1 else None,
                    "l2": "inputs larger than L2: a step streams %.2f GB (>> 126 MB L2) between reuses of any buffer"
                          % (step_bytes / 1e9),
-                   "launch": "one CUDA graph per step" if graphs.get(True) is not None else "direct launches"},
+                   "launch": "one CUDA graph per step" if graphs.get(True) is not None else "direct launches",
+                   "stage2": "deferred: row pass per layer, one grouped reduce launch per step (gnsb_ln_bwd_reduce)"},
         "overhead_pct": 100.0 * (step_f - step_p) / step_p, "overhead_pct_D_ge_1024": overhead_ge1024,
         "step_ms_fused": step_f, "step_ms_plain": step_p,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "peak_kind": peak_kind, "frac_of_8TBps": achieved / 8000.0, "traffic": traffic,
-                     "kernel": "ln_bwd_kernel<bf16,...,HAS_MEAN=1> + ln_bwd_reduce_kernel<float,NORMS=1> (one pair per D, 5 per step)",
+                     "kernel": "ln_bwd_kernel<bf16,...,HAS_MEAN=1> (one per D) + one ln_bwd_reduce_group_kernel<float,NORMS=1> per step",
                      "achieved_def": "algorithmic bytes of the 5 launches / median graph-replayed step time"},
         "sweep": sweep_rows, "e2e": e2e, "cpu_baseline": cpu, **extra,
-        "gpu_launches": len(cases) * args.steps * (4 if world > 1 else 2), "clocks": clk.summary(),
+        "gpu_launches": (len(cases) + 1 + (2 * len(cases) if world > 1 else 0)) * args.steps, "clocks": clk.summary(),
     }
     if rank == 0:
         print(json.dumps(line))
@@ -466,15 +486,22 @@ def run_cfg4(m, lib, dev, torch, np):
         cases.append((x, f.cache.mean, f.cache.inv_std, dy, gamma, dx, ws, raw))
     acc = DeviceGnsAccumulator(["layernorm"] * NL, 0.5, dev)
 
+    from paper_2411_00999_b200 import _lib as L
+
+    pend = (L.LnBwdPending * NL)(*[
+        L.LnBwdPending(ws.data_ptr(), ws.numel(), B, T_, D, 1, bk.grad(l)[0].data_ptr(), bk.grad(l)[1].data_ptr(),
+                       raw[0].data_ptr(), raw[1].data_ptr(), bk.record(l).data_ptr())
+        for l, (x, mean, rstd, dy, gamma, dx, ws, raw) in enumerate(cases)])
+
     def fn():
         sp = torch.cuda.current_stream(dev).cuda_stream
         for l, (x, mean, rstd, dy, gamma, dx, ws, raw) in enumerate(cases):
-            dg, db = bk.grad(l)
-            rc = lib.gnsb_ln_bwd(x.data_ptr(), mean.data_ptr(), rstd.data_ptr(), dy.data_ptr(), gamma.data_ptr(),
-                                 dx.data_ptr(), dg.data_ptr(), db.data_ptr(), raw[0].data_ptr(), raw[1].data_ptr(),
-                                 bk.record(l).data_ptr(), 1, B, T_, D, 1, ws.data_ptr(), ws.numel(), sp)
+            rc = lib.gnsb_ln_bwd_rows(x.data_ptr(), mean.data_ptr(), rstd.data_ptr(), dy.data_ptr(), gamma.data_ptr(),
+                                      dx.data_ptr(), B, T_, D, 1, ws.data_ptr(), ws.numel(), sp)
             if rc:
                 raise RuntimeError(lib.gnsb_last_error().decode())
+        if lib.gnsb_ln_bwd_reduce(pend, NL, 1, sp):
+            raise RuntimeError(lib.gnsb_last_error().decode())
         acc.step(bk.records, B)
 
     ms = time_graph(fn, torch, np, dev)
@@ -483,7 +510,7 @@ def run_cfg4(m, lib, dev, torch, np):
     out = {"workload": "cfg4: GNS over 25 LayerNorms, B=64 T=1024 D=768 bf16, sigma=3 (synthetic)",
            "ms_per_step": ms, "GBps": nbytes / (ms * 1e-3) / 1e9, "alg_bytes": nbytes,
            "gns_total": {"g2": float(groups[0, 0]), "s": float(groups[0, 1]), "b_simple_ema": float(groups[0, 2])},
-           "launches_per_step": 2 * NL + 1}
+           "launches_per_step": NL + 2, "stage2": "deferred: one grouped reduce for the 25 layers"}
     del cases
     torch.cuda.empty_cache()
     return out

@@ -85,6 +85,33 @@ gnsb_status gnsb_ln_bwd(const void* x_or_xhat, const void* mean, const void* rst
                         const void* gamma, void* dx, void* dgamma, void* dbeta, double* raw_sq_gamma,
                         double* raw_sq_beta, double* sums, int32_t with_norms, int64_t B, int64_t M, int64_t D,
                         gnsb_dtype dt, void* ws, size_t ws_bytes, void* stream);
+/* Deferred stage 2 (one launch for several LayerNorms).
+ * gnsb_ln_bwd == gnsb_ln_bwd_rows followed by gnsb_ln_bwd_reduce of that one
+ * layer.  A backward pass may instead run the row pass of every LayerNorm as
+ * it comes (dx is final when gnsb_ln_bwd_rows returns in stream order) and
+ * reduce all of them at the end in one launch: the per-example combine,
+ * squares and dgamma/dbeta sums then cost one stage-2 tail per step instead of
+ * one per layer.  Each pending layer needs its own workspace, untouched
+ * between its row pass and the reduce.  Results are identical to gnsb_ln_bwd.
+ */
+gnsb_status gnsb_ln_bwd_rows(const void* x_or_xhat, const void* mean, const void* rstd, const void* dy,
+                             const void* gamma, void* dx, int64_t B, int64_t M, int64_t D, gnsb_dtype dt, void* ws,
+                             size_t ws_bytes, void* stream);
+typedef struct {
+    void* ws;                 /* the workspace its gnsb_ln_bwd_rows call used */
+    size_t ws_bytes;
+    int64_t B, M, D;          /* the shape of that call */
+    int32_t dt;               /* gnsb_dtype of that call */
+    void* dgamma;             /* outputs, as for gnsb_ln_bwd */
+    void* dbeta;
+    double* raw_sq_gamma;
+    double* raw_sq_beta;
+    double* sums;
+} gnsb_ln_bwd_pending;
+/* All items must share the statistics dtype (fp32 for F32/BF16 rows, fp64 for
+ * F64) and with_norms; at most 64 items. */
+gnsb_status gnsb_ln_bwd_reduce(const gnsb_ln_bwd_pending* items, int32_t n, int32_t with_norms, void* stream);
+
 /* Launch geometry the backward uses for this shape (reporting / roofline). */
 gnsb_status gnsb_ln_bwd_geometry(int64_t B, int64_t M, int64_t D, gnsb_dtype dt, int32_t* grid, int32_t* threads,
                                  int32_t* stages);

@@ -50,6 +50,14 @@ class EmaState(ctypes.Structure):
     _fields_ = [("alpha", c_f64), ("value", c_f64), ("count", c_i64)]
 
 
+class LnBwdPending(ctypes.Structure):
+    """gnsb_ln_bwd_pending (include/gnsb.h): one LayerNorm whose stage 2 is deferred."""
+
+    _fields_ = [("ws", c_vp), ("ws_bytes", ctypes.c_size_t), ("B", c_i64), ("M", c_i64), ("D", c_i64),
+                ("dt", c_i32), ("dgamma", c_vp), ("dbeta", c_vp), ("raw_sq_gamma", c_vp), ("raw_sq_beta", c_vp),
+                ("sums", c_vp)]
+
+
 _SIGS = {
     "gnsb_version": (ctypes.c_char_p, []),
     "gnsb_last_error": (ctypes.c_char_p, []),
@@ -60,6 +68,9 @@ _SIGS = {
         [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i64, c_i64, c_i64, c_i32, c_vp,
          ctypes.c_size_t, c_vp],
     ),
+    "gnsb_ln_bwd_rows": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i32, c_vp,
+                                 ctypes.c_size_t, c_vp]),
+    "gnsb_ln_bwd_reduce": (c_i32, [ctypes.POINTER(LnBwdPending), c_i32, c_i32, c_vp]),
     "gnsb_ln_bwd_geometry": (
         c_i32,
         [c_i64, c_i64, c_i64, c_i32, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32), ctypes.POINTER(c_i32)],

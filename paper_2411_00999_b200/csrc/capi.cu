@@ -1,3 +1,4 @@
+#include <vector>
 #include <utility>
 #include <map>
 #include <cstdio>
@@ -319,6 +320,94 @@ gnsb_status gnsb_ln_bwd(const void* x, const void* mean, const void* rstd, const
     if (rc == 1) return fail(GNSB_EINVAL, why ? why : "layers: invalid argument");
     if (rc == 2) return cuda_fail(ce, why ? why : "ln_bwd launch");
     return debug_ok("gnsb_ln_bwd");
+}
+
+gnsb_status gnsb_ln_bwd_rows(const void* x, const void* mean, const void* rstd, const void* dy, const void* gamma,
+                             void* dx, int64_t B, int64_t M, int64_t D, gnsb_dtype dt, void* ws, size_t ws_bytes,
+                             void* stream) {
+    if (B == 0) return fail(GNSB_EINVAL, "layers: empty batch");
+    if (B < 0 || M < 0) return fail(GNSB_EINVAL, "layers: invalid extents");
+    if (D < 1) return fail(GNSB_EINVAL, "layers: gradient trailing extent does not match gamma");
+    if (dt != GNSB_F32 && dt != GNSB_BF16 && dt != GNSB_F64) return fail(GNSB_EINVAL, "layers: unknown dtype");
+    if (gnsb_status s = need_device("gnsb_ln_bwd_rows")) return s;
+    if (M == 0) return debug_ok("gnsb_ln_bwd_rows");  // nothing to stream; the reduce writes zeros
+    if (!x || !rstd || !dy || !gamma || !ws) return fail(GNSB_EINVAL, "layers: null input pointer");
+    gnsb::LnBwdCall c{x, mean, rstd, dy, gamma, dx, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
+                      B, M, D, ws, ws_bytes};
+    const char* why = nullptr;
+    cudaError_t ce = cudaSuccess;
+    int rc = 1;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    switch (dt) {
+        case GNSB_F32: rc = gnsb::ln_bwd_rows_run<float>(c, st, &why, &ce); break;
+        case GNSB_BF16: rc = gnsb::ln_bwd_rows_run<__nv_bfloat16>(c, st, &why, &ce); break;
+        case GNSB_F64: rc = gnsb::ln_bwd_rows_run<double>(c, st, &why, &ce); break;
+        default: break;
+    }
+    if (rc == 1) return fail(GNSB_EINVAL, why ? why : "layers: invalid argument");
+    if (rc == 2) return cuda_fail(ce, why ? why : "ln_bwd rows launch");
+    return debug_ok("gnsb_ln_bwd_rows");
+}
+
+gnsb_status gnsb_ln_bwd_reduce(const gnsb_ln_bwd_pending* items, int32_t n, int32_t with_norms, void* stream) {
+    if (n < 0 || (n > 0 && !items)) return fail(GNSB_EINVAL, "layers: invalid pending list");
+    if (n > 64) return fail(GNSB_EINVAL, "layers: too many pending LayerNorms in one reduce (max 64)");
+    if (gnsb_status s = need_device("gnsb_ln_bwd_reduce")) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    std::vector<gnsb::LnRedItem> list;
+    int acc_f64 = -1;
+    for (int32_t i = 0; i < n; ++i) {
+        const gnsb_ln_bwd_pending& p = items[i];
+        const gnsb_dtype dt = static_cast<gnsb_dtype>(p.dt);
+        if (dt != GNSB_F32 && dt != GNSB_BF16 && dt != GNSB_F64) return fail(GNSB_EINVAL, "layers: unknown dtype");
+        if (p.B <= 0 || p.M < 0 || p.D < 1) return fail(GNSB_EINVAL, "layers: invalid extents");
+        if (!p.dgamma || !p.dbeta || !p.ws) return fail(GNSB_EINVAL, "layers: null output pointer");
+        const int f64 = dt == GNSB_F64 ? 1 : 0;
+        if (acc_f64 >= 0 && f64 != acc_f64)
+            return fail(GNSB_EINVAL, "layers: pending LayerNorms mix fp64 and fp32 statistics");
+        acc_f64 = f64;
+        if (p.M == 0) {  // no rows: zeros (layers.cpp:248-275 with an empty loop)
+            cudaError_t e = cudaMemsetAsync(p.dgamma, 0, (size_t)p.D * stat_size(dt), st);
+            if (e == cudaSuccess) e = cudaMemsetAsync(p.dbeta, 0, (size_t)p.D * stat_size(dt), st);
+            if (with_norms) {
+                if (e == cudaSuccess && p.raw_sq_gamma) e = cudaMemsetAsync(p.raw_sq_gamma, 0, (size_t)p.B * 8, st);
+                if (e == cudaSuccess && p.raw_sq_beta) e = cudaMemsetAsync(p.raw_sq_beta, 0, (size_t)p.B * 8, st);
+                if (e == cudaSuccess && p.sums) e = cudaMemsetAsync(p.sums, 0, 4 * 8, st);
+            }
+            if (e != cudaSuccess) return cuda_fail(e, "memset");
+            continue;
+        }
+        gnsb::LnRedItem it{};
+        const char* why = nullptr;
+        int rc = 1;
+        switch (dt) {
+            case GNSB_F32: rc = gnsb::ln_bwd_plan_info<float>(p.B, p.M, p.D, &it.info, &why); break;
+            case GNSB_BF16: rc = gnsb::ln_bwd_plan_info<__nv_bfloat16>(p.B, p.M, p.D, &it.info, &why); break;
+            case GNSB_F64: rc = gnsb::ln_bwd_plan_info<double>(p.B, p.M, p.D, &it.info, &why); break;
+            default: break;
+        }
+        if (rc) return fail(GNSB_EINVAL, why ? why : "layers: invalid argument");
+        if (p.ws_bytes < it.info.total)
+            return fail(GNSB_EINVAL, "layers: workspace too small (query gnsb_ln_bwd_workspace_size)");
+        it.B = p.B;
+        it.M = p.M;
+        it.D = p.D;
+        it.ws = p.ws;
+        it.dgamma = p.dgamma;
+        it.dbeta = p.dbeta;
+        it.raw_g = with_norms ? p.raw_sq_gamma : nullptr;
+        it.raw_b = with_norms ? p.raw_sq_beta : nullptr;
+        it.sums = with_norms ? p.sums : nullptr;
+        list.push_back(it);
+    }
+    if (list.empty()) return debug_ok("gnsb_ln_bwd_reduce");
+    const char* why = nullptr;
+    cudaError_t ce = cudaSuccess;
+    const int rc = gnsb::ln_bwd_reduce_run(acc_f64 == 1, with_norms ? 1 : 0, list.data(), (int)list.size(), st,
+                                           nullptr, &why, &ce);
+    if (rc == 1) return fail(GNSB_EINVAL, why ? why : "layers: invalid argument");
+    if (rc == 2) return cuda_fail(ce, why ? why : "ln_bwd reduce launch");
+    return debug_ok("gnsb_ln_bwd_reduce");
 }
 
 // ---------------------------------------------------------------- linear --

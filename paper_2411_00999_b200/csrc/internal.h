@@ -34,7 +34,28 @@ struct LnBwdCall {
     unsigned long long* trace2 = nullptr;  // profiling only: reduce kernel [grid][3] phase stamps
 };
 
+// Where a row pass left its partial slots and how the reduce must read them.
+struct LnRedPlanInfo {
+    int Dp = 0, G = 0, grid_rows = 0;
+    size_t off_partial = 0, off_q = 0, off_qbig = 0, off_raw = 0, total = 0;
+};
+// One LayerNorm whose stage 2 (per-example combine, squares, dgamma/dbeta) is pending.
+struct LnRedItem {
+    LnRedPlanInfo info;
+    int64_t B, M, D;
+    void* ws;
+    void* dgamma; void* dbeta;
+    double* raw_g; double* raw_b; double* sums;
+};
+
 // Returns 0 ok, 1 invalid (message in *why), 2 CUDA error (cudaError_t in *cerr).
+// Row pass only (the stage-2 inputs stay in ws); plan info of that pass.
+template <typename T> int ln_bwd_rows_run(const LnBwdCall& c, cudaStream_t st, const char** why, cudaError_t* cerr);
+template <typename T> int ln_bwd_plan_info(int64_t B, int64_t M, int64_t D, LnRedPlanInfo* out, const char** why);
+// Stage 2 of n pending LayerNorms in one launch (ln_reduce.cu).  acc_f64: the
+// statistics dtype is fp64 (fp64 rows), else fp32.
+int ln_bwd_reduce_run(int acc_f64, int norms, const LnRedItem* items, int n, cudaStream_t st,
+                      unsigned long long* trace, const char** why, cudaError_t* cerr);
 template <typename T> int ln_fwd_run(const LnFwdCall& c, cudaStream_t st, const char** why, cudaError_t* cerr);
 template <typename T> int ln_bwd_run(const LnBwdCall& c, cudaStream_t st, const char** why, cudaError_t* cerr);
 template <typename T> int ln_bwd_workspace(int64_t B, int64_t M, int64_t D, size_t* bytes, const char** why);

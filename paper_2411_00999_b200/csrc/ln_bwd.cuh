@@ -556,13 +556,13 @@ struct LnRedLayout {  // shared-memory carve-up of the reduce kernel (host + dev
     }
 };
 
+// The stage-2 work of CTA `cta` of the `grid` CTAs assigned to one LayerNorm.
 template <typename Acc, bool NORMS>
-__global__ void __launch_bounds__(kReduceThreads) ln_bwd_reduce_kernel(LnRedArgs a) {
+__device__ __forceinline__ void ln_bwd_reduce_body(const LnRedArgs& a, const int cta, const int grid,
+                                                   unsigned char* smem) {
     constexpr int V = 16 / sizeof(Acc);  // columns per 16-byte vector
-    extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nthreads = blockDim.x, nwarps = nthreads / 32;
-    const int grid = gridDim.x, cta = blockIdx.x;
     const int64_t B = a.B, M = a.M, N = a.N, D = a.D;
     const int64_t U = (a.Dp + V - 1) / V;
     const int u0 = (int)((int64_t)cta * U / grid), u1 = (int)((int64_t)(cta + 1) * U / grid);
@@ -789,6 +789,30 @@ __global__ void __launch_bounds__(kReduceThreads) ln_bwd_reduce_kernel(LnRedArgs
     }
     if (threadIdx.x == 0) *a.ticket = 0u;  // (visible to the next kernel at grid completion)
     stamp(4);
+}
+
+template <typename Acc, bool NORMS>
+__global__ void __launch_bounds__(kReduceThreads) ln_bwd_reduce_kernel(LnRedArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    ln_bwd_reduce_body<Acc, NORMS>(a, blockIdx.x, gridDim.x, smem);
+}
+
+// Deferred stage 2 of several LayerNorms in one launch: CTAs
+// [begin[l], begin[l+1]) work on layer l (each layer keeps its own workspace,
+// ticket and outputs).  Amortises the stage-2 tail over a whole backward.
+constexpr int kMaxReduceGroup = 64;
+struct LnRedGroup {
+    LnRedArgs items[kMaxReduceGroup];
+    int begin[kMaxReduceGroup + 1];
+    int n;
+};
+
+template <typename Acc, bool NORMS>
+__global__ void __launch_bounds__(kReduceThreads) ln_bwd_reduce_group_kernel(const __grid_constant__ LnRedGroup g) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    int l = 0;
+    while (l + 1 < g.n && (int)blockIdx.x >= g.begin[l + 1]) ++l;
+    ln_bwd_reduce_body<Acc, NORMS>(g.items[l], (int)blockIdx.x - g.begin[l], g.begin[l + 1] - g.begin[l], smem);
 }
 
 }  // namespace gnsb

@@ -37,8 +37,7 @@ inline cudaError_t ensure_smem(const void* kernel, size_t bytes) { return ensure
 
 struct BwdPlan {
     int Dp = 0, stages = 0, threads = 0, grid = 0, G = 0;
-    int rgrid = 0, rthreads = kReduceThreads, eb = 0;  // stage-2 (reduce) kernel
-    size_t smem = 0, rsmem = 0;
+    size_t smem = 0;
     size_t off_partial = 0, off_q = 0, off_qbig = 0, off_raw = 0, total = 0;
 };
 
@@ -67,38 +66,13 @@ int plan_bwd(int64_t B, int64_t M, int64_t D, BwdPlan& p, const char** why) {
     const int sms = device_sm_count();
     p.grid = (int)(N < sms ? N : sms);
     if (p.grid < 1) p.grid = 1;
-    // reduce kernel: one contiguous range of 16-byte column vectors per CTA
-    constexpr int V = 16 / sizeof(Acc);
-    const int64_t U = (p.Dp + V - 1) / V;
-    // (at least four vectors per CTA: below that the per-CTA fixed cost and the
-    // final fold over CTAs dominate)
-    int64_t rg = (U + 3) / 4;
-    if (rg > sms) rg = sms;
-    if (rg > kMaxReduceGrid) rg = kMaxReduceGrid;
-    p.rgrid = (int)(rg < 1 ? 1 : rg);
-    const int64_t ncol = (U + p.rgrid - 1) / p.rgrid * V;
-    // examples per shared-memory block: as many as fit 160 KB with their slots
-    const int64_t rows_per_cta = N / p.grid;  // floor; a block of eb examples spans <= eb*M/rows_per_cta + 2 CTAs
-    auto layout = [&](int64_t eb) {
-        const int64_t span = rows_per_cta > 0 ? (eb * M + rows_per_cta - 1) / rows_per_cta + 2 : N;
-        LnRedLayout l{ncol, eb, span + eb};
-        return l;
-    };
-    int64_t eb = B < kMaxReduceEb ? B : kMaxReduceEb;
-    while (eb > 1 && layout(eb).bytes(sizeof(Acc)) > (size_t)(160 << 10)) eb = (eb + 1) / 2;
-    if (layout(eb).bytes(sizeof(Acc)) > budget) {
-        *why = "layers: trailing extent too wide for the stage-2 shared memory";
-        return 1;
-    }
-    p.eb = (int)eb;
-    p.rsmem = layout(eb).bytes(sizeof(Acc));
     size_t off = 256;  // counters
     p.off_partial = off;
     off = align_up(off + (size_t)(p.grid + B) * G * 2 * p.Dp * sizeof(Acc), 256);
     p.off_q = off;
-    off = align_up(off + (size_t)B * p.rgrid * 2 * sizeof(double), 256);
+    off = align_up(off + (size_t)B * sms * 2 * sizeof(double), 256);  // q: up to one column range per SM
     p.off_qbig = off;
-    off = align_up(off + (size_t)p.rgrid * 2 * sizeof(double), 256);
+    off = align_up(off + (size_t)sms * 2 * sizeof(double), 256);
     p.off_raw = off;
     off = align_up(off + (size_t)B * 2 * sizeof(double), 256);
     p.total = off;
@@ -161,14 +135,27 @@ struct BwdOp {
         return 0;
     }
 
-    static int run(const LnBwdCall& c, cudaStream_t st, const char** why, cudaError_t* cerr) {
+    static void fill_info(const BwdPlan& p, LnRedPlanInfo* info) {
+        info->Dp = p.Dp;
+        info->G = C::kG;
+        info->grid_rows = p.grid;
+        info->off_partial = p.off_partial;
+        info->off_q = p.off_q;
+        info->off_qbig = p.off_qbig;
+        info->off_raw = p.off_raw;
+        info->total = p.total;
+    }
+
+    // Row pass only: dx plus the per-(CTA, example) partial slots in c.ws.
+    static int run_rows(const LnBwdCall& c, cudaStream_t st, const char** why, cudaError_t* cerr,
+                        LnRedPlanInfo* info) {
         BwdPlan p;
         if (int rc = cached_plan(c.B, c.M, c.D, p, why, cerr)) return rc;
         if (c.ws_bytes < p.total) {
             *why = "layers: workspace too small (query gnsb_ln_bwd_workspace_size)";
             return 1;
         }
-        using Acc = typename C::Acc;
+        fill_info(p, info);
         LnBwdArgs a{};
         a.x = c.x;
         a.mean = c.mean;
@@ -183,8 +170,7 @@ struct BwdOp {
         a.Dp = p.Dp;
         a.stages = p.stages;
         a.aligned = ((c.D * (int64_t)sizeof(T)) % 16 == 0) && ptr16(c.x) && ptr16(c.dy) && (c.dx == nullptr || ptr16(c.dx));
-        unsigned char* ws = static_cast<unsigned char*>(c.ws);
-        a.partial = ws + p.off_partial;
+        a.partial = static_cast<unsigned char*>(c.ws) + p.off_partial;
         a.trace = c.trace;
 
         void (*k)(LnBwdArgs) = c.mean != nullptr ? ln_bwd_kernel<C, true> : ln_bwd_kernel<C, false>;
@@ -204,60 +190,22 @@ struct BwdOp {
             *why = "ln_bwd rows launch";
             return 2;
         }
-
-        LnRedArgs r{};
-        r.partial = a.partial;
-        r.slot_stride = (int64_t)C::kG * 2 * p.Dp;
-        r.B = c.B;
-        r.M = c.M;
-        r.N = a.N;
-        r.D = c.D;
-        r.Dp = p.Dp;
-        r.grid_rows = p.grid;
-        r.eb = p.eb;
-        r.dgamma = c.dgamma;
-        r.dbeta = c.dbeta;
-        r.raw_g = c.raw_g;
-        r.raw_b = c.raw_b;
-        r.sums = c.sums;
-        r.q = reinterpret_cast<double*>(ws + p.off_q);
-        r.qbig = reinterpret_cast<double*>(ws + p.off_qbig);
-        r.rawws = reinterpret_cast<double*>(ws + p.off_raw);
-        r.ticket = reinterpret_cast<unsigned*>(ws) + 1;
-        r.trace = c.trace2;
-        void (*rk)(LnRedArgs) = c.norms ? ln_bwd_reduce_kernel<Acc, true> : ln_bwd_reduce_kernel<Acc, false>;
-        e = ensure_smem(reinterpret_cast<const void*>(rk), p.rsmem);
-        if (e != cudaSuccess) {
-            *cerr = e;
-            *why = "ln_bwd reduce smem attribute";
-            return 2;
-        }
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(p.rgrid);
-        cfg.blockDim = dim3(p.rthreads);
-        cfg.dynamicSmemBytes = p.rsmem;
-        cfg.stream = st;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[0].val.programmaticStreamSerializationAllowed = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        e = cudaLaunchKernelEx(&cfg, rk, r);
-        if (e != cudaSuccess) {
-            *cerr = e;
-            *why = "ln_bwd reduce launch";
-            if (std::getenv("GNSB_DEBUG")) {
-                cudaFuncAttributes fa{};
-                cudaFuncGetAttributes(&fa, rk);
-                std::fprintf(stderr,
-                             "gnsb: reduce launch failed: grid=%d threads=%d dyn_smem=%zu static=%zu max_dyn=%d "
-                             "eb=%d B=%lld M=%lld D=%lld rows_grid=%d stream=%p err=%s\n",
-                             p.rgrid, p.rthreads, p.rsmem, fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes, p.eb,
-                             (long long)c.B, (long long)c.M, (long long)c.D, p.grid, (void*)st, cudaGetErrorString(e));
-            }
-            return 2;
-        }
         return 0;
+    }
+
+    static int run(const LnBwdCall& c, cudaStream_t st, const char** why, cudaError_t* cerr) {
+        LnRedItem item{};
+        if (int rc = run_rows(c, st, why, cerr, &item.info)) return rc;
+        item.B = c.B;
+        item.M = c.M;
+        item.D = c.D;
+        item.ws = c.ws;
+        item.dgamma = c.dgamma;
+        item.dbeta = c.dbeta;
+        item.raw_g = c.raw_g;
+        item.raw_b = c.raw_b;
+        item.sums = c.sums;
+        return ln_bwd_reduce_run(sizeof(typename C::Acc) == 8, c.norms, &item, 1, st, c.trace2, why, cerr);
     }
 };
 
@@ -339,6 +287,33 @@ int ln_bwd_run(const LnBwdCall& c, cudaStream_t st, const char** why, cudaError_
     return dispatch_bwd<T, BwdRunOp>(c.D, why, 1, c, st, why, cerr);
 }
 
+template <typename C>
+struct BwdRowsOp {
+    static int call(const LnBwdCall& c, cudaStream_t st, const char** why, cudaError_t* cerr, LnRedPlanInfo* info) {
+        return BwdOp<C>::run_rows(c, st, why, cerr, info);
+    }
+};
+template <typename C>
+struct BwdInfoOp {
+    static int call(int64_t B, int64_t M, int64_t D, LnRedPlanInfo* info, const char** why) {
+        BwdPlan p;
+        if (int rc = BwdOp<C>::plan(B, M, D, p, why)) return rc;
+        BwdOp<C>::fill_info(p, info);
+        return 0;
+    }
+};
+
+template <typename T>
+int ln_bwd_rows_run(const LnBwdCall& c, cudaStream_t st, const char** why, cudaError_t* cerr) {
+    LnRedPlanInfo info;
+    return dispatch_bwd<T, BwdRowsOp>(c.D, why, 1, c, st, why, cerr, &info);
+}
+
+template <typename T>
+int ln_bwd_plan_info(int64_t B, int64_t M, int64_t D, LnRedPlanInfo* out, const char** why) {
+    return dispatch_bwd<T, BwdInfoOp>(D, why, 1, B, M, D, out, why);
+}
+
 template <typename T>
 int ln_bwd_workspace(int64_t B, int64_t M, int64_t D, size_t* bytes, const char** why) {
     BwdPlan p;
@@ -367,6 +342,8 @@ int ln_fwd_run(const LnFwdCall& c, cudaStream_t st, const char** why, cudaError_
 
 #define GNSB_INSTANTIATE_LN(T)                                                                          \
     template int ln_bwd_run<T>(const LnBwdCall&, cudaStream_t, const char**, cudaError_t*);             \
+    template int ln_bwd_rows_run<T>(const LnBwdCall&, cudaStream_t, const char**, cudaError_t*);        \
+    template int ln_bwd_plan_info<T>(int64_t, int64_t, int64_t, LnRedPlanInfo*, const char**);          \
     template int ln_bwd_workspace<T>(int64_t, int64_t, int64_t, size_t*, const char**);                 \
     template int ln_bwd_geometry<T>(int64_t, int64_t, int64_t, int*, int*, int*);                       \
     template int ln_fwd_run<T>(const LnFwdCall&, cudaStream_t, const char**, cudaError_t*);

@@ -274,3 +274,72 @@ def sqnorm(v: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
     v = v.contiguous()
     _lib.check(_lib.lib().gnsb_sqnorm(_ptr(v), v.numel(), gnsb_dtype(v.dtype), _ptr(out), _stream_ptr(v.device)))
     return out
+
+
+class PendingLayerNorm:
+    """A LayerNorm whose row pass ran (dx is final) and whose stage 2 is
+    deferred to `layernorm_backward_reduce` (gnsb_ln_bwd_rows / gnsb_ln_bwd_reduce).
+    Holds its own workspace and the output tensors the reduce will fill."""
+
+    def __init__(self, B, M, D, dt, ws, dgamma, dbeta, raw_g, raw_b, sums):
+        self.B, self.M, self.D, self.dt = B, M, D, dt
+        self.ws, self.dgamma, self.dbeta, self.raw_g, self.raw_b, self.sums = ws, dgamma, dbeta, raw_g, raw_b, sums
+
+    def _c(self):
+        return _lib.LnBwdPending(self.ws.data_ptr(), self.ws.numel(), self.B, self.M, self.D, self.dt,
+                                 self.dgamma.data_ptr(), self.dbeta.data_ptr(), self.raw_g.data_ptr(),
+                                 self.raw_b.data_ptr(), self.sums.data_ptr())
+
+    def result(self, with_norms: bool = True) -> LayerGradOutput:
+        per_ex, raw = {}, {}
+        if with_norms:
+            bd = float(self.B)
+            per_ex = {"gamma": self.sums[0] / bd * (bd * bd), "beta": self.sums[1] / bd * (bd * bd)}
+            raw = {"gamma": self.raw_g, "beta": self.raw_b}
+        return LayerGradOutput({"gamma": self.dgamma, "beta": self.dbeta}, per_ex, raw, self.B, self.sums)
+
+
+def layernorm_backward_rows(layer: LayerNormLayer, cache: LayerNormCache, g: torch.Tensor,
+                            need_input_grad: bool = True):
+    """Row pass of the fused backward: returns (dx, PendingLayerNorm).  The
+    per-example combine, squares and dgamma/dbeta of any number of pending
+    layers then run in one `layernorm_backward_reduce` launch."""
+    k = layer.gamma.numel()
+    src = cache.x if (cache.x is not None and cache.mean is not None) else cache.normalized
+    if src is None:
+        raise ValueError("layers: cache holds neither (x, mean) nor normalized")
+    if tuple(src.shape) != tuple(g.shape):
+        raise ValueError("layers: cache/gradient shape mismatch")
+    B, M, D = _bmk(g.shape)
+    if D != k:
+        raise ValueError("layers: gradient trailing extent does not match gamma")
+    if B == 0:
+        raise ValueError("layers: empty batch")
+    dev = g.device
+    sd = stat_dtype(g.dtype)
+    g = g.contiguous()
+    src = src.contiguous()
+    mean = cache.mean.to(sd).contiguous() if src is cache.x else None
+    rstd = cache.inv_std.to(sd).contiguous()
+    gamma = layer.gamma.to(device=dev, dtype=sd).contiguous()
+    dx = torch.empty_like(g) if need_input_grad else None
+    dt = gnsb_dtype(g.dtype)
+    ws = torch.zeros(ctypes_size(B, M, D, dt), dtype=torch.uint8, device=dev)  # owned by the pending layer
+    _lib.check(_lib.lib().gnsb_ln_bwd_rows(_ptr(src), _ptr(mean), _ptr(rstd), _ptr(g), _ptr(gamma), _ptr(dx), B, M,
+                                           D, dt, _ptr(ws), ws.numel(), _stream_ptr(dev)))
+    pend = PendingLayerNorm(B, M, D, dt, ws, torch.empty(D, dtype=sd, device=dev), torch.empty(D, dtype=sd, device=dev),
+                            torch.zeros(B, dtype=torch.float64, device=dev),
+                            torch.zeros(B, dtype=torch.float64, device=dev),
+                            torch.zeros(4, dtype=torch.float64, device=dev))
+    return dx, pend
+
+
+def layernorm_backward_reduce(pending, with_norms: bool = True):
+    """Stage 2 of every pending layer in one launch; returns their LayerGradOutputs."""
+    pending = list(pending)
+    if not pending:
+        return []
+    arr = (_lib.LnBwdPending * len(pending))(*[p._c() for p in pending])
+    dev = pending[0].ws.device
+    _lib.check(_lib.lib().gnsb_ln_bwd_reduce(arr, len(pending), 1 if with_norms else 0, _stream_ptr(dev)))
+    return [p.result(with_norms) for p in pending]

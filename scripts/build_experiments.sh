@@ -2,6 +2,6 @@
 set -e
 cd "$(dirname "$0")/../experiments"
 NV="nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xcompiler -fPIC -shared -I../include"
-$NV -o libln_sweep.so ln_sweep.cu &
+$NV -o libln_sweep.so ln_sweep.cu ../paper_2411_00999_b200/csrc/ln_reduce.cu &
 $NV -o liblaunch_overhead.so launch_overhead.cu &
 wait

@@ -312,3 +312,47 @@ def test_two_streams_distinct_workspaces(cuda):
     for o in outs:
         assert torch.equal(o.input_grad, base.input_grad)
         assert torch.equal(o.grads.sums4, base.grads.sums4)
+
+
+def test_deferred_grouped_reduce_matches_per_layer(cuda):
+    """gnsb_ln_bwd_rows for several LayerNorms + one gnsb_ln_bwd_reduce equals
+    per-layer gnsb_ln_bwd: dx and dgamma/dbeta bitwise (same kernels, same
+    per-column order), norm records to 1e-12 (the per-example squares are
+    summed over different column ranges)."""
+    m = _mod()
+    from paper_2411_00999_b200 import layers
+
+    shapes = [(torch.bfloat16, 4, 96, 768), (torch.bfloat16, 3, 70, 4096), (torch.float32, 5, 33, 1024),
+              (torch.bfloat16, 2, 8, 13)]
+    pend, ref, dxs = [], [], []
+    for i, (dt, B, T, D) in enumerate(shapes):
+        x, dy, gamma, beta = m.synth_ln(B, T, D, dt, cuda, stream0=40 + 8 * i)
+        layer = m.LayerNormLayer(gamma, beta)
+        f = m.layernorm_forward(layer, x)
+        ref.append(m.layernorm_backward_simultaneous(layer, f.cache, dy))
+        dx, p = layers.layernorm_backward_rows(layer, f.cache, dy)
+        dxs.append(dx)
+        pend.append(p)
+    out = layers.layernorm_backward_reduce(pend)
+    torch.cuda.synchronize()
+    for r, o, dx in zip(ref, out, dxs):
+        assert torch.equal(r.input_grad, dx)
+        assert torch.equal(r.grads.weight_grads["gamma"], o.weight_grads["gamma"])
+        assert torch.equal(r.grads.weight_grads["beta"], o.weight_grads["beta"])
+        assert close(r.grads.per_example_sqnorms_raw["gamma"].cpu().numpy(),
+                     o.per_example_sqnorms_raw["gamma"].cpu().numpy(), 1e-12)
+        assert close(r.grads.per_example_sqnorms_raw["beta"].cpu().numpy(),
+                     o.per_example_sqnorms_raw["beta"].cpu().numpy(), 1e-12)
+        assert close(r.grads.sums4.cpu().numpy(), o.sums4.cpu().numpy(), 1e-12)
+    # the plain twin through the same path
+    pend2 = []
+    for i, (dt, B, T, D) in enumerate(shapes[:2]):
+        x, dy, gamma, beta = m.synth_ln(B, T, D, dt, cuda, stream0=40 + 8 * i)
+        layer = m.LayerNormLayer(gamma, beta)
+        f = m.layernorm_forward(layer, x)
+        pend2.append(layers.layernorm_backward_rows(layer, f.cache, dy)[1])
+    out2 = layers.layernorm_backward_reduce(pend2, with_norms=False)
+    torch.cuda.synchronize()
+    for r, o in zip(ref[:2], out2):
+        assert torch.equal(r.grads.weight_grads["gamma"], o.weight_grads["gamma"])
+        assert o.per_example_sqnorms == {}
