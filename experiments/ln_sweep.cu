@@ -40,13 +40,24 @@ using bf = __nv_bfloat16;
     X(28, 1, 4, 8, 2, true, 0) \
     X(29, 2, 2, 8, 1, true, 0) \
     X(30, 2, 4, 4, 2, true, 0) \
+    X(31, 16, 2, 1, 2, true, 0) \
+    X(32, 16, 2, 1, 2, true, 1) \
+    X(33, 8, 4, 1, 1, true, 0) \
+    X(34, 8, 4, 1, 2, true, 0) \
+    X(35, 3, 1, 2, 2, true, 1, 2) \
+    X(36, 3, 1, 4, 1, true, 1, 2) \
+    X(37, 4, 1, 2, 2, true, 1, 2) \
+    X(38, 4, 1, 3, 1, true, 1, 2) \
+    X(39, 8, 1, 1, 2, true, 1, 2) \
+    X(40, 4, 2, 1, 2, true, 1, 2) \
+    X(41, 1, 3, 4, 2, true, 1, 2) \
 
 extern "C" {
-int sweep_n() { return 31; }
+int sweep_n() { return 42; }
 
 int sweep_desc(int id, int* out) {
-#define DESC(i, gw, vpt, g, rpg, prod, keep) \
-    if (id == i) { out[0] = gw; out[1] = vpt; out[2] = g; out[3] = rpg; out[4] = prod; out[5] = LnBwdCfg<bf, gw, vpt, g, rpg, prod, keep>::KEEP; return 0; }
+#define DESC(i, gw, vpt, g, rpg, prod, keep, ...) \
+    if (id == i) { out[0] = gw; out[1] = vpt; out[2] = g; out[3] = rpg; out[4] = prod; out[5] = LnBwdCfg<bf, gw, vpt, g, rpg, prod, keep, ##__VA_ARGS__>::KEEP; return 0; }
     CFGS(DESC)
     return -1;
 }
@@ -58,8 +69,8 @@ int sweep_run(int id, const void* x, const void* mean, const void* rstd, const v
     LnBwdCall c{x, mean, rstd, dy, gamma, dx, dgamma, dbeta, rg, rb, sums, norms, B, M, D, ws, wsb, trace, trace2};
     const char* why = nullptr;
     cudaError_t ce = cudaSuccess;
-#define RUN(i, gw, vpt, g, rpg, prod, keep) \
-    if (id == i) { int rc = BwdOp<LnBwdCfg<bf, gw, vpt, g, rpg, prod, keep>>::run(c, (cudaStream_t)stream, &why, &ce); if (rc == 1) fprintf(stderr, "cfg%d: %s\n", i, why ? why : "?"); return rc ? (rc == 2 ? 1000 + (int)ce : 1) : 0; }
+#define RUN(i, gw, vpt, g, rpg, prod, keep, ...) \
+    if (id == i) { int rc = BwdOp<LnBwdCfg<bf, gw, vpt, g, rpg, prod, keep, ##__VA_ARGS__>>::run(c, (cudaStream_t)stream, &why, &ce); if (rc == 1) fprintf(stderr, "cfg%d: %s\n", i, why ? why : "?"); return rc ? (rc == 2 ? 1000 + (int)ce : 1) : 0; }
     CFGS(RUN)
     return -1;
 }

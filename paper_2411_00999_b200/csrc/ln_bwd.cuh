@@ -76,7 +76,7 @@ struct LnRedArgs {
     unsigned long long* trace;  // optional [grid][6]
 };
 
-template <typename T, int GW, int VPT, int G, int RPG, bool PROD_ = true, int KEEP_ = -1>
+template <typename T, int GW, int VPT, int G, int RPG, bool PROD_ = true, int KEEP_ = -1, int CPS_ = 1>
 struct LnBwdCfg {
     using Acc = typename Traits<T>::Acc;
     using Row = T;
@@ -88,6 +88,7 @@ struct LnBwdCfg {
     // registers are allocated for warps in groups of 4: bound the register
     // budget by the rounded-up block so one CTA always fits on an SM
     static constexpr int kBoundThreads = (kThreads + 127) / 128 * 128;
+    static constexpr int kCps = CPS_;             // resident CTAs per SM (1, or 2 for narrow rows)
     static constexpr int R = G * RPG;           // rows per stage
     static constexpr int GT = GW * 32;          // threads per row group
     static constexpr int NQ = 2 * RPG;          // row sums per stage and group: (s1, s2) per row
@@ -118,7 +119,7 @@ struct LnBwdCfg {
 };
 
 template <typename C, bool HAS_MEAN>
-__global__ void __launch_bounds__(C::kBoundThreads, 1) ln_bwd_kernel(LnBwdArgs a) {
+__global__ void __launch_bounds__(C::kBoundThreads, C::kCps) ln_bwd_kernel(LnBwdArgs a) {
     using T = typename C::Row;
     constexpr int GW = C::kGW, VPT = C::kVPT, G = C::kG, RPG = C::kRPG;
     using Acc = typename C::Acc;

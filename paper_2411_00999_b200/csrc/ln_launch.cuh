@@ -48,7 +48,9 @@ int plan_bwd(int64_t B, int64_t M, int64_t D, BwdPlan& p, const char** why) {
     constexpr int W = Traits<T>::W;
     constexpr int G = C::kG;
     p.Dp = (int)((D + W - 1) / W * W);
-    const size_t budget = (size_t)smem_optin_bytes() - 1024;
+    // kCps CTAs share an SM's shared memory (1 KB per CTA is reserved by the driver)
+    const size_t budget = (C::kCps == 1) ? (size_t)smem_optin_bytes() - 1024
+                                         : (size_t)(228 * 1024) / C::kCps - 2048;
     p.stages = 0;
     for (int s = 8; s >= 2; --s)  // >= 2: pass 2 holds a slot while the next stage is consumed
         if (C::smem_bytes(s, p.Dp) <= budget) {
@@ -64,7 +66,7 @@ int plan_bwd(int64_t B, int64_t M, int64_t D, BwdPlan& p, const char** why) {
     p.G = G;
     const int64_t N = B * M;
     const int sms = device_sm_count();
-    p.grid = (int)(N < sms ? N : sms);
+    p.grid = (int)(N < (int64_t)sms * C::kCps ? N : (int64_t)sms * C::kCps);
     if (p.grid < 1) p.grid = 1;
     size_t off = 256;  // counters
     p.off_partial = off;
@@ -122,7 +124,7 @@ struct BwdOp {
                 *why = "ln_bwd plan (smem attribute / occupancy)";
                 return 2;
             }
-            if (occ >= 1) break;
+            if (occ >= C::kCps) break;
             if (p.stages <= 2) {
                 *cerr = cudaErrorLaunchOutOfResources;
                 return 2;

@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -25 > gpurun_out/pytest_gpu.log
-timeout 900 python bench.py --no-cpu > gpurun_out/bench.log 2>&1
+timeout 600 python experiments/ln_sweep.py 768,1024,2048,4096 15,35,36,37,38,41,10,5,39,40,0 > gpurun_out/sweep_cps.log 2>&1
