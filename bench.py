@@ -234,21 +234,25 @@ def run_ours(args):
 
     pend = (_lib.LnBwdPending * len(cases))(*[c.pending(_lib) for c in cases])
 
-    def run_step(norms, with_collective):
-        """One step: the fused (or plain) LN backward for every D of the sweep,
-        as a backward pass runs it: the row pass of each layer as it comes, then
-        the deferred stage 2 of all of them in one launch (gnsb_ln_bwd_reduce);
-        plus for N > 1 the all-reduce of the two exchange buckets (all layers'
-        [dgamma | dbeta] fp32 and their fp64 norm records) and the re-formed
-        ||G_big||^2 of the reduced gradients."""
+    def run_step(norms):
+        """The compute of one step (captured as one CUDA graph): the fused (or
+        plain) LN backward for every D of the sweep, as a backward pass runs it:
+        the row pass of each layer as it comes, then the deferred stage 2 of all
+        of them in one launch (gnsb_ln_bwd_reduce)."""
         sp_now = torch.cuda.current_stream(dev).cuda_stream
         for c in cases:
             c.run_rows(sp_now)
         rc = lib.gnsb_ln_bwd_reduce(pend, len(cases), 1 if norms else 0, sp_now)
         if rc:
             raise RuntimeError(lib.gnsb_last_error().decode())
-        if with_collective and world > 1:
-            buckets.reduce()
+
+    def exchange(norms):
+        """N > 1: the step's one exchange, issued eagerly after the
+        graph: all-reduce of every layer's [dgamma | dbeta] (fp32 bucket) and,
+        with norms, of the fp64 norm records, then ||G_big||^2 re-formed from
+        the reduced gradients.  The plain twin all-reduces its gradients too."""
+        if world > 1:
+            buckets.reduce(records=norms)
 
     def timed(case, norms):
         """Single kernel, cold: L2 flushed (256 MiB write) before, CUDA events around."""
@@ -264,28 +268,21 @@ def run_ours(args):
     side.wait_stream(stream)
     with torch.cuda.stream(side):
         for _ in range(args.warmup):
-            run_step(True, True)
-            run_step(False, False)
+            run_step(True)
+            run_step(False)
     stream.wait_stream(side)
     torch.cuda.synchronize()
     graphs = {}
     for norms in (True, False):
-        try:
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                run_step(norms, norms)
-            graphs[norms] = g
-        except Exception as exc:  # fall back to direct launches
-            graphs[norms] = None
-            graph_error = repr(exc)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            run_step(norms)
+        graphs[norms] = g
     torch.cuda.synchronize()
 
     def replay(norms):
-        g = graphs[norms]
-        if g is not None:
-            g.replay()
-        else:
-            run_step(norms, norms)
+        graphs[norms].replay()
+        exchange(norms)
 
     for _ in range(args.warmup):
         replay(True)
@@ -365,6 +362,22 @@ def run_ours(args):
     if rank == 0 and not args.no_cpu:
         cpu = cpu_baseline(args)
 
+    # ---- the dominant kernel alone: the row pass at the widest D of the sweep
+    # (largest share of the step), back-to-back launches, events on its stream
+    dom = max(cases, key=lambda c: c.D)
+    for _ in range(3):
+        dom.run_rows(sp)
+    nrep = max(args.steps, 10)
+    d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    d0.record(stream)
+    for _ in range(nrep):
+        dom.run_rows(sp)
+    d1.record(stream)
+    torch.cuda.synchronize()
+    dom_us = d0.elapsed_time(d1) * 1e3 / nrep
+    dom_bytes = dom.bytes - 8 * dom.D - 16 * dom.B  # the row pass: all but the dgamma/dbeta and norm outputs
+    dom_achieved = dom_bytes / (dom_us * 1e-6) / 1e9
+
     extra = {}
     if rank == 0 and not args.no_extra:
         extra["cfg3_linear"] = run_cfg3(m, lib, dev, torch, np)
@@ -380,14 +393,19 @@ def run_ours(args):
                    "parallelism": f"dp{world}", "backend": backend if world > 1 else None,
                    "l2": "inputs larger than L2: a step streams %.2f GB (>> 126 MB L2) between reuses of any buffer"
                          % (step_bytes / 1e9),
-                   "launch": "one CUDA graph per step" if graphs.get(True) is not None else "direct launches",
+                   "launch": "one CUDA graph per step (compute); N > 1: the bucket all-reduce eagerly after it",
                    "stage2": "deferred: row pass per layer, one grouped reduce launch per step (gnsb_ln_bwd_reduce)"},
         "overhead_pct": 100.0 * (step_f - step_p) / step_p, "overhead_pct_D_ge_1024": overhead_ge1024,
         "step_ms_fused": step_f, "step_ms_plain": step_p,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "peak_kind": peak_kind, "frac_of_8TBps": achieved / 8000.0, "traffic": traffic,
-                     "kernel": "ln_bwd_kernel<bf16,...,HAS_MEAN=1> (one per D) + one ln_bwd_reduce_group_kernel<float,NORMS=1> per step",
-                     "achieved_def": "algorithmic bytes of the 5 launches / median graph-replayed step time"},
+        "roofline": {"bound": "hbm", "achieved": dom_achieved, "peak": peak, "unit": "GB/s",
+                     "frac": dom_achieved / peak, "peak_kind": peak_kind, "frac_of_8TBps": dom_achieved / 8000.0,
+                     "traffic": traffic, "alg_bytes_per_launch": dom_bytes, "us_per_launch": dom_us,
+                     "kernel": f"ln_bwd_kernel<bf16, D={dom.D}> row pass (largest share of the step)",
+                     "achieved_def": "algorithmic bytes per launch / CUDA-event duration, back-to-back launches"},
+        "roofline_step": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                          "frac_of_8TBps": achieved / 8000.0,
+                          "kernels": "5 row passes (one per D) + one ln_bwd_reduce_group_kernel<float,NORMS=1>",
+                          "achieved_def": "algorithmic bytes of the step / median graph-replayed step time"},
         "sweep": sweep_rows, "e2e": e2e, "cpu_baseline": cpu, **extra,
         "gpu_launches": (len(cases) + 1 + (2 * len(cases) if world > 1 else 0)) * args.steps, "clocks": clk.summary(),
     }
@@ -653,7 +671,7 @@ def load_traffic():
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(p) as f:
-            return json.load(f).get("ln_bwd_bf16_D4096_bytes_per_launch")
+            return json.load(f).get("ln_rows_bf16_D8192_bytes_per_launch")
     except Exception:
         return None
 

@@ -66,12 +66,13 @@ class GradBuckets:
     def record(self, l: int) -> torch.Tensor:
         return self.records[l]
 
-    def reduce(self, group=None, sqnorm: Optional[Callable] = None) -> None:
+    def reduce(self, group=None, sqnorm: Optional[Callable] = None, records: bool = True) -> None:
         """Sum both buckets over the process group, then re-form ||grad||^2
         of every reduced parameter vector into record slots 2 and 3.
 
         `sqnorm(v, out)` writes the fp64 squared norm of v into the 0-d
         tensor `out`. The default is the device kernel `gnsb_sqnorm`.
+        records=False reduces the gradients only (a plain backward without norms).
         """
         if sqnorm is None:
             from .layers import sqnorm as _device_sqnorm
@@ -79,7 +80,10 @@ class GradBuckets:
             sqnorm = _device_sqnorm
         if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
             dist.all_reduce(self.grads, group=group)
-            dist.all_reduce(self.records, group=group)
+            if records:
+                dist.all_reduce(self.records, group=group)
+        if not records:
+            return
         for l, (p0, p1) in enumerate(self._views):
             sqnorm(p0, out=self.records[l, 2])
             sqnorm(p1, out=self.records[l, 3])
