@@ -153,6 +153,28 @@ gnsb_status gnsb_linear_dx(const void* g, const void* W, void* dx, int64_t rows,
                            void* stream);
 
 /* ------------------------------------------------------------------------
+ * Embedding layer: table gradient + per-example squared norms (paper Alg. 3).
+ * Replaces gnstk::embedding_backward_simultaneous
+ * (proj/include/gnstk/layers.hpp:85-88, proj/src/layers.cpp:315-368).
+ *   ids   : [B, T] int32 device token ids in [0, V)
+ *   g     : [B, T, D] upstream gradient (dtype dt) of a MEAN-reduced loss
+ *   dW    : [V, D] fp32 (fp64 for GNSB_F64 rows); untouched rows are zero
+ *   raw_w : [B] fp64 uncorrected per-example ||dW_b||^2 (nullable)
+ *   sums  : [4] fp64 (nullable): sums[0] = sum_b raw_w, sums[2] = ||dW||^2
+ *   bad_ids : nullable device int32, set to 1 when an id was outside [0, V)
+ *             (such tokens contribute nothing; the reference throws
+ *             "layers: id out of range", which the C++ drop-in does after
+ *             checking the host ids).
+ * With fp64 rows dW and raw_w reproduce the reference's operation order bit
+ * for bit.  Limit: T <= 16384 (one example's ids are sorted on chip).
+ */
+gnsb_status gnsb_embedding_pe_workspace_size(int64_t B, int64_t T, int64_t V, int64_t D, gnsb_dtype dt,
+                                             size_t* bytes);
+gnsb_status gnsb_embedding_pe(const int32_t* ids, const void* g, void* dW, double* raw_w, double* sums, int64_t B,
+                              int64_t T, int64_t V, int64_t D, gnsb_dtype dt, void* ws, size_t ws_bytes,
+                              int32_t* bad_ids, void* stream);
+
+/* ------------------------------------------------------------------------
  * Deterministic fp64 squared norm of a device vector (fp32 or fp64 data):
  * out[0] = sum_i v[i]^2.  Used after the batch-sharded all-reduce, where
  * ||G_big||^2 must be formed from the REDUCED gradient.

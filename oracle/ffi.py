@@ -53,6 +53,8 @@ class Oracle:
         h.orc_linear_backward.argtypes = [_dp, _dp, _dp, ctypes.c_int, _i64, _i64, _i64, _i64, _dp, _dp, _dp, _dp,
                                           _dp, _dp]
         h.orc_linear_frobenius.argtypes = [_dp, _dp, _i64, _i64, _i64, _i64, _dp]
+        h.orc_embedding_backward.argtypes = [ctypes.POINTER(ctypes.c_int32), _dp, _i64, _i64, _i64, _i64, _dp, _dp,
+                                             _dp]
         h.orc_crossover_t.argtypes = [_i64, _i64, ctypes.c_int, _dp]
         h.orc_flops.argtypes = [_i64, _i64, _i64, _i64, ctypes.c_int, ctypes.POINTER(_i64)]
         h.orc_io_values.argtypes = [_i64, _i64, _i64, _i64, ctypes.c_int, ctypes.POINTER(_i64)]
@@ -153,6 +155,20 @@ class Oracle:
         if rc:
             raise ValueError(self.err())
         return out
+
+    def embedding_backward(self, ids, g, V):
+        """layers.cpp:315-368: ids [B, T] int32, g [B, T, D] -> dW [V, D], raw [B], corrected."""
+        ids = np.ascontiguousarray(ids, np.int32)
+        g = np.ascontiguousarray(g, np.float64)
+        B, T, D = g.shape
+        dW = np.empty((V, D))
+        raw = np.empty(B)
+        corr = np.empty(1)
+        rc = self.h.orc_embedding_backward(ids.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), _p(g), B, T, V, D,
+                                           _p(dW), _p(raw), _p(corr))
+        if rc:
+            raise ValueError(self.err())
+        return dict(dW=dW, raw_w=raw, corrected=float(corr[0]))
 
     def crossover_t(self, k, l, criterion):
         out = ctypes.c_double()

@@ -13,6 +13,8 @@
 //   lin_kat       proj/tests/test_layers.cpp:51-63, 77-85, 109-118
 //   lin_rand17    proj/tests/test_layers.cpp:87-107    (seed 17, 25 reps)
 //   frob_rand23   proj/tests/test_layers.cpp:135-149   (seed 23, 25 reps)
+//   emb_kat       proj/tests/test_layers.cpp:300-319   (embedding worked examples)
+//   emb_rand43    proj/tests/test_layers.cpp:321-347   (seed 43, 25 reps)
 //   ln_cfg1       BASELINE config 1 (B=8 T=128 D=768), synthetic recipe of SURVEY.md §8(d)
 #include <cmath>
 #include <cstdio>
@@ -178,6 +180,22 @@ void ln_cfg1() {
 
 }  // namespace
 
+void emit_emb(const char* fam, const EmbeddingLayer& layer, const std::vector<std::int32_t>& ids, Index b, Index t,
+              const Tensor& g) {
+    auto res = embedding_backward_simultaneous(layer, ids, b, t, g);
+    begin(fam);
+    std::fprintf(out, "\"B\": %lld, \"T\": %lld, \"V\": %lld, \"D\": %lld, ", (long long)b, (long long)t,
+                 (long long)layer.vocab(), (long long)layer.dim());
+    std::vector<double> idd(ids.begin(), ids.end());
+    arr("ids", idd.data(), (Index)idd.size());
+    arr("g", g);
+    arr("dW", res.weight_grads.at("weight"));
+    arr("raw_w", res.per_example_sqnorms_raw.at("weight"));
+    double corr[1] = {res.per_example_sqnorms.at("weight")};
+    arr("corrected", corr, 1);
+    end();
+}
+
 int main(int argc, char** argv) {
     out = argc > 1 ? std::fopen(argv[1], "w") : stdout;
     std::fprintf(out, "[");
@@ -262,6 +280,23 @@ int main(int argc, char** argv) {
             Tensor x = rnd({b, t, k}, rng);
             Tensor g = rnd({b, t, l}, rng);
             emit_linear("frob_rand23", layer, x, g, true);
+        }
+    }
+    {  // test_layers.cpp:300-319 (embedding worked examples)
+        EmbeddingLayer layer{Tensor({3, 1})};
+        emit_emb("emb_kat", layer, {0, 0}, 1, 2, Tensor({1, 2, 1}, {1, 2}));
+        emit_emb("emb_kat", layer, {0, 1}, 1, 2, Tensor({1, 2, 1}, {1, 2}));
+        emit_emb("emb_kat", layer, {0, 1}, 1, 2, Tensor({1, 2, 1}));
+    }
+    {  // test_layers.cpp:321-347 (seed 43, 25 reps)
+        GaussianStream rng(43);
+        for (int rep = 0; rep < 25; ++rep) {
+            const Index b = draw(rng, 1, 4), t = draw(rng, 1, 5), v = draw(rng, 2, 8), d = draw(rng, 1, 6);
+            EmbeddingLayer layer{rnd({v, d}, rng)};
+            std::vector<std::int32_t> ids(static_cast<std::size_t>(b * t));
+            for (auto& id : ids) id = static_cast<std::int32_t>(rng.rng.next_below(static_cast<std::uint64_t>(v)));
+            Tensor g = rnd({b, t, d}, rng);
+            emit_emb("emb_rand43", layer, ids, b, t, g);
         }
     }
     {  // a handful of Gaussian draws to pin the RNG restatement

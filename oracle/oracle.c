@@ -355,6 +355,61 @@ int orc_linear_frobenius(const double* x, const double* g, int64_t B, int64_t T,
     return ORC_OK;
 }
 
+/* layers.cpp:315-368.  Per example: rows of the table touched by the
+ * example accumulate g over its tokens (t order); the touched ids, ascending,
+ * give raw_b = one flat sum of squares and are added into dW (b order).
+ * Errors: an id outside [0, V) (layers.cpp:333), B == 0 (:322). */
+int orc_embedding_backward(const int32_t* ids, const double* g, int64_t B, int64_t T, int64_t V, int64_t D,
+                           double* dW, double* raw, double* corrected) {
+    if (B == 0) LFAIL("empty batch");
+    for (int64_t i = 0; i < B * T; ++i)
+        if (ids[i] < 0 || ids[i] >= V) LFAIL("id out of range");
+    double* scratch = (double*)calloc((size_t)(V * D > 0 ? V * D : 1), sizeof(double));
+    char* seen = (char*)calloc((size_t)(V > 0 ? V : 1), 1);
+    int64_t* touched = (int64_t*)malloc(sizeof(int64_t) * (size_t)(T > 0 ? T : 1));
+    for (int64_t i = 0; i < V * D; ++i) dW[i] = 0.0;
+    double sum_sq = 0.0;
+    for (int64_t b = 0; b < B; ++b) {
+        int64_t nt = 0;
+        for (int64_t t = 0; t < T; ++t) {
+            const int64_t id = ids[b * T + t];
+            if (!seen[id]) {
+                seen[id] = 1;
+                touched[nt++] = id;
+            }
+            const double* gr = g + (b * T + t) * D;
+            double* row = scratch + id * D;
+            for (int64_t j = 0; j < D; ++j) row[j] += gr[j];
+        }
+        /* ascending ids (insertion sort: T is small in every test family) */
+        for (int64_t i = 1; i < nt; ++i) {
+            const int64_t v = touched[i];
+            int64_t k = i - 1;
+            while (k >= 0 && touched[k] > v) {
+                touched[k + 1] = touched[k];
+                --k;
+            }
+            touched[k + 1] = v;
+        }
+        double sb = 0.0;
+        for (int64_t i = 0; i < nt; ++i) {
+            double* src = scratch + touched[i] * D;
+            for (int64_t j = 0; j < D; ++j) sb += src[j] * src[j];
+            double* dst = dW + touched[i] * D;
+            for (int64_t j = 0; j < D; ++j) dst[j] += src[j];
+            for (int64_t j = 0; j < D; ++j) src[j] = 0.0;
+            seen[touched[i]] = 0;
+        }
+        raw[b] = sb;
+        sum_sq += sb;
+    }
+    *corrected = sum_sq / (double)B * ((double)B * (double)B);
+    free(scratch);
+    free(seen);
+    free(touched);
+    return ORC_OK;
+}
+
 /* ------------------------------------------------------------------ gns -- */
 /* gns.cpp:14-18 */
 static int check_batches(const orc_grad_stats* s) {

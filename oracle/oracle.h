@@ -88,6 +88,9 @@ int orc_linear_backward(const double* x, const double* g, const double* W, int h
 int orc_linear_frobenius(const double* x, const double* g, int64_t B, int64_t T, int64_t K,
                          int64_t L, double* out);
 
+int orc_embedding_backward(const int32_t* ids, const double* g, int64_t B, int64_t T, int64_t V, int64_t D,
+                           double* dW, double* raw, double* corrected); /* layers.cpp:315-368 */
+
 /* ---- gns (proj/src/gns.cpp) ----------------------------------------------- */
 typedef struct {
     double g_big_sqnorm;

@@ -21,6 +21,7 @@ from .layers import (
     synth_linear,
     synth_ln,
 )
+from .embedding import embedding_backward_simultaneous
 from .nn import GnsTracker, LayerNormPE
 from .linear import LinearBackwardResult, LinearLayer, linear_backward_simultaneous, linear_perexample_sqnorm_frobenius
 from .gns import (
@@ -42,4 +43,5 @@ __all__ = [
     "DeviceGnsAccumulator", "EmaState", "GnsEstimate", "GradStats", "aggregate", "ema_update", "estimate_g2",
     "estimate_s", "make_gns_estimate", "smoothed_gns", "LinearBackwardResult", "LinearLayer",
     "linear_backward_simultaneous", "linear_perexample_sqnorm_frobenius", "GnsTracker", "LayerNormPE",
+    "embedding_backward_simultaneous",
 ]

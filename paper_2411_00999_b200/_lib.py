@@ -80,6 +80,9 @@ _SIGS = {
     "gnsb_linear_pe_norms": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i32, c_i32, c_vp,
                                      ctypes.c_size_t, c_vp]),
     "gnsb_linear_bias_pe": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i32, c_vp, ctypes.c_size_t, c_vp]),
+    "gnsb_embedding_pe_workspace_size": (c_i32, [c_i64, c_i64, c_i64, c_i64, c_i32, c_szp]),
+    "gnsb_embedding_pe": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i32, c_vp,
+                                  ctypes.c_size_t, c_vp, c_vp]),
     "gnsb_linear_dx": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i32, c_vp]),
     "gnsb_estimate_g2": (c_i32, [ctypes.POINTER(GradStats), c_dp]),
     "gnsb_estimate_s": (c_i32, [ctypes.POINTER(GradStats), c_dp]),

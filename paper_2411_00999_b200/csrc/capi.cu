@@ -472,6 +472,41 @@ gnsb_status gnsb_linear_bias_pe(const void* g, void* dbias, double* raw_b, doubl
     return e == cudaSuccess ? debug_ok("gnsb_linear_bias_pe") : cuda_fail(e, "linear_bias_pe launch");
 }
 
+gnsb_status gnsb_embedding_pe_workspace_size(int64_t B, int64_t T, int64_t V, int64_t D, gnsb_dtype dt,
+                                             size_t* bytes) {
+    if (!bytes || B < 0 || T < 0 || V < 1 || D < 1) return fail(GNSB_EINVAL, "layers: invalid extents");
+    if (dt != GNSB_F32 && dt != GNSB_BF16 && dt != GNSB_F64) return fail(GNSB_EINVAL, "layers: unknown dtype");
+    if (gnsb_status s = need_device("gnsb_embedding_pe_workspace_size")) return s;
+    *bytes = gnsb::embedding_workspace(B, T, V, D, (int)dt);
+    return debug_ok("gnsb_embedding_pe_workspace_size");
+}
+
+gnsb_status gnsb_embedding_pe(const int32_t* ids, const void* g, void* dW, double* raw_w, double* sums, int64_t B,
+                              int64_t T, int64_t V, int64_t D, gnsb_dtype dt, void* ws, size_t ws_bytes,
+                              int32_t* bad_ids, void* stream) {
+    if (B == 0) return fail(GNSB_EINVAL, "layers: empty batch");  // layers.cpp:322
+    if (B < 0 || T < 0 || V < 1 || D < 1) return fail(GNSB_EINVAL, "layers: invalid extents");
+    if (dt != GNSB_F32 && dt != GNSB_BF16 && dt != GNSB_F64) return fail(GNSB_EINVAL, "layers: unknown dtype");
+    if (T > 0 && !gnsb::embedding_shape_ok(T))
+        return fail(GNSB_EINVAL, "layers: sequence too long for the embedding kernel (T <= 16384)");
+    if (gnsb_status s = need_device("gnsb_embedding_pe")) return s;
+    if (!dW || !ws || (T > 0 && (!ids || !g))) return fail(GNSB_EINVAL, "layers: null pointer");
+    size_t need = 0;
+    gnsb_embedding_pe_workspace_size(B, T, V, D, dt, &need);
+    if (ws_bytes < need) return fail(GNSB_EINVAL, "layers: workspace too small (query gnsb_embedding_pe_workspace_size)");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaError_t e;
+    if (T == 0) {  // no tokens: zero table gradient and norms
+        e = cudaMemsetAsync(dW, 0, (size_t)V * D * stat_size(dt), st);
+        if (e == cudaSuccess && raw_w) e = cudaMemsetAsync(raw_w, 0, (size_t)B * 8, st);
+        if (e == cudaSuccess && sums) e = cudaMemsetAsync(sums, 0, 4 * 8, st);
+        if (e == cudaSuccess && bad_ids) e = cudaMemsetAsync(bad_ids, 0, 4, st);
+    } else {
+        e = gnsb::launch_embedding_pe((int)dt, ids, g, dW, raw_w, sums, B, T, V, D, ws, bad_ids, st);
+    }
+    return e == cudaSuccess ? debug_ok("gnsb_embedding_pe") : cuda_fail(e, "embedding_pe launch");
+}
+
 gnsb_status gnsb_linear_dx(const void* g, const void* W, void* dx, int64_t rows, int64_t K, int64_t L, gnsb_dtype dt,
                            void* stream) {
     if (rows < 0 || K < 1 || L < 1) return fail(GNSB_EINVAL, "layers: invalid extents");

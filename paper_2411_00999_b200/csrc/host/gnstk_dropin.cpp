@@ -257,6 +257,42 @@ Tensor linear_perexample_sqnorm_frobenius(const Tensor& x, const Tensor& g) {
     return out;
 }
 
+// -------------------------------------------------------------- embedding --
+LayerGradOutput embedding_backward_simultaneous(const EmbeddingLayer& layer, std::span<const std::int32_t> ids,
+                                                Index batch, Index t_len, const Tensor& g) {
+    const Index v = layer.vocab();
+    const Index d = layer.dim();
+    // layers.cpp:318-322, in the reference's order; ids are host data here
+    if (static_cast<Index>(ids.size()) != batch * t_len) fail("id count does not match batch * t_len");
+    if (g.shape() != Shape{batch, t_len, d}) fail("gradient shape mismatch");
+    if (batch == 0) fail("empty batch");
+    for (std::int32_t id : ids)
+        if (id < 0 || id >= v) fail("id out of range");
+    LayerGradOutput out;
+    out.batch_size = batch;
+    Tensor wgrad({v, d}), raw({batch});
+    double sums[4] = {0, 0, 0, 0};
+    DevBuf dg = upload(g), dids(sizeof(std::int32_t) * (ids.size() ? ids.size() : 1));
+    if (!ids.empty())
+        cuda_check(cudaMemcpy(dids.p, ids.data(), sizeof(std::int32_t) * ids.size(), cudaMemcpyHostToDevice), "upload");
+    DevBuf dW(sizeof(double) * v * d), draw(sizeof(double) * batch), dsums(sizeof(double) * 4, true);
+    std::size_t wsb = 0;
+    check(gnsb_embedding_pe_workspace_size(batch, t_len, v, d, GNSB_F64, &wsb));
+    DevBuf ws(wsb, true);
+    check(gnsb_embedding_pe(static_cast<const std::int32_t*>(dids.p), dg.p, dW.p, draw.as<double>(),
+                            dsums.as<double>(), batch, t_len, v, d, GNSB_F64, ws.p, wsb, nullptr, nullptr));
+    download(wgrad, dW);
+    download(raw, draw);
+    download(sums, dsums, 4);
+    // the reference sums the per-example values in example order (layers.cpp:360-366)
+    double sum_sq = 0.0;
+    for (Index b = 0; b < batch; ++b) sum_sq += raw[b];
+    out.weight_grads["weight"] = std::move(wgrad);
+    out.per_example_sqnorms["weight"] = corrected(sum_sq, batch);
+    out.per_example_sqnorms_raw["weight"] = std::move(raw);
+    return out;
+}
+
 // -------------------------------------------------------------------- gns --
 namespace {
 gnsb_grad_stats to_c(const GradStats& s) {

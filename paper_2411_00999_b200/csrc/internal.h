@@ -84,6 +84,11 @@ cudaError_t launch_gram_norms(const void* x, const void* g, double* raw, double*
 // raw[b] = sum_j q[b][j], sums[sum_slot] = sum_b raw[b] (fixed order, one CTA)
 cudaError_t launch_fold_rows(const double* q, int nb, int ncol, double* raw, double* sums, int sum_slot,
                              cudaStream_t st);
+// embedding table gradient + per-example norms (embedding_pe.cu); T <= 16384
+bool embedding_shape_ok(int64_t T);
+size_t embedding_workspace(int64_t B, int64_t T, int64_t V, int64_t D, int dt);
+cudaError_t launch_embedding_pe(int dt, const int32_t* ids, const void* g, void* dW, double* raw, double* sums,
+                                int64_t B, int64_t T, int64_t V, int64_t D, void* ws, int32_t* bad, cudaStream_t st);
 cudaError_t launch_linear_dx(int dt, const void* g, const void* W, void* dx, int64_t rows, int64_t K, int64_t L,
                              cudaStream_t st);
 

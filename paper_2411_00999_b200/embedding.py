@@ -1,0 +1,43 @@
+"""Embedding-table gradient with per-example squared norms (paper Alg. 3).
+
+Mirrors gnstk::embedding_backward_simultaneous (proj/include/gnstk/layers.hpp:85-88,
+proj/src/layers.cpp:315-368) over the C ABI `gnsb_embedding_pe`.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from .layers import _WS, LayerGradOutput, _ptr, _stream_ptr, gnsb_dtype, stat_dtype
+
+
+def embedding_backward_simultaneous(ids: torch.Tensor, g: torch.Tensor, vocab: int) -> LayerGradOutput:
+    """ids [B, T] int32 (device), g [B, T, D] gradient of a mean-reduced loss.
+    Returns weight grad [V, D] (fp32, fp64 for fp64 rows), the corrected
+    per-example norm (B * sum_b raw) and the raw per-example norms [B]."""
+    if g.dim() != 3:
+        raise ValueError("layers: gradient shape mismatch")
+    B, T, D = (int(v) for v in g.shape)
+    if ids.numel() != B * T:
+        raise ValueError("layers: id count does not match batch * t_len")
+    if B == 0:
+        raise ValueError("layers: empty batch")
+    if ids.numel() and (int(ids.min()) < 0 or int(ids.max()) >= vocab):  # layers.cpp:333
+        raise ValueError("layers: id out of range")
+    dev = g.device
+    ids = ids.to(device=dev, dtype=torch.int32).contiguous()
+    g = g.contiguous()
+    dt = gnsb_dtype(g.dtype)
+    sd = stat_dtype(g.dtype)
+    n = ctypes.c_size_t()
+    _lib.check(_lib.lib().gnsb_embedding_pe_workspace_size(B, T, vocab, D, dt, ctypes.byref(n)))
+    ws = _WS.get(dev, n.value, "embedding")
+    dW = torch.empty(vocab, D, dtype=sd, device=dev)
+    raw = torch.empty(B, dtype=torch.float64, device=dev)
+    sums = torch.zeros(4, dtype=torch.float64, device=dev)
+    _lib.check(_lib.lib().gnsb_embedding_pe(_ptr(ids), _ptr(g), _ptr(dW), _ptr(raw), _ptr(sums), B, T, vocab, D, dt,
+                                            _ptr(ws), ws.numel(), None, _stream_ptr(dev)))
+    bd = float(B)
+    return LayerGradOutput({"weight": dW}, {"weight": sums[0] / bd * (bd * bd)}, {"weight": raw}, B, sums)

@@ -182,6 +182,53 @@ int main() {
         CHECK(scaled.grads.per_example_sqnorms.at("bias") == 4.0 * base.grads.per_example_sqnorms.at("bias"));
         CHECK_THROWS_INVALID(linear_backward_simultaneous(layer, Tensor({2, 2, 5}), Tensor({2, 2, 4})));
     }
+    // ---- embedding (test_layers.cpp:300-347) ----
+    {
+        EmbeddingLayer layer{Tensor({3, 1})};
+        const std::int32_t ids_repeat[] = {0, 0};
+        Tensor g({1, 2, 1}, {1, 2});
+        auto res = embedding_backward_simultaneous(layer, ids_repeat, 1, 2, g);
+        CHECK(res.weight_grads.at("weight")[0] == 3);
+        CHECK(res.per_example_sqnorms.at("weight") == 9);
+        const std::int32_t ids_distinct[] = {0, 1};
+        auto res2 = embedding_backward_simultaneous(layer, ids_distinct, 1, 2, g);
+        CHECK(res2.weight_grads.at("weight")[0] == 1);
+        CHECK(res2.weight_grads.at("weight")[1] == 2);
+        CHECK(res2.per_example_sqnorms.at("weight") == 5);
+        auto zero = embedding_backward_simultaneous(layer, ids_distinct, 1, 2, Tensor({1, 2, 1}));
+        CHECK(zero.per_example_sqnorms.at("weight") == 0);
+        const std::int32_t bad_ids[] = {0, 5};
+        CHECK_THROWS_INVALID(embedding_backward_simultaneous(layer, bad_ids, 1, 2, g));
+    }
+    {
+        Rng rng{43};  // dense one-hot contraction per example, exact in fp64
+        for (int rep = 0; rep < 25; ++rep) {
+            const Index b = 1 + rng.below(4), t = 1 + rng.below(5), v = 2 + rng.below(7), d = 1 + rng.below(6);
+            EmbeddingLayer layer{rnd({v, d}, rng)};
+            std::vector<std::int32_t> ids((std::size_t)(b * t));
+            for (auto& id : ids) id = (std::int32_t)rng.below(v);
+            Tensor g = rnd({b, t, d}, rng);
+            auto res = embedding_backward_simultaneous(layer, ids, b, t, g);
+            Tensor total({v, d});
+            double mean_single = 0.0;
+            const Tensor& raw = res.per_example_sqnorms_raw.at("weight");
+            for (Index eb = 0; eb < b; ++eb) {
+                Tensor single({v, d});
+                for (Index tt = 0; tt < t; ++tt)
+                    for (Index j = 0; j < d; ++j) single[ids[eb * t + tt] * d + j] += g[(eb * t + tt) * d + j];
+                double sq = 0.0;
+                for (Index i = 0; i < single.size(); ++i) sq += single[i] * single[i];
+                mean_single += sq;
+                CHECK(close(raw[eb], sq, 1e-12, 1e-300));
+                for (Index i = 0; i < total.size(); ++i) total[i] += single[i];
+            }
+            mean_single /= (double)b;
+            bool eq = true;
+            for (Index i = 0; i < total.size(); ++i) eq = eq && res.weight_grads.at("weight")[i] == total[i];
+            CHECK(eq);
+            CHECK(close(res.per_example_sqnorms.at("weight"), (double)(b * b) * mean_single, 1e-9));
+        }
+    }
     // ---- gns (test_gns.cpp:15-124) ----
     {
         GradStats st{1.25, 1.5, 2, 1, 2};
