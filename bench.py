@@ -347,6 +347,35 @@ def run_ours(args):
             "grid": geo["grid"], "threads": geo["threads"], "stages": geo["stages"],
             "timing": "single cold launch: L2 flushed before, CUDA events around (includes launch latency)",
         })
+    # ---- per D in a model-like step: NL LayerNorms of that width back to back
+    # (distinct buffers, row pass each) + one grouped reduce, graph-replayed;
+    # the sustained rate of each width as a backward pass runs it
+    NL = 8
+    for i, c in enumerate(cases):
+        if args.no_extra:
+            break
+        extra_cases = [c] + [LnCase(m, lib, c.D, B_LOCAL, rank, dev, torch, GradBuckets([c.D], dev), 0)
+                             for _ in range(NL - 1)]
+        pend_d = (_lib.LnBwdPending * NL)(*[e.pending(_lib) for e in extra_cases])
+
+        def layer_step(norms, extra_cases=extra_cases, pend_d=pend_d):
+            spn = torch.cuda.current_stream(dev).cuda_stream
+            for e in extra_cases:
+                e.run_rows(spn)
+            if lib.gnsb_ln_bwd_reduce(pend_d, NL, 1 if norms else 0, spn):
+                raise RuntimeError(lib.gnsb_last_error().decode())
+
+        ms_f = time_graph(lambda: layer_step(True), torch, np, dev, reps=max(args.steps, 10))
+        ms_p = time_graph(lambda: layer_step(False), torch, np, dev, reps=max(args.steps, 10))
+        gbs = NL * c.bytes / (ms_f * 1e-3) / 1e9
+        sweep_rows[i].update({
+            "steady_layers": NL, "steady_fused_GBps": gbs, "steady_frac_of_measured_peak": gbs / peak,
+            "steady_plain_GBps": NL * c.bytes_plain / (ms_p * 1e-3) / 1e9,
+            "steady_overhead_pct": 100.0 * (ms_f - ms_p) / ms_p,
+            "steady_timing": f"{NL} layers of this width (distinct buffers) + one grouped reduce, CUDA graph",
+        })
+        del extra_cases
+        torch.cuda.empty_cache()
     big = [r for r in sweep_rows if r["D"] >= 1024]
     overhead_ge1024 = 100.0 * (sum(r["fused_us"] for r in big) - sum(r["plain_us"] for r in big)) / max(
         sum(r["plain_us"] for r in big), 1e-9)
