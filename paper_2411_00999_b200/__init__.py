@@ -23,6 +23,7 @@ from .layers import (
 )
 from .embedding import embedding_backward_simultaneous
 from .nn import GnsTracker, LayerNormPE
+from .model import EmbeddingPE, LinearPE, ToyModelPE
 from .linear import LinearBackwardResult, LinearLayer, linear_backward_simultaneous, linear_perexample_sqnorm_frobenius
 from .gns import (
     DeviceGnsAccumulator,
@@ -42,6 +43,6 @@ __all__ = [
     "layernorm_backward_simultaneous", "layernorm_forward", "ln_bwd_geometry", "sqnorm", "synth_linear", "synth_ln",
     "DeviceGnsAccumulator", "EmaState", "GnsEstimate", "GradStats", "aggregate", "ema_update", "estimate_g2",
     "estimate_s", "make_gns_estimate", "smoothed_gns", "LinearBackwardResult", "LinearLayer",
-    "linear_backward_simultaneous", "linear_perexample_sqnorm_frobenius", "GnsTracker", "LayerNormPE",
+    "linear_backward_simultaneous", "linear_perexample_sqnorm_frobenius", "GnsTracker", "LayerNormPE", "EmbeddingPE", "LinearPE", "ToyModelPE",
     "embedding_backward_simultaneous",
 ]

@@ -1,0 +1,194 @@
+"""GPU toy model over the three instrumented layer types.
+
+The reference's residual MLP language model (proj/include/gnstk/model.hpp:14-31,
+proj/src/model.cpp): embedding -> n_blocks x [LayerNorm -> linear -> tanh ->
+linear + residual] -> LayerNorm -> linear head, next-token cross-entropy
+(mean over tokens, mean over examples).  Here every layer's backward is the
+B200 kernel that also yields its per-example squared gradient norms, exactly
+what `model_backward` (proj/src/model.cpp:144-188) collects:
+
+    LayerNormPE  -> gnsb_ln_fwd / gnsb_ln_bwd            (fused LN backward)
+    LinearPE     -> torch GEMMs for y and dx (library), gnsb_linear_pe_norms
+                    for dW + per-example norms (tcgen05 when bf16 and aligned),
+                    gnsb_linear_bias_pe for the bias
+    EmbeddingPE  -> gnsb_embedding_pe
+
+After `loss.backward()` every layer holds a 4-double norm record
+{sum_b raw(p0), sum_b raw(p1), ||grad p0||^2, ||grad p1||^2} (p0 = weight or
+gamma, p1 = bias or beta); `GnsTracker` turns them into the PerExample GNS of
+Trainer::step (proj/src/trainer.cpp:363-418) on the device.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from typing import List, Optional, Tuple
+
+import torch
+
+from . import _lib
+from .layers import _WS, _ptr, _stream_ptr, gnsb_dtype, stat_dtype
+from .nn import LayerNormPE
+
+
+def _linear_norms(x: torch.Tensor, g: torch.Tensor, K: int, L: int, rec: torch.Tensor, has_bias: bool):
+    """dW [K, L] (+ dbias [L]) and the per-example norms of one linear layer."""
+    B = x.shape[0]
+    M = x.numel() // (B * K)
+    dt = gnsb_dtype(x.dtype)
+    sd = stat_dtype(x.dtype)
+    dev = x.device
+    n = ctypes.c_size_t()
+    _lib.check(_lib.lib().gnsb_linear_pe_workspace_size(B, M, K, L, dt, ctypes.byref(n)))
+    ws = _WS.get(dev, n.value, "linear")
+    dW = torch.empty(K, L, dtype=sd, device=dev)
+    raw = torch.empty(2, B, dtype=torch.float64, device=dev)
+    sp = _stream_ptr(dev)
+    _lib.check(_lib.lib().gnsb_linear_pe_norms(_ptr(x), _ptr(g), _ptr(dW), _ptr(raw[0]), _ptr(rec), B, M, K, L, 1, dt,
+                                               _ptr(ws), ws.numel(), sp))
+    db = None
+    if has_bias:
+        db = torch.empty(L, dtype=sd, device=dev)
+        _lib.check(_lib.lib().gnsb_linear_pe_workspace_size(B, M, 1, L, dt, ctypes.byref(n)))
+        ws2 = _WS.get(dev, n.value, "linear_bias")
+        _lib.check(_lib.lib().gnsb_linear_bias_pe(_ptr(g), _ptr(db), _ptr(raw[1]), _ptr(rec), B, M, L, dt, _ptr(ws2),
+                                                  ws2.numel(), sp))
+    return dW, db, raw
+
+
+class _LinearPEFunction(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, weight, bias, module):
+        if not x.is_cuda:
+            raise RuntimeError("LinearPE: the B200 path has no CPU fallback (input is on the CPU)")
+        y = torch.matmul(x, weight.to(x.dtype))
+        if bias is not None:
+            y = y + bias.to(x.dtype)
+        ctx.save_for_backward(x, weight)
+        ctx.has_bias = bias is not None
+        ctx.module = module
+        return y
+
+    @staticmethod
+    def backward(ctx, g):
+        x, weight = ctx.saved_tensors
+        module = ctx.module
+        g = g.contiguous().to(x.dtype)
+        x = x.contiguous()
+        K, L = weight.shape
+        rec = torch.zeros(4, dtype=torch.float64, device=x.device)
+        dW, db, raw = _linear_norms(x, g, K, L, rec, ctx.has_bias)
+        dx = torch.matmul(g, weight.to(g.dtype).t()) if ctx.needs_input_grad[0] else None
+        module.norm_record = rec
+        module.per_example_raw = {"weight": raw[0], "bias": raw[1]} if ctx.has_bias else {"weight": raw[0]}
+        module.batch_size = x.shape[0]
+        return dx, dW.to(weight.dtype), (db.to(weight.dtype) if db is not None else None), None
+
+
+class LinearPE(torch.nn.Module):
+    """y = x W + b with W [K, L] (the reference's layout, layers.hpp:13-16);
+    the backward also yields per-example ||dW_b||^2, ||db_b||^2 (raw) in
+    `per_example_raw` and the 4-double `norm_record`."""
+
+    layer_type = "linear"
+
+    def __init__(self, K: int, L: int, bias: bool = True, device=None, dtype=torch.float32):
+        super().__init__()
+        self.weight = torch.nn.Parameter(torch.zeros(K, L, device=device, dtype=dtype))
+        self.bias = torch.nn.Parameter(torch.zeros(L, device=device, dtype=dtype)) if bias else None
+        self.norm_record: Optional[torch.Tensor] = None
+        self.per_example_raw = None
+        self.batch_size = None
+
+    def forward(self, x):
+        return _LinearPEFunction.apply(x, self.weight, self.bias, self)
+
+
+class _EmbeddingPEFunction(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, ids, weight, module):
+        if not ids.is_cuda:
+            raise RuntimeError("EmbeddingPE: the B200 path has no CPU fallback (ids are on the CPU)")
+        ctx.save_for_backward(ids)
+        ctx.V = weight.shape[0]
+        ctx.module = module
+        return weight[ids.long()]
+
+    @staticmethod
+    def backward(ctx, g):
+        (ids,) = ctx.saved_tensors
+        module = ctx.module
+        from .embedding import embedding_backward_simultaneous
+
+        r = embedding_backward_simultaneous(ids, g.contiguous(), ctx.V)
+        module.norm_record = r.sums4
+        module.per_example_raw = {"weight": r.per_example_sqnorms_raw["weight"]}
+        module.batch_size = ids.shape[0]
+        return None, r.weight_grads["weight"], None
+
+
+class EmbeddingPE(torch.nn.Module):
+    """Token embedding [V, D]; the backward yields per-example ||dE_b||^2."""
+
+    layer_type = "embedding"
+
+    def __init__(self, V: int, D: int, device=None, dtype=torch.float32):
+        super().__init__()
+        self.weight = torch.nn.Parameter(torch.zeros(V, D, device=device, dtype=dtype))
+        self.norm_record = None
+        self.per_example_raw = None
+        self.batch_size = None
+
+    def forward(self, ids):
+        return _EmbeddingPEFunction.apply(ids, self.weight, self)
+
+
+class ToyModelPE(torch.nn.Module):
+    """proj/include/gnstk/model.hpp:14-31 on the GPU, initialised as
+    make_toy_model (proj/src/model.cpp:30-55): Gaussian weights with std 1
+    (embedding), 1/sqrt(D) (fc1, head), 1/sqrt(H) (fc2); zero biases; LN gamma 1,
+    beta 0.  (The draws come from torch's generator, not the reference's.)"""
+
+    def __init__(self, vocab: int, dim: int, hidden_multiplier: int, n_blocks: int, seed: int = 0, device=None):
+        super().__init__()
+        if vocab < 2 or dim < 2 or hidden_multiplier < 1 or n_blocks < 1:
+            raise ValueError("model: invalid model dims")
+        H = dim * hidden_multiplier
+        gen = torch.Generator(device="cpu").manual_seed(seed)
+        self.embed = EmbeddingPE(vocab, dim, device=device)
+        self.lns = torch.nn.ModuleList([LayerNormPE(dim, device=device) for _ in range(n_blocks)])
+        self.fc1 = torch.nn.ModuleList([LinearPE(dim, H, device=device) for _ in range(n_blocks)])
+        self.fc2 = torch.nn.ModuleList([LinearPE(H, dim, device=device) for _ in range(n_blocks)])
+        self.final_ln = LayerNormPE(dim, device=device)
+        self.head = LinearPE(dim, vocab, device=device)
+        with torch.no_grad():
+            self.embed.weight.copy_(torch.randn(vocab, dim, generator=gen))
+            for f1, f2 in zip(self.fc1, self.fc2):
+                f1.weight.copy_(torch.randn(dim, H, generator=gen) / math.sqrt(dim))
+                f2.weight.copy_(torch.randn(H, dim, generator=gen) / math.sqrt(H))
+            self.head.weight.copy_(torch.randn(dim, vocab, generator=gen) / math.sqrt(dim))
+
+    def forward(self, ids: torch.Tensor) -> torch.Tensor:
+        x = self.embed(ids)
+        for ln, f1, f2 in zip(self.lns, self.fc1, self.fc2):
+            x = x + f2(torch.tanh(f1(ln(x))))
+        return self.head(self.final_ln(x))
+
+    def loss(self, ids: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
+        """Mean over examples of the per-example mean-token cross-entropy
+        (proj/src/model.cpp:150-156: dlogits scaled by 1/(T*B))."""
+        logits = self.forward(ids)
+        B, T, V = logits.shape
+        ce = torch.nn.functional.cross_entropy(logits.reshape(B * T, V).float(), targets.reshape(-1).long(),
+                                               reduction="none")
+        return ce.reshape(B, T).mean(1).mean(0)
+
+    def instrumented_layers(self) -> List[Tuple[str, torch.nn.Module]]:
+        """Layers in the reference's LayerKey order of model_backward's output
+        (proj/src/model.cpp:183-187): embed, then per block ln, fc1, fc2, then
+        final_ln, head."""
+        out = [("embed", self.embed)]
+        for i, (ln, f1, f2) in enumerate(zip(self.lns, self.fc1, self.fc2)):
+            out += [(f"block{i}.ln", ln), (f"block{i}.fc1", f1), (f"block{i}.fc2", f2)]
+        out += [("final_ln", self.final_ln), ("head", self.head)]
+        return out

@@ -94,6 +94,8 @@ class LayerNormPE(torch.nn.Module):
     B examples.
     """
 
+    layer_type = "layernorm"
+
     def __init__(self, normalized_shape: int, eps: float = 1e-5, device=None, track_norms: bool = True):
         super().__init__()
         if not eps > 0.0:
@@ -121,19 +123,20 @@ class LayerNormPE(torch.nn.Module):
 
 
 class GnsTracker:
-    """Collects the norm records of tracked LayerNormPE modules after a backward
-    and runs the device GNS step (the PerExample packaging of Trainer::step,
-    proj/src/trainer.cpp:363-418): per layer g_big = ||dbeta||^2 + ||dgamma||^2,
-    g_small = corrected(beta) + corrected(gamma); groups {total, embedding,
-    linear, layernorm}; EMA with `alpha`."""
+    """Collects the norm records of tracked modules (LayerNormPE, and LinearPE /
+    EmbeddingPE from model.py) after a backward and runs the device GNS step:
+    the PerExample packaging of Trainer::step (proj/src/trainer.cpp:363-418):
+    per layer g_big = ||grad p1||^2 + ||grad p0||^2, g_small = corrected(p1) +
+    corrected(p0); groups {total, embedding, linear, layernorm} by each
+    module's `layer_type`; EMA with `alpha`."""
 
-    def __init__(self, modules: Iterable[LayerNormPE], alpha: float = 1.0):
+    def __init__(self, modules: Iterable[torch.nn.Module], alpha: float = 1.0):
         self.modules = list(modules)
         if not self.modules:
             raise ValueError("gns: no layers to track")
-        dev = self.modules[0].weight.device
+        dev = next(self.modules[0].parameters()).device
         self.records = torch.zeros(len(self.modules), 4, dtype=torch.float64, device=dev)
-        self.acc = DeviceGnsAccumulator(["layernorm"] * len(self.modules), alpha, dev)
+        self.acc = DeviceGnsAccumulator([m.layer_type for m in self.modules], alpha, dev)
 
     def step(self):
         """Returns device tensors (groups [4, 4] {g2, s, gns_ema, defined}, layers [n, 2])."""
