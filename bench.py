@@ -409,6 +409,7 @@ def run_ours(args):
 
     extra = {}
     if rank == 0 and not args.no_extra:
+        extra["ln_forward"] = run_ln_fwd(m, lib, cases, dev, torch, np)
         extra["cfg3_linear"] = run_cfg3(m, lib, dev, torch, np)
         extra["cfg4_gns"] = run_cfg4(m, lib, dev, torch, np)
         extra["cfg5_g1"] = run_cfg5(m, lib, dev, torch, np)
@@ -470,6 +471,28 @@ def time_graph(fn, torch, np, dev, reps=10, warm=3):
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))
     return float(np.median(ts))
+
+
+def run_ln_fwd(m, lib, cases, dev, torch, np):
+    """LayerNorm forward (gnsb_ln_fwd: y, mean, rstd) at every D of the sweep:
+    bytes = N*D*(s_in + s_out) + 8N + 8D."""
+    out = []
+    for c in cases:
+        y = torch.empty_like(c.x)
+        N = c.B * T
+
+        def fn(c=c, y=y):
+            rc = lib.gnsb_ln_fwd(c.x.data_ptr(), c.gamma.data_ptr(), c.beta.data_ptr(), y.data_ptr(),
+                                 c.mean.data_ptr(), c.rstd.data_ptr(), None, N, c.D, 1e-5, 1,
+                                 torch.cuda.current_stream(dev).cuda_stream)
+            if rc:
+                raise RuntimeError(lib.gnsb_last_error().decode())
+
+        ms = time_graph(fn, torch, np, dev, reps=10)
+        nbytes = N * c.D * 4 + 8 * N + 8 * c.D
+        out.append({"D": c.D, "us": ms * 1e3, "GBps": nbytes / (ms * 1e-3) / 1e9})
+        del y
+    return out
 
 
 def run_cfg3(m, lib, dev, torch, np):

@@ -27,11 +27,14 @@ struct LnFwdArgs {
     int64_t N, D;
     double eps;
     int aligned;
+    int64_t Dp;  // D rounded up to the thread coverage (gamma/beta staging)
 };
 
 template <typename T, int GW, int VPT>
 struct LnFwdCfg {
-    static constexpr int G = GW * 32 >= 256 ? 1 : 256 / (GW * 32);
+    // row groups per CTA (<= 15 when groups sync on named barriers 1..G)
+    static constexpr int G0 = GW * 32 >= 1024 ? 1 : 1024 / (GW * 32);
+    static constexpr int G = (GW > 1 && G0 > 15) ? 15 : G0;
     static constexpr int kThreads = G * GW * 32;
 };
 
@@ -70,8 +73,17 @@ __global__ void __launch_bounds__(LnFwdCfg<T, GW, VPT>::kThreads) ln_fwd_kernel(
         }
     };
 
-    for (int64_t row = (int64_t)blockIdx.x * G + g; row < N; row += (int64_t)gridDim.x * G) {
-        Acc xv[VPT][W];
+    // gamma/beta staged once per CTA in shared memory; the next row's x is
+    // loaded before this row's reductions (one row of latency hidden per group)
+    extern __shared__ __align__(16) unsigned char fsmem[];
+    Acc* gs = reinterpret_cast<Acc*>(fsmem);
+    Acc* bs = gs + a.Dp;
+    for (int64_t c = threadIdx.x; c < a.Dp; c += blockDim.x) {
+        gs[c] = c < D ? gam[c] : Acc(0);
+        bs[c] = c < D ? bet[c] : Acc(0);
+    }
+    __syncthreads();
+    auto load_row = [&](int64_t row, Acc (&xv)[VPT][W]) {
         const T* xr = xg + row * D;
 #pragma unroll
         for (int k = 0; k < VPT; ++k) {
@@ -88,6 +100,15 @@ __global__ void __launch_bounds__(LnFwdCfg<T, GW, VPT>::kThreads) ln_fwd_kernel(
                 for (int e = 0; e < W; ++e) xv[k][e] = (c0 + e < D) ? to_acc<T>(xr[c0 + e]) : Acc(0);
             }
         }
+    };
+
+    const int64_t stride = (int64_t)gridDim.x * G;
+    int64_t row = (int64_t)blockIdx.x * G + g;
+    Acc xv[VPT][W];
+    if (row < N) load_row(row, xv);
+    for (; row < N; row += stride) {
+        Acc xn[VPT][W];
+        if (row + stride < N) load_row(row + stride, xn);
         Acc s = 0;
 #pragma unroll
         for (int k = 0; k < VPT; ++k)
@@ -118,7 +139,7 @@ __global__ void __launch_bounds__(LnFwdCfg<T, GW, VPT>::kThreads) ln_fwd_kernel(
             for (int e = 0; e < W; ++e) {
                 const int64_t col = c0 + e;
                 xo[e] = (xv[k][e] - mu) * inv;
-                yo[e] = col < D ? gam[col] * xo[e] + bet[col] : Acc(0);
+                yo[e] = col < D ? gs[col] * xo[e] + bs[col] : Acc(0);
             }
             if (a.aligned) {
                 if (yg) st_stream(yg + row * D + c0, pack<T>(yo));
@@ -131,6 +152,205 @@ __global__ void __launch_bounds__(LnFwdCfg<T, GW, VPT>::kThreads) ln_fwd_kernel(
                         if (xhg) xhg[row * D + c0 + e] = from_acc<T>(xo[e]);
                     }
             }
+        }
+#pragma unroll
+        for (int k = 0; k < VPT; ++k)
+#pragma unroll
+            for (int e = 0; e < W; ++e) xv[k][e] = xn[k][e];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// TMA-ring variant (16-byte-aligned rows): the forward is a pure stream, so the
+// bytes in flight per SM decide its speed.  A producer warp keeps S stages of R
+// consecutive rows in flight with 1-D cp.async.bulk (L2 evict-first) on
+// mbarriers; G row groups of GW warps consume one row of each stage
+// (registers: the thread's VPT vectors of that row), do the two reductions
+// (warp butterfly + cross-warp through shared memory) and stream y (and
+// mean/rstd, x-hat) out.  CTA c owns rows [c*N/grid, (c+1)*N/grid).
+template <typename T, int GW, int VPT, int G>
+struct LnFwdRingCfg {
+    static constexpr int kWarps = GW * G;
+    static constexpr int kThreads = (kWarps + 1) * 32;  // + producer warp
+    static constexpr int R = G;                          // rows per stage
+    static __host__ __device__ constexpr size_t bars_bytes(int S) { return (size_t)16 * S; }
+    static __host__ __device__ constexpr size_t red_off(int S) { return (bars_bytes(S) + 15) / 16 * 16; }
+    static __host__ __device__ constexpr size_t gam_off(int S) {
+        return red_off(S) + (size_t)2 * G * GW * sizeof(typename Traits<T>::Acc) * 2;
+    }
+    static __host__ __device__ constexpr size_t ring_off(int S, int64_t Dp) {
+        return (gam_off(S) + (size_t)2 * Dp * sizeof(typename Traits<T>::Acc) + 127) / 128 * 128;
+    }
+    // ring rows are packed at stride D (one bulk copy per stage)
+    static __host__ __device__ constexpr size_t smem_bytes(int S, int64_t Dp, int64_t D) {
+        return ring_off(S, Dp) + (size_t)S * R * D * sizeof(T);
+    }
+};
+
+template <typename T, int GW, int VPT, int G>
+__global__ void __launch_bounds__(LnFwdRingCfg<T, GW, VPT, G>::kThreads, 1) ln_fwd_ring_kernel(LnFwdArgs a, int S) {
+    using C = LnFwdRingCfg<T, GW, VPT, G>;
+    using Acc = typename Traits<T>::Acc;
+    constexpr int W = Traits<T>::W;
+    constexpr int GT = GW * 32;
+    constexpr int R = C::R;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* empty = full + S;
+    Acc* red = reinterpret_cast<Acc*>(smem + C::red_off(S));  // [2 buffers][2 sums][G][GW]
+    Acc* gs = reinterpret_cast<Acc*>(smem + C::gam_off(S));
+    const int64_t Dp = a.Dp;
+    Acc* bs = gs + Dp;
+    T* ring = reinterpret_cast<T*>(smem + C::ring_off(S, Dp));
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int grid = gridDim.x, cta = blockIdx.x;
+    const int64_t N = a.N, D = a.D;
+    const int64_t r_begin = (int64_t)cta * N / grid, r_end = (int64_t)(cta + 1) * N / grid;
+    const int64_t n_stage = (r_end - r_begin + R - 1) / R;
+    const T* xg = static_cast<const T*>(a.x);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], C::kWarps);
+        }
+        fence_mbar_init();
+    }
+    {
+        const Acc* gam = static_cast<const Acc*>(a.gamma);
+        const Acc* bet = static_cast<const Acc*>(a.beta);
+        for (int64_t c = threadIdx.x; c < Dp; c += blockDim.x) {
+            gs[c] = c < D ? gam[c] : Acc(0);
+            bs[c] = c < D ? bet[c] : Acc(0);
+        }
+    }
+    __syncthreads();
+
+    if (warp == C::kWarps) {  // ---- producer
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            for (int64_t st = 0; st < n_stage; ++st) {
+                const int slot = (int)(st % S);
+                if (st >= S) mbar_wait(&empty[slot], (uint32_t)(((st / S) - 1) & 1));
+                const int64_t r0 = r_begin + st * R;
+                const int nr = (int)((r_end - r0) < (int64_t)R ? (r_end - r0) : (int64_t)R);
+                const uint32_t bytes = (uint32_t)(nr * D * (int64_t)sizeof(T));
+                mbar_expect_tx(&full[slot], bytes);
+                bulk_g2s(ring + (size_t)slot * R * D, xg + r0 * D, bytes, &full[slot], pol);
+                mbar_arrive(&full[slot]);
+            }
+        }
+        return;
+    }
+
+    // ---- consumers: group g takes row g of every stage
+    const int g = warp / GW, wig = warp % GW, tig = wig * 32 + lane;
+    T* yg = static_cast<T*>(a.y);
+    T* xhg = static_cast<T*>(a.xhat);
+    Acc* meang = static_cast<Acc*>(a.mean);
+    Acc* rstdg = static_cast<Acc*>(a.rstd);
+    const Acc invD = Acc(1) / Acc(D);
+    const Acc eps = (Acc)a.eps;
+    // both row sums in one round: warp butterflies, then one named barrier
+    auto group_sum2 = [&](Acc& v1, Acc& v2, int buf) {
+        Acc vv[2] = {v1, v2};
+        warp_sum_n(vv);
+        if constexpr (GW == 1) {
+            v1 = vv[0];
+            v2 = vv[1];
+        } else {
+            Acc* rb = red + ((size_t)(buf * 2) * G + g) * GW;
+            Acc* rb2 = red + ((size_t)(buf * 2 + 1) * G + g) * GW;
+            if (lane == 0) {
+                rb[wig] = vv[0];
+                rb2[wig] = vv[1];
+            }
+            named_bar_sync(1 + g, GT);
+            Acc t1 = 0, t2 = 0;
+#pragma unroll
+            for (int w = 0; w < GW; ++w) {
+                t1 += rb[w];
+                t2 += rb2[w];
+            }
+            v1 = t1;
+            v2 = t2;
+        }
+    };
+    // the thread's gamma/beta columns, in registers for the whole kernel
+    Acc gv[VPT][W], bv[VPT][W];
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+        const int64_t c0 = (int64_t)(tig + k * GT) * W;
+#pragma unroll
+        for (int e = 0; e < W; ++e) {
+            gv[k][e] = c0 + e < Dp ? gs[c0 + e] : Acc(0);
+            bv[k][e] = c0 + e < Dp ? bs[c0 + e] : Acc(0);
+        }
+    }
+    int slot = 0;
+    uint32_t ph = 0;
+    for (int64_t st = 0; st < n_stage; ++st) {
+        mbar_wait(&full[slot], ph);
+        const int64_t row = r_begin + st * R + g;
+        const bool valid = row < r_end;
+        Acc xv[VPT][W];
+        const T* sx = ring + ((size_t)slot * R + g) * D;
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+            const int64_t c0 = (int64_t)(tig + k * GT) * W;
+            if (valid && c0 < D) {
+                unpack<T>(*reinterpret_cast<const uint4*>(sx + c0), xv[k]);
+            } else {
+#pragma unroll
+                for (int e = 0; e < W; ++e) xv[k][e] = Acc(0);
+            }
+        }
+        // one-pass moments about a shift K = the row's first element (the
+        // same value for every thread of the group): sum (x-K), sum (x-K)^2;
+        // shifting keeps the cancellation of var = E[d^2] - E[d]^2 small
+        const Acc K = valid ? to_acc<T>(sx[0]) : Acc(0);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);  // the row is in registers
+        const int buf = (int)(st & 1);
+        Acc s1 = 0, s2 = 0;
+#pragma unroll
+        for (int k = 0; k < VPT; ++k)
+#pragma unroll
+            for (int e = 0; e < W; ++e) {
+                const int64_t col = (int64_t)(tig + k * GT) * W + e;
+                const Acc d = col < D ? xv[k][e] - K : Acc(0);
+                s1 += d;
+                s2 = fma(d, d, s2);
+            }
+        group_sum2(s1, s2, buf);
+        const Acc m1 = s1 * invD;
+        const Acc mu = K + m1;
+        Acc var = s2 * invD - m1 * m1;
+        var = var > Acc(0) ? var : Acc(0);
+        const Acc inv = Acc(1) / sqrt(var + eps);
+        if (valid) {
+            if (tig == 0) {
+                if (meang) meang[row] = mu;
+                if (rstdg) rstdg[row] = inv;
+            }
+#pragma unroll
+            for (int k = 0; k < VPT; ++k) {
+                const int64_t c0 = (int64_t)(tig + k * GT) * W;
+                if (c0 >= D) continue;
+                Acc yo[W], xo[W];
+#pragma unroll
+                for (int e = 0; e < W; ++e) {
+                    xo[e] = (xv[k][e] - mu) * inv;
+                    yo[e] = gv[k][e] * xo[e] + bv[k][e];
+                }
+                if (yg) st_stream(yg + row * D + c0, pack<T>(yo));
+                if (xhg) st_stream(xhg + row * D + c0, pack<T>(xo));
+            }
+        }
+        if (++slot == S) {
+            slot = 0;
+            ph ^= 1u;
         }
     }
 }

@@ -229,11 +229,53 @@ struct FwdOp {
         a.aligned = ((c.D * (int64_t)sizeof(T)) % 16 == 0) && ptr16(c.x) && (c.y == nullptr || ptr16(c.y)) &&
                     (c.xhat == nullptr || ptr16(c.xhat));
         const int sms = device_sm_count();
+        if (a.aligned && c.D % Traits<T>::W == 0) {
+            // TMA ring: G groups so that the CTA has ~16 consumer warps
+            constexpr int GR = GW >= 16 ? 1 : (16 / GW > 15 ? 15 : 16 / GW);
+            using RC = LnFwdRingCfg<T, GW, VPT, GR>;
+            a.Dp = (int64_t)GW * 32 * VPT * Traits<T>::W;
+            if (a.Dp < c.D) a.Dp = c.D;
+            const size_t budget = (size_t)smem_optin_bytes() - 1024;
+            int S = 0;
+            for (int s2 = 32; s2 >= 2; --s2)  // as many stages as fit: bytes in flight set the speed
+                if (RC::smem_bytes(s2, a.Dp, c.D) <= budget) {
+                    S = s2;
+                    break;
+                }
+            if (S > 0) {
+                const size_t smem = RC::smem_bytes(S, a.Dp, c.D);
+                auto k = ln_fwd_ring_kernel<T, GW, VPT, GR>;
+                cudaError_t se = ensure_smem(reinterpret_cast<const void*>(k), smem);
+                if (se != cudaSuccess) {
+                    *cerr = se;
+                    *why = "ln_fwd smem attribute";
+                    return 2;
+                }
+                const int grid = (int)(c.N < sms ? c.N : sms);
+                k<<<grid, RC::kThreads, smem, st>>>(a, S);
+                cudaError_t e = cudaGetLastError();
+                if (e != cudaSuccess) {
+                    *cerr = e;
+                    *why = "ln_fwd launch";
+                    return 2;
+                }
+                return 0;
+            }
+        }
         int64_t blocks = (c.N + F::G - 1) / F::G;
         const int64_t cap = (int64_t)sms * (2048 / F::kThreads);
         if (blocks > cap) blocks = cap;
         if (blocks < 1) blocks = 1;
-        ln_fwd_kernel<T, GW, VPT><<<(int)blocks, F::kThreads, 0, st>>>(a);
+        a.Dp = (int64_t)GW * 32 * VPT * Traits<T>::W;
+        if (a.Dp < c.D) a.Dp = c.D;
+        const size_t smem = (size_t)2 * a.Dp * sizeof(typename Traits<T>::Acc);
+        cudaError_t se = ensure_smem(reinterpret_cast<const void*>(ln_fwd_kernel<T, GW, VPT>), smem);
+        if (se != cudaSuccess) {
+            *cerr = se;
+            *why = "ln_fwd smem attribute";
+            return 2;
+        }
+        ln_fwd_kernel<T, GW, VPT><<<(int)blocks, F::kThreads, smem, st>>>(a);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) {
             *cerr = e;
