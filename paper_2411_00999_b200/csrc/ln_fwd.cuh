@@ -277,15 +277,22 @@ __global__ void __launch_bounds__(LnFwdRingCfg<T, GW, VPT, G>::kThreads, 1) ln_f
             v2 = t2;
         }
     };
-    // the thread's gamma/beta columns, in registers for the whole kernel
-    Acc gv[VPT][W], bv[VPT][W];
+    // the thread's gamma/beta columns, in registers for the whole kernel;
+    // packed fp32x2 (FFMA2/FADD2) math on pairs of columns.  Rows are whole
+    // 16-byte vectors here (D % W == 0), so a vector is either all in or all out.
+    using PR = Pair<Acc>;
+    using P = typename PR::P;
+    constexpr int NP = W / 2;
+    P gv[VPT][NP], bv[VPT][NP];
+    bool vin[VPT];
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
         const int64_t c0 = (int64_t)(tig + k * GT) * W;
+        vin[k] = c0 < D;
 #pragma unroll
-        for (int e = 0; e < W; ++e) {
-            gv[k][e] = c0 + e < Dp ? gs[c0 + e] : Acc(0);
-            bv[k][e] = c0 + e < Dp ? bs[c0 + e] : Acc(0);
+        for (int p = 0; p < NP; ++p) {
+            gv[k][p] = vin[k] ? PR::make(gs[c0 + 2 * p], gs[c0 + 2 * p + 1]) : PR::splat(Acc(0));
+            bv[k][p] = vin[k] ? PR::make(bs[c0 + 2 * p], bs[c0 + 2 * p + 1]) : PR::splat(Acc(0));
         }
     }
     int slot = 0;
@@ -294,16 +301,15 @@ __global__ void __launch_bounds__(LnFwdRingCfg<T, GW, VPT, G>::kThreads, 1) ln_f
         mbar_wait(&full[slot], ph);
         const int64_t row = r_begin + st * R + g;
         const bool valid = row < r_end;
-        Acc xv[VPT][W];
+        P xv[VPT][NP];
         const T* sx = ring + ((size_t)slot * R + g) * D;
 #pragma unroll
         for (int k = 0; k < VPT; ++k) {
-            const int64_t c0 = (int64_t)(tig + k * GT) * W;
-            if (valid && c0 < D) {
-                unpack<T>(*reinterpret_cast<const uint4*>(sx + c0), xv[k]);
+            if (valid && vin[k]) {
+                unpack2<T>(*reinterpret_cast<const uint4*>(sx + (int64_t)(tig + k * GT) * W), xv[k]);
             } else {
 #pragma unroll
-                for (int e = 0; e < W; ++e) xv[k][e] = Acc(0);
+                for (int p = 0; p < NP; ++p) xv[k][p] = PR::splat(Acc(0));
             }
         }
         // one-pass moments about a shift K = the row's first element (the
@@ -313,16 +319,19 @@ __global__ void __launch_bounds__(LnFwdRingCfg<T, GW, VPT, G>::kThreads, 1) ln_f
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);  // the row is in registers
         const int buf = (int)(st & 1);
-        Acc s1 = 0, s2 = 0;
+        const P nK = PR::splat(-K);
+        P s1p = PR::splat(Acc(0)), s2p = PR::splat(Acc(0));
 #pragma unroll
-        for (int k = 0; k < VPT; ++k)
+        for (int k = 0; k < VPT; ++k) {
+            if (!vin[k]) continue;
 #pragma unroll
-            for (int e = 0; e < W; ++e) {
-                const int64_t col = (int64_t)(tig + k * GT) * W + e;
-                const Acc d = col < D ? xv[k][e] - K : Acc(0);
-                s1 += d;
-                s2 = fma(d, d, s2);
+            for (int p = 0; p < NP; ++p) {
+                const P d = PR::add(xv[k][p], nK);
+                s1p = PR::add(s1p, d);
+                s2p = PR::fma(d, d, s2p);
             }
+        }
+        Acc s1 = s1p.x + s1p.y, s2 = s2p.x + s2p.y;
         group_sum2(s1, s2, buf);
         const Acc m1 = s1 * invD;
         const Acc mu = K + m1;
@@ -334,18 +343,19 @@ __global__ void __launch_bounds__(LnFwdRingCfg<T, GW, VPT, G>::kThreads, 1) ln_f
                 if (meang) meang[row] = mu;
                 if (rstdg) rstdg[row] = inv;
             }
+            const P inv2 = PR::splat(inv), nmi2 = PR::splat(-mu * inv);
 #pragma unroll
             for (int k = 0; k < VPT; ++k) {
+                if (!vin[k]) continue;
                 const int64_t c0 = (int64_t)(tig + k * GT) * W;
-                if (c0 >= D) continue;
-                Acc yo[W], xo[W];
+                P yo[NP], xo[NP];
 #pragma unroll
-                for (int e = 0; e < W; ++e) {
-                    xo[e] = (xv[k][e] - mu) * inv;
-                    yo[e] = gv[k][e] * xo[e] + bv[k][e];
+                for (int p = 0; p < NP; ++p) {
+                    xo[p] = PR::fma(xv[k][p], inv2, nmi2);
+                    yo[p] = PR::fma(gv[k][p], xo[p], bv[k][p]);
                 }
-                if (yg) st_stream(yg + row * D + c0, pack<T>(yo));
-                if (xhg) st_stream(xhg + row * D + c0, pack<T>(xo));
+                if (yg) st_stream(yg + row * D + c0, pack2<T>(yo));
+                if (xhg) st_stream(xhg + row * D + c0, pack2<T>(xo));
             }
         }
         if (++slot == S) {
