@@ -51,9 +51,16 @@ using bf = __nv_bfloat16;
     X(39, 8, 1, 1, 2, true, 1, 2) \
     X(40, 4, 2, 1, 2, true, 1, 2) \
     X(41, 1, 3, 4, 2, true, 1, 2) \
+    X(42, 11, 3, 1, 1, true, 1) \
+    X(43, 12, 3, 1, 1, true, 1) \
+    X(44, 11, 3, 1, 1, true, 0) \
+    X(45, 6, 3, 1, 1, true, 1) \
+    X(46, 6, 3, 1, 2, true, 1) \
+    X(47, 5, 4, 1, 1, true, 1) \
+    X(48, 3, 3, 3, 1, true, 1) \
 
 extern "C" {
-int sweep_n() { return 42; }
+int sweep_n() { return 49; }
 
 int sweep_desc(int id, int* out) {
 #define DESC(i, gw, vpt, g, rpg, prod, keep, ...) \

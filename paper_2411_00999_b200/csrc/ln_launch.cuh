@@ -299,7 +299,9 @@ R dispatch_bwd(int64_t D, const char** why, R bad, A&&... args) {
     if (nv <= 128) return Op<LnBwdCfg<T, 4, 1, 4, 2, true>>::call(args...);
     if (nv <= 256) return Op<LnBwdCfg<T, 8, 1, 2, 2, true>>::call(args...);
     if (nv <= 512) return Op<LnBwdCfg<T, 8, 2, 1, 2, true, 1>>::call(args...);
-    if (nv <= 1024) return Op<LnBwdCfg<T, 16, 2, 1, 1, true, 1>>::call(args...);
+    // 11 consumer warps x 3 vectors (3 % of the lanes idle at D=8192): 12 warps leave
+    // ~168 registers per thread, no spills (16 x 2 forced 96 and spilled)
+    if (nv <= 1024) return Op<LnBwdCfg<T, 11, 3, 1, 1, true, 1>>::call(args...);
     if (nv <= 2048) return Op<LnBwdCfg<T, 16, 4, 1, 1, false>>::call(args...);
     *why = "layers: trailing extent exceeds the kernel limit (2048 16-byte vectors per row)";
     return bad;
