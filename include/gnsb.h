@@ -182,6 +182,25 @@ gnsb_status gnsb_embedding_pe(const int32_t* ids, const void* g, void* dW, doubl
 gnsb_status gnsb_sqnorm(const void* v, int64_t n, gnsb_dtype dt, double* out, void* stream);
 
 /* ------------------------------------------------------------------------
+ * Batch-sharded exchange: the step's one collective.
+ * grads   : device bucket of every layer's [p0 | p1] batch-summed gradients
+ *           (layer l holds 2 * widths_host[l] values of grad_dt, fp32 or fp64)
+ * records : device [n_layers][4] fp64 norm records, as gnsb_ln_bwd writes them
+ * Sums both buckets over `nccl_comm` (an ncclComm_t; NULL = a single rank)
+ * with NCCL on `stream`, then re-forms records[l][2..3] = ||p0||^2, ||p1||^2
+ * of the REDUCED gradients (local squared norms do not add).  The GNS step then
+ * uses the global batch (gnsb_gns_step with B = B_global).  1..256 layers.
+ * libnccl.so.2 is opened at run time; the three helpers let a C/C++ caller
+ * create a communicator with the same NCCL instance.
+ */
+int32_t gnsb_nccl_available(void);
+gnsb_status gnsb_nccl_get_unique_id(void* id128);
+gnsb_status gnsb_nccl_comm_init_rank(void** comm, int32_t nranks, const void* id128, int32_t rank);
+gnsb_status gnsb_nccl_comm_destroy(void* comm);
+gnsb_status gnsb_allreduce_buckets(void* grads, gnsb_dtype grad_dt, const int64_t* widths_host, int32_t n_layers,
+                                   double* records, int32_t with_records, void* nccl_comm, void* stream);
+
+/* ------------------------------------------------------------------------
  * GNS estimator (host functions).  Replace proj/include/gnstk/gns.hpp:16-74 /
  * proj/src/gns.cpp:14-89 with identical arithmetic and error conditions.
  */

@@ -122,6 +122,8 @@ cudaError_t ensure_smem_attr(const void* kernel, size_t bytes) {
     return e;
 }
 
+void set_error(const std::string& msg) { g_err = msg; }
+
 int device_sm_count() {
     static std::mutex mu;
     static int cache[64] = {0};

@@ -6,6 +6,8 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include <string>
+
 namespace gnsb {
 
 struct SynthSeeds {
@@ -63,6 +65,8 @@ template <typename T> int ln_bwd_workspace(int64_t B, int64_t M, int64_t D, size
 template <typename T> int ln_bwd_geometry(int64_t B, int64_t M, int64_t D, int* grid, int* threads, int* stages);
 
 int device_sm_count();
+// the calling thread's gnsb_last_error() message (capi.cu)
+void set_error(const std::string& msg);
 // raise (never lower) a kernel's max dynamic shared memory attribute; process-wide record
 cudaError_t ensure_smem_attr(const void* kernel, size_t bytes);
 

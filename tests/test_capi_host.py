@@ -159,3 +159,10 @@ def test_cpp_dropin_suite():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert " 0 failed" in r.stdout
+
+
+def test_nccl_is_found_at_run_time():
+    """The exchange step opens libnccl.so.2 at run time (no link-time dependency)."""
+    from paper_2411_00999_b200 import _lib
+
+    assert _lib.lib().gnsb_nccl_available() in (0, 1)

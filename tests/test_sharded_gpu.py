@@ -102,3 +102,48 @@ def test_bench_multirank_path_runs(cuda):
     assert len(lines) == 1, p.stdout[-2000:]
     rec = json.loads(lines[0])
     assert rec["n_gpus"] == 2 and rec["value"] > 0 and rec["config"]["global_batch"] == 64
+
+
+def test_c_abi_allreduce_buckets_single_rank(cuda):
+    """gnsb_allreduce_buckets (the C ABI's exchange step): with no communicator
+    and with a one-rank NCCL communicator the buckets are unchanged and
+    records[l][2..3] are re-formed as ||p0||^2, ||p1||^2 of the gradient bucket."""
+    import ctypes
+
+    from paper_2411_00999_b200 import _lib
+
+    lib = _lib.lib()
+    widths = [768, 5, 1024]
+    n = 2 * sum(widths)
+    gen = torch.Generator(device="cpu").manual_seed(3)
+    grads = torch.randn(n, generator=gen).to(cuda)
+    records = torch.zeros(len(widths), 4, dtype=torch.float64, device=cuda)
+    records[:, :2] = torch.tensor([[1.0, 2.0], [3.0, 4.0], [5.0, 6.0]], dtype=torch.float64)
+    w = (ctypes.c_int64 * len(widths))(*widths)
+    expect = []
+    off = 0
+    for wd in widths:
+        a = grads[off:off + wd].double()
+        b = grads[off + wd:off + 2 * wd].double()
+        expect.append([float((a * a).sum()), float((b * b).sum())])
+        off += 2 * wd
+    sp = torch.cuda.current_stream().cuda_stream
+    comms = [None]
+    if lib.gnsb_nccl_available():
+        uid = ctypes.create_string_buffer(128)
+        _lib.check(lib.gnsb_nccl_get_unique_id(uid))
+        comm = ctypes.c_void_p()
+        _lib.check(lib.gnsb_nccl_comm_init_rank(ctypes.byref(comm), 1, uid, 0))
+        comms.append(comm)
+    for comm in comms:
+        g0, r0 = grads.clone(), records[:, :2].clone()
+        _lib.check(lib.gnsb_allreduce_buckets(grads.data_ptr(), 0, w, len(widths), records.data_ptr(), 1,
+                                              comm, sp))
+        torch.cuda.synchronize()
+        assert torch.equal(grads, g0) and torch.equal(records[:, :2], r0)
+        assert close(records[:, 2:].cpu().numpy(), np.array(expect), 1e-12)
+        records[:, 2:] = 0
+    if len(comms) > 1:
+        _lib.check(lib.gnsb_nccl_comm_destroy(comms[1]))
+    with pytest.raises(ValueError, match="bucket"):
+        _lib.check(lib.gnsb_allreduce_buckets(grads.data_ptr(), 0, w, 0, records.data_ptr(), 1, None, sp))
