@@ -356,3 +356,48 @@ def test_deferred_grouped_reduce_matches_per_layer(cuda):
     for r, o in zip(ref[:2], out2):
         assert torch.equal(r.grads.weight_grads["gamma"], o.weight_grads["gamma"])
         assert o.per_example_sqnorms == {}
+
+
+@pytest.mark.parametrize("dt,B,T,D", [(torch.bfloat16, 2048, 4, 768), (torch.float32, 1100, 3, 96)])
+def test_many_examples_blocked_stage2(orc, cuda, dt, B, T, D):
+    """B beyond one shared-memory block of the reduce (512 examples) and beyond
+    the final fold's on-chip buffer: still the oracle's norms."""
+    m = _mod()
+    x, dy, gamma, beta = m.synth_ln(B, T, D, dt, cuda, stream0=9)
+    layer = m.LayerNormLayer(gamma, beta)
+    f = m.layernorm_forward(layer, x)
+    r = m.layernorm_backward_simultaneous(layer, f.cache, dy)
+    ref = _oracle_on_device_stats(orc, x, dy, gamma, f.cache.mean, f.cache.inv_std)
+    torch.cuda.synchronize()
+    assert close(r.grads.per_example_sqnorms_raw["gamma"].cpu().numpy(), ref["raw_gamma"], NORM_TOL)
+    assert close(r.grads.per_example_sqnorms_raw["beta"].cpu().numpy(), ref["raw_beta"], NORM_TOL)
+    assert close(float(r.grads.per_example_sqnorms["gamma"]), ref["corrected"][0], NORM_TOL)
+    gt = F32_TOL if dt == torch.float32 else NORM_TOL
+    assert _close_inf(r.grads.weight_grads["gamma"].double().cpu().numpy(), ref["dgamma"], gt)
+
+
+def test_deferred_reduce_limits(cuda):
+    """64 pending LayerNorms in one launch; more, or mixed fp32/fp64
+    statistics, are rejected with the reference-style error."""
+    m = _mod()
+    from paper_2411_00999_b200 import layers
+
+    pend = []
+    for i in range(64):
+        x, dy, gamma, beta = m.synth_ln(2, 3, 32, torch.bfloat16, cuda, stream0=100 + i)
+        layer = m.LayerNormLayer(gamma, beta)
+        f = m.layernorm_forward(layer, x)
+        pend.append(layers.layernorm_backward_rows(layer, f.cache, dy)[1])
+        if i == 63:
+            ref = m.layernorm_backward_simultaneous(layer, f.cache, dy)
+    out = layers.layernorm_backward_reduce(pend)
+    torch.cuda.synchronize()
+    assert torch.equal(out[-1].weight_grads["gamma"], ref.grads.weight_grads["gamma"])
+    assert close(out[-1].sums4.cpu().numpy(), ref.grads.sums4.cpu().numpy(), 1e-12)
+    with pytest.raises(ValueError, match="too many pending"):
+        layers.layernorm_backward_reduce(pend + pend[:1])
+    x, dy, gamma, beta = m.synth_ln(2, 3, 8, torch.float64, cuda)
+    f = m.layernorm_forward(m.LayerNormLayer(gamma, beta), x)
+    p64 = layers.layernorm_backward_rows(m.LayerNormLayer(gamma, beta), f.cache, dy)[1]
+    with pytest.raises(ValueError, match="mix fp64 and fp32"):
+        layers.layernorm_backward_reduce([pend[0], p64])
