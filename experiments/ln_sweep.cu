@@ -58,9 +58,26 @@ using bf = __nv_bfloat16;
     X(46, 6, 3, 1, 2, true, 1) \
     X(47, 5, 4, 1, 1, true, 1) \
     X(48, 3, 3, 3, 1, true, 1) \
+    X(49, 4, 2, 2, 2, true, 1) \
+    X(50, 8, 1, 1, 4, true, 1) \
+    X(51, 4, 2, 1, 4, true, 1) \
+    X(52, 4, 1, 2, 4, true, 1) \
+    X(53, 2, 2, 4, 2, true, 1) \
+    X(54, 2, 2, 2, 4, true, 1) \
+    X(55, 3, 1, 3, 4, true, 1) \
+    X(56, 3, 1, 2, 4, true, 1) \
+    X(57, 4, 1, 1, 8, true, 1) \
+    X(58, 1, 4, 8, 2, true, 1) \
+    X(59, 1, 4, 16, 1, true, 1) \
+    X(60, 1, 3, 16, 1, true, 1) \
+    X(61, 1, 3, 8, 2, true, 1) \
+    X(62, 2, 2, 8, 1, true, 1) \
+    X(63, 2, 4, 8, 1, true, 1) \
+    X(64, 2, 4, 4, 2, true, 1) \
+    X(65, 1, 4, 12, 1, true, 1) \
 
 extern "C" {
-int sweep_n() { return 49; }
+int sweep_n() { return 66; }
 
 int sweep_desc(int id, int* out) {
 #define DESC(i, gw, vpt, g, rpg, prod, keep, ...) \

@@ -33,7 +33,7 @@ struct LnBwdCall {
     int64_t B, M, D;
     void* ws; size_t ws_bytes;
     unsigned long long* trace = nullptr;   // profiling only: row kernel [grid][6] phase stamps
-    unsigned long long* trace2 = nullptr;  // profiling only: reduce kernel [grid][3] phase stamps
+    unsigned long long* trace2 = nullptr;  // profiling only: reduce kernel [grid][6] phase stamps
 };
 
 // Where a row pass left its partial slots and how the reduce must read them.

@@ -3,8 +3,6 @@
 // template instantiations compile in parallel.
 #pragma once
 
-#include <cstdio>
-#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <utility>
