@@ -31,6 +31,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -235,6 +236,209 @@ __global__ void __launch_bounds__(gr::THREADS, 1)
     }
 }
 
+// ------------------------------------------------- CTA-pair (2SM) variant --
+// Units (example b, 256-token row block I, 256-token column block J >= I) on a
+// CTA pair: cta_group::2 MMAs of M=256 (each CTA holds 128 rows of A) and
+// N=256 (each CTA holds 128 rows of B), so per 64-feature stage a CTA loads
+// 32 KB for 4.2 MFLOP of its half of the tile — a third less operand traffic
+// than the single-CTA 128x256 block.  The leader CTA issues the MMAs; both
+// CTAs' TMA loads complete on the leader's full barrier; the MMA commit
+// multicasts to both CTAs' empty / accumulator-full barriers; both CTAs'
+// epilogue warps release the accumulators on the leader's barrier.
+namespace gr2 {
+constexpr int BH = 128;                      // rows of A (and of B) per CTA
+constexpr int BK = 64;
+constexpr int STAGES = 6;
+constexpr int A_BYTES = BH * BK * 2;         // 16 KB
+constexpr int B_BYTES = BH * BK * 2;         // 16 KB (this CTA's half of N = 256)
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int EPI_WARPS = 4;
+constexpr int THREADS = (2 + EPI_WARPS) * 32;
+constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 1024;
+constexpr int TMEM_COLS = 512;               // X-Gram [0, 256) + G-Gram [256, 512)
+}  // namespace gr2
+
+struct Gram2Args {
+    int B, T, K, L;
+    int nt;        // T / 128 (token tiles)
+    int nI;        // ceil(nt / 2) (256-token blocks)
+    int nunits;    // nI * (nI + 1) / 2 per example
+    double* q;     // [B][nunits][2] (one partial per CTA of the pair)
+};
+
+__device__ __forceinline__ void unit_IJ(int p, int nI, int& I, int& J) {
+    I = 0;
+    while (p >= nI - I) {
+        p -= nI - I;
+        ++I;
+    }
+    J = I + p;
+}
+
+__global__ void __launch_bounds__(gr2::THREADS, 1)
+    gram2_norms_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmg, Gram2Args a) {
+    using namespace gr2;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char* ring = smem;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)STAGES * STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+    double* red = reinterpret_cast<double*>(tmem_slot + 4);  // [EPI_WARPS]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = tc::cluster_ctarank();
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const int64_t units = (int64_t)a.B * a.nunits;
+    const int kbx = a.K / BK, kbg = a.L / BK;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            // the leader's arrive.expect_tx(both CTAs' bytes); the peer's TMA only
+            // completes bytes on it (a release-arrive from the peer would add a
+            // cluster-scope fence per stage to its producer)
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);  // the leader's multicast commit
+        }
+        mbar_init(tfull, 1);
+        mbar_init(tempty, 2 * EPI_WARPS);  // both CTAs' epilogue warps
+        fence_mbar_init();
+        tc::prefetch_tmap(&tmx);
+        tc::prefetch_tmap(&tmg);
+    }
+    if (warp == 1) tc::tmem_alloc_pair<TMEM_COLS>(tmem_slot);
+    tc::fence_before_sync();
+    tc::cluster_sync();
+    tc::fence_after_sync();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------------ TMA producer --
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            for (int64_t u = pair; u < units; u += npairs) {
+                const int b = (int)(u / a.nunits);
+                int I, J;
+                unit_IJ((int)(u - (int64_t)b * a.nunits), a.nI, I, J);
+                for (int op = 0; op < 2; ++op) {
+                    const CUtensorMap* m = op == 0 ? &tmx : &tmg;
+                    const int nkb = op == 0 ? kbx : kbg;
+                    for (int kb = 0; kb < nkb; ++kb) {
+                        mbar_wait(&empty[s], ph ^ 1u);
+                        unsigned char* st = ring + (size_t)s * STAGE_BYTES;
+                        const uint32_t leader_full = tc::mapa(smem_u32(&full[s]), 0);
+                        if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * STAGE_BYTES);
+                        tc::tma_load_3d_2sm(st, m, kb * BK, I * 2 * BH + (int)rank * BH, b, leader_full);
+                        tc::tma_load_3d_2sm(st + A_BYTES, m, kb * BK, J * 2 * BH + (int)rank * BH, b, leader_full);
+                        if (++s == STAGES) {
+                            s = 0;
+                            ph ^= 1u;
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------- MMA issuer (leader only) --
+        if (rank == 0 && lane == 0) {
+            constexpr uint32_t idesc = tc::idesc_bf16(2 * BH, 2 * BH, false, false);  // M=256, N=256, K-major
+            int s = 0;
+            uint32_t ph = 0, tph = 0;
+            for (int64_t u = pair; u < units; u += npairs) {
+                tc::mbar_wait_cluster(tempty, tph ^ 1u);  // both epilogues drained the accumulators
+                tc::fence_after_sync();
+                for (int op = 0; op < 2; ++op) {
+                    const uint32_t dcol = tmem + (uint32_t)(op * 2 * BH);
+                    const int nkb = op == 0 ? kbx : kbg;
+                    for (int kb = 0; kb < nkb; ++kb) {
+                        tc::mbar_wait_cluster(&full[s], ph);
+                        tc::fence_after_sync();
+                        const uint32_t abase = smem_u32(ring + (size_t)s * STAGE_BYTES);
+                        const uint32_t bbase = abase + A_BYTES;
+#pragma unroll
+                        for (int k = 0; k < BK / 16; ++k) {
+                            const uint64_t ad = tc::smem_desc_sw128(abase + k * 32, 16, 1024);
+                            const uint64_t bd = tc::smem_desc_sw128(bbase + k * 32, 16, 1024);
+                            tc::mma_bf16_pair(dcol, ad, bd, idesc, (kb | k) != 0);
+                        }
+                        tc::commit_pair(&empty[s], 0x3);
+                        if (++s == STAGES) {
+                            s = 0;
+                            ph ^= 1u;
+                        }
+                    }
+                }
+                tc::commit_pair(tfull, 0x3);
+                tph ^= 1u;
+            }
+        }
+    } else {
+        // ------------------------------------------------- epilogue (both CTAs) --
+        const int e = warp - 2;
+        const int quad = warp & 3;
+        const uint32_t leader_tempty = tc::mapa(smem_u32(tempty), 0);
+        uint32_t tph = 0;
+        for (int64_t u = pair; u < units; u += npairs) {
+            const int b = (int)(u / a.nunits);
+            const int p = (int)(u - (int64_t)b * a.nunits);
+            int I, J;
+            unit_IJ(p, a.nI, I, J);
+            tc::mbar_wait_cluster(tfull, tph);
+            tph ^= 1u;
+            tc::fence_after_sync();
+            const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16);
+            float w2[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                float acc = 0.f;
+#pragma unroll 1
+                for (int cc = 0; cc < BH / 32; ++cc) {
+                    uint32_t rx[32], rg[32];
+                    const uint32_t col = (uint32_t)(h * BH + cc * 32);
+                    tc::tmem_ld_32x32b_x32(base + col, rx);
+                    tc::tmem_ld_32x32b_x32(base + 2 * BH + col, rg);
+                    tc::tmem_ld_wait();
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) acc = fmaf(__uint_as_float(rx[k]), __uint_as_float(rg[k]), acc);
+                }
+                w2[h] = acc;
+            }
+            tc::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive_cluster(leader_tempty);
+            warp_sum_n(w2);
+            if (lane == 0) {
+                const int i = 2 * I + (int)rank;  // this CTA's 128-token row tile
+                double t = 0.0;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int j = 2 * J + h;
+                    const double wgt = j < i ? 0.0 : (j == i ? 1.0 : 2.0);
+                    t += wgt * (double)w2[h];
+                }
+                red[e] = t;
+            }
+            named_bar_sync(1, EPI_WARPS * 32);
+            if (e == 0 && lane == 0) {
+                double t = 0.0;
+#pragma unroll
+                for (int k = 0; k < EPI_WARPS; ++k) t += red[k];
+                a.q[((size_t)b * a.nunits + p) * 2 + rank] = t;
+            }
+            named_bar_sync(1, EPI_WARPS * 32);
+        }
+    }
+    tc::fence_before_sync();
+    tc::cluster_sync();
+    if (warp == 1) {
+        tc::fence_after_sync();
+        tc::tmem_dealloc_pair<TMEM_COLS>(tmem);
+    }
+}
+
 // ------------------------------------------------------------------ host --
 namespace {
 
@@ -277,15 +481,63 @@ int gram_units(int64_t T) {  // units per example: sum over row tiles i of (nJ -
 
 }  // namespace
 
+int gram2_units(int64_t T) {
+    const int64_t nt = T / gr::BM, nI = (nt + 1) / 2;
+    return (int)(nI * (nI + 1) / 2);
+}
+
+cudaError_t launch_gram2_norms(const void* x, const void* g, double* raw, double* sums, int64_t B, int64_t T,
+                               int64_t K, int64_t L, void* ws, cudaStream_t st) {
+    CUtensorMap mx, mg;
+    if (!make_map_rows(&mx, x, (int)B, (int)T, (int)K, gr2::BH) || !make_map_rows(&mg, g, (int)B, (int)T, (int)L, gr2::BH))
+        return cudaErrorInvalidValue;
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(gram2_norms_kernel), gr2::SMEM);
+    if (e != cudaSuccess) return e;
+    Gram2Args a{};
+    a.B = (int)B;
+    a.T = (int)T;
+    a.K = (int)K;
+    a.L = (int)L;
+    a.nt = (int)(T / gr::BM);
+    a.nI = (a.nt + 1) / 2;
+    a.nunits = gram2_units(T);
+    a.q = static_cast<double*>(ws);
+    const int64_t units = B * a.nunits;
+    const int sms = device_sm_count() / 2 * 2;
+    int grid = (int)(2 * units < sms ? 2 * units : sms);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(gr2::THREADS);
+    cfg.dynamicSmemBytes = gr2::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, gram2_norms_kernel, mx, mg, a);
+    if (e != cudaSuccess) return e;
+    return launch_fold_rows(a.q, (int)B, 2 * a.nunits, raw, sums, 0, st);
+}
+
 bool gram_shape_ok(int64_t B, int64_t T, int64_t K, int64_t L) {
     return B >= 1 && T >= gr::BM && T % gr::BM == 0 && K % gr::BK == 0 && L % gr::BK == 0 && K > 0 && L > 0 &&
            T < (1 << 20) && B < (1 << 20) && (int64_t)B * gram_units(T) < (1ll << 31);
 }
 
-size_t gram_workspace(int64_t B, int64_t T) { return (size_t)B * gram_units(T) * sizeof(double) + 256; }
+size_t gram_workspace(int64_t B, int64_t T) {
+    const int64_t u = gram_units(T) > 2 * gram2_units(T) ? gram_units(T) : 2 * gram2_units(T);
+    return (size_t)B * u * sizeof(double) + 256;
+}
 
 cudaError_t launch_gram_norms(const void* x, const void* g, double* raw, double* sums, int64_t B, int64_t T,
                               int64_t K, int64_t L, void* ws, cudaStream_t st) {
+    // the CTA-pair kernel by default (measured 2-3 % faster at cfg3);
+    // GNSB_GRAM_IMPL=1 selects the single-CTA 128x256 kernel
+    const char* impl = std::getenv("GNSB_GRAM_IMPL");
+    if (!(impl && impl[0] == '1')) return launch_gram2_norms(x, g, raw, sums, B, T, K, L, ws, st);
     CUtensorMap mxa, mxb, mga, mgb;
     if (!make_map_rows(&mxa, x, (int)B, (int)T, (int)K, gr::BM) || !make_map_rows(&mxb, x, (int)B, (int)T, (int)K, gr::BN) ||
         !make_map_rows(&mga, g, (int)B, (int)T, (int)L, gr::BM) || !make_map_rows(&mgb, g, (int)B, (int)T, (int)L, gr::BN))
