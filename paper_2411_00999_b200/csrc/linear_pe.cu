@@ -26,6 +26,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -57,28 +58,46 @@ struct WgradArgs {
     double* qbig;  // [tiles] ||dW tile||^2
 };
 
+// PAIR: a 2-CTA cluster computes a 256 x 256 tile of dW with
+// tcgen05.mma.cta_group::2 (M = 256 input features, 128 per CTA; N = 256 output
+// features, each CTA loading 128 of them): per token stage a CTA loads 32 KB
+// instead of 48 KB for the same MMA work.  Sub-tile (the CTA's 128 x 256
+// half) indices equal the single-CTA tile indices, so q / qbig / tickets /
+// split parts keep their layout.
+template <bool PAIR>
 __global__ void __launch_bounds__(wg::THREADS, 1)
     wgrad_norms_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmg, WgradArgs a) {
     using namespace wg;
+    constexpr int BNL = PAIR ? BN / 2 : BN;             // output features this CTA loads per stage
+    constexpr int LOAD_BYTES = A_BYTES + BNL * BK * 2;  // bytes this CTA's TMA brings per stage
+    constexpr int NST = PAIR ? 6 : STAGES;              // same ring bytes: 6 x 32 KB = 4 x 48 KB
+    static_assert(NST * LOAD_BYTES <= STAGES * STAGE_BYTES, "ring");
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     unsigned char* ring = smem;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)STAGES * STAGE_BYTES);
-    uint64_t* empty = full + STAGES;
-    uint64_t* tfull = empty + STAGES;   // [2]
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NST * LOAD_BYTES);
+    uint64_t* empty = full + NST;
+    uint64_t* tfull = empty + NST;      // [2]
     uint64_t* tempty = tfull + 2;       // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     float* red = reinterpret_cast<float*>(tmem_slot + 4);  // [EPI_WARPS]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int ntiles = a.tiles_m * a.tiles_n;
+    const int ntiles = a.tiles_m * a.tiles_n;  // 128 x 256 sub-tiles (q / qbig / ticket indexing)
     const int kblocks = a.T / BK;
+    const uint32_t rank = PAIR ? tc::cluster_ctarank() : 0u;
+    // scheduled tiles: 256 x 256 pair tiles (PAIR) or 128 x 256 tiles
+    const int tiles_ms = PAIR ? a.tiles_m / 2 : a.tiles_m;
+    const int stiles = tiles_ms * a.tiles_n;
+    auto sub_of = [&](int tile) {  // this CTA's 128 x 256 sub-tile of a scheduled tile
+        return PAIR ? ((tile % tiles_ms) * 2 + (int)rank) + (tile / tiles_ms) * a.tiles_m : tile;
+    };
     // Schedule (identical in every role).  Full rounds: CTA c takes tile
     // r*grid + c with all examples, so at any moment every CTA works on the
     // same example and X_b, G_b are shared through L2.  The remaining
     // R = tiles % grid tiles are split into P = grid / R example ranges each.
-    const int grid = gridDim.x, c = blockIdx.x;
-    const int full_rounds = ntiles / grid, R = ntiles % grid;
+    const int grid = PAIR ? (int)gridDim.x / 2 : (int)gridDim.x, c = PAIR ? (int)blockIdx.x / 2 : (int)blockIdx.x;
+    const int full_rounds = stiles / grid, R = stiles % grid;
     const int P = R > 0 ? (grid / R < a.B ? grid / R : a.B) : 1;
     const int nseg = full_rounds + ((R > 0 && c < R * P) ? 1 : 0);
     auto segment = [&](int si, int& tile, int& b0, int& b1, int& nparts, int& part) {
@@ -98,21 +117,29 @@ __global__ void __launch_bounds__(wg::THREADS, 1)
     };
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) {
+        for (int s = 0; s < NST; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&tfull[s], 1);
-            mbar_init(&tempty[s], EPI_WARPS);
+            mbar_init(&tempty[s], PAIR ? 2 * EPI_WARPS : EPI_WARPS);  // (PAIR: both CTAs' epilogues)
         }
         fence_mbar_init();
         tc::prefetch_tmap(&tmx);
         tc::prefetch_tmap(&tmg);
     }
-    if (warp == 1) tc::tmem_alloc<TMEM_COLS>(tmem_slot);
+    if (warp == 1) {
+        if constexpr (PAIR)
+            tc::tmem_alloc_pair<TMEM_COLS>(tmem_slot);
+        else
+            tc::tmem_alloc<TMEM_COLS>(tmem_slot);
+    }
     tc::fence_before_sync();
-    __syncthreads();
+    if constexpr (PAIR)
+        tc::cluster_sync();
+    else
+        __syncthreads();
     tc::fence_after_sync();
     const uint32_t tmem = *tmem_slot;
 
@@ -124,19 +151,35 @@ __global__ void __launch_bounds__(wg::THREADS, 1)
             for (int si = 0; si < nseg; ++si) {
                 int tile, b0, b1, np_, pt;
                 segment(si, tile, b0, b1, np_, pt);
-                const int i0 = (tile % a.tiles_m) * BM, j0 = (tile / a.tiles_m) * BN;
+                const int sub = sub_of(tile);
+                const int i0 = (sub % a.tiles_m) * BM, j0 = (sub / a.tiles_m) * BN + (int)rank * BNL;
+                const uint32_t bar_leader = PAIR ? tc::mapa(smem_u32(&full[0]), 0) : 0u;
                 for (int b = b0; b < b1; ++b) {
                     for (int kb = 0; kb < kblocks; ++kb) {
                         mbar_wait(&empty[s], ph ^ 1u);
-                        unsigned char* st = ring + (size_t)s * STAGE_BYTES;
-                        mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+                        unsigned char* st = ring + (size_t)s * LOAD_BYTES;
                         const int t0 = kb * BK;
+                        if constexpr (PAIR) {
+                            // both CTAs' bytes complete on the leader's barrier; only the
+                            // leader arrives (expecting both halves)
+                            const uint32_t fb = bar_leader + (uint32_t)(s * 8);
+                            if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * LOAD_BYTES);
 #pragma unroll
-                        for (int h = 0; h < BM / 64; ++h) tc::tma_load_3d(st + h * 8192, &tmx, i0 + 64 * h, t0, b, &full[s]);
+                            for (int h = 0; h < BM / 64; ++h)
+                                tc::tma_load_3d_2sm(st + h * 8192, &tmx, i0 + 64 * h, t0, b, fb);
 #pragma unroll
-                        for (int h = 0; h < BN / 64; ++h)
-                            tc::tma_load_3d(st + A_BYTES + h * 8192, &tmg, j0 + 64 * h, t0, b, &full[s]);
-                        if (++s == STAGES) {
+                            for (int h = 0; h < BNL / 64; ++h)
+                                tc::tma_load_3d_2sm(st + A_BYTES + h * 8192, &tmg, j0 + 64 * h, t0, b, fb);
+                        } else {
+                            mbar_arrive_expect_tx(&full[s], LOAD_BYTES);
+#pragma unroll
+                            for (int h = 0; h < BM / 64; ++h)
+                                tc::tma_load_3d(st + h * 8192, &tmx, i0 + 64 * h, t0, b, &full[s]);
+#pragma unroll
+                            for (int h = 0; h < BNL / 64; ++h)
+                                tc::tma_load_3d(st + A_BYTES + h * 8192, &tmg, j0 + 64 * h, t0, b, &full[s]);
+                        }
+                        if (++s == NST) {
                             s = 0;
                             ph ^= 1u;
                         }
@@ -146,21 +189,27 @@ __global__ void __launch_bounds__(wg::THREADS, 1)
         }
     } else if (warp == 1) {
         // ------------------------------------------------------- MMA issuer --
-        if (lane == 0) {
-            constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, true, true);
+        if (lane == 0 && rank == 0) {
+            constexpr uint32_t idesc = tc::idesc_bf16(PAIR ? 2 * BM : BM, BN, true, true);
             int s = 0, buf = 0;
             uint32_t ph = 0, tph = 0;
             for (int si = 0; si < nseg; ++si) {
                 int tile, b0, b1, np_, pt;
                 segment(si, tile, b0, b1, np_, pt);
                 for (int b = b0; b < b1; ++b) {
-                    mbar_wait(&tempty[buf], tph ^ 1u);  // epilogue drained this accumulator
+                    if constexpr (PAIR)
+                        tc::mbar_wait_cluster(&tempty[buf], tph ^ 1u);  // both epilogues drained it
+                    else
+                        mbar_wait(&tempty[buf], tph ^ 1u);  // epilogue drained this accumulator
                     tc::fence_after_sync();
                     const uint32_t dcol = tmem + (uint32_t)(buf * BN);
                     for (int kb = 0; kb < kblocks; ++kb) {
-                        mbar_wait(&full[s], ph);
+                        if constexpr (PAIR)
+                            tc::mbar_wait_cluster(&full[s], ph);
+                        else
+                            mbar_wait(&full[s], ph);
                         tc::fence_after_sync();
-                        const uint32_t abase = smem_u32(ring + (size_t)s * STAGE_BYTES);
+                        const uint32_t abase = smem_u32(ring + (size_t)s * LOAD_BYTES);
                         const uint32_t bbase = abase + A_BYTES;
 #pragma unroll
                         for (int k = 0; k < BK / 16; ++k) {
@@ -168,15 +217,26 @@ __global__ void __launch_bounds__(wg::THREADS, 1)
                             // LBO = next 64 features (8 KB); a K step of 16 rows = 2 KB
                             const uint64_t ad = tc::smem_desc_sw128(abase + k * 2048, 8192, 1024);
                             const uint64_t bd = tc::smem_desc_sw128(bbase + k * 2048, 8192, 1024);
-                            tc::mma_bf16(dcol, ad, bd, idesc, (kb | k) != 0);
+                            if constexpr (PAIR)
+                                tc::mma_bf16_pair(dcol, ad, bd, idesc, (kb | k) != 0);
+                            else
+                                tc::mma_bf16(dcol, ad, bd, idesc, (kb | k) != 0);
                         }
-                        tc::commit(&empty[s]);  // smem slot free once these MMAs retire
-                        if (++s == STAGES) {
+                        // smem slot free once these MMAs retire (PAIR: in both CTAs)
+                        if constexpr (PAIR)
+                            tc::commit_pair(&empty[s], 0x3);
+                        else
+                            tc::commit(&empty[s]);
+                        if (++s == NST) {
                             s = 0;
                             ph ^= 1u;
                         }
                     }
-                    tc::commit(&tfull[buf]);  // accumulator of example b complete
+                    // accumulator of example b complete
+                    if constexpr (PAIR)
+                        tc::commit_pair(&tfull[buf], 0x3);
+                    else
+                        tc::commit(&tfull[buf]);
                     if (++buf == 2) {
                         buf = 0;
                         tph ^= 1u;
@@ -255,13 +315,18 @@ __global__ void __launch_bounds__(wg::THREADS, 1)
             if (e == 0 && lane == 0) a.ticket[tile] = 0u;
             store_tile(tile);
         };
+        const uint32_t tempty_leader = PAIR ? tc::mapa(smem_u32(&tempty[0]), 0) : 0u;
         for (int si = 0; si < nseg; ++si) {
-            int tile, b0, b1, nparts, mypart;
-            segment(si, tile, b0, b1, nparts, mypart);
+            int stile, b0, b1, nparts, mypart;
+            segment(si, stile, b0, b1, nparts, mypart);
+            const int tile = sub_of(stile);
 #pragma unroll
             for (int cc = 0; cc < 128; ++cc) S[cc] = 0.f;
             for (int b = b0; b < b1; ++b) {
-                mbar_wait(&tfull[buf], tph);
+                if constexpr (PAIR)
+                    tc::mbar_wait_cluster(&tfull[buf], tph);
+                else
+                    mbar_wait(&tfull[buf], tph);
                 tc::fence_after_sync();
                 float sq = 0.f;
                 const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN + half * 128);
@@ -279,8 +344,13 @@ __global__ void __launch_bounds__(wg::THREADS, 1)
                 }
                 tc::fence_before_sync();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&tempty[buf]);
-                fold8(sq, &a.q[(size_t)b * ntiles + tile]);  // the tile's share of raw_b
+                if (lane == 0) {
+                    if constexpr (PAIR)
+                        tc::mbar_arrive_cluster(tempty_leader + (uint32_t)(buf * 8));
+                    else
+                        mbar_arrive(&tempty[buf]);
+                }
+                fold8(sq, &a.q[(size_t)b * ntiles + tile]);  // the sub-tile's share of raw_b
                 if (++buf == 2) {
                     buf = 0;
                     tph ^= 1u;
@@ -289,10 +359,17 @@ __global__ void __launch_bounds__(wg::THREADS, 1)
             flush_tile(tile, nparts, mypart);
         }
     }
-    __syncthreads();
+    tc::fence_before_sync();
+    if constexpr (PAIR)
+        tc::cluster_sync();
+    else
+        __syncthreads();
     if (warp == 1) {
         tc::fence_after_sync();
-        tc::tmem_dealloc<TMEM_COLS>(tmem);
+        if constexpr (PAIR)
+            tc::tmem_dealloc_pair<TMEM_COLS>(tmem);
+        else
+            tc::tmem_dealloc<TMEM_COLS>(tmem);
     }
 }
 
@@ -377,38 +454,64 @@ int wgrad_max_parts(int64_t B, int64_t tiles, int grid) {
     const int64_t P = grid / R;
     return (int)(P < B ? P : B);
 }
+// the CTA-pair kernel (256 x 256 tiles over a 2-CTA cluster) unless K is not a
+// multiple of 256 or GNSB_WGRAD_IMPL=1 selects the single-CTA kernel
+bool wgrad_use_pair(int64_t K) {
+    if (K % (2 * wg::BM) != 0) return false;
+    const char* impl = std::getenv("GNSB_WGRAD_IMPL");
+    return !(impl && impl[0] == '1');
+}
+// scheduled tiles and the number of schedulers (CTAs, or CTA pairs)
+struct WgradSched {
+    int64_t stiles;
+    int grid;
+    int max_parts;
+};
+WgradSched wgrad_sched(int64_t B, int64_t K, int64_t L, bool pair) {
+    WgradSched w;
+    w.stiles = (K / (pair ? 2 * wg::BM : wg::BM)) * (L / wg::BN);
+    const int64_t units = w.stiles * B;
+    const int sms = pair ? device_sm_count() / 2 : device_sm_count();
+    w.grid = (int)(units < sms ? units : sms);
+    w.max_parts = wgrad_max_parts(B, w.stiles, w.grid);
+    return w;
+}
 struct WgradLayout {
     size_t q, qbig, ticket, part, total;
 };
-WgradLayout wgrad_layout(int64_t B, int64_t K, int64_t L, int grid) {
-    const int64_t tiles = (K / wg::BM) * (L / wg::BN);
+WgradLayout wgrad_layout(int64_t B, int64_t K, int64_t L, int max_parts) {
+    const int64_t tiles = (K / wg::BM) * (L / wg::BN);  // 128 x 256 sub-tiles
     WgradLayout w;
     w.q = 0;
     w.qbig = (size_t)B * tiles * sizeof(double);
     w.ticket = (w.qbig + (size_t)tiles * sizeof(double) + 255) / 256 * 256;
     w.part = (w.ticket + (size_t)tiles * sizeof(unsigned) + 255) / 256 * 256;
-    w.total = w.part + (size_t)tiles * wgrad_max_parts(B, tiles, grid) * wg::BM * wg::BN * sizeof(float);
+    w.total = w.part + (size_t)tiles * max_parts * wg::BM * wg::BN * sizeof(float);
     return w;
-}
-int wgrad_grid(int64_t B, int64_t K, int64_t L) {
-    const int64_t units = (K / wg::BM) * (L / wg::BN) * B;
-    const int sms = device_sm_count();
-    return (int)(units < sms ? units : sms);
 }
 // (grid may exceed the tile count: the extra CTAs take example ranges of tiles)
 }  // namespace
 
-size_t wgrad_workspace(int64_t B, int64_t K, int64_t L) { return wgrad_layout(B, K, L, wgrad_grid(B, K, L)).total; }
+size_t wgrad_workspace(int64_t B, int64_t K, int64_t L) {
+    // large enough for either kernel (the choice may change with the environment)
+    int mp = wgrad_sched(B, K, L, false).max_parts;
+    if (K % (2 * wg::BM) == 0) {
+        const int m2 = wgrad_sched(B, K, L, true).max_parts;
+        mp = m2 > mp ? m2 : mp;
+    }
+    return wgrad_layout(B, K, L, mp).total;
+}
 
 cudaError_t launch_wgrad_norms(const void* x, const void* g, float* dW, double* raw, double* sums, int64_t B,
                                int64_t T, int64_t K, int64_t L, void* ws, cudaStream_t st) {
     CUtensorMap mx, mg;
     if (!make_map_btf(&mx, x, (int)B, (int)T, (int)K) || !make_map_btf(&mg, g, (int)B, (int)T, (int)L))
         return cudaErrorInvalidValue;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        cudaFuncSetAttribute(wgrad_norms_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wg::SMEM);
-    });
+    const bool pair = wgrad_use_pair(K);
+    const void* fn = pair ? reinterpret_cast<const void*>(wgrad_norms_kernel<true>)
+                          : reinterpret_cast<const void*>(wgrad_norms_kernel<false>);
+    cudaError_t e = ensure_smem_attr(fn, wg::SMEM);
+    if (e != cudaSuccess) return e;
     WgradArgs a{};
     a.B = (int)B;
     a.T = (int)T;
@@ -418,22 +521,38 @@ cudaError_t launch_wgrad_norms(const void* x, const void* g, float* dW, double* 
     a.tiles_n = (int)(L / wg::BN);
     a.dW = dW;
     const int ntiles = a.tiles_m * a.tiles_n;
-    const int grid = wgrad_grid(B, K, L);
-    const WgradLayout w = wgrad_layout(B, K, L, grid);
+    const WgradSched sc = wgrad_sched(B, K, L, pair);
+    const WgradLayout w = wgrad_layout(B, K, L, sc.max_parts);
     unsigned char* base = static_cast<unsigned char*>(ws);
     a.q = reinterpret_cast<double*>(base + w.q);
     a.qbig = reinterpret_cast<double*>(base + w.qbig);
     a.ticket = reinterpret_cast<unsigned*>(base + w.ticket);
     a.part = reinterpret_cast<float*>(base + w.part);
-    a.max_parts = wgrad_max_parts(B, ntiles, grid);
+    a.max_parts = sc.max_parts;
     // the split-tile tickets must start at zero; the workspace may have been
     // used by another linear-path kernel with a different layout since
     if (a.max_parts > 1) {
         cudaError_t me = cudaMemsetAsync(a.ticket, 0, (size_t)ntiles * sizeof(unsigned), st);
         if (me != cudaSuccess) return me;
     }
-    wgrad_norms_kernel<<<grid, wg::THREADS, wg::SMEM, st>>>(mx, mg, a);
-    cudaError_t e = cudaGetLastError();
+    if (pair) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(2 * sc.grid);
+        cfg.blockDim = dim3(wg::THREADS);
+        cfg.dynamicSmemBytes = wg::SMEM;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, wgrad_norms_kernel<true>, mx, mg, a);
+    } else {
+        wgrad_norms_kernel<false><<<sc.grid, wg::THREADS, wg::SMEM, st>>>(mx, mg, a);
+        e = cudaGetLastError();
+    }
     if (e != cudaSuccess) return e;
     fold_rows_kernel<<<1, 256, 0, st>>>(a.q, (int)B, ntiles, raw, sums, 0);
     if (sums) fold_rows_kernel<<<1, 256, 0, st>>>(a.qbig, 1, ntiles, nullptr, sums, 2);

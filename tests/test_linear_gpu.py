@@ -70,9 +70,17 @@ def _oracle_linear(orc, x, g):
                                np.zeros((x.shape[-1], g.shape[-1])))
 
 
-@pytest.mark.parametrize("B,T,K,L", [(2, 64, 128, 256), (3, 128, 256, 512), (4, 192, 128, 256), (1, 64, 384, 256)])
-def test_tcgen05_weight_grad_form_matches_oracle(orc, cuda, B, T, K, L):
-    """bf16 rows on the tensor-core kernel vs the fp64 oracle on identical inputs."""
+@pytest.mark.parametrize("impl", ["pair", "single"])
+@pytest.mark.parametrize("B,T,K,L", [(2, 64, 128, 256), (3, 128, 256, 512), (4, 192, 128, 256), (1, 64, 384, 256),
+                                     (5, 64, 512, 768), (3, 64, 2048, 2560)])
+def test_tcgen05_weight_grad_form_matches_oracle(orc, cuda, monkeypatch, impl, B, T, K, L):
+    """bf16 rows on the tensor-core kernel vs the fp64 oracle on identical inputs.
+    "pair": the default CTA-pair kernel (256 x 256 tiles; K % 256 == 0, else the
+    single-CTA kernel runs); "single": GNSB_WGRAD_IMPL=1.  The shapes cover
+    tiles split into example ranges (few tiles, many examples) and a full round
+    plus split remainder (80 pair tiles on 74 pairs)."""
+    if impl == "single":
+        monkeypatch.setenv("GNSB_WGRAD_IMPL", "1")
     import paper_2411_00999_b200 as m
     from paper_2411_00999_b200 import linear
 
