@@ -164,4 +164,61 @@ int run_ldg(int u, int blocks_per_sm, const void* x, const void* dy, void* dx, i
     *ms /= reps;
     return cudaGetLastError();
 }
+
+// Same kernels over `nsets` distinct buffer sets, launch r on set r % nsets,
+// so no launch finds its inputs in L2 (the LN-bwd "steady" condition).
+int run_tma_sets(int cw, const void* const* x, const void* const* dy, void* const* dx, int nsets, int64_t N, int D,
+                 int R, int S, float* ms, int reps) {
+    const size_t smem = 1024 + (size_t)S * 2 * R * D * 2;
+    void (*k)(const __nv_bfloat16*, const __nv_bfloat16*, __nv_bfloat16*, int64_t, int, int, int) = nullptr;
+    if (cw == 4) k = tma_ring<4>;
+    else if (cw == 8) k = tma_ring<8>;
+    else if (cw == 16) k = tma_ring<16>;
+    else return -1;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) return -2;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    auto launch = [&](int r) {
+        const int i = r % nsets;
+        k<<<sms, (cw + 1) * 32, smem>>>((const __nv_bfloat16*)x[i], (const __nv_bfloat16*)dy[i], (__nv_bfloat16*)dx[i],
+                                        N, D, R, S);
+    };
+    for (int r = 0; r < nsets; ++r) launch(r);
+    cudaEventRecord(a);
+    for (int r = 0; r < reps; ++r) launch(r);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    cudaEventElapsedTime(ms, a, b);
+    *ms /= reps;
+    return cudaGetLastError();
+}
+
+int run_ldg_sets(int u, int blocks_per_sm, const void* const* x, const void* const* dy, void* const* dx, int nsets,
+                 int64_t n16, float* ms, int reps) {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int grid = sms * blocks_per_sm;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    auto launch = [&](int r) {
+        const int i = r % nsets;
+        const uint4 *xi = (const uint4*)x[i], *di = (const uint4*)dy[i];
+        uint4* oi = (uint4*)dx[i];
+        if (u == 1) ldg_stream<1><<<grid, 256>>>(xi, di, oi, n16);
+        if (u == 2) ldg_stream<2><<<grid, 256>>>(xi, di, oi, n16);
+        if (u == 4) ldg_stream<4><<<grid, 256>>>(xi, di, oi, n16);
+    };
+    for (int r = 0; r < nsets; ++r) launch(r);
+    cudaEventRecord(a);
+    for (int r = 0; r < reps; ++r) launch(r);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    cudaEventElapsedTime(ms, a, b);
+    *ms /= reps;
+    return cudaGetLastError();
+}
 }

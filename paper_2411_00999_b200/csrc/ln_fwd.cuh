@@ -187,7 +187,9 @@ struct LnFwdRingCfg {
     }
 };
 
-template <typename T, int GW, int VPT, int G>
+// GBS: gamma/beta read from shared memory per row instead of held in registers
+// (wide per-thread slices)
+template <typename T, int GW, int VPT, int G, bool GBS = false>
 __global__ void __launch_bounds__(LnFwdRingCfg<T, GW, VPT, G>::kThreads, 1) ln_fwd_ring_kernel(LnFwdArgs a, int S) {
     using C = LnFwdRingCfg<T, GW, VPT, G>;
     using Acc = typename Traits<T>::Acc;
@@ -267,14 +269,26 @@ __global__ void __launch_bounds__(LnFwdRingCfg<T, GW, VPT, G>::kThreads, 1) ln_f
                 rb2[wig] = vv[1];
             }
             named_bar_sync(1 + g, GT);
-            Acc t1 = 0, t2 = 0;
+            if constexpr (GW <= 8) {  // a few vectorised shared loads: shortest latency
+                Acc t1 = 0, t2 = 0;
 #pragma unroll
-            for (int w = 0; w < GW; ++w) {
-                t1 += rb[w];
-                t2 += rb2[w];
+                for (int w = 0; w < GW; ++w) {
+                    t1 += rb[w];
+                    t2 += rb2[w];
+                }
+                v1 = t1;
+                v2 = t2;
+            } else {
+                // lanes 0..15 fold the first sum, lanes 16..31 the second: one
+                // shared load and a 4-step butterfly instead of GW loads each
+                static_assert(GW <= 16, "cross-warp fold assumes at most 16 warps per row");
+                const int j = lane & 15;
+                Acc t = j < GW ? (lane < 16 ? rb[j] : rb2[j]) : Acc(0);
+#pragma unroll
+                for (int m = 8; m >= 1; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
+                v1 = __shfl_sync(0xffffffffu, t, 0);
+                v2 = __shfl_sync(0xffffffffu, t, 16);
             }
-            v1 = t1;
-            v2 = t2;
         }
     };
     // the thread's gamma/beta columns, in registers for the whole kernel;
@@ -283,7 +297,7 @@ __global__ void __launch_bounds__(LnFwdRingCfg<T, GW, VPT, G>::kThreads, 1) ln_f
     using PR = Pair<Acc>;
     using P = typename PR::P;
     constexpr int NP = W / 2;
-    P gv[VPT][NP], bv[VPT][NP];
+    P gv[GBS ? 1 : VPT][NP], bv[GBS ? 1 : VPT][NP];
     bool vin[VPT];
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
@@ -291,8 +305,10 @@ __global__ void __launch_bounds__(LnFwdRingCfg<T, GW, VPT, G>::kThreads, 1) ln_f
         vin[k] = c0 < D;
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
-            gv[k][p] = vin[k] ? PR::make(gs[c0 + 2 * p], gs[c0 + 2 * p + 1]) : PR::splat(Acc(0));
-            bv[k][p] = vin[k] ? PR::make(bs[c0 + 2 * p], bs[c0 + 2 * p + 1]) : PR::splat(Acc(0));
+            if constexpr (!GBS) {
+                gv[k][p] = vin[k] ? PR::make(gs[c0 + 2 * p], gs[c0 + 2 * p + 1]) : PR::splat(Acc(0));
+                bv[k][p] = vin[k] ? PR::make(bs[c0 + 2 * p], bs[c0 + 2 * p + 1]) : PR::splat(Acc(0));
+            }
         }
     }
     int slot = 0;
@@ -352,7 +368,10 @@ __global__ void __launch_bounds__(LnFwdRingCfg<T, GW, VPT, G>::kThreads, 1) ln_f
 #pragma unroll
                 for (int p = 0; p < NP; ++p) {
                     xo[p] = PR::fma(xv[k][p], inv2, nmi2);
-                    yo[p] = PR::fma(gv[k][p], xo[p], bv[k][p]);
+                    if constexpr (GBS)
+                        yo[p] = PR::fma(reinterpret_cast<const P*>(gs + c0)[p], xo[p], reinterpret_cast<const P*>(bs + c0)[p]);
+                    else
+                        yo[p] = PR::fma(gv[k][p], xo[p], bv[k][p]);
                 }
                 if (yg) st_stream(yg + row * D + c0, pack2<T>(yo));
                 if (xhg) st_stream(xhg + row * D + c0, pack2<T>(xo));
@@ -361,6 +380,115 @@ __global__ void __launch_bounds__(LnFwdRingCfg<T, GW, VPT, G>::kThreads, 1) ln_f
         if (++slot == S) {
             slot = 0;
             ph ^= 1u;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Warp-per-row variant for aligned rows up to 16 16-byte vectors per lane: a
+// warp owns whole rows (lane l holds vectors l, l+32, ... as packed T), so
+// both reductions are warp butterflies with no barrier.  PF: the warp loads
+// its next row before reducing the current one (narrow rows); without PF the
+// other warps of the SM hide the latency (wide rows, fewer registers).  The
+// vectors stay packed in registers and are unpacked per pass.  gamma/beta are
+// read from shared memory.  Two-pass moments from registers, as the reference.
+template <typename T, int VPT, int MINB, bool PF>
+__global__ void __launch_bounds__(256, MINB) ln_fwd_warp_kernel(LnFwdArgs a) {
+    using Acc = typename Traits<T>::Acc;
+    using PR = Pair<Acc>;
+    using P = typename PR::P;
+    constexpr int W = Traits<T>::W;
+    constexpr int NP = W / 2;
+    extern __shared__ __align__(16) unsigned char fsmem[];
+    Acc* gs = reinterpret_cast<Acc*>(fsmem);
+    const int64_t N = a.N, D = a.D;
+    const int nvec = (int)(D / W);
+    Acc* bs = gs + (size_t)nvec * W;
+    {
+        const Acc* gam = static_cast<const Acc*>(a.gamma);
+        const Acc* bet = static_cast<const Acc*>(a.beta);
+        for (int c = threadIdx.x; c < nvec * W; c += blockDim.x) {
+            gs[c] = gam[c];
+            bs[c] = bet[c];
+        }
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t wpb = blockDim.x >> 5;
+    const int64_t stride = (int64_t)gridDim.x * wpb;
+    int64_t row = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5);
+    const T* xg = static_cast<const T*>(a.x);
+    T* yg = static_cast<T*>(a.y);
+    T* xhg = static_cast<T*>(a.xhat);
+    Acc* meang = static_cast<Acc*>(a.mean);
+    Acc* rstdg = static_cast<Acc*>(a.rstd);
+    const Acc invD = Acc(1) / Acc(D);
+    const Acc eps = (Acc)a.eps;
+    bool vin[VPT];
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) vin[k] = lane + 32 * k < nvec;
+    auto load = [&](int64_t r, uint4 (&v)[VPT]) {
+        const T* xr = xg + r * D;
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) v[k] = vin[k] ? ld_stream(xr + (lane + 32 * k) * W) : make_uint4(0, 0, 0, 0);
+    };
+    uint4 cur[VPT];
+    if (PF && row < N) load(row, cur);
+    for (; row < N; row += stride) {
+        uint4 nxt[PF ? VPT : 1];
+        if constexpr (PF) {
+            if (row + stride < N) load(row + stride, nxt);
+        } else {
+            load(row, cur);
+        }
+        P s1 = PR::splat(Acc(0));
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+            P xv[NP];
+            unpack2<T>(cur[k], xv);
+#pragma unroll
+            for (int p = 0; p < NP; ++p) s1 = PR::add(s1, xv[p]);
+        }
+        const Acc mu = warp_sum(s1.x + s1.y) * invD;
+        const P nmu = PR::splat(-mu);
+        P s2 = PR::splat(Acc(0));
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+            if (!vin[k]) continue;
+            P xv[NP];
+            unpack2<T>(cur[k], xv);
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                const P d = PR::add(xv[p], nmu);
+                s2 = PR::fma(d, d, s2);
+            }
+        }
+        const Acc var = warp_sum(s2.x + s2.y) * invD;
+        const Acc inv = Acc(1) / sqrt(var + eps);
+        if (lane == 0) {
+            if (meang) meang[row] = mu;
+            if (rstdg) rstdg[row] = inv;
+        }
+        const P inv2 = PR::splat(inv), nmi2 = PR::splat(-mu * inv);
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+            if (!vin[k]) continue;
+            const int c0 = (lane + 32 * k) * W;
+            const P* gp = reinterpret_cast<const P*>(gs + c0);
+            const P* bp = reinterpret_cast<const P*>(bs + c0);
+            P xv[NP], yo[NP], xo[NP];
+            unpack2<T>(cur[k], xv);
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                xo[p] = PR::fma(xv[p], inv2, nmi2);
+                yo[p] = PR::fma(gp[p], xo[p], bp[p]);
+            }
+            if (yg) st_stream(yg + row * D + c0, pack2<T>(yo));
+            if (xhg) st_stream(xhg + row * D + c0, pack2<T>(xo));
+        }
+        if constexpr (PF) {
+#pragma unroll
+            for (int k = 0; k < VPT; ++k) cur[k] = nxt[k];
         }
     }
 }

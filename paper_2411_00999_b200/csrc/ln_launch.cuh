@@ -209,6 +209,51 @@ struct BwdOp {
     }
 };
 
+// Aligned rows of at most 16 16-byte vectors per lane: the warp-per-row
+// forward (ln_fwd_warp_kernel); register bound, prefetch and CTAs per SM per
+// width measured on B200 (experiments/ln_fwd_sweep.py, bf16).
+template <typename T, int VPT, int MINB, bool PF>
+inline int launch_fwd_warp(const LnFwdArgs& a, int per_sm, cudaStream_t st, const char** why, cudaError_t* cerr) {
+    const size_t smem = (size_t)2 * a.D * sizeof(typename Traits<T>::Acc);
+    auto k = ln_fwd_warp_kernel<T, VPT, MINB, PF>;
+    cudaError_t se = ensure_smem(reinterpret_cast<const void*>(k), smem);
+    if (se != cudaSuccess) {
+        *cerr = se;
+        *why = "ln_fwd smem attribute";
+        return 2;
+    }
+    int64_t grid = (int64_t)device_sm_count() * per_sm;
+    const int64_t need = (a.N + 7) / 8;  // one row per warp at least
+    if (grid > need) grid = need;
+    k<<<(int)grid, 256, smem, st>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        *cerr = e;
+        *why = "ln_fwd launch";
+        return 2;
+    }
+    return 0;
+}
+
+template <typename T>
+inline int try_fwd_warp(const LnFwdArgs& a, cudaStream_t st, const char** why, cudaError_t* cerr, bool* done) {
+    constexpr int W = Traits<T>::W;
+    *done = false;
+    if (!a.aligned || a.D % W != 0) return 0;
+    const int64_t per_lane = (a.D / W + 31) / 32;
+    *done = true;
+    switch (per_lane) {
+        case 1: return launch_fwd_warp<T, 1, 4, true>(a, 4, st, why, cerr);
+        case 2: return launch_fwd_warp<T, 2, 4, true>(a, 4, st, why, cerr);
+        case 3: return launch_fwd_warp<T, 3, 4, true>(a, 4, st, why, cerr);
+        case 4: return launch_fwd_warp<T, 4, 1, true>(a, 2, st, why, cerr);
+        case 5: case 6: case 7: case 8: return launch_fwd_warp<T, 8, 2, true>(a, 2, st, why, cerr);
+        case 9: case 10: case 11: case 12: case 13: case 14: case 15: case 16:
+            return launch_fwd_warp<T, 16, 2, false>(a, 2, st, why, cerr);
+        default: *done = false; return 0;
+    }
+}
+
 template <typename T, int GW, int VPT>
 struct FwdOp {
     static int run(const LnFwdCall& c, cudaStream_t st, const char** why, cudaError_t* cerr) {
@@ -227,6 +272,9 @@ struct FwdOp {
         a.aligned = ((c.D * (int64_t)sizeof(T)) % 16 == 0) && ptr16(c.x) && (c.y == nullptr || ptr16(c.y)) &&
                     (c.xhat == nullptr || ptr16(c.xhat));
         const int sms = device_sm_count();
+        bool done = false;
+        const int wrc = try_fwd_warp<T>(a, st, why, cerr, &done);
+        if (done) return wrc;
         if (a.aligned && c.D % Traits<T>::W == 0) {
             // TMA ring: G groups so that the CTA has ~16 consumer warps
             constexpr int GR = GW >= 16 ? 1 : (16 / GW > 15 ? 15 : 16 / GW);
@@ -242,7 +290,7 @@ struct FwdOp {
                 }
             if (S > 0) {
                 const size_t smem = RC::smem_bytes(S, a.Dp, c.D);
-                auto k = ln_fwd_ring_kernel<T, GW, VPT, GR>;
+                auto k = ln_fwd_ring_kernel<T, GW, VPT, GR, (VPT >= 4)>;  // wide slices: gamma/beta from smem
                 cudaError_t se = ensure_smem(reinterpret_cast<const void*>(k), smem);
                 if (se != cudaSuccess) {
                     *cerr = se;
@@ -320,7 +368,10 @@ struct BwdPlanOp {
 template <typename C>
 struct FwdRunOp {
     static int call(const LnFwdCall& c, cudaStream_t st, const char** why, cudaError_t* cerr) {
-        return FwdOp<typename C::Row, C::kGW, C::kVPT>::run(c, st, why, cerr);
+        // widest rows: 16 warps x 2 vectors per row beats the backward's
+        // 11 x 3 for the forward (experiments/ln_fwd_sweep.py, D = 8192)
+        constexpr bool wide = C::kGW == 11 && C::kVPT == 3;
+        return FwdOp<typename C::Row, wide ? 16 : C::kGW, wide ? 2 : C::kVPT>::run(c, st, why, cerr);
     }
 };
 
