@@ -408,7 +408,7 @@ def run_ours(args):
     dom_achieved = dom_bytes / (dom_us * 1e-6) / 1e9
 
     extra = {}
-    if rank == 0 and not args.no_extra:
+    if rank == 0 and not (args.no_extra or args.no_side):
         extra["ln_forward"] = run_ln_fwd(m, lib, cases, dev, torch, np)
         extra["cfg3_linear"] = run_cfg3(m, lib, dev, torch, np)
         extra["cfg4_gns"] = run_cfg4(m, lib, dev, torch, np)
@@ -736,7 +736,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--d-list", type=lambda s: [int(v) for v in s.split(",")], default=SWEEP_D)
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
-    ap.add_argument("--no-extra", action="store_true", help="skip the config-3/4 side measurements")
+    ap.add_argument("--no-extra", action="store_true", help="skip the per-width steady runs and the side measurements")
+    ap.add_argument("--no-side", action="store_true", help="skip the side measurements (forward, configs 3/4/5)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -401,3 +401,65 @@ def test_deferred_reduce_limits(cuda):
     p64 = layers.layernorm_backward_rows(m.LayerNormLayer(gamma, beta), f.cache, dy)[1]
     with pytest.raises(ValueError, match="mix fp64 and fp32"):
         layers.layernorm_backward_reduce([pend[0], p64])
+
+
+@pytest.mark.parametrize(
+    "dt,B,T,D,offset,use_xhat",
+    [
+        (torch.bfloat16, 5, 13, 256, 0, False),
+        (torch.bfloat16, 7, 8, 512, 0, False),
+        (torch.bfloat16, 4, 9, 768, 0, False),
+        (torch.bfloat16, 37, 11, 1024, 0, False), # many examples per CTA
+        (torch.float32, 3, 50, 384, 0, False),
+        (torch.float32, 2, 64, 512, 0, True),     # x-hat cache (no mean)
+        (torch.bfloat16, 3, 20, 768, 3, False),   # rows not 16-byte aligned: element-wise path
+        (torch.float32, 3, 20, 256, 1, True),
+        (torch.float64, 3, 16, 96, 0, False),
+        (torch.bfloat16, 2, 7, 768, 0, False),
+    ],
+)
+def test_row_pass_edge_cases_match_oracle(orc, cuda, dt, B, T, D, offset, use_xhat):
+    """Row pass against the oracle at example boundaries in every position of
+    a row stage, with the x-hat cache (no mean), with row pointers that are not
+    16-byte aligned (storage offset: the non-TMA producer) and through the
+    deferred grouped reduce."""
+    m = _mod()
+    bf = dt == torch.bfloat16
+    x, dy, gamma, beta = m.synth_ln(B, T, D, dt, cuda, stream0=11)
+    if offset:
+        def shift(t):
+            buf = torch.empty(t.numel() + offset, dtype=t.dtype, device=cuda)
+            v = buf[offset:].view(t.shape)
+            v.copy_(t)
+            return v
+        x, dy = shift(x), shift(dy)
+        assert x.data_ptr() % 16 != 0
+    layer = m.LayerNormLayer(gamma, beta, 1e-5)
+    f = m.layernorm_forward(layer, x)
+    cache = f.cache
+    if use_xhat:
+        xh = ((x.double() - f.cache.mean.double()[..., None]) * f.cache.inv_std.double()[..., None]).to(dt)
+        if offset:
+            xh = shift(xh)
+        cache = m.LayerNormCache(normalized=xh, inv_std=f.cache.inv_std)
+        ref = orc.ln_backward(xh.cpu().double().numpy(), f.cache.inv_std.cpu().double().numpy(),
+                              dy.cpu().double().numpy(), gamma.cpu().double().numpy())
+    else:
+        ref = _oracle_on_device_stats(orc, x, dy, gamma, f.cache.mean, f.cache.inv_std)
+    from paper_2411_00999_b200 import layers
+
+    r = m.layernorm_backward_simultaneous(layer, cache, dy)
+    dxd, pend = layers.layernorm_backward_rows(layer, cache, dy)
+    rd = layers.layernorm_backward_reduce([pend])[0]
+    torch.cuda.synchronize()
+    dxt = {torch.float64: 1e-11, torch.float32: F32_TOL, torch.bfloat16: BF16_DX}[dt]
+    gt = {torch.float64: 1e-11, torch.float32: F32_TOL, torch.bfloat16: NORM_TOL}[dt]
+    nt = {torch.float64: 1e-11, torch.float32: NORM_TOL, torch.bfloat16: NORM_TOL}[dt]
+    for dxv, gr in ((r.input_grad, r.grads), (dxd, rd)):
+        assert _close_inf(dxv.double().cpu().numpy(), ref["dx"], dxt)
+        assert _close_inf(gr.weight_grads["gamma"].double().cpu().numpy(), ref["dgamma"], gt)
+        assert _close_inf(gr.weight_grads["beta"].double().cpu().numpy(), ref["dbeta"], gt)
+        assert close(gr.per_example_sqnorms_raw["gamma"].cpu().numpy(), ref["raw_gamma"], nt)
+        assert close(gr.per_example_sqnorms_raw["beta"].cpu().numpy(), ref["raw_beta"], nt)
+    assert torch.equal(r.input_grad, dxd)
+    assert torch.equal(r.grads.weight_grads["gamma"], rd.weight_grads["gamma"])
