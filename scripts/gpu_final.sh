@@ -11,6 +11,10 @@ timeout 600 $NCU --metrics gpu__time_duration.sum -c 700 --csv --log-file gpurun
     python bench.py --steps 2 --warmup 3 --no-cpu --no-extra > /dev/null 2>&1
 timeout 600 $NCU --set full --import-source on -k regex:ln_bwd_kernel -s 9 -c 1 -o gpurun_out/final_rows_d8192 \
     python bench.py --steps 1 --warmup 3 --no-cpu --no-extra --d-list 8192 > /dev/null 2>&1
-timeout 600 $NCU --set full --import-source on -k regex:ln_fwd_ring -s 1 -c 1 -o gpurun_out/final_fwd_d4096 \
-    python bench.py --steps 1 --warmup 3 --no-cpu --no-extra --d-list 4096 > /dev/null 2>&1
+timeout 600 $NCU --set full --import-source on -k regex:ln_fwd -s 1 -c 1 -o gpurun_out/final_fwd_d1024 \
+    python bench.py --steps 1 --warmup 3 --no-cpu --d-list 1024 > /dev/null 2>&1
 ls -la gpurun_out/final_*
+# memcheck over the kernels changed since the last sanitizer pass (CTA-pair wgrad, warp forward)
+timeout 900 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_linear_gpu.py -q -k "weight_grad_form_matches" > gpurun_out/final_memcheck_lin.log 2>&1
+timeout 900 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_ln_gpu.py -q -k "forward or edge or oracle" > gpurun_out/final_memcheck_ln.log 2>&1
+tail -3 gpurun_out/final_memcheck_*.log
