@@ -147,26 +147,46 @@ class ToyModelPE(torch.nn.Module):
     """proj/include/gnstk/model.hpp:14-31 on the GPU, initialised as
     make_toy_model (proj/src/model.cpp:30-55): Gaussian weights with std 1
     (embedding), 1/sqrt(D) (fc1, head), 1/sqrt(H) (fc2); zero biases; LN gamma 1,
-    beta 0.  (The draws come from torch's generator, not the reference's.)"""
+    beta 0.  init="reference" draws them from the reference's own stream
+    (GaussianStream(mix_seed(seed, "init")), same order), so the weights equal
+    make_toy_model's bit for bit; init="torch" uses torch's generator.
+    dtype: fp32 (default) or fp64 parameters and activations."""
 
-    def __init__(self, vocab: int, dim: int, hidden_multiplier: int, n_blocks: int, seed: int = 0, device=None):
+    _INIT_TAG = 0x696E6974  # model.cpp:16
+
+    def __init__(self, vocab: int, dim: int, hidden_multiplier: int, n_blocks: int, seed: int = 0, device=None,
+                 dtype=torch.float32, init: str = "torch"):
         super().__init__()
         if vocab < 2 or dim < 2 or hidden_multiplier < 1 or n_blocks < 1:
             raise ValueError("model: invalid model dims")
+        if init not in ("torch", "reference"):
+            raise ValueError("model: init must be 'torch' or 'reference'")
         H = dim * hidden_multiplier
-        gen = torch.Generator(device="cpu").manual_seed(seed)
-        self.embed = EmbeddingPE(vocab, dim, device=device)
-        self.lns = torch.nn.ModuleList([LayerNormPE(dim, device=device) for _ in range(n_blocks)])
-        self.fc1 = torch.nn.ModuleList([LinearPE(dim, H, device=device) for _ in range(n_blocks)])
-        self.fc2 = torch.nn.ModuleList([LinearPE(H, dim, device=device) for _ in range(n_blocks)])
-        self.final_ln = LayerNormPE(dim, device=device)
-        self.head = LinearPE(dim, vocab, device=device)
+        self.embed = EmbeddingPE(vocab, dim, device=device, dtype=dtype)
+        self.lns = torch.nn.ModuleList([LayerNormPE(dim, device=device, dtype=dtype) for _ in range(n_blocks)])
+        self.fc1 = torch.nn.ModuleList([LinearPE(dim, H, device=device, dtype=dtype) for _ in range(n_blocks)])
+        self.fc2 = torch.nn.ModuleList([LinearPE(H, dim, device=device, dtype=dtype) for _ in range(n_blocks)])
+        self.final_ln = LayerNormPE(dim, device=device, dtype=dtype)
+        self.head = LinearPE(dim, vocab, device=device, dtype=dtype)
+        if init == "reference":
+            from .data import GaussianStream, mix_seed
+
+            g = GaussianStream(mix_seed(seed, self._INIT_TAG))
+
+            def draw(shape, std):
+                n = shape[0] * shape[1]
+                return torch.from_numpy(std * g.draw(n)).reshape(shape)
+        else:
+            gen = torch.Generator(device="cpu").manual_seed(seed)
+
+            def draw(shape, std):
+                return torch.randn(*shape, generator=gen, dtype=torch.float64) * std
         with torch.no_grad():
-            self.embed.weight.copy_(torch.randn(vocab, dim, generator=gen))
+            self.embed.weight.copy_(draw((vocab, dim), 1.0))
             for f1, f2 in zip(self.fc1, self.fc2):
-                f1.weight.copy_(torch.randn(dim, H, generator=gen) / math.sqrt(dim))
-                f2.weight.copy_(torch.randn(H, dim, generator=gen) / math.sqrt(H))
-            self.head.weight.copy_(torch.randn(dim, vocab, generator=gen) / math.sqrt(dim))
+                f1.weight.copy_(draw((dim, H), 1.0 / math.sqrt(dim)))
+                f2.weight.copy_(draw((H, dim), 1.0 / math.sqrt(H)))
+            self.head.weight.copy_(draw((dim, vocab), 1.0 / math.sqrt(dim)))
 
     def forward(self, ids: torch.Tensor) -> torch.Tensor:
         x = self.embed(ids)
@@ -179,8 +199,10 @@ class ToyModelPE(torch.nn.Module):
         (proj/src/model.cpp:150-156: dlogits scaled by 1/(T*B))."""
         logits = self.forward(ids)
         B, T, V = logits.shape
-        ce = torch.nn.functional.cross_entropy(logits.reshape(B * T, V).float(), targets.reshape(-1).long(),
-                                               reduction="none")
+        lg = logits.reshape(B * T, V)
+        if lg.dtype != torch.float64:
+            lg = lg.float()
+        ce = torch.nn.functional.cross_entropy(lg, targets.reshape(-1).long(), reduction="none")
         return ce.reshape(B, T).mean(1).mean(0)
 
     def instrumented_layers(self) -> List[Tuple[str, torch.nn.Module]]:

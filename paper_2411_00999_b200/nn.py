@@ -91,12 +91,14 @@ class LayerNormPE(torch.nn.Module):
                        norm = record[i] * B, proj/src/layers.cpp:39-42)
       per_example_raw  {"gamma": [B], "beta": [B]} fp64 device tensors
     The per-example values are exact only for a loss that is a MEAN over the
-    B examples.
+    B examples.  dtype=torch.float64 gives fp64 gamma/beta for
+    fp64 rows (the reference's own precision).
     """
 
     layer_type = "layernorm"
 
-    def __init__(self, normalized_shape: int, eps: float = 1e-5, device=None, track_norms: bool = True):
+    def __init__(self, normalized_shape: int, eps: float = 1e-5, device=None, track_norms: bool = True,
+                 dtype=torch.float32):
         super().__init__()
         if not eps > 0.0:
             raise ValueError("layers: epsilon must be positive")
@@ -104,8 +106,10 @@ class LayerNormPE(torch.nn.Module):
             raise ValueError("layers: layernorm needs trailing extent >= 2")
         self.normalized_shape = int(normalized_shape)
         self.eps = float(eps)
-        self.weight = torch.nn.Parameter(torch.ones(self.normalized_shape, dtype=torch.float32, device=device))
-        self.bias = torch.nn.Parameter(torch.zeros(self.normalized_shape, dtype=torch.float32, device=device))
+        if dtype not in (torch.float32, torch.float64):
+            raise TypeError("LayerNormPE: gamma/beta are fp32 (bf16/fp32 rows) or fp64 (fp64 rows)")
+        self.weight = torch.nn.Parameter(torch.ones(self.normalized_shape, dtype=dtype, device=device))
+        self.bias = torch.nn.Parameter(torch.zeros(self.normalized_shape, dtype=dtype, device=device))
         self.track_norms = track_norms
         self.norm_record: Optional[torch.Tensor] = None
         self.per_example_raw: Optional[dict] = None

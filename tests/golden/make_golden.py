@@ -1,5 +1,6 @@
 #!/usr/bin/env python
-"""Regenerate tests/golden/reference_cases.json from the UNMODIFIED reference.
+"""Regenerate tests/golden/reference_cases.json and trainer_cases.json from the
+UNMODIFIED reference.
 
 TEST INFRASTRUCTURE ONLY.  Runs in the dev container, where /root/reference
 exists:
@@ -13,6 +14,11 @@ known-answer tests and seeded random families (see the family list at the top
 of oracle/gen_golden.cpp) and prints every case with its inputs and the
 reference's outputs as JSON.  --check only verifies that the committed file is
 what the reference produces today.
+
+oracle/_ref/gen_trainer_golden (oracle/gen_trainer_golden.cpp linked against
+the reference's model.cpp / dataset.cpp / trainer.cpp as well) prints
+MarkovDataset streams, make_toy_model weights, scheduled_batch values and
+Trainer::step logs of PerExample runs -> trainer_cases.json.
 """
 import argparse
 import json
@@ -24,6 +30,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 GEN = os.path.join(ROOT, "oracle", "_ref", "gen_golden")
 OUT = os.path.join(HERE, "reference_cases.json")
+GEN_T = os.path.join(ROOT, "oracle", "_ref", "gen_trainer_golden")
+OUT_T = os.path.join(HERE, "trainer_cases.json")
 
 
 def main() -> int:
@@ -32,17 +40,20 @@ def main() -> int:
     args = ap.parse_args()
     if not os.path.exists(GEN):
         subprocess.run(["make", "-C", os.path.join(ROOT, "oracle")], check=True)
-    text = subprocess.run([GEN], check=True, capture_output=True, text=True).stdout
-    cases = json.loads(text)
-    if args.check:
-        with open(OUT) as f:
-            same = json.load(f) == cases
-        print("golden up to date" if same else "golden DIFFERS from the reference output")
-        return 0 if same else 1
-    with open(OUT, "w") as f:
-        f.write(text)
-    print(f"wrote {len(cases)} cases to {OUT}")
-    return 0
+    rc = 0
+    for gen, out in ((GEN, OUT), (GEN_T, OUT_T)):
+        text = subprocess.run([gen], check=True, capture_output=True, text=True).stdout
+        cases = json.loads(text)
+        if args.check:
+            with open(out) as f:
+                same = json.load(f) == cases
+            print(f"{os.path.basename(out)}: " + ("up to date" if same else "DIFFERS from the reference output"))
+            rc |= 0 if same else 1
+            continue
+        with open(out, "w") as f:
+            f.write(text)
+        print(f"wrote {len(cases)} cases to {out}")
+    return rc
 
 
 if __name__ == "__main__":
