@@ -20,6 +20,9 @@
 //     squares for ||dW||^2.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+#include <type_traits>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -195,6 +198,279 @@ __global__ void __launch_bounds__(kEmbThreads) emb_table_kernel(int64_t B, int64
     }
 }
 
+// ---------------------------------------------------------------------------
+// Fast path for fp32 / bf16 rows (fp32 accumulation): no materialised
+// per-example rows.
+//   * emb_sort_kernel: one CTA per example sorts its (id, t) keys and writes
+//     the token order perm[b][i] (sorted t) and one entry per run,
+//     ent[b][k] = {id, first position in perm, length, first token}, plus the
+//     run count U[b] (parallel run detection by a block scan).
+//   * emb_rows_kernel: one warp per block of kRowsPerWarp table rows.  Lane j
+//     of group G tracks example 32G + j: a lower_bound into its sorted entry
+//     list once per block, then it holds its next entry in registers (the
+//     following one is loaded as soon as a row consumes it).  For row v the
+//     warp ballots the matching examples and walks them in example order; for
+//     each it sums the run's token rows (token order, lanes over 16-byte
+//     column vectors; a one-token run needs no perm load) into dE_b[v], adds
+//     that to dW[v] and reduces ||dE_b[v]||^2 into q[b][k].  g is read once
+//     and dW written once, 16 bytes per lane per vector.
+//   * emb_raw_kernel: raw_b = sum_k q[b][k] (one warp per example, fixed-order
+//     tree).
+// dW matches the original path bit for bit (same per-example Acc sums, added
+// in example order); raw_b differs in summation order only.
+constexpr int kEmbSortThreads = 512;
+constexpr int kRowsPerWarp = 8;
+constexpr int kEmbRowsThreads = 256;
+constexpr int kEmbMaxGroups = 8;  // examples handled by the fast path: B <= 32 * 8
+
+struct EmbFastWs {
+    int32_t* perm;  // [B][Tn]
+    int4* ent;      // [B][Tn] {id, start, len, first token}
+    int32_t* U;     // [B]
+    double* q;      // [B][Tn]
+    double* qbig;   // [rows-kernel CTAs]
+    int32_t* bad;
+};
+
+template <int NT>
+__device__ __forceinline__ int block_exclusive_scan(int v, int* s_warp, int* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        int w = lane < NT / 32 ? s_warp[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < NT / 32) s_warp[lane] = w;  // inclusive warp totals
+    }
+    __syncthreads();
+    const int before = warp > 0 ? s_warp[warp - 1] : 0;
+    *total = s_warp[NT / 32 - 1];
+    return before + x - v;
+}
+
+__global__ void __launch_bounds__(kEmbSortThreads) emb_sort_kernel(const int32_t* ids, int64_t Tn, int64_t V,
+                                                                   EmbFastWs w, int Tp) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint64_t* keys = reinterpret_cast<uint64_t*>(smem);  // [Tp]
+    __shared__ int s_warp[kEmbSortThreads / 32];
+    __shared__ int s_nvalid;
+    const int64_t b = blockIdx.x;
+    const int tid = threadIdx.x;
+    const int32_t* idb = ids + b * Tn;
+    if (tid == 0) s_nvalid = 0;
+    for (int i = tid; i < Tp; i += blockDim.x) {
+        uint64_t k = ~0ull;
+        if (i < Tn) {
+            const int32_t id = idb[i];
+            if (id < 0 || id >= V)
+                atomicExch(w.bad, 1);
+            else
+                k = ((uint64_t)(uint32_t)id << 32) | (uint32_t)i;
+        }
+        keys[i] = k;
+    }
+    __syncthreads();
+    for (int size = 2; size <= Tp; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = tid; i < Tp; i += blockDim.x) {
+                const int j = i ^ stride;
+                if (j > i) {
+                    const uint64_t a = keys[i], c = keys[j];
+                    const bool up = (i & size) == 0;
+                    if ((a > c) == up) {
+                        keys[i] = c;
+                        keys[j] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    // run heads: a valid key whose id differs from its predecessor's.  Each
+    // thread scans a contiguous chunk; a block scan numbers the runs.
+    const int per = (Tp + kEmbSortThreads - 1) / kEmbSortThreads;
+    const int i0 = tid * per, i1 = min(i0 + per, Tp);
+    auto valid = [&](int i) { return i < Tp && keys[i] != ~0ull; };
+    auto head = [&](int i) { return valid(i) && (i == 0 || (uint32_t)(keys[i - 1] >> 32) != (uint32_t)(keys[i] >> 32)); };
+    int cnt = 0, nv = 0;
+    for (int i = i0; i < i1; ++i) {
+        if (!valid(i)) break;
+        cnt += head(i) ? 1 : 0;
+        nv = i + 1;
+    }
+    if (nv > 0) atomicMax(&s_nvalid, nv);
+    int total = 0;
+    int r = block_exclusive_scan<kEmbSortThreads>(cnt, s_warp, &total);  // (its barriers publish s_nvalid)
+    const int nvalid = s_nvalid;
+    int32_t* perm = w.perm + b * Tn;
+    int4* ent = w.ent + b * Tn;
+    for (int i = i0; i < i1; ++i) {
+        if (!valid(i)) break;
+        perm[i] = (int32_t)(uint32_t)(keys[i] & 0xffffffffu);
+        if (head(i)) {
+            int e = i + 1;
+            while (e < nvalid && (uint32_t)(keys[e] >> 32) == (uint32_t)(keys[i] >> 32)) ++e;
+            ent[r] = make_int4((int)(keys[i] >> 32), i, e - i, (int)(uint32_t)(keys[i] & 0xffffffffu));
+            ++r;
+        }
+    }
+    if (tid == 0) w.U[b] = total;
+}
+
+template <typename T, int NVC, int NG>
+__global__ void __launch_bounds__(kEmbRowsThreads) emb_rows_kernel(const T* g, int64_t B, int64_t Tn, int64_t V,
+                                                                   int64_t D, EmbFastWs w, float* dW) {
+    constexpr int W = Traits<T>::W;
+    constexpr int NP = W / 2;
+    using P = float2;
+    __shared__ double s_red[kEmbRowsThreads / 32];
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int nvec = (int)(D / W);
+    const int nchunk = (nvec + 32 * NVC - 1) / (32 * NVC);
+    double qb = 0.0;  // this lane's share of ||dW||^2
+    for (int64_t v0 = gw * kRowsPerWarp; v0 < V; v0 += nw * kRowsPerWarp) {
+        int p[NG], Ub[NG];
+        int4 cur[NG];  // the lane's next unconsumed entry of its example
+#pragma unroll
+        for (int G = 0; G < NG; ++G) {
+            p[G] = 0;
+            Ub[G] = 0;
+            cur[G] = make_int4(-1, 0, 0, 0);
+            const int64_t b = 32 * G + lane;
+            if (b < B) {  // lower_bound(ids of example b, v0)
+                const int4* eb = w.ent + b * Tn;
+                int lo = 0, hi = w.U[b];
+                Ub[G] = hi;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (eb[mid].x < (int32_t)v0) lo = mid + 1;
+                    else hi = mid;
+                }
+                p[G] = lo;
+                if (lo < Ub[G]) cur[G] = eb[lo];
+            }
+        }
+        const int64_t v1 = v0 + kRowsPerWarp < V ? v0 + kRowsPerWarp : V;
+        for (int64_t v = v0; v < v1; ++v) {
+            unsigned mask[NG];
+#pragma unroll
+            for (int G = 0; G < NG; ++G) mask[G] = __ballot_sync(0xffffffffu, cur[G].x == (int32_t)v);
+            double qacc[NG];
+#pragma unroll
+            for (int G = 0; G < NG; ++G) qacc[G] = 0.0;
+            for (int c = 0; c < nchunk; ++c) {
+                P acc[NVC][NP];
+#pragma unroll
+                for (int k = 0; k < NVC; ++k)
+#pragma unroll
+                    for (int e = 0; e < NP; ++e) acc[k][e] = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int G = 0; G < NG; ++G) {
+                    unsigned mk = mask[G];
+                    while (mk) {
+                        const int bb = __ffs(mk) - 1;
+                        mk &= mk - 1;
+                        const int64_t b = 32 * G + bb;
+                        const int start = __shfl_sync(0xffffffffu, cur[G].y, bb);
+                        const int len = __shfl_sync(0xffffffffu, cur[G].z, bb);
+                        const int t0 = __shfl_sync(0xffffffffu, cur[G].w, bb);
+                        P tmp[NVC][NP];
+#pragma unroll
+                        for (int q = 0; q < NVC; ++q)
+#pragma unroll
+                            for (int e = 0; e < NP; ++e) tmp[q][e] = make_float2(0.f, 0.f);
+                        for (int i = 0; i < len; ++i) {  // the run's tokens in token order
+                            const int64_t t = i == 0 ? t0 : w.perm[b * Tn + start + i];
+                            const T* row = g + (b * Tn + t) * D;
+#pragma unroll
+                            for (int q = 0; q < NVC; ++q) {
+                                const int vi = (c * NVC + q) * 32 + lane;
+                                if (vi < nvec) {
+                                    P x[NP];
+                                    unpack2<T>(__ldg(reinterpret_cast<const uint4*>(row) + vi), x);
+#pragma unroll
+                                    for (int e = 0; e < NP; ++e) {
+                                        tmp[q][e].x += x[e].x;
+                                        tmp[q][e].y += x[e].y;
+                                    }
+                                }
+                            }
+                        }
+                        double sq = 0.0;
+#pragma unroll
+                        for (int q = 0; q < NVC; ++q)
+#pragma unroll
+                            for (int e = 0; e < NP; ++e) {
+                                acc[q][e].x += tmp[q][e].x;
+                                acc[q][e].y += tmp[q][e].y;
+                                sq = fma((double)tmp[q][e].x, (double)tmp[q][e].x, sq);
+                                sq = fma((double)tmp[q][e].y, (double)tmp[q][e].y, sq);
+                            }
+                        sq = warp_sum(sq);
+                        if (lane == bb) qacc[G] += sq;
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < NVC; ++q) {
+                    const int vi = (c * NVC + q) * 32 + lane;
+                    if (vi < nvec) {
+                        float* dst = dW + v * D + (int64_t)vi * W;
+#pragma unroll
+                        for (int e = 0; e < NP; e += 2) {
+                            const float4 o = make_float4(acc[q][e].x, acc[q][e].y, acc[q][e + 1].x, acc[q][e + 1].y);
+                            reinterpret_cast<float4*>(dst)[e / 2] = o;
+                            qb = fma((double)o.x, (double)o.x, qb);
+                            qb = fma((double)o.y, (double)o.y, qb);
+                            qb = fma((double)o.z, (double)o.z, qb);
+                            qb = fma((double)o.w, (double)o.w, qb);
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int G = 0; G < NG; ++G) {
+                if ((mask[G] >> lane) & 1u) {  // consume the entry, fetch the next
+                    const int64_t b = 32 * G + lane;
+                    w.q[b * Tn + p[G]] = qacc[G];
+                    ++p[G];
+                    cur[G] = p[G] < Ub[G] ? w.ent[b * Tn + p[G]] : make_int4(-1, 0, 0, 0);
+                }
+            }
+        }
+    }
+    qb = warp_sum(qb);
+    if (lane == 0) s_red[threadIdx.x >> 5] = qb;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int k = 0; k < kEmbRowsThreads / 32; ++k) t += s_red[k];
+        w.qbig[blockIdx.x] = t;
+    }
+}
+
+__global__ void __launch_bounds__(256) emb_raw_kernel(int64_t B, int64_t Tn, EmbFastWs w, double* raw) {
+    const int lane = threadIdx.x & 31;
+    const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (b >= B) return;
+    const int U = w.U[b];
+    double s = 0.0;
+    for (int k = lane; k < U; k += 32) s += w.q[b * Tn + k];
+    s = warp_sum(s);
+    if (lane == 0) raw[b] = s;
+}
+
 int pow2_at_least(int64_t n) {
     int p = 1;
     while (p < n) p <<= 1;
@@ -233,8 +509,113 @@ EmbLayout emb_layout(int64_t B, int64_t Tn, int64_t V, int64_t D, int acc_bytes)
 
 bool embedding_shape_ok(int64_t T) { return T >= 1 && T <= kEmbMaxT; }
 
+
+namespace {
+
+struct EmbFastLayout {
+    size_t perm, ent, U, q, qbig, bad, raw, total;
+    int grid;
+};
+
+EmbFastLayout emb_fast_layout(int64_t B, int64_t Tn, int64_t V) {
+    EmbFastLayout l{};
+    const int sms = device_sm_count();
+    const int64_t blocks = (V + kRowsPerWarp - 1) / kRowsPerWarp;  // row blocks, one per warp
+    const int64_t wpc = kEmbRowsThreads / 32;
+    const int64_t grid = (blocks + wpc - 1) / wpc;
+    const int64_t cap = (int64_t)sms * 16;
+    l.grid = (int)(grid < cap ? (grid > 0 ? grid : 1) : cap);
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off = (off + bytes + 255) / 256 * 256;
+        return o;
+    };
+    l.perm = take((size_t)B * Tn * 4);
+    l.ent = take((size_t)B * Tn * 16);
+    l.U = take((size_t)B * 4);
+    l.q = take((size_t)B * Tn * 8);
+    l.qbig = take((size_t)l.grid * 8);
+    l.bad = take(4);
+    l.raw = take((size_t)B * 8);
+    l.total = off;
+    return l;
+}
+
+// the fast path: fp32 / bf16 rows made of whole 16-byte vectors (D a multiple
+// of the vector width), 16-byte aligned g and dW, B <= 256
+bool emb_fast_ok(int dt, int64_t B, int64_t D) {
+    static const bool forced_slow = [] {  // GNSB_EMB_IMPL=slow: the two-kernel path (A/B runs)
+        const char* e = std::getenv("GNSB_EMB_IMPL");
+        return e && e[0] == 's';
+    }();
+    const int W = dt == 1 ? 8 : 4;
+    return !forced_slow && dt != 2 && B >= 1 && B <= 32 * kEmbMaxGroups && D % W == 0 && D > 0;
+}
+
+}  // namespace
+
 size_t embedding_workspace(int64_t B, int64_t T, int64_t V, int64_t D, int dt) {
-    return emb_layout(B, T, V, D, dt == 2 ? 8 : 4).total;
+    // (the path also depends on pointer alignment: room for either)
+    const size_t slow = emb_layout(B, T, V, D, dt == 2 ? 8 : 4).total;
+    if (!emb_fast_ok(dt, B, D)) return slow;
+    const size_t fast = emb_fast_layout(B, T, V).total;
+    return fast > slow ? fast : slow;
+}
+
+template <typename T>
+cudaError_t emb_fast_run(const int32_t* ids, const void* g, void* dW, double* raw, double* sums, int64_t B,
+                         int64_t Tn, int64_t V, int64_t D, void* ws, int32_t* bad_flag_out, cudaStream_t st) {
+    const EmbFastLayout l = emb_fast_layout(B, Tn, V);
+    unsigned char* base = static_cast<unsigned char*>(ws);
+    EmbFastWs w{reinterpret_cast<int32_t*>(base + l.perm), reinterpret_cast<int4*>(base + l.ent),
+                reinterpret_cast<int32_t*>(base + l.U),    reinterpret_cast<double*>(base + l.q),
+                reinterpret_cast<double*>(base + l.qbig),  reinterpret_cast<int32_t*>(base + l.bad)};
+    if (raw == nullptr) raw = reinterpret_cast<double*>(base + l.raw);
+    cudaError_t e = cudaMemsetAsync(w.bad, 0, 4, st);
+    if (e != cudaSuccess) return e;
+    const int Tp = pow2_at_least(Tn);
+    const size_t smem = (size_t)Tp * 8;
+    e = ensure_smem_attr(reinterpret_cast<const void*>(emb_sort_kernel), smem);
+    if (e != cudaSuccess) return e;
+    emb_sort_kernel<<<(unsigned)B, kEmbSortThreads, smem, st>>>(ids, Tn, V, w, Tp);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    constexpr int W = Traits<T>::W;
+    const int64_t nvec = D / W;
+    const T* gp = static_cast<const T*>(g);
+    float* dWp = static_cast<float*>(dW);
+    const int ng = (int)((B + 31) / 32);
+    auto launch = [&](auto nvc) {
+        constexpr int NVC = decltype(nvc)::value;
+        if (ng <= 1)
+            emb_rows_kernel<T, NVC, 1><<<l.grid, kEmbRowsThreads, 0, st>>>(gp, B, Tn, V, D, w, dWp);
+        else if (ng <= 2)
+            emb_rows_kernel<T, NVC, 2><<<l.grid, kEmbRowsThreads, 0, st>>>(gp, B, Tn, V, D, w, dWp);
+        else if (ng <= 4)
+            emb_rows_kernel<T, NVC, 4><<<l.grid, kEmbRowsThreads, 0, st>>>(gp, B, Tn, V, D, w, dWp);
+        else
+            emb_rows_kernel<T, NVC, 8><<<l.grid, kEmbRowsThreads, 0, st>>>(gp, B, Tn, V, D, w, dWp);
+    };
+    if (nvec <= 32)
+        launch(std::integral_constant<int, 1>{});
+    else if (nvec <= 64)
+        launch(std::integral_constant<int, 2>{});
+    else if (nvec <= 96)
+        launch(std::integral_constant<int, 3>{});
+    else
+        launch(std::integral_constant<int, 4>{});
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    emb_raw_kernel<<<(unsigned)((B * 32 + 255) / 256), 256, 0, st>>>(B, Tn, w, raw);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    if (sums) {
+        e = launch_fold_rows(raw, 1, (int)B, nullptr, sums, 0, st);
+        if (e == cudaSuccess) e = launch_fold_rows(w.qbig, 1, l.grid, nullptr, sums, 2, st);
+    }
+    if (e == cudaSuccess && bad_flag_out) e = cudaMemcpyAsync(bad_flag_out, w.bad, 4, cudaMemcpyDeviceToDevice, st);
+    return e;
 }
 
 template <typename T>
@@ -271,6 +652,11 @@ cudaError_t emb_run(const int32_t* ids, const void* g, void* dW, double* raw, do
 
 cudaError_t launch_embedding_pe(int dt, const int32_t* ids, const void* g, void* dW, double* raw, double* sums,
                                 int64_t B, int64_t T, int64_t V, int64_t D, void* ws, int32_t* bad, cudaStream_t st) {
+    const bool aligned = (reinterpret_cast<uintptr_t>(g) & 15u) == 0 && (reinterpret_cast<uintptr_t>(dW) & 15u) == 0;
+    if (aligned && emb_fast_ok(dt, B, D)) {
+        if (dt == 0) return emb_fast_run<float>(ids, g, dW, raw, sums, B, T, V, D, ws, bad, st);
+        return emb_fast_run<__nv_bfloat16>(ids, g, dW, raw, sums, B, T, V, D, ws, bad, st);
+    }
     switch (dt) {
         case 0: return emb_run<float>(ids, g, dW, raw, sums, B, T, V, D, ws, bad, st);
         case 1: return emb_run<__nv_bfloat16>(ids, g, dW, raw, sums, B, T, V, D, ws, bad, st);
