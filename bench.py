@@ -413,6 +413,7 @@ def run_ours(args):
         extra["cfg3_linear"] = run_cfg3(m, lib, dev, torch, np)
         extra["cfg4_gns"] = run_cfg4(m, lib, dev, torch, np)
         extra["cfg5_g1"] = run_cfg5(m, lib, dev, torch, np)
+        extra["embedding"] = run_embedding(m, lib, dev, torch, np)
 
     traffic = load_traffic()
     line = {
@@ -582,6 +583,41 @@ def run_cfg4(m, lib, dev, torch, np):
            "gns_total": {"g2": float(groups[0, 0]), "s": float(groups[0, 1]), "b_simple_ema": float(groups[0, 2])},
            "launches_per_step": NL + 2, "stage2": "deferred: one grouped reduce for the 25 layers"}
     del cases
+    torch.cuda.empty_cache()
+    return out
+
+
+def run_embedding(m, lib, dev, torch, np):
+    """embedding-table gradient + per-example norms at a
+    GPT-2 embedding (B=32 T=1024 V=50257 D=768, bf16 gradient rows, fp32 dW).
+    Algorithmic bytes: g + ids in, dW out (every table row is written)."""
+    import ctypes
+
+    B, T_, V, D = 32, 1024, 50257, 768
+    gen = torch.Generator(device="cpu").manual_seed(0)
+    ids = torch.randint(0, V, (B, T_), generator=gen, dtype=torch.int32).to(dev)
+    g = torch.randn(B, T_, D, generator=gen).to(dev, torch.bfloat16)
+    n = ctypes.c_size_t()
+    lib.gnsb_embedding_pe_workspace_size(B, T_, V, D, 1, ctypes.byref(n))
+    ws = torch.zeros(n.value, dtype=torch.uint8, device=dev)
+    dW = torch.empty(V, D, device=dev)
+    raw = torch.empty(B, dtype=torch.float64, device=dev)
+    sums = torch.zeros(4, dtype=torch.float64, device=dev)
+
+    def fn():
+        sp = torch.cuda.current_stream(dev).cuda_stream
+        rc = lib.gnsb_embedding_pe(ids.data_ptr(), g.data_ptr(), dW.data_ptr(), raw.data_ptr(), sums.data_ptr(), B,
+                                   T_, V, D, 1, ws.data_ptr(), ws.numel(), None, sp)
+        if rc:
+            raise RuntimeError(lib.gnsb_last_error().decode())
+
+    ms = time_graph(fn, torch, np, dev, reps=10)
+    nbytes = B * T_ * D * 2 + B * T_ * 4 + V * D * 4
+    peak, _ = load_peaks()
+    out = {"workload": "embedding per-example norms B=32 T=1024 V=50257 D=768 bf16 rows, fp32 dW",
+           "us": ms * 1e3, "GBps": nbytes / (ms * 1e-3) / 1e9, "frac_of_measured_peak":
+           nbytes / (ms * 1e-3) / 1e9 / peak, "alg_bytes": nbytes}
+    del ids, g, ws, dW
     torch.cuda.empty_cache()
     return out
 

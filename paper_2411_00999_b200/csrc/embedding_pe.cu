@@ -206,8 +206,9 @@ __global__ void __launch_bounds__(kEmbThreads) emb_table_kernel(int64_t B, int64
 //     ent[b][k] = {id, first position in perm, length, first token}, plus the
 //     run count U[b] (parallel run detection by a block scan).
 //   * emb_rows_kernel: one warp per block of kRowsPerWarp table rows.  Lane j
-//     of group G tracks example 32G + j: a lower_bound into its sorted entry
-//     list once per block, then it holds its next entry in registers (the
+//     of group G tracks example 32G + j: its first entry at or after the
+//     block comes from a per-(example, block) table the sort kernel writes,
+//     then it holds its next entry in registers (the
 //     following one is loaded as soon as a row consumes it).  For row v the
 //     warp ballots the matching examples and walks them in example order; for
 //     each it sums the run's token rows (token order, lanes over 16-byte
@@ -215,10 +216,10 @@ __global__ void __launch_bounds__(kEmbThreads) emb_table_kernel(int64_t B, int64
 //     that to dW[v] and reduces ||dE_b[v]||^2 into q[b][k].  g is read once
 //     and dW written once, 16 bytes per lane per vector.
 //   * emb_raw_kernel: raw_b = sum_k q[b][k] (one warp per example, fixed-order
-//     tree).
+//     tree); the scalar sums by fold_rows_kernel.
 // dW matches the original path bit for bit (same per-example Acc sums, added
 // in example order); raw_b differs in summation order only.
-constexpr int kEmbSortThreads = 512;
+constexpr int kEmbSortThreads = 1024;
 constexpr int kRowsPerWarp = 8;
 constexpr int kEmbRowsThreads = 256;
 constexpr int kEmbMaxGroups = 8;  // examples handled by the fast path: B <= 32 * 8
@@ -230,6 +231,8 @@ struct EmbFastWs {
     double* q;      // [B][Tn]
     double* qbig;   // [rows-kernel CTAs]
     int32_t* bad;
+    int32_t* blk;      // [B][nblk + 1]: first entry of example b with id >= j * kRowsPerWarp
+    int64_t nblk;      // row blocks: ceil(V / kRowsPerWarp)
 };
 
 template <int NT>
@@ -280,8 +283,11 @@ __global__ void __launch_bounds__(kEmbSortThreads) emb_sort_kernel(const int32_t
         keys[i] = k;
     }
     __syncthreads();
+    // bitonic sort, ascending (id, t): strides >= 32 through shared memory,
+    // strides < 32 inside the warp with shuffles (Tp is a multiple of 32)
     for (int size = 2; size <= Tp; size <<= 1) {
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        int stride = size >> 1;
+        for (; stride >= 32; stride >>= 1) {
             for (int i = tid; i < Tp; i += blockDim.x) {
                 const int j = i ^ stride;
                 if (j > i) {
@@ -295,6 +301,19 @@ __global__ void __launch_bounds__(kEmbSortThreads) emb_sort_kernel(const int32_t
             }
             __syncthreads();
         }
+        for (int i0 = 0; i0 < Tp; i0 += blockDim.x) {
+            if (i0 + (tid & ~31) >= Tp) break;  // warp-uniform
+            const int i = i0 + tid;
+            uint64_t v = keys[i];
+            const bool up = (i & size) == 0;
+            for (int s2 = stride; s2 > 0; s2 >>= 1) {
+                const uint64_t o = __shfl_xor_sync(0xffffffffu, v, s2);
+                const bool keep_min = ((i & s2) == 0) == up;  // the lower element keeps the min when ascending
+                v = keep_min ? (o < v ? o : v) : (o > v ? o : v);
+            }
+            keys[i] = v;
+        }
+        __syncthreads();
     }
     // run heads: a valid key whose id differs from its predecessor's.  Each
     // thread scans a contiguous chunk; a block scan numbers the runs.
@@ -314,16 +333,25 @@ __global__ void __launch_bounds__(kEmbSortThreads) emb_sort_kernel(const int32_t
     const int nvalid = s_nvalid;
     int32_t* perm = w.perm + b * Tn;
     int4* ent = w.ent + b * Tn;
+    int32_t* blk = w.blk + b * (w.nblk + 1);
     for (int i = i0; i < i1; ++i) {
         if (!valid(i)) break;
         perm[i] = (int32_t)(uint32_t)(keys[i] & 0xffffffffu);
         if (head(i)) {
+            const uint32_t id = (uint32_t)(keys[i] >> 32);
             int e = i + 1;
-            while (e < nvalid && (uint32_t)(keys[e] >> 32) == (uint32_t)(keys[i] >> 32)) ++e;
-            ent[r] = make_int4((int)(keys[i] >> 32), i, e - i, (int)(uint32_t)(keys[i] & 0xffffffffu));
+            while (e < nvalid && (uint32_t)(keys[e] >> 32) == id) ++e;
+            ent[r] = make_int4((int)id, i, e - i, (int)(uint32_t)(keys[i] & 0xffffffffu));
+            // row blocks whose first row lies in (previous id, id] start at entry r
+            const int64_t j_lo = r == 0 ? 0 : (int64_t)((uint32_t)(keys[i - 1] >> 32) / kRowsPerWarp) + 1;
+            const int64_t j_hi = (int64_t)(id / kRowsPerWarp);
+            for (int64_t j = j_lo; j <= j_hi; ++j) blk[j] = r;
             ++r;
         }
     }
+    // blocks after the last id start past the end
+    const int64_t j_tail = nvalid > 0 ? (int64_t)((uint32_t)(keys[nvalid - 1] >> 32) / kRowsPerWarp) + 1 : 0;
+    for (int64_t j = j_tail + tid; j <= w.nblk; j += blockDim.x) blk[j] = total;
     if (tid == 0) w.U[b] = total;
 }
 
@@ -349,17 +377,10 @@ __global__ void __launch_bounds__(kEmbRowsThreads) emb_rows_kernel(const T* g, i
             Ub[G] = 0;
             cur[G] = make_int4(-1, 0, 0, 0);
             const int64_t b = 32 * G + lane;
-            if (b < B) {  // lower_bound(ids of example b, v0)
-                const int4* eb = w.ent + b * Tn;
-                int lo = 0, hi = w.U[b];
-                Ub[G] = hi;
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (eb[mid].x < (int32_t)v0) lo = mid + 1;
-                    else hi = mid;
-                }
-                p[G] = lo;
-                if (lo < Ub[G]) cur[G] = eb[lo];
+            if (b < B) {  // first entry with id >= v0 (the sort kernel's block table)
+                Ub[G] = w.U[b];
+                p[G] = w.blk[b * (w.nblk + 1) + v0 / kRowsPerWarp];
+                if (p[G] < Ub[G]) cur[G] = w.ent[b * Tn + p[G]];
             }
         }
         const int64_t v1 = v0 + kRowsPerWarp < V ? v0 + kRowsPerWarp : V;
@@ -460,6 +481,7 @@ __global__ void __launch_bounds__(kEmbRowsThreads) emb_rows_kernel(const T* g, i
     }
 }
 
+// raw_b = sum_k q[b][k]: one warp per example, fixed-order tree
 __global__ void __launch_bounds__(256) emb_raw_kernel(int64_t B, int64_t Tn, EmbFastWs w, double* raw) {
     const int lane = threadIdx.x & 31;
     const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -513,8 +535,9 @@ bool embedding_shape_ok(int64_t T) { return T >= 1 && T <= kEmbMaxT; }
 namespace {
 
 struct EmbFastLayout {
-    size_t perm, ent, U, q, qbig, bad, raw, total;
+    size_t perm, ent, U, q, qbig, bad, raw, blk, total;
     int grid;
+    int64_t nblk;
 };
 
 EmbFastLayout emb_fast_layout(int64_t B, int64_t Tn, int64_t V) {
@@ -538,6 +561,8 @@ EmbFastLayout emb_fast_layout(int64_t B, int64_t Tn, int64_t V) {
     l.qbig = take((size_t)l.grid * 8);
     l.bad = take(4);
     l.raw = take((size_t)B * 8);
+    l.nblk = blocks;
+    l.blk = take((size_t)B * (blocks + 1) * 4);
     l.total = off;
     return l;
 }
@@ -570,11 +595,12 @@ cudaError_t emb_fast_run(const int32_t* ids, const void* g, void* dW, double* ra
     unsigned char* base = static_cast<unsigned char*>(ws);
     EmbFastWs w{reinterpret_cast<int32_t*>(base + l.perm), reinterpret_cast<int4*>(base + l.ent),
                 reinterpret_cast<int32_t*>(base + l.U),    reinterpret_cast<double*>(base + l.q),
-                reinterpret_cast<double*>(base + l.qbig),  reinterpret_cast<int32_t*>(base + l.bad)};
+                reinterpret_cast<double*>(base + l.qbig),  reinterpret_cast<int32_t*>(base + l.bad),
+                reinterpret_cast<int32_t*>(base + l.blk),   l.nblk};
     if (raw == nullptr) raw = reinterpret_cast<double*>(base + l.raw);
     cudaError_t e = cudaMemsetAsync(w.bad, 0, 4, st);
     if (e != cudaSuccess) return e;
-    const int Tp = pow2_at_least(Tn);
+    const int Tp = pow2_at_least(Tn < 32 ? 32 : Tn);  // whole warps in the shuffle stages
     const size_t smem = (size_t)Tp * 8;
     e = ensure_smem_attr(reinterpret_cast<const void*>(emb_sort_kernel), smem);
     if (e != cudaSuccess) return e;
