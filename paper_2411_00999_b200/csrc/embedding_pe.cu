@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(kEmbSortThreads) emb_sort_kernel(const int32_t
 }
 
 template <typename T, int NVC, int NG>
-__global__ void __launch_bounds__(kEmbRowsThreads) emb_rows_kernel(const T* g, int64_t B, int64_t Tn, int64_t V,
+__global__ void __launch_bounds__(kEmbRowsThreads, 3) emb_rows_kernel(const T* g, int64_t B, int64_t Tn, int64_t V,
                                                                    int64_t D, EmbFastWs w, float* dW) {
     constexpr int W = Traits<T>::W;
     constexpr int NP = W / 2;
