@@ -2,7 +2,7 @@
 # A/B of an environment switch on the per-width steady numbers:  bash scripts/gpu_ab.sh VAR "v1 v2 ..." [d-list]
 VAR=$1; VALS=$2; DL=${3:-768,1024,2048,4096,8192}
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_ln_gpu.py -x -q 2>&1 | tail -2
+[ -z "$NO_TEST" ] && timeout 600 python -m pytest tests/test_ln_gpu.py -x -q 2>&1 | tail -2
 show() { python -c "
 import json
 d=json.loads([l for l in open('$1') if l.startswith('{')][-1])
