@@ -17,4 +17,4 @@ ls -la gpurun_out/final_*
 # memcheck over the kernels changed since the last sanitizer pass (CTA-pair wgrad, warp forward)
 timeout 900 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_linear_gpu.py -q -k "weight_grad_form_matches" > gpurun_out/final_memcheck_lin.log 2>&1
 timeout 900 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_ln_gpu.py -q -k "forward or edge or oracle" > gpurun_out/final_memcheck_ln.log 2>&1
-tail -3 gpurun_out/final_memcheck_*.log
+tail -n 3 gpurun_out/final_memcheck_*.log
