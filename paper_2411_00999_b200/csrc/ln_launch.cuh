@@ -341,7 +341,7 @@ R dispatch_bwd(int64_t D, const char** why, R bad, A&&... args) {
     // and xhat/h kept in registers win at every width
     if (nv <= 32) return Op<LnBwdCfg<T, 1, 1, 8, 2, true>>::call(args...);
     if (nv <= 64) return Op<LnBwdCfg<T, 2, 1, 8, 1, true>>::call(args...);
-    if (nv <= 96) return Op<LnBwdCfg<T, 3, 1, 5, 2, true>>::call(args...);
+    if (nv <= 96) return Op<LnBwdCfg<T, 3, 1, 5, 2, true, -1, 1, true>>::call(args...);  // parked first example
     if (nv <= 128) return Op<LnBwdCfg<T, 4, 1, 4, 2, true>>::call(args...);
     if (nv <= 256) return Op<LnBwdCfg<T, 8, 1, 2, 2, true>>::call(args...);
     if (nv <= 512) return Op<LnBwdCfg<T, 8, 2, 1, 2, true, 1>>::call(args...);

@@ -416,6 +416,8 @@ def test_deferred_reduce_limits(cuda):
         (torch.float32, 3, 20, 256, 1, True),
         (torch.float64, 3, 16, 96, 0, False),
         (torch.bfloat16, 2, 7, 768, 0, False),
+        (torch.bfloat16, 300, 2, 768, 0, False),  # CTAs spanning 3+ examples (parked first example + L2 middle)
+        (torch.bfloat16, 5, 700, 768, 0, False),  # CTAs inside one example and across one boundary
     ],
 )
 def test_row_pass_edge_cases_match_oracle(orc, cuda, dt, B, T, D, offset, use_xhat):
