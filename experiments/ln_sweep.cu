@@ -75,9 +75,17 @@ using bf = __nv_bfloat16;
     X(63, 2, 4, 8, 1, true, 1) \
     X(64, 2, 4, 4, 2, true, 1) \
     X(65, 1, 4, 12, 1, true, 1) \
+    X(66, 4, 1, 4, 2, true, 1, 1, true) \
+    X(67, 4, 1, 4, 1, true, 1, 1, true) \
+    X(68, 4, 1, 4, 1, true, 1) \
+    X(69, 8, 1, 2, 2, true, 1, 1, true) \
+    X(70, 8, 1, 2, 1, true, 1, 1, true) \
+    X(71, 8, 1, 2, 1, true, 1) \
+    X(72, 3, 1, 5, 2, true, 1, 1, true) \
+    X(73, 4, 1, 3, 2, true, 1, 1, true) \
 
 extern "C" {
-int sweep_n() { return 66; }
+int sweep_n() { return 74; }
 
 int sweep_desc(int id, int* out) {
 #define DESC(i, gw, vpt, g, rpg, prod, keep, ...) \
