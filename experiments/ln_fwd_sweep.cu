@@ -45,7 +45,7 @@ extern "C" int fwd_warp_run(int vpt, int minb, int pf, int bps, const void* x, c
     return -2;
 }
 
-template <int GW, int VPT, int G, bool GBS>
+template <int GW, int VPT, int G, bool GBS, int CPS = 1>
 static int ring_launch(const LnFwdArgs& a0, int smax, cudaStream_t st) {
     using RC = LnFwdRingCfg<__nv_bfloat16, GW, VPT, G>;
     LnFwdArgs a = a0;
@@ -55,7 +55,7 @@ static int ring_launch(const LnFwdArgs& a0, int smax, cudaStream_t st) {
     int optin = 0, sms = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const size_t budget = (size_t)optin - 1024;
+    const size_t budget = CPS == 1 ? (size_t)optin - 1024 : (size_t)(228 * 1024) / CPS - 2048;
     int S = 0;
     for (int s2 = smax; s2 >= 2; --s2)
         if (RC::smem_bytes(s2, a.Dp, a.D) <= budget) {
@@ -64,9 +64,9 @@ static int ring_launch(const LnFwdArgs& a0, int smax, cudaStream_t st) {
         }
     if (!S) return -3;
     const size_t smem = RC::smem_bytes(S, a.Dp, a.D);
-    auto k = ln_fwd_ring_kernel<__nv_bfloat16, GW, VPT, G, GBS>;
+    auto k = ln_fwd_ring_kernel<__nv_bfloat16, GW, VPT, G, GBS, CPS>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) return -4;
-    k<<<sms, RC::kThreads, smem, st>>>(a, S);
+    k<<<sms * CPS, RC::kThreads, smem, st>>>(a, S);
     return (int)cudaGetLastError();
 }
 
@@ -99,6 +99,13 @@ extern "C" int fwd_ring_run(int cfg, int smax, const void* x, const void* gamma,
         case 13: return ring_launch<8, 4, 2, false>(a, smax, st);
         case 14: return ring_launch<16, 2, 1, false>(a, smax, st);
         case 15: return ring_launch<4, 8, 3, true>(a, smax, st);
+        // two CTAs per SM
+        case 16: return ring_launch<16, 2, 1, true, 2>(a, smax, st);
+        case 17: return ring_launch<16, 2, 1, false, 2>(a, smax, st);
+        case 18: return ring_launch<8, 4, 1, true, 2>(a, smax, st);
+        case 6: return ring_launch<8, 2, 2, true, 2>(a, smax, st);
+        case 7: return ring_launch<8, 2, 1, true, 2>(a, smax, st);
+        case 8: return ring_launch<16, 1, 1, false, 2>(a, smax, st);
         default: return -2;
     }
 }

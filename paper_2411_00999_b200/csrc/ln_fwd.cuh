@@ -189,8 +189,8 @@ struct LnFwdRingCfg {
 
 // GBS: gamma/beta read from shared memory per row instead of held in registers
 // (wide per-thread slices)
-template <typename T, int GW, int VPT, int G, bool GBS = false>
-__global__ void __launch_bounds__(LnFwdRingCfg<T, GW, VPT, G>::kThreads, 1) ln_fwd_ring_kernel(LnFwdArgs a, int S) {
+template <typename T, int GW, int VPT, int G, bool GBS = false, int MINB = 1>
+__global__ void __launch_bounds__(LnFwdRingCfg<T, GW, VPT, G>::kThreads, MINB) ln_fwd_ring_kernel(LnFwdArgs a, int S) {
     using C = LnFwdRingCfg<T, GW, VPT, G>;
     using Acc = typename Traits<T>::Acc;
     constexpr int W = Traits<T>::W;
