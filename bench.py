@@ -759,9 +759,17 @@ def cpu_baseline(args):
         nbytes += alg_bytes(b_sample, T, D)
         if time.perf_counter() - t0 > 60:
             break
+    # the reference is single-threaded by design: one example per
+    # width on one core as well
+    t1, n1 = 0.0, 0
+    for D in args.d_list:
+        t1 += ref_layer_sample(ref, orc, D, 1, 1)
+        n1 += alg_bytes(1, T, D)
     return {"value": nbytes / tsum / 1e9, "unit": "GB/s", "cores": threads, "kind": "reference",
+            "value_1core": n1 / t1 / 1e9,
             "sample": f"{b_sample} examples x T={T} per D (one pass of the sweep), reference gnstk fp64 "
-                      f"layernorm_backward_simultaneous over {threads} threads; bytes by the bf16 workload formula"}
+                      f"layernorm_backward_simultaneous over {threads} threads; bytes by the bf16 workload formula; "
+                      f"value_1core: 1 example per D on one thread"}
 
 
 def load_traffic():
