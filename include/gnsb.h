@@ -182,14 +182,31 @@ gnsb_status gnsb_embedding_pe(const int32_t* ids, const void* g, void* dW, doubl
 gnsb_status gnsb_sqnorm(const void* v, int64_t n, gnsb_dtype dt, double* out, void* stream);
 
 /* ------------------------------------------------------------------------
- * Batch-sharded exchange: the step's one collective.
- * grads   : device bucket of every layer's [p0 | p1] batch-summed gradients
- *           (layer l holds 2 * widths_host[l] values of grad_dt, fp32 or fp64)
- * records : device [n_layers][4] fp64 norm records, as gnsb_ln_bwd writes them
- * Sums both buckets over `nccl_comm` (an ncclComm_t; NULL = a single rank)
- * with NCCL on `stream`, then re-forms records[l][2..3] = ||p0||^2, ||p1||^2
- * of the REDUCED gradients (local squared norms do not add).  The GNS step then
- * uses the global batch (gnsb_gns_step with B = B_global).  1..256 layers.
+ * Batch-sharded exchange: the step's ONE collective.
+ * No reference equivalent (the reference has no distributed runtime,
+ * SPEC.md:9); the arithmetic after the sum is Trainer::step's packaging
+ * (proj/src/trainer.cpp:363-378) with the global batch.
+ *
+ * widths2 : host [2 * n_layers]: (p0, p1) parameter widths per layer, e.g.
+ *           (D, D) for a LayerNorm, (K*L, L) for a linear layer, (K*L, 0)
+ *           for a bias-less one.  1..256 layers.
+ * grads   : device bucket, layer after layer [p0 | p1], fp32 or fp64
+ * records : device [n_layers][4] fp64 norm records as gnsb_ln_bwd /
+ *           gnsb_linear_pe_norms / gnsb_embedding_pe write them
+ *           {sum_b raw(p0), sum_b raw(p1), ||p0||^2, ||p1||^2}; NULL = gradients
+ *           only (the plain backward's exchange)
+ * ws      : device workspace of gnsb_exchange_workspace_size bytes (zeroed once;
+ *           every call leaves it reusable)
+ *
+ * gnsb_allreduce_buckets = pack (records + gradients promoted to ONE fp64
+ * buffer) -> one ncclAllReduce(sum) on `stream` over `nccl_comm` (an
+ * ncclComm_t; NULL = a single rank: no collective) -> unpack: gradients back in
+ * their dtype, records[l][0..1] summed, records[l][2..3] re-formed as the fp64
+ * squared norms of the REDUCED gradients (local squared norms do not add).
+ * Stream-ordered, no host synchronisation: capturable in a CUDA graph.  The GNS
+ * step then uses the global batch (gnsb_gns_step with B = B_global).
+ * gnsb_exchange_pack / _unpack are the two halves, for callers that run the
+ * sum themselves (e.g. a torch.distributed process group).
  * libnccl.so.2 is opened at run time; the three helpers let a C/C++ caller
  * create a communicator with the same NCCL instance.
  */
@@ -197,8 +214,13 @@ int32_t gnsb_nccl_available(void);
 gnsb_status gnsb_nccl_get_unique_id(void* id128);
 gnsb_status gnsb_nccl_comm_init_rank(void** comm, int32_t nranks, const void* id128, int32_t rank);
 gnsb_status gnsb_nccl_comm_destroy(void* comm);
-gnsb_status gnsb_allreduce_buckets(void* grads, gnsb_dtype grad_dt, const int64_t* widths_host, int32_t n_layers,
-                                   double* records, int32_t with_records, void* nccl_comm, void* stream);
+gnsb_status gnsb_exchange_workspace_size(const int64_t* widths2, int32_t n_layers, size_t* bytes);
+gnsb_status gnsb_exchange_pack(const void* grads, gnsb_dtype grad_dt, const int64_t* widths2, int32_t n_layers,
+                               const double* records, void* ws, size_t ws_bytes, void* stream);
+gnsb_status gnsb_exchange_unpack(void* grads, gnsb_dtype grad_dt, const int64_t* widths2, int32_t n_layers,
+                                 double* records, void* ws, size_t ws_bytes, void* stream);
+gnsb_status gnsb_allreduce_buckets(void* grads, gnsb_dtype grad_dt, const int64_t* widths2, int32_t n_layers,
+                                   double* records, void* ws, size_t ws_bytes, void* nccl_comm, void* stream);
 
 /* ------------------------------------------------------------------------
  * GNS estimator (host functions).  Replace proj/include/gnstk/gns.hpp:16-74 /

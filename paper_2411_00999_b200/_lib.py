@@ -87,7 +87,11 @@ _SIGS = {
     "gnsb_nccl_get_unique_id": (c_i32, [c_vp]),
     "gnsb_nccl_comm_init_rank": (c_i32, [ctypes.POINTER(c_vp), c_i32, c_vp, c_i32]),
     "gnsb_nccl_comm_destroy": (c_i32, [c_vp]),
-    "gnsb_allreduce_buckets": (c_i32, [c_vp, c_i32, ctypes.POINTER(c_i64), c_i32, c_vp, c_i32, c_vp, c_vp]),
+    "gnsb_exchange_workspace_size": (c_i32, [ctypes.POINTER(c_i64), c_i32, c_szp]),
+    "gnsb_exchange_pack": (c_i32, [c_vp, c_i32, ctypes.POINTER(c_i64), c_i32, c_vp, c_vp, ctypes.c_size_t, c_vp]),
+    "gnsb_exchange_unpack": (c_i32, [c_vp, c_i32, ctypes.POINTER(c_i64), c_i32, c_vp, c_vp, ctypes.c_size_t, c_vp]),
+    "gnsb_allreduce_buckets": (c_i32, [c_vp, c_i32, ctypes.POINTER(c_i64), c_i32, c_vp, c_vp, ctypes.c_size_t, c_vp,
+                                       c_vp]),
     "gnsb_linear_dx": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i32, c_vp]),
     "gnsb_estimate_g2": (c_i32, [ctypes.POINTER(GradStats), c_dp]),
     "gnsb_estimate_s": (c_i32, [ctypes.POINTER(GradStats), c_dp]),

@@ -200,8 +200,9 @@ __global__ void gns_step_kernel(const __grid_constant__ GnsStepArgs a) {
             any = true;
         }
         double* o = a.out_groups + 4 * grp;
-        if (!any) {
-            o[0] = o[1] = o[2] = o[3] = CUDART_NAN;
+        if (!any) {  // empty selection (the reference's aggregate throws): no estimate, not defined
+            o[0] = o[1] = o[2] = CUDART_NAN;
+            o[3] = 0.0;
             continue;
         }
         const double g2 = (bb * big - bs * small) / (bb - bs);

@@ -52,6 +52,7 @@ struct LnBwdArgs {
     int Dp;             // smem row stride in elements (D rounded up to the vector width)
     int stages;         // ring depth
     int aligned;        // 1: rows are 16-byte aligned -> TMA producer
+    int gamma16;        // 1: gamma is 16-byte aligned and D*sizeof(Acc) % 16 == 0 -> vector staging
     void* partial;      // [(grid + B) * G][2][Dp] Acc; slot (cta + example, 0) holds the CTA's fold
     unsigned long long* trace;  // optional [grid][6] globaltimer stamps (profiling only)
 };
@@ -254,7 +255,7 @@ __global__ void __launch_bounds__(C::kBoundThreads, C::kCps) ln_bwd_kernel(LnBwd
 
     {  // gamma -> shared memory (while the first stages are in flight)
         const Acc* gg = static_cast<const Acc*>(a.gamma);
-        if (a.aligned && (D * (int64_t)sizeof(Acc)) % 16 == 0) {
+        if (a.gamma16) {
             constexpr int E = 16 / sizeof(Acc);
             for (int i = threadIdx.x; i < Dp / E; i += blockDim.x)
                 *reinterpret_cast<uint4*>(gam_s + i * E) = __ldg(reinterpret_cast<const uint4*>(gg) + i);

@@ -170,6 +170,8 @@ struct BwdOp {
         a.Dp = p.Dp;
         a.stages = p.stages;
         a.aligned = ((c.D * (int64_t)sizeof(T)) % 16 == 0) && ptr16(c.x) && ptr16(c.dy) && (c.dx == nullptr || ptr16(c.dx));
+        // gamma may be a view into a flat parameter buffer at any offset
+        a.gamma16 = ((c.D * (int64_t)sizeof(typename Traits<T>::Acc)) % 16 == 0) && ptr16(c.gamma);
         a.partial = static_cast<unsigned char*>(c.ws) + p.off_partial;
         a.trace = c.trace;
 

@@ -152,4 +152,6 @@ class GnsTracker:
             B = m.batch_size if B is None else B
             if m.batch_size != B:
                 raise ValueError("gns: layers disagree on the batch size")
+        for m in self.modules:  # consumed: a layer without a backward next step must not reuse it
+            m.norm_record = None
         return self.acc.step(self.records, B)

@@ -172,7 +172,9 @@ class Trainer:
         self.data = MarkovDataset(cfg.vocab, cfg.seed)
         self.model = ToyModelPE(cfg.vocab, cfg.model_dim, cfg.hidden_multiplier, cfg.n_blocks, seed=cfg.seed,
                                 device=self.device, dtype=dtype, init="reference")
-        self.layers = self.model.instrumented_layers()
+        # std::map<LayerKey> order (gns.hpp:42-55): the aggregate sums g_big /
+        # g_small over layers in (name, type) order, as gns.cpp:71-89 does
+        self.layers = sorted(self.model.instrumented_layers(), key=lambda nm: (nm[0], _TYPE_ORDER[nm[1].layer_type]))
         self.tracker = GnsTracker([m for _, m in self.layers], alpha=cfg.ema_alpha)
         self.step_index = 0
         self.tokens = 0
@@ -238,7 +240,7 @@ class Trainer:
         for i, name in enumerate(("total", "embedding", "linear", "layernorm")):
             setattr(log, name, GroupLog(g[i][0], g[i][1], g[i][2], bool(g[i][3] != 0.0)))
         rows = [PerLayerLog(n, m.layer_type, pl[i][0], pl[i][1]) for i, (n, m) in enumerate(self.layers)]
-        log.layers = sorted(rows, key=lambda r: (r.name, _TYPE_ORDER[r.type]))  # std::map<LayerKey> order
+        log.layers = rows  # already in std::map<LayerKey> order
         self._apply_update(self.current_lr())
         self.tokens += b * t
         self.step_index += 1

@@ -465,3 +465,26 @@ def test_row_pass_edge_cases_match_oracle(orc, cuda, dt, B, T, D, offset, use_xh
         assert close(gr.per_example_sqnorms_raw["beta"].cpu().numpy(), ref["raw_beta"], nt)
     assert torch.equal(r.input_grad, dxd)
     assert torch.equal(r.grads.weight_grads["gamma"], rd.weight_grads["gamma"])
+
+
+@pytest.mark.parametrize("dt,D", [(torch.bfloat16, 1024), (torch.float32, 768)])
+def test_gamma_view_at_unaligned_offset(orc, cuda, dt, D):
+    """gamma as a view into a flat parameter buffer at a 4-byte (not 16-byte)
+    offset: the kernel stages it element-wise instead of faulting on a uint4 load
+    (ln_bwd.cuh gamma staging)."""
+    m = _mod()
+    x, dy, gamma, beta = m.synth_ln(4, 64, D, dt, cuda, stream0=21)
+    flat = torch.empty(D + 1, dtype=torch.float32, device=cuda)
+    gv = flat[1:]
+    gv.copy_(gamma)
+    assert gv.data_ptr() % 16 != 0
+    layer = m.LayerNormLayer(gv, beta)
+    f = m.layernorm_forward(layer, x)
+    r = m.layernorm_backward_simultaneous(layer, f.cache, dy)
+    ref = _oracle_on_device_stats(orc, x, dy, gamma, f.cache.mean, f.cache.inv_std)
+    torch.cuda.synchronize()
+    dxt = BF16_DX if dt == torch.bfloat16 else F32_TOL
+    assert _close_inf(r.input_grad.double().cpu().numpy(), ref["dx"], dxt)
+    assert close(r.grads.per_example_sqnorms_raw["gamma"].cpu().numpy(), ref["raw_gamma"], NORM_TOL)
+    base = m.layernorm_backward_simultaneous(m.LayerNormLayer(gamma, beta), f.cache, dy)
+    assert torch.equal(base.input_grad, r.input_grad)

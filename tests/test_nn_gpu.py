@@ -87,8 +87,7 @@ def test_gns_tracker_over_two_layers(cuda):
     groups, layers = tr.step()
     torch.cuda.synchronize()
     big = small = 0.0
-    for m in (l1, l2):
-        r = m.norm_record.cpu().numpy()
+    for r in tr.records.cpu().numpy():
         big += r[3] + r[2]
         small += r[1] * B + r[0] * B
     st = gns.GradStats(big, small, B, 1, B)
@@ -96,6 +95,11 @@ def test_gns_tracker_over_two_layers(cuda):
     assert close(g[0, 0], gns.estimate_g2(st), 1e-10)
     assert close(g[0, 1], gns.estimate_s(st), 1e-10)
     assert close(g[3, :2], g[0, :2], 0.0)
+    # records are consumed: a step whose backward skipped a tracked layer fails loudly
+    assert l1.norm_record is None and l2.norm_record is None
+    l1(x).sum().backward()
+    with pytest.raises(RuntimeError, match="no norm record"):
+        tr.step()
 
 
 def test_layernorm_pe_rejects_cpu_and_bad_shapes():

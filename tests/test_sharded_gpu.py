@@ -104,46 +104,61 @@ def test_bench_multirank_path_runs(cuda):
     assert rec["n_gpus"] == 2 and rec["value"] > 0 and rec["config"]["global_batch"] == 64
 
 
-def test_c_abi_allreduce_buckets_single_rank(cuda):
+@pytest.mark.parametrize("gdt", [torch.float32, torch.float64])
+def test_c_abi_allreduce_buckets_single_rank(cuda, gdt):
     """gnsb_allreduce_buckets (the C ABI's exchange step): with no communicator
-    and with a one-rank NCCL communicator the buckets are unchanged and
-    records[l][2..3] are re-formed as ||p0||^2, ||p1||^2 of the gradient bucket."""
+    and with a one-rank NCCL communicator the gradients are unchanged (an
+    fp64 round trip), records[l][0..1] too, and records[l][2..3] are
+    re-formed as ||p0||^2, ||p1||^2 of the gradient bucket.  Layers of
+    unequal (p0, p1) widths: a LayerNorm (768, 768), a linear layer (K*L, L)
+    with K*L spanning several unpack chunks, a bias-less layer (n, 0)."""
     import ctypes
 
     from paper_2411_00999_b200 import _lib
+    from paper_2411_00999_b200.sharded import GradBuckets
 
     lib = _lib.lib()
-    widths = [768, 5, 1024]
-    n = 2 * sum(widths)
+    pairs = [(768, 768), (5, 5), (256 * 300, 300), (1024, 0), (40000, 1)]
+    n = sum(a + b for a, b in pairs)
     gen = torch.Generator(device="cpu").manual_seed(3)
-    grads = torch.randn(n, generator=gen).to(cuda)
-    records = torch.zeros(len(widths), 4, dtype=torch.float64, device=cuda)
-    records[:, :2] = torch.tensor([[1.0, 2.0], [3.0, 4.0], [5.0, 6.0]], dtype=torch.float64)
-    w = (ctypes.c_int64 * len(widths))(*widths)
+    bk = GradBuckets(pairs, cuda, grad_dtype=gdt)
+    bk.grads.copy_(torch.randn(n, generator=gen, dtype=torch.float64))
+    bk.records[:, :2] = torch.arange(2 * len(pairs), dtype=torch.float64).reshape(-1, 2)
     expect = []
-    off = 0
-    for wd in widths:
-        a = grads[off:off + wd].double()
-        b = grads[off + wd:off + 2 * wd].double()
+    for l in range(len(pairs)):
+        a, b = (v.double() for v in bk.grad(l))
         expect.append([float((a * a).sum()), float((b * b).sum())])
-        off += 2 * wd
-    sp = torch.cuda.current_stream().cuda_stream
     comms = [None]
     if lib.gnsb_nccl_available():
+        class _C:
+            pass
         uid = ctypes.create_string_buffer(128)
         _lib.check(lib.gnsb_nccl_get_unique_id(uid))
-        comm = ctypes.c_void_p()
-        _lib.check(lib.gnsb_nccl_comm_init_rank(ctypes.byref(comm), 1, uid, 0))
+        comm = _C()
+        comm.handle = ctypes.c_void_p()
+        _lib.check(lib.gnsb_nccl_comm_init_rank(ctypes.byref(comm.handle), 1, uid, 0))
         comms.append(comm)
     for comm in comms:
-        g0, r0 = grads.clone(), records[:, :2].clone()
-        _lib.check(lib.gnsb_allreduce_buckets(grads.data_ptr(), 0, w, len(widths), records.data_ptr(), 1,
-                                              comm, sp))
-        torch.cuda.synchronize()
-        assert torch.equal(grads, g0) and torch.equal(records[:, :2], r0)
-        assert close(records[:, 2:].cpu().numpy(), np.array(expect), 1e-12)
-        records[:, 2:] = 0
+        for rec in (True, False):
+            g0, r0 = bk.grads.clone(), bk.records[:, :2].clone()
+            bk.records[:, 2:] = -1.0
+            if comm is None:
+                bk.reduce(records=rec)
+            else:
+                bk.allreduce_nccl(comm, records=rec)
+            torch.cuda.synchronize()
+            assert torch.equal(bk.grads, g0) and torch.equal(bk.records[:, :2], r0)
+            if rec:
+                assert close(bk.records[:, 2:].cpu().numpy(), np.array(expect), 1e-12)
+            else:
+                assert (bk.records[:, 2:] == -1.0).all()
     if len(comms) > 1:
-        _lib.check(lib.gnsb_nccl_comm_destroy(comms[1]))
+        _lib.check(lib.gnsb_nccl_comm_destroy(comms[1].handle))
+    w = (ctypes.c_int64 * 2)(4, 4)
+    sp = torch.cuda.current_stream().cuda_stream
     with pytest.raises(ValueError, match="bucket"):
-        _lib.check(lib.gnsb_allreduce_buckets(grads.data_ptr(), 0, w, 0, records.data_ptr(), 1, None, sp))
+        _lib.check(lib.gnsb_allreduce_buckets(bk.grads.data_ptr(), 0, w, 0, bk.records.data_ptr(),
+                                              bk._ws.data_ptr(), bk._ws.numel(), None, sp))
+    with pytest.raises(ValueError, match="workspace too small"):
+        _lib.check(lib.gnsb_allreduce_buckets(bk.grads.data_ptr(), 0, w, 1, bk.records.data_ptr(),
+                                              bk._ws.data_ptr(), 8, None, sp))
