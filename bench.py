@@ -216,6 +216,9 @@ def run_ours(args):
         local = local % torch.cuda.device_count()
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        # communicator lines (nranks, NVLS/NVLink transport) in the log
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local)
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -224,6 +227,8 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     lib = _lib.lib()
+    if world > 1:
+        return run_sharded_main(args, m, lib, dev, torch, np, world, rank, local, backend)
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
     sweep = args.d_list
@@ -413,6 +418,10 @@ def run_ours(args):
         extra["cfg3_linear"] = run_cfg3(m, lib, dev, torch, np)
         extra["cfg4_gns"] = run_cfg4(m, lib, dev, torch, np)
         extra["cfg5_g1"] = run_cfg5(m, lib, dev, torch, np)
+        # the G=1 point of the configs[4] strong-scaling curve, measured the way
+        # `bench.py --gpus N` measures N > 1 (same step, exchange without a peer)
+        extra["cfg5_strong_g1"] = Cfg5Strong(args, m, lib, dev, torch, np, 1, 0, "none").measure(args.steps,
+                                                                                                args.warmup)
         extra["embedding"] = run_embedding(m, lib, dev, torch, np)
 
     traffic = load_traffic()
@@ -665,6 +674,310 @@ def run_cfg5(m, lib, dev, torch, np):
     return out
 
 
+CFG5_WORKLOAD = ("cfg5: batch-sharded LN bwd + per-example norms + GNS, B_global=256 T=2048 D=4096 bf16, "
+                 "strong scaling (B_global/N examples per GPU), one packed fp64 all-reduce per step")
+
+
+class Cfg5Strong:
+    """BASELINE.json configs[4]: the batch-sharded step at N GPUs, strong scaling.
+
+    Rank r owns the contiguous examples [b0, b1) = shard_bounds(B_global, N, r)
+    of a globally-indexed synthetic batch (dy scaled by 1/B_global), so every
+    value is the same whichever rank holds it.  One step, captured as ONE CUDA
+    graph on the NCCL path:
+      gnsb_ln_bwd_rows (dx + per-(CTA, example) partials)
+      gnsb_ln_bwd_reduce (per-example squares, dgamma/dbeta into the exchange bucket)
+      gnsb_allreduce_buckets: pack -> ONE ncclAllReduce of the fp64 bucket
+        {record, dgamma, dbeta} -> unpack (||G_big||^2 of the reduced gradients)
+      gnsb_gns_step (B = B_global)
+    The gloo test mode (several ranks on one device) runs the same kernels with
+    the all-reduce of the packed buffer issued eagerly between two graphs.
+    N = 1: the same step with no collective (pack -> unpack)."""
+
+    def __init__(self, args, m, lib, dev, torch, np, world, rank, backend):
+        import ctypes
+
+        from paper_2411_00999_b200 import _lib
+        from paper_2411_00999_b200.gns import DeviceGnsAccumulator
+        from paper_2411_00999_b200.sharded import GradBuckets, NcclComm, shard_bounds
+
+        self.torch, self.np, self.lib, self.dev = torch, np, lib, dev
+        self.world, self.rank, self.backend = world, rank, backend
+        Bg, T5, D5 = args.cfg5
+        self.Bg, self.T5, self.D5 = Bg, T5, D5
+        b0, b1 = shard_bounds(Bg, world, rank)
+        self.b0, self.Bl = b0, b1 - b0
+        bf = torch.bfloat16
+        self.x, self.dy, self.gamma, self.beta = m.synth_ln(self.Bl, T5, D5, bf, dev, b_offset=b0, B_div=Bg)
+        f = m.layernorm_forward(m.LayerNormLayer(self.gamma, self.beta), self.x)
+        self.mean, self.rstd = f.cache.mean, f.cache.inv_std
+        self.dx = torch.empty_like(self.x)
+        self.bk = GradBuckets([D5], dev)
+        self.raw = torch.zeros(2, self.Bl, dtype=torch.float64, device=dev)
+        self.ws = torch.zeros(m.layers.ctypes_size(self.Bl, T5, D5, 1), dtype=torch.uint8, device=dev)
+        dg, db = self.bk.grad(0)
+        self.pend = (_lib.LnBwdPending * 1)(_lib.LnBwdPending(
+            self.ws.data_ptr(), self.ws.numel(), self.Bl, T5, D5, 1, dg.data_ptr(), db.data_ptr(),
+            self.raw[0].data_ptr(), self.raw[1].data_ptr(), self.bk.record(0).data_ptr()))
+        self.acc = DeviceGnsAccumulator(["layernorm"], 0.5, dev)
+        self.comm = NcclComm() if (world > 1 and backend == "nccl") else None
+        self.bytes_local = alg_bytes(self.Bl, T5, D5)
+        self.bytes_local_plain = alg_bytes(self.Bl, T5, D5, norms=False)
+        self.rows_bytes = self.bytes_local - 8 * D5 - 16 * self.Bl
+        self.graph_all = world == 1 or self.comm is not None
+        self.packed_bytes = 8 * (4 + 2 * D5)
+        self._graphs = {}
+        self._ctypes = ctypes
+
+    # ---------------------------------------------------------------- pieces
+    def rows(self, sp):
+        p = lambda t: t.data_ptr()
+        if self.lib.gnsb_ln_bwd_rows(p(self.x), p(self.mean), p(self.rstd), p(self.dy), p(self.gamma), p(self.dx),
+                                     self.Bl, self.T5, self.D5, 1, p(self.ws), self.ws.numel(), sp):
+            raise RuntimeError(self.lib.gnsb_last_error().decode())
+
+    def compute(self, norms):
+        sp = self.torch.cuda.current_stream(self.dev).cuda_stream
+        self.rows(sp)
+        if self.lib.gnsb_ln_bwd_reduce(self.pend, 1, 1 if norms else 0, sp):
+            raise RuntimeError(self.lib.gnsb_last_error().decode())
+
+    def head(self, norms):
+        """Graph part 1: compute, then the exchange (NCCL / one rank) or its pack (gloo)."""
+        self.compute(norms)
+        if self.graph_all:
+            self.bk.allreduce_nccl(self.comm, records=norms)
+            if norms:
+                self.acc.step(self.bk.records, self.Bg)
+        else:
+            self.bk.pack(records=norms)
+
+    def tail(self, norms):
+        """gloo only: the collective on the packed buffer, then unpack + GNS step."""
+        import torch.distributed as dist
+
+        dist.all_reduce(self.bk.packed(records=norms))
+        self.bk.unpack(records=norms)
+        if norms:
+            self.acc.step(self.bk.records, self.Bg)
+
+    def launches_per_step(self, norms=True):
+        # rows, reduce, pack, unpack (+ gns step); the NCCL kernel is not ours
+        return 4 + (1 if norms else 0)
+
+    def capture(self):
+        torch = self.torch
+        side = torch.cuda.Stream(self.dev)
+        side.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(side):
+            for norms in (True, False):
+                self.head(norms)
+                if not self.graph_all:
+                    self.tail(norms)
+        torch.cuda.current_stream(self.dev).wait_stream(side)
+        torch.cuda.synchronize()
+        for norms in (True, False):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                self.head(norms)
+            self._graphs[norms] = g
+        torch.cuda.synchronize()
+
+    def step(self, norms=True):
+        self._graphs[norms].replay()
+        if not self.graph_all:
+            self.tail(norms)
+
+    def _barrier(self):
+        import torch.distributed as dist
+
+        if self.world > 1:
+            dist.barrier()
+
+    def _max(self, v):
+        import torch.distributed as dist
+
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=self.dev)
+        if self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def _sum(self, v):
+        import torch.distributed as dist
+
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=self.dev)
+        if self.world > 1:
+            dist.all_reduce(t)
+        return float(t.item())
+
+    def timed_steps(self, k, norms=True):
+        """K steps between barrier + synchronize, device time (events on the
+        replay stream), max over ranks (ms)."""
+        torch = self.torch
+        self._barrier()
+        torch.cuda.synchronize()
+        st = torch.cuda.current_stream(self.dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(k):
+            self.step(norms)
+        e1.record(st)
+        torch.cuda.synchronize()
+        self._barrier()
+        return self._max(e0.elapsed_time(e1))
+
+    def measure(self, steps, warmup, clocks=None):
+        torch, np = self.torch, self.np
+        if not self._graphs:
+            self.capture()
+        for _ in range(warmup):
+            self.step(True)
+            self.step(False)
+        torch.cuda.synchronize()
+        if clocks is not None:
+            clocks.__enter__()
+            time.sleep(0.3)
+        t_ms = self.timed_steps(steps, True)
+        total_bytes = self._sum(self.bytes_local)
+        value = total_bytes * steps / (t_ms * 1e-3) / 1e9
+        # fused vs plain twin (plain: no squares, gradients-only exchange, no GNS
+        # step), alternating blocks of steps; median + IQR of the per-block ratio
+        kb = max(3, min(steps, 10))
+        ov, tf, tp = [], [], []
+        for _ in range(7):
+            a = self.timed_steps(kb, True)
+            b = self.timed_steps(kb, False)
+            tf.append(a / kb)
+            tp.append(b / kb)
+            ov.append(100.0 * (a - b) / b)
+        # the exchange alone (graph of gnsb_allreduce_buckets), and the row pass
+        # alone back to back (the dominant kernel), max over ranks
+        ex_us = None
+        if self.graph_all:
+            from paper_2411_00999_b200 import _lib  # noqa: F401
+
+            ex_ms = time_graph(lambda: self.bk.allreduce_nccl(self.comm, records=True), torch, np, self.dev, reps=20)
+            ex_us = self._max(ex_ms * 1e3)
+        st = torch.cuda.current_stream(self.dev)
+        sp = st.cuda_stream
+        for _ in range(3):
+            self.rows(sp)
+        nrep = max(steps, 10)
+        self._barrier()
+        torch.cuda.synchronize()
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d0.record(st)
+        for _ in range(nrep):
+            self.rows(sp)
+        d1.record(st)
+        torch.cuda.synchronize()
+        rows_us = self._max(d0.elapsed_time(d1) * 1e3 / nrep)
+        if clocks is not None:
+            clocks.__exit__()
+        peak, peak_kind = load_peaks()
+        per_gpu = value / self.world
+        q = lambda v: [float(np.percentile(v, 25)), float(np.percentile(v, 75))]
+        return {
+            "workload": CFG5_WORKLOAD, "n_gpus": self.world, "value": value, "unit": "GB/s",
+            "ms_per_step": t_ms / steps, "steps": steps, "B_global": self.Bg, "B_per_gpu_rank0": self.Bl,
+            "T": self.T5, "D": self.D5, "per_gpu_GBps": per_gpu, "frac_of_measured_peak_per_gpu": per_gpu / peak,
+            "overhead_pct": float(np.median(ov)), "overhead_pct_iqr": q(ov),
+            "step_ms_fused": float(np.median(tf)), "step_ms_plain": float(np.median(tp)),
+            "exchange_us": ex_us, "exchange_bytes": self.packed_bytes,
+            "exchange": ("gnsb_allreduce_buckets: pack, one ncclAllReduce(fp64, %d B), unpack, in the step graph"
+                         % self.packed_bytes) if self.comm is not None else (
+                "pack, unpack (one rank: no collective)" if self.world == 1 else
+                "pack, torch.distributed all_reduce of the packed fp64 buffer (%s), unpack" % self.backend),
+            "rows_us": rows_us, "rows_GBps": self.rows_bytes / (rows_us * 1e-6) / 1e9,
+            "rows_frac_of_measured_peak": self.rows_bytes / (rows_us * 1e-6) / 1e9 / peak,
+            "rows_alg_bytes": self.rows_bytes, "peak": peak, "peak_kind": peak_kind,
+            "gpu_launches_per_step": self.launches_per_step(True),
+            "collectives_per_step": 1 if self.world > 1 else 0,
+        }
+
+    def e2e(self, steps):
+        """The same step through the C ABI with this rank's shard in pinned host
+        memory: H2D of x, dy, mean, rstd; the step; D2H of dx, dgamma, dbeta,
+        the per-example norms and the record.  Max over ranks."""
+        torch = self.torch
+        h = {k: getattr(self, k).cpu().pin_memory() for k in ("x", "dy", "mean", "rstd")}
+        hdx = torch.empty(self.dx.shape, dtype=self.dx.dtype).pin_memory()
+        hg = torch.empty(self.bk.grads.shape, dtype=self.bk.grads.dtype).pin_memory()
+        hraw = torch.empty(self.raw.shape, dtype=self.raw.dtype).pin_memory()
+        hrec = torch.empty(self.bk.records.shape, dtype=torch.float64).pin_memory()
+        h2d = sum(v.numel() * v.element_size() for v in h.values())
+        d2h = hdx.numel() * 2 + hg.numel() * 4 + hraw.numel() * 8 + hrec.numel() * 8
+
+        def one():
+            for k, v in h.items():
+                getattr(self, k).copy_(v, non_blocking=True)
+            self.step(True)
+            hdx.copy_(self.dx, non_blocking=True)
+            hg.copy_(self.bk.grads, non_blocking=True)
+            hraw.copy_(self.raw, non_blocking=True)
+            hrec.copy_(self.bk.records, non_blocking=True)
+
+        one()
+        torch.cuda.synchronize()
+        k = max(3, min(steps, 5))
+        self._barrier()
+        torch.cuda.synchronize()
+        st = torch.cuda.current_stream(self.dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(k):
+            one()
+        e1.record(st)
+        torch.cuda.synchronize()
+        self._barrier()
+        ms = self._max(e0.elapsed_time(e1)) / k
+        total = self._sum(self.bytes_local)
+        return {"value": total / (ms * 1e-3) / 1e9, "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "ms_per_step": ms, "steps": k,
+                "path": "per rank: pinned host shard -> H2D -> step graph (C ABI kernels + exchange) -> D2H, "
+                        "one stream, max over ranks"}
+
+    def close(self):
+        if self.comm is not None:
+            self.comm.close()
+
+
+def run_sharded_main(args, m, lib, dev, torch, np, world, rank, local, backend):
+    """N > 1: BASELINE.json configs[4], strong scaling."""
+    import torch.distributed as dist
+
+    c5 = Cfg5Strong(args, m, lib, dev, torch, np, world, rank, backend)
+    clk = ClockSampler(local)
+    r = c5.measure(args.steps, args.warmup, clocks=clk)
+    e2e = c5.e2e(args.steps)
+    line = {
+        "metric": METRIC, "value": r["value"], "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (SURVEY §8(d) recipe, global example index, on device)",
+        "config": {"workload": CFG5_WORKLOAD, "B_global": c5.Bg, "T": c5.T5, "D": c5.D5, "global_batch": c5.Bg,
+                   "parallelism": f"dp{world}", "backend": backend,
+                   "l2": "inputs larger than L2: %.2f GB per rank per step" % (c5.bytes_local / 1e9),
+                   "launch": "one CUDA graph per step incl. the NCCL all-reduce" if c5.graph_all else
+                             "two CUDA graphs per step around the eager gloo all-reduce (test mode)"},
+        "overhead_pct": r["overhead_pct"], "overhead_pct_iqr": r["overhead_pct_iqr"],
+        "step_ms_fused": r["step_ms_fused"], "step_ms_plain": r["step_ms_plain"],
+        "per_gpu_GBps": r["per_gpu_GBps"], "frac_of_measured_peak_per_gpu": r["frac_of_measured_peak_per_gpu"],
+        "exchange": r["exchange"], "exchange_us": r["exchange_us"], "collectives_per_step": 1,
+        "roofline": {"bound": "hbm", "achieved": r["rows_GBps"], "peak": r["peak"], "unit": "GB/s",
+                     "frac": r["rows_frac_of_measured_peak"], "peak_kind": r["peak_kind"], "traffic": None,
+                     "alg_bytes_per_launch": r["rows_alg_bytes"], "us_per_launch": r["rows_us"],
+                     "kernel": f"ln_bwd_kernel<bf16, D={c5.D5}> row pass, {c5.Bl} examples per rank",
+                     "achieved_def": "algorithmic bytes per launch / CUDA-event duration, back-to-back, max over ranks"},
+        "e2e": e2e, "cpu_baseline": None, "gpu_launches": r["gpu_launches_per_step"] * args.steps,
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    c5.close()
+    dist.destroy_process_group()
+    return 0
+
+
 def run_e2e(args, m, lib, cases, dev, stream, torch, np):
     """Same metric through the public C ABI with host-resident inputs/outputs."""
     sp = stream.cuda_stream
@@ -791,6 +1104,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-extra", action="store_true", help="skip the per-width steady runs and the side measurements")
     ap.add_argument("--no-side", action="store_true", help="skip the side measurements (forward, configs 3/4/5)")
+    ap.add_argument("--cfg5", type=lambda s: [int(v) for v in s.split(",")], default=[256, 2048, 4096],
+                    help="B_global,T,D of the N > 1 strong-scaling step (BASELINE configs[4]; smaller for tests)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

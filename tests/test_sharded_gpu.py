@@ -90,18 +90,24 @@ def _free_port():
 
 
 def test_bench_multirank_path_runs(cuda):
-    """bench.py under torchrun with 2 ranks (gloo, both on cuda:0): one JSON line
-    from rank 0 with n_gpus=2 and a positive value (timing is not meaningful here)."""
+    """bench.py under torchrun with 2 ranks (gloo, both on cuda:0): the N > 1
+    line is the configs[4] strong-scaling step (here at a reduced B_global,T,D):
+    one JSON line from rank 0, n_gpus=2, scaling strong, ONE collective per
+    step (the packed fp64 bucket) and the C-ABI kernels of the step counted."""
     env = dict(os.environ, GNSB_DIST_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"),
-           "--gpus", "2", "--steps", "2", "--warmup", "3", "--no-cpu", "--no-extra", "--d-list", "768,1024"]
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--no-cpu", "--cfg5", "64,256,1024"]
     p = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stderr[-3000:]
     lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1, p.stdout[-2000:]
     rec = json.loads(lines[0])
-    assert rec["n_gpus"] == 2 and rec["value"] > 0 and rec["config"]["global_batch"] == 64
+    assert rec["n_gpus"] == 2 and rec["value"] > 0 and rec["scaling"] == "strong"
+    assert rec["config"]["global_batch"] == 64 and rec["config"]["B_global"] == 64
+    assert rec["collectives_per_step"] == 1 and rec["gpu_launches"] == 5 * 3
+    assert rec["e2e"]["h2d_bytes_per_step"] == 32 * 256 * 1024 * 4 + 32 * 256 * 8
+    assert rec["roofline"]["achieved"] > 0
 
 
 @pytest.mark.parametrize("gdt", [torch.float32, torch.float64])
