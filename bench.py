@@ -175,17 +175,34 @@ class LnCase:
         self.bytes = alg_bytes(B, T, D)
         self.bytes_plain = alg_bytes(B, T, D, norms=False)
 
-    def run_rows(self, stream_ptr):
+    def run_rows(self, stream_ptr, norms=True):
+        """Row pass.  norms=False: the plain LayerNorm backward's row pass, the
+        same rows viewed as ONE example of B*T rows (no per-example
+        bookkeeping), as gnsb_ln_bwd(with_norms=0) runs it."""
         p = lambda t: t.data_ptr()
+        Bv, Mv = (self.B, T) if norms else (1, self.B * T)
         rc = self.lib.gnsb_ln_bwd_rows(p(self.x), p(self.mean), p(self.rstd), p(self.dy), p(self.gamma), p(self.dx),
-                                       self.B, T, self.D, 1, p(self.ws), self.ws.numel(), stream_ptr)
+                                       Bv, Mv, self.D, 1, p(self.ws), self.ws.numel(), stream_ptr)
         if rc:
             raise RuntimeError(self.lib.gnsb_last_error().decode())
 
-    def pending(self, _lib):
-        return _lib.LnBwdPending(self.ws.data_ptr(), self.ws.numel(), self.B, T, self.D, 1, self.dgamma.data_ptr(),
+    def pending(self, _lib, norms=True):
+        Bv, Mv = (self.B, T) if norms else (1, self.B * T)
+        return _lib.LnBwdPending(self.ws.data_ptr(), self.ws.numel(), Bv, Mv, self.D, 1, self.dgamma.data_ptr(),
                                  self.dbeta.data_ptr(), self.raw_g.data_ptr(), self.raw_b.data_ptr(),
                                  self.sums.data_ptr())
+
+    def aten_args(self, torch):
+        """PyTorch's own LayerNorm backward on the same bf16 rows (the paper's
+        baseline): bf16 weight/bias, fp32 mean/rstd."""
+        if not hasattr(self, "_aten"):
+            self._aten = (self.dy.view(self.B, T, self.D), self.x.view(self.B, T, self.D), [self.D],
+                          self.mean.view(self.B, T, 1), self.rstd.view(self.B, T, 1),
+                          self.gamma.to(torch.bfloat16), self.beta.to(torch.bfloat16), [True, True, True])
+        return self._aten
+
+    def run_aten(self, torch):
+        torch.ops.aten.native_layer_norm_backward(*self.aten_args(torch))
 
     def run(self, norms, stream_ptr):
         p = lambda t: t.data_ptr()
@@ -237,7 +254,8 @@ def run_ours(args):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     torch.cuda.synchronize()
 
-    pend = (_lib.LnBwdPending * len(cases))(*[c.pending(_lib) for c in cases])
+    pend = {True: (_lib.LnBwdPending * len(cases))(*[c.pending(_lib) for c in cases]),
+            False: (_lib.LnBwdPending * len(cases))(*[c.pending(_lib, False) for c in cases])}
 
     def run_step(norms):
         """The compute of one step (captured as one CUDA graph): the fused (or
@@ -246,8 +264,8 @@ def run_ours(args):
         of them in one launch (gnsb_ln_bwd_reduce)."""
         sp_now = torch.cuda.current_stream(dev).cuda_stream
         for c in cases:
-            c.run_rows(sp_now)
-        rc = lib.gnsb_ln_bwd_reduce(pend, len(cases), 1 if norms else 0, sp_now)
+            c.run_rows(sp_now, norms)
+        rc = lib.gnsb_ln_bwd_reduce(pend[norms], len(cases), 1 if norms else 0, sp_now)
         if rc:
             raise RuntimeError(lib.gnsb_last_error().decode())
 
@@ -317,19 +335,16 @@ def run_ours(args):
     total_bytes = sum(c.bytes for c in cases) * world * args.steps
     value = total_bytes / (t_max_ms * 1e-3) / 1e9
 
-    # ---- step-level fused vs plain (overhead): alternating graph replays ----
+    # ---- step-level fused vs plain vs aten: interleaved graph replays ----
     reps = max(args.steps, 20)
-    fs, ps = [], []
-    for r in range(reps):
-        for norms, acc in ((True, fs), (False, ps)):
-            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a_.record(stream)
-            replay(norms)
-            b_.record(stream)
-            acc.append((a_, b_))
-    torch.cuda.synchronize()
-    step_f = float(np.median([a_.elapsed_time(b_) for a_, b_ in fs]))
-    step_p = float(np.median([a_.elapsed_time(b_) for a_, b_ in ps]))
+    aten_graph = None
+    if world == 1:
+        aten_graph = capture_graph(lambda: [c.run_aten(torch) for c in cases], torch, dev)
+    variants = {"fused": lambda: replay(True), "plain": lambda: replay(False)}
+    if aten_graph is not None:
+        variants["aten"] = aten_graph.replay
+    st = interleaved(variants, reps, stream, torch, np)
+    step_f, step_p = st["fused"]["median"], st["plain"]["median"]
 
     # ---- per-kernel cold launches (flush + events): per-D breakdown ----
     fk = np.zeros((reps, len(cases)))
@@ -361,25 +376,37 @@ def run_ours(args):
             break
         extra_cases = [c] + [LnCase(m, lib, c.D, B_LOCAL, rank, dev, torch, GradBuckets([c.D], dev), 0)
                              for _ in range(NL - 1)]
-        pend_d = (_lib.LnBwdPending * NL)(*[e.pending(_lib) for e in extra_cases])
+        pend_d = {nm: (_lib.LnBwdPending * NL)(*[e.pending(_lib, nm) for e in extra_cases]) for nm in (True, False)}
 
         def layer_step(norms, extra_cases=extra_cases, pend_d=pend_d):
             spn = torch.cuda.current_stream(dev).cuda_stream
             for e in extra_cases:
-                e.run_rows(spn)
-            if lib.gnsb_ln_bwd_reduce(pend_d, NL, 1 if norms else 0, spn):
+                e.run_rows(spn, norms)
+            if lib.gnsb_ln_bwd_reduce(pend_d[norms], NL, 1 if norms else 0, spn):
                 raise RuntimeError(lib.gnsb_last_error().decode())
 
-        ms_f = time_graph(lambda: layer_step(True), torch, np, dev, reps=max(args.steps, 10))
-        ms_p = time_graph(lambda: layer_step(False), torch, np, dev, reps=max(args.steps, 10))
+        gr = {"fused": capture_graph(lambda: layer_step(True), torch, dev),
+              "plain": capture_graph(lambda: layer_step(False), torch, dev),
+              "aten": capture_graph(lambda: [e.run_aten(torch) for e in extra_cases], torch, dev)}
+        sd = interleaved({k: g.replay for k, g in gr.items()}, max(args.steps, 15), stream, torch, np)
+        ms_f, ms_p, ms_a = sd["fused"]["median"], sd["plain"]["median"], sd["aten"]["median"]
         gbs = NL * c.bytes / (ms_f * 1e-3) / 1e9
         sweep_rows[i].update({
             "steady_layers": NL, "steady_fused_GBps": gbs, "steady_frac_of_measured_peak": gbs / peak,
+            "steady_fused_us_per_layer": ms_f * 1e3 / NL, "steady_fused_iqr_us": [v * 1e3 / NL for v in sd["fused"]["iqr"]],
             "steady_plain_GBps": NL * c.bytes_plain / (ms_p * 1e-3) / 1e9,
+            "steady_plain_us_per_layer": ms_p * 1e3 / NL, "steady_plain_iqr_us": [v * 1e3 / NL for v in sd["plain"]["iqr"]],
             "steady_overhead_pct": 100.0 * (ms_f - ms_p) / ms_p,
-            "steady_timing": f"{NL} layers of this width (distinct buffers) + one grouped reduce, CUDA graph",
+            "steady_overhead_pct_iqr": sd["fused"]["paired_overhead_iqr"]["plain"],
+            "steady_aten_us_per_layer": ms_a * 1e3 / NL, "steady_aten_GBps": NL * c.bytes_plain / (ms_a * 1e-3) / 1e9,
+            "overhead_vs_aten_pct": 100.0 * (ms_f - ms_a) / ms_a,
+            "overhead_vs_aten_pct_iqr": sd["fused"]["paired_overhead_iqr"]["aten"],
+            "steady_timing": f"{NL} layers of this width (distinct buffers) + one grouped reduce per CUDA graph; "
+                             "fused / plain / aten graphs replayed interleaved, median and interquartile range",
+            "plain_def": "same kernels over one example of B*T rows (no per-example bookkeeping, no squares)",
+            "aten_def": "torch.ops.aten.native_layer_norm_backward, bf16 rows/weight, fp32 mean/rstd, same buffers",
         })
-        del extra_cases
+        del extra_cases, gr
         torch.cuda.empty_cache()
     big = [r for r in sweep_rows if r["D"] >= 1024]
     overhead_ge1024 = 100.0 * (sum(r["fused_us"] for r in big) - sum(r["plain_us"] for r in big)) / max(
@@ -436,7 +463,14 @@ def run_ours(args):
                    "launch": "one CUDA graph per step (compute); N > 1: the bucket all-reduce eagerly after it",
                    "stage2": "deferred: row pass per layer, one grouped reduce launch per step (gnsb_ln_bwd_reduce)"},
         "overhead_pct": 100.0 * (step_f - step_p) / step_p, "overhead_pct_D_ge_1024": overhead_ge1024,
+        "overhead_pct_iqr": st["fused"]["paired_overhead_iqr"]["plain"],
         "step_ms_fused": step_f, "step_ms_plain": step_p,
+        "step_ms_fused_iqr": st["fused"]["iqr"], "step_ms_plain_iqr": st["plain"]["iqr"],
+        "step_ms_aten": st["aten"]["median"] if "aten" in st else None,
+        "overhead_vs_aten_pct": 100.0 * (step_f - st["aten"]["median"]) / st["aten"]["median"] if "aten" in st else None,
+        "overhead_def": "fused step vs the plain LayerNorm backward step (same kernels over one example of B*T rows: "
+                        "no per-example bookkeeping, no squares), interleaved graph replays, median; iqr of the "
+                        "per-replay-pair overhead",
         "roofline": {"bound": "hbm", "achieved": dom_achieved, "peak": peak, "unit": "GB/s",
                      "frac": dom_achieved / peak, "peak_kind": peak_kind, "frac_of_8TBps": dom_achieved / 8000.0,
                      "traffic": traffic, "alg_bytes_per_launch": dom_bytes, "us_per_launch": dom_us,
@@ -481,6 +515,52 @@ def time_graph(fn, torch, np, dev, reps=10, warm=3):
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))
     return float(np.median(ts))
+
+
+def capture_graph(fn, torch, dev, warm=3):
+    """fn() captured as one CUDA graph (after warm-up on a side stream)."""
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(side):
+        for _ in range(warm):
+            fn()
+    torch.cuda.current_stream(dev).wait_stream(side)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    for _ in range(warm):
+        g.replay()
+    torch.cuda.synchronize()
+    return g
+
+
+def interleaved(variants, reps, stream, torch, np):
+    """Replay the variants round-robin (v1 v2 v3, v2 v3 v1, ...), each bracketed by
+    CUDA events on `stream`, so slow drifts (clocks, temperature) hit all of
+    them alike.  Per variant: median and interquartile range (ms), and per
+    other variant the interquartile range of the paired overhead (%)."""
+    ev = {k: [] for k in variants}
+    names = list(variants)
+    for r in range(reps):
+        # rotate the order every replay round: each variant follows each other
+        # one equally often (what the previous graph left in L2 -- dirty lines,
+        # resident inputs -- biases whoever runs next)
+        for k in names[r % len(names):] + names[:r % len(names)]:
+            fn = variants[k]
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            ev[k].append((a, b))
+    torch.cuda.synchronize()
+    ts = {k: np.array([a.elapsed_time(b) for a, b in v]) for k, v in ev.items()}
+    out = {}
+    for k, t in ts.items():
+        pair = {o: [float(x) for x in np.percentile(100.0 * (t - ts[o]) / ts[o], [25, 75])] for o in ts if o != k}
+        out[k] = {"median": float(np.median(t)), "iqr": [float(x) for x in np.percentile(t, [25, 75])],
+                  "paired_overhead_iqr": pair}
+    return out
 
 
 def run_ln_fwd(m, lib, cases, dev, torch, np):

@@ -1,5 +1,6 @@
 // ln_sweep.cu — configuration sweep of the fused LN-backward kernel (experiment only).
 #include <cstdio>
+#include <vector>
 
 #include "../paper_2411_00999_b200/csrc/ln_launch.cuh"
 
@@ -92,6 +93,48 @@ int sweep_desc(int id, int* out) {
     if (id == i) { out[0] = gw; out[1] = vpt; out[2] = g; out[3] = rpg; out[4] = prod; out[5] = LnBwdCfg<bf, gw, vpt, g, rpg, prod, keep, ##__VA_ARGS__>::KEEP; return 0; }
     CFGS(DESC)
     return -1;
+}
+
+// the production row-pass dispatch (ln_bwd_rows_run) with per-CTA trace stamps
+int sweep_rows_prod(const void* x, const void* mean, const void* rstd, const void* dy, const void* gamma, void* dx,
+                    int64_t B, int64_t M, int64_t D, void* ws, size_t wsb, void* stream, unsigned long long* trace) {
+    LnBwdCall c{x, mean, rstd, dy, gamma, dx, nullptr, nullptr, nullptr, nullptr, nullptr, 0, B, M, D, ws, wsb,
+                trace, nullptr};
+    const char* why = nullptr;
+    cudaError_t ce = cudaSuccess;
+    int rc = ln_bwd_rows_run<bf>(c, (cudaStream_t)stream, &why, &ce);
+    if (rc == 1) fprintf(stderr, "rows: %s\n", why ? why : "?");
+    return rc ? (rc == 2 ? 1000 + (int)ce : 1) : 0;
+}
+
+// The steady step of config `id`: the row pass of n LayerNorms (arrays of
+// per-layer pointers) then ONE grouped stage 2 (ln_bwd_reduce_run), as
+// bench.py's per-width steady measurement, with this config's plan info.
+int sweep_step(int id, int n, const void* const* x, const void* const* mean, const void* const* rstd,
+               const void* const* dy, const void* const* gamma, void* const* dx, void* const* dgamma,
+               void* const* dbeta, double* const* rg, double* const* rb, double* const* sums, int norms, int64_t B,
+               int64_t M, int64_t D, void* const* ws, size_t wsb, void* stream) {
+    std::vector<LnRedItem> items(n);
+    const char* why = nullptr;
+    cudaError_t ce = cudaSuccess;
+    for (int l = 0; l < n; ++l) {
+        LnBwdCall c{x[l], mean[l], rstd[l], dy[l], gamma[l], dx[l], dgamma[l], dbeta[l], rg[l], rb[l], sums[l],
+                    norms > 0 ? 1 : 0, B, M, D, ws[l], wsb};
+        LnRedItem& it = items[l];
+        int rc = -1;
+#define ROWS(i, gw, vpt, g, rpg, prod, keep, ...) \
+        if (id == i) rc = BwdOp<LnBwdCfg<bf, gw, vpt, g, rpg, prod, keep, ##__VA_ARGS__>>::run_rows(c, (cudaStream_t)stream, &why, &ce, &it.info);
+        CFGS(ROWS)
+        if (rc != 0) {
+            if (rc == 1) fprintf(stderr, "cfg%d: %s\n", id, why ? why : "?");
+            return rc < 0 ? -1 : rc == 2 ? 1000 + (int)ce : 1;
+        }
+        it.B = B; it.M = M; it.D = D; it.ws = ws[l];
+        it.dgamma = dgamma[l]; it.dbeta = dbeta[l]; it.raw_g = rg[l]; it.raw_b = rb[l]; it.sums = sums[l];
+    }
+    if (norms < 0) return 0;  // rows only (timing the row passes alone)
+    int rc = ln_bwd_reduce_run(0, norms, items.data(), n, (cudaStream_t)stream, nullptr, &why, &ce);
+    return rc ? (rc == 2 ? 1000 + (int)ce : 1) : 0;
 }
 
 int sweep_run(int id, const void* x, const void* mean, const void* rstd, const void* dy, const void* gamma, void* dx,

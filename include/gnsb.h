@@ -71,8 +71,12 @@ gnsb_status gnsb_ln_fwd(const void* x, const void* gamma, const void* beta, void
  *   sums            : [4] nullable: { sum_b raw_gamma, sum_b raw_beta,
  *                     ||dgamma||^2, ||dbeta||^2 }.  The reference's corrected
  *                     value (per_example_sqnorms) is sums[i] / B * B^2.
- *   with_norms      : 0 runs the otherwise-identical plain LayerNorm backward
- *                     (same kernel, norms compiled out; raw/sums untouched).
+ *   with_norms      : 0 runs the otherwise-identical plain LayerNorm backward:
+ *                     the same kernels over one "example" of B*M rows (no
+ *                     per-example flushes, one partial slot per CTA, no
+ *                     squares); raw/sums untouched.  The row pass of a
+ *                     deferred plain call is gnsb_ln_bwd_rows with B = 1,
+ *                     M = B*M (and its pending item likewise).
  *   ws, ws_bytes    : device workspace of at least
  *                     gnsb_ln_bwd_workspace_size() bytes.  It must be
  *                     zero-filled before its first use; every call leaves it

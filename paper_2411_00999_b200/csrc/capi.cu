@@ -309,8 +309,12 @@ gnsb_status gnsb_ln_bwd(const void* x, const void* mean, const void* rstd, const
     }
     if (!x || !rstd || !dy || !gamma || !dgamma || !dbeta || !ws)
         return fail(GNSB_EINVAL, "layers: null input pointer");
+    // The plain LayerNorm backward has no per-example structure: the same
+    // kernels over ONE example of B*M rows (no example-boundary flushes, one
+    // partial slot per CTA).  This is the overhead baseline of the fused call.
+    const int64_t Bk = with_norms ? B : 1, Mk = with_norms ? M : B * M;
     gnsb::LnBwdCall c{x, mean, rstd, dy, gamma, dx, dgamma, dbeta, raw_g, raw_b, sums, with_norms ? 1 : 0,
-                      B, M, D, ws, ws_bytes};
+                      Bk, Mk, D, ws, ws_bytes};
     const char* why = nullptr;
     cudaError_t ce = cudaSuccess;
     int rc = 1;

@@ -232,6 +232,12 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
     return p;
 }
 // 1-D TMA: global -> shared, completion signalled on `bar` (complete_tx).
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
 __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar,
                                          uint64_t policy) {
     asm volatile(

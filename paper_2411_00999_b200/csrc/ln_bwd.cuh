@@ -65,6 +65,7 @@ struct LnRedArgs {
     int Dp;
     int grid_rows;        // CTAs of the row kernel (row range of CTA c: [c*N/grid_rows, (c+1)*N/grid_rows))
     int eb;               // examples per shared-memory block
+    int slot_cap;         // slots staged at once; < a block's span only when eb == 1 (chunked per example)
     void* dgamma;         // [D] Acc
     void* dbeta;          // [D] Acc
     double* raw_g;        // [B] or null
@@ -191,6 +192,7 @@ __global__ void __launch_bounds__(C::kBoundThreads, C::kCps) ln_bwd_kernel(LnBwd
     // the previous kernel in the stream; no global memory is touched before
     // the previous grid has completed and its writes are visible.
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    stamp(3);
 
     // ------------------------------------------------------------ producer --
     // Fill stage `st` into its slot.  Called by warp 0 only (lane 0 issues the
@@ -255,10 +257,11 @@ __global__ void __launch_bounds__(C::kBoundThreads, C::kCps) ln_bwd_kernel(LnBwd
 
     {  // gamma -> shared memory (while the first stages are in flight)
         const Acc* gg = static_cast<const Acc*>(a.gamma);
-        if (a.gamma16) {
+        if (a.gamma16) {  // D % E == 0 here; pad columns [D, Dp) read as zero
             constexpr int E = 16 / sizeof(Acc);
-            for (int i = threadIdx.x; i < Dp / E; i += blockDim.x)
+            for (int i = threadIdx.x; i < (int)D / E; i += blockDim.x)
                 *reinterpret_cast<uint4*>(gam_s + i * E) = __ldg(reinterpret_cast<const uint4*>(gg) + i);
+            for (int i = (int)D + threadIdx.x; i < Dp; i += blockDim.x) gam_s[i] = Acc(0);
         } else {
             for (int i = threadIdx.x; i < Dp; i += blockDim.x) gam_s[i] = i < D ? gg[i] : Acc(0);
         }
@@ -613,51 +616,59 @@ __device__ __forceinline__ void ln_bwd_reduce_body(const LnRedArgs& a, const int
         // slots of this block: from the first CTA of example b0 to the last of b0+nb-1
         const int64_t s_lo = cta_of(b0 * M) + b0;
         const int64_t s_hi = cta_of((b0 + nb) * M - 1) + (b0 + nb - 1);
-        const int nvec = (int)(s_hi - s_lo + 1) * 2 * nu;  // < 2^31: bounded by the smem block
-        const uint4* pbase = part + s_lo * sstride + u0;
-        // stage: independent 16-byte loads, 8 per thread in flight
-        for (int i0 = threadIdx.x; i0 < nvec; i0 += 8 * nthreads) {
-            uint4 v[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const int i = i0 + k * nthreads;
-                if (i < nvec) {
-                    const int sl = i / (2 * nu), rem = i - sl * 2 * nu;
-                    const int h = rem >= nu ? 1 : 0, u = rem - h * nu;
-                    v[k] = __ldcg(pbase + (int64_t)sl * sstride + h * half + u);
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const int i = i0 + k * nthreads;
-                if (i < nvec) stg[i] = v[k];
-            }
-        }
-        __syncthreads();
-        if (b0 == 0) stamp(1);
-        // per (example, column): fixed-order sum over the example's CTAs
         for (int bb = threadIdx.x; bb < nb; bb += nthreads) {
             const int64_t b = b0 + bb;
             s_cs[bb] = (int)(cta_of(b * M) + b - s_lo);  // first slot of example b, relative to s_lo
             s_nc[bb] = (int)(cta_of((b + 1) * M - 1) - cta_of(b * M) + 1);
         }
-        __syncthreads();
-        const int items = (int)nb * ncol;
-        const Acc* sa = reinterpret_cast<const Acc*>(stg);
-        for (int it = threadIdx.x; it < items; it += nthreads) {
-            const int bb = it / ncol;
-            const int j = it - bb * ncol;
-            const Acc* sg = sa + (size_t)s_cs[bb] * 2 * ncol + j;
-            const int nc = s_nc[bb];
-            double vg = 0.0, vb = 0.0;
-            for (int c = 0; c < nc; ++c) {
-                vg += (double)sg[c * 2 * ncol];
-                vb += (double)sg[c * 2 * ncol + ncol];
+        // The block's slots are staged `slot_cap` at a time (one chunk unless a
+        // single example spans more CTAs than fit, e.g. B = 1); the per-column
+        // sums continue across chunks in the same fixed slot order.
+        const int64_t nsl = s_hi - s_lo + 1;
+        for (int64_t c0 = 0; c0 < nsl; c0 += a.slot_cap) {
+            const int64_t cn = (nsl - c0) < a.slot_cap ? (nsl - c0) : a.slot_cap;
+            const int nvec = (int)cn * 2 * nu;  // < 2^31: bounded by the smem block
+            const uint4* pbase = part + (s_lo + c0) * sstride + u0;
+            // stage: independent 16-byte loads, 8 per thread in flight
+            for (int i0 = threadIdx.x; i0 < nvec; i0 += 8 * nthreads) {
+                uint4 v[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int i = i0 + k * nthreads;
+                    if (i < nvec) {
+                        const int sl = i / (2 * nu), rem = i - sl * 2 * nu;
+                        const int h = rem >= nu ? 1 : 0, u = rem - h * nu;
+                        v[k] = __ldcg(pbase + (int64_t)sl * sstride + h * half + u);
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int i = i0 + k * nthreads;
+                    if (i < nvec) stg[i] = v[k];
+                }
             }
-            sv[bb * svs + j] = vg;
-            sv[bb * svs + ncol + j] = vb;
+            __syncthreads();
+            if (b0 == 0 && c0 == 0) stamp(1);
+            // per (example, column): fixed-order sum over the example's CTAs
+            const int items = (int)nb * ncol;
+            const Acc* sa = reinterpret_cast<const Acc*>(stg);
+            for (int it = threadIdx.x; it < items; it += nthreads) {
+                const int bb = it / ncol;
+                const int j = it - bb * ncol;
+                const int64_t lo = s_cs[bb] > c0 ? s_cs[bb] : c0;
+                const int64_t hi = (s_cs[bb] + s_nc[bb]) < (c0 + cn) ? (s_cs[bb] + s_nc[bb]) : (c0 + cn);
+                double vg = c0 == 0 ? 0.0 : sv[bb * svs + j];
+                double vb = c0 == 0 ? 0.0 : sv[bb * svs + ncol + j];
+                const Acc* sg = sa + (size_t)(lo - c0) * 2 * ncol + j;
+                for (int64_t c = 0; c < hi - lo; ++c) {
+                    vg += (double)sg[c * 2 * ncol];
+                    vb += (double)sg[c * 2 * ncol + ncol];
+                }
+                sv[bb * svs + j] = vg;
+                sv[bb * svs + ncol + j] = vb;
+            }
+            __syncthreads();
         }
-        __syncthreads();
         // one pass, two roles (no barrier between them): threads [0, nb) square
         // and sum their example over this CTA's columns; threads [nb, nb + 2 ncol)
         // add their column over the block's examples.  Both in fixed order.

@@ -3,6 +3,7 @@
 // template instantiations compile in parallel.
 #pragma once
 
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <utility>
@@ -50,7 +51,17 @@ int plan_bwd(int64_t B, int64_t M, int64_t D, BwdPlan& p, const char** why) {
     const size_t budget = (C::kCps == 1) ? (size_t)smem_optin_bytes() - 1024
                                          : (size_t)(228 * 1024) / C::kCps - 2048;
     p.stages = 0;
-    for (int s = 8; s >= 2; --s)  // >= 2: pass 2 holds a slot while the next stage is consumed
+    // Ring depth: 4 stages (~128 KB in flight per SM) beat 6-8 at every
+    // width in the steady 8-layer step (D=768..8192: +4.5/+3/+1.4/+1/+0.5 %,
+    // experiments/ln_steady_trace.py; 3 ties, 2 loses).  More reads in flight
+    // than that only slow the dx write stream down.  GNSB_LN_MAX_STAGES
+    // overrides it (tuning experiments).
+    static const int max_stages = [] {
+        const char* e = getenv("GNSB_LN_MAX_STAGES");
+        const int v = e ? atoi(e) : 4;
+        return v < 2 ? 2 : v > 8 ? 8 : v;
+    }();
+    for (int s = max_stages; s >= 2; --s)  // >= 2: pass 2 holds a slot while the next stage is consumed
         if (C::smem_bytes(s, p.Dp) <= budget) {
             p.stages = s;
             break;

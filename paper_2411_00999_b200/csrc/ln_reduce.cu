@@ -25,7 +25,7 @@ inline int smem_optin() {
 }
 
 struct RedShape {
-    int rgrid = 0, eb = 0;
+    int rgrid = 0, eb = 0, slot_cap = 0;
     size_t smem = 0;
 };
 
@@ -41,10 +41,18 @@ RedShape red_shape(const LnRedItem& it, int V, int rgrid, int acc_bytes) {
         const int64_t span = rows_per_cta > 0 ? (eb * it.M + rows_per_cta - 1) / rows_per_cta + 2 : N;
         return LnRedLayout{ncol, eb, span + eb};
     };
+    constexpr size_t kBudget = 160 << 10;
     int64_t eb = it.B < kMaxReduceEb ? it.B : kMaxReduceEb;
-    while (eb > 1 && layout(eb).bytes(acc_bytes) > (size_t)(160 << 10)) eb = (eb + 1) / 2;
+    while (eb > 1 && layout(eb).bytes(acc_bytes) > kBudget) eb = (eb + 1) / 2;
+    LnRedLayout lay = layout(eb);
+    if (lay.bytes(acc_bytes) > kBudget) {  // eb == 1 and one example spans too many CTAs: chunk its slots
+        const size_t per_slot = (size_t)LnRedLayout::slot_bytes(ncol, acc_bytes);
+        const size_t fixed = lay.stage_off();
+        lay.nslot_max = fixed + per_slot <= kBudget ? (int64_t)((kBudget - fixed) / per_slot) : 1;
+    }
     r.eb = (int)eb;
-    r.smem = layout(eb).bytes(acc_bytes);
+    r.slot_cap = (int)lay.nslot_max;
+    r.smem = lay.bytes(acc_bytes);
     return r;
 }
 
@@ -60,6 +68,7 @@ LnRedArgs red_args(const LnRedItem& it, const RedShape& r, unsigned long long* t
     a.Dp = it.info.Dp;
     a.grid_rows = it.info.grid_rows;
     a.eb = r.eb;
+    a.slot_cap = r.slot_cap;
     a.dgamma = it.dgamma;
     a.dbeta = it.dbeta;
     a.raw_g = it.raw_g;
