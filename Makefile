@@ -21,7 +21,7 @@ CXX_OBJS  := $(patsubst $(SRC)/%.cpp,$(OBJDIR)/%.o,$(CXX_SRCS))
 CUDA_HOME ?= /usr/local/cuda
 HDRS      := $(wildcard $(SRC)/*.cuh) $(wildcard $(SRC)/*.h) include/gnsb.h $(wildcard include/gnstk/*.hpp)
 
-all: lib oracle cpptest
+all: lib oracle cpptest refsuites
 
 lib: $(LIBDIR)/libgnsb.so
 
@@ -47,8 +47,36 @@ cpptest: tests/cpp/test_dropin
 tests/cpp/test_dropin: tests/cpp/test_dropin.cpp $(LIBDIR)/libgnsb.so $(wildcard include/gnstk/*.hpp)
 	g++ -O2 -std=c++20 -Iinclude -o $@ $< -L$(LIBDIR) -lgnsb -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)'
 
+# The reference's OWN unit tests and acceptance harness, compiled UNMODIFIED from
+# /root/reference/proj against the drop-in: our include/gnstk headers shadow the
+# reference's tensor/layers/gns/costmodel.hpp and libgnsb replaces
+# tensor/layers/gns/costmodel.cpp; the reference's other sources (dataset, model,
+# trainer, simulator, csv, cli) are compiled as they are -- the swap INTEGRATION.md
+# documents.  tests/cpp/doctest/doctest.h stands in for the absent vendored
+# doctest.  Outputs go to tests/cpp/_ref/ (git-ignored; they travel to the GPU
+# box with the snapshot).  Skipped when /root/reference is absent.
+REF       ?= /root/reference/proj
+NLOHMANN  ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann
+REF_FLAGS := -O2 -std=c++20 -Iinclude -I$(REF)/include -I$(REF)/tests -Itests/cpp/doctest -I$(NLOHMANN)
+REF_LINK  := -L$(LIBDIR) -lgnsb -Wl,-rpath,'$$ORIGIN/../../../$(LIBDIR)'
+REF_SRCS  := $(addprefix $(REF)/src/,dataset.cpp model.cpp trainer.cpp simulator.cpp csv.cpp cli.cpp)
+REF_UNIT  := $(addprefix $(REF)/tests/,test_main.cpp test_tensor.cpp test_layers.cpp test_gns.cpp \
+             test_costmodel.cpp test_dataset.cpp test_trainer.cpp test_simulator.cpp)
+
+refsuites: refsuite-unit refsuite-acceptance
+
+refsuite-unit: $(LIBDIR)/libgnsb.so
+	@if [ -d $(REF)/tests ]; then mkdir -p tests/cpp/_ref && \
+	  g++ $(REF_FLAGS) -o tests/cpp/_ref/unit_tests $(REF_UNIT) $(REF_SRCS) $(REF_LINK); \
+	else echo "refsuites: $(REF) absent, skipped"; fi
+
+refsuite-acceptance: $(LIBDIR)/libgnsb.so
+	@if [ -d $(REF)/tests ]; then mkdir -p tests/cpp/_ref && \
+	  g++ $(REF_FLAGS) -o tests/cpp/_ref/acceptance $(REF)/tests/acceptance.cpp $(REF_SRCS) $(REF_LINK); \
+	else echo "refsuites: $(REF) absent, skipped"; fi
+
 clean:
 	rm -rf build $(LIBDIR)/libgnsb.so
 	$(MAKE) -C oracle clean
 
-.PHONY: all lib oracle cpptest clean
+.PHONY: all lib oracle cpptest refsuites refsuite-unit refsuite-acceptance clean

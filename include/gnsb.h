@@ -151,10 +151,35 @@ gnsb_status gnsb_linear_pe_norms(const void* x, const void* g, void* dW, double*
  * sums[3] = ||dbias||^2.  Workspace: gnsb_linear_pe_workspace_size(B, T, 1, L). */
 gnsb_status gnsb_linear_bias_pe(const void* g, void* dbias, double* raw_b, double* sums, int64_t B, int64_t T,
                                 int64_t L, gnsb_dtype dt, void* ws, size_t ws_bytes, void* stream);
-/* Input gradient dx[r, i] = sum_j g[r, j] W[i, j] (layers.cpp:142-155); W [K, L]
- * fp32 (fp64 for GNSB_F64). */
+/* ------------------------------------------------------------------------
+ * Linear-layer GEMMs.
+ *   gnsb_linear_fwd replaces gnstk::linear_forward (proj/include/gnstk/layers.hpp:64,
+ *     proj/src/layers.cpp:52-78): y[r, l] = sum_k x[r, k] W[k, l] (+ bias[l]).
+ *   gnsb_linear_dx is the input gradient of gnstk::linear_backward_simultaneous
+ *     (proj/src/layers.cpp:142-155): dx[r, k] = sum_l g[r, l] W[k, l].
+ * x / g / y / dx: [rows, *] row tensors of dtype dt.  W [K, L] of dtype w_dt:
+ * dt itself, or GNSB_F32 master weights with bf16 rows (rounded to a bf16
+ * operand copy in the workspace each call).  bias [L]: fp32 (fp64 for fp64
+ * rows), nullable.
+ * bf16 rows with K % 8 == 0, L % 8 == 0 and 16-byte aligned buffers run the
+ * tcgen05 tensor-core kernel (bf16 operands, fp32 accumulation, any row count;
+ * tile tails are zero-filled by TMA).  Other shapes and fp32 rows run a
+ * generic fp64-accumulating kernel; fp64 rows reproduce the reference's
+ * operation order bit for bit.
+ * Workspace: gnsb_linear_gemm_workspace_size bytes (0 unless W must be converted).
+ */
+gnsb_status gnsb_linear_gemm_workspace_size(int64_t K, int64_t L, gnsb_dtype dt, gnsb_dtype w_dt, size_t* bytes);
+gnsb_status gnsb_linear_fwd(const void* x, const void* W, const void* bias, void* y, int64_t rows, int64_t K, int64_t L,
+                            gnsb_dtype dt, gnsb_dtype w_dt, void* ws, size_t ws_bytes, void* stream);
 gnsb_status gnsb_linear_dx(const void* g, const void* W, void* dx, int64_t rows, int64_t K, int64_t L, gnsb_dtype dt,
-                           void* stream);
+                           gnsb_dtype w_dt, void* ws, size_t ws_bytes, void* stream);
+
+/* Embedding row lookup out[i, :] = W[ids[i], :] (replaces gnstk::embedding_forward,
+ * proj/include/gnstk/layers.hpp:83, proj/src/layers.cpp:300-313).  ids [n] int32
+ * device, W [V, D] and out [n, D] of dtype dt.  bad_ids (nullable device int32)
+ * is set to 1 when an id was outside [0, V) (its row is written as zeros). */
+gnsb_status gnsb_embedding_fwd(const int32_t* ids, const void* W, void* out, int64_t n, int64_t V, int64_t D,
+                               gnsb_dtype dt, int32_t* bad_ids, void* stream);
 
 /* ------------------------------------------------------------------------
  * Embedding layer: table gradient + per-example squared norms (paper Alg. 3).

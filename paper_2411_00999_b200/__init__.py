@@ -21,10 +21,11 @@ from .layers import (
     synth_linear,
     synth_ln,
 )
-from .embedding import embedding_backward_simultaneous
+from .embedding import embedding_backward_simultaneous, embedding_forward
 from .nn import GnsTracker, LayerNormPE
 from .model import EmbeddingPE, LinearPE, ToyModelPE
-from .linear import LinearBackwardResult, LinearLayer, linear_backward_simultaneous, linear_perexample_sqnorm_frobenius
+from .linear import (LinearBackwardResult, LinearLayer, linear_backward_simultaneous, linear_forward,
+                     linear_perexample_sqnorm_frobenius)
 from .gns import (
     DeviceGnsAccumulator,
     EmaState,
@@ -44,5 +45,5 @@ __all__ = [
     "DeviceGnsAccumulator", "EmaState", "GnsEstimate", "GradStats", "aggregate", "ema_update", "estimate_g2",
     "estimate_s", "make_gns_estimate", "smoothed_gns", "LinearBackwardResult", "LinearLayer",
     "linear_backward_simultaneous", "linear_perexample_sqnorm_frobenius", "GnsTracker", "LayerNormPE", "EmbeddingPE", "LinearPE", "ToyModelPE",
-    "embedding_backward_simultaneous",
+    "embedding_backward_simultaneous", "embedding_forward", "linear_forward",
 ]

@@ -514,13 +514,51 @@ gnsb_status gnsb_embedding_pe(const int32_t* ids, const void* g, void* dW, doubl
     return e == cudaSuccess ? debug_ok("gnsb_embedding_pe") : cuda_fail(e, "embedding_pe launch");
 }
 
-gnsb_status gnsb_linear_dx(const void* g, const void* W, void* dx, int64_t rows, int64_t K, int64_t L, gnsb_dtype dt,
-                           void* stream) {
+static bool gemm_dtypes_ok(gnsb_dtype dt, gnsb_dtype w_dt) {
+    return (dt == GNSB_F64 && w_dt == GNSB_F64) || (dt == GNSB_F32 && w_dt == GNSB_F32) ||
+           (dt == GNSB_BF16 && (w_dt == GNSB_F32 || w_dt == GNSB_BF16));
+}
+
+gnsb_status gnsb_linear_gemm_workspace_size(int64_t K, int64_t L, gnsb_dtype dt, gnsb_dtype w_dt, size_t* bytes) {
+    if (!bytes || K < 1 || L < 1) return fail(GNSB_EINVAL, "layers: invalid extents");
+    if (!gemm_dtypes_ok(dt, w_dt)) return fail(GNSB_EINVAL, "layers: unsupported row/weight dtype pair");
+    *bytes = gnsb::gemm_workspace((int)dt, (int)w_dt, K, L);
+    return debug_ok("gnsb_linear_gemm_workspace_size");
+}
+
+static gnsb_status linear_gemm(int kind, const char* fn, const void* in, const void* W, const void* bias, void* out,
+                               int64_t rows, int64_t K, int64_t L, gnsb_dtype dt, gnsb_dtype w_dt, void* ws,
+                               size_t ws_bytes, void* stream) {
     if (rows < 0 || K < 1 || L < 1) return fail(GNSB_EINVAL, "layers: invalid extents");
+    if (!gemm_dtypes_ok(dt, w_dt)) return fail(GNSB_EINVAL, "layers: unsupported row/weight dtype pair");
+    if (gnsb_status s = need_device(fn)) return s;
+    if (rows > 0 && (!in || !W || !out)) return fail(GNSB_EINVAL, "layers: null pointer");
+    if (ws_bytes < gnsb::gemm_workspace((int)dt, (int)w_dt, K, L) || (ws_bytes > 0 && !ws))
+        return fail(GNSB_EINVAL, "layers: workspace too small (query gnsb_linear_gemm_workspace_size)");
+    const cudaError_t e = gnsb::launch_linear_gemm(kind, (int)dt, (int)w_dt, in, W, bias, out, rows, K, L, ws,
+                                                   static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? debug_ok(fn) : cuda_fail(e, "linear gemm launch");
+}
+
+gnsb_status gnsb_linear_fwd(const void* x, const void* W, const void* bias, void* y, int64_t rows, int64_t K, int64_t L,
+                            gnsb_dtype dt, gnsb_dtype w_dt, void* ws, size_t ws_bytes, void* stream) {
+    return linear_gemm(0, "gnsb_linear_fwd", x, W, bias, y, rows, K, L, dt, w_dt, ws, ws_bytes, stream);
+}
+
+gnsb_status gnsb_linear_dx(const void* g, const void* W, void* dx, int64_t rows, int64_t K, int64_t L, gnsb_dtype dt,
+                           gnsb_dtype w_dt, void* ws, size_t ws_bytes, void* stream) {
+    return linear_gemm(1, "gnsb_linear_dx", g, W, nullptr, dx, rows, K, L, dt, w_dt, ws, ws_bytes, stream);
+}
+
+gnsb_status gnsb_embedding_fwd(const int32_t* ids, const void* W, void* out, int64_t n, int64_t V, int64_t D,
+                               gnsb_dtype dt, int32_t* bad_ids, void* stream) {
+    if (n < 0 || V < 1 || D < 1) return fail(GNSB_EINVAL, "layers: invalid extents");
     if (dt != GNSB_F32 && dt != GNSB_BF16 && dt != GNSB_F64) return fail(GNSB_EINVAL, "layers: unknown dtype");
-    if (gnsb_status s = need_device("gnsb_linear_dx")) return s;
-    const cudaError_t e = gnsb::launch_linear_dx((int)dt, g, W, dx, rows, K, L, static_cast<cudaStream_t>(stream));
-    return e == cudaSuccess ? debug_ok("gnsb_linear_dx") : cuda_fail(e, "linear_dx launch");
+    if (gnsb_status s = need_device("gnsb_embedding_fwd")) return s;
+    if (n > 0 && (!ids || !W || !out)) return fail(GNSB_EINVAL, "layers: null pointer");
+    const cudaError_t e =
+        gnsb::launch_embedding_fwd((int)dt, ids, W, out, n, V, D, bad_ids, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? debug_ok("gnsb_embedding_fwd") : cuda_fail(e, "embedding_fwd launch");
 }
 
 gnsb_status gnsb_sqnorm(const void* v, int64_t n, gnsb_dtype dt, double* out, void* stream) {

@@ -691,4 +691,53 @@ cudaError_t launch_embedding_pe(int dt, const int32_t* ids, const void* g, void*
     return cudaErrorInvalidValue;
 }
 
+// ---------------------------------------------------------------- forward --
+// out[i, :] = W[ids[i], :] (proj/src/layers.cpp:300-313): one warp per token,
+// 16-byte vectors when the rows are aligned.  Ids outside [0, V) write zero
+// rows and raise *bad (the C++ drop-in checks the host ids first and throws
+// the reference's "layers: id out of range").
+template <typename T>
+__global__ void __launch_bounds__(256) emb_fwd_kernel(const int32_t* __restrict__ ids, const T* __restrict__ W,
+                                                      T* __restrict__ out, int64_t n, int64_t V, int64_t D, int vec,
+                                                      int32_t* bad) {
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= n) return;
+    const int32_t id = __ldg(ids + i);
+    const bool ok = id >= 0 && id < V;
+    if (!ok && lane == 0 && bad) *bad = 1;
+    T* dst = out + i * D;
+    if (vec) {
+        constexpr int E = 16 / sizeof(T);
+        const uint4* src = reinterpret_cast<const uint4*>(W + (ok ? (int64_t)id : 0) * D);
+        for (int64_t v = lane; v < D / E; v += 32)
+            reinterpret_cast<uint4*>(dst)[v] = ok ? __ldg(src + v) : make_uint4(0, 0, 0, 0);
+    } else {
+        for (int64_t d = lane; d < D; d += 32) dst[d] = ok ? W[(int64_t)id * D + d] : T(0);
+    }
+}
+
+cudaError_t launch_embedding_fwd(int dt, const int32_t* ids, const void* W, void* out, int64_t n, int64_t V, int64_t D,
+                                 int32_t* bad, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    const size_t es = dt == 2 ? 8 : dt == 0 ? 4 : 2;
+    const int vec = (D * (int64_t)es) % 16 == 0 && (reinterpret_cast<uintptr_t>(W) & 15u) == 0 &&
+                    (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
+    const unsigned grid = (unsigned)((n + 7) / 8);
+    if (bad) {
+        cudaError_t e = cudaMemsetAsync(bad, 0, 4, st);
+        if (e != cudaSuccess) return e;
+    }
+    switch (dt) {
+        case 0: emb_fwd_kernel<float><<<grid, 256, 0, st>>>(ids, (const float*)W, (float*)out, n, V, D, vec, bad); break;
+        case 1:
+            emb_fwd_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(ids, (const __nv_bfloat16*)W, (__nv_bfloat16*)out, n,
+                                                                V, D, vec, bad);
+            break;
+        case 2: emb_fwd_kernel<double><<<grid, 256, 0, st>>>(ids, (const double*)W, (double*)out, n, V, D, vec, bad); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
 }  // namespace gnsb

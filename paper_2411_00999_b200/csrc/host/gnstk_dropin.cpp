@@ -10,6 +10,8 @@
 
 #include <cmath>
 #include <cstring>
+#include <optional>
+#include <span>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -21,48 +23,6 @@
 #include "gnstk/tensor.hpp"
 
 namespace gnstk {
-
-// ---------------------------------------------------------------- Tensor --
-namespace {
-std::size_t numel(const Shape& s) {
-    std::size_t n = 1;
-    for (Index e : s) {
-        if (e < 0) throw std::invalid_argument("tensor: negative extent");
-        n *= static_cast<std::size_t>(e);
-    }
-    return n;
-}
-}  // namespace
-
-Tensor::Tensor(Shape shape) : shape_(std::move(shape)), data_(numel(shape_), 0.0) {}
-Tensor::Tensor(Shape shape, std::vector<double> data) : shape_(std::move(shape)), data_(std::move(data)) {
-    if (data_.size() != numel(shape_)) throw std::invalid_argument("tensor: data size does not match shape");
-}
-Tensor Tensor::scalar(double v) { return Tensor(Shape{}, std::vector<double>{v}); }
-Tensor Tensor::full(Shape shape, double v) {
-    Tensor t(std::move(shape));
-    for (auto& x : t.data_) x = v;
-    return t;
-}
-double Tensor::item() const {
-    if (data_.size() != 1) throw std::invalid_argument("tensor: item() needs exactly one element");
-    return data_[0];
-}
-Tensor scale(const Tensor& a, double c) {
-    Tensor r(a.shape());
-    for (Index i = 0; i < a.size(); ++i) r[i] = a[i] * c;
-    return r;
-}
-double sum_all(const Tensor& a) {
-    double s = 0.0;
-    for (Index i = 0; i < a.size(); ++i) s += a[i];
-    return s;
-}
-double sqnorm_all(const Tensor& a) {
-    double s = 0.0;
-    for (Index i = 0; i < a.size(); ++i) s += a[i] * a[i];
-    return s;
-}
 
 // ------------------------------------------------------- device plumbing --
 namespace {
@@ -235,9 +195,27 @@ LinearBackwardResult linear_backward_simultaneous(const LinearLayer& layer, cons
     if (layer.bias) res.grads.per_example_sqnorms["bias"] = corrected(sums[1], vx.b);
     res.input_grad = Tensor(x.shape());
     DevBuf ddx(sizeof(double) * x.size());
-    check(gnsb_linear_dx(dg.p, dWt.p, ddx.p, vx.b * vx.m, k, l, GNSB_F64, nullptr));
+    check(gnsb_linear_dx(dg.p, dWt.p, ddx.p, vx.b * vx.m, k, l, GNSB_F64, GNSB_F64, nullptr, 0, nullptr));
     download(res.input_grad, ddx);
     return res;
+}
+
+Tensor linear_forward(const LinearLayer& layer, const Tensor& x) {
+    const Index k = layer.weight.rank() == 2 ? layer.weight.shape()[0] : 0;
+    const Index l = layer.weight.rank() == 2 ? layer.weight.shape()[1] : 0;
+    const Bmk v = bmk_view(x);  // layers.cpp:55-57, in the reference's order
+    if (v.k != k) fail("input trailing extent does not match weight rows");
+    if (layer.bias && layer.bias->shape() != Shape{l}) fail("bias extent does not match weight columns");
+    Shape os = x.shape();
+    os.back() = l;
+    Tensor y(os);
+    const Index rows = v.b * v.m;
+    if (rows == 0 || l == 0) return y;
+    DevBuf dx = upload(x), dw = upload(layer.weight), dy(sizeof(double) * y.size());
+    DevBuf db = layer.bias ? upload(*layer.bias) : DevBuf(0);
+    check(gnsb_linear_fwd(dx.p, dw.p, db.p, dy.p, rows, k, l, GNSB_F64, GNSB_F64, nullptr, 0, nullptr));
+    download(y, dy);
+    return y;
 }
 
 Tensor linear_perexample_sqnorm_frobenius(const Tensor& x, const Tensor& g) {
@@ -258,6 +236,21 @@ Tensor linear_perexample_sqnorm_frobenius(const Tensor& x, const Tensor& g) {
 }
 
 // -------------------------------------------------------------- embedding --
+Tensor embedding_forward(const EmbeddingLayer& layer, std::span<const std::int32_t> ids, Index batch, Index t_len) {
+    const Index v = layer.vocab(), d = layer.dim();
+    if (static_cast<Index>(ids.size()) != batch * t_len) fail("id count does not match batch * t_len");
+    for (std::int32_t id : ids)  // layers.cpp:307; the host ids are checked before any device work
+        if (id < 0 || id >= v) fail("id out of range");
+    Tensor out({batch, t_len, d});
+    if (out.size() == 0) return out;
+    DevBuf dw = upload(layer.weight), dids(sizeof(std::int32_t) * ids.size()), dout(sizeof(double) * out.size());
+    cuda_check(cudaMemcpy(dids.p, ids.data(), sizeof(std::int32_t) * ids.size(), cudaMemcpyHostToDevice), "upload");
+    check(gnsb_embedding_fwd(static_cast<const std::int32_t*>(dids.p), dw.p, dout.p, batch * t_len, v, d, GNSB_F64,
+                             nullptr, nullptr));
+    download(out, dout);
+    return out;
+}
+
 LayerGradOutput embedding_backward_simultaneous(const EmbeddingLayer& layer, std::span<const std::int32_t> ids,
                                                 Index batch, Index t_len, const Tensor& g) {
     const Index v = layer.vocab();
@@ -355,6 +348,99 @@ GradStats aggregate(const std::map<LayerKey, GradStats>& stats_by_layer, std::op
     return GradStats{out.g_big_sqnorm, out.g_small_sqnorm_mean, out.b_big, out.b_small, out.n_small};
 }
 
+// Offline statistics over logged GNS series (proj/src/gns.cpp:91-196).  Host
+// code: O(steps) scalars, consumed by the reference's simulator and CLI.
+JackknifeResult jackknife_ratio_stderr(std::span<const std::pair<double, double>> pairs) {
+    auto bad = [](const char* m) { throw std::invalid_argument(std::string("gns: ") + m); };
+    const std::size_t n = pairs.size();
+    if (n < 2) bad("jackknife needs at least 2 pairs");
+    double ts = 0.0, tg = 0.0;
+    for (const auto& p : pairs) {
+        ts += p.first;
+        tg += p.second;
+    }
+    if (tg == 0.0) bad("jackknife ratio denominator is zero");
+    const double nd = static_cast<double>(n);
+    JackknifeResult r;
+    r.ratio = (ts / nd) / (tg / nd);
+    // leave-one-out ratios, then their spread about their mean
+    std::vector<double> loo;
+    loo.reserve(n);
+    double mean = 0.0;
+    for (const auto& p : pairs) {
+        if (tg - p.second == 0.0) bad("jackknife leave-one-out denominator is zero");
+        loo.push_back((ts - p.first) / (tg - p.second));
+        mean += loo.back();
+    }
+    mean /= nd;
+    double ss = 0.0;
+    for (double v : loo) ss += (v - mean) * (v - mean);
+    r.std_error = std::sqrt((nd - 1.0) / nd * ss);
+    return r;
+}
+
+namespace {
+// EMA-smoothed B_simple per step under one alpha; nullopt where undefined
+std::vector<std::optional<double>> smoothed_ratios(const GnsSeries& s, double alpha) {
+    std::vector<std::optional<double>> out(s.g2.size());
+    EmaState eg{alpha}, es{alpha};
+    for (std::size_t i = 0; i < s.g2.size(); ++i) {
+        eg = ema_update(eg, s.g2[i]);
+        es = ema_update(es, s.s[i]);
+        const GnsEstimate e = smoothed_gns(eg, es);
+        if (e.b_simple_defined) out[i] = e.b_simple;
+    }
+    return out;
+}
+}  // namespace
+
+std::vector<RegressionRow> regress_layer_gns(const GnsSeries& total, const std::map<LayerType, GnsSeries>& per_type,
+                                             std::span<const double> alphas) {
+    auto bad = [](const char* m) { throw std::invalid_argument(std::string("gns: ") + m); };
+    if (total.g2.size() != total.s.size()) bad("total series components misaligned");
+    std::vector<RegressionRow> rows;
+    for (const auto& [type, ser] : per_type) {
+        if (ser.g2.size() != total.g2.size() || ser.s.size() != total.s.size())
+            bad("per-type series not aligned with total");
+        for (double alpha : alphas) {
+            const auto ys = smoothed_ratios(total, alpha), xs = smoothed_ratios(ser, alpha);
+            std::vector<double> x, y;  // pairwise-complete steps
+            for (std::size_t i = 0; i < xs.size(); ++i)
+                if (xs[i] && ys[i]) {
+                    x.push_back(*xs[i]);
+                    y.push_back(*ys[i]);
+                }
+            if (x.size() < 3) bad("fewer than 3 aligned points for regression");
+            const double nd = static_cast<double>(x.size());
+            double mx = 0.0, my = 0.0;
+            for (std::size_t i = 0; i < x.size(); ++i) {
+                mx += x[i];
+                my += y[i];
+            }
+            mx /= nd;
+            my /= nd;
+            double sxx = 0.0, syy = 0.0, sxy = 0.0;
+            for (std::size_t i = 0; i < x.size(); ++i) {
+                const double dx = x[i] - mx, dy = y[i] - my;
+                sxx += dx * dx;
+                syy += dy * dy;
+                sxy += dx * dy;
+            }
+            RegressionRow row{type, alpha};
+            if (sxx > 0.0) {
+                row.slope = sxy / sxx;
+                row.slope_defined = true;
+                if (syy > 0.0) {
+                    row.pearson_r = sxy / std::sqrt(sxx * syy);
+                    row.r_defined = true;
+                }
+            }
+            rows.push_back(row);
+        }
+    }
+    return rows;
+}
+
 // -------------------------------------------------------------- costmodel --
 std::string cost_method_name(CostMethod m) { return m == CostMethod::Simultaneous ? "simultaneous" : "frobenius"; }
 
@@ -371,8 +457,8 @@ CostPair io_values(const CostShape& s, CostMethod m) {
 }
 
 CostPair io_bytes(const CostShape& s, CostMethod m) {
+    const CostPair v = io_values(s, m);  // extents are checked first, as in the reference
     if (s.bytes_per_value < 1) throw std::invalid_argument("costmodel: bytes_per_value must be positive");
-    const CostPair v = io_values(s, m);
     return CostPair{v.weight_grad * s.bytes_per_value, v.grad_norms * s.bytes_per_value};
 }
 
@@ -380,6 +466,26 @@ double crossover_t(std::int64_t k, std::int64_t l, CostCriterion c) {
     double out = 0.0;
     check(gnsb_crossover_t(k, l, c == CostCriterion::IO ? 0 : 1, &out));
     return out;
+}
+
+std::vector<SweepRow> sweep(std::span<const CostShape> shapes) {
+    if (shapes.empty()) throw std::invalid_argument("costmodel: empty sweep grid");
+    std::vector<SweepRow> rows;
+    for (const CostShape& s : shapes) {
+        const double frob_norms = static_cast<double>(flops(s, CostMethod::Frobenius).grad_norms);
+        for (CostMethod m : {CostMethod::Simultaneous, CostMethod::Frobenius}) {
+            const CostPair f = flops(s, m), io = io_values(s, m);
+            rows.push_back(SweepRow{m, s.b, s.t, s.k, s.l, f.weight_grad, f.grad_norms, io.weight_grad, io.grad_norms,
+                                    static_cast<double>(f.grad_norms) / frob_norms});
+        }
+    }
+    return rows;
+}
+
+std::int64_t layernorm_norms_io_values(const CostShape& s) {
+    io_values(s, CostMethod::Simultaneous);  // the reference's shape check
+    if (s.bytes_per_value < 1) throw std::invalid_argument("costmodel: bytes_per_value must be positive");
+    return s.b * s.k + s.b;
 }
 
 }  // namespace gnstk

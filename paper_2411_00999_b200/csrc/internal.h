@@ -93,7 +93,12 @@ bool embedding_shape_ok(int64_t T);
 size_t embedding_workspace(int64_t B, int64_t T, int64_t V, int64_t D, int dt);
 cudaError_t launch_embedding_pe(int dt, const int32_t* ids, const void* g, void* dW, double* raw, double* sums,
                                 int64_t B, int64_t T, int64_t V, int64_t D, void* ws, int32_t* bad, cudaStream_t st);
-cudaError_t launch_linear_dx(int dt, const void* g, const void* W, void* dx, int64_t rows, int64_t K, int64_t L,
-                             cudaStream_t st);
+cudaError_t launch_embedding_fwd(int dt, const int32_t* ids, const void* W, void* out, int64_t n, int64_t V, int64_t D,
+                                 int32_t* bad, cudaStream_t st);
+// linear-layer GEMMs (linear_gemm.cu): kind 0 forward y = x W + bias, kind 1 dx = g W^T
+bool gemm_tc_ok(int dt, int64_t K, int64_t L);
+size_t gemm_workspace(int dt, int w_dt, int64_t K, int64_t L);
+cudaError_t launch_linear_gemm(int kind, int dt, int w_dt, const void* in, const void* W, const void* bias, void* out,
+                               int64_t rows, int64_t K, int64_t L, void* ws, cudaStream_t st);
 
 }  // namespace gnsb

@@ -1,0 +1,375 @@
+// linear_gemm.cu — the two dense GEMMs of a linear layer on sm_100a tensor
+// cores (tcgen05 + TMEM + TMA), any row count and tile tails:
+//
+//   forward   y[r, l]  = sum_k x[r, k] W[k, l] (+ bias[l])   (proj/src/layers.cpp:52-78)
+//   input grad dx[r, k] = sum_l g[r, l] W[k, l]               (proj/src/layers.cpp:142-155)
+//
+// Both are D[M=rows, N] = A[M, Kr] * B with A the row tensor (K-major: the
+// reduced axis is contiguous).  B is W read in place: MN-major for the
+// forward (W[k, :] contiguous along N = L), K-major for dx (W[k, :]
+// contiguous along the reduced L).  bf16 operands, fp32 accumulation in TMEM.
+//
+// Kernel (gemm_kernel<B_KMAJOR, BIAS>): persistent, one CTA per SM, static
+// round-robin over 128 x 256 output tiles with the N tile fastest (the CTAs
+// of one wave share an A row block through L2; W stays L2-resident).
+//   warp 0      TMA producer: A box 64 x 128 (16 KB) and B 64 x 256 (32 KB)
+//               per 64-deep K block into a 4-stage ring; rows, columns and K
+//               past the tensor are zero-filled by TMA, so no shape is
+//               special-cased;
+//   warp 1      one elected thread issues tcgen05.mma M=128 N=256 K=16 into
+//               one of two 256-column TMEM accumulators (tiles alternate, so
+//               the epilogue of tile i overlaps the MMAs of tile i+1);
+//   warps 2..9  epilogue: tcgen05.ld 32 columns at a time, + bias, round to
+//               bf16, 16-byte stores (rows / columns past the output skipped).
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <mutex>
+
+#include "common.cuh"
+#include "internal.h"
+#include "tc.cuh"
+
+namespace gnsb {
+
+namespace gm {
+constexpr int BM = 128, BN = 256, BK = 64;
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;  // 16 KB
+constexpr int B_BYTES = BN * BK * 2;  // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int EPI_WARPS = 8;
+constexpr int THREADS = (2 + EPI_WARPS) * 32;
+constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 256;
+constexpr int TMEM_COLS = 512;
+}  // namespace gm
+
+struct GemmArgs {
+    int M, N, Kr;         // output rows, output columns, reduced extent
+    int tiles_m, tiles_n;
+    const float* bias;    // [N] (BIAS)
+    __nv_bfloat16* out;   // [M, N]
+};
+
+template <bool B_KMAJOR, bool BIAS>
+__global__ void __launch_bounds__(gm::THREADS, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb, GemmArgs a) {
+    using namespace gm;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem =
+        reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char* ring = smem;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)STAGES * STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;  // [2]
+    uint64_t* tempty = tfull + 2;      // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ntiles = a.tiles_m * a.tiles_n;
+    const int kblocks = (a.Kr + BK - 1) / BK;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&tfull[s], 1);
+            mbar_init(&tempty[s], EPI_WARPS);
+        }
+        fence_mbar_init();
+        tc::prefetch_tmap(&tma);
+        tc::prefetch_tmap(&tmb);
+    }
+    if (warp == 1) tc::tmem_alloc<TMEM_COLS>(tmem_slot);
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tmem = *tmem_slot;
+    // the inputs may be produced by the previous kernel in the stream (PDL)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+
+    if (warp == 0) {
+        // -------------------------------------------------------- producer --
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const int m0 = (t / a.tiles_n) * BM, n0 = (t % a.tiles_n) * BN;
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    mbar_wait(&empty[s], ph ^ 1u);
+                    unsigned char* st = ring + (size_t)s * STAGE_BYTES;
+                    mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+                    const int k0 = kb * BK;
+                    tc::tma_load_3d(st, &tma, k0, m0, 0, &full[s]);  // A: 64 (K) x 128 rows
+                    if constexpr (B_KMAJOR) {
+                        tc::tma_load_3d(st + A_BYTES, &tmb, k0, n0, 0, &full[s]);  // B: 64 (K) x 256 rows
+                    } else {
+#pragma unroll
+                        for (int h = 0; h < BN / 64; ++h)  // B: 64 (N) x 64 (K) chunks along N
+                            tc::tma_load_3d(st + A_BYTES + h * 8192, &tmb, n0 + 64 * h, k0, 0, &full[s]);
+                    }
+                    if (++s == STAGES) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------ MMA issuer --
+        if (lane == 0) {
+            constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, false, !B_KMAJOR);
+            int s = 0, buf = 0;
+            uint32_t ph = 0, tph = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                mbar_wait(&tempty[buf], tph ^ 1u);  // epilogue drained this accumulator
+                tc::fence_after_sync();
+                const uint32_t dcol = tmem + (uint32_t)(buf * BN);
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    mbar_wait(&full[s], ph);
+                    tc::fence_after_sync();
+                    const uint32_t abase = smem_u32(ring + (size_t)s * STAGE_BYTES);
+                    const uint32_t bbase = abase + A_BYTES;
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k) {
+                        // K-major SW128: 8-row x 128-byte atoms (SBO 1 KB), a K step of 16 = 32 bytes;
+                        // MN-major SW128: 64-element x 8-row atoms, LBO = next 64 columns (8 KB),
+                        // SBO = next 8 K rows (1 KB), a K step of 16 rows = 2 KB
+                        const uint64_t ad = tc::smem_desc_sw128(abase + k * 32, 16, 1024);
+                        const uint64_t bd = B_KMAJOR ? tc::smem_desc_sw128(bbase + k * 32, 16, 1024)
+                                                     : tc::smem_desc_sw128(bbase + k * 2048, 8192, 1024);
+                        tc::mma_bf16(dcol, ad, bd, idesc, (kb | k) != 0);
+                    }
+                    tc::commit(&empty[s]);  // smem slot free once these MMAs retire
+                    if (++s == STAGES) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+                tc::commit(&tfull[buf]);  // accumulator of this tile complete
+                if (++buf == 2) {
+                    buf = 0;
+                    tph ^= 1u;
+                }
+            }
+        }
+    } else {
+        // -------------------------------------------------------- epilogue --
+        const int e = warp - 2;
+        const int quad = warp & 3;  // TMEM lanes this warp may access
+        const int half = e / 4;     // column half of the 256-wide tile
+        int buf = 0;
+        uint32_t tph = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const int m0 = (t / a.tiles_n) * BM, n0 = (t % a.tiles_n) * BN;
+            const int row = m0 + quad * 32 + lane;
+            mbar_wait(&tfull[buf], tph);
+            tc::fence_after_sync();
+            const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN + half * 128);
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) {
+                uint32_t r[32];
+                tc::tmem_ld_32x32b_x32(base + cc * 32, r);
+                tc::tmem_ld_wait();
+                if (cc == 3) {  // the accumulator is in registers: hand it back to the MMA warp
+                    tc::fence_before_sync();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[buf]);
+                }
+                const int c0 = n0 + half * 128 + cc * 32;
+                if (row >= a.M) continue;
+                __nv_bfloat16* dst = a.out + (size_t)row * a.N + c0;
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    if (c0 + 8 * v >= a.N) break;  // N % 8 == 0: a vector is fully in or out
+                    float f[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) f[j] = __uint_as_float(r[8 * v + j]);
+                    if constexpr (BIAS) {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) f[j] += __ldg(a.bias + c0 + 8 * v + j);
+                    }
+                    uint4 o;
+                    o.x = pack_bf16x2(f[0], f[1]);
+                    o.y = pack_bf16x2(f[2], f[3]);
+                    o.z = pack_bf16x2(f[4], f[5]);
+                    o.w = pack_bf16x2(f[6], f[7]);
+                    *reinterpret_cast<uint4*>(dst + 8 * v) = o;
+                }
+            }
+            if (++buf == 2) {
+                buf = 0;
+                tph ^= 1u;
+            }
+        }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 1) {
+        tc::fence_after_sync();
+        tc::tmem_dealloc<TMEM_COLS>(tmem);
+    }
+}
+
+// fp32 master weights -> bf16 operand copy (RNE)
+__global__ void __launch_bounds__(256) f32_to_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
+                                                          int64_t n) {
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    if (i + 4 <= n) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(in + i));
+        uint2 o;
+        o.x = pack_bf16x2(v.x, v.y);
+        o.y = pack_bf16x2(v.z, v.w);
+        *reinterpret_cast<uint2*>(out + i) = o;
+    } else {
+        for (int64_t j = i; j < n; ++j) out[j] = __float2bfloat16_rn(in[j]);
+    }
+}
+
+// ----------------------------------------------------- generic (any dtype) --
+// One thread per output; fp64 accumulation in the reference's order (k, then
+// bias last) without contraction, so fp64 rows reproduce layers.cpp:52-78 and
+// :142-155 bit for bit.
+template <typename T, typename WT, bool FWD>
+__global__ void __launch_bounds__(256) gemm_generic_kernel(const T* a, const WT* W, const void* bias, int bias_f64,
+                                                           T* out, int64_t rows, int64_t N, int64_t Kr, int64_t ldw) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= rows * N) return;
+    const int64_t r = idx / N, n = idx % N;
+    double acc = 0.0;
+    for (int64_t k = 0; k < Kr; ++k) {
+        const double w = (double)to_acc<WT>(FWD ? W[k * ldw + n] : W[n * ldw + k]);
+        acc = __dadd_rn(acc, __dmul_rn((double)to_acc<T>(a[r * Kr + k]), w));
+    }
+    if (bias) acc = __dadd_rn(acc, bias_f64 ? static_cast<const double*>(bias)[n] : (double)static_cast<const float*>(bias)[n]);
+    out[idx] = from_acc<T>((typename Traits<T>::Acc)acc);
+}
+
+// ------------------------------------------------------------------ host --
+namespace {
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    });
+    return fn;
+}
+
+// [rows, cols] bf16 row-major (cols innermost) as a 3-D map with a unit
+// outer axis; box {bc, br}, 128-byte swizzle, out-of-range elements read 0
+bool make_map_2d(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int bc, int br) {
+    EncodeFn enc = encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, 1};
+    cuuint64_t strides[2] = {(cuuint64_t)cols * 2, (cuuint64_t)rows * cols * 2};
+    cuuint32_t box[3] = {(cuuint32_t)bc, (cuuint32_t)br, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <bool BK_, bool BIAS>
+cudaError_t launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, cudaStream_t st) {
+    const void* fn = reinterpret_cast<const void*>(gemm_kernel<BK_, BIAS>);
+    cudaError_t e = ensure_smem_attr(fn, gm::SMEM);
+    if (e != cudaSuccess) return e;
+    const int ntiles = a.tiles_m * a.tiles_n;
+    const int sms = device_sm_count();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ntiles < sms ? ntiles : sms);
+    cfg.blockDim = dim3(gm::THREADS);
+    cfg.dynamicSmemBytes = gm::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, gemm_kernel<BK_, BIAS>, ma, mb, a);
+}
+
+}  // namespace
+
+bool gemm_tc_ok(int dt, int64_t K, int64_t L) {
+    return dt == 1 && K % 8 == 0 && L % 8 == 0 && K < (1ll << 31) && L < (1ll << 31);
+}
+static bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+size_t gemm_workspace(int dt, int w_dt, int64_t K, int64_t L) {
+    return (dt == 1 && w_dt == 0 && gemm_tc_ok(dt, K, L)) ? (size_t)K * L * 2 : 0;
+}
+
+// kind 0: forward y = x W + bias; kind 1: dx = g W^T.  dt / w_dt: 0 f32, 1 bf16, 2 f64.
+cudaError_t launch_linear_gemm(int kind, int dt, int w_dt, const void* in, const void* W, const void* bias, void* out,
+                               int64_t rows, int64_t K, int64_t L, void* ws, cudaStream_t st) {
+    const int64_t N = kind == 0 ? L : K, Kr = kind == 0 ? K : L;
+    if (rows == 0) return cudaSuccess;
+    if (gemm_tc_ok(dt, K, L) && rows < (1ll << 31) && al16(in) && al16(out) && (w_dt == 0 || al16(W))) {
+        const void* wb = W;
+        if (w_dt == 0) {  // fp32 master weights: bf16 operand copy in the workspace
+            const int64_t n = K * L;
+            f32_to_bf16_kernel<<<(unsigned)((n / 4 + 255) / 256 + 1), 256, 0, st>>>(
+                static_cast<const float*>(W), static_cast<__nv_bfloat16*>(ws), n);
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) return e;
+            wb = ws;
+        }
+        CUtensorMap ma, mb;
+        if (!make_map_2d(&ma, in, rows, Kr, gm::BK, gm::BM)) return cudaErrorInvalidValue;
+        const bool ok = kind == 0 ? make_map_2d(&mb, wb, K, L, 64, gm::BK)       // W [K, L]: box 64 (L) x 64 (K)
+                                  : make_map_2d(&mb, wb, K, L, gm::BK, gm::BN);  // W [K, L]: box 64 (L) x 256 (K)
+        if (!ok) return cudaErrorInvalidValue;
+        GemmArgs a{};
+        a.M = (int)rows;
+        a.N = (int)N;
+        a.Kr = (int)Kr;
+        a.tiles_m = (int)((rows + gm::BM - 1) / gm::BM);
+        a.tiles_n = (int)((N + gm::BN - 1) / gm::BN);
+        a.bias = static_cast<const float*>(bias);
+        a.out = static_cast<__nv_bfloat16*>(out);
+        if (kind == 1) return launch_tc<true, false>(ma, mb, a, st);
+        return bias ? launch_tc<false, true>(ma, mb, a, st) : launch_tc<false, false>(ma, mb, a, st);
+    }
+    const int64_t n = rows * N;
+    const unsigned grid = (unsigned)((n + 255) / 256);
+    const int bias_f64 = dt == 2;
+    const int64_t ldw = L;
+#define GNSB_GEMM_GENERIC(T, WT)                                                                                     \
+    do {                                                                                                             \
+        if (kind == 0)                                                                                               \
+            gemm_generic_kernel<T, WT, true><<<grid, 256, 0, st>>>(static_cast<const T*>(in),                       \
+                                                                   static_cast<const WT*>(W), bias, bias_f64,        \
+                                                                   static_cast<T*>(out), rows, N, Kr, ldw);          \
+        else                                                                                                         \
+            gemm_generic_kernel<T, WT, false><<<grid, 256, 0, st>>>(static_cast<const T*>(in),                      \
+                                                                    static_cast<const WT*>(W), nullptr, 0,           \
+                                                                    static_cast<T*>(out), rows, N, Kr, ldw);         \
+    } while (0)
+    if (dt == 2 && w_dt == 2)
+        GNSB_GEMM_GENERIC(double, double);
+    else if (dt == 0 && w_dt == 0)
+        GNSB_GEMM_GENERIC(float, float);
+    else if (dt == 1 && w_dt == 0)
+        GNSB_GEMM_GENERIC(__nv_bfloat16, float);
+    else if (dt == 1 && w_dt == 1)
+        GNSB_GEMM_GENERIC(__nv_bfloat16, __nv_bfloat16);
+    else
+        return cudaErrorInvalidValue;
+#undef GNSB_GEMM_GENERIC
+    return cudaGetLastError();
+}
+
+}  // namespace gnsb

@@ -640,18 +640,6 @@ __global__ void __launch_bounds__(256) bias_pe_kernel(const T* g, int64_t B, int
     }
 }
 
-// dx[row, i] = sum_j g[row, j] * W[i, j] (layers.cpp:142-155), fp64 accumulation
-template <typename T, typename WT>
-__global__ void __launch_bounds__(256) linear_dx_kernel(const T* g, const WT* W, T* dx, int64_t rows, int64_t K,
-                                                        int64_t L) {
-    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= rows * K) return;
-    const int64_t r = idx / K, i = idx % K;
-    double acc = 0.0;
-    for (int64_t j = 0; j < L; ++j) acc += (double)to_acc<T>(g[r * L + j]) * (double)W[i * L + j];
-    dx[idx] = from_acc<T>((typename Traits<T>::Acc)acc);
-}
-
 // Gram form, generic: raw_b = sum_{t,u} (x_t . x_u)(g_t . g_u), one thread per (t, u)
 template <typename T>
 __global__ void __launch_bounds__(256) gram_generic_kernel(const T* x, const T* g, int64_t B, int64_t Tn, int64_t K,
@@ -722,28 +710,6 @@ cudaError_t launch_linear_generic(int dt, int kind, const void* x, const void* g
         case 2: return launch_generic_t<double>(kind, x, g, out_grad, out_f64, raw, sums, sum_slot, B, T, K, L, ws, st);
     }
     return cudaErrorInvalidValue;
-}
-
-cudaError_t launch_linear_dx(int dt, const void* g, const void* W, void* dx, int64_t rows, int64_t K, int64_t L,
-                             cudaStream_t st) {
-    const int64_t n = rows * K;
-    const int grid = (int)((n + 255) / 256);
-    if (n == 0) return cudaSuccess;
-    switch (dt) {
-        case 0:
-            linear_dx_kernel<float, float><<<grid, 256, 0, st>>>((const float*)g, (const float*)W, (float*)dx, rows, K, L);
-            break;
-        case 1:
-            linear_dx_kernel<__nv_bfloat16, float><<<grid, 256, 0, st>>>((const __nv_bfloat16*)g, (const float*)W,
-                                                                         (__nv_bfloat16*)dx, rows, K, L);
-            break;
-        case 2:
-            linear_dx_kernel<double, double><<<grid, 256, 0, st>>>((const double*)g, (const double*)W, (double*)dx,
-                                                                   rows, K, L);
-            break;
-        default: return cudaErrorInvalidValue;
-    }
-    return cudaGetLastError();
 }
 
 }  // namespace gnsb

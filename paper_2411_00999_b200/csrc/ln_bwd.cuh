@@ -669,30 +669,30 @@ __device__ __forceinline__ void ln_bwd_reduce_body(const LnRedArgs& a, const int
             }
             __syncthreads();
         }
-        // one pass, two roles (no barrier between them): threads [0, nb) square
-        // and sum their example over this CTA's columns; threads [nb, nb + 2 ncol)
-        // add their column over the block's examples.  Both in fixed order.
-        {
-            const int t = threadIdx.x;
-            const int nroles = (NORMS ? (int)nb : 0) + 2 * ncol;
-            for (int r = t; r < nroles; r += nthreads) {
-                if (NORMS && r < nb) {
-                    const double* vg = sv + (size_t)r * svs;
-                    double qg = 0.0, qb = 0.0;
-#pragma unroll 4
-                    for (int j = 0; j < ncol; ++j) {
-                        qg = fma(vg[j], vg[j], qg);
-                        qb = fma(vg[ncol + j], vg[ncol + j], qb);
-                    }
-                    a.q[((size_t)(b0 + r) * grid + cta) * 2 + 0] = qg;
-                    a.q[((size_t)(b0 + r) * grid + cta) * 2 + 1] = qb;
-                } else {
-                    const int j = r - (NORMS ? (int)nb : 0);
-                    const int h = j / ncol, jj = j - h * ncol;
-                    double acc = 0.0;
+        // two roles over the same read-only sv (no barrier between them): a
+        // thread per column adds it over the block's examples; a warp per
+        // example squares and sums it over this CTA's columns (lane-strided,
+        // then a fixed butterfly: the chain per lane is ncol/16 long, not
+        // 2 ncol).  Both in fixed order.
+        for (int j = threadIdx.x; j < 2 * ncol; j += nthreads) {
+            const int h = j / ncol, jj = j - h * ncol;
+            double acc = 0.0;
 #pragma unroll 8
-                    for (int64_t bb = 0; bb < nb; ++bb) acc += sv[bb * svs + h * ncol + jj];
-                    colsum[j] += acc;
+            for (int64_t bb = 0; bb < nb; ++bb) acc += sv[bb * svs + h * ncol + jj];
+            colsum[j] += acc;
+        }
+        if constexpr (NORMS) {
+            for (int r = warp; r < nb; r += nwarps) {
+                const double* vg = sv + (size_t)r * svs;
+                double q2[2] = {0.0, 0.0};
+                for (int j = lane; j < ncol; j += 32) {
+                    q2[0] = fma(vg[j], vg[j], q2[0]);
+                    q2[1] = fma(vg[ncol + j], vg[ncol + j], q2[1]);
+                }
+                warp_sum_n(q2);
+                if (lane == 0) {
+                    a.q[((size_t)(b0 + r) * grid + cta) * 2 + 0] = q2[0];
+                    a.q[((size_t)(b0 + r) * grid + cta) * 2 + 1] = q2[1];
                 }
             }
         }

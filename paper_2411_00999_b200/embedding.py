@@ -1,7 +1,9 @@
 """Embedding-table gradient with per-example squared norms (paper Alg. 3).
 
-Mirrors gnstk::embedding_backward_simultaneous (proj/include/gnstk/layers.hpp:85-88,
-proj/src/layers.cpp:315-368) over the C ABI `gnsb_embedding_pe`.
+Mirrors gnstk::embedding_forward (proj/include/gnstk/layers.hpp:83,
+proj/src/layers.cpp:300-313) over `gnsb_embedding_fwd` and
+gnstk::embedding_backward_simultaneous (layers.hpp:85-88, layers.cpp:315-368)
+over `gnsb_embedding_pe`.
 """
 from __future__ import annotations
 
@@ -41,3 +43,21 @@ def embedding_backward_simultaneous(ids: torch.Tensor, g: torch.Tensor, vocab: i
                                             _ptr(ws), ws.numel(), None, _stream_ptr(dev)))
     bd = float(B)
     return LayerGradOutput({"weight": dW}, {"weight": sums[0] / bd * (bd * bd)}, {"weight": raw}, B, sums)
+
+
+def embedding_forward(weight: torch.Tensor, ids: torch.Tensor, batch: int, t_len: int) -> torch.Tensor:
+    """out[b, t, :] = weight[ids[b * t_len + t], :] (layers.cpp:300-313); [batch, t_len, D]."""
+    if ids.numel() != batch * t_len:
+        raise ValueError("layers: id count does not match batch * t_len")
+    V, D = int(weight.shape[0]), int(weight.shape[1])
+    if ids.numel() and (int(ids.min()) < 0 or int(ids.max()) >= V):
+        raise ValueError("layers: id out of range")
+    if not weight.is_cuda:
+        raise RuntimeError("layers: the B200 path has no CPU fallback (weights are on the CPU)")
+    dev = weight.device
+    ids = ids.to(device=dev, dtype=torch.int32).contiguous()
+    w = weight.contiguous()
+    out = torch.empty(batch, t_len, D, dtype=w.dtype, device=dev)
+    _lib.check(_lib.lib().gnsb_embedding_fwd(_ptr(ids), _ptr(w), _ptr(out), batch * t_len, V, D, gnsb_dtype(w.dtype),
+                                             None, _stream_ptr(dev)))
+    return out

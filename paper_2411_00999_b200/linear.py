@@ -101,10 +101,58 @@ def linear_backward_simultaneous(layer: LinearLayer, x: torch.Tensor, g: torch.T
         raw["bias"] = raw_b
     dx = None
     if need_input_grad:
-        W = layer.weight.to(device=dev, dtype=sd).contiguous()
         dx = torch.empty_like(x)
-        _lib.check(h.gnsb_linear_dx(_ptr(g), _ptr(W), _ptr(dx), B * M, K, L, dt, sp))
+        linear_gemm("dx", g, layer.weight, None, dx, B * M, K, L)
     return LinearBackwardResult(LayerGradOutput(weight_grads, per_ex, raw, B, sums), dx)
+
+
+def _weight_operand(W: torch.Tensor, rows_dtype: torch.dtype, dev) -> torch.Tensor:
+    """W as the GEMM's weight operand: bf16 rows take bf16 or fp32 (master)
+    weights as they are; fp32 / fp64 rows take weights of their own dtype."""
+    W = W.to(device=dev)
+    if rows_dtype == torch.bfloat16 and W.dtype in (torch.bfloat16, torch.float32):
+        return W.contiguous()
+    return W.to(rows_dtype).contiguous()
+
+
+def linear_gemm(kind: str, a: torch.Tensor, W: torch.Tensor, bias: Optional[torch.Tensor], out: torch.Tensor,
+                rows: int, K: int, L: int) -> torch.Tensor:
+    """kind "fwd": out = a W (+ bias) (gnsb_linear_fwd); "dx": out = a W^T
+    (gnsb_linear_dx).  bf16 rows run the tcgen05 GEMM (linear_gemm.cu)."""
+    dev = a.device
+    dt = gnsb_dtype(a.dtype)
+    Wop = _weight_operand(W, a.dtype, dev)
+    wdt = gnsb_dtype(Wop.dtype)
+    n = ctypes.c_size_t()
+    h = _lib.lib()
+    _lib.check(h.gnsb_linear_gemm_workspace_size(K, L, dt, wdt, ctypes.byref(n)))
+    ws = _WS.get(dev, n.value, "gemm") if n.value else None
+    sp = _stream_ptr(dev)
+    if kind == "fwd":
+        b = None if bias is None else bias.to(device=dev, dtype=stat_dtype(a.dtype)).contiguous()
+        _lib.check(h.gnsb_linear_fwd(_ptr(a), _ptr(Wop), None if b is None else _ptr(b), _ptr(out), rows, K, L, dt,
+                                     wdt, None if ws is None else _ptr(ws), 0 if ws is None else ws.numel(), sp))
+    else:
+        _lib.check(h.gnsb_linear_dx(_ptr(a), _ptr(Wop), _ptr(out), rows, K, L, dt, wdt,
+                                    None if ws is None else _ptr(ws), 0 if ws is None else ws.numel(), sp))
+    return out
+
+
+def linear_forward(layer: LinearLayer, x: torch.Tensor) -> torch.Tensor:
+    """y = x W (+ bias), x [B, ..., K] -> [B, ..., L] (layers.hpp:64, layers.cpp:52-78)."""
+    K, L = int(layer.weight.shape[0]), int(layer.weight.shape[1])
+    if x.dim() < 2:
+        raise ValueError("layers: expected rank >= 2")
+    if int(x.shape[-1]) != K:
+        raise ValueError("layers: input trailing extent does not match weight rows")
+    if layer.bias is not None and tuple(layer.bias.shape) != (L,):
+        raise ValueError("layers: bias extent does not match weight columns")
+    if not x.is_cuda:
+        raise RuntimeError("layers: the B200 path has no CPU fallback (input is on the CPU)")
+    x = x.contiguous()
+    rows = x.numel() // K if K else 0
+    y = torch.empty(*x.shape[:-1], L, dtype=x.dtype, device=x.device)
+    return linear_gemm("fwd", x, layer.weight, layer.bias, y, rows, K, L)
 
 
 def linear_perexample_sqnorm_frobenius(x: torch.Tensor, g: torch.Tensor) -> torch.Tensor:
