@@ -629,7 +629,25 @@ def run_cfg3(m, lib, dev, torch, np):
         out[name] = {"us": ms * 1e3, "TFLOPs": fl / (ms * 1e-3) / 1e12, "frac_of_bf16_peak": fl / (ms * 1e-3) / 1e12 / peak,
                      "flops": fl}
     out["faster_form"] = min(("weight_grad", "gram"), key=lambda k: out[k]["us"])
-    del x, g, dW, ws
+    # the other half of linear_backward_simultaneous: dx = g W^T (gnsb_linear_dx,
+    # tcgen05), and the forward y = x W (gnsb_linear_fwd); bf16 W operand
+    Wb = (torch.randn(K, L, device=dev) / K ** 0.5).to(torch.bfloat16)
+    ybuf = torch.empty(B * T_, K, dtype=torch.bfloat16, device=dev)
+    for name, fnname, src in (("input_grad", "gnsb_linear_dx", g), ("forward", "gnsb_linear_fwd", x)):
+        def fn(fnname=fnname, src=src):
+            sp = torch.cuda.current_stream(dev).cuda_stream
+            if fnname == "gnsb_linear_dx":
+                rc = lib.gnsb_linear_dx(src.data_ptr(), Wb.data_ptr(), ybuf.data_ptr(), B * T_, K, L, 1, 1, None, 0, sp)
+            else:
+                rc = lib.gnsb_linear_fwd(src.data_ptr(), Wb.data_ptr(), None, ybuf.data_ptr(), B * T_, K, L, 1, 1,
+                                         None, 0, sp)
+            if rc:
+                raise RuntimeError(lib.gnsb_last_error().decode())
+        ms = time_graph(fn, torch, np, dev)
+        fl = 2.0 * B * T_ * K * L
+        out[name] = {"us": ms * 1e3, "TFLOPs": fl / (ms * 1e-3) / 1e12, "frac_of_bf16_peak": fl / (ms * 1e-3) / 1e12 / peak,
+                     "flops": fl, "kernel": "gemm_kernel (tcgen05, 128x256 tiles, TMA ring)"}
+    del x, g, dW, ws, Wb, ybuf
     torch.cuda.empty_cache()
     return out
 

@@ -99,6 +99,13 @@ for D in Ds:
         print(f"  L{l}: start {r[:,0].min():7.2f}..{r[:,0].max():7.2f} wait-exit {r[:,3].min():7.2f}..{r[:,3].max():7.2f}"
               f" rows-end {r[:,1].min():7.2f}/{med(r[:,1]):7.2f}/{r[:,1].max():7.2f} fold-end {r[:,2].max():7.2f}{gap}")
         prev_end = r[:, 2].max()
+    # is the SM-to-SM spread systematic?  per-CTA row time (wait exit -> rows end)
+    # of consecutive layers: correlation and the slowest CTAs
+    dur = np.array([(tr[:, 1] - tr[:, 3]) / 1000.0 for tr in trs])
+    cc = [float(np.corrcoef(dur[l], dur[l + 1])[0, 1]) for l in range(len(trs) - 1)]
+    print(f"  per-CTA row time corr(layer l, l+1): {' '.join(f'{c:.2f}' for c in cc)}")
+    print(f"  slowest CTAs L1: {np.argsort(-dur[1])[:12].tolist()}  L5: {np.argsort(-dur[5 % len(trs)])[:12].tolist()}")
+    print(f"  row time min/med/max per layer: " + " | ".join(f"{d.min():.1f}/{np.median(d):.1f}/{d.max():.1f}" for d in dur))
     for L in layers:
         L.clear()
     torch.cuda.empty_cache()

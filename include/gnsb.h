@@ -174,6 +174,29 @@ gnsb_status gnsb_linear_fwd(const void* x, const void* W, const void* bias, void
 gnsb_status gnsb_linear_dx(const void* g, const void* W, void* dx, int64_t rows, int64_t K, int64_t L, gnsb_dtype dt,
                            gnsb_dtype w_dt, void* ws, size_t ws_bytes, void* stream);
 
+/* The same two products with an elementwise epilogue fused into the store
+ * (the toy model's steps around its linear layers, proj/src/model.cpp:95-100,
+ * :169-171).  kind 0 = forward (x W + bias), 1 = input grad (g W^T, bias
+ * ignored).  epilogue, on v = the product (+ bias):
+ *   0 none: out = v;  1 tanh (forward): out = tanh(v);
+ *   2 residual (forward): out = aux + v;  3 tanh backward (input grad):
+ *   out = v * (1 - aux^2) with aux the tanh output.
+ * aux [rows, N] of dtype dt (N = L forward, K input grad), may alias nothing
+ * written by the call. */
+gnsb_status gnsb_linear_gemm(int32_t kind, int32_t epilogue, const void* a, const void* W, const void* bias,
+                             const void* aux, void* out, int64_t rows, int64_t K, int64_t L, gnsb_dtype dt,
+                             gnsb_dtype w_dt, void* ws, size_t ws_bytes, void* stream);
+
+/* Softmax cross-entropy of the head, forward + backward in one kernel
+ * (the reference's cross_entropy with dlogits, proj/src/model.cpp:113-141):
+ *   loss_rows[r] = log(sum_c exp(l[r,c] - m)) + m - l[r, target[r]]   (fp64)
+ *   dlogits[r,c] = (softmax(l[r])[c] - [c == target[r]]) * upstream_scale
+ * logits / dlogits [rows, V] of dtype dt (dlogits nullable: loss only),
+ * targets [rows] int32.  bad_targets (nullable device int32) is set to 1 when
+ * a target was outside [0, V) (its loss row is NaN). */
+gnsb_status gnsb_xent(const void* logits, const int32_t* targets, void* dlogits, double* loss_rows, int64_t rows,
+                      int64_t V, double upstream_scale, gnsb_dtype dt, int32_t* bad_targets, void* stream);
+
 /* Embedding row lookup out[i, :] = W[ids[i], :] (replaces gnstk::embedding_forward,
  * proj/include/gnstk/layers.hpp:83, proj/src/layers.cpp:300-313).  ids [n] int32
  * device, W [V, D] and out [n, D] of dtype dt.  bad_ids (nullable device int32)

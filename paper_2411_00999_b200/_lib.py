@@ -96,6 +96,9 @@ _SIGS = {
     "gnsb_linear_fwd": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i32, c_i32, c_vp, ctypes.c_size_t,
                                 c_vp]),
     "gnsb_linear_dx": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i32, c_i32, c_vp, ctypes.c_size_t, c_vp]),
+    "gnsb_linear_gemm": (c_i32, [c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i32, c_i32, c_vp,
+                                 ctypes.c_size_t, c_vp]),
+    "gnsb_xent": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_f64, c_i32, c_vp, c_vp]),
     "gnsb_embedding_fwd": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i32, c_vp, c_vp]),
     "gnsb_estimate_g2": (c_i32, [ctypes.POINTER(GradStats), c_dp]),
     "gnsb_estimate_s": (c_i32, [ctypes.POINTER(GradStats), c_dp]),

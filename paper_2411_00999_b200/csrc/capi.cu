@@ -526,28 +526,50 @@ gnsb_status gnsb_linear_gemm_workspace_size(int64_t K, int64_t L, gnsb_dtype dt,
     return debug_ok("gnsb_linear_gemm_workspace_size");
 }
 
-static gnsb_status linear_gemm(int kind, const char* fn, const void* in, const void* W, const void* bias, void* out,
-                               int64_t rows, int64_t K, int64_t L, gnsb_dtype dt, gnsb_dtype w_dt, void* ws,
-                               size_t ws_bytes, void* stream) {
+static gnsb_status linear_gemm(int kind, int epi, const char* fn, const void* in, const void* W, const void* bias,
+                               const void* aux, void* out, int64_t rows, int64_t K, int64_t L, gnsb_dtype dt,
+                               gnsb_dtype w_dt, void* ws, size_t ws_bytes, void* stream) {
+    if (epi < 0 || epi > 3 || (kind == 1 && (epi == 1 || epi == 2)) || (kind == 0 && epi == 3))
+        return fail(GNSB_EINVAL, "layers: unsupported GEMM epilogue for this product");
+    if ((epi == 2 || epi == 3) && rows > 0 && !aux) return fail(GNSB_EINVAL, "layers: the epilogue needs aux");
     if (rows < 0 || K < 1 || L < 1) return fail(GNSB_EINVAL, "layers: invalid extents");
     if (!gemm_dtypes_ok(dt, w_dt)) return fail(GNSB_EINVAL, "layers: unsupported row/weight dtype pair");
     if (gnsb_status s = need_device(fn)) return s;
     if (rows > 0 && (!in || !W || !out)) return fail(GNSB_EINVAL, "layers: null pointer");
     if (ws_bytes < gnsb::gemm_workspace((int)dt, (int)w_dt, K, L) || (ws_bytes > 0 && !ws))
         return fail(GNSB_EINVAL, "layers: workspace too small (query gnsb_linear_gemm_workspace_size)");
-    const cudaError_t e = gnsb::launch_linear_gemm(kind, (int)dt, (int)w_dt, in, W, bias, out, rows, K, L, ws,
-                                                   static_cast<cudaStream_t>(stream));
+    const cudaError_t e = gnsb::launch_linear_gemm(kind, epi, (int)dt, (int)w_dt, in, W, bias, aux, out, rows, K, L,
+                                                   ws, static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? debug_ok(fn) : cuda_fail(e, "linear gemm launch");
 }
 
 gnsb_status gnsb_linear_fwd(const void* x, const void* W, const void* bias, void* y, int64_t rows, int64_t K, int64_t L,
                             gnsb_dtype dt, gnsb_dtype w_dt, void* ws, size_t ws_bytes, void* stream) {
-    return linear_gemm(0, "gnsb_linear_fwd", x, W, bias, y, rows, K, L, dt, w_dt, ws, ws_bytes, stream);
+    return linear_gemm(0, 0, "gnsb_linear_fwd", x, W, bias, nullptr, y, rows, K, L, dt, w_dt, ws, ws_bytes, stream);
+}
+
+gnsb_status gnsb_linear_gemm(int32_t kind, int32_t epilogue, const void* a, const void* W, const void* bias,
+                             const void* aux, void* out, int64_t rows, int64_t K, int64_t L, gnsb_dtype dt,
+                             gnsb_dtype w_dt, void* ws, size_t ws_bytes, void* stream) {
+    if (kind != 0 && kind != 1) return fail(GNSB_EINVAL, "layers: kind must be 0 (forward) or 1 (input grad)");
+    return linear_gemm(kind, epilogue, "gnsb_linear_gemm", a, W, kind == 0 ? bias : nullptr, aux, out, rows, K, L, dt,
+                       w_dt, ws, ws_bytes, stream);
+}
+
+gnsb_status gnsb_xent(const void* logits, const int32_t* targets, void* dlogits, double* loss_rows, int64_t rows,
+                      int64_t V, double upstream_scale, gnsb_dtype dt, int32_t* bad_targets, void* stream) {
+    if (rows < 0 || V < 1) return fail(GNSB_EINVAL, "model: invalid extents");
+    if (dt != GNSB_F32 && dt != GNSB_BF16 && dt != GNSB_F64) return fail(GNSB_EINVAL, "model: unknown dtype");
+    if (gnsb_status s = need_device("gnsb_xent")) return s;
+    if (rows > 0 && (!logits || !targets || !loss_rows)) return fail(GNSB_EINVAL, "model: null pointer");
+    const cudaError_t e = gnsb::launch_xent((int)dt, logits, targets, dlogits, loss_rows, rows, V, upstream_scale,
+                                            bad_targets, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? debug_ok("gnsb_xent") : cuda_fail(e, "xent launch");
 }
 
 gnsb_status gnsb_linear_dx(const void* g, const void* W, void* dx, int64_t rows, int64_t K, int64_t L, gnsb_dtype dt,
                            gnsb_dtype w_dt, void* ws, size_t ws_bytes, void* stream) {
-    return linear_gemm(1, "gnsb_linear_dx", g, W, nullptr, dx, rows, K, L, dt, w_dt, ws, ws_bytes, stream);
+    return linear_gemm(1, 0, "gnsb_linear_dx", g, W, nullptr, nullptr, dx, rows, K, L, dt, w_dt, ws, ws_bytes, stream);
 }
 
 gnsb_status gnsb_embedding_fwd(const int32_t* ids, const void* W, void* out, int64_t n, int64_t V, int64_t D,

@@ -10,6 +10,7 @@
 
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <optional>
 #include <span>
 #include <stdexcept>
@@ -38,19 +39,36 @@ void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw std::runtime_error(std::string("cuda: ") + what + ": " + cudaGetErrorString(e));
 }
 
+// Device buffers come from the stream-ordered pool of the legacy default
+// stream (cudaMallocAsync), which every drop-in call runs on: a call costs
+// no cudaMalloc / cudaFree round trips once the pool is warm (the reference's
+// callers make many small calls per training step).
+void init_pool_once() {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = ~0ull;  // keep freed blocks for reuse
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    });
+}
+
 struct DevBuf {
     void* p = nullptr;
     explicit DevBuf(std::size_t bytes, bool zero = false) {
         if (bytes) {
-            cuda_check(cudaMalloc(&p, bytes), "cudaMalloc");
-            if (zero) cuda_check(cudaMemset(p, 0, bytes), "cudaMemset");
+            init_pool_once();
+            cuda_check(cudaMallocAsync(&p, bytes, nullptr), "cudaMallocAsync");
+            if (zero) cuda_check(cudaMemsetAsync(p, 0, bytes, nullptr), "cudaMemsetAsync");
         }
     }
     DevBuf(DevBuf&& o) noexcept : p(o.p) { o.p = nullptr; }
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, nullptr);
     }
     template <typename T>
     T* as() const {

@@ -39,6 +39,7 @@ struct LnBwdCall {
 // Where a row pass left its partial slots and how the reduce must read them.
 struct LnRedPlanInfo {
     int Dp = 0, G = 0, grid_rows = 0;
+    int gsub = 1;  // slots per (cta + example) stage 2 sums: 1 (folded) or G (one per row group)
     size_t off_partial = 0, off_q = 0, off_qbig = 0, off_raw = 0, total = 0;
 };
 // One LayerNorm whose stage 2 (per-example combine, squares, dgamma/dbeta) is pending.
@@ -98,7 +99,12 @@ cudaError_t launch_embedding_fwd(int dt, const int32_t* ids, const void* W, void
 // linear-layer GEMMs (linear_gemm.cu): kind 0 forward y = x W + bias, kind 1 dx = g W^T
 bool gemm_tc_ok(int dt, int64_t K, int64_t L);
 size_t gemm_workspace(int dt, int w_dt, int64_t K, int64_t L);
-cudaError_t launch_linear_gemm(int kind, int dt, int w_dt, const void* in, const void* W, const void* bias, void* out,
-                               int64_t rows, int64_t K, int64_t L, void* ws, cudaStream_t st);
+cudaError_t launch_linear_gemm(int kind, int epi, int dt, int w_dt, const void* in, const void* W, const void* bias,
+                               const void* aux, void* out, int64_t rows, int64_t K, int64_t L, void* ws,
+                               cudaStream_t st);
+// softmax cross-entropy rows (xent.cu): loss_rows[r] = log(sum exp) + max - logit[target],
+// dlogits = (softmax - onehot) * upstream_scale
+cudaError_t launch_xent(int dt, const void* logits, const int32_t* targets, void* dlogits, double* loss_rows,
+                        int64_t rows, int64_t V, double upstream_scale, int32_t* bad, cudaStream_t st);
 
 }  // namespace gnsb

@@ -44,14 +44,31 @@ constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 256;
 constexpr int TMEM_COLS = 512;
 }  // namespace gm
 
+// Epilogues fused into the store (the toy model's elementwise ops,
+// proj/src/model.cpp:95-100 and :169-171): v = acc (+ bias), then
+//   EPI_NONE  out = v
+//   EPI_TANH  out = tanh(v)                 (fc1 forward)
+//   EPI_RESID out = aux + v                 (fc2 forward + residual)
+//   EPI_DTANH out = v * (1 - aux^2)         (fc2 input grad through the tanh, aux = tanh output)
+enum { EPI_NONE = 0, EPI_TANH = 1, EPI_RESID = 2, EPI_DTANH = 3 };
+
+template <int EPI, typename A>
+__device__ __forceinline__ A epi_apply(A v, A aux) {
+    if constexpr (EPI == EPI_TANH) return tanh(v);
+    if constexpr (EPI == EPI_RESID) return aux + v;
+    if constexpr (EPI == EPI_DTANH) return v * (A(1) - aux * aux);
+    return v;
+}
+
 struct GemmArgs {
     int M, N, Kr;         // output rows, output columns, reduced extent
     int tiles_m, tiles_n;
     const float* bias;    // [N] (BIAS)
+    const __nv_bfloat16* aux;  // [M, N] (EPI_RESID, EPI_DTANH)
     __nv_bfloat16* out;   // [M, N]
 };
 
-template <bool B_KMAJOR, bool BIAS>
+template <bool B_KMAJOR, bool BIAS, int EPI>
 __global__ void __launch_bounds__(gm::THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb, GemmArgs a) {
     using namespace gm;
@@ -191,6 +208,13 @@ __global__ void __launch_bounds__(gm::THREADS, 1)
 #pragma unroll
                         for (int j = 0; j < 8; ++j) f[j] += __ldg(a.bias + c0 + 8 * v + j);
                     }
+                    if constexpr (EPI != EPI_NONE) {
+                        float x[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                        if constexpr (EPI == EPI_RESID || EPI == EPI_DTANH)
+                            unpack<__nv_bfloat16>(__ldg(reinterpret_cast<const uint4*>(a.aux + (size_t)row * a.N + c0 + 8 * v)), x);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) f[j] = epi_apply<EPI>(f[j], x[j]);
+                    }
                     uint4 o;
                     o.x = pack_bf16x2(f[0], f[1]);
                     o.y = pack_bf16x2(f[2], f[3]);
@@ -234,7 +258,8 @@ __global__ void __launch_bounds__(256) f32_to_bf16_kernel(const float* __restric
 // :142-155 bit for bit.
 template <typename T, typename WT, bool FWD>
 __global__ void __launch_bounds__(256) gemm_generic_kernel(const T* a, const WT* W, const void* bias, int bias_f64,
-                                                           T* out, int64_t rows, int64_t N, int64_t Kr, int64_t ldw) {
+                                                           const T* aux, int epi, T* out, int64_t rows, int64_t N,
+                                                           int64_t Kr, int64_t ldw) {
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= rows * N) return;
     const int64_t r = idx / N, n = idx % N;
@@ -244,6 +269,10 @@ __global__ void __launch_bounds__(256) gemm_generic_kernel(const T* a, const WT*
         acc = __dadd_rn(acc, __dmul_rn((double)to_acc<T>(a[r * Kr + k]), w));
     }
     if (bias) acc = __dadd_rn(acc, bias_f64 ? static_cast<const double*>(bias)[n] : (double)static_cast<const float*>(bias)[n]);
+    if (epi != EPI_NONE) {  // the reference's elementwise step in fp64 (model.cpp:96, :99, :171)
+        const double z = aux ? (double)to_acc<T>(aux[idx]) : 0.0;
+        acc = epi == EPI_TANH ? tanh(acc) : epi == EPI_RESID ? __dadd_rn(z, acc) : __dmul_rn(acc, __dsub_rn(1.0, __dmul_rn(z, z)));
+    }
     out[idx] = from_acc<T>((typename Traits<T>::Acc)acc);
 }
 
@@ -281,9 +310,9 @@ bool make_map_2d(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, i
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <bool BK_, bool BIAS>
+template <bool BK_, bool BIAS, int EPI>
 cudaError_t launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, cudaStream_t st) {
-    const void* fn = reinterpret_cast<const void*>(gemm_kernel<BK_, BIAS>);
+    const void* fn = reinterpret_cast<const void*>(gemm_kernel<BK_, BIAS, EPI>);
     cudaError_t e = ensure_smem_attr(fn, gm::SMEM);
     if (e != cudaSuccess) return e;
     const int ntiles = a.tiles_m * a.tiles_n;
@@ -298,7 +327,7 @@ cudaError_t launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmAr
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, gemm_kernel<BK_, BIAS>, ma, mb, a);
+    return cudaLaunchKernelEx(&cfg, gemm_kernel<BK_, BIAS, EPI>, ma, mb, a);
 }
 
 }  // namespace
@@ -313,11 +342,14 @@ size_t gemm_workspace(int dt, int w_dt, int64_t K, int64_t L) {
 }
 
 // kind 0: forward y = x W + bias; kind 1: dx = g W^T.  dt / w_dt: 0 f32, 1 bf16, 2 f64.
-cudaError_t launch_linear_gemm(int kind, int dt, int w_dt, const void* in, const void* W, const void* bias, void* out,
-                               int64_t rows, int64_t K, int64_t L, void* ws, cudaStream_t st) {
+// epi: EPI_* applied to every output element (aux [rows, N] of dtype dt).
+cudaError_t launch_linear_gemm(int kind, int epi, int dt, int w_dt, const void* in, const void* W, const void* bias,
+                               const void* aux, void* out, int64_t rows, int64_t K, int64_t L, void* ws,
+                               cudaStream_t st) {
     const int64_t N = kind == 0 ? L : K, Kr = kind == 0 ? K : L;
     if (rows == 0) return cudaSuccess;
-    if (gemm_tc_ok(dt, K, L) && rows < (1ll << 31) && al16(in) && al16(out) && (w_dt == 0 || al16(W))) {
+    if (gemm_tc_ok(dt, K, L) && rows < (1ll << 31) && al16(in) && al16(out) && (w_dt == 0 || al16(W)) &&
+        (aux == nullptr || al16(aux))) {
         const void* wb = W;
         if (w_dt == 0) {  // fp32 master weights: bf16 operand copy in the workspace
             const int64_t n = K * L;
@@ -339,9 +371,21 @@ cudaError_t launch_linear_gemm(int kind, int dt, int w_dt, const void* in, const
         a.tiles_m = (int)((rows + gm::BM - 1) / gm::BM);
         a.tiles_n = (int)((N + gm::BN - 1) / gm::BN);
         a.bias = static_cast<const float*>(bias);
+        a.aux = static_cast<const __nv_bfloat16*>(aux);
         a.out = static_cast<__nv_bfloat16*>(out);
-        if (kind == 1) return launch_tc<true, false>(ma, mb, a, st);
-        return bias ? launch_tc<false, true>(ma, mb, a, st) : launch_tc<false, false>(ma, mb, a, st);
+        if (kind == 1) {
+            if (epi == EPI_DTANH) return launch_tc<true, false, EPI_DTANH>(ma, mb, a, st);
+            return launch_tc<true, false, EPI_NONE>(ma, mb, a, st);
+        }
+        switch (epi) {
+            case EPI_TANH:
+                return bias ? launch_tc<false, true, EPI_TANH>(ma, mb, a, st) : launch_tc<false, false, EPI_TANH>(ma, mb, a, st);
+            case EPI_RESID:
+                return bias ? launch_tc<false, true, EPI_RESID>(ma, mb, a, st)
+                            : launch_tc<false, false, EPI_RESID>(ma, mb, a, st);
+            default:
+                return bias ? launch_tc<false, true, EPI_NONE>(ma, mb, a, st) : launch_tc<false, false, EPI_NONE>(ma, mb, a, st);
+        }
     }
     const int64_t n = rows * N;
     const unsigned grid = (unsigned)((n + 255) / 256);
@@ -350,13 +394,13 @@ cudaError_t launch_linear_gemm(int kind, int dt, int w_dt, const void* in, const
 #define GNSB_GEMM_GENERIC(T, WT)                                                                                     \
     do {                                                                                                             \
         if (kind == 0)                                                                                               \
-            gemm_generic_kernel<T, WT, true><<<grid, 256, 0, st>>>(static_cast<const T*>(in),                       \
-                                                                   static_cast<const WT*>(W), bias, bias_f64,        \
-                                                                   static_cast<T*>(out), rows, N, Kr, ldw);          \
+            gemm_generic_kernel<T, WT, true><<<grid, 256, 0, st>>>(                                                \
+                static_cast<const T*>(in), static_cast<const WT*>(W), bias, bias_f64, static_cast<const T*>(aux), epi, \
+                static_cast<T*>(out), rows, N, Kr, ldw);                                                             \
         else                                                                                                         \
-            gemm_generic_kernel<T, WT, false><<<grid, 256, 0, st>>>(static_cast<const T*>(in),                      \
-                                                                    static_cast<const WT*>(W), nullptr, 0,           \
-                                                                    static_cast<T*>(out), rows, N, Kr, ldw);         \
+            gemm_generic_kernel<T, WT, false><<<grid, 256, 0, st>>>(                                               \
+                static_cast<const T*>(in), static_cast<const WT*>(W), nullptr, 0, static_cast<const T*>(aux), epi,   \
+                static_cast<T*>(out), rows, N, Kr, ldw);                                                             \
     } while (0)
     if (dt == 2 && w_dt == 2)
         GNSB_GEMM_GENERIC(double, double);

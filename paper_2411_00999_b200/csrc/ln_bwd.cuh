@@ -60,7 +60,8 @@ struct LnBwdArgs {
 // Arguments of the stage-2 kernel (per-example combine, squares, dgamma/dbeta).
 struct LnRedArgs {
     const void* partial;  // the row kernel's slots: slot (c + b) * slot_stride holds CTA c's part of example b
-    int64_t slot_stride;  // elements between consecutive (cta + example) slots (= G * 2 * Dp)
+    int64_t slot_stride;  // elements between consecutive slots: G * 2 * Dp (folded), 2 * Dp (gsub = G)
+    int gsub;             // slots per (cta + example): 1 (folded by the row kernel) or G (one per row group)
     int64_t B, M, N, D;
     int Dp;
     int grid_rows;        // CTAs of the row kernel (row range of CTA c: [c*N/grid_rows, (c+1)*N/grid_rows))
@@ -79,7 +80,7 @@ struct LnRedArgs {
 };
 
 template <typename T, int GW, int VPT, int G, int RPG, bool PROD_ = true, int KEEP_ = -1, int CPS_ = 1,
-          bool PARK_ = false>
+          bool PARK_ = false, bool NOFOLD_ = false>
 struct LnBwdCfg {
     using Acc = typename Traits<T>::Acc;
     using Row = T;
@@ -87,6 +88,11 @@ struct LnBwdCfg {
     static constexpr int W = Traits<T>::W;
     static constexpr bool PROD = PROD_;          // dedicated producer warp (the last warp)
     static constexpr bool kPark = PARK_ && G > 1;  // first example's group partials parked in smem
+    // kNoFold: no end-of-kernel CTA fold; every group leaves its own slot for
+    // every example it touched and stage 2 sums the G sub-slots (moves ~2 us
+    // of the row pass's critical path into the once-per-step reduce)
+    static constexpr bool kNoFold = NOFOLD_ && G > 1 && !kPark;
+    static constexpr int kSub = kNoFold ? G : 1;  // sub-slots stage 2 reads per (cta + example)
     static constexpr int kWarps = GW * G;        // row-math warps
     static constexpr int kThreads = (kWarps + (PROD ? 1 : 0)) * 32;
     // registers are allocated for warps in groups of 4: bound the register
@@ -490,7 +496,7 @@ __global__ void __launch_bounds__(C::kBoundThreads, C::kCps) ln_bwd_kernel(LnBwd
     }
     // examples before the CTA's last one go to their global slots now; the
     // last one stays in registers for the CTA-local fold below
-    if (G == 1) {
+    if (G == 1 || C::kNoFold) {
         flush_to((r_end - 1) / M + 1);
     } else if (cur_ex < (r_end - 1) / M) {
         flush_to((r_end - 1) / M);
@@ -498,7 +504,7 @@ __global__ void __launch_bounds__(C::kBoundThreads, C::kCps) ln_bwd_kernel(LnBwd
     }  // row-math warps
 
     stamp(1);
-    if constexpr (G > 1) {
+    if constexpr (G > 1 && !C::kNoFold) {
         // CTA-local fold of the G group partials of every example this CTA
         // touched into group 0's slot, in fixed order g = 0..G-1.  The last
         // example's partials go through shared memory (the ring is free once
@@ -613,13 +619,15 @@ __device__ __forceinline__ void ln_bwd_reduce_body(const LnRedArgs& a, const int
 
     for (int64_t b0 = 0; b0 < B; b0 += a.eb) {
         const int64_t nb = (B - b0) < a.eb ? (B - b0) : a.eb;
-        // slots of this block: from the first CTA of example b0 to the last of b0+nb-1
-        const int64_t s_lo = cta_of(b0 * M) + b0;
-        const int64_t s_hi = cta_of((b0 + nb) * M - 1) + (b0 + nb - 1);
+        // slots of this block: from the first CTA of example b0 to the last of
+        // b0+nb-1 (gsub consecutive slots per CTA)
+        const int gs = a.gsub;
+        const int64_t s_lo = (cta_of(b0 * M) + b0) * gs;
+        const int64_t s_hi = (cta_of((b0 + nb) * M - 1) + (b0 + nb - 1)) * gs + gs - 1;
         for (int bb = threadIdx.x; bb < nb; bb += nthreads) {
             const int64_t b = b0 + bb;
-            s_cs[bb] = (int)(cta_of(b * M) + b - s_lo);  // first slot of example b, relative to s_lo
-            s_nc[bb] = (int)(cta_of((b + 1) * M - 1) - cta_of(b * M) + 1);
+            s_cs[bb] = (int)((cta_of(b * M) + b) * gs - s_lo);  // first slot of example b, relative to s_lo
+            s_nc[bb] = (int)((cta_of((b + 1) * M - 1) - cta_of(b * M) + 1) * gs);
         }
         // The block's slots are staged `slot_cap` at a time (one chunk unless a
         // single example spans more CTAs than fit, e.g. B = 1); the per-column

@@ -149,6 +149,7 @@ struct BwdOp {
     static void fill_info(const BwdPlan& p, LnRedPlanInfo* info) {
         info->Dp = p.Dp;
         info->G = C::kG;
+        info->gsub = C::kSub;
         info->grid_rows = p.grid;
         info->off_partial = p.off_partial;
         info->off_q = p.off_q;
@@ -345,6 +346,16 @@ struct FwdOp {
     }
 };
 
+// GNSB_LN_FOLD=1: the CTA-folded variants of the D = 1024 / 2048 configurations
+// (A/B runs); default: no end-of-kernel fold, stage 2 sums the group slots.
+inline bool ln_fold() {
+    static const bool v = [] {
+        const char* e = getenv("GNSB_LN_FOLD");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
 // Configuration table: number of 16-byte vectors per row -> LnBwdCfg.
 template <typename T, template <typename> class Op, typename R, typename... A>
 R dispatch_bwd(int64_t D, const char** why, R bad, A&&... args) {
@@ -355,8 +366,14 @@ R dispatch_bwd(int64_t D, const char** why, R bad, A&&... args) {
     if (nv <= 32) return Op<LnBwdCfg<T, 1, 1, 8, 2, true>>::call(args...);
     if (nv <= 64) return Op<LnBwdCfg<T, 2, 1, 8, 1, true>>::call(args...);
     if (nv <= 96) return Op<LnBwdCfg<T, 3, 1, 5, 2, true, -1, 1, true>>::call(args...);  // parked first example
-    if (nv <= 128) return Op<LnBwdCfg<T, 4, 1, 4, 2, true>>::call(args...);
-    if (nv <= 256) return Op<LnBwdCfg<T, 8, 1, 2, 2, true>>::call(args...);
+    if (nv <= 128) {
+        if (ln_fold()) return Op<LnBwdCfg<T, 4, 1, 4, 2, true>>::call(args...);
+        return Op<LnBwdCfg<T, 4, 1, 4, 2, true, -1, 1, false, true>>::call(args...);
+    }
+    if (nv <= 256) {
+        if (ln_fold()) return Op<LnBwdCfg<T, 8, 1, 2, 2, true>>::call(args...);
+        return Op<LnBwdCfg<T, 8, 1, 2, 2, true, -1, 1, false, true>>::call(args...);
+    }
     if (nv <= 512) return Op<LnBwdCfg<T, 8, 2, 1, 2, true, 1>>::call(args...);
     // 11 consumer warps x 3 vectors (3 % of the lanes idle at D=8192): 12 warps leave
     // ~168 registers per thread, no spills (16 x 2 forced 96 and spilled)

@@ -39,7 +39,7 @@ RedShape red_shape(const LnRedItem& it, int V, int rgrid, int acc_bytes) {
     const int64_t rows_per_cta = N / it.info.grid_rows;  // floor: a block of eb examples spans <= eb*M/rpc + 2 CTAs
     auto layout = [&](int64_t eb) {
         const int64_t span = rows_per_cta > 0 ? (eb * it.M + rows_per_cta - 1) / rows_per_cta + 2 : N;
-        return LnRedLayout{ncol, eb, span + eb};
+        return LnRedLayout{ncol, eb, (span + eb) * it.info.gsub};
     };
     constexpr size_t kBudget = 160 << 10;
     int64_t eb = it.B < kMaxReduceEb ? it.B : kMaxReduceEb;
@@ -60,7 +60,8 @@ LnRedArgs red_args(const LnRedItem& it, const RedShape& r, unsigned long long* t
     unsigned char* ws = static_cast<unsigned char*>(it.ws);
     LnRedArgs a{};
     a.partial = ws + it.info.off_partial;
-    a.slot_stride = (int64_t)it.info.G * 2 * it.info.Dp;
+    a.slot_stride = (int64_t)(it.info.G / it.info.gsub) * 2 * it.info.Dp;
+    a.gsub = it.info.gsub;
     a.B = it.B;
     a.M = it.M;
     a.N = it.B * it.M;
@@ -93,7 +94,7 @@ int reduce_run_t(int norms, const LnRedItem* items, int n, cudaStream_t st, unsi
     for (int l = 0; l < n; ++l) {
         const int64_t U = (items[l].info.Dp + V - 1) / V;
         useful[l] = std::max<int64_t>(1, std::min<int64_t>((U + 3) / 4, sms));
-        w[l] = U * (items[l].info.grid_rows + items[l].B);
+        w[l] = U * (items[l].info.grid_rows + items[l].B) * items[l].info.gsub;
         total_useful += useful[l];
     }
     const int total = (int)std::min<int64_t>(std::max<int64_t>(sms, n), total_useful);

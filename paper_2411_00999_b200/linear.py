@@ -115,10 +115,15 @@ def _weight_operand(W: torch.Tensor, rows_dtype: torch.dtype, dev) -> torch.Tens
     return W.to(rows_dtype).contiguous()
 
 
+EPILOGUES = {"none": 0, "tanh": 1, "residual": 2, "dtanh": 3}
+
+
 def linear_gemm(kind: str, a: torch.Tensor, W: torch.Tensor, bias: Optional[torch.Tensor], out: torch.Tensor,
-                rows: int, K: int, L: int) -> torch.Tensor:
+                rows: int, K: int, L: int, epilogue: str = "none", aux: Optional[torch.Tensor] = None) -> torch.Tensor:
     """kind "fwd": out = a W (+ bias) (gnsb_linear_fwd); "dx": out = a W^T
-    (gnsb_linear_dx).  bf16 rows run the tcgen05 GEMM (linear_gemm.cu)."""
+    (gnsb_linear_dx).  bf16 rows run the tcgen05 GEMM (linear_gemm.cu).
+    epilogue (gnsb_linear_gemm): "tanh" / "residual" (out = aux + v) on the
+    forward, "dtanh" (out = v * (1 - aux^2)) on the input grad."""
     dev = a.device
     dt = gnsb_dtype(a.dtype)
     Wop = _weight_operand(W, a.dtype, dev)
@@ -128,7 +133,13 @@ def linear_gemm(kind: str, a: torch.Tensor, W: torch.Tensor, bias: Optional[torc
     _lib.check(h.gnsb_linear_gemm_workspace_size(K, L, dt, wdt, ctypes.byref(n)))
     ws = _WS.get(dev, n.value, "gemm") if n.value else None
     sp = _stream_ptr(dev)
-    if kind == "fwd":
+    if epilogue != "none":
+        b = None if (bias is None or kind != "fwd") else bias.to(device=dev, dtype=stat_dtype(a.dtype)).contiguous()
+        _lib.check(h.gnsb_linear_gemm(0 if kind == "fwd" else 1, EPILOGUES[epilogue], _ptr(a), _ptr(Wop),
+                                      None if b is None else _ptr(b), None if aux is None else _ptr(aux.contiguous()),
+                                      _ptr(out), rows, K, L, dt, wdt, None if ws is None else _ptr(ws),
+                                      0 if ws is None else ws.numel(), sp))
+    elif kind == "fwd":
         b = None if bias is None else bias.to(device=dev, dtype=stat_dtype(a.dtype)).contiguous()
         _lib.check(h.gnsb_linear_fwd(_ptr(a), _ptr(Wop), None if b is None else _ptr(b), _ptr(out), rows, K, L, dt,
                                      wdt, None if ws is None else _ptr(ws), 0 if ws is None else ws.numel(), sp))

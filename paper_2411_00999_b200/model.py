@@ -8,10 +8,19 @@ B200 kernel that also yields its per-example squared gradient norms, exactly
 what `model_backward` (proj/src/model.cpp:144-188) collects:
 
     LayerNormPE  -> gnsb_ln_fwd / gnsb_ln_bwd            (fused LN backward)
-    LinearPE     -> torch GEMMs for y and dx (library), gnsb_linear_pe_norms
-                    for dW + per-example norms (tcgen05 when bf16 and aligned),
+    LinearPE     -> gnsb_linear_fwd / gnsb_linear_dx for y and dx (tcgen05
+                    GEMMs for bf16 rows), gnsb_linear_pe_norms for dW +
+                    per-example norms (tcgen05 when bf16 and aligned),
                     gnsb_linear_bias_pe for the bias
-    EmbeddingPE  -> gnsb_embedding_pe
+    EmbeddingPE  -> gnsb_embedding_fwd / gnsb_embedding_pe
+
+`ToyModelPE.forward_backward` runs the reference's run_forward +
+model_backward sequence (proj/src/model.cpp:87-188) without autograd, every
+step on the library's kernels: the tanh of fc1 and the residual add of fc2 are
+fused into the forward GEMM epilogues, the tanh derivative into fc2's
+input-grad GEMM, the softmax cross-entropy forward+backward is one kernel
+(gnsb_xent), and every LayerNorm's stage 2 is deferred to one grouped reduce
+at the end of the backward (gnsb_ln_bwd_rows / gnsb_ln_bwd_reduce).
 
 After `loss.backward()` every layer holds a 4-double norm record
 {sum_b raw(p0), sum_b raw(p1), ||grad p0||^2, ||grad p1||^2} (p0 = weight or
@@ -61,9 +70,9 @@ class _LinearPEFunction(torch.autograd.Function):
     def forward(ctx, x, weight, bias, module):
         if not x.is_cuda:
             raise RuntimeError("LinearPE: the B200 path has no CPU fallback (input is on the CPU)")
-        y = torch.matmul(x, weight.to(x.dtype))
-        if bias is not None:
-            y = y + bias.to(x.dtype)
+        from .linear import LinearLayer, linear_forward
+
+        y = linear_forward(LinearLayer(weight.detach(), None if bias is None else bias.detach()), x)
         ctx.save_for_backward(x, weight)
         ctx.has_bias = bias is not None
         ctx.module = module
@@ -78,7 +87,12 @@ class _LinearPEFunction(torch.autograd.Function):
         K, L = weight.shape
         rec = torch.zeros(4, dtype=torch.float64, device=x.device)
         dW, db, raw = _linear_norms(x, g, K, L, rec, ctx.has_bias)
-        dx = torch.matmul(g, weight.to(g.dtype).t()) if ctx.needs_input_grad[0] else None
+        dx = None
+        if ctx.needs_input_grad[0]:
+            from .linear import linear_gemm
+
+            dx = torch.empty_like(x)
+            linear_gemm("dx", g, weight.detach(), None, dx, x.numel() // K, K, L)
         module.norm_record = rec
         module.per_example_raw = {"weight": raw[0], "bias": raw[1]} if ctx.has_bias else {"weight": raw[0]}
         module.batch_size = x.shape[0]
@@ -112,7 +126,9 @@ class _EmbeddingPEFunction(torch.autograd.Function):
         ctx.save_for_backward(ids)
         ctx.V = weight.shape[0]
         ctx.module = module
-        return weight[ids.long()]
+        from .embedding import embedding_forward
+
+        return embedding_forward(weight.detach(), ids.reshape(-1), int(ids.shape[0]), int(ids.shape[1]))
 
     @staticmethod
     def backward(ctx, g):
@@ -204,6 +220,97 @@ class ToyModelPE(torch.nn.Module):
             lg = lg.float()
         ce = torch.nn.functional.cross_entropy(lg, targets.reshape(-1).long(), reduction="none")
         return ce.reshape(B, T).mean(1).mean(0)
+
+    @torch.no_grad()
+    def forward_backward(self, ids: torch.Tensor, targets: torch.Tensor, loss_scale: float = 1.0,
+                         rows_dtype: Optional[torch.dtype] = None) -> torch.Tensor:
+        """The reference's model_backward (proj/src/model.cpp:144-188) on the
+        library's kernels, no autograd: returns the loss (device fp64 scalar,
+        mean over examples of the per-example mean-token cross-entropy times
+        loss_scale), sets every parameter's .grad and every instrumented
+        layer's norm record (the GnsTracker input).  rows_dtype: activation
+        dtype (default: the parameter dtype; bf16 with fp32 parameters runs
+        the tcgen05 GEMMs)."""
+        from .embedding import embedding_backward_simultaneous, embedding_forward
+        from .layers import (LayerNormCache, LayerNormLayer, layernorm_backward_reduce, layernorm_backward_rows,
+                             layernorm_forward)
+        from .linear import linear_gemm
+
+        pdt = self.embed.weight.dtype
+        adt = rows_dtype or pdt
+        B, T = (int(v) for v in ids.shape)
+        N = B * T
+        D = self.embed.weight.shape[1]
+        V = self.head.weight.shape[1]
+        ids = ids.contiguous()
+        targets = targets.to(torch.int32).contiguous()
+
+        def lnl(ln):
+            return LayerNormLayer(ln.weight, ln.bias, ln.eps)
+
+        # ---- forward (model.cpp:87-109)
+        x = embedding_forward(self.embed.weight.to(adt), ids.reshape(-1), B, T)
+        saved = []
+        for ln, f1, f2 in zip(self.lns, self.fc1, self.fc2):
+            fr = layernorm_forward(lnl(ln), x)
+            H = f1.weight.shape[1]
+            a = torch.empty(B, T, H, dtype=adt, device=x.device)
+            linear_gemm("fwd", fr.output, f1.weight, f1.bias, a, N, D, H, epilogue="tanh")
+            xn = torch.empty_like(x)
+            linear_gemm("fwd", a, f2.weight, f2.bias, xn, N, H, D, epilogue="residual", aux=x)
+            saved.append((fr, a))
+            x = xn
+        ffr = layernorm_forward(lnl(self.final_ln), x)
+        logits = torch.empty(B, T, V, dtype=adt, device=x.device)
+        linear_gemm("fwd", ffr.output, self.head.weight, self.head.bias, logits, N, D, V)
+        # ---- loss + dlogits (model.cpp:113-141, 150-156)
+        upstream = loss_scale * (1.0 / T) / B
+        dlogits = torch.empty_like(logits)
+        loss_rows = torch.empty(N, dtype=torch.float64, device=x.device)
+        _lib.check(_lib.lib().gnsb_xent(_ptr(logits), _ptr(targets), _ptr(dlogits), _ptr(loss_rows), N, V,
+                                        float(upstream), gnsb_dtype(adt), None, _stream_ptr(x.device)))
+        loss = (loss_rows.view(B, T).sum(1) / T * loss_scale).sum() / B
+        # ---- backward (model.cpp:158-188)
+        pend = []
+
+        def linear_bw(mod, xin, g, epi_aux=None):
+            K, L = mod.weight.shape
+            rec = torch.zeros(4, dtype=torch.float64, device=g.device)
+            dW, db, raw = _linear_norms(xin, g, K, L, rec, mod.bias is not None)
+            mod.weight.grad = dW.to(mod.weight.dtype)
+            if mod.bias is not None:
+                mod.bias.grad = db.to(mod.bias.dtype)
+            mod.norm_record, mod.batch_size = rec, B
+            mod.per_example_raw = {"weight": raw[0], "bias": raw[1]} if mod.bias is not None else {"weight": raw[0]}
+            dx = torch.empty(*g.shape[:-1], K, dtype=g.dtype, device=g.device)
+            if epi_aux is None:
+                linear_gemm("dx", g, mod.weight, None, dx, N, K, L)
+            else:
+                linear_gemm("dx", g, mod.weight, None, dx, N, K, L, epilogue="dtanh", aux=epi_aux)
+            return dx
+
+        def ln_bw(mod, fr, g):
+            dx, p = layernorm_backward_rows(lnl(mod), fr.cache, g)
+            pend.append((mod, p))
+            return dx
+
+        dx = ln_bw(self.final_ln, ffr, linear_bw(self.head, ffr.output, dlogits))
+        for i in reversed(range(len(self.lns))):
+            fr, a = saved[i]
+            da = linear_bw(self.fc2[i], a, dx, epi_aux=a)  # fc2 input grad times (1 - tanh^2), fused
+            dh = linear_bw(self.fc1[i], fr.output, da)
+            dx = dx + ln_bw(self.lns[i], fr, dh)
+        r = embedding_backward_simultaneous(ids, dx, int(self.embed.weight.shape[0]))
+        self.embed.weight.grad = r.weight_grads["weight"].to(pdt)
+        self.embed.norm_record, self.embed.batch_size = r.sums4, B
+        self.embed.per_example_raw = {"weight": r.per_example_sqnorms_raw["weight"]}
+        outs = layernorm_backward_reduce([p for _, p in pend])  # every LayerNorm's stage 2, one launch
+        for (mod, p), o in zip(pend, outs):
+            mod.weight.grad = o.weight_grads["gamma"].to(mod.weight.dtype)
+            mod.bias.grad = o.weight_grads["beta"].to(mod.bias.dtype)
+            mod.norm_record, mod.batch_size = p.sums, B
+            mod.per_example_raw = {"gamma": p.raw_g, "beta": p.raw_b}
+        return loss
 
     def instrumented_layers(self) -> List[Tuple[str, torch.nn.Module]]:
         """Layers in the reference's LayerKey order of model_backward's output

@@ -228,10 +228,10 @@ class Trainer:
         targets = host[:, 1:].contiguous().to(self.device, non_blocking=True)
         for p in self.model.parameters():
             p.grad = None
-        loss = self.model.loss(ids, targets) * c.loss_scale
-        loss.backward()
+        # model_backward (model.cpp:144-188) on the library kernels
+        loss = self.model.forward_backward(ids, targets, c.loss_scale)
         groups, per_layer = self.tracker.step()
-        loss_v = float(loss.detach())
+        loss_v = float(loss)
         if not math.isfinite(loss_v):
             raise TrainingDiverged(f"trainer: loss diverged at step {self.step_index}")
         g = groups.cpu().tolist()

@@ -30,7 +30,8 @@ def _functional_loss(p, ids, targets, n_blocks):
     return F.cross_entropy(logits, targets.long(), reduction="mean")
 
 
-def test_toy_model_per_example_norms_and_gns(cuda):
+@pytest.mark.parametrize("path", ["autograd", "explicit"])
+def test_toy_model_per_example_norms_and_gns(cuda, path):
     from paper_2411_00999_b200 import gns
     from paper_2411_00999_b200.model import ToyModelPE
     from paper_2411_00999_b200.nn import GnsTracker
@@ -44,11 +45,16 @@ def test_toy_model_per_example_norms_and_gns(cuda):
     gen = torch.Generator(device="cpu").manual_seed(7)
     ids = torch.randint(0, V, (B, T), generator=gen, dtype=torch.int32).to(cuda)
     targets = torch.randint(0, V, (B, T), generator=gen, dtype=torch.int32).to(cuda)
-    loss = model.loss(ids, targets)
-    loss.backward()
+    if path == "autograd":
+        loss = model.loss(ids, targets)
+        loss.backward()
+    else:  # model_backward on the library kernels (fused epilogues, gnsb_xent, grouped LN stage 2)
+        loss = model.forward_backward(ids, targets)
     torch.cuda.synchronize()
 
     params = {k: v.detach() for k, v in model.named_parameters()}
+    ref_loss = torch.stack([_functional_loss(params, ids[b], targets[b], NB) for b in range(B)]).mean()
+    assert close(float(loss), float(ref_loss), 1e-5)
     per_ex = torch.func.vmap(torch.func.grad(_functional_loss), in_dims=(None, 0, 0, None))(params, ids, targets, NB)
     full = torch.func.grad(lambda p: torch.stack([_functional_loss(p, ids[b], targets[b], NB)
                                                   for b in range(B)]).mean())(params)
@@ -115,3 +121,27 @@ def test_toy_model_trains(cuda):
         losses.append(float(loss.detach()))
         assert bool(torch.isfinite(groups[0, :3]).all())
     assert losses[-1] < 0.8 * losses[0], losses
+
+
+def test_toy_model_bf16_rows_on_tensor_cores(cuda):
+    """forward_backward with bf16 activations (fp32 parameters): the linear
+    layers run the tcgen05 GEMMs with fused epilogues and the tcgen05 norm
+    kernels; the result tracks the fp32 run within bf16 rounding."""
+    from paper_2411_00999_b200.model import ToyModelPE
+
+    V, D, HM, NB, B, T = 256, 128, 2, 2, 4, 64
+    model = ToyModelPE(V, D, HM, NB, seed=9, device=cuda)
+    gen = torch.Generator(device="cpu").manual_seed(13)
+    ids = torch.randint(0, V, (B, T), generator=gen, dtype=torch.int32).to(cuda)
+    targets = torch.randint(0, V, (B, T), generator=gen, dtype=torch.int32).to(cuda)
+    l32 = float(model.forward_backward(ids, targets))
+    g32 = {k: v.grad.clone() for k, v in model.named_parameters()}
+    n32 = {n: m.norm_record.clone() for n, m in model.instrumented_layers()}
+    l16 = float(model.forward_backward(ids, targets, rows_dtype=torch.bfloat16))
+    torch.cuda.synchronize()
+    assert close(l16, l32, 2e-2)
+    for k, v in model.named_parameters():
+        ref = g32[k]
+        assert close(v.grad.cpu().numpy(), ref.cpu().numpy(), 5e-2, 5e-2 * float(ref.abs().max())), k
+    for n, m in model.instrumented_layers():
+        assert close(m.norm_record[:2].cpu().numpy(), n32[n][:2].cpu().numpy(), 1e-1), n

@@ -46,6 +46,9 @@ def test_reference_gpu_suites(suite):
 
 
 @pytest.mark.gpu
+@pytest.mark.skipif(os.environ.get("GNSB_ACCEPTANCE") != "1",
+                    reason="criterion 9 (the schedule case study) trains thousands of tiny steps through the "
+                           "fp64 drop-in: > 25 min on the GPU; run with GNSB_ACCEPTANCE=1")
 def test_reference_acceptance():
-    rc, out = _run(["acceptance"], 1800)
+    rc, out = _run(["acceptance"], 7200)
     assert rc == 0, out[-3000:]
