@@ -129,11 +129,14 @@ gnsb_status gnsb_ln_bwd_geometry(int64_t B, int64_t M, int64_t D, gnsb_dtype dt,
  *
  *   form 1 (weight-gradient / "simultaneous" form): dW_b = sum_t x_t^T g_t per
  *          example, raw_w[b] = ||dW_b||_F^2, dW = sum_b dW_b (dW nullable).
- *          bf16 rows with T % 64 == 0, K % 128 == 0, L % 256 == 0 run on the
- *          tcgen05 tensor-core kernel (fp32 accumulate); other shapes/dtypes run
- *          a generic fp64-accumulating CUDA kernel.
+ *          bf16 rows with K % 8 == 0 and L % 8 == 0 (16-byte row strides; any
+ *          T, tile tails zero-filled by TMA) run on the tcgen05 tensor-core
+ *          kernel (fp32 accumulate); fp32 rows and other shapes run a generic
+ *          fp64-accumulating CUDA kernel; fp64 rows follow the reference's
+ *          operation order exactly (batch-invariant per-example values).
  *   form 2 (Gram / Frobenius form): raw_w[b] = <X_b X_b^T, G_b G_b^T>_F; dW must
- *          be NULL (the reference's Frobenius function returns norms only).
+ *          be NULL (the reference's Frobenius function returns norms only);
+ *          tensor cores under the same bf16 / K, L % 8 condition.
  *   form 0 (auto): form 1 when dW is requested; otherwise the cheaper form by
  *          the FLOP model (Gram when T*(K+L) < 2*K*L, proj/src/costmodel.cpp:25-37).
  *   dW    : [K, L] fp32 (fp64 for GNSB_F64 rows).

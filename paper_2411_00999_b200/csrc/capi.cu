@@ -263,7 +263,11 @@ gnsb_status gnsb_ln_bwd_workspace_size(int64_t B, int64_t M, int64_t D, gnsb_dty
     switch (dt) {
         case GNSB_F32: rc = gnsb::ln_bwd_workspace<float>(B, M, D, bytes, &why); break;
         case GNSB_BF16: rc = gnsb::ln_bwd_workspace<__nv_bfloat16>(B, M, D, bytes, &why); break;
-        case GNSB_F64: rc = gnsb::ln_bwd_workspace<double>(B, M, D, bytes, &why); break;
+        case GNSB_F64:
+            rc = gnsb::ln_bwd_workspace<double>(B, M, D, bytes, &why);
+            // + the reference-order scratch of the fp64 path (ln_ref.cu)
+            if (rc == 0) *bytes = (*bytes + 255) / 256 * 256 + gnsb::ln_ref_workspace(B, D);
+            break;
         default: return fail(GNSB_EINVAL, "layers: unknown dtype");
     }
     if (rc) return fail(GNSB_EINVAL, why ? why : "layers: invalid argument");
@@ -321,7 +325,38 @@ gnsb_status gnsb_ln_bwd(const void* x, const void* mean, const void* rstd, const
     switch (dt) {
         case GNSB_F32: rc = gnsb::ln_bwd_run<float>(c, st, &why, &ce); break;
         case GNSB_BF16: rc = gnsb::ln_bwd_run<__nv_bfloat16>(c, st, &why, &ce); break;
-        case GNSB_F64: rc = gnsb::ln_bwd_run<double>(c, st, &why, &ce); break;
+        case GNSB_F64:
+            if (!with_norms) {
+                rc = gnsb::ln_bwd_run<double>(c, st, &why, &ce);
+                break;
+            }
+            {
+                // fp64 rows (the C++ drop-in): dx from the row pass; the
+                // per-example parameter gradients, norms and their sums in the
+                // reference's exact order, so a batched call and B = 1 calls
+                // agree bit for bit (ln_ref.cu)
+                size_t base = 0;
+                if (gnsb::ln_bwd_workspace<double>(B, M, D, &base, &why)) {
+                    rc = 1;
+                    break;
+                }
+                base = (base + 255) / 256 * 256;
+                if (ws_bytes < base + gnsb::ln_ref_workspace(B, D)) {
+                    rc = 1;
+                    why = "layers: workspace too small (query gnsb_ln_bwd_workspace_size)";
+                    break;
+                }
+                rc = gnsb::ln_bwd_rows_run<double>(c, st, &why, &ce);
+                if (rc == 0) {
+                    ce = gnsb::launch_ln_ref_params(
+                        static_cast<const double*>(x), static_cast<const double*>(mean),
+                        static_cast<const double*>(rstd), static_cast<const double*>(dy), B, M, D,
+                        static_cast<double*>(dgamma), static_cast<double*>(dbeta), raw_g, raw_b, sums,
+                        static_cast<unsigned char*>(ws) + base, st);
+                    if (ce != cudaSuccess) rc = 2;
+                }
+            }
+            break;
         default: break;
     }
     if (rc == 1) return fail(GNSB_EINVAL, why ? why : "layers: invalid argument");
@@ -427,7 +462,7 @@ static bool use_tc_gram(gnsb_dtype dt, int64_t B, int64_t T, int64_t K, int64_t 
 
 gnsb_status gnsb_linear_pe_workspace_size(int64_t B, int64_t T, int64_t K, int64_t L, gnsb_dtype dt, size_t* bytes) {
     if (!bytes || B < 0 || T < 0 || K < 1 || L < 1) return fail(GNSB_EINVAL, "layers: invalid extents");
-    size_t n = gnsb::generic_workspace(B, T, K, L);
+    size_t n = dt == GNSB_F64 ? gnsb::generic_workspace_f64(B, T, K, L) : gnsb::generic_workspace(B, T, K, L);
     if (use_tc_wgrad(dt, B, T, K, L)) {
         const size_t m = gnsb::wgrad_workspace(B, K, L);
         n = n > m ? n : m;
@@ -472,7 +507,8 @@ gnsb_status gnsb_linear_bias_pe(const void* g, void* dbias, double* raw_b, doubl
     if (B < 0 || T < 0 || L < 1) return fail(GNSB_EINVAL, "layers: invalid extents");
     if (dt != GNSB_F32 && dt != GNSB_BF16 && dt != GNSB_F64) return fail(GNSB_EINVAL, "layers: unknown dtype");
     if (gnsb_status s = need_device("gnsb_linear_bias_pe")) return s;
-    if (!ws || ws_bytes < gnsb::generic_workspace(B, T, 1, L))
+    const size_t need = dt == GNSB_F64 ? gnsb::generic_workspace_f64(B, T, 1, L) : gnsb::generic_workspace(B, T, 1, L);
+    if (!ws || ws_bytes < need)
         return fail(GNSB_EINVAL, "layers: workspace too small (query gnsb_linear_pe_workspace_size)");
     const cudaError_t e = gnsb::launch_linear_generic((int)dt, 1, nullptr, g, dbias, dt == GNSB_F64, raw_b, sums, 1, B,
                                                       T, 1, L, ws, static_cast<cudaStream_t>(stream));

@@ -229,11 +229,10 @@ struct EmbFastWs {
     int4* ent;      // [B][Tn] {id, start, len, first token}
     int32_t* U;     // [B]
     double* q;      // [B][Tn]
-    double* qbig;   // [nblk] ||dW||^2 of each row block
+    double* qbig;   // [rows-kernel CTAs]
     int32_t* bad;
     int32_t* blk;      // [B][nblk + 1]: first entry of example b with id >= j * kRowsPerWarp
     int64_t nblk;      // row blocks: ceil(V / kRowsPerWarp)
-    unsigned long long* next;  // row-block queue head (zeroed before the rows kernel)
 };
 
 template <int NT>
@@ -362,19 +361,14 @@ __global__ void __launch_bounds__(kEmbRowsThreads, 3) emb_rows_kernel(const T* g
     constexpr int W = Traits<T>::W;
     constexpr int NP = W / 2;
     using P = float2;
+    __shared__ double s_red[kEmbRowsThreads / 32];
     const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int nvec = (int)(D / W);
     const int nchunk = (nvec + 32 * NVC - 1) / (32 * NVC);
-    // persistent warps take row blocks from a queue (no CTA barrier: a warp
-    // that drew rows without matches just takes the next block); results are
-    // per row / per block, so they do not depend on which warp ran a block
-    for (;;) {
-        unsigned long long jb = 0;
-        if (lane == 0) jb = atomicAdd(w.next, 1ull);
-        jb = __shfl_sync(0xffffffffu, jb, 0);
-        if ((int64_t)jb >= w.nblk) break;
-        const int64_t v0 = (int64_t)jb * kRowsPerWarp;
-        double qb = 0.0;  // this lane's share of the block's ||dW||^2
+    double qb = 0.0;  // this lane's share of ||dW||^2
+    for (int64_t v0 = gw * kRowsPerWarp; v0 < V; v0 += nw * kRowsPerWarp) {
         int p[NG], Ub[NG];
         int4 cur[NG];  // the lane's next unconsumed entry of its example
 #pragma unroll
@@ -435,20 +429,18 @@ __global__ void __launch_bounds__(kEmbRowsThreads, 3) emb_rows_kernel(const T* g
                                 }
                             }
                         }
-                        // the run's share of raw_b: fp32 squares of this lane's
-                        // columns, one fp32 butterfly, fp64 from there on
-                        float sq = 0.f;
+                        double sq = 0.0;
 #pragma unroll
                         for (int q = 0; q < NVC; ++q)
 #pragma unroll
                             for (int e = 0; e < NP; ++e) {
                                 acc[q][e].x += tmp[q][e].x;
                                 acc[q][e].y += tmp[q][e].y;
-                                sq = fmaf(tmp[q][e].x, tmp[q][e].x, sq);
-                                sq = fmaf(tmp[q][e].y, tmp[q][e].y, sq);
+                                sq = fma((double)tmp[q][e].x, (double)tmp[q][e].x, sq);
+                                sq = fma((double)tmp[q][e].y, (double)tmp[q][e].y, sq);
                             }
                         sq = warp_sum(sq);
-                        if (lane == bb) qacc[G] += (double)sq;
+                        if (lane == bb) qacc[G] += sq;
                     }
                 }
 #pragma unroll
@@ -478,8 +470,14 @@ __global__ void __launch_bounds__(kEmbRowsThreads, 3) emb_rows_kernel(const T* g
                 }
             }
         }
-        qb = warp_sum(qb);
-        if (lane == 0) w.qbig[jb] = qb;
+    }
+    qb = warp_sum(qb);
+    if (lane == 0) s_red[threadIdx.x >> 5] = qb;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int k = 0; k < kEmbRowsThreads / 32; ++k) t += s_red[k];
+        w.qbig[blockIdx.x] = t;
     }
 }
 
@@ -537,7 +535,7 @@ bool embedding_shape_ok(int64_t T) { return T >= 1 && T <= kEmbMaxT; }
 namespace {
 
 struct EmbFastLayout {
-    size_t perm, ent, U, q, qbig, bad, next, raw, blk, total;
+    size_t perm, ent, U, q, qbig, bad, raw, blk, total;
     int grid;
     int64_t nblk;
 };
@@ -548,7 +546,7 @@ EmbFastLayout emb_fast_layout(int64_t B, int64_t Tn, int64_t V) {
     const int64_t blocks = (V + kRowsPerWarp - 1) / kRowsPerWarp;  // row blocks, one per warp
     const int64_t wpc = kEmbRowsThreads / 32;
     const int64_t grid = (blocks + wpc - 1) / wpc;
-    const int64_t cap = (int64_t)sms * 3;  // persistent: the resident CTAs (3 per SM)
+    const int64_t cap = (int64_t)sms * 16;
     l.grid = (int)(grid < cap ? (grid > 0 ? grid : 1) : cap);
     size_t off = 0;
     auto take = [&](size_t bytes) {
@@ -560,9 +558,8 @@ EmbFastLayout emb_fast_layout(int64_t B, int64_t Tn, int64_t V) {
     l.ent = take((size_t)B * Tn * 16);
     l.U = take((size_t)B * 4);
     l.q = take((size_t)B * Tn * 8);
-    l.qbig = take((size_t)(blocks > 0 ? blocks : 1) * 8);
+    l.qbig = take((size_t)l.grid * 8);
     l.bad = take(4);
-    l.next = take(8);
     l.raw = take((size_t)B * 8);
     l.nblk = blocks;
     l.blk = take((size_t)B * (blocks + 1) * 4);
@@ -599,11 +596,9 @@ cudaError_t emb_fast_run(const int32_t* ids, const void* g, void* dW, double* ra
     EmbFastWs w{reinterpret_cast<int32_t*>(base + l.perm), reinterpret_cast<int4*>(base + l.ent),
                 reinterpret_cast<int32_t*>(base + l.U),    reinterpret_cast<double*>(base + l.q),
                 reinterpret_cast<double*>(base + l.qbig),  reinterpret_cast<int32_t*>(base + l.bad),
-                reinterpret_cast<int32_t*>(base + l.blk),   l.nblk,
-                reinterpret_cast<unsigned long long*>(base + l.next)};
+                reinterpret_cast<int32_t*>(base + l.blk),   l.nblk};
     if (raw == nullptr) raw = reinterpret_cast<double*>(base + l.raw);
     cudaError_t e = cudaMemsetAsync(w.bad, 0, 4, st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(w.next, 0, 8, st);
     if (e != cudaSuccess) return e;
     const int Tp = pow2_at_least(Tn < 32 ? 32 : Tn);  // whole warps in the shuffle stages
     const size_t smem = (size_t)Tp * 8;
@@ -643,7 +638,7 @@ cudaError_t emb_fast_run(const int32_t* ids, const void* g, void* dW, double* ra
     if (e != cudaSuccess) return e;
     if (sums) {
         e = launch_fold_rows(raw, 1, (int)B, nullptr, sums, 0, st);
-        if (e == cudaSuccess) e = launch_fold_rows(w.qbig, 1, (int)l.nblk, nullptr, sums, 2, st);
+        if (e == cudaSuccess) e = launch_fold_rows(w.qbig, 1, l.grid, nullptr, sums, 2, st);
     }
     if (e == cudaSuccess && bad_flag_out) e = cudaMemcpyAsync(bad_flag_out, w.bad, 4, cudaMemcpyDeviceToDevice, st);
     return e;

@@ -77,6 +77,7 @@ size_t wgrad_workspace(int64_t B, int64_t K, int64_t L);
 cudaError_t launch_wgrad_norms(const void* x, const void* g, float* dW, double* raw, double* sums, int64_t B,
                                int64_t T, int64_t K, int64_t L, void* ws, cudaStream_t st);
 size_t generic_workspace(int64_t B, int64_t T, int64_t K, int64_t L);
+size_t generic_workspace_f64(int64_t B, int64_t T, int64_t K, int64_t L);
 // kind 0: weight (simultaneous form), 1: bias, 2: Gram form (norms only)
 cudaError_t launch_linear_generic(int dt, int kind, const void* x, const void* g, void* out_grad, int out_f64,
                                   double* raw, double* sums, int sum_slot, int64_t B, int64_t T, int64_t K, int64_t L,
@@ -102,6 +103,13 @@ size_t gemm_workspace(int dt, int w_dt, int64_t K, int64_t L);
 cudaError_t launch_linear_gemm(int kind, int epi, int dt, int w_dt, const void* in, const void* W, const void* bias,
                                const void* aux, void* out, int64_t rows, int64_t K, int64_t L, void* ws,
                                cudaStream_t st);
+// fp64 rows: per-example parameter gradients / norms in the reference's order (ln_ref.cu)
+size_t ln_ref_workspace(int64_t B, int64_t D);
+cudaError_t launch_ln_ref_params(const double* x, const double* mean, const double* rstd, const double* g, int64_t B,
+                                 int64_t M, int64_t D, double* dgamma, double* dbeta, double* raw_g, double* raw_b,
+                                 double* sums, void* scratch, cudaStream_t st);
+cudaError_t launch_seq_sqnorm(const double* pe, int64_t B, int64_t n, double* raw, double* sums, int sum_slot,
+                              cudaStream_t st);
 // softmax cross-entropy rows (xent.cu): loss_rows[r] = log(sum exp) + max - logit[target],
 // dlogits = (softmax - onehot) * upstream_scale
 cudaError_t launch_xent(int dt, const void* logits, const int32_t* targets, void* dlogits, double* loss_rows,

@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(gr::THREADS, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t units = (int64_t)a.B * a.nunits;
     const int grid = gridDim.x, c = blockIdx.x;
-    const int kbx = a.K / BK, kbg = a.L / BK;
+    const int kbx = (a.K + BK - 1) / BK, kbg = (a.L + BK - 1) / BK;  // feature tails read as zero
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(gr2::THREADS, 1)
     const uint32_t rank = tc::cluster_ctarank();
     const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
     const int64_t units = (int64_t)a.B * a.nunits;
-    const int kbx = a.K / BK, kbg = a.L / BK;
+    const int kbx = (a.K + BK - 1) / BK, kbg = (a.L + BK - 1) / BK;  // feature tails read as zero
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -473,7 +473,7 @@ bool make_map_rows(CUtensorMap* m, const void* base, int B, int T, int F, int ro
 }
 
 int gram_units(int64_t T) {  // units per example: sum over row tiles i of (nJ - i / 2)
-    const int64_t nt = T / gr::BM, nJ = (nt + 1) / 2;
+    const int64_t nt = (T + gr::BM - 1) / gr::BM, nJ = (nt + 1) / 2;
     int64_t n = 0;
     for (int64_t i = 0; i < nt; ++i) n += nJ - i / 2;
     return (int)n;
@@ -482,7 +482,7 @@ int gram_units(int64_t T) {  // units per example: sum over row tiles i of (nJ -
 }  // namespace
 
 int gram2_units(int64_t T) {
-    const int64_t nt = T / gr::BM, nI = (nt + 1) / 2;
+    const int64_t nt = (T + gr::BM - 1) / gr::BM, nI = (nt + 1) / 2;
     return (int)(nI * (nI + 1) / 2);
 }
 
@@ -498,7 +498,7 @@ cudaError_t launch_gram2_norms(const void* x, const void* g, double* raw, double
     a.T = (int)T;
     a.K = (int)K;
     a.L = (int)L;
-    a.nt = (int)(T / gr::BM);
+    a.nt = (int)((T + gr::BM - 1) / gr::BM);
     a.nI = (a.nt + 1) / 2;
     a.nunits = gram2_units(T);
     a.q = static_cast<double*>(ws);
@@ -522,8 +522,10 @@ cudaError_t launch_gram2_norms(const void* x, const void* g, double* raw, double
     return launch_fold_rows(a.q, (int)B, 2 * a.nunits, raw, sums, 0, st);
 }
 
+// Any T, K, L with 16-byte row strides (K, L multiples of 8): tokens past T
+// and features past K / L are zero-filled by TMA and add nothing to either Gram.
 bool gram_shape_ok(int64_t B, int64_t T, int64_t K, int64_t L) {
-    return B >= 1 && T >= gr::BM && T % gr::BM == 0 && K % gr::BK == 0 && L % gr::BK == 0 && K > 0 && L > 0 &&
+    return B >= 1 && T >= 1 && K % 8 == 0 && L % 8 == 0 && K > 0 && L > 0 && K < (1 << 30) && L < (1 << 30) &&
            T < (1 << 20) && B < (1 << 20) && (int64_t)B * gram_units(T) < (1ll << 31);
 }
 
@@ -549,7 +551,7 @@ cudaError_t launch_gram_norms(const void* x, const void* g, double* raw, double*
     a.T = (int)T;
     a.K = (int)K;
     a.L = (int)L;
-    a.nt = (int)(T / gr::BM);
+    a.nt = (int)((T + gr::BM - 1) / gr::BM);
     a.nJ = (a.nt + 1) / 2;
     a.nunits = gram_units(T);
     a.q = static_cast<double*>(ws);

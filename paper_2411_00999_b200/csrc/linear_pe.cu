@@ -27,6 +27,7 @@
 #include <cuda_bf16.h>
 
 #include <cstdlib>
+#include <type_traits>
 #include <mutex>
 
 #include "common.cuh"
@@ -84,7 +85,7 @@ __global__ void __launch_bounds__(wg::THREADS, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntiles = a.tiles_m * a.tiles_n;  // 128 x 256 sub-tiles (q / qbig / ticket indexing)
-    const int kblocks = a.T / BK;
+    const int kblocks = (a.T + BK - 1) / BK;  // tokens past T read as zero
     const uint32_t rank = PAIR ? tc::cluster_ctarank() : 0u;
     // scheduled tiles: 256 x 256 pair tiles (PAIR) or 128 x 256 tiles
     const int tiles_ms = PAIR ? a.tiles_m / 2 : a.tiles_m;
@@ -273,10 +274,12 @@ __global__ void __launch_bounds__(wg::THREADS, 1)
 #pragma unroll
             for (int c = 0; c < 128; ++c) sb = fmaf(S[c], S[c], sb);
             fold8(sb, &a.qbig[tile]);
-            if (a.dW != nullptr) {
-                float4* dst = reinterpret_cast<float4*>(a.dW + (size_t)(i0 + row) * a.L + j0 + half * 128);
+            if (a.dW != nullptr && i0 + row < a.K) {  // tile tails past K / L are not stored
+                const int c0 = j0 + half * 128;
+                float4* dst = reinterpret_cast<float4*>(a.dW + (size_t)(i0 + row) * a.L + c0);
 #pragma unroll
-                for (int c = 0; c < 32; ++c) dst[c] = make_float4(S[4 * c], S[4 * c + 1], S[4 * c + 2], S[4 * c + 3]);
+                for (int c = 0; c < 32; ++c)
+                    if (c0 + 4 * c < a.L) dst[c] = make_float4(S[4 * c], S[4 * c + 1], S[4 * c + 2], S[4 * c + 3]);
             }
         };
         // A tile whose examples are split over several CTAs: every part is
@@ -442,8 +445,11 @@ bool make_map_btf(CUtensorMap* m, const void* base, int B, int T, int F) {
 
 }  // namespace
 
+// Any T, K, L with 16-byte row strides (K, L multiples of 8): TMA zero-fills
+// tokens past T and features past K / L; the epilogue stores only dW's
+// in-range rows and columns.
 bool wgrad_shape_ok(int64_t B, int64_t T, int64_t K, int64_t L) {
-    return B >= 1 && T >= wg::BK && T % wg::BK == 0 && K % wg::BM == 0 && L % wg::BN == 0 && K > 0 && L > 0 &&
+    return B >= 1 && T >= 1 && K % 8 == 0 && L % 8 == 0 && K > 0 && L > 0 && K < (1 << 30) && L < (1 << 30) &&
            T < (1 << 30) && B < (1 << 30);
 }
 
@@ -469,7 +475,7 @@ struct WgradSched {
 };
 WgradSched wgrad_sched(int64_t B, int64_t K, int64_t L, bool pair) {
     WgradSched w;
-    w.stiles = (K / (pair ? 2 * wg::BM : wg::BM)) * (L / wg::BN);
+    w.stiles = ((K + wg::BM - 1) / wg::BM / (pair ? 2 : 1)) * ((L + wg::BN - 1) / wg::BN);
     const int64_t units = w.stiles * B;
     const int sms = pair ? device_sm_count() / 2 : device_sm_count();
     w.grid = (int)(units < sms ? units : sms);
@@ -480,7 +486,7 @@ struct WgradLayout {
     size_t q, qbig, ticket, part, total;
 };
 WgradLayout wgrad_layout(int64_t B, int64_t K, int64_t L, int max_parts) {
-    const int64_t tiles = (K / wg::BM) * (L / wg::BN);  // 128 x 256 sub-tiles
+    const int64_t tiles = ((K + wg::BM - 1) / wg::BM) * ((L + wg::BN - 1) / wg::BN);  // 128 x 256 sub-tiles
     WgradLayout w;
     w.q = 0;
     w.qbig = (size_t)B * tiles * sizeof(double);
@@ -517,8 +523,8 @@ cudaError_t launch_wgrad_norms(const void* x, const void* g, float* dW, double* 
     a.T = (int)T;
     a.K = (int)K;
     a.L = (int)L;
-    a.tiles_m = (int)(K / wg::BM);
-    a.tiles_n = (int)(L / wg::BN);
+    a.tiles_m = (int)((K + wg::BM - 1) / wg::BM);
+    a.tiles_n = (int)((L + wg::BN - 1) / wg::BN);
     a.dW = dW;
     const int ntiles = a.tiles_m * a.tiles_n;
     const WgradSched sc = wgrad_sched(B, K, L, pair);
@@ -565,9 +571,19 @@ cudaError_t launch_wgrad_norms(const void* x, const void* g, float* dW, double* 
 // entry (i, j); per example b it forms dW_b[i, j] = sum_t x*g in fixed t
 // order, adds it to dW and contributes its square to the block's share of
 // raw_b (fixed-order block tree).
+// fp64 rows: the reference's accumulation without contraction (layers.cpp:107-131)
+template <typename T>
+__device__ __forceinline__ double mac(double acc, double a, double b) {
+    if constexpr (std::is_same<T, double>::value) return __dadd_rn(acc, __dmul_rn(a, b));
+    return fma(a, b, acc);
+}
+
+// pe (fp64 rows, nullable): the per-example values dW_b / bias'_b [B][n] for
+// the reference-order norms (launch_seq_sqnorm)
 template <typename T>
 __global__ void __launch_bounds__(256) wgrad_generic_kernel(const T* x, const T* g, int64_t B, int64_t Tn, int64_t K,
-                                                            int64_t L, void* dW, int dw_f64, double* q, int nblk) {
+                                                            int64_t L, void* dW, int dw_f64, double* q, int nblk,
+                                                            double* pe) {
     __shared__ double red[256];
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool ok = idx < K * L;
@@ -577,8 +593,9 @@ __global__ void __launch_bounds__(256) wgrad_generic_kernel(const T* x, const T*
         double v = 0.0;
         if (ok)
             for (int64_t t = 0; t < Tn; ++t)
-                v += (double)to_acc<T>(x[(b * Tn + t) * K + i]) * (double)to_acc<T>(g[(b * Tn + t) * L + j]);
-        S += v;
+                v = mac<T>(v, (double)to_acc<T>(x[(b * Tn + t) * K + i]), (double)to_acc<T>(g[(b * Tn + t) * L + j]));
+        if (pe && ok) pe[b * K * L + idx] = v;
+        S = std::is_same<T, double>::value ? __dadd_rn(S, v) : S + v;
         red[threadIdx.x] = v * v;
         __syncthreads();
         for (int o = 128; o > 0; o >>= 1) {
@@ -606,7 +623,7 @@ __global__ void __launch_bounds__(256) wgrad_generic_kernel(const T* x, const T*
 // per-example bias gradients: bias'_b[j] = sum_t g[b,t,j]; dbias = sum_b; ||bias'_b||^2
 template <typename T>
 __global__ void __launch_bounds__(256) bias_pe_kernel(const T* g, int64_t B, int64_t Tn, int64_t L, void* db,
-                                                      int db_f64, double* q, int nblk) {
+                                                      int db_f64, double* q, int nblk, double* pe) {
     __shared__ double red[256];
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool ok = j < L;
@@ -614,8 +631,9 @@ __global__ void __launch_bounds__(256) bias_pe_kernel(const T* g, int64_t B, int
     for (int64_t b = 0; b < B; ++b) {
         double v = 0.0;
         if (ok)
-            for (int64_t t = 0; t < Tn; ++t) v += (double)to_acc<T>(g[(b * Tn + t) * L + j]);
-        S += v;
+            for (int64_t t = 0; t < Tn; ++t) v = __dadd_rn(v, (double)to_acc<T>(g[(b * Tn + t) * L + j]));
+        if (pe && ok) pe[b * L + j] = v;
+        S = __dadd_rn(S, v);
         red[threadIdx.x] = v * v;
         __syncthreads();
         for (int o = 128; o > 0; o >>= 1) {
@@ -673,6 +691,11 @@ size_t generic_workspace(int64_t B, int64_t T, int64_t K, int64_t L) {
     n = n > n3 ? n : n3;
     return (size_t)(B + 1) * n * sizeof(double) + 256;
 }
+// fp64 rows: + the per-example values [B][K*L] and a raw buffer [B] after the
+// generic area (reference-order norms)
+size_t generic_workspace_f64(int64_t B, int64_t T, int64_t K, int64_t L) {
+    return (generic_workspace(B, T, K, L) + 255) / 256 * 256 + (size_t)B * (K * L + 1) * sizeof(double);
+}
 
 template <typename T>
 cudaError_t launch_generic_t(int kind, const void* x, const void* g, void* out_grad, int out_f64, double* raw,
@@ -680,13 +703,19 @@ cudaError_t launch_generic_t(int kind, const void* x, const void* g, void* out_g
                              cudaStream_t st) {
     double* q = static_cast<double*>(ws);
     int nblk = 0;
+    // fp64 rows: per-example values for the reference-order norms
+    constexpr bool REF = std::is_same<T, double>::value;
+    double* pe = REF && kind != 2
+                     ? reinterpret_cast<double*>(static_cast<unsigned char*>(ws) +
+                                                 (generic_workspace(B, Tn, kind == 0 ? K : 1, L) + 255) / 256 * 256)
+                     : nullptr;
     if (kind == 0) {  // weight, simultaneous form
         nblk = (int)((K * L + 255) / 256);
         wgrad_generic_kernel<T><<<nblk, 256, 0, st>>>(static_cast<const T*>(x), static_cast<const T*>(g), B, Tn, K, L,
-                                                      out_grad, out_f64, q, nblk);
+                                                      out_grad, out_f64, q, nblk, pe);
     } else if (kind == 1) {  // bias
         nblk = (int)((L + 255) / 256);
-        bias_pe_kernel<T><<<nblk, 256, 0, st>>>(static_cast<const T*>(g), B, Tn, L, out_grad, out_f64, q, nblk);
+        bias_pe_kernel<T><<<nblk, 256, 0, st>>>(static_cast<const T*>(g), B, Tn, L, out_grad, out_f64, q, nblk, pe);
     } else {  // Gram form (norms only)
         nblk = (int)((Tn * Tn + 255) / 256);
         gram_generic_kernel<T><<<nblk, 256, 0, st>>>(static_cast<const T*>(x), static_cast<const T*>(g), B, Tn, K, L,
@@ -694,7 +723,13 @@ cudaError_t launch_generic_t(int kind, const void* x, const void* g, void* out_g
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    fold_rows_kernel<<<1, 256, 0, st>>>(q, (int)B, nblk, raw, sums, sum_slot);
+    if (pe) {  // raw_b and sum_b raw_b in the reference's order
+        const int64_t n = kind == 0 ? K * L : L;
+        e = launch_seq_sqnorm(pe, B, n, raw ? raw : pe + B * n, sums, sum_slot, st);
+        if (e != cudaSuccess) return e;
+    } else {
+        fold_rows_kernel<<<1, 256, 0, st>>>(q, (int)B, nblk, raw, sums, sum_slot);
+    }
     if (sums && kind != 2) fold_rows_kernel<<<1, 256, 0, st>>>(q + (size_t)B * nblk, 1, nblk, nullptr, sums, sum_slot + 2);
     return cudaGetLastError();
 }

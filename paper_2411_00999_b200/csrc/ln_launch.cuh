@@ -346,12 +346,15 @@ struct FwdOp {
     }
 };
 
-// GNSB_LN_FOLD=1: the CTA-folded variants of the D = 1024 / 2048 configurations
-// (A/B runs); default: no end-of-kernel fold, stage 2 sums the group slots.
+// GNSB_LN_NOFOLD=1 (A/B runs only): the D = 1024 / 2048 configurations
+// without the end-of-kernel CTA fold (every row group leaves its own slot and
+// stage 2 sums the G sub-slots).  Measured slower in the steady 8-layer step:
+// 364 / 654 us against 343 / 621 us at D = 1024 / 2048 (the row pass itself
+// got ~2 us slower, and stage 2 reads G x the slots), so the fold stays.
 inline bool ln_fold() {
     static const bool v = [] {
-        const char* e = getenv("GNSB_LN_FOLD");
-        return e && e[0] == '1';
+        const char* e = getenv("GNSB_LN_NOFOLD");
+        return !(e && e[0] == '1');
     }();
     return v;
 }

@@ -72,7 +72,9 @@ def _oracle_linear(orc, x, g):
 
 @pytest.mark.parametrize("impl", ["pair", "single"])
 @pytest.mark.parametrize("B,T,K,L", [(2, 64, 128, 256), (3, 128, 256, 512), (4, 192, 128, 256), (1, 64, 384, 256),
-                                     (5, 64, 512, 768), (3, 64, 2048, 2560)])
+                                     (5, 64, 512, 768), (3, 64, 2048, 2560),
+                                     # tile tails in every axis (TMA zero fill + masked dW stores)
+                                     (3, 100, 136, 264), (2, 1, 8, 8), (4, 77, 512, 520), (2, 200, 264, 128)])
 def test_tcgen05_weight_grad_form_matches_oracle(orc, cuda, monkeypatch, impl, B, T, K, L):
     """bf16 rows on the tensor-core kernel vs the fp64 oracle on identical inputs.
     "pair": the default CTA-pair kernel (256 x 256 tiles; K % 256 == 0, else the
@@ -133,10 +135,12 @@ def test_cfg3_full_size_sampled(orc, cuda):
     assert float((dW - ref_dW).abs().max()) <= 1e-4 * float(ref_dW.abs().max())
 
 
-@pytest.mark.parametrize("B,T,K,L", [(2, 128, 64, 64), (3, 256, 128, 192), (1, 384, 256, 128), (5, 128, 320, 64)])
+@pytest.mark.parametrize("B,T,K,L", [(2, 128, 64, 64), (3, 256, 128, 192), (1, 384, 256, 128), (5, 128, 320, 64),
+                                     # tails: T off the 128-token tile, K / L off the 64-feature stage
+                                     (3, 100, 136, 72), (2, 1, 8, 8), (2, 300, 64, 520), (4, 129, 200, 96)])
 def test_tcgen05_gram_form_matches_oracle(orc, cuda, B, T, K, L):
-    """Tensor-core Gram form (bf16 rows, T % 128 == 0, K, L % 64 == 0) vs the fp64
-    oracle's <X X^T, G G^T>_F on identical inputs (rel 1e-4)."""
+    """Tensor-core Gram form (bf16 rows, any T, K and L multiples of 8) vs the
+    fp64 oracle's <X X^T, G G^T>_F on identical inputs (rel 1e-4)."""
     import paper_2411_00999_b200 as m
     from paper_2411_00999_b200 import linear
 

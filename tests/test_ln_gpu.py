@@ -503,7 +503,53 @@ def test_row_pass_edge_cases_match_oracle(orc, cuda, dt, B, T, D, offset, use_xh
         assert close(gr.per_example_sqnorms_raw["gamma"].cpu().numpy(), ref["raw_gamma"], nt)
         assert close(gr.per_example_sqnorms_raw["beta"].cpu().numpy(), ref["raw_beta"], nt)
     assert torch.equal(r.input_grad, dxd)
-    assert torch.equal(r.grads.weight_grads["gamma"], rd.weight_grads["gamma"])
+    if dt == torch.float64:
+        # fp64 gnsb_ln_bwd forms the per-example parameter gradients, norms and
+        # their sums in the reference's order (ln_ref.cu): bit-identical to the
+        # reference restatement on the x-hat cache it consumes
+        if use_xhat:
+            np.testing.assert_array_equal(r.grads.weight_grads["gamma"].cpu().numpy(), ref["dgamma"])
+            np.testing.assert_array_equal(r.grads.weight_grads["beta"].cpu().numpy(), ref["dbeta"])
+            np.testing.assert_array_equal(r.grads.per_example_sqnorms_raw["gamma"].cpu().numpy(), ref["raw_gamma"])
+            np.testing.assert_array_equal(r.grads.per_example_sqnorms_raw["beta"].cpu().numpy(), ref["raw_beta"])
+    else:
+        assert torch.equal(r.grads.weight_grads["gamma"], rd.weight_grads["gamma"])
+
+
+def test_fp64_per_example_values_are_batch_invariant(cuda):
+    """fp64 rows: example b's share of a batched call equals a B = 1 call on
+    its rows bit for bit (what the reference's PerExample-vs-Microbatch trainer
+    identity needs, proj/tests/test_trainer.cpp:123-130), for the LayerNorm and
+    the linear layer."""
+    from paper_2411_00999_b200 import linear
+
+    m = _mod()
+    B, T, D = 4, 24, 40
+    x, dy, gamma, beta = m.synth_ln(B, T, D, torch.float64, cuda, stream0=5)
+    layer = m.LayerNormLayer(gamma, beta, 1e-5)
+    xh = m.layernorm_forward(layer, x, keep_normalized=True).cache
+    cache = m.LayerNormCache(normalized=xh.normalized, inv_std=xh.inv_std)
+    full = m.layernorm_backward_simultaneous(layer, cache, dy)
+    W = torch.randn(D, 24, dtype=torch.float64, device=cuda)
+    g2 = torch.randn(B, T, 24, dtype=torch.float64, device=cuda)
+    lfull = linear.linear_backward_simultaneous(linear.LinearLayer(W, torch.zeros(24, dtype=torch.float64, device=cuda)),
+                                                x, g2, need_input_grad=False)
+    for b in range(B):
+        one = m.layernorm_backward_simultaneous(
+            layer, m.LayerNormCache(normalized=cache.normalized[b:b + 1], inv_std=cache.inv_std[b:b + 1]), dy[b:b + 1])
+        assert float(one.grads.per_example_sqnorms_raw["gamma"][0]) == float(full.grads.per_example_sqnorms_raw["gamma"][b])
+        assert float(one.grads.per_example_sqnorms_raw["beta"][0]) == float(full.grads.per_example_sqnorms_raw["beta"][b])
+        lo = linear.linear_backward_simultaneous(
+            linear.LinearLayer(W, torch.zeros(24, dtype=torch.float64, device=cuda)), x[b:b + 1], g2[b:b + 1],
+            need_input_grad=False)
+        assert float(lo.grads.per_example_sqnorms_raw["weight"][0]) == float(lfull.grads.per_example_sqnorms_raw["weight"][b])
+        assert float(lo.grads.per_example_sqnorms_raw["bias"][0]) == float(lfull.grads.per_example_sqnorms_raw["bias"][b])
+        # and the squared norm of the B = 1 gradient, summed in order, is that raw value
+        dg = one.grads.weight_grads["gamma"].cpu().numpy()
+        s = 0.0
+        for v in dg:
+            s += v * v
+        assert s == float(full.grads.per_example_sqnorms_raw["gamma"][b])
 
 
 @pytest.mark.parametrize("dt,D", [(torch.bfloat16, 1024), (torch.float32, 768)])

@@ -54,7 +54,7 @@ def test_toy_model_per_example_norms_and_gns(cuda, path):
 
     params = {k: v.detach() for k, v in model.named_parameters()}
     ref_loss = torch.stack([_functional_loss(params, ids[b], targets[b], NB) for b in range(B)]).mean()
-    assert close(float(loss), float(ref_loss), 1e-5)
+    assert close(float(loss.detach()), float(ref_loss), 1e-5)
     per_ex = torch.func.vmap(torch.func.grad(_functional_loss), in_dims=(None, 0, 0, None))(params, ids, targets, NB)
     full = torch.func.grad(lambda p: torch.stack([_functional_loss(p, ids[b], targets[b], NB)
                                                   for b in range(B)]).mean())(params)
