@@ -36,6 +36,9 @@ __global__ void ldred_kernel(const float* mc_f, float* out, int n) {
     out[i] = v;
 }
 
+#ifndef NDEV
+#define NDEV 1
+#endif
 int main() {
     CK(cuInit(0));
     CUdevice dev;
@@ -50,21 +53,33 @@ int main() {
     std::printf("multicast_supported=%d fabric_handles=%d posix_fd_handles=%d\n", mc, fab, posix);
     if (!mc) return 0;
     CUmulticastObjectProp mp = {};
-    mp.numDevices = 1;
-    mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
     size_t gran = 0;
-    mp.size = 1 << 21;
-    CK(cuMulticastGetGranularity(&gran, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED));
-    mp.size = (mp.size + gran - 1) / gran * gran;
-    std::printf("granularity=%zu size=%zu\n", gran, mp.size);
     CUmemGenericAllocationHandle mch;
-    CK(cuMulticastCreate(&mch, &mp));
+    bool made = false;
+    const CUmemAllocationHandleType types[3] = {CU_MEM_HANDLE_TYPE_FABRIC, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR,
+                                                CU_MEM_HANDLE_TYPE_NONE};
+    for (int ti = 0; ti < 3 && !made; ++ti) {
+        mp = CUmulticastObjectProp{};
+        mp.numDevices = NDEV;
+        mp.handleTypes = types[ti];
+        mp.size = 1 << 21;
+        CUresult r = cuMulticastGetGranularity(&gran, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED);
+        if (r != CUDA_SUCCESS) {
+            std::printf("granularity(handle type %d): %d\n", (int)types[ti], (int)r);
+            continue;
+        }
+        mp.size = (mp.size + gran - 1) / gran * gran;
+        r = cuMulticastCreate(&mch, &mp);
+        std::printf("cuMulticastCreate(numDevices=%d, handle type %d, size %zu): %d\n", NDEV, (int)types[ti], mp.size, (int)r);
+        made = r == CUDA_SUCCESS;
+    }
+    if (!made) return 1;
     CK(cuMulticastAddDevice(mch, dev));
     CUmemAllocationProp ap = {};
     ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
     ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
     ap.location.id = 0;
-    ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    ap.requestedHandleTypes = static_cast<CUmemAllocationHandleType>(mp.handleTypes);
     CUmemGenericAllocationHandle mem;
     CK(cuMemCreate(&mem, mp.size, &ap, 0));
     CK(cuMulticastBindMem(mch, 0, mem, 0, mp.size, 0));

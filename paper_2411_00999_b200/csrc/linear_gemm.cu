@@ -40,9 +40,38 @@ constexpr int B_BYTES = BN * BK * 2;  // 32 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = (2 + EPI_WARPS) * 32;
-constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 256;
+constexpr int OUT_BOX_BYTES = 32 * 128;      // one epilogue warp's store box: 32 rows x 64 bf16 (128B swizzle)
+// align slack + ring + barrier block (1 KB) + the epilogue store boxes
+constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 1024 + (size_t)EPI_WARPS * OUT_BOX_BYTES;
+static_assert(SMEM <= 232448, "dynamic shared memory of one CTA");
 constexpr int TMEM_COLS = 512;
+constexpr int GROUP_M = 8;  // tile raster: GROUP_M row blocks x all column tiles, row block fastest
 }  // namespace gm
+
+// TMA store of a staged shared-memory box to global (bulk async group)
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* smem_src, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(smem_u32(smem_src)), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// tile index -> (row block, column tile): GROUP_M row blocks share a band of
+// column tiles so one wave of CTAs reuses both A row blocks and W column
+// tiles through L2 (a plain column-fastest order re-reads W from DRAM once
+// W outgrows L2)
+__device__ __forceinline__ void tile_mn(int t, int tiles_m, int tiles_n, int& mt, int& nt) {
+    const int band = t / (gm::GROUP_M * tiles_n);
+    const int first = band * gm::GROUP_M;
+    const int rows = tiles_m - first < gm::GROUP_M ? tiles_m - first : gm::GROUP_M;
+    const int local = t - band * gm::GROUP_M * tiles_n;
+    mt = first + local % rows;
+    nt = local / rows;
+}
 
 // Epilogues fused into the store (the toy model's elementwise ops,
 // proj/src/model.cpp:95-100 and :169-171): v = acc (+ bias), then
@@ -70,7 +99,8 @@ struct GemmArgs {
 
 template <bool B_KMAJOR, bool BIAS, int EPI>
 __global__ void __launch_bounds__(gm::THREADS, 1)
-    gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb, GemmArgs a) {
+    gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
+                const __grid_constant__ CUtensorMap tmo, GemmArgs a) {
     using namespace gm;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem =
@@ -81,6 +111,7 @@ __global__ void __launch_bounds__(gm::THREADS, 1)
     uint64_t* tfull = empty + STAGES;  // [2]
     uint64_t* tempty = tfull + 2;      // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    unsigned char* obox = smem + (size_t)STAGES * STAGE_BYTES + 1024;  // [EPI_WARPS][32 rows][128 B], 1 KB aligned
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntiles = a.tiles_m * a.tiles_n;
@@ -98,6 +129,7 @@ __global__ void __launch_bounds__(gm::THREADS, 1)
         fence_mbar_init();
         tc::prefetch_tmap(&tma);
         tc::prefetch_tmap(&tmb);
+        tc::prefetch_tmap(&tmo);
     }
     if (warp == 1) tc::tmem_alloc<TMEM_COLS>(tmem_slot);
     tc::fence_before_sync();
@@ -113,7 +145,9 @@ __global__ void __launch_bounds__(gm::THREADS, 1)
             int s = 0;
             uint32_t ph = 0;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-                const int m0 = (t / a.tiles_n) * BM, n0 = (t % a.tiles_n) * BN;
+                int mt, nt;
+                tile_mn(t, a.tiles_m, a.tiles_n, mt, nt);
+                const int m0 = mt * BM, n0 = nt * BN;
                 for (int kb = 0; kb < kblocks; ++kb) {
                     mbar_wait(&empty[s], ph ^ 1u);
                     unsigned char* st = ring + (size_t)s * STAGE_BYTES;
@@ -174,53 +208,75 @@ __global__ void __launch_bounds__(gm::THREADS, 1)
         }
     } else {
         // -------------------------------------------------------- epilogue --
+        // Each warp owns 32 TMEM lanes (rows) x 128 columns of the tile.  Per
+        // 64-column group it rounds its values to bf16 into a 32 x 64 box in
+        // shared memory (128-byte swizzle: conflict-free 16-byte writes) and
+        // one lane stores the box with TMA (coalesced; rows / columns past the
+        // output are clipped by the tensor map).
         const int e = warp - 2;
         const int quad = warp & 3;  // TMEM lanes this warp may access
         const int half = e / 4;     // column half of the 256-wide tile
+        unsigned char* box = obox + (size_t)e * OUT_BOX_BYTES;
         int buf = 0;
         uint32_t tph = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            const int m0 = (t / a.tiles_n) * BM, n0 = (t % a.tiles_n) * BN;
+            int mt, nt;
+            tile_mn(t, a.tiles_m, a.tiles_n, mt, nt);
+            const int m0 = mt * BM, n0 = nt * BN;
             const int row = m0 + quad * 32 + lane;
             mbar_wait(&tfull[buf], tph);
             tc::fence_after_sync();
             const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN + half * 128);
 #pragma unroll
-            for (int cc = 0; cc < 4; ++cc) {
-                uint32_t r[32];
-                tc::tmem_ld_32x32b_x32(base + cc * 32, r);
-                tc::tmem_ld_wait();
-                if (cc == 3) {  // the accumulator is in registers: hand it back to the MMA warp
-                    tc::fence_before_sync();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&tempty[buf]);
+            for (int gi = 0; gi < 2; ++gi) {
+                // the previous TMA store from this box has finished reading it
+                if (lane == 0) bulk_wait_read0();
+                __syncwarp();
+#pragma unroll
+                for (int c2 = 0; c2 < 2; ++c2) {
+                    const int cc = gi * 2 + c2;
+                    uint32_t r[32];
+                    tc::tmem_ld_32x32b_x32(base + cc * 32, r);
+                    tc::tmem_ld_wait();
+                    if (cc == 3) {  // the accumulator is in registers: hand it back to the MMA warp
+                        tc::fence_before_sync();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&tempty[buf]);
+                    }
+                    const int c0 = n0 + half * 128 + cc * 32;
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        float f[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) f[j] = __uint_as_float(r[8 * v + j]);
+                        if constexpr (BIAS) {
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) f[j] += c0 + 8 * v + j < a.N ? __ldg(a.bias + c0 + 8 * v + j) : 0.f;
+                        }
+                        if constexpr (EPI != EPI_NONE) {
+                            float x[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                            if constexpr (EPI == EPI_RESID || EPI == EPI_DTANH) {
+                                if (row < a.M && c0 + 8 * v < a.N)
+                                    unpack<__nv_bfloat16>(
+                                        __ldg(reinterpret_cast<const uint4*>(a.aux + (size_t)row * a.N + c0 + 8 * v)), x);
+                            }
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) f[j] = epi_apply<EPI>(f[j], x[j]);
+                        }
+                        uint4 o;
+                        o.x = pack_bf16x2(f[0], f[1]);
+                        o.y = pack_bf16x2(f[2], f[3]);
+                        o.z = pack_bf16x2(f[4], f[5]);
+                        o.w = pack_bf16x2(f[6], f[7]);
+                        const int chunk = c2 * 4 + v;  // 16-byte chunk of the 128-byte box row
+                        *reinterpret_cast<uint4*>(box + lane * 128 + ((chunk ^ (lane & 7)) << 4)) = o;
+                    }
                 }
-                const int c0 = n0 + half * 128 + cc * 32;
-                if (row >= a.M) continue;
-                __nv_bfloat16* dst = a.out + (size_t)row * a.N + c0;
-#pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                    if (c0 + 8 * v >= a.N) break;  // N % 8 == 0: a vector is fully in or out
-                    float f[8];
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) f[j] = __uint_as_float(r[8 * v + j]);
-                    if constexpr (BIAS) {
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) f[j] += __ldg(a.bias + c0 + 8 * v + j);
-                    }
-                    if constexpr (EPI != EPI_NONE) {
-                        float x[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                        if constexpr (EPI == EPI_RESID || EPI == EPI_DTANH)
-                            unpack<__nv_bfloat16>(__ldg(reinterpret_cast<const uint4*>(a.aux + (size_t)row * a.N + c0 + 8 * v)), x);
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) f[j] = epi_apply<EPI>(f[j], x[j]);
-                    }
-                    uint4 o;
-                    o.x = pack_bf16x2(f[0], f[1]);
-                    o.y = pack_bf16x2(f[2], f[3]);
-                    o.z = pack_bf16x2(f[4], f[5]);
-                    o.w = pack_bf16x2(f[6], f[7]);
-                    *reinterpret_cast<uint4*>(dst + 8 * v) = o;
+                fence_proxy_async_smem();  // generic-proxy writes -> visible to the TMA (async proxy)
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_3d(&tmo, box, n0 + half * 128 + gi * 64, m0 + quad * 32, 0);
+                    bulk_commit();
                 }
             }
             if (++buf == 2) {
@@ -228,6 +284,7 @@ __global__ void __launch_bounds__(gm::THREADS, 1)
                 tph ^= 1u;
             }
         }
+        if (lane == 0) bulk_wait0();  // every store of this warp complete before the CTA exits
     }
     tc::fence_before_sync();
     __syncthreads();
@@ -311,7 +368,8 @@ bool make_map_2d(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, i
 }
 
 template <bool BK_, bool BIAS, int EPI>
-cudaError_t launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, cudaStream_t st) {
+cudaError_t launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo, const GemmArgs& a,
+                      cudaStream_t st) {
     const void* fn = reinterpret_cast<const void*>(gemm_kernel<BK_, BIAS, EPI>);
     cudaError_t e = ensure_smem_attr(fn, gm::SMEM);
     if (e != cudaSuccess) return e;
@@ -327,7 +385,7 @@ cudaError_t launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const GemmAr
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, gemm_kernel<BK_, BIAS, EPI>, ma, mb, a);
+    return cudaLaunchKernelEx(&cfg, gemm_kernel<BK_, BIAS, EPI>, ma, mb, mo, a);
 }
 
 }  // namespace
@@ -364,6 +422,8 @@ cudaError_t launch_linear_gemm(int kind, int epi, int dt, int w_dt, const void* 
         const bool ok = kind == 0 ? make_map_2d(&mb, wb, K, L, 64, gm::BK)       // W [K, L]: box 64 (L) x 64 (K)
                                   : make_map_2d(&mb, wb, K, L, gm::BK, gm::BN);  // W [K, L]: box 64 (L) x 256 (K)
         if (!ok) return cudaErrorInvalidValue;
+        CUtensorMap mo;  // the output [rows, N], stored by 32-row x 64-column boxes
+        if (!make_map_2d(&mo, out, rows, N, 64, 32)) return cudaErrorInvalidValue;
         GemmArgs a{};
         a.M = (int)rows;
         a.N = (int)N;
@@ -374,17 +434,17 @@ cudaError_t launch_linear_gemm(int kind, int epi, int dt, int w_dt, const void* 
         a.aux = static_cast<const __nv_bfloat16*>(aux);
         a.out = static_cast<__nv_bfloat16*>(out);
         if (kind == 1) {
-            if (epi == EPI_DTANH) return launch_tc<true, false, EPI_DTANH>(ma, mb, a, st);
-            return launch_tc<true, false, EPI_NONE>(ma, mb, a, st);
+            if (epi == EPI_DTANH) return launch_tc<true, false, EPI_DTANH>(ma, mb, mo, a, st);
+            return launch_tc<true, false, EPI_NONE>(ma, mb, mo, a, st);
         }
         switch (epi) {
             case EPI_TANH:
-                return bias ? launch_tc<false, true, EPI_TANH>(ma, mb, a, st) : launch_tc<false, false, EPI_TANH>(ma, mb, a, st);
+                return bias ? launch_tc<false, true, EPI_TANH>(ma, mb, mo, a, st) : launch_tc<false, false, EPI_TANH>(ma, mb, mo, a, st);
             case EPI_RESID:
-                return bias ? launch_tc<false, true, EPI_RESID>(ma, mb, a, st)
-                            : launch_tc<false, false, EPI_RESID>(ma, mb, a, st);
+                return bias ? launch_tc<false, true, EPI_RESID>(ma, mb, mo, a, st)
+                            : launch_tc<false, false, EPI_RESID>(ma, mb, mo, a, st);
             default:
-                return bias ? launch_tc<false, true, EPI_NONE>(ma, mb, a, st) : launch_tc<false, false, EPI_NONE>(ma, mb, a, st);
+                return bias ? launch_tc<false, true, EPI_NONE>(ma, mb, mo, a, st) : launch_tc<false, false, EPI_NONE>(ma, mb, mo, a, st);
         }
     }
     const int64_t n = rows * N;
