@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kEmbThreads) emb_table_kernel(int64_t B, int64
 //     column vectors; a one-token run needs no perm load) into dE_b[v], adds
 //     that to dW[v] and reduces ||dE_b[v]||^2 into q[b][k].  g is read once
 //     and dW written once, 16 bytes per lane per vector.
-//   * emb_raw_kernel: raw_b = sum_k q[b][k] (one warp per example, fixed-order
+//   * emb_raw_kernel: raw_b = sum_k q[b][k] (one CTA per example, fixed-order
 //     tree); the scalar sums by fold_rows_kernel.
 // dW matches the original path bit for bit (same per-example Acc sums, added
 // in example order); raw_b differs in summation order only.
@@ -261,10 +261,15 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* s_warp, int* tot
     return before + x - v;
 }
 
+// Key = id << SH | t (SH = 32 with 64-bit keys; with 32-bit keys SH = log2(Tp),
+// used when every id fits: half the shared-memory and shuffle traffic).
+template <typename KT>
 __global__ void __launch_bounds__(kEmbSortThreads) emb_sort_kernel(const int32_t* ids, int64_t Tn, int64_t V,
-                                                                   EmbFastWs w, int Tp) {
+                                                                   EmbFastWs w, int Tp, int SH) {
     extern __shared__ __align__(16) unsigned char smem[];
-    uint64_t* keys = reinterpret_cast<uint64_t*>(smem);  // [Tp]
+    KT* keys = reinterpret_cast<KT*>(smem);  // [Tp]
+    const KT TM = (KT(1) << SH) - 1;         // token mask
+    const KT NONE = ~KT(0);
     __shared__ int s_warp[kEmbSortThreads / 32];
     __shared__ int s_nvalid;
     const int64_t b = blockIdx.x;
@@ -272,13 +277,13 @@ __global__ void __launch_bounds__(kEmbSortThreads) emb_sort_kernel(const int32_t
     const int32_t* idb = ids + b * Tn;
     if (tid == 0) s_nvalid = 0;
     for (int i = tid; i < Tp; i += blockDim.x) {
-        uint64_t k = ~0ull;
+        KT k = NONE;
         if (i < Tn) {
             const int32_t id = idb[i];
             if (id < 0 || id >= V)
                 atomicExch(w.bad, 1);
             else
-                k = ((uint64_t)(uint32_t)id << 32) | (uint32_t)i;
+                k = ((KT)(uint32_t)id << SH) | (KT)(uint32_t)i;
         }
         keys[i] = k;
     }
@@ -291,7 +296,7 @@ __global__ void __launch_bounds__(kEmbSortThreads) emb_sort_kernel(const int32_t
             for (int i = tid; i < Tp; i += blockDim.x) {
                 const int j = i ^ stride;
                 if (j > i) {
-                    const uint64_t a = keys[i], c = keys[j];
+                    const KT a = keys[i], c = keys[j];
                     const bool up = (i & size) == 0;
                     if ((a > c) == up) {
                         keys[i] = c;
@@ -304,10 +309,10 @@ __global__ void __launch_bounds__(kEmbSortThreads) emb_sort_kernel(const int32_t
         for (int i0 = 0; i0 < Tp; i0 += blockDim.x) {
             if (i0 + (tid & ~31) >= Tp) break;  // warp-uniform
             const int i = i0 + tid;
-            uint64_t v = keys[i];
+            KT v = keys[i];
             const bool up = (i & size) == 0;
             for (int s2 = stride; s2 > 0; s2 >>= 1) {
-                const uint64_t o = __shfl_xor_sync(0xffffffffu, v, s2);
+                const KT o = __shfl_xor_sync(0xffffffffu, v, s2);
                 const bool keep_min = ((i & s2) == 0) == up;  // the lower element keeps the min when ascending
                 v = keep_min ? (o < v ? o : v) : (o > v ? o : v);
             }
@@ -319,8 +324,8 @@ __global__ void __launch_bounds__(kEmbSortThreads) emb_sort_kernel(const int32_t
     // thread scans a contiguous chunk; a block scan numbers the runs.
     const int per = (Tp + kEmbSortThreads - 1) / kEmbSortThreads;
     const int i0 = tid * per, i1 = min(i0 + per, Tp);
-    auto valid = [&](int i) { return i < Tp && keys[i] != ~0ull; };
-    auto head = [&](int i) { return valid(i) && (i == 0 || (uint32_t)(keys[i - 1] >> 32) != (uint32_t)(keys[i] >> 32)); };
+    auto valid = [&](int i) { return i < Tp && keys[i] != NONE; };
+    auto head = [&](int i) { return valid(i) && (i == 0 || (uint32_t)(keys[i - 1] >> SH) != (uint32_t)(keys[i] >> SH)); };
     int cnt = 0, nv = 0;
     for (int i = i0; i < i1; ++i) {
         if (!valid(i)) break;
@@ -336,32 +341,32 @@ __global__ void __launch_bounds__(kEmbSortThreads) emb_sort_kernel(const int32_t
     int32_t* blk = w.blk + b * (w.nblk + 1);
     for (int i = i0; i < i1; ++i) {
         if (!valid(i)) break;
-        perm[i] = (int32_t)(uint32_t)(keys[i] & 0xffffffffu);
+        perm[i] = (int32_t)(uint32_t)(keys[i] & TM);
         if (head(i)) {
-            const uint32_t id = (uint32_t)(keys[i] >> 32);
+            const uint32_t id = (uint32_t)(keys[i] >> SH);
             int e = i + 1;
-            while (e < nvalid && (uint32_t)(keys[e] >> 32) == id) ++e;
-            ent[r] = make_int4((int)id, i, e - i, (int)(uint32_t)(keys[i] & 0xffffffffu));
+            while (e < nvalid && (uint32_t)(keys[e] >> SH) == id) ++e;
+            ent[r] = make_int4((int)id, i, e - i, (int)(uint32_t)(keys[i] & TM));
             // row blocks whose first row lies in (previous id, id] start at entry r
-            const int64_t j_lo = r == 0 ? 0 : (int64_t)((uint32_t)(keys[i - 1] >> 32) / kRowsPerWarp) + 1;
+            const int64_t j_lo = r == 0 ? 0 : (int64_t)((uint32_t)(keys[i - 1] >> SH) / kRowsPerWarp) + 1;
             const int64_t j_hi = (int64_t)(id / kRowsPerWarp);
             for (int64_t j = j_lo; j <= j_hi; ++j) blk[j] = r;
             ++r;
         }
     }
     // blocks after the last id start past the end
-    const int64_t j_tail = nvalid > 0 ? (int64_t)((uint32_t)(keys[nvalid - 1] >> 32) / kRowsPerWarp) + 1 : 0;
+    const int64_t j_tail = nvalid > 0 ? (int64_t)((uint32_t)(keys[nvalid - 1] >> SH) / kRowsPerWarp) + 1 : 0;
     for (int64_t j = j_tail + tid; j <= w.nblk; j += blockDim.x) blk[j] = total;
     if (tid == 0) w.U[b] = total;
 }
 
-template <typename T, int NVC, int NG>
-__global__ void __launch_bounds__(kEmbRowsThreads, 3) emb_rows_kernel(const T* g, int64_t B, int64_t Tn, int64_t V,
-                                                                   int64_t D, EmbFastWs w, float* dW) {
+template <typename T, int NVC, int NG, int NT = kEmbRowsThreads>
+__global__ void __launch_bounds__(NT, 768 / NT) emb_rows_kernel(const T* g, int64_t B, int64_t Tn, int64_t V,
+                                                                int64_t D, EmbFastWs w, float* dW) {
     constexpr int W = Traits<T>::W;
     constexpr int NP = W / 2;
     using P = float2;
-    __shared__ double s_red[kEmbRowsThreads / 32];
+    __shared__ double s_red[NT / 32];
     const int lane = threadIdx.x & 31;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -476,21 +481,30 @@ __global__ void __launch_bounds__(kEmbRowsThreads, 3) emb_rows_kernel(const T* g
     __syncthreads();
     if (threadIdx.x == 0) {
         double t = 0.0;
-        for (int k = 0; k < kEmbRowsThreads / 32; ++k) t += s_red[k];
+        for (int k = 0; k < NT / 32; ++k) t += s_red[k];
         w.qbig[blockIdx.x] = t;
     }
 }
 
-// raw_b = sum_k q[b][k]: one warp per example, fixed-order tree
+// raw_b = sum_k q[b][k]: one 256-thread CTA per example.  Every load is
+// issued before the first add (a thread owns a strided set of at most
+// Tn / 256 entries), then a fixed-order tree: one L2 round trip instead of
+// U / 32 dependent ones (the warp-per-example version was latency-bound,
+// 9.5 us at T = 1024).
 __global__ void __launch_bounds__(256) emb_raw_kernel(int64_t B, int64_t Tn, EmbFastWs w, double* raw) {
-    const int lane = threadIdx.x & 31;
-    const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (b >= B) return;
+    __shared__ double s_red[256];
+    const int64_t b = blockIdx.x;
     const int U = w.U[b];
     double s = 0.0;
-    for (int k = lane; k < U; k += 32) s += w.q[b * Tn + k];
-    s = warp_sum(s);
-    if (lane == 0) raw[b] = s;
+#pragma unroll 8
+    for (int k = threadIdx.x; k < U; k += 256) s += __ldcg(w.q + b * Tn + k);
+    s_red[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) s_red[threadIdx.x] += s_red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) raw[b] = s_red[0];
 }
 
 int pow2_at_least(int64_t n) {
@@ -540,13 +554,25 @@ struct EmbFastLayout {
     int64_t nblk;
 };
 
+// threads per row-walk CTA: 256, or 64 (B <= 32; GNSB_EMB_CTA=64, A/B runs).
+// Smaller CTAs retire independently (one warp with many matched rows holds
+// back a 2-warp CTA instead of an 8-warp one) but measured no faster at GPT-2
+// size: 84.0 us against 82.7 us.
+int emb_rows_threads(int64_t B) {
+    static const int v = [] {
+        const char* e = std::getenv("GNSB_EMB_CTA");
+        return (e && std::atoi(e) == 64) ? 64 : kEmbRowsThreads;
+    }();
+    return B <= 32 ? v : kEmbRowsThreads;
+}
+
 EmbFastLayout emb_fast_layout(int64_t B, int64_t Tn, int64_t V) {
     EmbFastLayout l{};
     const int sms = device_sm_count();
     const int64_t blocks = (V + kRowsPerWarp - 1) / kRowsPerWarp;  // row blocks, one per warp
-    const int64_t wpc = kEmbRowsThreads / 32;
+    const int64_t wpc = emb_rows_threads(B) / 32;
     const int64_t grid = (blocks + wpc - 1) / wpc;
-    const int64_t cap = (int64_t)sms * 16;
+    const int64_t cap = (int64_t)sms * 16 * (kEmbRowsThreads / 32) / wpc;
     l.grid = (int)(grid < cap ? (grid > 0 ? grid : 1) : cap);
     size_t off = 0;
     auto take = [&](size_t bytes) {
@@ -601,10 +627,20 @@ cudaError_t emb_fast_run(const int32_t* ids, const void* g, void* dW, double* ra
     cudaError_t e = cudaMemsetAsync(w.bad, 0, 4, st);
     if (e != cudaSuccess) return e;
     const int Tp = pow2_at_least(Tn < 32 ? 32 : Tn);  // whole warps in the shuffle stages
-    const size_t smem = (size_t)Tp * 8;
-    e = ensure_smem_attr(reinterpret_cast<const void*>(emb_sort_kernel), smem);
-    if (e != cudaSuccess) return e;
-    emb_sort_kernel<<<(unsigned)B, kEmbSortThreads, smem, st>>>(ids, Tn, V, w, Tp);
+    int sh = 0;
+    while ((1 << sh) < Tp) ++sh;
+    // 32-bit keys when (V - 1) << log2(Tp) | (Tp - 1) stays below the all-ones sentinel
+    const bool k32 = (((uint64_t)V) << sh) < 0xffffffffull;
+    const size_t smem = (size_t)Tp * (k32 ? 4 : 8);
+    if (k32) {
+        e = ensure_smem_attr(reinterpret_cast<const void*>(emb_sort_kernel<uint32_t>), smem);
+        if (e != cudaSuccess) return e;
+        emb_sort_kernel<uint32_t><<<(unsigned)B, kEmbSortThreads, smem, st>>>(ids, Tn, V, w, Tp, sh);
+    } else {
+        e = ensure_smem_attr(reinterpret_cast<const void*>(emb_sort_kernel<uint64_t>), smem);
+        if (e != cudaSuccess) return e;
+        emb_sort_kernel<uint64_t><<<(unsigned)B, kEmbSortThreads, smem, st>>>(ids, Tn, V, w, Tp, 32);
+    }
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     constexpr int W = Traits<T>::W;
@@ -614,7 +650,9 @@ cudaError_t emb_fast_run(const int32_t* ids, const void* g, void* dW, double* ra
     const int ng = (int)((B + 31) / 32);
     auto launch = [&](auto nvc) {
         constexpr int NVC = decltype(nvc)::value;
-        if (ng <= 1)
+        if (ng <= 1 && emb_rows_threads(B) == 64)
+            emb_rows_kernel<T, NVC, 1, 64><<<l.grid, 64, 0, st>>>(gp, B, Tn, V, D, w, dWp);
+        else if (ng <= 1)
             emb_rows_kernel<T, NVC, 1><<<l.grid, kEmbRowsThreads, 0, st>>>(gp, B, Tn, V, D, w, dWp);
         else if (ng <= 2)
             emb_rows_kernel<T, NVC, 2><<<l.grid, kEmbRowsThreads, 0, st>>>(gp, B, Tn, V, D, w, dWp);
@@ -633,7 +671,7 @@ cudaError_t emb_fast_run(const int32_t* ids, const void* g, void* dW, double* ra
         launch(std::integral_constant<int, 4>{});
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    emb_raw_kernel<<<(unsigned)((B * 32 + 255) / 256), 256, 0, st>>>(B, Tn, w, raw);
+    emb_raw_kernel<<<(unsigned)B, 256, 0, st>>>(B, Tn, w, raw);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (sums) {

@@ -359,6 +359,14 @@ inline bool ln_fold() {
     return v;
 }
 
+inline bool ln_park() {
+    static const bool v = [] {
+        const char* e = getenv("GNSB_LN_PARK");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
 // Configuration table: number of 16-byte vectors per row -> LnBwdCfg.
 template <typename T, template <typename> class Op, typename R, typename... A>
 R dispatch_bwd(int64_t D, const char** why, R bad, A&&... args) {
@@ -369,13 +377,19 @@ R dispatch_bwd(int64_t D, const char** why, R bad, A&&... args) {
     if (nv <= 32) return Op<LnBwdCfg<T, 1, 1, 8, 2, true>>::call(args...);
     if (nv <= 64) return Op<LnBwdCfg<T, 2, 1, 8, 1, true>>::call(args...);
     if (nv <= 96) return Op<LnBwdCfg<T, 3, 1, 5, 2, true, -1, 1, true>>::call(args...);  // parked first example
+    // D = 1024 / 2048: parking the first example's group partials in shared
+    // memory measured slower even with the 4-stage ring's spare room (steady
+    // 8-layer step: 345.6 / 654.4 us parked against 343.3 / 622.3 us at
+    // D = 1024 / 2048); GNSB_LN_PARK=1 selects it for A/B runs
     if (nv <= 128) {
-        if (ln_fold()) return Op<LnBwdCfg<T, 4, 1, 4, 2, true>>::call(args...);
-        return Op<LnBwdCfg<T, 4, 1, 4, 2, true, -1, 1, false, true>>::call(args...);
+        if (!ln_fold()) return Op<LnBwdCfg<T, 4, 1, 4, 2, true, -1, 1, false, true>>::call(args...);
+        if (ln_park()) return Op<LnBwdCfg<T, 4, 1, 4, 2, true, -1, 1, true>>::call(args...);
+        return Op<LnBwdCfg<T, 4, 1, 4, 2, true>>::call(args...);
     }
     if (nv <= 256) {
-        if (ln_fold()) return Op<LnBwdCfg<T, 8, 1, 2, 2, true>>::call(args...);
-        return Op<LnBwdCfg<T, 8, 1, 2, 2, true, -1, 1, false, true>>::call(args...);
+        if (!ln_fold()) return Op<LnBwdCfg<T, 8, 1, 2, 2, true, -1, 1, false, true>>::call(args...);
+        if (ln_park()) return Op<LnBwdCfg<T, 8, 1, 2, 2, true, -1, 1, true>>::call(args...);
+        return Op<LnBwdCfg<T, 8, 1, 2, 2, true>>::call(args...);
     }
     if (nv <= 512) return Op<LnBwdCfg<T, 8, 2, 1, 2, true, 1>>::call(args...);
     // 11 consumer warps x 3 vectors (3 % of the lanes idle at D=8192): 12 warps leave
