@@ -471,6 +471,10 @@ gnsb_status gnsb_linear_pe_workspace_size(int64_t B, int64_t T, int64_t K, int64
         const size_t m = gnsb::gram_workspace(B, T);
         n = n > m ? n : m;
     }
+    if (use_tc_wgrad(dt, 1, B * T, K, L)) {  // the plain dW pass of the short-sequence dispatch
+        const size_t m = gnsb::wgrad_workspace(1, K, L);
+        n = n > m ? n : m;
+    }
     *bytes = n;
     return debug_ok("gnsb_linear_pe_workspace_size");
 }
@@ -489,8 +493,22 @@ gnsb_status gnsb_linear_pe_norms(const void* x, const void* g, void* dW, double*
     if (!ws || ws_bytes < need) return fail(GNSB_EINVAL, "layers: workspace too small (query gnsb_linear_pe_workspace_size)");
     if ((T > 0) && (!x || !g)) return fail(GNSB_EINVAL, "layers: null input pointer");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (form == 0) form = (dW != nullptr || T * (K + L) >= 2 * K * L) ? 1 : 2;
     cudaError_t e;
+    // Auto with dW on the tensor cores: for short sequences the weight-gradient
+    // form is bound by its per-(tile, example) epilogue, not the MMAs, and the
+    // Gram form for the norms plus ONE plain dW pass over all B*T tokens
+    // (the weight-gradient kernel on a single "example") is faster
+    // (experiments/form_sweep.py at K = L = 4096, B*T = 32768: T = 128 /
+    // 256: 0.89 / 0.81 ms against 1.79 / 1.18 ms; from T = 512 the
+    // weight-gradient form wins, 0.84 against 0.84 + ...).
+    if (form == 0 && dW != nullptr && T < 384 && T * (K + L) < 2 * K * L && use_tc_gram(dt, B, T, K, L) &&
+        use_tc_wgrad(dt, 1, B * T, K, L)) {
+        e = gnsb::launch_wgrad_norms(x, g, static_cast<float*>(dW), nullptr, sums, 1, B * T, K, L, ws, st);
+        // (sums[2] = ||dW||^2 from that pass; sums[0] and raw_w from the Gram form)
+        if (e == cudaSuccess) e = gnsb::launch_gram_norms(x, g, raw_w, sums, B, T, K, L, ws, st);
+        return e == cudaSuccess ? debug_ok("gnsb_linear_pe_norms") : cuda_fail(e, "linear_pe_norms launch");
+    }
+    if (form == 0) form = (dW != nullptr || T * (K + L) >= 2 * K * L) ? 1 : 2;
     if (form == 1 && use_tc_wgrad(dt, B, T, K, L))
         e = gnsb::launch_wgrad_norms(x, g, static_cast<float*>(dW), raw_w, sums, B, T, K, L, ws, st);
     else if (form == 2 && use_tc_gram(dt, B, T, K, L))

@@ -53,7 +53,8 @@ def _linear_norms(x: torch.Tensor, g: torch.Tensor, K: int, L: int, rec: torch.T
     dW = torch.empty(K, L, dtype=sd, device=dev)
     raw = torch.empty(2, B, dtype=torch.float64, device=dev)
     sp = _stream_ptr(dev)
-    _lib.check(_lib.lib().gnsb_linear_pe_norms(_ptr(x), _ptr(g), _ptr(dW), _ptr(raw[0]), _ptr(rec), B, M, K, L, 1, dt,
+    # form 0 (auto): the weight-gradient form, or Gram + one plain dW pass for short sequences
+    _lib.check(_lib.lib().gnsb_linear_pe_norms(_ptr(x), _ptr(g), _ptr(dW), _ptr(raw[0]), _ptr(rec), B, M, K, L, 0, dt,
                                                _ptr(ws), ws.numel(), sp))
     db = None
     if has_bias:

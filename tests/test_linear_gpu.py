@@ -101,6 +101,26 @@ def test_tcgen05_weight_grad_form_matches_oracle(orc, cuda, monkeypatch, impl, B
     assert close(float(r.grads.sums4[2]), float(np.sum(ref["dW"] ** 2)), 1e-4)
 
 
+@pytest.mark.parametrize("B,T,K,L", [(8, 128, 256, 256), (4, 100, 264, 136)])
+def test_auto_form_short_sequences_gram_plus_plain_dw(orc, cuda, B, T, K, L):
+    """form "auto" with dW at short T takes the Gram form for the norms and one
+    plain dW pass over all B*T tokens (experiments/form_sweep.py): same dW,
+    norms and record as the oracle."""
+    import paper_2411_00999_b200 as m
+    from paper_2411_00999_b200 import linear
+
+    x, g = m.synth_linear(B, T, K, L, torch.bfloat16, cuda)
+    r = linear.linear_backward_simultaneous(linear.LinearLayer(torch.zeros(K, L, device=cuda)), x, g, form="auto",
+                                            need_input_grad=False)
+    ref = _oracle_linear(orc, x, g)
+    torch.cuda.synchronize()
+    dW = r.grads.weight_grads["weight"].double().cpu().numpy()
+    assert close(dW, ref["dW"], 1e-4, 1e-4 * np.max(np.abs(ref["dW"])))
+    assert close(r.grads.per_example_sqnorms_raw["weight"].cpu().numpy(), ref["raw_w"], 1e-4)
+    assert close(float(r.grads.sums4[0]), float(np.sum(ref["raw_w"])), 1e-4)
+    assert close(float(r.grads.sums4[2]), float(np.sum(ref["dW"] ** 2)), 1e-4)
+
+
 def test_weight_grad_form_equals_gram_form(cuda):
     """<X X^T, G G^T>_F equals ||sum_t x_t^T g_t||^2 (test_layers.cpp:135-149)."""
     import paper_2411_00999_b200 as m
