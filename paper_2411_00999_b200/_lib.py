@@ -13,6 +13,10 @@ import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libgnsb.so")
+# A/B experiments only: GNSB_LIB_VARIANT=<tag> loads lib/libgnsb_<tag>.so (a
+# build of the same sources with different compile-time knobs)
+if os.environ.get("GNSB_LIB_VARIANT"):
+    LIB_PATH = os.path.join(_HERE, "lib", "libgnsb_%s.so" % os.environ["GNSB_LIB_VARIANT"])
 
 GNSB_OK, GNSB_EINVAL, GNSB_ECUDA, GNSB_ENCCL, GNSB_ENOMEM = 0, 1, 2, 3, 4
 GNSB_F32, GNSB_BF16, GNSB_F64 = 0, 1, 2

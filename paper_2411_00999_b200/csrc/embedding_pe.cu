@@ -220,7 +220,11 @@ __global__ void __launch_bounds__(kEmbThreads) emb_table_kernel(int64_t B, int64
 // dW matches the original path bit for bit (same per-example Acc sums, added
 // in example order); raw_b differs in summation order only.
 constexpr int kEmbSortThreads = 1024;
-constexpr int kRowsPerWarp = 8;
+constexpr int kEmbBuckets = 4096;  // id buckets of the sort kernel's bucket sort
+#ifndef GNSB_EMB_RPW
+#define GNSB_EMB_RPW 8
+#endif
+constexpr int kRowsPerWarp = GNSB_EMB_RPW;  // table rows per warp (A/B: -DGNSB_EMB_RPW=4 / 2)
 constexpr int kEmbRowsThreads = 256;
 constexpr int kEmbMaxGroups = 8;  // examples handled by the fast path: B <= 32 * 8
 
@@ -265,7 +269,7 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* s_warp, int* tot
 // used when every id fits: half the shared-memory and shuffle traffic).
 template <typename KT>
 __global__ void __launch_bounds__(kEmbSortThreads) emb_sort_kernel(const int32_t* ids, int64_t Tn, int64_t V,
-                                                                   EmbFastWs w, int Tp, int SH) {
+                                                                   EmbFastWs w, int Tp, int SH, int BSH, int NB) {
     extern __shared__ __align__(16) unsigned char smem[];
     KT* keys = reinterpret_cast<KT*>(smem);  // [Tp]
     const KT TM = (KT(1) << SH) - 1;         // token mask
@@ -275,50 +279,132 @@ __global__ void __launch_bounds__(kEmbSortThreads) emb_sort_kernel(const int32_t
     const int64_t b = blockIdx.x;
     const int tid = threadIdx.x;
     const int32_t* idb = ids + b * Tn;
-    if (tid == 0) s_nvalid = 0;
-    for (int i = tid; i < Tp; i += blockDim.x) {
-        KT k = NONE;
-        if (i < Tn) {
-            const int32_t id = idb[i];
-            if (id < 0 || id >= V)
-                atomicExch(w.bad, 1);
-            else
-                k = ((KT)(uint32_t)id << SH) | (KT)(uint32_t)i;
-        }
-        keys[i] = k;
+    __shared__ int s_maxb;
+    if (tid == 0) {
+        s_nvalid = 0;
+        s_maxb = 0;
     }
-    __syncthreads();
-    // bitonic sort, ascending (id, t): strides >= 32 through shared memory,
-    // strides < 32 inside the warp with shuffles (Tp is a multiple of 32)
-    for (int size = 2; size <= Tp; size <<= 1) {
-        int stride = size >> 1;
-        for (; stride >= 32; stride >>= 1) {
-            for (int i = tid; i < Tp; i += blockDim.x) {
-                const int j = i ^ stride;
-                if (j > i) {
-                    const KT a = keys[i], c = keys[j];
-                    const bool up = (i & size) == 0;
-                    if ((a > c) == up) {
-                        keys[i] = c;
-                        keys[j] = a;
+    bool bitonic = NB == 0;
+    if (NB > 0) {
+        // Bucket sort by id >> BSH (NB <= kEmbBuckets buckets): histogram,
+        // block scan, scatter, then an insertion sort inside each bucket by the
+        // full (id, t) key (about T / NB keys per bucket).  Five barriers in
+        // all, against ~15 shared-memory rounds of the bitonic network.
+        KT* tmp = keys + Tp;                                         // [Tp] scattered keys
+        int* cnt = reinterpret_cast<int*>(tmp + Tp);                 // [NB + 1] counts -> bucket starts
+        int* cur = cnt + NB + 1;                                     // [NB] scatter cursors
+        for (int i = tid; i <= NB; i += blockDim.x) cnt[i] = 0;
+        __syncthreads();
+        for (int i = tid; i < Tp; i += blockDim.x) {
+            KT k = NONE;
+            if (i < Tn) {
+                const int32_t id = idb[i];
+                if (id < 0 || id >= V)
+                    atomicExch(w.bad, 1);
+                else {
+                    k = ((KT)(uint32_t)id << SH) | (KT)(uint32_t)i;
+                    atomicAdd(&cnt[id >> BSH], 1);
+                }
+            }
+            tmp[i] = k;
+        }
+        __syncthreads();
+        // a heavy bucket (one id repeated, e.g. padding) would make the
+        // per-bucket insertion sort quadratic: take the bitonic network then
+        for (int c = tid; c < NB; c += blockDim.x)
+            if (cnt[c] > 64) atomicMax(&s_maxb, cnt[c]);
+        __syncthreads();
+        bitonic = s_maxb > 64;
+    }
+    if (!bitonic) {
+        KT* tmp = keys + Tp;
+        int* cnt = reinterpret_cast<int*>(tmp + Tp);
+        int* cur = cnt + NB + 1;
+        // exclusive scan of the counts: a contiguous chunk per thread
+        const int per = (NB + kEmbSortThreads - 1) / kEmbSortThreads;
+        const int c0 = tid * per, c1 = min(c0 + per, NB);
+        int local = 0;
+        for (int c = c0; c < c1; ++c) local += cnt[c];
+        int total = 0;
+        int run = block_exclusive_scan<kEmbSortThreads>(local, s_warp, &total);
+        for (int c = c0; c < c1; ++c) {
+            const int n = cnt[c];
+            cnt[c] = run;
+            cur[c] = run;
+            run += n;
+        }
+        if (tid == 0) cnt[NB] = total;
+        __syncthreads();
+        // scatter (order inside a bucket is fixed by the insertion sort below);
+        // invalid / pad keys fill the tail
+        for (int i = tid; i < Tp; i += blockDim.x) {
+            const KT k = tmp[i];
+            if (k != NONE) keys[atomicAdd(&cur[(int)((uint32_t)(k >> SH) >> BSH)], 1)] = k;
+        }
+        for (int i = total + tid; i < Tp; i += blockDim.x) keys[i] = NONE;
+        __syncthreads();
+        for (int c = tid; c < NB; c += blockDim.x) {
+            const int lo = cnt[c], hi = cnt[c + 1];
+            for (int i = lo + 1; i < hi; ++i) {
+                const KT v = keys[i];
+                int j = i - 1;
+                while (j >= lo && keys[j] > v) {
+                    keys[j + 1] = keys[j];
+                    --j;
+                }
+                keys[j + 1] = v;
+            }
+        }
+        __syncthreads();
+    } else {
+        if (NB > 0) {  // the keys are in tmp, in token order: sort them in place in keys
+            const KT* tmp = keys + Tp;
+            for (int i = tid; i < Tp; i += blockDim.x) keys[i] = tmp[i];
+        } else
+        for (int i = tid; i < Tp; i += blockDim.x) {
+            KT k = NONE;
+            if (i < Tn) {
+                const int32_t id = idb[i];
+                if (id < 0 || id >= V)
+                    atomicExch(w.bad, 1);
+                else
+                    k = ((KT)(uint32_t)id << SH) | (KT)(uint32_t)i;
+            }
+            keys[i] = k;
+        }
+        __syncthreads();
+        // bitonic sort, ascending (id, t): strides >= 32 through shared memory,
+        // strides < 32 inside the warp with shuffles (Tp is a multiple of 32)
+        for (int size = 2; size <= Tp; size <<= 1) {
+            int stride = size >> 1;
+            for (; stride >= 32; stride >>= 1) {
+                for (int i = tid; i < Tp; i += blockDim.x) {
+                    const int j = i ^ stride;
+                    if (j > i) {
+                        const KT a = keys[i], c = keys[j];
+                        const bool up = (i & size) == 0;
+                        if ((a > c) == up) {
+                            keys[i] = c;
+                            keys[j] = a;
+                        }
                     }
                 }
+                __syncthreads();
+            }
+            for (int i0 = 0; i0 < Tp; i0 += blockDim.x) {
+                if (i0 + (tid & ~31) >= Tp) break;  // warp-uniform
+                const int i = i0 + tid;
+                KT v = keys[i];
+                const bool up = (i & size) == 0;
+                for (int s2 = stride; s2 > 0; s2 >>= 1) {
+                    const KT o = __shfl_xor_sync(0xffffffffu, v, s2);
+                    const bool keep_min = ((i & s2) == 0) == up;  // the lower element keeps the min when ascending
+                    v = keep_min ? (o < v ? o : v) : (o > v ? o : v);
+                }
+                keys[i] = v;
             }
             __syncthreads();
         }
-        for (int i0 = 0; i0 < Tp; i0 += blockDim.x) {
-            if (i0 + (tid & ~31) >= Tp) break;  // warp-uniform
-            const int i = i0 + tid;
-            KT v = keys[i];
-            const bool up = (i & size) == 0;
-            for (int s2 = stride; s2 > 0; s2 >>= 1) {
-                const KT o = __shfl_xor_sync(0xffffffffu, v, s2);
-                const bool keep_min = ((i & s2) == 0) == up;  // the lower element keeps the min when ascending
-                v = keep_min ? (o < v ? o : v) : (o > v ? o : v);
-            }
-            keys[i] = v;
-        }
-        __syncthreads();
     }
     // run heads: a valid key whose id differs from its predecessor's.  Each
     // thread scans a contiguous chunk; a block scan numbers the runs.
@@ -631,15 +717,25 @@ cudaError_t emb_fast_run(const int32_t* ids, const void* g, void* dW, double* ra
     while ((1 << sh) < Tp) ++sh;
     // 32-bit keys when (V - 1) << log2(Tp) | (Tp - 1) stays below the all-ones sentinel
     const bool k32 = (((uint64_t)V) << sh) < 0xffffffffull;
-    const size_t smem = (size_t)Tp * (k32 ? 4 : 8);
+    // buckets of 2^bsh ids, at most kEmbBuckets of them (the bitonic network
+    // when that table plus two key arrays would not fit in shared memory)
+    int bsh = 0;
+    while (((V - 1) >> bsh) >= kEmbBuckets) ++bsh;
+    const int nb = (int)(((V - 1) >> bsh) + 1);
+    const size_t kb = k32 ? 4 : 8;
+    const size_t smem_bucket = 2 * (size_t)Tp * kb + (2 * (size_t)nb + 1) * 4;
+    const bool bucket = smem_bucket <= (size_t)200 * 1024 && std::getenv("GNSB_EMB_SORT") == nullptr;
+    const size_t smem = bucket ? smem_bucket : (size_t)Tp * kb;
     if (k32) {
         e = ensure_smem_attr(reinterpret_cast<const void*>(emb_sort_kernel<uint32_t>), smem);
         if (e != cudaSuccess) return e;
-        emb_sort_kernel<uint32_t><<<(unsigned)B, kEmbSortThreads, smem, st>>>(ids, Tn, V, w, Tp, sh);
+        emb_sort_kernel<uint32_t><<<(unsigned)B, kEmbSortThreads, smem, st>>>(ids, Tn, V, w, Tp, sh, bsh,
+                                                                            bucket ? nb : 0);
     } else {
         e = ensure_smem_attr(reinterpret_cast<const void*>(emb_sort_kernel<uint64_t>), smem);
         if (e != cudaSuccess) return e;
-        emb_sort_kernel<uint64_t><<<(unsigned)B, kEmbSortThreads, smem, st>>>(ids, Tn, V, w, Tp, 32);
+        emb_sort_kernel<uint64_t><<<(unsigned)B, kEmbSortThreads, smem, st>>>(ids, Tn, V, w, Tp, 32, bsh,
+                                                                            bucket ? nb : 0);
     }
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;

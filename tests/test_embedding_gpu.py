@@ -30,14 +30,24 @@ def test_fp64_matches_reference_golden_bitwise(golden, cuda):
         assert close(float(r.per_example_sqnorms["weight"]), c["corrected"][0], 1e-12)
 
 
-@pytest.mark.parametrize("dt,B,T,V,D", [(torch.float32, 8, 512, 1000, 256), (torch.bfloat16, 4, 2048, 50257, 128),
-                                        (torch.float32, 3, 7, 5, 33), (torch.bfloat16, 2, 1, 3, 8)])
-def test_matches_oracle(orc, cuda, dt, B, T, V, D):
+@pytest.mark.parametrize("dt,B,T,V,D,mode", [(torch.float32, 8, 512, 1000, 256, "skew"),
+                                             (torch.bfloat16, 4, 2048, 50257, 128, "skew"),
+                                             (torch.float32, 3, 7, 5, 33, "skew"), (torch.bfloat16, 2, 1, 3, 8, "skew"),
+                                             # the sort kernel's bucket sort (uniform ids) and its bitonic
+                                             # fallback (one id fills a bucket: padding)
+                                             (torch.bfloat16, 4, 4096, 50257, 64, "uniform"),
+                                             (torch.bfloat16, 3, 1024, 50257, 64, "pad")])
+def test_matches_oracle(orc, cuda, dt, B, T, V, D, mode):
     from paper_2411_00999_b200.embedding import embedding_backward_simultaneous
 
     gen = torch.Generator(device="cpu").manual_seed(B * 1000 + T)
-    # skewed ids: frequent tokens repeat within an example (long runs) as in text
-    ids = (torch.rand(B, T, generator=gen) ** 3 * V).to(torch.int32).clamp_(0, V - 1)
+    if mode == "skew":  # frequent tokens repeat within an example (long runs) as in text
+        ids = (torch.rand(B, T, generator=gen) ** 3 * V).to(torch.int32).clamp_(0, V - 1)
+    elif mode == "uniform":
+        ids = torch.randint(0, V, (B, T), generator=gen, dtype=torch.int32)
+    else:  # 90 % padding id, the rest uniform
+        ids = torch.randint(0, V, (B, T), generator=gen, dtype=torch.int32)
+        ids[torch.rand(B, T, generator=gen) < 0.9] = 7
     g = torch.randn(B, T, D, generator=gen).to(dt)
     r = embedding_backward_simultaneous(ids.to(cuda), g.to(cuda), V)
     ref = orc.embedding_backward(ids.numpy(), g.double().numpy(), V)
