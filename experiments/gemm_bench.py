@@ -15,19 +15,25 @@ dev = torch.device("cuda")
 PEAK = 1647.2
 shapes = [(32768, 4096, 4096), (32768, 4096, 16384), (32768, 16384, 4096), (8192, 1024, 4096), (32768, 768, 50264),
           (30000, 4000, 4000)]
+DT = torch.bfloat16
+if "--fp32" in sys.argv:  # fp32 rows and weights: the 3xTF32 kernel
+    DT = torch.float32
+    sys.argv.remove("--fp32")
+    shapes = [(32768, 4096, 4096), (8192, 1024, 4096), (30000, 4000, 4000)]
 if len(sys.argv) > 1:
     shapes = [tuple(int(v) for v in sys.argv[1:4])]
+GD = 0 if DT == torch.float32 else 1
 for rows, K, L in shapes:
-    a_fwd = torch.randn(rows, K, device=dev).bfloat16()
-    a_dx = torch.randn(rows, L, device=dev).bfloat16()
-    W = (torch.randn(K, L, device=dev) / K ** 0.5).bfloat16()
-    y = torch.empty(rows, L, device=dev, dtype=torch.bfloat16)
-    dx = torch.empty(rows, K, device=dev, dtype=torch.bfloat16)
+    a_fwd = torch.randn(rows, K, device=dev).to(DT)
+    a_dx = torch.randn(rows, L, device=dev).to(DT)
+    W = (torch.randn(K, L, device=dev) / K ** 0.5).to(DT)
+    y = torch.empty(rows, L, device=dev, dtype=DT)
+    dx = torch.empty(rows, K, device=dev, dtype=DT)
     sp = torch.cuda.current_stream().cuda_stream
-    for name, fn in (("dx ", lambda: lib.gnsb_linear_dx(a_dx.data_ptr(), W.data_ptr(), dx.data_ptr(), rows, K, L, 1, 1,
+    for name, fn in (("dx ", lambda: lib.gnsb_linear_dx(a_dx.data_ptr(), W.data_ptr(), dx.data_ptr(), rows, K, L, GD, GD,
                                                          None, 0, sp)),
                      ("fwd", lambda: lib.gnsb_linear_fwd(a_fwd.data_ptr(), W.data_ptr(), None, y.data_ptr(), rows, K,
-                                                         L, 1, 1, None, 0, sp))):
+                                                         L, GD, GD, None, 0, sp))):
         for _ in range(3):
             assert fn() == 0, lib.gnsb_last_error()
         torch.cuda.synchronize()

@@ -166,9 +166,12 @@ gnsb_status gnsb_linear_bias_pe(const void* g, void* dbias, double* raw_b, doubl
  * rows), nullable.
  * bf16 rows with K % 8 == 0, L % 8 == 0 and 16-byte aligned buffers run the
  * tcgen05 tensor-core kernel (bf16 operands, fp32 accumulation, any row count;
- * tile tails are zero-filled by TMA).  Other shapes and fp32 rows run a
- * generic fp64-accumulating kernel; fp64 rows reproduce the reference's
- * operation order bit for bit.
+ * tile tails are zero-filled by TMA).  fp32 rows with fp32 weights (K, L
+ * multiples of 4) run the 3xTF32 tensor-core kernel: both operands split into
+ * tf32 hi + lo parts once per call, each product formed as lo*hi + hi*lo +
+ * hi*hi with fp32 accumulation (fp32-level accuracy; the split copies come
+ * from the stream-ordered pool).  Other shapes run a generic fp64-accumulating
+ * kernel; fp64 rows reproduce the reference's operation order bit for bit.
  * Workspace: gnsb_linear_gemm_workspace_size bytes (0 unless W must be converted).
  */
 gnsb_status gnsb_linear_gemm_workspace_size(int64_t K, int64_t L, gnsb_dtype dt, gnsb_dtype w_dt, size_t* bytes);

@@ -294,6 +294,276 @@ __global__ void __launch_bounds__(gm::THREADS, 1)
     }
 }
 
+
+// ---------------------------------------------------------- fp32 rows: 3xTF32 --
+// fp32 operands on the tensor cores at fp32 accuracy: every operand is split
+// once into tf32 hi + lo parts (split_tf32_kernel: hi = rna(a), lo = rna(a - hi)),
+// and each product is formed as lo*hi + hi*lo + hi*hi (kind::tf32, fp32
+// accumulation in TMEM), dropping only lo*lo (~2^-22 relative).  Same
+// structure as gemm_kernel with BM = BN = 128, 32-element (128-byte) K blocks,
+// hi and lo tiles of A and B per stage, fp32 output boxes.  kind::tf32 takes
+// K-major operands only: the forward's W is split into transposed copies.
+namespace g3 {
+constexpr int BM = 128, BN = 128, BK = 32;     // BK fp32 = one 128-byte swizzle row
+constexpr int STAGES = 3;
+constexpr int TILE = BM * BK * 4;              // 16 KB (A or B, hi or lo)
+constexpr int STAGE_BYTES = 4 * TILE;          // A hi, A lo, B hi, B lo
+constexpr int EPI_WARPS = 8;
+constexpr int THREADS = (2 + EPI_WARPS) * 32;
+constexpr int OUT_BOX_BYTES = 32 * 128;        // 32 rows x 32 fp32
+constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 1024 + (size_t)EPI_WARPS * OUT_BOX_BYTES;
+static_assert(SMEM <= 232448, "dynamic shared memory of one CTA");
+constexpr int TMEM_COLS = 256;
+}  // namespace g3
+
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, bool a_mn_major, bool b_mn_major) {
+    return (1u << 4)                          // c_format = F32
+           | (2u << 7)                        // a_format = TF32
+           | (2u << 10)                       // b_format = TF32
+           | ((a_mn_major ? 1u : 0u) << 15) | ((b_mn_major ? 1u : 0u) << 16) | ((uint32_t)(N >> 3) << 17) |
+           ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__global__ void __launch_bounds__(256) split_tf32_kernel(const float* __restrict__ in, float* __restrict__ hi,
+                                                         float* __restrict__ lo, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float a = in[i];
+        uint32_t h, l;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(a));
+        const float r = a - __uint_as_float(h);  // exact
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(r));
+        hi[i] = __uint_as_float(h);
+        lo[i] = __uint_as_float(l);
+    }
+}
+
+// W [K, L] -> hi^T, lo^T [L, K] (the forward's B operand, K-major: kind::tf32
+// takes K-major operands only), 32 x 32 tiles through shared memory
+__global__ void __launch_bounds__(256) split_tf32_t_kernel(const float* __restrict__ in, float* __restrict__ hi_t,
+                                                           float* __restrict__ lo_t, int64_t K, int64_t L) {
+    __shared__ float th[32][33], tl[32][33];
+    const int64_t k0 = (int64_t)blockIdx.y * 32, l0 = (int64_t)blockIdx.x * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    for (int r = ty; r < 32; r += 8) {
+        const int64_t k = k0 + r, l = l0 + tx;
+        float h = 0.f, lo = 0.f;
+        if (k < K && l < L) {
+            const float a = in[k * L + l];
+            uint32_t hb, lb;
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(a));
+            const float rr = a - __uint_as_float(hb);
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lb) : "f"(rr));
+            h = __uint_as_float(hb);
+            lo = __uint_as_float(lb);
+        }
+        th[r][tx] = h;
+        tl[r][tx] = lo;
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+        const int64_t l = l0 + r, k = k0 + tx;
+        if (k < K && l < L) {
+            hi_t[l * K + k] = th[tx][r];
+            lo_t[l * K + k] = tl[tx][r];
+        }
+    }
+}
+
+template <bool B_KMAJOR, bool BIAS, int EPI>
+__global__ void __launch_bounds__(g3::THREADS, 1)
+    gemm3_kernel(const __grid_constant__ CUtensorMap tah, const __grid_constant__ CUtensorMap tal,
+                 const __grid_constant__ CUtensorMap tbh, const __grid_constant__ CUtensorMap tbl,
+                 const __grid_constant__ CUtensorMap tmo, GemmArgs a, const float* aux32, const float* bias32) {
+    using namespace g3;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem =
+        reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char* ring = smem;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)STAGES * STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;  // [2]
+    uint64_t* tempty = tfull + 2;      // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    unsigned char* obox = smem + (size_t)STAGES * STAGE_BYTES + 1024;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ntiles = a.tiles_m * a.tiles_n;
+    const int kblocks = (a.Kr + BK - 1) / BK;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&tfull[s], 1);
+            mbar_init(&tempty[s], EPI_WARPS);
+        }
+        fence_mbar_init();
+        tc::prefetch_tmap(&tah);
+        tc::prefetch_tmap(&tal);
+        tc::prefetch_tmap(&tbh);
+        tc::prefetch_tmap(&tbl);
+        tc::prefetch_tmap(&tmo);
+    }
+    if (warp == 1) tc::tmem_alloc<TMEM_COLS>(tmem_slot);
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tmem = *tmem_slot;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                int mt, nt;
+                tile_mn(t, a.tiles_m, a.tiles_n, mt, nt);
+                const int m0 = mt * BM, n0 = nt * BN;
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    mbar_wait(&empty[s], ph ^ 1u);
+                    unsigned char* st = ring + (size_t)s * STAGE_BYTES;
+                    mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+                    const int k0 = kb * BK;
+                    tc::tma_load_3d(st, &tah, k0, m0, 0, &full[s]);
+                    tc::tma_load_3d(st + TILE, &tal, k0, m0, 0, &full[s]);
+                    if constexpr (B_KMAJOR) {
+                        tc::tma_load_3d(st + 2 * TILE, &tbh, k0, n0, 0, &full[s]);
+                        tc::tma_load_3d(st + 3 * TILE, &tbl, k0, n0, 0, &full[s]);
+                    } else {
+#pragma unroll
+                        for (int h = 0; h < BN / 32; ++h) {  // 32 (N) x 32 (K) chunks along N
+                            tc::tma_load_3d(st + 2 * TILE + h * 4096, &tbh, n0 + 32 * h, k0, 0, &full[s]);
+                            tc::tma_load_3d(st + 3 * TILE + h * 4096, &tbl, n0 + 32 * h, k0, 0, &full[s]);
+                        }
+                    }
+                    if (++s == STAGES) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_tf32(BM, BN, false, !B_KMAJOR);
+            int s = 0, buf = 0;
+            uint32_t ph = 0, tph = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                mbar_wait(&tempty[buf], tph ^ 1u);
+                tc::fence_after_sync();
+                const uint32_t dcol = tmem + (uint32_t)(buf * BN);
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    mbar_wait(&full[s], ph);
+                    tc::fence_after_sync();
+                    const uint32_t ah = smem_u32(ring + (size_t)s * STAGE_BYTES), al = ah + TILE;
+                    const uint32_t bh = ah + 2 * TILE, bl = ah + 3 * TILE;
+#pragma unroll
+                    for (int k = 0; k < BK / 8; ++k) {
+                        // K-major SW128: a K step of 8 tf32 = 32 bytes; MN-major SW128:
+                        // 32-element x 8-row atoms, LBO = next 32 columns (4 KB), SBO = 8 K rows (1 KB)
+                        const uint64_t dah = tc::smem_desc_sw128(ah + k * 32, 16, 1024);
+                        const uint64_t dal = tc::smem_desc_sw128(al + k * 32, 16, 1024);
+                        const uint64_t dbh = B_KMAJOR ? tc::smem_desc_sw128(bh + k * 32, 16, 1024)
+                                                      : tc::smem_desc_sw128(bh + k * 1024, 4096, 1024);
+                        const uint64_t dbl = B_KMAJOR ? tc::smem_desc_sw128(bl + k * 32, 16, 1024)
+                                                      : tc::smem_desc_sw128(bl + k * 1024, 4096, 1024);
+                        mma_tf32(dcol, dal, dbh, idesc, (kb | k) != 0);  // small terms first
+                        mma_tf32(dcol, dah, dbl, idesc, 1);
+                        mma_tf32(dcol, dah, dbh, idesc, 1);
+                    }
+                    tc::commit(&empty[s]);
+                    if (++s == STAGES) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+                tc::commit(&tfull[buf]);
+                if (++buf == 2) {
+                    buf = 0;
+                    tph ^= 1u;
+                }
+            }
+        }
+    } else {
+        // epilogue: warp (quad, half) owns 32 rows x 64 columns; two 32-column
+        // boxes per tile, staged in shared memory (128B swizzle) and TMA-stored
+        const int e = warp - 2;
+        const int quad = warp & 3;
+        const int half = e / 4;
+        unsigned char* box = obox + (size_t)e * OUT_BOX_BYTES;
+        int buf = 0;
+        uint32_t tph = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            int mt, nt;
+            tile_mn(t, a.tiles_m, a.tiles_n, mt, nt);
+            const int m0 = mt * BM, n0 = nt * BN;
+            const int row = m0 + quad * 32 + lane;
+            mbar_wait(&tfull[buf], tph);
+            tc::fence_after_sync();
+            const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN + half * 64);
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc) {
+                if (lane == 0) bulk_wait_read0();
+                __syncwarp();
+                uint32_t r[32];
+                tc::tmem_ld_32x32b_x32(base + cc * 32, r);
+                tc::tmem_ld_wait();
+                if (cc == 1) {
+                    tc::fence_before_sync();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[buf]);
+                }
+                const int c0 = n0 + half * 64 + cc * 32;
+#pragma unroll
+                for (int v = 0; v < 8; ++v) {  // 16-byte chunks of the 128-byte box row
+                    float f[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        f[j] = __uint_as_float(r[4 * v + j]);
+                        const int col = c0 + 4 * v + j;
+                        if constexpr (BIAS) f[j] += col < a.N ? __ldg(bias32 + col) : 0.f;
+                        if constexpr (EPI != EPI_NONE) {
+                            const float x = (EPI == EPI_RESID || EPI == EPI_DTANH) && row < a.M && col < a.N
+                                                ? __ldg(aux32 + (size_t)row * a.N + col)
+                                                : 0.f;
+                            f[j] = epi_apply<EPI>(f[j], x);
+                        }
+                    }
+                    *reinterpret_cast<float4*>(box + lane * 128 + ((v ^ (lane & 7)) << 4)) =
+                        make_float4(f[0], f[1], f[2], f[3]);
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_3d(&tmo, box, c0, m0 + quad * 32, 0);
+                    bulk_commit();
+                }
+            }
+            if (++buf == 2) {
+                buf = 0;
+                tph ^= 1u;
+            }
+        }
+        if (lane == 0) bulk_wait0();
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 1) {
+        tc::fence_after_sync();
+        tc::tmem_dealloc<TMEM_COLS>(tmem);
+    }
+}
+
 // fp32 master weights -> bf16 operand copy (RNE)
 __global__ void __launch_bounds__(256) f32_to_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
                                                           int64_t n) {
@@ -388,15 +658,84 @@ cudaError_t launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtens
     return cudaLaunchKernelEx(&cfg, gemm_kernel<BK_, BIAS, EPI>, ma, mb, mo, a);
 }
 
+
+// [rows, cols] fp32 row-major as a 3-D map, box {bc, br}, 128-byte swizzle
+bool make_map_2d_f32(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int bc, int br) {
+    EncodeFn enc = encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, 1};
+    cuuint64_t strides[2] = {(cuuint64_t)cols * 4, (cuuint64_t)rows * cols * 4};
+    cuuint32_t box[3] = {(cuuint32_t)bc, (cuuint32_t)br, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <bool BK_, bool BIAS, int EPI>
+cudaError_t launch_tc3(const CUtensorMap* maps, const GemmArgs& a, const float* aux, const float* bias,
+                       cudaStream_t st) {
+    const void* fn = reinterpret_cast<const void*>(gemm3_kernel<BK_, BIAS, EPI>);
+    cudaError_t e = ensure_smem_attr(fn, g3::SMEM);
+    if (e != cudaSuccess) return e;
+    const int ntiles = a.tiles_m * a.tiles_n;
+    const int sms = device_sm_count();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ntiles < sms ? ntiles : sms);
+    cfg.blockDim = dim3(g3::THREADS);
+    cfg.dynamicSmemBytes = g3::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, gemm3_kernel<BK_, BIAS, EPI>, maps[0], maps[1], maps[2], maps[3], maps[4], a, aux,
+                              bias);
+}
 }  // namespace
 
 bool gemm_tc_ok(int dt, int64_t K, int64_t L) {
     return dt == 1 && K % 8 == 0 && L % 8 == 0 && K < (1ll << 31) && L < (1ll << 31);
 }
+// fp32 rows and fp32 weights on the 3xTF32 kernel: 16-byte row strides
+static bool gemm3_ok(int dt, int w_dt, int64_t rows, int64_t K, int64_t L) {
+    return dt == 0 && w_dt == 0 && K % 4 == 0 && L % 4 == 0 && K < (1ll << 31) && L < (1ll << 31) &&
+           rows < (1ll << 31);
+}
 static bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 size_t gemm_workspace(int dt, int w_dt, int64_t K, int64_t L) {
     return (dt == 1 && w_dt == 0 && gemm_tc_ok(dt, K, L)) ? (size_t)K * L * 2 : 0;
+}
+// the 3xTF32 path splits both operands into hi / lo copies: a scratch of
+// 2 * (rows * Kr + K * L) fp32 (gnsb_linear_gemm_workspace_size has no row
+// count) from a library-owned stream-ordered pool that keeps its memory
+// (the default pool would hand gigabytes back to the driver at every
+// synchronisation and re-map them on the next call)
+static size_t gemm3_scratch(int64_t rows, int64_t Kr, int64_t K, int64_t L) {
+    return (size_t)2 * (rows * Kr + K * L) * sizeof(float) + 512;
+}
+static cudaError_t scratch_pool(cudaMemPool_t* out) {
+    static std::mutex mu;
+    static cudaMemPool_t pools[64] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess || dev < 0 || dev >= 64) return e != cudaSuccess ? e : cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!pools[dev]) {
+        cudaMemPoolProps pp = {};
+        pp.allocType = cudaMemAllocationTypePinned;
+        pp.location.type = cudaMemLocationTypeDevice;
+        pp.location.id = dev;
+        e = cudaMemPoolCreate(&pools[dev], &pp);
+        if (e != cudaSuccess) return e;
+        uint64_t keep = ~0ull;
+        e = cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+        if (e != cudaSuccess) return e;
+    }
+    *out = pools[dev];
+    return cudaSuccess;
 }
 
 // kind 0: forward y = x W + bias; kind 1: dx = g W^T.  dt / w_dt: 0 f32, 1 bf16, 2 f64.
@@ -446,6 +785,59 @@ cudaError_t launch_linear_gemm(int kind, int epi, int dt, int w_dt, const void* 
             default:
                 return bias ? launch_tc<false, true, EPI_NONE>(ma, mb, mo, a, st) : launch_tc<false, false, EPI_NONE>(ma, mb, mo, a, st);
         }
+    }
+    if (gemm3_ok(dt, w_dt, rows, K, L) && al16(in) && al16(out) && al16(W) && (aux == nullptr || al16(aux))) {
+        // fp32: split A and W into tf32 hi / lo copies, then 3xTF32 on the tensor cores
+        void* scratch = nullptr;
+        cudaMemPool_t pool;
+        cudaError_t e = scratch_pool(&pool);
+        if (e == cudaSuccess) e = cudaMallocFromPoolAsync(&scratch, gemm3_scratch(rows, Kr, K, L), pool, st);
+        if (e != cudaSuccess) return e;
+        float* ah = static_cast<float*>(scratch);
+        float* alo = ah + rows * Kr;
+        float* wh = alo + rows * Kr;
+        float* wl = wh + K * L;
+        const int sg = device_sm_count() * 8;
+        split_tf32_kernel<<<sg, 256, 0, st>>>(static_cast<const float*>(in), ah, alo, rows * Kr);
+        // B in K-major form [N, Kr]: W itself for dx (W[k, :] runs along the
+        // reduced L), W transposed for the forward
+        if (kind == 0)
+            split_tf32_t_kernel<<<dim3((unsigned)((L + 31) / 32), (unsigned)((K + 31) / 32)), 256, 0, st>>>(
+                static_cast<const float*>(W), wh, wl, K, L);
+        else
+            split_tf32_kernel<<<sg, 256, 0, st>>>(static_cast<const float*>(W), wh, wl, K * L);
+        e = cudaGetLastError();
+        CUtensorMap maps[5];
+        bool ok = e == cudaSuccess && make_map_2d_f32(&maps[0], ah, rows, Kr, g3::BK, g3::BM) &&
+                  make_map_2d_f32(&maps[1], alo, rows, Kr, g3::BK, g3::BM) &&
+                  make_map_2d_f32(&maps[2], wh, N, Kr, g3::BK, g3::BN) &&  // [N, Kr]: 32 (Kr) x 128 (N)
+                  make_map_2d_f32(&maps[3], wl, N, Kr, g3::BK, g3::BN) &&
+                  make_map_2d_f32(&maps[4], out, rows, N, 32, 32);
+        if (e == cudaSuccess && !ok) e = cudaErrorInvalidValue;
+        if (e == cudaSuccess) {
+            GemmArgs a{};
+            a.M = (int)rows;
+            a.N = (int)N;
+            a.Kr = (int)Kr;
+            a.tiles_m = (int)((rows + g3::BM - 1) / g3::BM);
+            a.tiles_n = (int)((N + g3::BN - 1) / g3::BN);
+            const float* ax = static_cast<const float*>(aux);
+            const float* bs = static_cast<const float*>(bias);
+            if (kind == 1)
+                e = epi == EPI_DTANH ? launch_tc3<true, false, EPI_DTANH>(maps, a, ax, bs, st)
+                                     : launch_tc3<true, false, EPI_NONE>(maps, a, ax, bs, st);
+            else if (epi == EPI_TANH)
+                e = bias ? launch_tc3<true, true, EPI_TANH>(maps, a, ax, bs, st)
+                         : launch_tc3<true, false, EPI_TANH>(maps, a, ax, bs, st);
+            else if (epi == EPI_RESID)
+                e = bias ? launch_tc3<true, true, EPI_RESID>(maps, a, ax, bs, st)
+                         : launch_tc3<true, false, EPI_RESID>(maps, a, ax, bs, st);
+            else
+                e = bias ? launch_tc3<true, true, EPI_NONE>(maps, a, ax, bs, st)
+                         : launch_tc3<true, false, EPI_NONE>(maps, a, ax, bs, st);
+        }
+        const cudaError_t f = cudaFreeAsync(scratch, st);
+        return e != cudaSuccess ? e : f;
     }
     const int64_t n = rows * N;
     const unsigned grid = (unsigned)((n + 255) / 256);

@@ -119,3 +119,49 @@ def test_embedding_forward(cuda):
         assert torch.equal(out, W[ids.long()])
     with pytest.raises(ValueError, match="layers: id out of range"):
         m.embedding_forward(W, torch.tensor([0, 50], dtype=torch.int32, device=cuda), 1, 2)
+
+
+F32_SHAPES = [(7, 4, 4), (128, 256, 256), (300, 132, 260), (1000, 516, 68), (4096, 1024, 2048)]
+
+
+@pytest.mark.parametrize("rows,K,L", F32_SHAPES)
+def test_fp32_rows_3xtf32(cuda, rows, K, L):
+    """fp32 rows on the 3xTF32 tensor-core kernel (operands split into tf32
+    hi + lo, lo*hi + hi*lo + hi*hi) against fp64 (forward with bias and the
+    fused epilogues, and dx).  Tolerance rel 1e-5 with atol 5e-5 * ||ref||_inf:
+    the split itself is good to ~2^-22, but the tensor core's fp32
+    accumulation over the K-long reduction loses ~1e-5 of the largest partial
+    sums at K ~ 500 (measured 1.3e-5), as any tensor-core fp32-accumulate GEMM
+    does."""
+    from paper_2411_00999_b200 import linear
+
+    gen = torch.Generator(device="cpu").manual_seed(rows + 3 * K + 7 * L)
+    x = torch.randn(rows, K, generator=gen).to(cuda)
+    g = torch.randn(rows, L, generator=gen).to(cuda)
+    W = (torch.randn(K, L, generator=gen) / K ** 0.5).to(cuda)
+    bias = torch.randn(L, generator=gen).to(cuda)
+    res = torch.randn(rows, L, generator=gen).to(cuda)
+
+    def chk(out, ref, what):
+        o, r = out.double().cpu().numpy(), ref.cpu().numpy()
+        atol = 5e-5 * float(np.max(np.abs(r)))
+        assert close(o, r, 1e-5, atol), (what, float(np.max(np.abs(o - r)) / max(float(np.max(np.abs(r))), 1e-300)))
+
+    y = torch.empty(rows, L, device=cuda)
+    linear.linear_gemm("fwd", x, W, bias, y, rows, K, L)
+    torch.cuda.synchronize()
+    chk(y, x.double() @ W.double() + bias.double(), "fwd+bias")
+    linear.linear_gemm("fwd", x, W, bias, y, rows, K, L, epilogue="tanh")
+    torch.cuda.synchronize()
+    chk(y, torch.tanh(x.double() @ W.double() + bias.double()), "fwd tanh")
+    linear.linear_gemm("fwd", x, W, None, y, rows, K, L, epilogue="residual", aux=res)
+    torch.cuda.synchronize()
+    chk(y, res.double() + x.double() @ W.double(), "fwd residual")
+    dx = torch.empty(rows, K, device=cuda)
+    linear.linear_gemm("dx", g, W, None, dx, rows, K, L)
+    torch.cuda.synchronize()
+    chk(dx, g.double() @ W.double().t(), "dx")
+    z = torch.tanh(torch.randn(rows, K, generator=gen)).to(cuda)
+    linear.linear_gemm("dx", g, W, None, dx, rows, K, L, epilogue="dtanh", aux=z)
+    torch.cuda.synchronize()
+    chk(dx, (g.double() @ W.double().t()) * (1 - z.double() ** 2), "dx dtanh")
