@@ -463,6 +463,10 @@ static bool use_tc_gram(gnsb_dtype dt, int64_t B, int64_t T, int64_t K, int64_t 
 gnsb_status gnsb_linear_pe_workspace_size(int64_t B, int64_t T, int64_t K, int64_t L, gnsb_dtype dt, size_t* bytes) {
     if (!bytes || B < 0 || T < 0 || K < 1 || L < 1) return fail(GNSB_EINVAL, "layers: invalid extents");
     size_t n = dt == GNSB_F64 ? gnsb::generic_workspace_f64(B, T, K, L) : gnsb::generic_workspace(B, T, K, L);
+    if (K == 1 && dt != GNSB_F64) {  // the bias call's workspace: room for the streaming bias kernel
+        const size_t m = gnsb::bias_fast_workspace(B, T, L);
+        n = n > m ? n : m;
+    }
     if (use_tc_wgrad(dt, B, T, K, L)) {
         const size_t m = gnsb::wgrad_workspace(B, K, L);
         n = n > m ? n : m;
@@ -528,6 +532,11 @@ gnsb_status gnsb_linear_bias_pe(const void* g, void* dbias, double* raw_b, doubl
     const size_t need = dt == GNSB_F64 ? gnsb::generic_workspace_f64(B, T, 1, L) : gnsb::generic_workspace(B, T, 1, L);
     if (!ws || ws_bytes < need)
         return fail(GNSB_EINVAL, "layers: workspace too small (query gnsb_linear_pe_workspace_size)");
+    if (T > 0 && gnsb::bias_fast_ok((int)dt, L, g, dbias) && ws_bytes >= gnsb::bias_fast_workspace(B, T, L)) {
+        const cudaError_t e = gnsb::launch_bias_fast((int)dt, g, dbias, raw_b, sums, B, T, L, ws,
+                                                     static_cast<cudaStream_t>(stream));
+        return e == cudaSuccess ? debug_ok("gnsb_linear_bias_pe") : cuda_fail(e, "linear_bias_pe launch");
+    }
     const cudaError_t e = gnsb::launch_linear_generic((int)dt, 1, nullptr, g, dbias, dt == GNSB_F64, raw_b, sums, 1, B,
                                                       T, 1, L, ws, static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? debug_ok("gnsb_linear_bias_pe") : cuda_fail(e, "linear_bias_pe launch");

@@ -78,6 +78,11 @@ cudaError_t launch_wgrad_norms(const void* x, const void* g, float* dW, double* 
                                int64_t T, int64_t K, int64_t L, void* ws, cudaStream_t st);
 size_t generic_workspace(int64_t B, int64_t T, int64_t K, int64_t L);
 size_t generic_workspace_f64(int64_t B, int64_t T, int64_t K, int64_t L);
+// bias gradient + per-example norms as an HBM stream (fp32 / bf16 rows, L % 8 == 0)
+bool bias_fast_ok(int dt, int64_t L, const void* g, const void* dbias);
+size_t bias_fast_workspace(int64_t B, int64_t T, int64_t L);
+cudaError_t launch_bias_fast(int dt, const void* g, void* dbias, double* raw, double* sums, int64_t B, int64_t T,
+                             int64_t L, void* ws, cudaStream_t st);
 // kind 0: weight (simultaneous form), 1: bias, 2: Gram form (norms only)
 cudaError_t launch_linear_generic(int dt, int kind, const void* x, const void* g, void* out_grad, int out_f64,
                                   double* raw, double* sums, int sum_slot, int64_t B, int64_t T, int64_t K, int64_t L,

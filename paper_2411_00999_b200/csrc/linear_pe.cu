@@ -665,6 +665,129 @@ __global__ void __launch_bounds__(256) bias_pe_kernel(const T* g, int64_t B, int
     }
 }
 
+
+// ------------------------------------------------- bias, fp32 / bf16 rows --
+// bias'_b[j] = sum_t g[b,t,j], raw_b = ||bias'_b||^2, dbias = sum_b bias'_b
+// (layers.cpp:118-119, 125-130) as an HBM stream: pass 1, grid (column
+// chunks, examples, token chunks), a thread owns 8 columns and sums its token
+// chunk (fp32 partials [B][TC][L]); pass 2, a thread per 8 columns combines
+// the token chunks in order (fp64) per example, adds the squares into a
+// per-(example, CTA) slot and the examples into dbias.  No atomics; the
+// generic kernel (one thread per column, every token in sequence) stays for
+// fp64 rows (reference order) and unaligned shapes.
+constexpr int kBiasRows = 64;  // tokens per pass-1 chunk
+template <typename T>
+__global__ void __launch_bounds__(256) bias_part_kernel(const T* __restrict__ g, int64_t Tn, int64_t L, int TC,
+                                                        float* __restrict__ part) {
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // 8-column vector
+    const int64_t b = blockIdx.y, tc = blockIdx.z;
+    if (v * 8 >= L) return;
+    const int64_t t0 = tc * kBiasRows, t1 = t0 + kBiasRows < Tn ? t0 + kBiasRows : Tn;
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const T* base = g + (b * Tn) * L + v * 8;
+#pragma unroll 4
+    for (int64_t t = t0; t < t1; ++t) {
+        float f[8];
+        if constexpr (std::is_same<T, float>::value) {
+            const float4 a = __ldg(reinterpret_cast<const float4*>(base + t * L));
+            const float4 c = __ldg(reinterpret_cast<const float4*>(base + t * L + 4));
+            f[0] = a.x, f[1] = a.y, f[2] = a.z, f[3] = a.w, f[4] = c.x, f[5] = c.y, f[6] = c.z, f[7] = c.w;
+        } else {
+            unpack<T>(__ldg(reinterpret_cast<const uint4*>(base + t * L)), f);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] += f[k];
+    }
+    float4* dst = reinterpret_cast<float4*>(part + ((b * TC + tc) * L) + v * 8);
+    dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    dst[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+}
+
+__global__ void __launch_bounds__(256) bias_combine_kernel(const float* __restrict__ part, int64_t B, int TC, int64_t L,
+                                                           float* __restrict__ dbias, double* __restrict__ q,
+                                                           double* __restrict__ qbig) {
+    __shared__ double s_red[256 / 32];
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool ok = v * 8 < L;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double tot[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int64_t b = 0; b < B; ++b) {
+        double sq = 0.0;
+        if (ok) {
+            double e[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int tc = 0; tc < TC; ++tc) {
+                const float4* src = reinterpret_cast<const float4*>(part + ((b * TC + tc) * L) + v * 8);
+                const float4 a = __ldg(src), c = __ldg(src + 1);
+                e[0] += a.x, e[1] += a.y, e[2] += a.z, e[3] += a.w, e[4] += c.x, e[5] += c.y, e[6] += c.z, e[7] += c.w;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                sq = fma(e[k], e[k], sq);
+                tot[k] += e[k];
+            }
+        }
+        sq = warp_sum(sq);
+        if (lane == 0) s_red[warp] = sq;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < 256 / 32; ++w) t += s_red[w];
+            q[b * gridDim.x + blockIdx.x] = t;
+        }
+        __syncthreads();
+    }
+    double sb = 0.0;
+    if (ok) {
+        float4* dst = reinterpret_cast<float4*>(dbias + v * 8);
+        const float4 o0 = make_float4((float)tot[0], (float)tot[1], (float)tot[2], (float)tot[3]);
+        const float4 o1 = make_float4((float)tot[4], (float)tot[5], (float)tot[6], (float)tot[7]);
+        dst[0] = o0;
+        dst[1] = o1;
+        const float of[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) sb = fma((double)of[k], (double)of[k], sb);
+    }
+    sb = warp_sum(sb);
+    if (lane == 0) s_red[warp] = sb;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 256 / 32; ++w) t += s_red[w];
+        qbig[blockIdx.x] = t;
+    }
+}
+
+bool bias_fast_ok(int dt, int64_t L, const void* g, const void* dbias) {
+    return (dt == 0 || dt == 1) && L % 8 == 0 && (reinterpret_cast<uintptr_t>(g) & 15u) == 0 &&
+           (reinterpret_cast<uintptr_t>(dbias) & 15u) == 0;
+}
+size_t bias_fast_workspace(int64_t B, int64_t T, int64_t L) {
+    const int64_t TC = (T + kBiasRows - 1) / kBiasRows, nblk = (L / 8 + 255) / 256;
+    return (size_t)B * TC * L * 4 + (size_t)(B + 1) * nblk * 8 + 512;
+}
+cudaError_t launch_bias_fast(int dt, const void* g, void* dbias, double* raw, double* sums, int64_t B, int64_t T,
+                             int64_t L, void* ws, cudaStream_t st) {
+    const int TC = (int)((T + kBiasRows - 1) / kBiasRows);
+    const int64_t nv = L / 8;
+    const unsigned nblk = (unsigned)((nv + 255) / 256);
+    float* part = static_cast<float*>(ws);
+    double* q = reinterpret_cast<double*>(static_cast<unsigned char*>(ws) + ((size_t)B * TC * L * 4 + 255) / 256 * 256);
+    double* qbig = q + B * nblk;
+    const dim3 g1(nblk, (unsigned)B, (unsigned)TC);
+    if (dt == 0)
+        bias_part_kernel<float><<<g1, 256, 0, st>>>(static_cast<const float*>(g), T, L, TC, part);
+    else
+        bias_part_kernel<__nv_bfloat16><<<g1, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(g), T, L, TC, part);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    bias_combine_kernel<<<nblk, 256, 0, st>>>(part, B, TC, L, static_cast<float*>(dbias), q, qbig);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    fold_rows_kernel<<<1, 256, 0, st>>>(q, (int)B, (int)nblk, raw, sums, 1);
+    if (sums) fold_rows_kernel<<<1, 256, 0, st>>>(qbig, 1, (int)nblk, nullptr, sums, 3);
+    return cudaGetLastError();
+}
+
 // Gram form, generic: raw_b = sum_{t,u} (x_t . x_u)(g_t . g_u), one thread per (t, u)
 template <typename T>
 __global__ void __launch_bounds__(256) gram_generic_kernel(const T* x, const T* g, int64_t B, int64_t Tn, int64_t K,

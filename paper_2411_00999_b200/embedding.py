@@ -15,7 +15,8 @@ from . import _lib
 from .layers import _WS, LayerGradOutput, _ptr, _stream_ptr, gnsb_dtype, stat_dtype
 
 
-def embedding_backward_simultaneous(ids: torch.Tensor, g: torch.Tensor, vocab: int) -> LayerGradOutput:
+def embedding_backward_simultaneous(ids: torch.Tensor, g: torch.Tensor, vocab: int,
+                                    validate: bool = True) -> LayerGradOutput:
     """ids [B, T] int32 (device), g [B, T, D] gradient of a mean-reduced loss.
     Returns weight grad [V, D] (fp32, fp64 for fp64 rows), the corrected
     per-example norm (B * sum_b raw) and the raw per-example norms [B]."""
@@ -26,7 +27,9 @@ def embedding_backward_simultaneous(ids: torch.Tensor, g: torch.Tensor, vocab: i
         raise ValueError("layers: id count does not match batch * t_len")
     if B == 0:
         raise ValueError("layers: empty batch")
-    if ids.numel() and (int(ids.min()) < 0 or int(ids.max()) >= vocab):  # layers.cpp:333
+    # layers.cpp:333 (a host round trip; validate=False skips it for ids valid
+    # by construction -- out-of-range ids then only raise the kernel's bad flag)
+    if validate and ids.numel() and (int(ids.min()) < 0 or int(ids.max()) >= vocab):
         raise ValueError("layers: id out of range")
     dev = g.device
     ids = ids.to(device=dev, dtype=torch.int32).contiguous()
@@ -45,12 +48,13 @@ def embedding_backward_simultaneous(ids: torch.Tensor, g: torch.Tensor, vocab: i
     return LayerGradOutput({"weight": dW}, {"weight": sums[0] / bd * (bd * bd)}, {"weight": raw}, B, sums)
 
 
-def embedding_forward(weight: torch.Tensor, ids: torch.Tensor, batch: int, t_len: int) -> torch.Tensor:
+def embedding_forward(weight: torch.Tensor, ids: torch.Tensor, batch: int, t_len: int,
+                      validate: bool = True) -> torch.Tensor:
     """out[b, t, :] = weight[ids[b * t_len + t], :] (layers.cpp:300-313); [batch, t_len, D]."""
     if ids.numel() != batch * t_len:
         raise ValueError("layers: id count does not match batch * t_len")
     V, D = int(weight.shape[0]), int(weight.shape[1])
-    if ids.numel() and (int(ids.min()) < 0 or int(ids.max()) >= V):
+    if validate and ids.numel() and (int(ids.min()) < 0 or int(ids.max()) >= V):
         raise ValueError("layers: id out of range")
     if not weight.is_cuda:
         raise RuntimeError("layers: the B200 path has no CPU fallback (weights are on the CPU)")

@@ -224,14 +224,15 @@ class ToyModelPE(torch.nn.Module):
 
     @torch.no_grad()
     def forward_backward(self, ids: torch.Tensor, targets: torch.Tensor, loss_scale: float = 1.0,
-                         rows_dtype: Optional[torch.dtype] = None) -> torch.Tensor:
+                         rows_dtype: Optional[torch.dtype] = None, validate: bool = True) -> torch.Tensor:
         """The reference's model_backward (proj/src/model.cpp:144-188) on the
         library's kernels, no autograd: returns the loss (device fp64 scalar,
         mean over examples of the per-example mean-token cross-entropy times
         loss_scale), sets every parameter's .grad and every instrumented
         layer's norm record (the GnsTracker input).  rows_dtype: activation
         dtype (default: the parameter dtype; bf16 with fp32 parameters runs
-        the tcgen05 GEMMs)."""
+        the tcgen05 GEMMs).  validate=False skips the host-side id range
+        checks (no host synchronisation: the step can be graph-captured)."""
         from .embedding import embedding_backward_simultaneous, embedding_forward
         from .layers import (LayerNormCache, LayerNormLayer, layernorm_backward_reduce, layernorm_backward_rows,
                              layernorm_forward)
@@ -250,7 +251,7 @@ class ToyModelPE(torch.nn.Module):
             return LayerNormLayer(ln.weight, ln.bias, ln.eps)
 
         # ---- forward (model.cpp:87-109)
-        x = embedding_forward(self.embed.weight.to(adt), ids.reshape(-1), B, T)
+        x = embedding_forward(self.embed.weight.to(adt), ids.reshape(-1), B, T, validate=validate)
         saved = []
         for ln, f1, f2 in zip(self.lns, self.fc1, self.fc2):
             fr = layernorm_forward(lnl(ln), x)
@@ -301,7 +302,7 @@ class ToyModelPE(torch.nn.Module):
             da = linear_bw(self.fc2[i], a, dx, epi_aux=a)  # fc2 input grad times (1 - tanh^2), fused
             dh = linear_bw(self.fc1[i], fr.output, da)
             dx = dx + ln_bw(self.lns[i], fr, dh)
-        r = embedding_backward_simultaneous(ids, dx, int(self.embed.weight.shape[0]))
+        r = embedding_backward_simultaneous(ids, dx, int(self.embed.weight.shape[0]), validate=validate)
         self.embed.weight.grad = r.weight_grads["weight"].to(pdt)
         self.embed.norm_record, self.embed.batch_size = r.sums4, B
         self.embed.per_example_raw = {"weight": r.per_example_sqnorms_raw["weight"]}

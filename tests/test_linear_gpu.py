@@ -121,6 +121,29 @@ def test_auto_form_short_sequences_gram_plus_plain_dw(orc, cuda, B, T, K, L):
     assert close(float(r.grads.sums4[2]), float(np.sum(ref["dW"] ** 2)), 1e-4)
 
 
+@pytest.mark.parametrize("dt,B,T,L", [(torch.bfloat16, 4, 300, 264), (torch.float32, 3, 1024, 3072),
+                                      (torch.bfloat16, 8, 64, 50304), (torch.float32, 2, 7, 8)])
+def test_bias_norms_streaming_kernel(orc, cuda, dt, B, T, L):
+    """The bias gradient and its per-example norms (layers.cpp:118-119, 125-130)
+    on the streaming kernel (fp32 / bf16 rows, L % 8 == 0) against the oracle on
+    the same rows: dbias rel 1e-5 of its max, raw_b and the record rel 1e-5."""
+    import paper_2411_00999_b200 as m
+    from paper_2411_00999_b200 import linear
+
+    K = 8
+    x, g = m.synth_linear(B, T, K, L, dt, cuda)
+    layer = linear.LinearLayer(torch.zeros(K, L, device=cuda), torch.zeros(L, device=cuda))
+    r = linear.linear_backward_simultaneous(layer, x, g, need_input_grad=False)
+    gd = g.double().cpu().numpy()
+    bb = gd.sum(axis=1)  # [B, L] per-example bias gradients
+    torch.cuda.synchronize()
+    db = r.grads.weight_grads["bias"].double().cpu().numpy()
+    assert close(db, bb.sum(0), 1e-5, 1e-5 * np.abs(bb.sum(0)).max())
+    assert close(r.grads.per_example_sqnorms_raw["bias"].cpu().numpy(), (bb ** 2).sum(1), 1e-5)
+    assert close(float(r.grads.sums4[1]), float((bb ** 2).sum()), 1e-5)
+    assert close(float(r.grads.sums4[3]), float((bb.sum(0) ** 2).sum()), 1e-5)
+
+
 def test_weight_grad_form_equals_gram_form(cuda):
     """<X X^T, G G^T>_F equals ||sum_t x_t^T g_t||^2 (test_layers.cpp:135-149)."""
     import paper_2411_00999_b200 as m
