@@ -450,6 +450,7 @@ def run_ours(args):
         extra["cfg5_strong_g1"] = Cfg5Strong(args, m, lib, dev, torch, np, 1, 0, "none").measure(args.steps,
                                                                                                 args.warmup)
         extra["embedding"] = run_embedding(m, lib, dev, torch, np)
+        extra["toy_model_step"] = run_toy_step(m, dev, torch, np)
 
     traffic = load_traffic()
     line = {
@@ -699,6 +700,68 @@ def run_cfg4(m, lib, dev, torch, np):
            "gns_total": {"g2": float(groups[0, 0]), "s": float(groups[0, 1]), "b_simple_ema": float(groups[0, 2])},
            "launches_per_step": NL + 2, "stage2": "deferred: one grouped reduce for the 25 layers"}
     del cases
+    torch.cuda.empty_cache()
+    return out
+
+
+def run_toy_step(m, dev, torch, np):
+    """SURVEY §8(f) rank 4 at GPT-2-small width: one training step (forward +
+    backward) of the reference toy model (proj/src/model.cpp) with EVERY
+    layer's per-example gradient norms and the device GNS step, all on the
+    library's kernels (ToyModelPE.forward_backward, bf16 activations, fp32
+    parameters), against the same architecture as an uninstrumented PyTorch
+    step (cuBLAS, autograd, bf16 autocast, no per-example norms) -- the
+    paper's deployment comparison.  Both graph-replayed."""
+    from paper_2411_00999_b200.model import ToyModelPE
+    from paper_2411_00999_b200.nn import GnsTracker
+
+    V, D, HM, NB, B, T_ = 50304, 768, 4, 12, 8, 1024
+    gen = torch.Generator(device="cpu").manual_seed(0)
+    ids = torch.randint(0, V, (B, T_), generator=gen, dtype=torch.int32).to(dev)
+    tg = torch.randint(0, V, (B, T_), generator=gen, dtype=torch.int32).to(dev)
+    model = ToyModelPE(V, D, HM, NB, seed=1, device=dev)
+    inst = model.instrumented_layers()
+    tracker = GnsTracker([mod for _, mod in inst], alpha=0.9)
+    nparam = sum(p.numel() for p in model.parameters())
+
+    def ours():
+        model.forward_backward(ids, tg, rows_dtype=torch.bfloat16, validate=False)
+        tracker.step()
+
+    ms_ours = time_graph(ours, torch, np, dev, reps=10)
+    H = D * HM
+    tm = torch.nn.ModuleDict({
+        "emb": torch.nn.Embedding(V, D), "lnf": torch.nn.LayerNorm(D), "head": torch.nn.Linear(D, V),
+        "lns": torch.nn.ModuleList([torch.nn.LayerNorm(D) for _ in range(NB)]),
+        "fc1": torch.nn.ModuleList([torch.nn.Linear(D, H) for _ in range(NB)]),
+        "fc2": torch.nn.ModuleList([torch.nn.Linear(H, D) for _ in range(NB)])}).to(dev)
+
+    def plain():
+        for p in tm.parameters():
+            p.grad = None
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            x = tm["emb"](ids.long())
+            for ln, f1, f2 in zip(tm["lns"], tm["fc1"], tm["fc2"]):
+                x = x + f2(torch.tanh(f1(ln(x))))
+            logits = tm["head"](tm["lnf"](x))
+            loss = torch.nn.functional.cross_entropy(logits.reshape(-1, V).float(), tg.reshape(-1).long())
+        loss.backward()
+
+    ms_torch = time_graph(plain, torch, np, dev, reps=10)
+    flops = 6.0 * nparam * B * T_
+    peak_tf = 1647.2
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peak_tf = float(json.load(f)["bf16_tflops"])
+    except Exception:
+        pass
+    out = {"workload": f"toy model (proj/src/model.cpp) V={V} D={D} H={H} blocks={NB}, B={B} T={T_}: forward + "
+                       f"backward + per-example norms of all {len(inst)} instrumented layers + device GNS step",
+           "params": nparam, "flops_per_step": flops, "ms_ours": ms_ours, "ms_torch_uninstrumented": ms_torch,
+           "ratio_ours_over_torch": ms_ours / ms_torch, "model_TFLOPs_ours": flops / ms_ours / 1e9,
+           "mfu_ours": flops / ms_ours / 1e9 / peak_tf,
+           "torch_def": "same architecture, cuBLAS + autograd, bf16 autocast, NO per-example norms"}
+    del model, tm, tracker
     torch.cuda.empty_cache()
     return out
 

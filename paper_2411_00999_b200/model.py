@@ -250,6 +250,17 @@ class ToyModelPE(torch.nn.Module):
         def lnl(ln):
             return LayerNormLayer(ln.weight, ln.bias, ln.eps)
 
+        # bf16 rows with fp32 parameters: one bf16 operand copy of each weight
+        # per step, shared by its forward and input-grad GEMMs
+        wop = {}
+
+        def wt(mod):
+            if adt == torch.bfloat16 and mod.weight.dtype != torch.bfloat16:
+                if mod not in wop:
+                    wop[mod] = mod.weight.to(torch.bfloat16)
+                return wop[mod]
+            return mod.weight
+
         # ---- forward (model.cpp:87-109)
         x = embedding_forward(self.embed.weight.to(adt), ids.reshape(-1), B, T, validate=validate)
         saved = []
@@ -257,14 +268,14 @@ class ToyModelPE(torch.nn.Module):
             fr = layernorm_forward(lnl(ln), x)
             H = f1.weight.shape[1]
             a = torch.empty(B, T, H, dtype=adt, device=x.device)
-            linear_gemm("fwd", fr.output, f1.weight, f1.bias, a, N, D, H, epilogue="tanh")
+            linear_gemm("fwd", fr.output, wt(f1), f1.bias, a, N, D, H, epilogue="tanh")
             xn = torch.empty_like(x)
-            linear_gemm("fwd", a, f2.weight, f2.bias, xn, N, H, D, epilogue="residual", aux=x)
+            linear_gemm("fwd", a, wt(f2), f2.bias, xn, N, H, D, epilogue="residual", aux=x)
             saved.append((fr, a))
             x = xn
         ffr = layernorm_forward(lnl(self.final_ln), x)
         logits = torch.empty(B, T, V, dtype=adt, device=x.device)
-        linear_gemm("fwd", ffr.output, self.head.weight, self.head.bias, logits, N, D, V)
+        linear_gemm("fwd", ffr.output, wt(self.head), self.head.bias, logits, N, D, V)
         # ---- loss + dlogits (model.cpp:113-141, 150-156)
         upstream = loss_scale * (1.0 / T) / B
         dlogits = torch.empty_like(logits)
@@ -286,9 +297,9 @@ class ToyModelPE(torch.nn.Module):
             mod.per_example_raw = {"weight": raw[0], "bias": raw[1]} if mod.bias is not None else {"weight": raw[0]}
             dx = torch.empty(*g.shape[:-1], K, dtype=g.dtype, device=g.device)
             if epi_aux is None:
-                linear_gemm("dx", g, mod.weight, None, dx, N, K, L)
+                linear_gemm("dx", g, wt(mod), None, dx, N, K, L)
             else:
-                linear_gemm("dx", g, mod.weight, None, dx, N, K, L, epilogue="dtanh", aux=epi_aux)
+                linear_gemm("dx", g, wt(mod), None, dx, N, K, L, epilogue="dtanh", aux=epi_aux)
             return dx
 
         def ln_bw(mod, fr, g):
