@@ -97,21 +97,33 @@ struct GemmArgs {
     __nv_bfloat16* out;   // [M, N]
 };
 
-template <bool B_KMAJOR, bool BIAS, int EPI>
+// BNT: output tile width, 256 (default) or 128 (skinny outputs: more tiles,
+// fewer idle SMs in the last wave; the ring then holds 6 stages in the same
+// shared memory)
+template <bool B_KMAJOR, bool BIAS, int EPI, int BNT = gm::BN>
 __global__ void __launch_bounds__(gm::THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
                 const __grid_constant__ CUtensorMap tmo, GemmArgs a) {
-    using namespace gm;
+    using gm::BM;
+    using gm::BK;
+    using gm::A_BYTES;
+    using gm::EPI_WARPS;
+    using gm::OUT_BOX_BYTES;
+    using gm::TMEM_COLS;
+    constexpr int BN = BNT;
+    constexpr int STAGE_BYTES = A_BYTES + BN * BK * 2;
+    constexpr int STAGES = gm::STAGES * gm::STAGE_BYTES / STAGE_BYTES;  // same ring bytes
+    static_assert(STAGES * STAGE_BYTES <= gm::STAGES * gm::STAGE_BYTES, "ring");
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem =
         reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     unsigned char* ring = smem;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)STAGES * STAGE_BYTES);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)gm::STAGES * gm::STAGE_BYTES);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;  // [2]
     uint64_t* tempty = tfull + 2;      // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-    unsigned char* obox = smem + (size_t)STAGES * STAGE_BYTES + 1024;  // [EPI_WARPS][32 rows][128 B], 1 KB aligned
+    unsigned char* obox = smem + (size_t)gm::STAGES * gm::STAGE_BYTES + 1024;  // [EPI_WARPS][32 rows][128 B], 1 KB aligned
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntiles = a.tiles_m * a.tiles_n;
@@ -215,7 +227,7 @@ __global__ void __launch_bounds__(gm::THREADS, 1)
         // output are clipped by the tensor map).
         const int e = warp - 2;
         const int quad = warp & 3;  // TMEM lanes this warp may access
-        const int half = e / 4;     // column half of the 256-wide tile
+        const int half = e / 4;     // column half of the tile
         unsigned char* box = obox + (size_t)e * OUT_BOX_BYTES;
         int buf = 0;
         uint32_t tph = 0;
@@ -226,9 +238,9 @@ __global__ void __launch_bounds__(gm::THREADS, 1)
             const int row = m0 + quad * 32 + lane;
             mbar_wait(&tfull[buf], tph);
             tc::fence_after_sync();
-            const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN + half * 128);
+            const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN + half * (BN / 2));
 #pragma unroll
-            for (int gi = 0; gi < 2; ++gi) {
+            for (int gi = 0; gi < BN / 128; ++gi) {
                 // the previous TMA store from this box has finished reading it
                 if (lane == 0) bulk_wait_read0();
                 __syncwarp();
@@ -238,12 +250,12 @@ __global__ void __launch_bounds__(gm::THREADS, 1)
                     uint32_t r[32];
                     tc::tmem_ld_32x32b_x32(base + cc * 32, r);
                     tc::tmem_ld_wait();
-                    if (cc == 3) {  // the accumulator is in registers: hand it back to the MMA warp
+                    if (cc == BN / 64 - 1) {  // the accumulator is in registers: hand it back to the MMA warp
                         tc::fence_before_sync();
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&tempty[buf]);
                     }
-                    const int c0 = n0 + half * 128 + cc * 32;
+                    const int c0 = n0 + half * (BN / 2) + cc * 32;
 #pragma unroll
                     for (int v = 0; v < 4; ++v) {
                         float f[8];
@@ -275,7 +287,7 @@ __global__ void __launch_bounds__(gm::THREADS, 1)
                 fence_proxy_async_smem();  // generic-proxy writes -> visible to the TMA (async proxy)
                 __syncwarp();
                 if (lane == 0) {
-                    tma_store_3d(&tmo, box, n0 + half * 128 + gi * 64, m0 + quad * 32, 0);
+                    tma_store_3d(&tmo, box, n0 + half * (BN / 2) + gi * 64, m0 + quad * 32, 0);
                     bulk_commit();
                 }
             }
@@ -637,10 +649,10 @@ bool make_map_2d(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, i
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <bool BK_, bool BIAS, int EPI>
-cudaError_t launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo, const GemmArgs& a,
-                      cudaStream_t st) {
-    const void* fn = reinterpret_cast<const void*>(gemm_kernel<BK_, BIAS, EPI>);
+template <bool BK_, bool BIAS, int EPI, int BNT>
+cudaError_t launch_tc_bn(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo, const GemmArgs& a,
+                         cudaStream_t st) {
+    const void* fn = reinterpret_cast<const void*>(gemm_kernel<BK_, BIAS, EPI, BNT>);
     cudaError_t e = ensure_smem_attr(fn, gm::SMEM);
     if (e != cudaSuccess) return e;
     const int ntiles = a.tiles_m * a.tiles_n;
@@ -655,7 +667,22 @@ cudaError_t launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtens
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, gemm_kernel<BK_, BIAS, EPI>, ma, mb, mo, a);
+    return cudaLaunchKernelEx(&cfg, gemm_kernel<BK_, BIAS, EPI, BNT>, ma, mb, mo, a);
+}
+template <bool BK_, bool BIAS, int EPI>
+cudaError_t launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo, const GemmArgs& a,
+                      cudaStream_t st, int bn) {
+    return bn == 128 ? launch_tc_bn<BK_, BIAS, EPI, 128>(ma, mb, mo, a, st)
+                     : launch_tc_bn<BK_, BIAS, EPI, 256>(ma, mb, mo, a, st);
+}
+// output tile width: 128 when the 256-wide tiling leaves the last wave of a
+// small tile count mostly idle (e.g. N = 768 outputs: 3 x 64 tiles = 1.3
+// waves at 8192 rows); the narrower tile pays ~8 % in operand traffic per FLOP
+int gemm_pick_bn(int64_t tiles_m, int64_t N) {
+    const int sms = device_sm_count();
+    auto eff = [&](int64_t t) { return (double)t / (double)(((t + sms - 1) / sms) * sms); };
+    const double e256 = eff(tiles_m * ((N + 255) / 256)), e128 = eff(tiles_m * ((N + 127) / 128));
+    return e128 * 0.92 > e256 ? 128 : 256;
 }
 
 
@@ -758,8 +785,9 @@ cudaError_t launch_linear_gemm(int kind, int epi, int dt, int w_dt, const void* 
         }
         CUtensorMap ma, mb;
         if (!make_map_2d(&ma, in, rows, Kr, gm::BK, gm::BM)) return cudaErrorInvalidValue;
-        const bool ok = kind == 0 ? make_map_2d(&mb, wb, K, L, 64, gm::BK)       // W [K, L]: box 64 (L) x 64 (K)
-                                  : make_map_2d(&mb, wb, K, L, gm::BK, gm::BN);  // W [K, L]: box 64 (L) x 256 (K)
+        const int bn = gemm_pick_bn((rows + gm::BM - 1) / gm::BM, N);
+        const bool ok = kind == 0 ? make_map_2d(&mb, wb, K, L, 64, gm::BK)  // W [K, L]: box 64 (L) x 64 (K)
+                                  : make_map_2d(&mb, wb, K, L, gm::BK, bn);  // W [K, L]: box 64 (L) x bn (K)
         if (!ok) return cudaErrorInvalidValue;
         CUtensorMap mo;  // the output [rows, N], stored by 32-row x 64-column boxes
         if (!make_map_2d(&mo, out, rows, N, 64, 32)) return cudaErrorInvalidValue;
@@ -768,22 +796,22 @@ cudaError_t launch_linear_gemm(int kind, int epi, int dt, int w_dt, const void* 
         a.N = (int)N;
         a.Kr = (int)Kr;
         a.tiles_m = (int)((rows + gm::BM - 1) / gm::BM);
-        a.tiles_n = (int)((N + gm::BN - 1) / gm::BN);
+        a.tiles_n = (int)((N + bn - 1) / bn);
         a.bias = static_cast<const float*>(bias);
         a.aux = static_cast<const __nv_bfloat16*>(aux);
         a.out = static_cast<__nv_bfloat16*>(out);
         if (kind == 1) {
-            if (epi == EPI_DTANH) return launch_tc<true, false, EPI_DTANH>(ma, mb, mo, a, st);
-            return launch_tc<true, false, EPI_NONE>(ma, mb, mo, a, st);
+            if (epi == EPI_DTANH) return launch_tc<true, false, EPI_DTANH>(ma, mb, mo, a, st, bn);
+            return launch_tc<true, false, EPI_NONE>(ma, mb, mo, a, st, bn);
         }
         switch (epi) {
             case EPI_TANH:
-                return bias ? launch_tc<false, true, EPI_TANH>(ma, mb, mo, a, st) : launch_tc<false, false, EPI_TANH>(ma, mb, mo, a, st);
+                return bias ? launch_tc<false, true, EPI_TANH>(ma, mb, mo, a, st, bn) : launch_tc<false, false, EPI_TANH>(ma, mb, mo, a, st, bn);
             case EPI_RESID:
-                return bias ? launch_tc<false, true, EPI_RESID>(ma, mb, mo, a, st)
-                            : launch_tc<false, false, EPI_RESID>(ma, mb, mo, a, st);
+                return bias ? launch_tc<false, true, EPI_RESID>(ma, mb, mo, a, st, bn)
+                            : launch_tc<false, false, EPI_RESID>(ma, mb, mo, a, st, bn);
             default:
-                return bias ? launch_tc<false, true, EPI_NONE>(ma, mb, mo, a, st) : launch_tc<false, false, EPI_NONE>(ma, mb, mo, a, st);
+                return bias ? launch_tc<false, true, EPI_NONE>(ma, mb, mo, a, st, bn) : launch_tc<false, false, EPI_NONE>(ma, mb, mo, a, st, bn);
         }
     }
     if (gemm3_ok(dt, w_dt, rows, K, L) && al16(in) && al16(out) && al16(W) && (aux == nullptr || al16(aux))) {

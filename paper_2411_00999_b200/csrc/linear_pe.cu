@@ -378,13 +378,29 @@ __global__ void __launch_bounds__(wg::THREADS, 1)
     }
 }
 
-// raw[b] = sum_j q[b][j] (fixed order), sums[sum_slot] = sum_b raw[b] (fixed order)
+// raw[b] = sum_j q[b][j] (fixed order), sums[sum_slot] = sum_b raw[b] (fixed
+// order); with q2: also sums[slot2] = sum_j q2[j] (a second, one-row fold in
+// the same launch -- the squared norm of the batch gradient)
 constexpr int kFoldSmemRows = 4096;
 __global__ void __launch_bounds__(256) fold_rows_kernel(const double* q, int nb, int ncol, double* raw, double* sums,
-                                                        int sum_slot) {
+                                                        int sum_slot, const double* q2 = nullptr, int ncol2 = 0,
+                                                        int slot2 = 0) {
     __shared__ double rs[kFoldSmemRows];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    auto row = [&](int b) {  // 8 independent partial sums per lane: loads in flight, fixed order
+    auto rowof = [&](const double* r, int n) {  // 8 independent partial sums per lane: loads in flight, fixed order
+        double t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        int j = lane;
+        for (; j + 32 * 7 < n; j += 32 * 8)
+#pragma unroll
+            for (int u = 0; u < 8; ++u) t[u] += __ldcg(r + j + 32 * u);
+        for (; j < n; j += 32) t[0] += __ldcg(r + j);
+        return warp_sum(((t[0] + t[1]) + (t[2] + t[3])) + ((t[4] + t[5]) + (t[6] + t[7])));
+    };
+    if (q2 != nullptr && sums != nullptr && warp == (int)(blockDim.x / 32) - 1) {
+        const double t = rowof(q2, ncol2);
+        if (lane == 0) sums[slot2] = t;
+    }
+    auto row = [&](int b) {
         double t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         const double* r = q + (size_t)b * ncol;
         int j = lane;
@@ -567,8 +583,7 @@ cudaError_t launch_wgrad_norms(const void* x, const void* g, float* dW, double* 
         e = cudaGetLastError();
     }
     if (e != cudaSuccess) return e;
-    fold_rows_kernel<<<1, 256, 0, st>>>(a.q, (int)B, ntiles, raw, sums, 0);
-    if (sums) fold_rows_kernel<<<1, 256, 0, st>>>(a.qbig, 1, ntiles, nullptr, sums, 2);
+    fold_rows_kernel<<<1, 256, 0, st>>>(a.q, (int)B, ntiles, raw, sums, 0, a.qbig, ntiles, 2);
     return cudaGetLastError();
 }
 
@@ -783,8 +798,7 @@ cudaError_t launch_bias_fast(int dt, const void* g, void* dbias, double* raw, do
     bias_combine_kernel<<<nblk, 256, 0, st>>>(part, B, TC, L, static_cast<float*>(dbias), q, qbig);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    fold_rows_kernel<<<1, 256, 0, st>>>(q, (int)B, (int)nblk, raw, sums, 1);
-    if (sums) fold_rows_kernel<<<1, 256, 0, st>>>(qbig, 1, (int)nblk, nullptr, sums, 3);
+    fold_rows_kernel<<<1, 256, 0, st>>>(q, (int)B, (int)nblk, raw, sums, 1, qbig, (int)nblk, 3);
     return cudaGetLastError();
 }
 

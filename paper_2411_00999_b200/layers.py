@@ -300,7 +300,7 @@ class PendingLayerNorm:
 
 
 def layernorm_backward_rows(layer: LayerNormLayer, cache: LayerNormCache, g: torch.Tensor,
-                            need_input_grad: bool = True):
+                            need_input_grad: bool = True, ws: Optional[torch.Tensor] = None):
     """Row pass of the fused backward: returns (dx, PendingLayerNorm).  The
     per-example combine, squares and dgamma/dbeta of any number of pending
     layers then run in one `layernorm_backward_reduce` launch."""
@@ -324,7 +324,11 @@ def layernorm_backward_rows(layer: LayerNormLayer, cache: LayerNormCache, g: tor
     gamma = layer.gamma.to(device=dev, dtype=sd).contiguous()
     dx = torch.empty_like(g) if need_input_grad else None
     dt = gnsb_dtype(g.dtype)
-    ws = torch.zeros(ctypes_size(B, M, D, dt), dtype=torch.uint8, device=dev)  # owned by the pending layer
+    nbytes = ctypes_size(B, M, D, dt)
+    if ws is None or ws.numel() < nbytes:
+        # owned by the pending layer; a caller may pass one back for the next
+        # step (the reduce leaves it zeroed, ready for reuse)
+        ws = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
     _lib.check(_lib.lib().gnsb_ln_bwd_rows(_ptr(src), _ptr(mean), _ptr(rstd), _ptr(g), _ptr(gamma), _ptr(dx), B, M,
                                            D, dt, _ptr(ws), ws.numel(), _stream_ptr(dev)))
     pend = PendingLayerNorm(B, M, D, dt, ws, torch.empty(D, dtype=sd, device=dev), torch.empty(D, dtype=sd, device=dev),

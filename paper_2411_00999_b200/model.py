@@ -303,7 +303,10 @@ class ToyModelPE(torch.nn.Module):
             return dx
 
         def ln_bw(mod, fr, g):
-            dx, p = layernorm_backward_rows(lnl(mod), fr.cache, g)
+            # the workspace of the layer's previous step is reused (the grouped
+            # reduce leaves it zeroed)
+            dx, p = layernorm_backward_rows(lnl(mod), fr.cache, g, ws=getattr(mod, "_rows_ws", None))
+            mod._rows_ws = p.ws
             pend.append((mod, p))
             return dx
 

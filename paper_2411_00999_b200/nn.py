@@ -145,13 +145,13 @@ class GnsTracker:
     def step(self):
         """Returns device tensors (groups [4, 4] {g2, s, gns_ema, defined}, layers [n, 2])."""
         B = None
-        for i, m in enumerate(self.modules):
+        for m in self.modules:
             if m.norm_record is None:
                 raise RuntimeError("gns: a tracked layer has no norm record (run backward first)")
-            self.records[i].copy_(m.norm_record)
             B = m.batch_size if B is None else B
             if m.batch_size != B:
                 raise ValueError("gns: layers disagree on the batch size")
+        torch.stack([m.norm_record for m in self.modules], out=self.records)  # one gather, not one copy per layer
         for m in self.modules:  # consumed: a layer without a backward next step must not reuse it
             m.norm_record = None
         return self.acc.step(self.records, B)
