@@ -24,6 +24,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -675,14 +676,18 @@ cudaError_t launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtens
     return bn == 128 ? launch_tc_bn<BK_, BIAS, EPI, 128>(ma, mb, mo, a, st)
                      : launch_tc_bn<BK_, BIAS, EPI, 256>(ma, mb, mo, a, st);
 }
-// output tile width: 128 when the 256-wide tiling leaves the last wave of a
-// small tile count mostly idle (e.g. N = 768 outputs: 3 x 64 tiles = 1.3
-// waves at 8192 rows); the narrower tile pays ~8 % in operand traffic per FLOP
+// output tile width: 256.  A 128-wide variant (GNSB_GEMM_BN=128, A/B runs)
+// fills the last wave of small tile counts better but measured slower on every
+// shape tried, including those (N = 768 outputs at 8192 rows: 60 against 48 us;
+// GPT-2 head dx: 754 against 603 us) where it had the better wave efficiency.
 int gemm_pick_bn(int64_t tiles_m, int64_t N) {
-    const int sms = device_sm_count();
-    auto eff = [&](int64_t t) { return (double)t / (double)(((t + sms - 1) / sms) * sms); };
-    const double e256 = eff(tiles_m * ((N + 255) / 256)), e128 = eff(tiles_m * ((N + 127) / 128));
-    return e128 * 0.92 > e256 ? 128 : 256;
+    static const int forced = [] {  // GNSB_GEMM_BN=128 / 256: A/B runs
+        const char* e = std::getenv("GNSB_GEMM_BN");
+        return e ? std::atoi(e) : 0;
+    }();
+    (void)tiles_m;
+    (void)N;
+    return forced == 128 ? 128 : 256;
 }
 
 

@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gemm_gpu.py tests/test_linear_gpu.py tests/test_model_gpu.py tests/test_trainer_gpu.py tests/test_nn_gpu.py -x -q 2>&1 | grep -E "Error|assert|passed|failed" | head -20 > gpurun_out/r3i_pytest.log
+timeout 600 python experiments/gemm_bench.py > gpurun_out/r3i_gemm.log 2>&1
+timeout 600 python experiments/gemm_bench.py 8192 768 3072 >> gpurun_out/r3i_gemm.log 2>&1
+timeout 600 python experiments/gemm_bench.py 8192 768 50304 >> gpurun_out/r3i_gemm.log 2>&1
+timeout 600 python experiments/toy_step.py > gpurun_out/r3i_toy.log 2>&1
