@@ -96,12 +96,54 @@ struct GemmArgs {
     const float* bias;    // [N] (BIAS)
     const __nv_bfloat16* aux;  // [M, N] (EPI_RESID, EPI_DTANH)
     __nv_bfloat16* out;   // [M, N]
+    int ksplit;           // split-K parts (SPLIT)
+    float* part;          // [ksplit][M][N] fp32 partials (SPLIT)
 };
+
+// split-K combine: out = epi(sum_p part[p] (+ bias)), parts in fixed order
+template <int EPI, bool BIAS>
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ part, int ksplit, int64_t M,
+                                                            int64_t N, const float* __restrict__ bias,
+                                                            const __nv_bfloat16* __restrict__ aux,
+                                                            __nv_bfloat16* __restrict__ out) {
+    const int64_t n8 = N / 8, total = M * n8;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / n8, c = (i - r * n8) * 8;
+        float f[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int p = 0; p < ksplit; ++p) {
+            const float4* src = reinterpret_cast<const float4*>(part + ((size_t)p * M + r) * N + c);
+            const float4 u = __ldg(src), w = __ldg(src + 1);
+            f[0] += u.x, f[1] += u.y, f[2] += u.z, f[3] += u.w, f[4] += w.x, f[5] += w.y, f[6] += w.z, f[7] += w.w;
+        }
+        if constexpr (BIAS) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) f[j] += __ldg(bias + c + j);
+        }
+        if constexpr (EPI != EPI_NONE) {
+            float x[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            if constexpr (EPI == EPI_RESID || EPI == EPI_DTANH)
+                unpack<__nv_bfloat16>(__ldg(reinterpret_cast<const uint4*>(aux + r * N + c)), x);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) f[j] = epi_apply<EPI>(f[j], x[j]);
+        }
+        uint4 o;
+        o.x = pack_bf16x2(f[0], f[1]);
+        o.y = pack_bf16x2(f[2], f[3]);
+        o.z = pack_bf16x2(f[4], f[5]);
+        o.w = pack_bf16x2(f[6], f[7]);
+        *reinterpret_cast<uint4*>(out + r * N + c) = o;
+    }
+}
 
 // BNT: output tile width, 256 (default) or 128 (skinny outputs: more tiles,
 // fewer idle SMs in the last wave; the ring then holds 6 stages in the same
 // shared memory)
-template <bool B_KMAJOR, bool BIAS, int EPI, int BNT = gm::BN>
+// SPLIT: split-K.  Work unit u = (tile u / ksplit, K part u % ksplit); the
+// epilogue stores the part's fp32 partial tile to a.part [ksplit][M][N] and
+// splitk_reduce_kernel sums the parts in order and applies bias / epilogue
+// (deterministic).  For outputs with few tiles and a long reduction (N = 768
+// at 8192 rows: 192 tiles = 1.3 waves on 148 SMs).
+template <bool B_KMAJOR, bool BIAS, int EPI, int BNT = gm::BN, bool SPLIT = false>
 __global__ void __launch_bounds__(gm::THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
                 const __grid_constant__ CUtensorMap tmo, GemmArgs a) {
@@ -127,8 +169,14 @@ __global__ void __launch_bounds__(gm::THREADS, 1)
     unsigned char* obox = smem + (size_t)gm::STAGES * gm::STAGE_BYTES + 1024;  // [EPI_WARPS][32 rows][128 B], 1 KB aligned
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int ntiles = a.tiles_m * a.tiles_n;
-    const int kblocks = (a.Kr + BK - 1) / BK;
+    const int ksplit = SPLIT ? a.ksplit : 1;
+    const int ntiles = a.tiles_m * a.tiles_n * ksplit;  // work units
+    const int kblocks_all = (a.Kr + BK - 1) / BK;
+    auto krange = [&](int u, int& kb0, int& kb1) {
+        const int p = SPLIT ? u % ksplit : 0;
+        kb0 = (int)((int64_t)kblocks_all * p / ksplit);
+        kb1 = (int)((int64_t)kblocks_all * (p + 1) / ksplit);
+    };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -158,10 +206,11 @@ __global__ void __launch_bounds__(gm::THREADS, 1)
             int s = 0;
             uint32_t ph = 0;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-                int mt, nt;
-                tile_mn(t, a.tiles_m, a.tiles_n, mt, nt);
+                int mt, nt, kb0, kb1;
+                tile_mn(t / ksplit, a.tiles_m, a.tiles_n, mt, nt);
+                krange(t, kb0, kb1);
                 const int m0 = mt * BM, n0 = nt * BN;
-                for (int kb = 0; kb < kblocks; ++kb) {
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&empty[s], ph ^ 1u);
                     unsigned char* st = ring + (size_t)s * STAGE_BYTES;
                     mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
@@ -191,7 +240,9 @@ __global__ void __launch_bounds__(gm::THREADS, 1)
                 mbar_wait(&tempty[buf], tph ^ 1u);  // epilogue drained this accumulator
                 tc::fence_after_sync();
                 const uint32_t dcol = tmem + (uint32_t)(buf * BN);
-                for (int kb = 0; kb < kblocks; ++kb) {
+                int kb0, kb1;
+                krange(t, kb0, kb1);
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&full[s], ph);
                     tc::fence_after_sync();
                     const uint32_t abase = smem_u32(ring + (size_t)s * STAGE_BYTES);
@@ -204,7 +255,7 @@ __global__ void __launch_bounds__(gm::THREADS, 1)
                         const uint64_t ad = tc::smem_desc_sw128(abase + k * 32, 16, 1024);
                         const uint64_t bd = B_KMAJOR ? tc::smem_desc_sw128(bbase + k * 32, 16, 1024)
                                                      : tc::smem_desc_sw128(bbase + k * 2048, 8192, 1024);
-                        tc::mma_bf16(dcol, ad, bd, idesc, (kb | k) != 0);
+                        tc::mma_bf16(dcol, ad, bd, idesc, (kb != kb0) || (k != 0));
                     }
                     tc::commit(&empty[s]);  // smem slot free once these MMAs retire
                     if (++s == STAGES) {
@@ -234,17 +285,46 @@ __global__ void __launch_bounds__(gm::THREADS, 1)
         uint32_t tph = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
             int mt, nt;
-            tile_mn(t, a.tiles_m, a.tiles_n, mt, nt);
+            tile_mn(t / ksplit, a.tiles_m, a.tiles_n, mt, nt);
             const int m0 = mt * BM, n0 = nt * BN;
             const int row = m0 + quad * 32 + lane;
             mbar_wait(&tfull[buf], tph);
             tc::fence_after_sync();
             const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN + half * (BN / 2));
+            if constexpr (SPLIT) {  // fp32 partial tile of this K part: plain 16-byte stores
+                float* prow = a.part + ((size_t)(t % ksplit) * a.M + row) * a.N;
+#pragma unroll
+                for (int cc = 0; cc < BN / 64; ++cc) {
+                    uint32_t r[32];
+                    tc::tmem_ld_32x32b_x32(base + cc * 32, r);
+                    tc::tmem_ld_wait();
+                    if (cc == BN / 64 - 1) {
+                        tc::fence_before_sync();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&tempty[buf]);
+                    }
+                    const int c0 = n0 + half * (BN / 2) + cc * 32;
+                    if (row < a.M) {
+#pragma unroll
+                        for (int v = 0; v < 8; ++v)
+                            if (c0 + 4 * v < a.N)
+                                *reinterpret_cast<float4*>(prow + c0 + 4 * v) =
+                                    make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                                                __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+                    }
+                }
+                if (++buf == 2) {
+                    buf = 0;
+                    tph ^= 1u;
+                }
+                continue;
+            }
 #pragma unroll
             for (int gi = 0; gi < BN / 128; ++gi) {
-                // the previous TMA store from this box has finished reading it
-                if (lane == 0) bulk_wait_read0();
-                __syncwarp();
+                // TMEM -> registers -> bf16 first; only then wait for the previous
+                // TMA store from this box to finish reading it (the wait overlaps
+                // the TMEM loads and the epilogue arithmetic)
+                uint4 o[2][4];
 #pragma unroll
                 for (int c2 = 0; c2 < 2; ++c2) {
                     const int cc = gi * 2 + c2;
@@ -276,15 +356,21 @@ __global__ void __launch_bounds__(gm::THREADS, 1)
 #pragma unroll
                             for (int j = 0; j < 8; ++j) f[j] = epi_apply<EPI>(f[j], x[j]);
                         }
-                        uint4 o;
-                        o.x = pack_bf16x2(f[0], f[1]);
-                        o.y = pack_bf16x2(f[2], f[3]);
-                        o.z = pack_bf16x2(f[4], f[5]);
-                        o.w = pack_bf16x2(f[6], f[7]);
-                        const int chunk = c2 * 4 + v;  // 16-byte chunk of the 128-byte box row
-                        *reinterpret_cast<uint4*>(box + lane * 128 + ((chunk ^ (lane & 7)) << 4)) = o;
+                        o[c2][v].x = pack_bf16x2(f[0], f[1]);
+                        o[c2][v].y = pack_bf16x2(f[2], f[3]);
+                        o[c2][v].z = pack_bf16x2(f[4], f[5]);
+                        o[c2][v].w = pack_bf16x2(f[6], f[7]);
                     }
                 }
+                if (lane == 0) bulk_wait_read0();
+                __syncwarp();
+#pragma unroll
+                for (int c2 = 0; c2 < 2; ++c2)
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        const int chunk = c2 * 4 + v;  // 16-byte chunk of the 128-byte box row
+                        *reinterpret_cast<uint4*>(box + lane * 128 + ((chunk ^ (lane & 7)) << 4)) = o[c2][v];
+                    }
                 fence_proxy_async_smem();  // generic-proxy writes -> visible to the TMA (async proxy)
                 __syncwarp();
                 if (lane == 0) {
@@ -670,6 +756,42 @@ cudaError_t launch_tc_bn(const CUtensorMap& ma, const CUtensorMap& mb, const CUt
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, gemm_kernel<BK_, BIAS, EPI, BNT>, ma, mb, mo, a);
 }
+template <bool BK_>
+cudaError_t launch_tc_split(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo, const GemmArgs& a,
+                            int units, cudaStream_t st) {
+    const void* fn = reinterpret_cast<const void*>(gemm_kernel<BK_, false, EPI_NONE, 256, true>);
+    cudaError_t e = ensure_smem_attr(fn, gm::SMEM);
+    if (e != cudaSuccess) return e;
+    const int sms = device_sm_count();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(units < sms ? units : sms);
+    cfg.blockDim = dim3(gm::THREADS);
+    cfg.dynamicSmemBytes = gm::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, gemm_kernel<BK_, false, EPI_NONE, 256, true>, ma, mb, mo, a);
+}
+template <int EPI, bool BIAS>
+cudaError_t launch_splitk_reduce(const GemmArgs& a, cudaStream_t st) {
+    splitk_reduce_kernel<EPI, BIAS><<<device_sm_count() * 4, 256, 0, st>>>(a.part, a.ksplit, a.M, a.N, a.bias, a.aux,
+                                                                         a.out);
+    return cudaGetLastError();
+}
+// split-K parts: only for long reductions whose tile count leaves the last
+// wave mostly idle (the partials cost an extra fp32 write + read of the output)
+int gemm_pick_split(int64_t tiles, int64_t kblocks) {
+    const int sms = device_sm_count();
+    auto eff = [&](int64_t t) { return (double)t / (double)(((t + sms - 1) / sms) * sms); };
+    if (kblocks < 64 || eff(tiles) >= 0.8) return 1;
+    for (int k = 2; k <= 4; ++k)
+        if (eff(tiles * k) >= 0.85 && kblocks / k >= 16) return k;
+    return kblocks / 4 >= 16 ? 4 : 1;
+}
+
 template <bool BK_, bool BIAS, int EPI>
 cudaError_t launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo, const GemmArgs& a,
                       cudaStream_t st, int bn) {
@@ -805,6 +927,29 @@ cudaError_t launch_linear_gemm(int kind, int epi, int dt, int w_dt, const void* 
         a.bias = static_cast<const float*>(bias);
         a.aux = static_cast<const __nv_bfloat16*>(aux);
         a.out = static_cast<__nv_bfloat16*>(out);
+        const int ks = bn == 256 ? gemm_pick_split((int64_t)a.tiles_m * a.tiles_n, (Kr + gm::BK - 1) / gm::BK) : 1;
+        if (ks > 1 && std::getenv("GNSB_GEMM_NOSPLIT") == nullptr) {
+            cudaMemPool_t pool;
+            void* scratch = nullptr;
+            cudaError_t e = scratch_pool(&pool);
+            if (e == cudaSuccess) e = cudaMallocFromPoolAsync(&scratch, (size_t)ks * rows * N * 4, pool, st);
+            if (e != cudaSuccess) return e;
+            a.ksplit = ks;
+            a.part = static_cast<float*>(scratch);
+            const int units = a.tiles_m * a.tiles_n * ks;
+            e = kind == 1 ? launch_tc_split<true>(ma, mb, mo, a, units, st)
+                          : launch_tc_split<false>(ma, mb, mo, a, units, st);
+            if (e == cudaSuccess) {
+                switch (epi) {
+                    case EPI_TANH: e = bias ? launch_splitk_reduce<EPI_TANH, true>(a, st) : launch_splitk_reduce<EPI_TANH, false>(a, st); break;
+                    case EPI_RESID: e = bias ? launch_splitk_reduce<EPI_RESID, true>(a, st) : launch_splitk_reduce<EPI_RESID, false>(a, st); break;
+                    case EPI_DTANH: e = launch_splitk_reduce<EPI_DTANH, false>(a, st); break;
+                    default: e = bias ? launch_splitk_reduce<EPI_NONE, true>(a, st) : launch_splitk_reduce<EPI_NONE, false>(a, st);
+                }
+            }
+            const cudaError_t f = cudaFreeAsync(scratch, st);
+            return e != cudaSuccess ? e : f;
+        }
         if (kind == 1) {
             if (epi == EPI_DTANH) return launch_tc<true, false, EPI_DTANH>(ma, mb, mo, a, st, bn);
             return launch_tc<true, false, EPI_NONE>(ma, mb, mo, a, st, bn);

@@ -35,7 +35,9 @@ def _check(out, ref):
     assert close(o, r, RT, atol), float(np.max(np.abs(o - r)))
 
 
-SHAPES = [(7, 8, 8), (128, 256, 256), (300, 136, 264), (1000, 520, 72), (257, 64, 1032), (2048, 1024, 4096)]
+SHAPES = [(7, 8, 8), (128, 256, 256), (300, 136, 264), (1000, 520, 72), (257, 64, 1032), (2048, 1024, 4096),
+          # split-K (few tiles, long reduction): dx of N = 264 over L = 8200, forward of N = 520 over K = 6000
+          (1000, 264, 8200), (900, 6000, 520)]
 
 
 @pytest.mark.parametrize("rows,K,L", SHAPES)
