@@ -50,12 +50,16 @@ def _bmk(t: torch.Tensor):
     return int(t.shape[0]), m, int(t.shape[-1])
 
 
-def linear_backward_simultaneous(layer: LinearLayer, x: torch.Tensor, g: torch.Tensor, form: str = "weight_grad",
+def linear_backward_simultaneous(layer: LinearLayer, x: torch.Tensor, g: torch.Tensor, form: str = "auto",
                                  need_input_grad: bool = True) -> LinearBackwardResult:
     """Weight (and bias) gradients plus corrected per-example squared norms.
 
     g must be the gradient of a mean-reduced loss over the B leading-axis
     examples (layers.hpp:66-69).  Middle axes are collapsed (layers.cpp:19-28).
+    form: "auto" (default: the weight-gradient form, or for short sequences the
+    Gram form for the norms plus one plain dW pass -- the same outputs,
+    DESIGN §4) or "weight_grad" / "simultaneous" (always the weight-gradient
+    kernel).  The norms-only Gram form is linear_perexample_sqnorm_frobenius.
     """
     K, L = int(layer.weight.shape[0]), int(layer.weight.shape[1])
     if x.dim() != g.dim():

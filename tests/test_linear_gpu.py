@@ -91,7 +91,7 @@ def test_tcgen05_weight_grad_form_matches_oracle(orc, cuda, monkeypatch, impl, B
     np.testing.assert_array_equal(x.float().cpu().numpy(), xo)
     np.testing.assert_array_equal(g.float().cpu().numpy(), go)
     r = linear.linear_backward_simultaneous(linear.LinearLayer(torch.zeros(K, L, device=cuda)), x, g,
-                                            need_input_grad=False)
+                                            form="weight_grad", need_input_grad=False)
     ref = _oracle_linear(orc, x, g)
     torch.cuda.synchronize()
     dW = r.grads.weight_grads["weight"].double().cpu().numpy()
@@ -152,7 +152,7 @@ def test_weight_grad_form_equals_gram_form(cuda):
     B, T, K, L = 2, 64, 128, 256
     x, g = m.synth_linear(B, T, K, L, torch.bfloat16, cuda)
     r = linear.linear_backward_simultaneous(linear.LinearLayer(torch.zeros(K, L, device=cuda)), x, g,
-                                            need_input_grad=False)
+                                            form="weight_grad", need_input_grad=False)
     f = linear.linear_perexample_sqnorm_frobenius(x, g)
     assert close(f.cpu().numpy(), r.grads.per_example_sqnorms_raw["weight"].cpu().numpy(), 1e-4)
 
