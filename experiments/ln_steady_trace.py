@@ -32,6 +32,7 @@ Ds = [int(v) for v in sys.argv[1].split(",")] if len(sys.argv) > 1 else [1024, 2
 NL = int(sys.argv[2]) if len(sys.argv) > 2 else 8
 PLAIN = "--plain" in sys.argv
 NOTRACE = "--notrace" in sys.argv  # timing only (the per-stage stamps perturb the kernel)
+NORED = "--noreduce" in sys.argv  # row passes only (the grouped reduce's share of the step)
 SMS = torch.cuda.get_device_properties(dev).multi_processor_count
 P = lambda t: ctypes.c_void_p(t.data_ptr())
 
@@ -60,7 +61,8 @@ for D in Ds:
                                     Bv, Mv, D, P(L["ws"]), L["ws"].numel(), sp,
                                     None if NOTRACE else P(L["trace"]))
             assert rc == 0, rc
-        assert lib.gnsb_ln_bwd_reduce(pend, NL, 0 if PLAIN else 1, sp) == 0
+        if not NORED:
+            assert lib.gnsb_ln_bwd_reduce(pend, NL, 0 if PLAIN else 1, sp) == 0
 
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
@@ -82,7 +84,7 @@ for D in Ds:
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 10
     nbytes = B * T * D * 6 + 8 * B * T
-    print(f"[{LIBTAG or 'wt'}] D={D} {'plain' if PLAIN else 'fused'}: step {ms*1e3:.1f} us for {NL} layers -> "
+    print(f"[{LIBTAG or 'wt'}] D={D} {'plain' if PLAIN else 'fused'}{' noreduce' if NORED else ''}: step {ms*1e3:.1f} us for {NL} layers -> "
           f"{NL*nbytes/ms/1e6:.0f} GB/s ({NL*nbytes/ms/1e6/6558.1*100:.1f} % of 6558)")
     if NOTRACE:
         continue
@@ -105,6 +107,13 @@ for D in Ds:
     cc = [float(np.corrcoef(dur[l], dur[l + 1])[0, 1]) for l in range(len(trs) - 1)]
     print(f"  per-CTA row time corr(layer l, l+1): {' '.join(f'{c:.2f}' for c in cc)}")
     print(f"  slowest CTAs L1: {np.argsort(-dur[1])[:12].tolist()}  L5: {np.argsort(-dur[5 % len(trs)])[:12].tolist()}")
+    rows = [(c * Bv * Mv // SMS, (c + 1) * Bv * Mv // SMS) for c in range(SMS)]
+    bnd = np.array([(r1 - 1) // Mv != r0 // Mv for r0, r1 in rows])
+    mdur = dur.mean(0)
+    print(f"  mean row time: CTAs with an example boundary {mdur[bnd].mean():.2f} us (n={int(bnd.sum())}, "
+          f"max {mdur[bnd].max():.2f}), without {mdur[~bnd].mean():.2f} us (n={int((~bnd).sum())}, max {mdur[~bnd].max():.2f})")
+    fold = np.array([(tr[:, 2] - tr[:, 1]) / 1000.0 for tr in trs]).mean(0)
+    print(f"  mean fold time: boundary CTAs {fold[bnd].mean():.2f} us, others {fold[~bnd].mean():.2f} us")
     print(f"  row time min/med/max per layer: " + " | ".join(f"{d.min():.1f}/{np.median(d):.1f}/{d.max():.1f}" for d in dur))
     for L in layers:
         L.clear()

@@ -80,7 +80,7 @@ struct LnRedArgs {
 };
 
 template <typename T, int GW, int VPT, int G, int RPG, bool PROD_ = true, int KEEP_ = -1, int CPS_ = 1,
-          bool PARK_ = false, bool NOFOLD_ = false>
+          bool PARK_ = false, bool NOFOLD_ = false, bool WIDE_ = true>
 struct LnBwdCfg {
     using Acc = typename Traits<T>::Acc;
     using Row = T;
@@ -93,6 +93,9 @@ struct LnBwdCfg {
     // of the row pass's critical path into the once-per-step reduce)
     static constexpr bool kNoFold = NOFOLD_ && G > 1 && !kPark;
     static constexpr int kSub = kNoFold ? G : 1;  // sub-slots stage 2 reads per (cta + example)
+    // kWide: partial slots are written with 16-byte stores (see write_slot);
+    // off where the register quads they need push the row loop into spills
+    static constexpr bool kWide = WIDE_;
     static constexpr int kWarps = GW * G;        // row-math warps
     static constexpr int kThreads = (kWarps + (PROD ? 1 : 0)) * 32;
     // registers are allocated for warps in groups of 4: bound the register
@@ -305,14 +308,27 @@ __global__ void __launch_bounds__(C::kBoundThreads, C::kCps) ln_bwd_kernel(LnBwd
     auto write_slot = [&](int64_t ex, bool zero) {
         Acc* base = (C::kPark && ex == ex_first) ? park + (size_t)g * 2 * Dp
                                                    : partial + ((size_t)(cta + ex) * G + g) * 2 * Dp;
+        // 16-byte stores: a thread's vector is contiguous and Dp is a multiple
+        // of the vector width.  8-byte pair stores (one 8-byte piece in each
+        // of 32 sectors per warp store, twice as many stores) clog the CTA's
+        // load/store pipe at an example boundary: boundary-crossing CTAs ran
+        // ~1.5 us longer at D = 1024 and set the launch's tail.
+        constexpr int PPC = C::kWide ? 16 / (int)sizeof(P) : 1;  // pairs per store
 #pragma unroll
         for (int k = 0; k < VPT; ++k) {
             if (!vok[k]) continue;
 #pragma unroll
-            for (int p = 0; p < NP; ++p) {
-                const P z = PR::splat(Acc(0));
-                *reinterpret_cast<P*>(base + vo[k] + 2 * p) = zero ? z : ag[k][p];
-                *reinterpret_cast<P*>(base + (size_t)Dp + vo[k] + 2 * p) = zero ? z : ab[k][p];
+            for (int c = 0; c < NP / PPC; ++c) {
+                Acc* dg = base + vo[k] + 2 * PPC * c;
+                Acc* db = dg + Dp;
+                if constexpr (PPC == 1) {
+                    *reinterpret_cast<P*>(dg) = zero ? PR::splat(Acc(0)) : ag[k][c];
+                    *reinterpret_cast<P*>(db) = zero ? PR::splat(Acc(0)) : ab[k][c];
+                } else {
+                    const uint4 z = make_uint4(0, 0, 0, 0);
+                    *reinterpret_cast<uint4*>(dg) = zero ? z : pack2<Acc>(&ag[k][PPC * c]);
+                    *reinterpret_cast<uint4*>(db) = zero ? z : pack2<Acc>(&ab[k][PPC * c]);
+                }
             }
         }
     };
@@ -519,10 +535,17 @@ __global__ void __launch_bounds__(C::kBoundThreads, C::kCps) ln_bwd_kernel(LnBwd
 #pragma unroll
             for (int k = 0; k < VPT; ++k) {
                 if (tig + k * GT >= NVp) continue;
+                constexpr int PPC = C::kWide ? 16 / (int)sizeof(P) : 1;
 #pragma unroll
-                for (int p = 0; p < NP; ++p) {
-                    *reinterpret_cast<P*>(fb + (tig + k * GT) * W + 2 * p) = ag[k][p];
-                    *reinterpret_cast<P*>(fb + Dp + (tig + k * GT) * W + 2 * p) = ab[k][p];
+                for (int c = 0; c < NP / PPC; ++c) {
+                    Acc* dg = fb + (tig + k * GT) * W + 2 * PPC * c;
+                    if constexpr (PPC == 1) {
+                        *reinterpret_cast<P*>(dg) = ag[k][c];
+                        *reinterpret_cast<P*>(dg + Dp) = ab[k][c];
+                    } else {
+                        *reinterpret_cast<uint4*>(dg) = pack2<Acc>(&ag[k][PPC * c]);
+                        *reinterpret_cast<uint4*>(dg + Dp) = pack2<Acc>(&ab[k][PPC * c]);
+                    }
                 }
             }
         }

@@ -389,7 +389,9 @@ R dispatch_bwd(int64_t D, const char** why, R bad, A&&... args) {
     if (nv <= 256) {
         if (!ln_fold()) return Op<LnBwdCfg<T, 8, 1, 2, 2, true, -1, 1, false, true>>::call(args...);
         if (ln_park()) return Op<LnBwdCfg<T, 8, 1, 2, 2, true, -1, 1, true>>::call(args...);
-        return Op<LnBwdCfg<T, 8, 1, 2, 2, true>>::call(args...);
+        // (8-byte slot stores: the 16-byte ones spill this 17-warp configuration's
+        // row loop and cost 9 % at D = 2048)
+        return Op<LnBwdCfg<T, 8, 1, 2, 2, true, -1, 1, false, false, false>>::call(args...);
     }
     if (nv <= 512) return Op<LnBwdCfg<T, 8, 2, 1, 2, true, 1>>::call(args...);
     // 11 consumer warps x 3 vectors (3 % of the lanes idle at D=8192): 12 warps leave
