@@ -25,6 +25,7 @@ sw = ctypes.CDLL(os.path.join(ROOT, "experiments", f"libln_sweep_{LIBTAG}.so" if
 _vp, _i64 = ctypes.c_void_p, ctypes.c_int64
 sw.sweep_rows_prod.argtypes = [_vp] * 6 + [_i64, _i64, _i64, _vp, ctypes.c_size_t, _vp, _vp]
 sw.sweep_rows_prod.restype = ctypes.c_int
+sw.sweep_reduce.restype = ctypes.c_int
 lib = _lib.lib()
 dev = torch.device("cuda")
 B, T = 32, 1024
@@ -32,7 +33,8 @@ Ds = [int(v) for v in sys.argv[1].split(",")] if len(sys.argv) > 1 else [1024, 2
 NL = int(sys.argv[2]) if len(sys.argv) > 2 else 8
 PLAIN = "--plain" in sys.argv
 NOTRACE = "--notrace" in sys.argv  # timing only (the per-stage stamps perturb the kernel)
-NORED = "--noreduce" in sys.argv  # row passes only (the grouped reduce's share of the step)
+NORED = "--noreduce" in sys.argv
+REDTRACE = "--redtrace" in sys.argv  # per-CTA stamps of the grouped reduce  # row passes only (the grouped reduce's share of the step)
 SMS = torch.cuda.get_device_properties(dev).multi_processor_count
 P = lambda t: ctypes.c_void_p(t.data_ptr())
 
@@ -54,6 +56,8 @@ for D in Ds:
         _lib.LnBwdPending(L["ws"].data_ptr(), L["ws"].numel(), Bv, Mv, D, 1, L["dg"].data_ptr(), L["db"].data_ptr(),
                           L["rg"].data_ptr(), L["rb"].data_ptr(), L["sums"].data_ptr()) for L in layers])
 
+    rtrace = torch.zeros(4 * SMS * 6, dtype=torch.int64, device=dev)
+
     def step():
         sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
         for L in layers:
@@ -61,7 +65,14 @@ for D in Ds:
                                     Bv, Mv, D, P(L["ws"]), L["ws"].numel(), sp,
                                     None if NOTRACE else P(L["trace"]))
             assert rc == 0, rc
-        if not NORED:
+        if NORED:
+            return
+        if REDTRACE:
+            arr = lambda key: (ctypes.c_void_p * NL)(*[L[key].data_ptr() for L in layers])
+            meta = (ctypes.c_int64 * (3 * NL))(*([Bv, Mv, D] * NL))
+            assert sw.sweep_reduce(NL, meta, arr("ws"), arr("dg"), arr("db"), arr("rg"), arr("rb"), arr("sums"),
+                                   0 if PLAIN else 1, sp, P(rtrace)) == 0
+        else:
             assert lib.gnsb_ln_bwd_reduce(pend, NL, 0 if PLAIN else 1, sp) == 0
 
     s = torch.cuda.Stream()
@@ -86,6 +97,18 @@ for D in Ds:
     nbytes = B * T * D * 6 + 8 * B * T
     print(f"[{LIBTAG or 'wt'}] D={D} {'plain' if PLAIN else 'fused'}{' noreduce' if NORED else ''}: step {ms*1e3:.1f} us for {NL} layers -> "
           f"{NL*nbytes/ms/1e6:.0f} GB/s ({NL*nbytes/ms/1e6/6558.1*100:.1f} % of 6558)")
+    if REDTRACE:
+        g.replay()
+        torch.cuda.synchronize()
+        rt = rtrace.view(-1, 6).cpu().numpy().astype(np.int64)
+        rt = rt[rt[:, 0] > 0]
+        t0 = rt[:, 0].min()
+        r = (rt - t0) / 1000.0
+        q = lambda a: f"{np.min(a):6.2f}/{np.median(a):6.2f}/{np.max(a):6.2f}"
+        last = r[rt[:, 3] > 0]
+        print(f"  reduce ({len(rt)} CTAs, us from first wait exit, min/med/max): wait-exit {q(r[:,0])} "
+              f"first-stage {q(r[:,1])} items {q(r[:,5])} main-end {q(r[:,2])} | last CTAs: start {q(last[:,3])} end {q(last[:,4])}")
+        rtrace.zero_()
     if NOTRACE:
         continue
     g.replay()

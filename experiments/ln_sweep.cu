@@ -95,6 +95,31 @@ int sweep_desc(int id, int* out) {
     return -1;
 }
 
+// the production grouped stage 2 (ln_bwd_reduce_run) of n bf16 LayerNorms of
+// extents meta[3l..3l+2] = (B, M, D), with per-CTA trace stamps ([total CTAs][6])
+int sweep_reduce(int n, const int64_t* meta, void* const* ws, void* const* dgamma, void* const* dbeta,
+                 double* const* rg, double* const* rb, double* const* sums, int norms, void* stream,
+                 unsigned long long* trace) {
+    std::vector<LnRedItem> items(n);
+    for (int l = 0; l < n; ++l) {
+        LnRedItem& it = items[l];
+        const char* why = nullptr;
+        if (ln_bwd_plan_info<bf>(meta[3 * l], meta[3 * l + 1], meta[3 * l + 2], &it.info, &why)) return 1;
+        it.B = meta[3 * l];
+        it.M = meta[3 * l + 1];
+        it.D = meta[3 * l + 2];
+        it.ws = ws[l];
+        it.dgamma = dgamma[l];
+        it.dbeta = dbeta[l];
+        it.raw_g = rg[l];
+        it.raw_b = rb[l];
+        it.sums = sums[l];
+    }
+    const char* why = nullptr;
+    cudaError_t ce = cudaSuccess;
+    return ln_bwd_reduce_run(0, norms, items.data(), n, (cudaStream_t)stream, trace, &why, &ce);
+}
+
 // the production row-pass dispatch (ln_bwd_rows_run) with per-CTA trace stamps
 int sweep_rows_prod(const void* x, const void* mean, const void* rstd, const void* dy, const void* gamma, void* dx,
                     int64_t B, int64_t M, int64_t D, void* ws, size_t wsb, void* stream, unsigned long long* trace) {

@@ -633,6 +633,14 @@ __device__ __forceinline__ void ln_bwd_reduce_body(const LnRedArgs& a, const int
     };
 
     for (int j = threadIdx.x; j < 2 * ncol; j += nthreads) colsum[j] = 0.0;
+    __shared__ __align__(8) uint64_t s_bar;  // stage-area bulk copies
+    uint32_t bar_phase = 0;
+    const uint64_t pol = policy_evict_first();
+    if (threadIdx.x == 0) {
+        mbar_init(&s_bar, 1);
+        fence_mbar_init();
+    }
+    // (the barrier before the first staging orders the init before any use)
     // the next kernel in the stream may start its prologue now (it waits for
     // this grid before touching global memory)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -658,53 +666,62 @@ __device__ __forceinline__ void ln_bwd_reduce_body(const LnRedArgs& a, const int
         const int64_t nsl = s_hi - s_lo + 1;
         for (int64_t c0 = 0; c0 < nsl; c0 += a.slot_cap) {
             const int64_t cn = (nsl - c0) < a.slot_cap ? (nsl - c0) : a.slot_cap;
-            const int nvec = (int)cn * 2 * nu;  // < 2^31: bounded by the smem block
             const uint4* pbase = part + (s_lo + c0) * sstride + u0;
-            // stage: independent 16-byte loads, 8 per thread in flight
-            for (int i0 = threadIdx.x; i0 < nvec; i0 += 8 * nthreads) {
-                uint4 v[8];
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const int i = i0 + k * nthreads;
-                    if (i < nvec) {
-                        const int sl = i / (2 * nu), rem = i - sl * 2 * nu;
-                        const int h = rem >= nu ? 1 : 0, u = rem - h * nu;
-                        v[k] = __ldcg(pbase + (int64_t)sl * sstride + h * half + u);
-                    }
-                }
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const int i = i0 + k * nthreads;
-                    if (i < nvec) stg[i] = v[k];
-                }
-            }
+            // stage: one bulk copy (TMA) per (slot, half) column slice, all in
+            // flight at once and completing on one mbarrier.  (16-byte loads,
+            // 8 per thread in flight, left the grouped reduce latency-bound at
+            // ~1-1.6 TB/s.)  The fence orders the previous chunk's generic
+            // reads of the stage area before these async-proxy writes.
+            const int nchunk = (int)cn * 2;
+            const uint32_t cbytes = (uint32_t)nu * 16u;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if (threadIdx.x == 0) mbar_arrive_expect_tx(&s_bar, (uint32_t)nchunk * cbytes);
             __syncthreads();
+            for (int c = threadIdx.x; c < nchunk; c += nthreads)
+                bulk_g2s(stg + (size_t)c * nu, pbase + (int64_t)(c >> 1) * sstride + (c & 1) * half, cbytes, &s_bar,
+                         pol);
+            mbar_wait(&s_bar, bar_phase);
+            bar_phase ^= 1u;
             if (b0 == 0 && c0 == 0) stamp(1);
-            // per (example, column): fixed-order sum over the example's CTAs
-            const int items = (int)nb * ncol;
+            // per (example, column pair): fixed-order sum over the example's
+            // CTAs (two columns per thread: pair loads, 4 independent chains)
+            const int hc = ncol / 2;  // ncol is a multiple of the 16-byte vector width
+            const int items = (int)nb * hc;
             const Acc* sa = reinterpret_cast<const Acc*>(stg);
+            using A2 = typename Pair<Acc>::P;
             for (int it = threadIdx.x; it < items; it += nthreads) {
-                const int bb = it / ncol;
-                const int j = it - bb * ncol;
+                const int bb = it / hc;
+                const int j = 2 * (it - bb * hc);
                 const int64_t lo = s_cs[bb] > c0 ? s_cs[bb] : c0;
                 const int64_t hi = (s_cs[bb] + s_nc[bb]) < (c0 + cn) ? (s_cs[bb] + s_nc[bb]) : (c0 + cn);
-                double vg = c0 == 0 ? 0.0 : sv[bb * svs + j];
-                double vb = c0 == 0 ? 0.0 : sv[bb * svs + ncol + j];
+                double* o = sv + (size_t)bb * svs + j;
+                double g0 = c0 == 0 ? 0.0 : o[0], g1 = c0 == 0 ? 0.0 : o[1];
+                double e0 = c0 == 0 ? 0.0 : o[ncol], e1 = c0 == 0 ? 0.0 : o[ncol + 1];
                 const Acc* sg = sa + (size_t)(lo - c0) * 2 * ncol + j;
-                for (int64_t c = 0; c < hi - lo; ++c) {
-                    vg += (double)sg[c * 2 * ncol];
-                    vb += (double)sg[c * 2 * ncol + ncol];
+                const int n = (int)(hi - lo);
+#pragma unroll 4
+                for (int c = 0; c < n; ++c) {
+                    const A2 vg = *reinterpret_cast<const A2*>(sg + (size_t)c * 2 * ncol);
+                    const A2 vb = *reinterpret_cast<const A2*>(sg + (size_t)c * 2 * ncol + ncol);
+                    g0 += (double)vg.x;
+                    g1 += (double)vg.y;
+                    e0 += (double)vb.x;
+                    e1 += (double)vb.y;
                 }
-                sv[bb * svs + j] = vg;
-                sv[bb * svs + ncol + j] = vb;
+                o[0] = g0;
+                o[1] = g1;
+                o[ncol] = e0;
+                o[ncol + 1] = e1;
             }
             __syncthreads();
+            if (b0 == 0 && c0 == 0) stamp(5);
         }
         // two roles over the same read-only sv (no barrier between them): a
         // thread per column adds it over the block's examples; a warp per
         // example squares and sums it over this CTA's columns (lane-strided,
         // then a fixed butterfly: the chain per lane is ncol/16 long, not
-        // 2 ncol).  Both in fixed order.
+        // 2 ncol).  Both in fixed order.  (A warp per two examples and four
+        // lanes per column sum were both measured slower at D >= 2048.)
         for (int j = threadIdx.x; j < 2 * ncol; j += nthreads) {
             const int h = j / ncol, jj = j - h * ncol;
             double acc = 0.0;

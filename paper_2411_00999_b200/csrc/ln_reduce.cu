@@ -156,7 +156,7 @@ int reduce_run_t(int norms, const LnRedItem* items, int n, cudaStream_t st, unsi
         g.n = n;
         int b = 0;
         for (int l = 0; l < n; ++l) {
-            g.items[l] = red_args(items[l], shapes[l], nullptr);
+            g.items[l] = red_args(items[l], shapes[l], trace ? trace + (size_t)b * 6 : nullptr);
             g.begin[l] = b;
             b += alloc[l];
         }
