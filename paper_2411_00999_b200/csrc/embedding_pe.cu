@@ -214,7 +214,9 @@ __global__ void __launch_bounds__(kEmbThreads) emb_table_kernel(int64_t B, int64
 //     each it sums the run's token rows (token order, lanes over 16-byte
 //     column vectors; a one-token run needs no perm load) into dE_b[v], adds
 //     that to dW[v] and reduces ||dE_b[v]||^2 into q[b][k].  g is read once
-//     and dW written once, 16 bytes per lane per vector.
+//     and dW written once, 16 bytes per lane per vector.  (4-column lane
+//     vectors for bf16 -- one float4 of dW per lane, 512 contiguous bytes per
+//     warp store -- measured slower: 81 against 75 us at GPT-2 size.)
 //   * emb_raw_kernel: raw_b = sum_k q[b][k] (one CTA per example, fixed-order
 //     tree); the scalar sums by fold_rows_kernel.
 // dW matches the original path bit for bit (same per-example Acc sums, added
@@ -446,8 +448,11 @@ __global__ void __launch_bounds__(kEmbSortThreads) emb_sort_kernel(const int32_t
     if (tid == 0) w.U[b] = total;
 }
 
+#ifndef GNSB_EMB_OCC
+#define GNSB_EMB_OCC 768  // resident threads per SM the row walk is compiled for (1024 = 64 registers spills: 93 against 76 us)
+#endif
 template <typename T, int NVC, int NG, int NT = kEmbRowsThreads>
-__global__ void __launch_bounds__(NT, 768 / NT) emb_rows_kernel(const T* g, int64_t B, int64_t Tn, int64_t V,
+__global__ void __launch_bounds__(NT, GNSB_EMB_OCC / NT) emb_rows_kernel(const T* g, int64_t B, int64_t Tn, int64_t V,
                                                                 int64_t D, EmbFastWs w, float* dW) {
     constexpr int W = Traits<T>::W;
     constexpr int NP = W / 2;
@@ -763,8 +768,14 @@ cudaError_t emb_fast_run(const int32_t* ids, const void* g, void* dW, double* ra
         launch(std::integral_constant<int, 2>{});
     else if (nvec <= 96)
         launch(std::integral_constant<int, 3>{});
-    else
+    else if constexpr (sizeof(T) != 4)  // (bf16: 16 accumulator registers per vector, at most 4)
         launch(std::integral_constant<int, 4>{});
+    else if (nvec <= 128)
+        launch(std::integral_constant<int, 4>{});
+    else if (nvec <= 192)  // fp32 rows at D = 768: one pass over the columns instead of two (94 -> 89 us)
+        launch(std::integral_constant<int, 6>{});
+    else
+        launch(std::integral_constant<int, 8>{});
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     emb_raw_kernel<<<(unsigned)B, 256, 0, st>>>(B, Tn, w, raw);

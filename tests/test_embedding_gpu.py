@@ -36,7 +36,10 @@ def test_fp64_matches_reference_golden_bitwise(golden, cuda):
                                              # the sort kernel's bucket sort (uniform ids) and its bitonic
                                              # fallback (one id fills a bucket: padding)
                                              (torch.bfloat16, 4, 4096, 50257, 64, "uniform"),
-                                             (torch.bfloat16, 3, 1024, 50257, 64, "pad")])
+                                             (torch.bfloat16, 3, 1024, 50257, 64, "pad"),
+                                             # fp32 rows wide enough for 6 and 8 column vectors per lane
+                                             (torch.float32, 2, 256, 3000, 768, "uniform"),
+                                             (torch.float32, 2, 128, 3000, 1000, "skew")])
 def test_matches_oracle(orc, cuda, dt, B, T, V, D, mode):
     from paper_2411_00999_b200.embedding import embedding_backward_simultaneous
 
