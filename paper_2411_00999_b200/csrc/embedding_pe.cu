@@ -20,6 +20,7 @@
 //     squares for ||dW||^2.
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <type_traits>
 
@@ -663,7 +664,16 @@ EmbFastLayout emb_fast_layout(int64_t B, int64_t Tn, int64_t V) {
     const int64_t blocks = (V + kRowsPerWarp - 1) / kRowsPerWarp;  // row blocks, one per warp
     const int64_t wpc = emb_rows_threads(B) / 32;
     const int64_t grid = (blocks + wpc - 1) / wpc;
-    const int64_t cap = (int64_t)sms * 16 * (kEmbRowsThreads / 32) / wpc;
+    int64_t cap = (int64_t)sms * 16 * (kEmbRowsThreads / 32) / wpc;
+    // One resident wave, grid-stride beyond it: warps never retire between row
+    // blocks, so no CTA waits on a predecessor's store drain (74 against 76 us
+    // with 1.8 waves of one-block warps at GPT-2 size).  GNSB_EMB_WAVES=k
+    // allows k waves (0 = one warp per block), A/B runs.
+    static const int waves = [] {
+        const char* e = std::getenv("GNSB_EMB_WAVES");
+        return e ? std::atoi(e) : 1;
+    }();
+    if (waves > 0) cap = std::min<int64_t>(cap, (int64_t)sms * (GNSB_EMB_OCC / (32 * wpc)) * waves);
     l.grid = (int)(grid < cap ? (grid > 0 ? grid : 1) : cap);
     size_t off = 0;
     auto take = [&](size_t bytes) {
