@@ -240,6 +240,10 @@ struct EmbFastWs {
     int32_t* bad;
     int32_t* blk;      // [B][nblk + 1]: first entry of example b with id >= j * kRowsPerWarp
     int64_t nblk;      // row blocks: ceil(V / kRowsPerWarp)
+    // mask walk (emb_mask_kernel) only; null for the cursor walk
+    uint32_t* mask;    // [V][mw]: bit b set when example b has a run at id v
+    int2* idx2;        // [V][B]: {run index r, first token | 0x80000000 when the run has > 1 token}
+    int mw;            // mask words per row: ceil(B / 32)
 };
 
 template <int NT>
@@ -435,17 +439,24 @@ __global__ void __launch_bounds__(kEmbSortThreads) emb_sort_kernel(const int32_t
             const uint32_t id = (uint32_t)(keys[i] >> SH);
             int e = i + 1;
             while (e < nvalid && (uint32_t)(keys[e] >> SH) == id) ++e;
-            ent[r] = make_int4((int)id, i, e - i, (int)(uint32_t)(keys[i] & TM));
-            // row blocks whose first row lies in (previous id, id] start at entry r
-            const int64_t j_lo = r == 0 ? 0 : (int64_t)((uint32_t)(keys[i - 1] >> SH) / kRowsPerWarp) + 1;
-            const int64_t j_hi = (int64_t)(id / kRowsPerWarp);
-            for (int64_t j = j_lo; j <= j_hi; ++j) blk[j] = r;
+            const int t0 = (int)(uint32_t)(keys[i] & TM);
+            ent[r] = make_int4((int)id, i, e - i, t0);
+            if (w.mask) {  // the mask walk: mark (id, b), record where its run lives
+                atomicOr(w.mask + (int64_t)id * w.mw + (b >> 5), 1u << (b & 31));
+                w.idx2[(int64_t)id * gridDim.x + b] = make_int2(r, e - i > 1 ? (int)(0x80000000u | (uint32_t)t0) : t0);
+            } else {
+                // row blocks whose first row lies in (previous id, id] start at entry r
+                const int64_t j_lo = r == 0 ? 0 : (int64_t)((uint32_t)(keys[i - 1] >> SH) / kRowsPerWarp) + 1;
+                const int64_t j_hi = (int64_t)(id / kRowsPerWarp);
+                for (int64_t j = j_lo; j <= j_hi; ++j) blk[j] = r;
+            }
             ++r;
         }
     }
     // blocks after the last id start past the end
     const int64_t j_tail = nvalid > 0 ? (int64_t)((uint32_t)(keys[nvalid - 1] >> SH) / kRowsPerWarp) + 1 : 0;
-    for (int64_t j = j_tail + tid; j <= w.nblk; j += blockDim.x) blk[j] = total;
+    if (!w.mask)
+        for (int64_t j = j_tail + tid; j <= w.nblk; j += blockDim.x) blk[j] = total;
     if (tid == 0) w.U[b] = total;
 }
 
@@ -578,14 +589,219 @@ __global__ void __launch_bounds__(NT, GNSB_EMB_OCC / NT) emb_rows_kernel(const T
     }
 }
 
+#ifndef GNSB_EMB_MOCC
+#define GNSB_EMB_MOCC 512  // resident threads per SM the mask walk is compiled for (128 registers)
+#endif
+// Mask walk: the same sums as emb_rows_kernel, in the same order (dW and the
+// per-run squares q are bitwise equal to it when one column chunk covers D),
+// without the per-example cursors.  The sort kernel marks, per table row v, a
+// bit per example with a run at v and records where that run lives
+// (idx2[v][b]).  Warps take blocks of RB consecutive rows from a queue (an
+// atomic counter; the next block's index and mask words are fetched while the
+// current block runs):
+//   1. lane l holds mask word l of the block (one coalesced load);
+//   2. a warp scan numbers the (row, example) pairs in (row, example) order,
+//      and the word lanes list them in shared memory, up to 32 at a time;
+//   3. lane j loads pair j's idx2 entry (all pairs at once);
+//   4. the warp loads the first token rows of PB pairs at once, sums each
+//      pair's run, and stores each row (zero rows too) once its pairs are done.
+// ||dW||^2 is kept per block (qbig[block]) so the queue order does not change
+// its rounding; emb_raw_kernel folds the blocks in index order.
+template <typename T, int NVC, int MW, int PB>
+__global__ void __launch_bounds__(kEmbRowsThreads, GNSB_EMB_MOCC / kEmbRowsThreads)
+    emb_mask_kernel(const T* g, int64_t B, int64_t Tn, int64_t V, int64_t D, EmbFastWs w, float* dW) {
+    constexpr int W = Traits<T>::W;
+    constexpr int NP = W / 2;
+    constexpr int RB = MW <= 4 ? kRowsPerWarp : 32 / MW;  // rows per block: RB * MW <= 32 mask words
+    constexpr int PC = 32;                                 // pairs listed per window
+    using P = float2;
+    __shared__ uint16_t s_pr[kEmbRowsThreads / 32][PC];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nvec = (int)(D / W);
+    const int nchunk = (nvec + 32 * NVC - 1) / (32 * NVC);
+    const int64_t nblocks = (V + RB - 1) / RB;
+    unsigned int* ctr = reinterpret_cast<unsigned int*>(w.mask + V * MW);  // zeroed with the mask
+    auto take = [&]() {
+        unsigned int x = 0;
+        if (lane == 0) x = atomicAdd(ctr, 1u);
+        return (int64_t)__shfl_sync(0xffffffffu, x, 0);
+    };
+    auto mask_of = [&](int64_t blk) {
+        const int64_t v0 = blk * RB;
+        const int nrow = blk < nblocks ? (int)(V - v0 < RB ? V - v0 : RB) : 0;
+        return lane < nrow * MW ? __ldcg(w.mask + v0 * MW + lane) : 0u;
+    };
+    int64_t blk = take();
+    uint32_t m = mask_of(blk);
+    while (blk < nblocks) {
+        const int64_t nxt = take();
+        const uint32_t mn = mask_of(nxt);  // in flight while this block runs
+        const int64_t v0 = blk * RB;
+        const int nrow = (int)(V - v0 < RB ? V - v0 : RB);
+        double qb = 0.0;  // this lane's share of the block's ||dW||^2
+        const int cnt = __popc(m);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int excl = incl - cnt;
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        for (int c = 0; c < nchunk; ++c) {
+            P acc[NVC][NP];
+#pragma unroll
+            for (int q = 0; q < NVC; ++q)
+#pragma unroll
+                for (int e = 0; e < NP; ++e) acc[q][e] = make_float2(0.f, 0.f);
+            int vr = 0;  // the row being accumulated
+            auto store_row = [&]() {
+#pragma unroll
+                for (int q = 0; q < NVC; ++q) {
+                    const int vi = (c * NVC + q) * 32 + lane;
+                    if (vi < nvec) {
+                        float* dst = dW + (v0 + vr) * D + (int64_t)vi * W;
+#pragma unroll
+                        for (int e = 0; e < NP; e += 2) {
+                            const float4 o = make_float4(acc[q][e].x, acc[q][e].y, acc[q][e + 1].x, acc[q][e + 1].y);
+                            reinterpret_cast<float4*>(dst)[e / 2] = o;
+                            qb = fma((double)o.x, (double)o.x, qb);
+                            qb = fma((double)o.y, (double)o.y, qb);
+                            qb = fma((double)o.z, (double)o.z, qb);
+                            qb = fma((double)o.w, (double)o.w, qb);
+                        }
+                    }
+#pragma unroll
+                    for (int e = 0; e < NP; ++e) acc[q][e] = make_float2(0.f, 0.f);
+                }
+                ++vr;
+            };
+            for (int base = 0; base < total; base += PC) {
+                __syncwarp();
+                if (cnt > 0 && excl < base + PC && incl > base) {
+                    uint32_t mm = m;
+                    for (int k = excl; mm && k < base + PC; ++k) {
+                        const int bit = __ffs(mm) - 1;
+                        mm &= mm - 1;
+                        if (k >= base) s_pr[wid][k - base] = (uint16_t)(((lane / MW) << 8) | ((lane % MW) * 32 + bit));
+                    }
+                }
+                __syncwarp();
+                const int n = total - base < PC ? total - base : PC;
+                int pi = 0, pb = 0, pr = 0, pt = 0, pst = 0, pln = 1;
+                if (lane < n) {
+                    const uint32_t e = s_pr[wid][lane];
+                    pi = (int)(e >> 8);
+                    pb = (int)(e & 255u);
+                    const int2 x = __ldcg(w.idx2 + (v0 + pi) * B + pb);
+                    pr = x.x;
+                    pt = x.y & 0x7fffffff;
+                    if (x.y < 0) {  // a run of several tokens: its start in the sorted list
+                        const int4 en = __ldcg(w.ent + (int64_t)pb * Tn + pr);
+                        pst = en.y;
+                        pln = en.z;
+                    }
+                }
+                for (int k0 = 0; k0 < n; k0 += PB) {
+                    uint4 xb[PB][NVC];  // the first token rows of PB pairs, all in flight at once
+#pragma unroll
+                    for (int u = 0; u < PB; ++u) {
+                        const int64_t b = __shfl_sync(0xffffffffu, pb, (k0 + u) & 31);
+                        const int64_t t = __shfl_sync(0xffffffffu, pt, (k0 + u) & 31);
+                        const uint4* row = reinterpret_cast<const uint4*>(g + (b * Tn + t) * D);
+#pragma unroll
+                        for (int q = 0; q < NVC; ++q) {
+                            const int vi = (c * NVC + q) * 32 + lane;
+                            xb[u][q] = (k0 + u < n && vi < nvec) ? __ldg(row + vi) : make_uint4(0u, 0u, 0u, 0u);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < PB; ++u) {
+                        const int k = k0 + u;
+                        if (k >= n) break;
+                        const int i = __shfl_sync(0xffffffffu, pi, k);
+                        const int64_t b = __shfl_sync(0xffffffffu, pb, k);
+                        const int r = __shfl_sync(0xffffffffu, pr, k);
+                        const int len = __shfl_sync(0xffffffffu, pln, k);
+                        const int st = __shfl_sync(0xffffffffu, pst, k);
+                        while (vr < i) store_row();
+                        P tmp[NVC][NP];
+#pragma unroll
+                        for (int q = 0; q < NVC; ++q) {
+                            P x[NP];
+                            unpack2<T>(xb[u][q], x);
+#pragma unroll
+                            for (int e = 0; e < NP; ++e) {
+                                tmp[q][e] = make_float2(0.f, 0.f);
+                                tmp[q][e].x += x[e].x;
+                                tmp[q][e].y += x[e].y;
+                            }
+                        }
+                        for (int j = 1; j < len; ++j) {  // the run's later tokens in token order
+                            const int64_t t = w.perm[b * Tn + st + j];
+                            const uint4* row = reinterpret_cast<const uint4*>(g + (b * Tn + t) * D);
+#pragma unroll
+                            for (int q = 0; q < NVC; ++q) {
+                                const int vi = (c * NVC + q) * 32 + lane;
+                                if (vi < nvec) {
+                                    P x[NP];
+                                    unpack2<T>(__ldg(row + vi), x);
+#pragma unroll
+                                    for (int e = 0; e < NP; ++e) {
+                                        tmp[q][e].x += x[e].x;
+                                        tmp[q][e].y += x[e].y;
+                                    }
+                                }
+                            }
+                        }
+                        double sq = 0.0;
+#pragma unroll
+                        for (int q = 0; q < NVC; ++q)
+#pragma unroll
+                            for (int e = 0; e < NP; ++e) {
+                                acc[q][e].x += tmp[q][e].x;
+                                acc[q][e].y += tmp[q][e].y;
+                                sq = fma((double)tmp[q][e].x, (double)tmp[q][e].x, sq);
+                                sq = fma((double)tmp[q][e].y, (double)tmp[q][e].y, sq);
+                            }
+                        sq = warp_sum(sq);
+                        if (lane == 0) {
+                            double* qd = w.q + b * Tn + r;
+                            *qd = c == 0 ? sq : *qd + sq;
+                        }
+                    }
+                }
+            }
+            while (vr < nrow) store_row();
+        }
+        qb = warp_sum(qb);
+        if (lane == 0) w.qbig[blk] = qb;
+        blk = nxt;
+        m = mn;
+    }
+}
+
 // raw_b = sum_k q[b][k]: one 256-thread CTA per example.  Every load is
 // issued before the first add (a thread owns a strided set of at most
 // Tn / 256 entries), then a fixed-order tree: one L2 round trip instead of
 // U / 32 dependent ones (the warp-per-example version was latency-bound,
 // 9.5 us at T = 1024).
-__global__ void __launch_bounds__(256) emb_raw_kernel(int64_t B, int64_t Tn, EmbFastWs w, double* raw) {
+__global__ void __launch_bounds__(256) emb_raw_kernel(int64_t B, int64_t Tn, EmbFastWs w, double* raw,
+                                                      const double* qblk = nullptr, int nq = 0, double* qtot = nullptr) {
     __shared__ double s_red[256];
     const int64_t b = blockIdx.x;
+    if (b == B) {  // the mask walk's per-block ||dW||^2 partials, in block order
+        double s = 0.0;
+        for (int k = threadIdx.x; k < nq; k += 256) s += __ldcg(qblk + k);
+        s_red[threadIdx.x] = s;
+        __syncthreads();
+        for (int o = 128; o > 0; o >>= 1) {
+            if (threadIdx.x < o) s_red[threadIdx.x] += s_red[threadIdx.x + o];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) *qtot = s_red[0];
+        return;
+    }
     const int U = w.U[b];
     double s = 0.0;
 #pragma unroll 8
@@ -641,10 +857,29 @@ bool embedding_shape_ok(int64_t T) { return T >= 1 && T <= kEmbMaxT; }
 namespace {
 
 struct EmbFastLayout {
-    size_t perm, ent, U, q, qbig, bad, raw, blk, total;
-    int grid;
+    size_t perm, ent, U, q, qbig, bad, raw, blk, mask, idx2, qtot, total;
+    int grid;   // row-walk CTAs (the mask walk's when `masked`)
     int64_t nblk;
+    int64_t nqblk;  // mask walk: row blocks = ||dW||^2 partials
+    bool masked;
+    int mw;
 };
+
+// GNSB_EMB_WALK=cursor: never the mask walk; =mask: always (tests, A/B runs)
+bool emb_mask_walk() {
+    static const bool v = [] {
+        const char* e = std::getenv("GNSB_EMB_WALK");
+        return !(e && e[0] == 'c');
+    }();
+    return v;
+}
+bool emb_mask_forced() {
+    static const bool v = [] {
+        const char* e = std::getenv("GNSB_EMB_WALK");
+        return e && e[0] == 'm';
+    }();
+    return v;
+}
 
 // threads per row-walk CTA: 256, or 64 (B <= 32; GNSB_EMB_CTA=64, A/B runs).
 // Smaller CTAs retire independently (one warp with many matched rows holds
@@ -658,7 +893,7 @@ int emb_rows_threads(int64_t B) {
     return B <= 32 ? v : kEmbRowsThreads;
 }
 
-EmbFastLayout emb_fast_layout(int64_t B, int64_t Tn, int64_t V) {
+EmbFastLayout emb_fast_layout(int64_t B, int64_t Tn, int64_t V, bool bf16) {
     EmbFastLayout l{};
     const int sms = device_sm_count();
     const int64_t blocks = (V + kRowsPerWarp - 1) / kRowsPerWarp;  // row blocks, one per warp
@@ -685,11 +920,35 @@ EmbFastLayout emb_fast_layout(int64_t B, int64_t Tn, int64_t V) {
     l.ent = take((size_t)B * Tn * 16);
     l.U = take((size_t)B * 4);
     l.q = take((size_t)B * Tn * 8);
-    l.qbig = take((size_t)l.grid * 8);
     l.bad = take(4);
     l.raw = take((size_t)B * 8);
     l.nblk = blocks;
-    l.blk = take((size_t)B * (blocks + 1) * 4);
+    // The mask walk for bf16 rows when the table has at least two row blocks
+    // per resident warp (the queue balances the warps); the cursor walk for
+    // fp32 rows and small tables.  Measured at B=32 T=1024 D=768: V=50257
+    // bf16 68 against 75 us (B=64: 84 against 129), but fp32 rows 115 against
+    // 89 us and V=8192 77 against 60 us.
+    const int ng = (int)((B + 31) / 32);
+    const int mw = ng <= 1 ? 1 : ng <= 2 ? 2 : ng <= 4 ? 4 : 8;  // the kernel's MW
+    const int64_t rb = mw <= 4 ? kRowsPerWarp : 32 / mw;
+    const int64_t resident_warps = (int64_t)sms * (GNSB_EMB_MOCC / 32);
+    l.masked = emb_mask_walk() && (emb_mask_forced() || (bf16 && (V + rb - 1) / rb >= 2 * resident_warps));
+    if (l.masked) {
+        l.mw = mw;
+        l.nqblk = (V + rb - 1) / rb;
+        const int64_t mwpc = kEmbRowsThreads / 32;
+        const int64_t mgrid = (l.nqblk + mwpc - 1) / mwpc;
+        const int64_t mcap = (int64_t)sms * (GNSB_EMB_MOCC / kEmbRowsThreads);  // one resident wave
+        l.grid = (int)(mgrid < mcap ? (mgrid > 0 ? mgrid : 1) : mcap);
+        l.blk = take(4);
+        l.mask = take((size_t)V * l.mw * 4 + 16);  // + the block queue's counter
+        l.idx2 = take((size_t)V * B * 8);
+        l.qbig = take((size_t)l.nqblk * 8);
+        l.qtot = take(8);
+    } else {
+        l.blk = take((size_t)B * (blocks + 1) * 4);
+        l.qbig = take((size_t)l.grid * 8);
+    }
     l.total = off;
     return l;
 }
@@ -711,22 +970,28 @@ size_t embedding_workspace(int64_t B, int64_t T, int64_t V, int64_t D, int dt) {
     // (the path also depends on pointer alignment: room for either)
     const size_t slow = emb_layout(B, T, V, D, dt == 2 ? 8 : 4).total;
     if (!emb_fast_ok(dt, B, D)) return slow;
-    const size_t fast = emb_fast_layout(B, T, V).total;
+    const size_t fast = emb_fast_layout(B, T, V, dt == 1).total;
     return fast > slow ? fast : slow;
 }
 
 template <typename T>
 cudaError_t emb_fast_run(const int32_t* ids, const void* g, void* dW, double* raw, double* sums, int64_t B,
                          int64_t Tn, int64_t V, int64_t D, void* ws, int32_t* bad_flag_out, cudaStream_t st) {
-    const EmbFastLayout l = emb_fast_layout(B, Tn, V);
+    const EmbFastLayout l = emb_fast_layout(B, Tn, V, sizeof(T) == 2);
     unsigned char* base = static_cast<unsigned char*>(ws);
     EmbFastWs w{reinterpret_cast<int32_t*>(base + l.perm), reinterpret_cast<int4*>(base + l.ent),
                 reinterpret_cast<int32_t*>(base + l.U),    reinterpret_cast<double*>(base + l.q),
                 reinterpret_cast<double*>(base + l.qbig),  reinterpret_cast<int32_t*>(base + l.bad),
-                reinterpret_cast<int32_t*>(base + l.blk),   l.nblk};
+                reinterpret_cast<int32_t*>(base + l.blk),   l.nblk,
+                l.masked ? reinterpret_cast<uint32_t*>(base + l.mask) : nullptr,
+                l.masked ? reinterpret_cast<int2*>(base + l.idx2) : nullptr, l.mw};
     if (raw == nullptr) raw = reinterpret_cast<double*>(base + l.raw);
     cudaError_t e = cudaMemsetAsync(w.bad, 0, 4, st);
     if (e != cudaSuccess) return e;
+    if (l.masked) {
+        e = cudaMemsetAsync(w.mask, 0, (size_t)V * l.mw * 4 + 16, st);
+        if (e != cudaSuccess) return e;
+    }
     const int Tp = pow2_at_least(Tn < 32 ? 32 : Tn);  // whole warps in the shuffle stages
     int sh = 0;
     while ((1 << sh) < Tp) ++sh;
@@ -761,7 +1026,18 @@ cudaError_t emb_fast_run(const int32_t* ids, const void* g, void* dW, double* ra
     const int ng = (int)((B + 31) / 32);
     auto launch = [&](auto nvc) {
         constexpr int NVC = decltype(nvc)::value;
-        if (ng <= 1 && emb_rows_threads(B) == 64)
+        if (l.masked) {
+            // first-token rows in flight per batch: 12-16 16-byte vectors per lane
+            constexpr int PB = NVC <= 3 ? 4 : NVC <= 4 ? 3 : NVC <= 6 ? 2 : 1;
+            if (l.mw == 1)
+                emb_mask_kernel<T, NVC, 1, PB><<<l.grid, kEmbRowsThreads, 0, st>>>(gp, B, Tn, V, D, w, dWp);
+            else if (l.mw == 2)
+                emb_mask_kernel<T, NVC, 2, PB><<<l.grid, kEmbRowsThreads, 0, st>>>(gp, B, Tn, V, D, w, dWp);
+            else if (l.mw == 4)
+                emb_mask_kernel<T, NVC, 4, PB><<<l.grid, kEmbRowsThreads, 0, st>>>(gp, B, Tn, V, D, w, dWp);
+            else
+                emb_mask_kernel<T, NVC, 8, PB><<<l.grid, kEmbRowsThreads, 0, st>>>(gp, B, Tn, V, D, w, dWp);
+        } else if (ng <= 1 && emb_rows_threads(B) == 64)
             emb_rows_kernel<T, NVC, 1, 64><<<l.grid, 64, 0, st>>>(gp, B, Tn, V, D, w, dWp);
         else if (ng <= 1)
             emb_rows_kernel<T, NVC, 1><<<l.grid, kEmbRowsThreads, 0, st>>>(gp, B, Tn, V, D, w, dWp);
@@ -788,12 +1064,18 @@ cudaError_t emb_fast_run(const int32_t* ids, const void* g, void* dW, double* ra
         launch(std::integral_constant<int, 8>{});
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    emb_raw_kernel<<<(unsigned)B, 256, 0, st>>>(B, Tn, w, raw);
+    double* qtot = l.masked ? reinterpret_cast<double*>(base + l.qtot) : nullptr;
+    if (l.masked)  // one more CTA folds the per-block ||dW||^2 partials
+        emb_raw_kernel<<<(unsigned)B + 1, 256, 0, st>>>(B, Tn, w, raw, w.qbig, (int)l.nqblk, qtot);
+    else
+        emb_raw_kernel<<<(unsigned)B, 256, 0, st>>>(B, Tn, w, raw);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (sums) {
         e = launch_fold_rows(raw, 1, (int)B, nullptr, sums, 0, st);
-        if (e == cudaSuccess) e = launch_fold_rows(w.qbig, 1, l.grid, nullptr, sums, 2, st);
+        if (e == cudaSuccess)
+            e = l.masked ? launch_fold_rows(qtot, 1, 1, nullptr, sums, 2, st)
+                         : launch_fold_rows(w.qbig, 1, l.grid, nullptr, sums, 2, st);
     }
     if (e == cudaSuccess && bad_flag_out) e = cudaMemcpyAsync(bad_flag_out, w.bad, 4, cudaMemcpyDeviceToDevice, st);
     return e;

@@ -39,7 +39,13 @@ def test_fp64_matches_reference_golden_bitwise(golden, cuda):
                                              (torch.bfloat16, 3, 1024, 50257, 64, "pad"),
                                              # fp32 rows wide enough for 6 and 8 column vectors per lane
                                              (torch.float32, 2, 256, 3000, 768, "uniform"),
-                                             (torch.float32, 2, 128, 3000, 1000, "skew")])
+                                             (torch.float32, 2, 128, 3000, 1000, "skew"),
+                                             # the mask walk: 2 and 8 mask words per row (4-row blocks),
+                                             # more than 32 (row, example) pairs in one row, 2 column chunks
+                                             (torch.bfloat16, 40, 256, 5000, 256, "uniform"),
+                                             (torch.bfloat16, 200, 64, 3000, 128, "skew"),
+                                             (torch.float32, 130, 64, 500, 64, "pad"),
+                                             (torch.bfloat16, 3, 512, 2000, 2048, "skew")])
 def test_matches_oracle(orc, cuda, dt, B, T, V, D, mode):
     from paper_2411_00999_b200.embedding import embedding_backward_simultaneous
 
@@ -79,3 +85,55 @@ def test_errors_and_determinism(cuda):
     b = embedding_backward_simultaneous(ids, gg, 300)
     assert torch.equal(a.weight_grads["weight"], b.weight_grads["weight"])
     assert torch.equal(a.per_example_sqnorms_raw["weight"], b.per_example_sqnorms_raw["weight"])
+
+
+_WALK_SCRIPT = """
+import sys, torch
+sys.path.insert(0, {root!r})
+from paper_2411_00999_b200.embedding import embedding_backward_simultaneous
+d = torch.load({inp!r})
+r = embedding_backward_simultaneous(d["ids"].cuda(), d["g"].cuda(), d["V"])
+torch.save({{"dW": r.weight_grads["weight"].cpu(), "raw": r.per_example_sqnorms_raw["weight"].cpu()}}, {out!r})
+"""
+
+
+@pytest.mark.parametrize("dt,B,T,V,D,mode", [(torch.bfloat16, 32, 1024, 50257, 768, "uniform"),
+                                             (torch.bfloat16, 64, 1024, 50257, 768, "skew"),
+                                             (torch.bfloat16, 40, 256, 5000, 256, "skew"),
+                                             (torch.bfloat16, 200, 64, 3000, 128, "skew"),
+                                             (torch.bfloat16, 3, 512, 2000, 2048, "skew"),
+                                             (torch.float32, 130, 64, 500, 64, "pad"),
+                                             (torch.float32, 2, 128, 3000, 1000, "uniform")])
+def test_mask_walk_bitwise_equals_cursor_walk(orc, cuda, tmp_path, dt, B, T, V, D, mode):
+    """The mask walk (forced with GNSB_EMB_WALK=mask; the default for bf16 rows
+    of large tables) and the per-example cursor walk (GNSB_EMB_WALK=cursor) add
+    the same rows in the same order: dW and raw_b are bitwise equal; the mask
+    walk also matches the oracle.  Cases: 1, 2 and 8 mask words per row, more
+    than 32 (row, example) pairs in a row (padding), two column chunks."""
+    import os
+    import subprocess
+    import sys
+
+    gen = torch.Generator(device="cpu").manual_seed(B + T + V)
+    if mode == "skew":
+        ids = (torch.rand(B, T, generator=gen) ** 3 * V).to(torch.int32).clamp_(0, V - 1)
+    else:
+        ids = torch.randint(0, V, (B, T), generator=gen, dtype=torch.int32)
+        if mode == "pad":
+            ids[torch.rand(B, T, generator=gen) < 0.9] = 7
+    g = torch.randn(B, T, D, generator=gen).to(dt)
+    inp = str(tmp_path / "in.pt")
+    torch.save({"ids": ids, "g": g, "V": V}, inp)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for walk in ("mask", "cursor"):
+        out = str(tmp_path / f"{walk}.pt")
+        env = dict(os.environ, GNSB_EMB_WALK=walk)
+        subprocess.run([sys.executable, "-c", _WALK_SCRIPT.format(root=root, inp=inp, out=out)], env=env, check=True)
+        outs[walk] = torch.load(out)
+    assert torch.equal(outs["mask"]["dW"], outs["cursor"]["dW"])
+    assert torch.equal(outs["mask"]["raw"], outs["cursor"]["raw"])
+    ref = orc.embedding_backward(ids.numpy(), g.double().numpy(), V)
+    dW = outs["mask"]["dW"].double().numpy()
+    assert close(dW, ref["dW"], 1e-5, 1e-5 * np.abs(ref["dW"]).max())
+    assert close(outs["mask"]["raw"].numpy(), ref["raw_w"], 1e-5)
