@@ -786,20 +786,68 @@ __global__ void __launch_bounds__(kEmbRowsThreads, GNSB_EMB_MOCC / kEmbRowsThrea
 // Tn / 256 entries), then a fixed-order tree: one L2 round trip instead of
 // U / 32 dependent ones (the warp-per-example version was latency-bound,
 // 9.5 us at T = 1024).
+// The mask walk's version (`tail` set) has one more CTA, which folds the
+// per-block ||dW||^2 partials in block order; the last CTA to finish (ticket)
+// then writes sums[0] = sum_b raw_b, sums[2] = ||dW||^2 and the bad-id flag,
+// in place of two fold launches and a copy.
+struct EmbRawTail {
+    const double* qblk;   // [nq] per-block ||dW||^2
+    int nq;
+    double* qtot;         // [1]
+    unsigned int* ticket; // zeroed with the mask
+    double* sums;         // may be null
+    const int32_t* bad;   // the sort kernel's flag
+    int32_t* bad_out;     // may be null
+};
+
 __global__ void __launch_bounds__(256) emb_raw_kernel(int64_t B, int64_t Tn, EmbFastWs w, double* raw,
-                                                      const double* qblk = nullptr, int nq = 0, double* qtot = nullptr) {
+                                                      EmbRawTail tl = EmbRawTail{}) {
     __shared__ double s_red[256];
+    __shared__ bool s_last;
     const int64_t b = blockIdx.x;
-    if (b == B) {  // the mask walk's per-block ||dW||^2 partials, in block order
-        double s = 0.0;
-        for (int k = threadIdx.x; k < nq; k += 256) s += __ldcg(qblk + k);
+    if (tl.ticket != nullptr) {
+        if (b == B) {  // the mask walk's per-block ||dW||^2 partials, in block order
+            double s = 0.0;
+            for (int k = threadIdx.x; k < tl.nq; k += 256) s += __ldcg(tl.qblk + k);
+            s_red[threadIdx.x] = s;
+        } else {
+            const int U = w.U[b];
+            double s = 0.0;
+#pragma unroll 8
+            for (int k = threadIdx.x; k < U; k += 256) s += __ldcg(w.q + b * Tn + k);
+            s_red[threadIdx.x] = s;
+        }
+        __syncthreads();
+        for (int o = 128; o > 0; o >>= 1) {
+            if (threadIdx.x < o) s_red[threadIdx.x] += s_red[threadIdx.x + o];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            if (b == B)
+                *tl.qtot = s_red[0];
+            else
+                raw[b] = s_red[0];
+            __threadfence();
+            s_last = atomicAdd(tl.ticket, 1u) == (unsigned)B;
+        }
+        __syncthreads();
+        if (!s_last) return;
+        __threadfence();
+        double s = 0.0;  // sum_b raw_b: a fixed tree over b
+        for (int k = threadIdx.x; k < B; k += 256) s += __ldcg(raw + k);
         s_red[threadIdx.x] = s;
         __syncthreads();
         for (int o = 128; o > 0; o >>= 1) {
             if (threadIdx.x < o) s_red[threadIdx.x] += s_red[threadIdx.x + o];
             __syncthreads();
         }
-        if (threadIdx.x == 0) *qtot = s_red[0];
+        if (threadIdx.x == 0) {
+            if (tl.sums) {
+                tl.sums[0] = s_red[0];
+                tl.sums[2] = __ldcg(tl.qtot);
+            }
+            if (tl.bad_out) *tl.bad_out = __ldcg(tl.bad);
+        }
         return;
     }
     const int U = w.U[b];
@@ -948,6 +996,8 @@ EmbFastLayout emb_fast_layout(int64_t B, int64_t Tn, int64_t V, bool bf16) {
     } else {
         l.blk = take((size_t)B * (blocks + 1) * 4);
         l.qbig = take((size_t)l.grid * 8);
+        l.qtot = take(8);
+        l.mask = take(16);  // no mask words: only the tail (counter, bad flag, ticket)
     }
     l.total = off;
     return l;
@@ -986,12 +1036,14 @@ cudaError_t emb_fast_run(const int32_t* ids, const void* g, void* dW, double* ra
                 l.masked ? reinterpret_cast<uint32_t*>(base + l.mask) : nullptr,
                 l.masked ? reinterpret_cast<int2*>(base + l.idx2) : nullptr, l.mw};
     if (raw == nullptr) raw = reinterpret_cast<double*>(base + l.raw);
-    cudaError_t e = cudaMemsetAsync(w.bad, 0, 4, st);
+    // the mask walk: one memset clears the mask words, the block queue's
+    // counter, the bad-id flag and the raw kernel's ticket (the mask's tail)
+    // (the cursor walk: the tail alone)
+    const size_t mask_words = l.masked ? (size_t)V * l.mw * 4 : 0;
+    unsigned int* tail = reinterpret_cast<unsigned int*>(base + l.mask + mask_words);
+    w.bad = reinterpret_cast<int32_t*>(tail + 1);
+    cudaError_t e = cudaMemsetAsync(base + l.mask, 0, mask_words + 16, st);
     if (e != cudaSuccess) return e;
-    if (l.masked) {
-        e = cudaMemsetAsync(w.mask, 0, (size_t)V * l.mw * 4 + 16, st);
-        if (e != cudaSuccess) return e;
-    }
     const int Tp = pow2_at_least(Tn < 32 ? 32 : Tn);  // whole warps in the shuffle stages
     int sh = 0;
     while ((1 << sh) < Tp) ++sh;
@@ -1064,21 +1116,12 @@ cudaError_t emb_fast_run(const int32_t* ids, const void* g, void* dW, double* ra
         launch(std::integral_constant<int, 8>{});
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    double* qtot = l.masked ? reinterpret_cast<double*>(base + l.qtot) : nullptr;
-    if (l.masked)  // one more CTA folds the per-block ||dW||^2 partials
-        emb_raw_kernel<<<(unsigned)B + 1, 256, 0, st>>>(B, Tn, w, raw, w.qbig, (int)l.nqblk, qtot);
-    else
-        emb_raw_kernel<<<(unsigned)B, 256, 0, st>>>(B, Tn, w, raw);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    if (sums) {
-        e = launch_fold_rows(raw, 1, (int)B, nullptr, sums, 0, st);
-        if (e == cudaSuccess)
-            e = l.masked ? launch_fold_rows(qtot, 1, 1, nullptr, sums, 2, st)
-                         : launch_fold_rows(w.qbig, 1, l.grid, nullptr, sums, 2, st);
-    }
-    if (e == cudaSuccess && bad_flag_out) e = cudaMemcpyAsync(bad_flag_out, w.bad, 4, cudaMemcpyDeviceToDevice, st);
-    return e;
+    // one more CTA folds the ||dW||^2 partials (per row block, or per walk CTA
+    // for the cursor walk); the last CTA writes sums[0], sums[2] and the flag
+    const EmbRawTail tl{w.qbig, (int)(l.masked ? l.nqblk : l.grid), reinterpret_cast<double*>(base + l.qtot),
+                        tail + 2, sums, w.bad, bad_flag_out};
+    emb_raw_kernel<<<(unsigned)B + 1, 256, 0, st>>>(B, Tn, w, raw, tl);
+    return cudaGetLastError();
 }
 
 template <typename T>

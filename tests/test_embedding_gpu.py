@@ -137,3 +137,52 @@ def test_mask_walk_bitwise_equals_cursor_walk(orc, cuda, tmp_path, dt, B, T, V, 
     dW = outs["mask"]["dW"].double().numpy()
     assert close(dW, ref["dW"], 1e-5, 1e-5 * np.abs(ref["dW"]).max())
     assert close(outs["mask"]["raw"].numpy(), ref["raw_w"], 1e-5)
+
+
+def test_mask_walk_flags_bad_ids_and_sums(cuda):
+    """The mask walk's raw kernel hands back the bad-id flag and sums[0] / sums[2]
+    (no separate fold launches): out-of-range ids still raise, and the sums
+    equal the per-example norms and ||dW||^2 it returns."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = f"""
+import sys, torch
+sys.path.insert(0, {root!r})
+from paper_2411_00999_b200.embedding import embedding_backward_simultaneous
+g = torch.randn(4, 64, 32, device="cuda").bfloat16()
+ids = torch.randint(0, 100, (4, 64), device="cuda", dtype=torch.int32)
+r = embedding_backward_simultaneous(ids, g, 100)
+dW = r.weight_grads["weight"].double()
+raw = r.per_example_sqnorms_raw["weight"]
+assert abs(float(r.sums4[0]) - float(raw.sum())) <= 1e-12 * float(raw.sum()), (r.sums4, raw.sum())
+assert abs(float(r.sums4[2]) - float((dW * dW).sum())) <= 1e-9 * float((dW * dW).sum()), r.sums4
+ids[2, 5] = 100
+try:
+    embedding_backward_simultaneous(ids, g, 100)
+except ValueError as e:
+    assert "id out of range" in str(e)
+# the kernel's own flag (no host check), handed back by the raw kernel's last CTA
+import ctypes
+from paper_2411_00999_b200 import _lib
+from paper_2411_00999_b200.layers import gnsb_dtype
+lib = _lib.lib()
+n = ctypes.c_size_t()
+_lib.check(lib.gnsb_embedding_pe_workspace_size(4, 64, 100, 32, gnsb_dtype(g.dtype), ctypes.byref(n)))
+ws = torch.zeros(n.value, dtype=torch.uint8, device="cuda")
+dW = torch.empty(100, 32, device="cuda")
+raw = torch.empty(4, dtype=torch.float64, device="cuda")
+for bad_id, want in ((100, 1), (7, 0)):
+    ids[2, 5] = bad_id
+    bad = torch.full((1,), -1, dtype=torch.int32, device="cuda")
+    _lib.check(lib.gnsb_embedding_pe(ids.data_ptr(), g.data_ptr(), dW.data_ptr(), raw.data_ptr(), None, 4, 64, 100, 32,
+                                     gnsb_dtype(g.dtype), ws.data_ptr(), ws.numel(), bad.data_ptr(),
+                                     torch.cuda.current_stream().cuda_stream))
+    assert int(bad.item()) == want, (bad_id, int(bad.item()))
+print("ok")
+"""
+    env = dict(os.environ, GNSB_EMB_WALK="mask")
+    out = subprocess.run([sys.executable, "-c", script], env=env, check=True, capture_output=True, text=True)
+    assert out.stdout.strip().endswith("ok")
