@@ -138,6 +138,9 @@ struct LnBwdCfg {
     static __host__ __device__ constexpr size_t smem_bytes(int S, int Dp) { return park_off(S, Dp) + park_bytes(Dp); }
 };
 
+#ifndef GNSB_LN_EARLYFOLD
+#define GNSB_LN_EARLYFOLD 0  // A/B: fold the CTA's first example at its boundary
+#endif
 template <typename C, bool HAS_MEAN>
 __global__ void __launch_bounds__(C::kBoundThreads, C::kCps) ln_bwd_kernel(LnBwdArgs a) {
     using T = typename C::Row;
@@ -191,6 +194,15 @@ __global__ void __launch_bounds__(C::kBoundThreads, C::kCps) ln_bwd_kernel(LnBwd
         }
         fence_mbar_init();
     }
+#if GNSB_LN_EARLYFOLD
+    // early fold of the CTA's first example (see flush_to)
+    __shared__ int s_fold_cnt, s_early;
+    __shared__ int s_fold_last[G];
+    if (threadIdx.x == 0) {
+        s_fold_cnt = 0;
+        s_early = 0;
+    }
+#endif
     if (!a.aligned) {  // padded rows: the pad columns must read as zero
         uint4* p = reinterpret_cast<uint4*>(ring);
         const size_t n16 = (size_t)S * C::stage_row_bytes(Dp) / 16;
@@ -334,6 +346,40 @@ __global__ void __launch_bounds__(C::kBoundThreads, C::kCps) ln_bwd_kernel(LnBwd
     };
     auto flush_to = [&](int64_t new_ex) {
         write_slot(cur_ex, false);
+#if GNSB_LN_EARLYFOLD
+        if constexpr (G > 1 && !C::kPark && !C::kNoFold) {
+            // The CTA's first example ends here for this group.  The last group
+            // to get past it folds the G group slots into slot 0 now, while
+            // the other groups keep streaming rows, instead of in the
+            // end-of-kernel fold behind the CTA's last row.
+            if (cur_ex == ex_first) {
+                __threadfence_block();
+                named_bar_sync(1 + g, GT);
+                if (tig == 0) s_fold_last[g] = atomicAdd(&s_fold_cnt, 1) == G - 1;
+                named_bar_sync(1 + g, GT);
+                if (s_fold_last[g]) {
+                    __threadfence_block();
+                    constexpr int E = 16 / sizeof(Acc);
+                    Acc* fb = partial + (size_t)(cta + ex_first) * G * 2 * Dp;
+                    for (int i = tig; i < 2 * Dp / E; i += GT) {
+                        uint4 v[G];
+#pragma unroll
+                        for (int gg = 0; gg < G; ++gg)
+                            v[gg] = __ldcg(reinterpret_cast<const uint4*>(fb + (size_t)gg * 2 * Dp + i * E));
+                        Acc t[E];
+#pragma unroll
+                        for (int e = 0; e < E; ++e) t[e] = reinterpret_cast<const Acc*>(&v[0])[e];
+#pragma unroll
+                        for (int gg = 1; gg < G; ++gg)
+#pragma unroll
+                            for (int e = 0; e < E; ++e) t[e] += reinterpret_cast<const Acc*>(&v[gg])[e];
+                        *reinterpret_cast<uint4*>(fb + i * E) = *reinterpret_cast<const uint4*>(t);
+                    }
+                    if (tig == 0) s_early = 1;
+                }
+            }
+        }
+#endif
 #pragma unroll
         for (int k = 0; k < VPT; ++k)
 #pragma unroll
@@ -553,6 +599,9 @@ __global__ void __launch_bounds__(C::kBoundThreads, C::kCps) ln_bwd_kernel(LnBwd
         const int64_t e0 = r_begin / M, e1 = (r_end - 1) / M;
         Acc* part = static_cast<Acc*>(a.partial);
         for (int64_t ex = e0; ex <= e1; ++ex) {
+#if GNSB_LN_EARLYFOLD
+            if (!C::kPark && ex == e0 && e0 < e1 && s_early) continue;  // folded at its boundary
+#endif
             Acc* base = part + (size_t)(cta + ex) * G * 2 * Dp;
             // shared memory: the last example (registers -> ring) and the first
             // (parked at its boundary); L2: examples in between (short rows)
