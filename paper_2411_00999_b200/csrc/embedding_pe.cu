@@ -54,6 +54,7 @@ __global__ void __launch_bounds__(kEmbThreads) emb_example_kernel(const int32_t*
     const int64_t b = blockIdx.x;
     const int tid = threadIdx.x;
     const int32_t* idb = ids + b * Tn;
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the walk may get scheduled
     for (int i = tid; i < Tp; i += blockDim.x) {
         uint64_t k = ~0ull;
         if (i < Tn) {
@@ -230,6 +231,27 @@ constexpr int kEmbBuckets = 4096;  // id buckets of the sort kernel's bucket sor
 constexpr int kRowsPerWarp = GNSB_EMB_RPW;  // table rows per warp (A/B: -DGNSB_EMB_RPW=4 / 2)
 constexpr int kEmbRowsThreads = 256;
 constexpr int kEmbMaxGroups = 8;  // examples handled by the fast path: B <= 32 * 8
+
+#ifndef GNSB_EMB_PDL
+#define GNSB_EMB_PDL 1  // the walk and the raw kernel launch with programmatic dependent launch (A/B: 0)
+#endif
+// Programmatic dependent launch: the kernel's CTAs are scheduled while its
+// predecessor drains; it calls griddepcontrol.wait before touching anything
+// the predecessor wrote.
+template <typename... KArgs, typename... Args>
+cudaError_t emb_launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = GNSB_EMB_PDL ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
 
 struct EmbFastWs {
     int32_t* perm;  // [B][Tn]
@@ -631,6 +653,8 @@ __global__ void __launch_bounds__(kEmbRowsThreads, GNSB_EMB_MOCC / kEmbRowsThrea
         const int nrow = blk < nblocks ? (int)(V - v0 < RB ? V - v0 : RB) : 0;
         return lane < nrow * MW ? __ldcg(w.mask + v0 * MW + lane) : 0u;
     };
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the sort kernel's mask, idx2, runs
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     int64_t blk = take();
     uint32_t m = mask_of(blk);
     while (blk < nblocks) {
@@ -805,6 +829,7 @@ __global__ void __launch_bounds__(256) emb_raw_kernel(int64_t B, int64_t Tn, Emb
     __shared__ double s_red[256];
     __shared__ bool s_last;
     const int64_t b = blockIdx.x;
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the walk's q, qbig
     if (tl.ticket != nullptr) {
         if (b == B) {  // the mask walk's per-block ||dW||^2 partials, in block order
             double s = 0.0;
@@ -1076,19 +1101,20 @@ cudaError_t emb_fast_run(const int32_t* ids, const void* g, void* dW, double* ra
     const T* gp = static_cast<const T*>(g);
     float* dWp = static_cast<float*>(dW);
     const int ng = (int)((B + 31) / 32);
+    cudaError_t le = cudaSuccess;  // (launch errors of the PDL launches)
     auto launch = [&](auto nvc) {
         constexpr int NVC = decltype(nvc)::value;
         if (l.masked) {
             // first-token rows in flight per batch: 12-16 16-byte vectors per lane
             constexpr int PB = NVC <= 3 ? 4 : NVC <= 4 ? 3 : NVC <= 6 ? 2 : 1;
             if (l.mw == 1)
-                emb_mask_kernel<T, NVC, 1, PB><<<l.grid, kEmbRowsThreads, 0, st>>>(gp, B, Tn, V, D, w, dWp);
+                le = emb_launch_pdl(emb_mask_kernel<T, NVC, 1, PB>, l.grid, kEmbRowsThreads, st, gp, B, Tn, V, D, w, dWp);
             else if (l.mw == 2)
-                emb_mask_kernel<T, NVC, 2, PB><<<l.grid, kEmbRowsThreads, 0, st>>>(gp, B, Tn, V, D, w, dWp);
+                le = emb_launch_pdl(emb_mask_kernel<T, NVC, 2, PB>, l.grid, kEmbRowsThreads, st, gp, B, Tn, V, D, w, dWp);
             else if (l.mw == 4)
-                emb_mask_kernel<T, NVC, 4, PB><<<l.grid, kEmbRowsThreads, 0, st>>>(gp, B, Tn, V, D, w, dWp);
+                le = emb_launch_pdl(emb_mask_kernel<T, NVC, 4, PB>, l.grid, kEmbRowsThreads, st, gp, B, Tn, V, D, w, dWp);
             else
-                emb_mask_kernel<T, NVC, 8, PB><<<l.grid, kEmbRowsThreads, 0, st>>>(gp, B, Tn, V, D, w, dWp);
+                le = emb_launch_pdl(emb_mask_kernel<T, NVC, 8, PB>, l.grid, kEmbRowsThreads, st, gp, B, Tn, V, D, w, dWp);
         } else if (ng <= 1 && emb_rows_threads(B) == 64)
             emb_rows_kernel<T, NVC, 1, 64><<<l.grid, 64, 0, st>>>(gp, B, Tn, V, D, w, dWp);
         else if (ng <= 1)
@@ -1114,14 +1140,13 @@ cudaError_t emb_fast_run(const int32_t* ids, const void* g, void* dW, double* ra
         launch(std::integral_constant<int, 6>{});
     else
         launch(std::integral_constant<int, 8>{});
-    e = cudaGetLastError();
+    e = le != cudaSuccess ? le : cudaGetLastError();
     if (e != cudaSuccess) return e;
     // one more CTA folds the ||dW||^2 partials (per row block, or per walk CTA
     // for the cursor walk); the last CTA writes sums[0], sums[2] and the flag
     const EmbRawTail tl{w.qbig, (int)(l.masked ? l.nqblk : l.grid), reinterpret_cast<double*>(base + l.qtot),
                         tail + 2, sums, w.bad, bad_flag_out};
-    emb_raw_kernel<<<(unsigned)B + 1, 256, 0, st>>>(B, Tn, w, raw, tl);
-    return cudaGetLastError();
+    return emb_launch_pdl(emb_raw_kernel, (unsigned)B + 1, 256, st, B, Tn, w, raw, tl);
 }
 
 template <typename T>
