@@ -108,6 +108,13 @@ size_t gemm_workspace(int dt, int w_dt, int64_t K, int64_t L);
 cudaError_t launch_linear_gemm(int kind, int epi, int dt, int w_dt, const void* in, const void* W, const void* bias,
                                const void* aux, void* out, int64_t rows, int64_t K, int64_t L, void* ws,
                                cudaStream_t st);
+// stream-ordered scratch from the library-owned pool (linear_gemm.cu)
+cudaError_t gemm_pool_alloc(void** p, size_t bytes, cudaStream_t st);
+cudaError_t gemm_pool_free(void* p, cudaStream_t st);
+// fp32 rows: per-example weight-gradient norms on the 3xTF32 GEMM (linear_f32.cu)
+bool wgrad_tf32_ok(int dt, const void* x, const void* g, const void* dW, int64_t T, int64_t K, int64_t L);
+cudaError_t launch_wgrad_tf32(const float* x, const float* g, float* dW, double* raw, double* sums, int sum_slot,
+                              int64_t B, int64_t T, int64_t K, int64_t L, cudaStream_t st);
 // fp64 rows: per-example parameter gradients / norms in the reference's order (ln_ref.cu)
 size_t ln_ref_workspace(int64_t B, int64_t D);
 cudaError_t launch_ln_ref_params(const double* x, const double* mean, const double* rstd, const double* g, int64_t B,

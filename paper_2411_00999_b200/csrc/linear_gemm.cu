@@ -892,6 +892,13 @@ static cudaError_t scratch_pool(cudaMemPool_t* out) {
     return cudaSuccess;
 }
 
+cudaError_t gemm_pool_alloc(void** p, size_t bytes, cudaStream_t st) {
+    cudaMemPool_t pool;
+    cudaError_t e = scratch_pool(&pool);
+    return e != cudaSuccess ? e : cudaMallocFromPoolAsync(p, bytes, pool, st);
+}
+cudaError_t gemm_pool_free(void* p, cudaStream_t st) { return cudaFreeAsync(p, st); }
+
 // kind 0: forward y = x W + bias; kind 1: dx = g W^T.  dt / w_dt: 0 f32, 1 bf16, 2 f64.
 // epi: EPI_* applied to every output element (aux [rows, N] of dtype dt).
 cudaError_t launch_linear_gemm(int kind, int epi, int dt, int w_dt, const void* in, const void* W, const void* bias,

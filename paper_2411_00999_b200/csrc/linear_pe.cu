@@ -881,6 +881,11 @@ cudaError_t launch_generic_t(int kind, const void* x, const void* g, void* out_g
 cudaError_t launch_linear_generic(int dt, int kind, const void* x, const void* g, void* out_grad, int out_f64,
                                   double* raw, double* sums, int sum_slot, int64_t B, int64_t T, int64_t K, int64_t L,
                                   void* ws, cudaStream_t st) {
+    // fp32 rows, weight-gradient or Gram form: 3xTF32 tensor cores (linear_f32.cu)
+    if ((kind == 0 || kind == 2) && wgrad_tf32_ok(dt, x, g, kind == 0 ? out_grad : nullptr, T, K, L))
+        return launch_wgrad_tf32(static_cast<const float*>(x), static_cast<const float*>(g),
+                                 kind == 0 ? static_cast<float*>(out_grad) : nullptr, raw, sums, sum_slot, B, T, K, L,
+                                 st);
     switch (dt) {
         case 0: return launch_generic_t<float>(kind, x, g, out_grad, out_f64, raw, sums, sum_slot, B, T, K, L, ws, st);
         case 1:

@@ -211,3 +211,29 @@ def test_tcgen05_gram_form_cfg3_sampled(cuda):
     for b in (0, 7, 15):
         dWb = x[b].double().T @ g[b].double()
         assert close(f[b], float((dWb * dWb).sum()), 1e-4)
+
+
+@pytest.mark.parametrize("B,T,K,L", [(3, 256, 384, 320), (2, 100, 72, 200), (4, 64, 1000, 8), (2, 130, 64, 64)])
+def test_fp32_rows_tensor_core_norms(orc, cuda, B, T, K, L):
+    """fp32 rows on the 3xTF32 path (linear_f32.cu: per-example x_b^T g_b on the
+    tensor cores; T % 4 == L % 4 == 0, else the generic kernels): dW, raw_b and
+    the record against the oracle at rel 1e-5 (north star, fp32), both forms,
+    bitwise deterministic run to run."""
+    import paper_2411_00999_b200 as m
+    from paper_2411_00999_b200 import linear
+
+    x, g = m.synth_linear(B, T, K, L, torch.float32, cuda)
+    layer = linear.LinearLayer(torch.zeros(K, L, device=cuda))
+    r = linear.linear_backward_simultaneous(layer, x, g, form="weight_grad", need_input_grad=False)
+    r2 = linear.linear_backward_simultaneous(layer, x, g, form="weight_grad", need_input_grad=False)
+    f = linear.linear_perexample_sqnorm_frobenius(x, g)
+    ref = _oracle_linear(orc, x, g)
+    torch.cuda.synchronize()
+    dW = r.grads.weight_grads["weight"].double().cpu().numpy()
+    assert close(dW, ref["dW"], 1e-5, 1e-5 * np.max(np.abs(ref["dW"])))
+    assert close(r.grads.per_example_sqnorms_raw["weight"].cpu().numpy(), ref["raw_w"], 1e-5)
+    assert close(f.cpu().numpy(), ref["raw_w"], 1e-5)
+    assert close(float(r.grads.sums4[0]), float(np.sum(ref["raw_w"])), 1e-5)
+    assert close(float(r.grads.sums4[2]), float(np.sum(ref["dW"] ** 2)), 1e-5)
+    assert torch.equal(r.grads.weight_grads["weight"], r2.grads.weight_grads["weight"])
+    assert torch.equal(r.grads.per_example_sqnorms_raw["weight"], r2.grads.per_example_sqnorms_raw["weight"])
