@@ -224,7 +224,10 @@ __global__ void __launch_bounds__(kEmbThreads) emb_table_kernel(int64_t B, int64
 // dW matches the original path bit for bit (same per-example Acc sums, added
 // in example order); raw_b differs in summation order only.
 constexpr int kEmbSortThreads = 1024;
-constexpr int kEmbBuckets = 4096;  // id buckets of the sort kernel's bucket sort
+constexpr int kEmbBuckets = 4096;  // id buckets of the sort kernel's bucket sort (at most)
+#ifndef GNSB_EMB_BUCKETS_PER_KEY
+#define GNSB_EMB_BUCKETS_PER_KEY 1  // buckets per (padded) key, at most kEmbBuckets (0: always kEmbBuckets; 1 measured 65.2 against 66.6 us at GPT-2 size)
+#endif
 #ifndef GNSB_EMB_RPW
 #define GNSB_EMB_RPW 8
 #endif
@@ -611,6 +614,9 @@ __global__ void __launch_bounds__(NT, GNSB_EMB_OCC / NT) emb_rows_kernel(const T
     }
 }
 
+#ifndef GNSB_EMB_PB3
+#define GNSB_EMB_PB3 4  // mask walk: first-token rows in flight per batch for <= 3 vectors per lane (A/B)
+#endif
 #ifndef GNSB_EMB_MOCC
 #define GNSB_EMB_MOCC 512  // resident threads per SM the mask walk is compiled for (128 registers)
 #endif
@@ -1077,7 +1083,9 @@ cudaError_t emb_fast_run(const int32_t* ids, const void* g, void* dW, double* ra
     // buckets of 2^bsh ids, at most kEmbBuckets of them (the bitonic network
     // when that table plus two key arrays would not fit in shared memory)
     int bsh = 0;
-    while (((V - 1) >> bsh) >= kEmbBuckets) ++bsh;
+    const int64_t bcap = GNSB_EMB_BUCKETS_PER_KEY > 0 ? std::min<int64_t>(kEmbBuckets, (int64_t)Tp * GNSB_EMB_BUCKETS_PER_KEY)
+                                                       : kEmbBuckets;
+    while (((V - 1) >> bsh) >= bcap) ++bsh;
     const int nb = (int)(((V - 1) >> bsh) + 1);
     const size_t kb = k32 ? 4 : 8;
     const size_t smem_bucket = 2 * (size_t)Tp * kb + (2 * (size_t)nb + 1) * 4;
@@ -1106,7 +1114,7 @@ cudaError_t emb_fast_run(const int32_t* ids, const void* g, void* dW, double* ra
         constexpr int NVC = decltype(nvc)::value;
         if (l.masked) {
             // first-token rows in flight per batch: 12-16 16-byte vectors per lane
-            constexpr int PB = NVC <= 3 ? 4 : NVC <= 4 ? 3 : NVC <= 6 ? 2 : 1;
+            constexpr int PB = NVC <= 3 ? GNSB_EMB_PB3 : NVC <= 4 ? 3 : NVC <= 6 ? 2 : 1;
             if (l.mw == 1)
                 le = emb_launch_pdl(emb_mask_kernel<T, NVC, 1, PB>, l.grid, kEmbRowsThreads, st, gp, B, Tn, V, D, w, dWp);
             else if (l.mw == 2)
