@@ -837,10 +837,14 @@ __global__ void __launch_bounds__(256) emb_raw_kernel(int64_t B, int64_t Tn, Emb
     const int64_t b = blockIdx.x;
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the walk's q, qbig
     if (tl.ticket != nullptr) {
-        if (b == B) {  // the mask walk's per-block ||dW||^2 partials, in block order
-            double s = 0.0;
-            for (int k = threadIdx.x; k < tl.nq; k += 256) s += __ldcg(tl.qblk + k);
-            s_red[threadIdx.x] = s;
+        if (b == B) {  // the ||dW||^2 partials: 8 independent chains (loads in flight), fixed order
+            double t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            int k = threadIdx.x;
+            for (; k + 256 * 7 < tl.nq; k += 256 * 8)
+#pragma unroll
+                for (int u = 0; u < 8; ++u) t[u] += __ldcg(tl.qblk + k + 256 * u);
+            for (; k < tl.nq; k += 256) t[0] += __ldcg(tl.qblk + k);
+            s_red[threadIdx.x] = ((t[0] + t[1]) + (t[2] + t[3])) + ((t[4] + t[5]) + (t[6] + t[7]));
         } else {
             const int U = w.U[b];
             double s = 0.0;
