@@ -745,13 +745,15 @@ __global__ void __launch_bounds__(kEmbRowsThreads, GNSB_EMB_MOCC / kEmbRowsThrea
                             xb[u][q] = (k0 + u < n && vi < nvec) ? __ldg(row + vi) : make_uint4(0u, 0u, 0u, 0u);
                         }
                     }
+                    double sqv[PB];  // per-lane squares of the batch's pairs, reduced together below
+#pragma unroll
+                    for (int u = 0; u < PB; ++u) sqv[u] = 0.0;
 #pragma unroll
                     for (int u = 0; u < PB; ++u) {
                         const int k = k0 + u;
                         if (k >= n) break;
                         const int i = __shfl_sync(0xffffffffu, pi, k);
                         const int64_t b = __shfl_sync(0xffffffffu, pb, k);
-                        const int r = __shfl_sync(0xffffffffu, pr, k);
                         const int len = __shfl_sync(0xffffffffu, pln, k);
                         const int st = __shfl_sync(0xffffffffu, pst, k);
                         while (vr < i) store_row();
@@ -794,10 +796,18 @@ __global__ void __launch_bounds__(kEmbRowsThreads, GNSB_EMB_MOCC / kEmbRowsThrea
                                 sq = fma((double)tmp[q][e].x, (double)tmp[q][e].x, sq);
                                 sq = fma((double)tmp[q][e].y, (double)tmp[q][e].y, sq);
                             }
-                        sq = warp_sum(sq);
-                        if (lane == 0) {
+                        sqv[u] = sq;
+                    }
+                    // PB interleaved butterflies (each result equals warp_sum of its pair's squares)
+                    warp_sum_n<PB>(sqv);
+#pragma unroll
+                    for (int u = 0; u < PB; ++u) {
+                        const int k = k0 + u;
+                        const int64_t b = __shfl_sync(0xffffffffu, pb, k & 31);
+                        const int r = __shfl_sync(0xffffffffu, pr, k & 31);
+                        if (lane == 0 && k < n) {
                             double* qd = w.q + b * Tn + r;
-                            *qd = c == 0 ? sq : *qd + sq;
+                            *qd = c == 0 ? sqv[u] : *qd + sqv[u];
                         }
                     }
                 }
