@@ -54,7 +54,6 @@ __global__ void __launch_bounds__(kEmbThreads) emb_example_kernel(const int32_t*
     const int64_t b = blockIdx.x;
     const int tid = threadIdx.x;
     const int32_t* idb = ids + b * Tn;
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the walk may get scheduled
     for (int i = tid; i < Tp; i += blockDim.x) {
         uint64_t k = ~0ull;
         if (i < Tn) {
@@ -269,6 +268,8 @@ struct EmbFastWs {
     uint32_t* mask;    // [V][mw]: bit b set when example b has a run at id v
     int2* idx2;        // [V][B]: {run index r, first token | 0x80000000 when the run has > 1 token}
     int mw;            // mask words per row: ceil(B / 32)
+    int hv;            // sort CTAs per example (mask walk: 2, each the ids of one half of the table); perm, ent,
+                       // q and U hold hv "virtual examples" of Tn entries per example, in id order
 };
 
 template <int NT>
@@ -308,9 +309,15 @@ __global__ void __launch_bounds__(kEmbSortThreads) emb_sort_kernel(const int32_t
     const KT NONE = ~KT(0);
     __shared__ int s_warp[kEmbSortThreads / 32];
     __shared__ int s_nvalid;
-    const int64_t b = blockIdx.x;
+    const int hv = w.hv;
+    const int64_t b = blockIdx.x / hv, vb = blockIdx.x;  // example, virtual example (example, half)
+    const int64_t Bn = gridDim.x / hv;
+    // ids this CTA sorts: one half of the table per CTA when hv == 2
+    const int64_t vmid = (V + 1) / 2;
+    const int64_t id_lo = (hv == 2 && (vb & 1)) ? vmid : 0, id_hi = (hv == 2 && !(vb & 1)) ? vmid : V;
     const int tid = threadIdx.x;
     const int32_t* idb = ids + b * Tn;
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the walk may get scheduled
     __shared__ int s_maxb;
     if (tid == 0) {
         s_nvalid = 0;
@@ -333,7 +340,7 @@ __global__ void __launch_bounds__(kEmbSortThreads) emb_sort_kernel(const int32_t
                 const int32_t id = idb[i];
                 if (id < 0 || id >= V)
                     atomicExch(w.bad, 1);
-                else {
+                else if (id >= id_lo && id < id_hi) {
                     k = ((KT)(uint32_t)id << SH) | (KT)(uint32_t)i;
                     atomicAdd(&cnt[id >> BSH], 1);
                 }
@@ -399,7 +406,7 @@ __global__ void __launch_bounds__(kEmbSortThreads) emb_sort_kernel(const int32_t
                 const int32_t id = idb[i];
                 if (id < 0 || id >= V)
                     atomicExch(w.bad, 1);
-                else
+                else if (id >= id_lo && id < id_hi)
                     k = ((KT)(uint32_t)id << SH) | (KT)(uint32_t)i;
             }
             keys[i] = k;
@@ -454,9 +461,10 @@ __global__ void __launch_bounds__(kEmbSortThreads) emb_sort_kernel(const int32_t
     int total = 0;
     int r = block_exclusive_scan<kEmbSortThreads>(cnt, s_warp, &total);  // (its barriers publish s_nvalid)
     const int nvalid = s_nvalid;
-    int32_t* perm = w.perm + b * Tn;
-    int4* ent = w.ent + b * Tn;
-    int32_t* blk = w.blk + b * (w.nblk + 1);
+    int32_t* perm = w.perm + vb * Tn;
+    int4* ent = w.ent + vb * Tn;
+    int32_t* blk = w.blk + b * (w.nblk + 1);  // (cursor walk: hv == 1, vb == b)
+    const int hoff = (int)(vb - b * hv) * (int)Tn;  // this half's offset inside the example's hv * Tn entries
     for (int i = i0; i < i1; ++i) {
         if (!valid(i)) break;
         perm[i] = (int32_t)(uint32_t)(keys[i] & TM);
@@ -465,10 +473,11 @@ __global__ void __launch_bounds__(kEmbSortThreads) emb_sort_kernel(const int32_t
             int e = i + 1;
             while (e < nvalid && (uint32_t)(keys[e] >> SH) == id) ++e;
             const int t0 = (int)(uint32_t)(keys[i] & TM);
-            ent[r] = make_int4((int)id, i, e - i, t0);
+            ent[r] = make_int4((int)id, hoff + i, e - i, t0);
             if (w.mask) {  // the mask walk: mark (id, b), record where its run lives
                 atomicOr(w.mask + (int64_t)id * w.mw + (b >> 5), 1u << (b & 31));
-                w.idx2[(int64_t)id * gridDim.x + b] = make_int2(r, e - i > 1 ? (int)(0x80000000u | (uint32_t)t0) : t0);
+                w.idx2[(int64_t)id * Bn + b] =
+                    make_int2(hoff + r, e - i > 1 ? (int)(0x80000000u | (uint32_t)t0) : t0);
             } else {
                 // row blocks whose first row lies in (previous id, id] start at entry r
                 const int64_t j_lo = r == 0 ? 0 : (int64_t)((uint32_t)(keys[i - 1] >> SH) / kRowsPerWarp) + 1;
@@ -482,7 +491,7 @@ __global__ void __launch_bounds__(kEmbSortThreads) emb_sort_kernel(const int32_t
     const int64_t j_tail = nvalid > 0 ? (int64_t)((uint32_t)(keys[nvalid - 1] >> SH) / kRowsPerWarp) + 1 : 0;
     if (!w.mask)
         for (int64_t j = j_tail + tid; j <= w.nblk; j += blockDim.x) blk[j] = total;
-    if (tid == 0) w.U[b] = total;
+    if (tid == 0) w.U[vb] = total;
 }
 
 #ifndef GNSB_EMB_OCC
@@ -648,6 +657,7 @@ __global__ void __launch_bounds__(kEmbRowsThreads, GNSB_EMB_MOCC / kEmbRowsThrea
     const int nvec = (int)(D / W);
     const int nchunk = (nvec + 32 * NVC - 1) / (32 * NVC);
     const int64_t nblocks = (V + RB - 1) / RB;
+    const int64_t PS = (int64_t)w.hv * Tn;  // entries per example in perm / ent / q
     unsigned int* ctr = reinterpret_cast<unsigned int*>(w.mask + V * MW);  // zeroed with the mask
     auto take = [&]() {
         unsigned int x = 0;
@@ -727,7 +737,7 @@ __global__ void __launch_bounds__(kEmbRowsThreads, GNSB_EMB_MOCC / kEmbRowsThrea
                     pr = x.x;
                     pt = x.y & 0x7fffffff;
                     if (x.y < 0) {  // a run of several tokens: its start in the sorted list
-                        const int4 en = __ldcg(w.ent + (int64_t)pb * Tn + pr);
+                        const int4 en = __ldcg(w.ent + (int64_t)pb * PS + pr);
                         pst = en.y;
                         pln = en.z;
                     }
@@ -770,7 +780,7 @@ __global__ void __launch_bounds__(kEmbRowsThreads, GNSB_EMB_MOCC / kEmbRowsThrea
                             }
                         }
                         for (int j = 1; j < len; ++j) {  // the run's later tokens in token order
-                            const int64_t t = w.perm[b * Tn + st + j];
+                            const int64_t t = w.perm[b * PS + st + j];
                             const uint4* row = reinterpret_cast<const uint4*>(g + (b * Tn + t) * D);
 #pragma unroll
                             for (int q = 0; q < NVC; ++q) {
@@ -806,7 +816,7 @@ __global__ void __launch_bounds__(kEmbRowsThreads, GNSB_EMB_MOCC / kEmbRowsThrea
                         const int64_t b = __shfl_sync(0xffffffffu, pb, k & 31);
                         const int r = __shfl_sync(0xffffffffu, pr, k & 31);
                         if (lane == 0 && k < n) {
-                            double* qd = w.q + b * Tn + r;
+                            double* qd = w.q + b * PS + r;
                             *qd = c == 0 ? sqv[u] : *qd + sqv[u];
                         }
                     }
@@ -856,10 +866,13 @@ __global__ void __launch_bounds__(256) emb_raw_kernel(int64_t B, int64_t Tn, Emb
             for (; k < tl.nq; k += 256) t[0] += __ldcg(tl.qblk + k);
             s_red[threadIdx.x] = ((t[0] + t[1]) + (t[2] + t[3])) + ((t[4] + t[5]) + (t[6] + t[7]));
         } else {
-            const int U = w.U[b];
+            // the example's runs in id order: the first half's U0, then the second half's (hv == 2)
+            const int hv = w.hv;
+            const int U0 = w.U[b * hv], U = U0 + (hv == 2 ? w.U[b * hv + 1] : 0);
+            const double* qb = w.q + b * hv * Tn;
             double s = 0.0;
 #pragma unroll 8
-            for (int k = threadIdx.x; k < U; k += 256) s += __ldcg(w.q + b * Tn + k);
+            for (int k = threadIdx.x; k < U; k += 256) s += __ldcg(qb + (k < U0 ? k : Tn + (k - U0)));
             s_red[threadIdx.x] = s;
         }
         __syncthreads();
@@ -954,6 +967,7 @@ struct EmbFastLayout {
     int grid;   // row-walk CTAs (the mask walk's when `masked`)
     int64_t nblk;
     int64_t nqblk;  // mask walk: row blocks = ||dW||^2 partials
+    int hv;         // sort CTAs per example
     bool masked;
     int mw;
 };
@@ -1009,13 +1023,6 @@ EmbFastLayout emb_fast_layout(int64_t B, int64_t Tn, int64_t V, bool bf16) {
         off = (off + bytes + 255) / 256 * 256;
         return o;
     };
-    l.perm = take((size_t)B * Tn * 4);
-    l.ent = take((size_t)B * Tn * 16);
-    l.U = take((size_t)B * 4);
-    l.q = take((size_t)B * Tn * 8);
-    l.bad = take(4);
-    l.raw = take((size_t)B * 8);
-    l.nblk = blocks;
     // The mask walk for bf16 rows when the table has at least two row blocks
     // per resident warp (the queue balances the warps); the cursor walk for
     // fp32 rows and small tables.  Measured at B=32 T=1024 D=768: V=50257
@@ -1026,6 +1033,20 @@ EmbFastLayout emb_fast_layout(int64_t B, int64_t Tn, int64_t V, bool bf16) {
     const int64_t rb = mw <= 4 ? kRowsPerWarp : 32 / mw;
     const int64_t resident_warps = (int64_t)sms * (GNSB_EMB_MOCC / 32);
     l.masked = emb_mask_walk() && (emb_mask_forced() || (bf16 && (V + rb - 1) / rb >= 2 * resident_warps));
+    // mask walk: two sort CTAs per example (each the ids of one half of the
+    // table) while that fits the SMs; GNSB_EMB_SORT_HALVES=0 keeps one (A/B)
+    static const bool halves_off = [] {
+        const char* e = std::getenv("GNSB_EMB_SORT_HALVES");
+        return e && e[0] == '0';
+    }();
+    l.hv = (l.masked && !halves_off && B <= sms) ? 2 : 1;
+    l.perm = take((size_t)B * l.hv * Tn * 4);
+    l.ent = take((size_t)B * l.hv * Tn * 16);
+    l.U = take((size_t)B * l.hv * 4);
+    l.q = take((size_t)B * l.hv * Tn * 8);
+    l.bad = take(4);
+    l.raw = take((size_t)B * 8);
+    l.nblk = blocks;
     if (l.masked) {
         l.mw = mw;
         l.nqblk = (V + rb - 1) / rb;
@@ -1079,7 +1100,7 @@ cudaError_t emb_fast_run(const int32_t* ids, const void* g, void* dW, double* ra
                 reinterpret_cast<double*>(base + l.qbig),  reinterpret_cast<int32_t*>(base + l.bad),
                 reinterpret_cast<int32_t*>(base + l.blk),   l.nblk,
                 l.masked ? reinterpret_cast<uint32_t*>(base + l.mask) : nullptr,
-                l.masked ? reinterpret_cast<int2*>(base + l.idx2) : nullptr, l.mw};
+                l.masked ? reinterpret_cast<int2*>(base + l.idx2) : nullptr, l.mw, l.hv};
     if (raw == nullptr) raw = reinterpret_cast<double*>(base + l.raw);
     // the mask walk: one memset clears the mask words, the block queue's
     // counter, the bad-id flag and the raw kernel's ticket (the mask's tail)
@@ -1108,12 +1129,12 @@ cudaError_t emb_fast_run(const int32_t* ids, const void* g, void* dW, double* ra
     if (k32) {
         e = ensure_smem_attr(reinterpret_cast<const void*>(emb_sort_kernel<uint32_t>), smem);
         if (e != cudaSuccess) return e;
-        emb_sort_kernel<uint32_t><<<(unsigned)B, kEmbSortThreads, smem, st>>>(ids, Tn, V, w, Tp, sh, bsh,
+        emb_sort_kernel<uint32_t><<<(unsigned)(B * l.hv), kEmbSortThreads, smem, st>>>(ids, Tn, V, w, Tp, sh, bsh,
                                                                             bucket ? nb : 0);
     } else {
         e = ensure_smem_attr(reinterpret_cast<const void*>(emb_sort_kernel<uint64_t>), smem);
         if (e != cudaSuccess) return e;
-        emb_sort_kernel<uint64_t><<<(unsigned)B, kEmbSortThreads, smem, st>>>(ids, Tn, V, w, Tp, 32, bsh,
+        emb_sort_kernel<uint64_t><<<(unsigned)(B * l.hv), kEmbSortThreads, smem, st>>>(ids, Tn, V, w, Tp, 32, bsh,
                                                                             bucket ? nb : 0);
     }
     e = cudaGetLastError();
